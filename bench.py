@@ -1,0 +1,475 @@
+#!/usr/bin/env python3
+"""Benchmark of the live PP-reconfiguration data path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one KV-patch round of BASELINE configs[1] (Llama-3-8B shape, PP2->4,
+16-token blocks, k=4): every live cell of the two migrating layer groups of
+B=256 requests x 2048 tokens is marked dirty, drained (K3 scan/compact) and
+pushed into the destination's paged pools (fused K4 gather -> K5 scatter).
+`value` is KV-patch GB/s (KvPatch.payload_bytes per second, inputs resident);
+`e2e` is the same round through the C-ABI with the KV arriving from pinned host
+memory each step.  Extra keys report switch pause, resize latency and
+paged-attention decode tokens/s.  Under torchrun every rank runs its own pair on
+its own GPU (weak scaling, no data-path collective); timing is max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--ctx", type=int, default=2048)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ dist
+def dist_init(n: int):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    return rank, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = Path(f"/tmp/pipelive_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        try:
+            rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r]
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if len(r) >= 9]
+        mx = [float(r[2]) for r in rows if len(r) >= 9]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for i, n in enumerate(names):
+                if len(r) >= 9 and r[5 + i].strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ CPU legs
+def cpu_patch_rate(wl, seconds: float = 12.0, n_req: int = 8) -> dict:
+    """The oracle port (oracle/oracle.c, the reference's _drain + PatchReceiver._apply
+    restated in C with real KV bytes) on the host cores: KV-patch GB/s of a bounded
+    sample of the same workload (n_req requests x ctx tokens x the migrating groups)."""
+    import numpy as np
+
+    import oracle
+    from paper_2604_12171_b200.events import stable_hash
+
+    threads = os.cpu_count() or 1
+    blocks = n_req * wl.blocks_per_req + 8
+    G = len(wl.src_groups)
+    src = oracle.OracleStore(1, wl.k, wl.s, blocks, wl.src_groups, num_groups=G,
+                             cell_bytes=wl.cell_bytes)
+    dst = oracle.OracleStore(2, wl.k, wl.s, blocks, wl.mig_groups, num_groups=G,
+                             cell_bytes=wl.cell_bytes)
+    for i in range(n_req):
+        for g in wl.mig_groups:
+            seed = stable_hash(f"r{i:04d}", g)
+            src.append(f"r{i:04d}", g, wl.ctx, [oracle.payload(seed, p) for p in range(wl.ctx)])
+    dirty = oracle.OracleDirty()
+    rank = src.reg.rank()
+    sample_bytes = n_req * wl.ctx * len(wl.mig_groups) * wl.k * wl.cell_bytes
+    rounds, t_total = 0, 0.0
+    while t_total < seconds or rounds < 2:
+        t0 = time.perf_counter()
+        for i in range(n_req):
+            h = src.reg.handle(f"r{i:04d}")
+            for g in wl.mig_groups:
+                dirty.mark(h, g, 0, wl.ctx)
+        keys, cells = dirty.patch_round(src, dst, rank, wl.k, threads)
+        t_total += time.perf_counter() - t0
+        rounds += 1
+        assert keys == n_req * wl.ctx * len(wl.mig_groups)
+    gbs = sample_bytes * rounds / t_total / 1e9
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{rounds} rounds x {n_req} requests x {wl.ctx} tokens x "
+                      f"{len(wl.mig_groups)} groups x k={wl.k} x {wl.cell_bytes} B "
+                      f"({sample_bytes / 1e9:.2f} GB/round), oracle/oracle.c with {threads} threads",
+            "seconds": round(t_total, 2)}
+
+
+def run_reference(args, wl, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    cb = cpu_patch_rate(wl, seconds=max(4.0, 2.0 * (K + W)))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GB/s",
+        "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": round(wl.payload_bytes / (cb["value"] * 1e9) * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic", "config": config_of(wl, world),
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_of(wl, world: int) -> dict:
+    return {"workload": wl.name, "model_shape": "llama-3-8b (32L, 32q/8kv x 128, bf16)",
+            "pp_change": "2->4", "migrating_layers": "9-16 (groups 2,3)",
+            "stacking_k": wl.k, "tokens_per_block": wl.s, "batch": wl.batch, "ctx": wl.ctx,
+            "kv_bytes_per_token_layer": wl.cell_bytes,
+            "bytes_per_step": wl.payload_bytes,
+            "l2": "inputs (>17 GB per step) exceed the 126 MB L2; no flush needed",
+            "parallelism": f"{world} independent pairs (1 per GPU)"}
+
+
+# ------------------------------------------------------------------------------ GPU legs
+def main() -> None:
+    args = parse()
+    rank, world = dist_init(args.gpus)
+    from paper_2604_12171_b200.perf import Workload
+
+    wl = Workload(batch=args.batch, ctx=args.ctx)
+    if args.impl == "reference":
+        run_reference(args, wl, rank, world)
+        return
+
+    import torch
+
+    from paper_2604_12171_b200 import _native as N
+    from paper_2604_12171_b200.perf import PatchRig, read_peaks
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    lib = N.lib()
+    peaks = read_peaks(ROOT / "MEASURED_PEAKS.json")
+    hbm_peak = float(peaks.get("hbm_gbs", HBM_FALLBACK_GBS))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    stream = torch.cuda.Stream(device=dev)
+    rig = PatchRig(wl, device=dev)
+    rig.use_stream(stream.cuda_stream)
+    rig.fill()
+    K, W = args.steps, args.warmup
+
+    # ---- value: bulk KV-patch rounds, everything resident in HBM
+    for _ in range(W):
+        rig.bulk_round()
+    torch.cuda.synchronize()
+    N.check(lib.pl_timing_reset())
+    N.check(lib.pl_timing_enable(1))
+    barrier(world)
+    launches0 = N.launch_count()
+    with Clocks(dev) as clocks:
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        keys_total = 0
+        for _ in range(K):
+            keys, cells = rig.bulk_round()
+            keys_total += keys
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = N.launch_count() - launches0
+    N.check(lib.pl_timing_enable(0))
+    ms = t0.elapsed_time(t1)
+    ms = allmax(ms, world)
+    barrier(world)
+    assert keys_total == K * wl.batch * wl.ctx * len(wl.mig_groups)
+    value = world * K * wl.payload_bytes / (ms / 1e3) / 1e9
+    push_ms, push_n = N.timing("patch_push")
+    drain_ms, drain_n = N.timing("drain")
+    push_avg = push_ms / max(push_n, 1)
+    # algorithmic HBM bytes of one push launch: payload read + payload write + 2 x 8 B fp
+    alg_bytes = 2 * wl.payload_bytes + 2 * 8 * wl.batch * wl.ctx * len(wl.mig_groups)
+    achieved = alg_bytes / (push_avg / 1e3) / 1e9
+    roofline = {"kernel": "copy_kernel<2> (K4 gather -> K5 scatter, fused push)",
+                "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                "avg_launch_ms": round(push_avg, 4),
+                "share_of_step": round(push_ms / ms, 4) if ms else None,
+                "drain_ms_per_step": round(drain_ms / max(K, 1), 4)}
+
+    # ---- switch pause (data-path part): residual patch after one decode round + barrier
+    pause = measure_switch_pause(rig, stream, torch, wl)
+
+    # ---- paged-attention decode over the source stage (16 layers)
+    decode = measure_decode(rig, stream, torch, wl, hbm_peak, K, W)
+
+    # ---- resize latency: post-commit cleanup on the source (drop groups, shrink, regrow)
+    resize = measure_resize(rig, stream, torch, wl)
+
+    # ---- e2e: KV arrives from pinned host memory every step, result read back
+    e2e = None if args.skip_e2e else measure_e2e(rig, stream, torch, wl, K, world)
+    rig.close()
+
+    if rank != 0:
+        return
+    cpu = None if args.skip_cpu else cpu_patch_rate(wl)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(ms / K, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": config_of(wl, world),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "switch_pause_ms": pause,
+        "decode": decode,
+        "resize": resize,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def measure_switch_pause(rig, stream, torch, wl) -> dict:
+    """After the bulk copy converged: one decode round writes B tokens into every
+    group (K1 fused with the dirty mark), then the switch: pause -> drain the
+    compute stream -> final residual patch -> barrier -> switch -> resume."""
+    from paper_2604_12171_b200 import _native as N
+    from paper_2604_12171_b200.perf import append_batch
+    from paper_2604_12171_b200.events import stable_hash
+
+    rig.bulk_round()
+    torch.cuda.synchronize()
+    reqs, groups, counts, seeds = [], [], [], []
+    for i, h in enumerate(rig.handles):
+        for g in wl.src_groups:
+            reqs.append(h)
+            groups.append(g)
+            counts.append(1)
+            seeds.append(stable_hash(f"r{i:04d}", g))
+    samples = []
+    for _ in range(5):
+        append_batch(rig.src, reqs, groups, counts, seeds, mark=True)
+        t0 = time.perf_counter()          # pause_admission
+        stream.synchronize()              # pipeline drained (in-flight writes done)
+        keys, cells = rig.patch.push(rig.dst, rig.registry.rank())   # final sync
+        stream.synchronize()              # barrier: residual applied on the destination
+        samples.append((time.perf_counter() - t0) * 1e3)
+        assert keys == wl.batch * len(wl.mig_groups)
+    return {"median": round(statistics.median(samples), 4), "max": round(max(samples), 4),
+            "residual_cells": wl.batch * len(wl.mig_groups) * wl.k,
+            "residual_bytes": wl.batch * len(wl.mig_groups) * wl.k * wl.cell_bytes,
+            "note": "data-path part of the pause (drain of queued writes + residual patch + "
+                    "barrier); excludes pipeline drain of model compute"}
+
+
+def measure_decode(rig, stream, torch, wl, hbm_peak, K, W) -> dict:
+    import ctypes as C
+
+    from paper_2604_12171_b200 import _native as N
+
+    lib = N.lib()
+    B = wl.batch
+    rows = torch.tensor(rig.handles, dtype=torch.int32, device="cuda")
+    ctx_now = wl.ctx
+    ctx = torch.full((B,), ctx_now, dtype=torch.int32, device="cuda")
+    q = torch.randn(B, wl.n_q, wl.head_dim, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty_like(q)
+    layers = [(g, j) for g in wl.src_groups for j in range(wl.k)]
+
+    def step():
+        for g, j in layers:
+            N.check(lib.pl_paged_attn_decode(rig.src._h, g, j, C.c_void_p(q.data_ptr()),
+                                             C.c_void_p(out.data_ptr()),
+                                             C.c_void_p(rows.data_ptr()),
+                                             C.c_void_p(ctx.data_ptr()), B, wl.n_q, wl.n_kv,
+                                             wl.head_dim, wl.head_dim ** -0.5, ctx_now,
+                                             C.c_void_p(stream.cuda_stream)))
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    N.check(lib.pl_timing_reset())
+    N.check(lib.pl_timing_enable(1))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    N.check(lib.pl_timing_enable(0))
+    ms = e0.elapsed_time(e1) / K
+    attn_ms, attn_n = N.timing("paged_attn")
+    per_launch = attn_ms / max(attn_n, 1)
+    kv_bytes_layer = B * ctx_now * wl.cell_bytes
+    q_bytes = 2 * B * wl.n_q * wl.head_dim * 2
+    achieved = (kv_bytes_layer + q_bytes) / (per_launch / 1e3) / 1e9
+    return {"tokens_per_s": round(B / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
+            "layers_per_step": len(layers), "batch": B, "ctx": ctx_now,
+            "roofline": {"kernel": "paged_attn_kernel<128,4,8> (+combine)", "bound": "hbm",
+                         "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved / hbm_peak, 4),
+                         "alg_bytes_per_launch": kv_bytes_layer + q_bytes,
+                         "avg_launch_ms": round(per_launch, 4)}}
+
+
+def measure_e2e(rig, stream, torch, wl, K, world) -> dict:
+    """The bulk round through the C-ABI with host buffers: each step the migrating
+    groups' KV of all B requests streams from pinned host memory (H2D, chunked and
+    double-buffered), is appended by K1 with the fused dirty mark, then drained and
+    pushed; the device drained count is read back (D2H)."""
+    from paper_2604_12171_b200 import _native as N
+    from paper_2604_12171_b200.perf import append_batch
+    from paper_2604_12171_b200.events import stable_hash
+
+    per_req = wl.ctx * wl.k * wl.cell_bytes          # one (request, group)
+    chunk_reqs = 16
+    chunk_bytes = chunk_reqs * len(wl.mig_groups) * per_req
+    host = torch.empty(chunk_bytes, dtype=torch.uint8, pin_memory=True)
+    host.random_(0, 255)
+    dev = [torch.empty(chunk_bytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
+    done_copy = [torch.cuda.Event() for _ in range(2)]
+    done_use = [torch.cuda.Event() for _ in range(2)]
+    result = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    e2e_names = [f"e2e{i:04d}" for i in range(wl.batch)]
+    handles = [rig.registry.handle(n) for n in e2e_names]
+
+    def one_step():
+        for n in e2e_names:   # the previous step's requests leave both stages
+            rig.src.free_request(n)
+            rig.dst.free_request(n)
+        for c0 in range(0, wl.batch, chunk_reqs):
+            b = (c0 // chunk_reqs) % 2
+            copy_stream.wait_event(done_use[b])
+            with torch.cuda.stream(copy_stream):
+                dev[b].copy_(host, non_blocking=True)
+                done_copy[b].record(copy_stream)
+            stream.wait_event(done_copy[b])
+            reqs, groups, counts, seeds = [], [], [], []
+            for i in range(c0, min(c0 + chunk_reqs, wl.batch)):
+                for g in wl.mig_groups:
+                    reqs.append(handles[i])
+                    groups.append(g)
+                    counts.append(wl.ctx)
+                    seeds.append(stable_hash(e2e_names[i], g))
+            append_batch(rig.src, reqs, groups, counts, seeds, kv_dev=dev[b].data_ptr(), mark=True)
+            done_use[b].record(stream)
+        keys, _ = rig.patch.push(rig.dst, rig.registry.rank())
+        # D2H of the step's result: the device's drained-key count
+        result[0] = rig.patch.device_drained()
+        return keys
+
+    # the e2e requests need room: the bulk requests leave both stages first
+    for i in range(wl.batch):
+        rig.src.free_request(f"r{i:04d}")
+        rig.dst.free_request(f"r{i:04d}")
+    one_step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(K):
+        keys = one_step()
+        stream.synchronize()
+    sec = time.perf_counter() - t0
+    sec = allmax(sec, world)
+    assert keys == wl.batch * wl.ctx * len(wl.mig_groups)
+    for n in e2e_names:
+        rig.src.free_request(n)
+        rig.dst.free_request(n)
+    return {"value": round(world * K * wl.payload_bytes / sec / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": (wl.batch // chunk_reqs) * chunk_bytes,
+            "d2h_bytes_per_step": 8, "ms_per_step": round(sec / K * 1e3, 2)}
+
+
+def measure_resize(rig, stream, torch, wl) -> dict:
+    """Post-commit cleanup on the source stage (coordinator.py:340-354): drop the groups
+    that left, compact + shrink to a smaller budget, then grow back; wall ms each."""
+    st = rig.src
+    out = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    freed = st.drop_layer_groups(list(wl.mig_groups))
+    out["drop_groups_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    # free a quarter of the requests so the shrink must relocate live tail blocks
+    for i in range(0, wl.batch, 4):
+        st.free_request(f"r{i:04d}")
+    cap = st.capacity_blocks
+    target = max(st.used_blocks + 16, int(cap * 0.8))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st.compact()
+    st.resize(target)
+    st.sync()
+    out["shrink_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    out["shrink_stats"] = st.last_resize_stats()
+    t0 = time.perf_counter()
+    st.resize(cap)
+    st.sync()
+    out["grow_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    out["grow_stats"] = st.last_resize_stats()
+    out["blocks"] = {"from": cap, "to": target, "live": st.used_blocks}
+    out["tokens_freed_by_drop"] = freed
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,217 @@
+/*
+ * pipelive.h -- C-ABI of the B200-native live PP-reconfiguration data path.
+ *
+ * This is the drop-in boundary for the reference package `pipeshift`
+ * (arXiv 2604.12171, /root/reference/pkg/src/pipeshift).  The reference has
+ * no FFI: its boundary is the Python object protocol of KvStore /
+ * MigrationManager.  Every entry point below replaces one
+ * reference method, cited as file:line into the reference tree.  The Python
+ * package `paper_2604_12171_b200` binds these with ctypes; INTEGRATION.md
+ * shows the binding a pipeshift maintainer would add.
+ *
+ * Conventions
+ *   - every call returns int status: 0 = ok, negative = error code below;
+ *     pl_last_error() gives the message of the last failure on this thread.
+ *   - plain pointers and sizes only; "host" pointers are CPU memory,
+ *     "dev" pointers are CUDA device memory on the store's device.
+ *   - request ids are int32 handles assigned by the caller (one registry
+ *     shared by every store of a run, so a handle names the same request on
+ *     the source and the destination of a migration).
+ *   - streams are cudaStream_t passed as void*; NULL = the store's stream.
+ *   - device memory of pools, tables, bitmaps and staging is owned by the
+ *     pl_store / pl_patch handle; buffers passed in are borrowed.
+ */
+#ifndef PIPELIVE_H
+#define PIPELIVE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define PL_ABI_VERSION 1
+
+/* status codes; negative codes map 1:1 onto the reference exceptions */
+#define PL_OK 0
+#define PL_E_KV_OVERFLOW -1          /* KvOverflow          kvstore.py:27-28 */
+#define PL_E_CAPACITY_BELOW_LIVE -2  /* CapacityBelowLive   kvstore.py:31-32 */
+#define PL_E_UNKNOWN_SLOT -3         /* UnknownSlot         kvstore.py:35-36 */
+#define PL_E_UNKNOWN_LAYER_GROUP -4  /* UnknownLayerGroup   kvstore.py:39-40 */
+#define PL_E_INSUFFICIENT_MEMORY -5  /* InsufficientMemory  kvstore.py:43-44 */
+#define PL_E_INVALID -6              /* ValueError */
+#define PL_E_CUDA -7                 /* CUDA runtime / driver failure */
+#define PL_E_STATE -8                /* call order misuse (e.g. two patches in flight) */
+
+/* payload modes of the KV write (K1) */
+#define PL_PAYLOAD_EXPLICIT 0  /* one fingerprint per token from a host array */
+#define PL_PAYLOAD_SEED 1      /* fingerprint = engine.py:252-261 mixing of a per-(req,group) seed */
+
+typedef struct pl_store pl_store;
+typedef struct pl_patch pl_patch;
+
+typedef struct pl_store_info {
+  int64_t capacity_blocks;   /* len(KvStore.blocks)            kvstore.py:138-140 */
+  int64_t used_blocks;       /* KvStore._used                  kvstore.py:142-144 */
+  int64_t free_blocks;       /* capacity - used                kvstore.py:146-148 */
+  int64_t occupied_cells;    /* KvStore._occupied              kvstore.py:103 */
+  int64_t n_resident;        /* len(resident_groups) */
+  int64_t tokens_per_block;  /* s */
+  int64_t stacking_factor;   /* k */
+  int64_t cell_bytes;        /* bytes stored per (token, layer) */
+  int64_t unit_bytes;        /* bytes of one (block, group) unit incl. fp header */
+  int64_t fp_header_bytes;   /* fingerprint header at the start of each unit */
+  int64_t mapped_bytes;      /* physical HBM currently mapped for the pool */
+  int64_t table_max_chain;   /* row stride of the device block table */
+  int64_t table_max_reqs;    /* rows of the device block table */
+  int64_t n_tables;          /* live block tables (len(KvStore.tables)) */
+} pl_store_info;
+
+const char* pl_last_error(void);
+int pl_abi_version(void);
+int pl_device_count(int* out);
+
+/* ---- store lifecycle: KvStore.__init__ (kvstore.py:91-119), kv_init (kvstore.py:363-373) */
+int pl_store_create(int device, int gpu_id, int stacking_factor, int tokens_per_block,
+                    int64_t cell_bytes, int num_model_groups, int64_t capacity_blocks,
+                    const int32_t* resident_groups, int n_resident, int64_t chunk_bytes,
+                    pl_store** out);
+int pl_store_destroy(pl_store* st);
+int pl_store_set_stream(pl_store* st, void* stream);
+int pl_store_get_info(pl_store* st, pl_store_info* out);
+/* resident_groups mutation (coordinator.py:205-206, kvstore.py:308); maps/unmaps pools */
+int pl_store_add_groups(pl_store* st, const int32_t* groups, int n);
+int pl_store_remove_groups(pl_store* st, const int32_t* groups, int n);
+int pl_store_resident(pl_store* st, int32_t* out_groups, int cap, int* n_out);
+
+/* ---- block accounting: blocks_needed (kvstore.py:154-159), chain_len (kvstore.py:150-152) */
+int pl_store_blocks_needed(pl_store* st, int32_t req, int64_t extra_tokens, int64_t* out);
+int pl_store_chain(pl_store* st, int32_t req, int64_t* out_block_ids, int64_t cap, int64_t* n_out);
+int pl_store_chain_slots(pl_store* st, int32_t req, int32_t* out_slots, int64_t cap, int64_t* n_out);
+int pl_store_written(pl_store* st, int32_t req, int32_t* out_groups, int64_t* out_counts,
+                     int cap, int* n_out);
+int pl_store_has_table(pl_store* st, int32_t req, int* out);
+int pl_store_tables(pl_store* st, int32_t* out_reqs, int64_t cap, int64_t* n_out);
+int pl_store_blocks(pl_store* st, int64_t* out_ids, int32_t* out_owner, int32_t* out_slot,
+                    int64_t cap, int64_t* n_out);
+int pl_store_block_occupied(pl_store* st, int64_t block_id, int64_t* out_tokens);
+int pl_store_block_occupancy(pl_store* st, int64_t block_id, int group, uint64_t* out_words,
+                             int cap_words, int* n_words);
+
+/* ---- KV writes (K1): KvStore.append (kvstore.py:163-199), write_slots (kvstore.py:201-227),
+ *      fused with the dirty mark of MigrationStream.on_kv_written (migrator.py:190-197) when
+ *      mark != 0.  payload_mode EXPLICIT reads payloads_host[n]; SEED uses seed.
+ *      kv_dev (optional, may be NULL) holds real KV bytes [n][k][cell_bytes]; without it the
+ *      cells are filled with the deterministic expansion of the fingerprint. */
+int pl_store_append(pl_store* st, int32_t req, int group, int64_t n, int payload_mode,
+                    const uint64_t* payloads_host, uint64_t seed, const void* kv_dev, int mark);
+/* batched engine path (engine.py:377-404): item i appends counts[i] tokens of group
+ * groups[i] to reqs[i] at its current written prefix.  Stops at the first overflow:
+ * *n_done = items fully applied; returns PL_E_KV_OVERFLOW for item *n_done.
+ * sched_cells_out (optional, per attached patch in attach order) accumulates n*k of the marks */
+int pl_store_append_batch(pl_store* st, int n_items, const int32_t* reqs, const int32_t* groups,
+                          const int64_t* counts, const uint64_t* seeds, const void* kv_dev,
+                          int mark, int* n_done, int64_t* sched_cells_out, int n_sched);
+int pl_store_write_slots(pl_store* st, int32_t req, int group, int64_t n,
+                         const int64_t* positions_host, const uint64_t* payloads_host);
+
+/* ---- reads: lookup (kvstore.py:229-237), read_checksum (kvstore.py:239-245),
+ *      snapshot_group (kvstore.py:331-343) */
+int pl_store_lookup(pl_store* st, int32_t req, int layer, int64_t token, uint64_t* out_address,
+                    int64_t* out_offset);
+int pl_store_read_checksum(pl_store* st, int32_t req, int group, int64_t token, uint64_t* out);
+int pl_store_read_fps(pl_store* st, int group, const int32_t* slots_host, int64_t n_slots,
+                      uint64_t* out_host);
+int pl_store_read_cell(pl_store* st, int32_t req, int group, int64_t token, int layer_in_group,
+                       void* out_host, int64_t nbytes);
+
+/* ---- lifecycle ops: compact (kvstore.py:247-257), resize (kvstore.py:259-282; K6 remap),
+ *      drop_layer_groups (kvstore.py:284-309), free_request (kvstore.py:311-322),
+ *      effective_utilization (kvstore.py:324-329) */
+int pl_store_compact(pl_store* st, int64_t* out_free_tail);
+int pl_store_resize(pl_store* st, int64_t new_capacity);
+int pl_store_drop_groups(pl_store* st, const int32_t* groups, int n, int64_t* out_freed_tokens);
+/* stats_out holds up to cap triples (group, consumed, allocated) in written-insertion order */
+int pl_store_free_request(pl_store* st, int32_t req, int64_t* stats_out, int cap, int* n_stats);
+int pl_store_utilization(pl_store* st, double* out);
+/* resize instrumentation: blocks relocated, table entries remapped, bytes mapped/unmapped */
+int pl_store_last_resize_stats(pl_store* st, int64_t* out4);
+
+/* ---- device views for kernels outside the store (K2 attention, perf drivers) */
+int pl_store_group_base(pl_store* st, int group, uint64_t* out_dev_ptr);
+int pl_store_table_dev(pl_store* st, uint64_t* out_dev_ptr, int64_t* out_row_stride);
+int pl_store_flush(pl_store* st);  /* push pending block-table deltas to the device */
+int pl_store_sync(pl_store* st);   /* flush + cudaStreamSynchronize */
+
+/* ---- patch engine: one migrating (src, dst) pair: DirtyBitmap (migrator.py:24-48) +
+ *      MigrationStream drain (migrator.py:227-243) + PatchReceiver._apply (migrator.py:115-132).
+ *      layers_per_group[i] = number of the pair's layers inside groups[i] (migrator.py:245-247) */
+int pl_patch_create(pl_store* src, const int32_t* groups, const int32_t* layers_per_group,
+                    int n_groups, pl_patch** out);
+int pl_patch_destroy(pl_patch* p);
+int pl_patch_set_active(pl_patch* p, int active);
+/* DirtyBitmap.mark of n tokens starting at pos (migrator.py:35-36, 194) */
+int pl_patch_mark(pl_patch* p, int32_t req, int group, int64_t start, int64_t n);
+/* MigrationStream.start seeding (migrator.py:170-183): *out_tokens = seeded tokens */
+int pl_patch_seed(pl_patch* p, int64_t* out_tokens);
+/* DirtyBitmap.discard_request (migrator.py:43-48): *out_cells = dirty keys dropped */
+int pl_patch_discard_request(pl_patch* p, int32_t req, int64_t* out_keys);
+int pl_patch_dirty_keys(pl_patch* p, int64_t* out_keys);
+/* drain (K3 scan/compact + K4 gather into staging): *out_keys = drained dirty keys,
+ * *out_cells = token_count of the patch = sum over keys of layers_per_group */
+int pl_patch_drain(pl_patch* p, int64_t* out_keys, int64_t* out_cells);
+/* list the drained keys of the in-flight patch (req, group, position), host arrays */
+int pl_patch_drained_keys(pl_patch* p, int32_t* reqs, int32_t* groups, int64_t* pos,
+                          int64_t cap, int64_t* n_out);
+/* apply the in-flight patch to dst (K5 scatter).  rank_of_req[h] orders requests like the
+ * reference's sorted(rid) (migrator.py:124); stale[h] != 0 skips requests freed at or after
+ * the drain (migrator.py:121-122).  On PL_E_KV_OVERFLOW the (req, group) items before the
+ * failing one are applied, like the reference's exception mid-loop. */
+int pl_patch_apply(pl_patch* p, pl_store* dst, const int32_t* rank_of_req, int64_t n_rank,
+                   const uint8_t* stale, int64_t n_stale);
+/* perf path: drain + extend dst chains + fused gather/scatter directly into dst (K3+K4+K5,
+ * no staging; dst may live on a peer device with P2P access) */
+int pl_patch_push(pl_patch* p, pl_store* dst, const int32_t* rank_of_req, int64_t n_rank,
+                  int64_t* out_keys, int64_t* out_cells);
+/* verification hooks: device popcount of the live bitmap; keys of the last device drain */
+int pl_patch_device_dirty_count(pl_patch* p, int64_t* out);
+int pl_patch_device_drained(pl_patch* p, int64_t* out);
+
+/* ---- K2 paged-attention decode over the store layout.
+ * q_dev [B, n_q, head_dim] bf16; out_dev [B, n_q, head_dim] bf16.
+ * req_rows_dev [B] int32 request handles (rows of the store's block table);
+ * ctx_lens_dev [B] int32; layer_in_group selects the layer inside the group's unit.
+ * Cell layout per (token, layer): [K: n_kv*head_dim bf16][V: n_kv*head_dim bf16]. */
+int pl_paged_attn_decode(pl_store* st, int group, int layer_in_group, const void* q_dev,
+                         void* out_dev, const int32_t* req_rows_dev, const int32_t* ctx_lens_dev,
+                         int batch, int n_q_heads, int n_kv_heads, int head_dim, float scale,
+                         int max_ctx, void* stream);
+/* same kernel over explicit buffers: pool_dev = unit array, unit_bytes/fp_bytes layout above,
+ * block_tables_dev [B][max_blocks] int32 slots */
+int pl_paged_attn_decode_raw(const void* pool_dev, int64_t unit_bytes, int64_t fp_bytes,
+                             int tokens_per_block, int stacking_factor, int layer_in_group,
+                             const void* q_dev, void* out_dev, const int32_t* block_tables_dev,
+                             int max_blocks, const int32_t* ctx_lens_dev, int batch,
+                             int n_q_heads, int n_kv_heads, int head_dim, float scale,
+                             int max_ctx, void* stream);
+
+/* ---- kernel launch accounting (bench gpu_launches) and per-kernel device timing:
+ * when enabled, CUDA events bracket every launch of the named kernels ("kv_write",
+ * "patch_gather", "patch_scatter", "patch_push", "drain", "paged_attn", "unit_move");
+ * pl_timing_read synchronises them and returns the summed device milliseconds. */
+int64_t pl_launch_count(void);
+int pl_timing_enable(int on);
+int pl_timing_read(const char* kernel, double* total_ms, int64_t* launches);
+int pl_timing_reset(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPELIVE_H */

@@ -1,0 +1,187 @@
+"""ctypes binding of libpipelive.so (include/pipelive.h).
+
+The product path has no CPU fallback: importing the data-plane classes works
+anywhere (so the CPU test-suite can check the ABI), but the first call that
+needs the library raises NativeUnavailable unless libpipelive.so is built and
+a CUDA device is visible.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("PIPELIVE_LIB", _HERE / "libpipelive.so"))
+
+PL_OK = 0
+PL_E_KV_OVERFLOW = -1
+PL_E_CAPACITY_BELOW_LIVE = -2
+PL_E_UNKNOWN_SLOT = -3
+PL_E_UNKNOWN_LAYER_GROUP = -4
+PL_E_INSUFFICIENT_MEMORY = -5
+PL_E_INVALID = -6
+PL_E_CUDA = -7
+PL_E_STATE = -8
+
+PL_PAYLOAD_EXPLICIT = 0
+PL_PAYLOAD_SEED = 1
+
+
+class NativeUnavailable(RuntimeError):
+    """libpipelive.so is missing or no CUDA device is visible (no CPU fallback exists)."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str) -> None:
+        super().__init__(msg)
+        self.code = code
+
+
+class StoreInfo(C.Structure):
+    _fields_ = [(name, C.c_int64) for name in (
+        "capacity_blocks", "used_blocks", "free_blocks", "occupied_cells", "n_resident",
+        "tokens_per_block", "stacking_factor", "cell_bytes", "unit_bytes", "fp_header_bytes",
+        "mapped_bytes", "table_max_chain", "table_max_reqs", "n_tables")]
+
+
+i32, i64, u64, dbl, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_void_p
+P = C.POINTER
+
+# (name, restype, argtypes) -- every symbol declared in include/pipelive.h
+SIGNATURES = [
+    ("pl_last_error", C.c_char_p, []),
+    ("pl_abi_version", C.c_int, []),
+    ("pl_device_count", C.c_int, [P(C.c_int)]),
+    ("pl_store_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, i64, C.c_int, i64, vp,
+                                  C.c_int, i64, P(vp)]),
+    ("pl_store_destroy", C.c_int, [vp]),
+    ("pl_store_set_stream", C.c_int, [vp, vp]),
+    ("pl_store_get_info", C.c_int, [vp, P(StoreInfo)]),
+    ("pl_store_add_groups", C.c_int, [vp, vp, C.c_int]),
+    ("pl_store_remove_groups", C.c_int, [vp, vp, C.c_int]),
+    ("pl_store_resident", C.c_int, [vp, vp, C.c_int, P(C.c_int)]),
+    ("pl_store_blocks_needed", C.c_int, [vp, i32, i64, P(i64)]),
+    ("pl_store_chain", C.c_int, [vp, i32, vp, i64, P(i64)]),
+    ("pl_store_chain_slots", C.c_int, [vp, i32, vp, i64, P(i64)]),
+    ("pl_store_written", C.c_int, [vp, i32, vp, vp, C.c_int, P(C.c_int)]),
+    ("pl_store_has_table", C.c_int, [vp, i32, P(C.c_int)]),
+    ("pl_store_tables", C.c_int, [vp, vp, i64, P(i64)]),
+    ("pl_store_blocks", C.c_int, [vp, vp, vp, vp, i64, P(i64)]),
+    ("pl_store_block_occupied", C.c_int, [vp, i64, P(i64)]),
+    ("pl_store_block_occupancy", C.c_int, [vp, i64, C.c_int, vp, C.c_int, P(C.c_int)]),
+    ("pl_store_append", C.c_int, [vp, i32, C.c_int, i64, C.c_int, vp, u64, vp, C.c_int]),
+    ("pl_store_append_batch", C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, C.c_int, P(C.c_int),
+                                        vp, C.c_int]),
+    ("pl_store_write_slots", C.c_int, [vp, i32, C.c_int, i64, vp, vp]),
+    ("pl_store_lookup", C.c_int, [vp, i32, C.c_int, i64, P(u64), P(i64)]),
+    ("pl_store_read_checksum", C.c_int, [vp, i32, C.c_int, i64, P(u64)]),
+    ("pl_store_read_fps", C.c_int, [vp, C.c_int, vp, i64, vp]),
+    ("pl_store_read_cell", C.c_int, [vp, i32, C.c_int, i64, C.c_int, vp, i64]),
+    ("pl_store_compact", C.c_int, [vp, P(i64)]),
+    ("pl_store_resize", C.c_int, [vp, i64]),
+    ("pl_store_drop_groups", C.c_int, [vp, vp, C.c_int, P(i64)]),
+    ("pl_store_free_request", C.c_int, [vp, i32, vp, C.c_int, P(C.c_int)]),
+    ("pl_store_utilization", C.c_int, [vp, P(dbl)]),
+    ("pl_store_last_resize_stats", C.c_int, [vp, vp]),
+    ("pl_store_group_base", C.c_int, [vp, C.c_int, P(u64)]),
+    ("pl_store_table_dev", C.c_int, [vp, P(u64), P(i64)]),
+    ("pl_store_flush", C.c_int, [vp]),
+    ("pl_store_sync", C.c_int, [vp]),
+    ("pl_patch_create", C.c_int, [vp, vp, vp, C.c_int, P(vp)]),
+    ("pl_patch_destroy", C.c_int, [vp]),
+    ("pl_patch_set_active", C.c_int, [vp, C.c_int]),
+    ("pl_patch_mark", C.c_int, [vp, i32, C.c_int, i64, i64]),
+    ("pl_patch_seed", C.c_int, [vp, P(i64)]),
+    ("pl_patch_discard_request", C.c_int, [vp, i32, P(i64)]),
+    ("pl_patch_dirty_keys", C.c_int, [vp, P(i64)]),
+    ("pl_patch_drain", C.c_int, [vp, P(i64), P(i64)]),
+    ("pl_patch_drained_keys", C.c_int, [vp, vp, vp, vp, i64, P(i64)]),
+    ("pl_patch_apply", C.c_int, [vp, vp, vp, i64, vp, i64]),
+    ("pl_patch_push", C.c_int, [vp, vp, vp, i64, P(i64), P(i64)]),
+    ("pl_patch_device_dirty_count", C.c_int, [vp, P(i64)]),
+    ("pl_patch_device_drained", C.c_int, [vp, P(i64)]),
+    ("pl_paged_attn_decode", C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, C.c_float, C.c_int, vp]),
+    ("pl_paged_attn_decode_raw", C.c_int, [vp, i64, i64, C.c_int, C.c_int, C.c_int, vp, vp, vp,
+                                           C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_float, C.c_int, vp]),
+    ("pl_launch_count", i64, []),
+    ("pl_timing_enable", C.c_int, [C.c_int]),
+    ("pl_timing_read", C.c_int, [C.c_char_p, P(dbl), P(i64)]),
+    ("pl_timing_reset", C.c_int, []),
+]
+
+_lib = None
+
+
+def load_library(path: Path | None = None, require_device: bool = True):
+    """Load and type the C-ABI; raise NativeUnavailable when it cannot run here."""
+    global _lib
+    if _lib is not None and path is None:
+        if require_device:
+            _require_device(_lib)
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise NativeUnavailable(
+            f"{p} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(str(p))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    if require_device:
+        _require_device(lib)
+    return lib
+
+
+def _require_device(lib) -> None:
+    n = C.c_int(0)
+    rc = lib.pl_device_count(C.byref(n))
+    if rc != PL_OK or n.value <= 0:
+        raise NativeUnavailable("no CUDA device visible: the pipelive data path is GPU-only "
+                                "(no CPU fallback by design)")
+
+
+def lib():
+    return load_library()
+
+
+def check(rc: int) -> None:
+    if rc != PL_OK:
+        msg = _lib.pl_last_error().decode(errors="replace") if _lib is not None else ""
+        raise NativeError(rc, msg)
+
+
+def ptr(a: np.ndarray | None):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def as_i32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int32))
+
+
+def as_i64(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int64))
+
+
+def as_u64(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.uint64))
+
+
+def launch_count() -> int:
+    return int(lib().pl_launch_count())
+
+
+def timing(kernel: str) -> tuple[float, int]:
+    """(summed device ms, launches) of one instrumented kernel since the last reset."""
+    ms = C.c_double()
+    n = C.c_int64()
+    check(lib().pl_timing_read(kernel.encode(), C.byref(ms), C.byref(n)))
+    return ms.value, n.value

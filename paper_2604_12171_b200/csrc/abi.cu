@@ -1,0 +1,545 @@
+// extern "C" boundary (include/pipelive.h): exceptions -> status codes, plain
+// pointers in and out, no C++ or torch types across the edge.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <mutex>
+
+#include "internal.h"
+
+struct pl_store {
+  pl::Store* s;
+};
+struct pl_patch {
+  pl::Patch* p;
+};
+
+namespace pl {
+namespace {
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+}  // namespace
+
+void fail(int code, const std::string& msg) { throw Error(code, msg); }
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(PL_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void cu_check(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) throw Error(PL_E_CUDA, std::string(what) + " failed with CUresult " + std::to_string((int)r));
+}
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+std::atomic<bool> g_timing{false};
+std::mutex g_timing_mu;
+struct TimedLaunch {
+  cudaEvent_t a, b;
+};
+std::map<std::string, std::vector<TimedLaunch>> g_timed;
+}  // namespace
+
+KernelTimer::KernelTimer(const char* n, cudaStream_t st) : name(n), stream(st) {
+  if (!g_timing.load()) return;
+  if (cudaEventCreate(&start) != cudaSuccess) { start = nullptr; return; }
+  cudaEventRecord(start, stream);
+}
+KernelTimer::~KernelTimer() {
+  if (!start) return;
+  cudaEvent_t end;
+  if (cudaEventCreate(&end) != cudaSuccess) return;
+  cudaEventRecord(end, stream);
+  std::lock_guard<std::mutex> lk(g_timing_mu);
+  g_timed[name].push_back({start, end});
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return PL_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PL_E_INVALID;
+  }
+}
+}  // namespace pl
+
+using pl::guard;
+
+extern "C" {
+
+const char* pl_last_error(void) { return pl::g_err.c_str(); }
+int pl_abi_version(void) { return PL_ABI_VERSION; }
+int64_t pl_launch_count(void) { return pl::g_launches.load(); }
+
+int pl_timing_enable(int on) {
+  pl::g_timing.store(on != 0);
+  return PL_OK;
+}
+int pl_timing_read(const char* kernel, double* total_ms, int64_t* launches) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(pl::g_timing_mu);
+    double ms = 0;
+    int64_t n = 0;
+    auto it = pl::g_timed.find(kernel);
+    if (it != pl::g_timed.end())
+      for (auto& t : it->second) {
+        PL_CUDA(cudaEventSynchronize(t.b));
+        float x = 0;
+        PL_CUDA(cudaEventElapsedTime(&x, t.a, t.b));
+        ms += x;
+        ++n;
+      }
+    *total_ms = ms;
+    *launches = n;
+  });
+}
+int pl_timing_reset(void) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(pl::g_timing_mu);
+    for (auto& kv : pl::g_timed)
+      for (auto& t : kv.second) {
+        cudaEventSynchronize(t.b);
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+      }
+    pl::g_timed.clear();
+  });
+}
+
+int pl_device_count(int* out) {
+  return guard([&] { PL_CUDA(cudaGetDeviceCount(out)); });
+}
+
+int pl_store_create(int device, int gpu_id, int k, int s, int64_t cell_bytes, int n_model_groups,
+                    int64_t capacity, const int32_t* groups, int n_groups, int64_t chunk_bytes,
+                    pl_store** out) {
+  return guard([&] {
+    *out = nullptr;
+    auto* st = new pl::Store(device, gpu_id, k, s, cell_bytes, n_model_groups, capacity, groups,
+                             n_groups, chunk_bytes);
+    *out = new pl_store{st};
+  });
+}
+int pl_store_destroy(pl_store* st) {
+  return guard([&] {
+    if (!st) return;
+    delete st->s;
+    delete st;
+  });
+}
+int pl_store_set_stream(pl_store* st, void* stream) {
+  return guard([&] {
+    PL_CUDA(cudaStreamSynchronize(st->s->stream));
+    st->s->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+int pl_store_get_info(pl_store* st, pl_store_info* o) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    o->capacity_blocks = s->capacity();
+    o->used_blocks = s->used;
+    o->free_blocks = s->free_blocks();
+    o->occupied_cells = s->occupied;
+    o->n_resident = s->n_resident;
+    o->tokens_per_block = s->s;
+    o->stacking_factor = s->k;
+    o->cell_bytes = s->cell_bytes;
+    o->unit_bytes = s->unit_bytes;
+    o->fp_header_bytes = s->fp_bytes;
+    o->mapped_bytes = s->mapped_bytes();
+    o->table_max_chain = s->max_chain;
+    o->table_max_reqs = s->max_reqs;
+    o->n_tables = s->n_tables;
+  });
+}
+int pl_store_add_groups(pl_store* st, const int32_t* groups, int n) {
+  return guard([&] { st->s->add_groups(groups, n); });
+}
+int pl_store_remove_groups(pl_store* st, const int32_t* groups, int n) {
+  return guard([&] { st->s->remove_groups(groups, n); });
+}
+int pl_store_resident(pl_store* st, int32_t* out, int cap, int* n_out) {
+  return guard([&] {
+    int n = 0;
+    for (int g = 0; g < st->s->n_model_groups; ++g)
+      if (st->s->resident[g]) {
+        if (n < cap) out[n] = g;
+        ++n;
+      }
+    *n_out = n;
+  });
+}
+
+int pl_store_blocks_needed(pl_store* st, int32_t req, int64_t extra, int64_t* out) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    const pl::ReqTable* t = s->table(req);
+    const int64_t longest = t ? s->longest_written(*t) : 0;
+    const int64_t have = t ? (int64_t)t->chain.size() : 0;
+    const int64_t need = (longest + extra + s->s - 1) / s->s - have;
+    *out = need > 0 ? need : 0;
+  });
+}
+int pl_store_chain(pl_store* st, int32_t req, int64_t* out, int64_t cap, int64_t* n_out) {
+  return guard([&] {
+    const pl::ReqTable* t = st->s->table(req);
+    *n_out = t ? (int64_t)t->chain.size() : 0;
+    if (t)
+      for (int64_t i = 0; i < *n_out && i < cap; ++i) out[i] = t->chain[i];
+  });
+}
+int pl_store_chain_slots(pl_store* st, int32_t req, int32_t* out, int64_t cap, int64_t* n_out) {
+  return guard([&] {
+    const pl::ReqTable* t = st->s->table(req);
+    *n_out = t ? (int64_t)t->chain.size() : 0;
+    if (t)
+      for (int64_t i = 0; i < *n_out && i < cap; ++i) out[i] = st->s->by_id.at(t->chain[i]).slot;
+  });
+}
+int pl_store_written(pl_store* st, int32_t req, int32_t* groups, int64_t* counts, int cap,
+                     int* n_out) {
+  return guard([&] {
+    const pl::ReqTable* t = st->s->table(req);
+    int n = 0;
+    if (t)
+      for (int32_t g : t->written_order) {
+        if (n < cap) {
+          groups[n] = g;
+          counts[n] = t->written[g];
+        }
+        ++n;
+      }
+    *n_out = n;
+  });
+}
+int pl_store_has_table(pl_store* st, int32_t req, int* out) {
+  return guard([&] { *out = st->s->table(req) != nullptr; });
+}
+int pl_store_tables(pl_store* st, int32_t* out, int64_t cap, int64_t* n_out) {
+  return guard([&] {
+    std::vector<std::pair<int64_t, int32_t>> v;
+    for (int32_t r = 0; r < (int32_t)st->s->tables.size(); ++r)
+      if (st->s->tables[r].present) v.push_back({st->s->tables[r].ins_seq, r});
+    std::sort(v.begin(), v.end());
+    *n_out = (int64_t)v.size();
+    for (int64_t i = 0; i < *n_out && i < cap; ++i) out[i] = v[i].second;
+  });
+}
+int pl_store_blocks(pl_store* st, int64_t* ids, int32_t* owner, int32_t* slot, int64_t cap,
+                    int64_t* n_out) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    *n_out = s->capacity();
+    for (int64_t i = 0; i < *n_out && i < cap; ++i) {
+      const pl::BlockRec& b = s->by_id.at(s->blocks[i]);
+      if (ids) ids[i] = b.id;
+      if (owner) owner[i] = b.owner;
+      if (slot) slot[i] = b.slot;
+    }
+  });
+}
+int pl_store_block_occupied(pl_store* st, int64_t block_id, int64_t* out) {
+  return guard([&] {
+    auto it = st->s->by_id.find(block_id);
+    if (it == st->s->by_id.end()) pl::fail(PL_E_INVALID, "unknown block id");
+    *out = st->s->block_occupied(it->second.slot);
+  });
+}
+int pl_store_block_occupancy(pl_store* st, int64_t block_id, int group, uint64_t* out, int cap,
+                             int* n_words) {
+  return guard([&] {
+    auto it = st->s->by_id.find(block_id);
+    if (it == st->s->by_id.end()) pl::fail(PL_E_INVALID, "unknown block id");
+    if (group < 0 || group >= st->s->n_model_groups) pl::fail(PL_E_INVALID, "group out of range");
+    *n_words = st->s->occ_words;
+    const uint64_t* w = st->s->occ_ptr(it->second.slot, group);
+    for (int i = 0; i < st->s->occ_words && i < cap; ++i) out[i] = w[i];
+  });
+}
+
+int pl_store_append(pl_store* st, int32_t req, int group, int64_t n, int mode,
+                    const uint64_t* payloads, uint64_t seed, const void* kv, int mark) {
+  return guard([&] { st->s->append(req, group, n, mode, payloads, seed, kv, mark); });
+}
+int pl_store_append_batch(pl_store* st, int n_items, const int32_t* reqs, const int32_t* groups,
+                          const int64_t* counts, const uint64_t* seeds, const void* kv, int mark,
+                          int* n_done, int64_t* sched, int n_sched) {
+  int status = PL_OK;
+  int rc = guard([&] {
+    status = st->s->append_batch(n_items, reqs, groups, counts, seeds, kv, mark, sched, n_sched,
+                                 n_done);
+  });
+  if (rc != PL_OK) return rc;
+  if (status != PL_OK) pl::g_err = st->s->last_msg;
+  return status;
+}
+int pl_store_write_slots(pl_store* st, int32_t req, int group, int64_t n, const int64_t* pos,
+                         const uint64_t* payloads) {
+  return guard([&] { st->s->write_slots(req, group, n, pos, payloads); });
+}
+
+int pl_store_lookup(pl_store* st, int32_t req, int layer, int64_t token, uint64_t* addr,
+                    int64_t* off) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    const int g = (layer - 1) / s->k;
+    const pl::ReqTable* t = s->table(req);
+    if (!t || token < 0 || g < 0 || g >= s->n_model_groups || token >= t->written[g])
+      pl::fail(PL_E_UNKNOWN_SLOT, "request " + std::to_string(req) + " layer " +
+                                      std::to_string(layer) + " token " + std::to_string(token));
+    *addr = s->address_of(t->chain[token / s->s]);
+    *off = token % s->s;
+  });
+}
+
+int pl_store_read_fps(pl_store* st, int group, const int32_t* slots, int64_t n, uint64_t* out) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    if (group < 0 || group >= s->n_model_groups || !s->materialised[group])
+      pl::fail(PL_E_INVALID, "group has no pool");
+    if (n <= 0) return;
+    s->flush();
+    pl::Upload up(s);
+    int a = up.add(slots, (size_t)n * 4);
+    up.go((size_t)n * s->s * 8);
+    uint64_t* d_out = reinterpret_cast<uint64_t*>(up.extra());
+    pl::launch_read_fps(s->group_base(group), s->unit_bytes, up.ptr<int32_t>(a), n, s->s, d_out,
+                        s->stream);
+    PL_CUDA(cudaMemcpyAsync(out, d_out, (size_t)n * s->s * 8, cudaMemcpyDeviceToHost, s->stream));
+    PL_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int pl_store_read_checksum(pl_store* st, int32_t req, int group, int64_t token, uint64_t* out) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    const pl::ReqTable* t = s->table(req);
+    if (!t || group < 0 || group >= s->n_model_groups || token < 0 || token >= t->written[group])
+      pl::fail(PL_E_UNKNOWN_SLOT, "request " + std::to_string(req) + " group " +
+                                      std::to_string(group) + " token " + std::to_string(token));
+    const int32_t slot = s->by_id.at(t->chain[token / s->s]).slot;
+    if (!s->occ_test(slot, group, (int)(token % s->s)))
+      pl::fail(PL_E_UNKNOWN_SLOT, "cell never written");
+    s->flush();
+    const uint64_t* p = reinterpret_cast<const uint64_t*>(
+        s->group_base(group) + (uint64_t)slot * s->unit_bytes) + token % s->s;
+    PL_CUDA(cudaMemcpyAsync(out, p, 8, cudaMemcpyDeviceToHost, s->stream));
+    PL_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int pl_store_read_cell(pl_store* st, int32_t req, int group, int64_t token, int j, void* out,
+                       int64_t nbytes) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    const pl::ReqTable* t = s->table(req);
+    if (!t || group < 0 || group >= s->n_model_groups || token < 0 || token >= t->written[group])
+      pl::fail(PL_E_UNKNOWN_SLOT, "cell out of range");
+    if (j < 0 || j >= s->k || nbytes > s->cell_bytes) pl::fail(PL_E_INVALID, "bad layer/size");
+    const int32_t slot = s->by_id.at(t->chain[token / s->s]).slot;
+    s->flush();
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(s->group_base(group)) +
+                       (int64_t)slot * s->unit_bytes + s->fp_bytes +
+                       ((int64_t)j * s->s + token % s->s) * s->cell_bytes;
+    PL_CUDA(cudaMemcpyAsync(out, p, nbytes, cudaMemcpyDeviceToHost, s->stream));
+    PL_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int pl_store_compact(pl_store* st, int64_t* out) {
+  return guard([&] {
+    const int64_t n = st->s->compact();
+    if (out) *out = n;
+  });
+}
+int pl_store_resize(pl_store* st, int64_t cap) {
+  return guard([&] { st->s->resize(cap); });
+}
+int pl_store_drop_groups(pl_store* st, const int32_t* groups, int n, int64_t* out) {
+  return guard([&] {
+    const int64_t f = st->s->drop_groups(groups, n);
+    if (out) *out = f;
+  });
+}
+int pl_store_free_request(pl_store* st, int32_t req, int64_t* stats, int cap, int* n_stats) {
+  return guard([&] { *n_stats = st->s->free_request(req, stats, cap); });
+}
+int pl_store_utilization(pl_store* st, double* out) {
+  return guard([&] { *out = st->s->utilization(); });
+}
+int pl_store_last_resize_stats(pl_store* st, int64_t* out4) {
+  return guard([&] {
+    for (int i = 0; i < 4; ++i) out4[i] = st->s->last_resize[i];
+  });
+}
+int pl_store_group_base(pl_store* st, int group, uint64_t* out) {
+  return guard([&] {
+    if (group < 0 || group >= st->s->n_model_groups) pl::fail(PL_E_INVALID, "group out of range");
+    *out = st->s->materialised[group] ? st->s->group_base(group) : 0;
+  });
+}
+int pl_store_table_dev(pl_store* st, uint64_t* ptr, int64_t* stride) {
+  return guard([&] {
+    st->s->flush();
+    *ptr = (uint64_t)st->s->d_table;
+    *stride = st->s->max_chain;
+  });
+}
+int pl_store_flush(pl_store* st) {
+  return guard([&] { st->s->flush(); });
+}
+int pl_store_sync(pl_store* st) {
+  return guard([&] {
+    st->s->flush();
+    PL_CUDA(cudaStreamSynchronize(st->s->stream));
+  });
+}
+
+// ---- patch
+int pl_patch_create(pl_store* src, const int32_t* groups, const int32_t* layers, int n,
+                    pl_patch** out) {
+  return guard([&] {
+    *out = nullptr;
+    auto* p = new pl::Patch(src->s, groups, layers, n);
+    *out = new pl_patch{p};
+  });
+}
+int pl_patch_destroy(pl_patch* p) {
+  return guard([&] {
+    if (!p) return;
+    delete p->p;
+    delete p;
+  });
+}
+int pl_patch_set_active(pl_patch* p, int active) {
+  return guard([&] { p->p->active = active != 0; });
+}
+int pl_patch_mark(pl_patch* p, int32_t req, int group, int64_t start, int64_t n) {
+  return guard([&] { p->p->mark(req, group, start, n, true); });
+}
+int pl_patch_seed(pl_patch* p, int64_t* out) {
+  return guard([&] { *out = p->p->seed(); });
+}
+int pl_patch_discard_request(pl_patch* p, int32_t req, int64_t* out) {
+  return guard([&] { *out = p->p->discard(req); });
+}
+int pl_patch_dirty_keys(pl_patch* p, int64_t* out) {
+  return guard([&] { *out = p->p->dirty_keys; });
+}
+int pl_patch_drain(pl_patch* p, int64_t* keys, int64_t* cells) {
+  return guard([&] { p->p->drain(keys, cells); });
+}
+int pl_patch_drained_keys(pl_patch* p, int32_t* reqs, int32_t* groups, int64_t* pos, int64_t cap,
+                          int64_t* n_out) {
+  return guard([&] {
+    int64_t n = 0;
+    for (auto& e : p->p->drained)
+      for (const pl::Interval& iv : std::get<2>(e))
+        for (int64_t x = iv.a; x < iv.b; ++x) {
+          if (n < cap) {
+            reqs[n] = std::get<0>(e);
+            groups[n] = p->p->groups[std::get<1>(e)];
+            pos[n] = x;
+          }
+          ++n;
+        }
+    *n_out = n;
+  });
+}
+int pl_patch_apply(pl_patch* p, pl_store* dst, const int32_t* rank, int64_t n_rank,
+                   const uint8_t* stale, int64_t n_stale) {
+  return guard([&] { p->p->apply(dst->s, rank, n_rank, stale, n_stale); });
+}
+int pl_patch_push(pl_patch* p, pl_store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
+                  int64_t* cells) {
+  return guard([&] { p->p->push(dst->s, rank, n_rank, keys, cells); });
+}
+int pl_patch_device_dirty_count(pl_patch* p, int64_t* out) {
+  return guard([&] { *out = p->p->device_dirty_count(); });
+}
+int pl_patch_device_drained(pl_patch* p, int64_t* out) {
+  return guard([&] {
+    pl::Patch* q = p->p;
+    PL_CUDA(cudaMemcpyAsync(out, q->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, q->src->stream));
+    PL_CUDA(cudaStreamSynchronize(q->src->stream));
+  });
+}
+
+// ---- K2
+int pl_paged_attn_decode(pl_store* st, int group, int layer, const void* q, void* out,
+                         const int32_t* rows, const int32_t* ctx, int B, int n_q, int n_kv, int D,
+                         float scale, int max_ctx, void* stream) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    if (group < 0 || group >= s->n_model_groups || !s->materialised[group])
+      pl::fail(PL_E_INVALID, "group has no pool");
+    if ((int64_t)2 * n_kv * D * 2 != s->cell_bytes)
+      pl::fail(PL_E_INVALID, "cell_bytes != 2 * n_kv_heads * head_dim * 2");
+    if (layer < 0 || layer >= s->k) pl::fail(PL_E_INVALID, "layer_in_group out of range");
+    s->flush();
+    cudaStream_t cs = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+    if (cs != s->stream) {
+      // table deltas were pushed on the store stream
+      cudaEvent_t ev;
+      PL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      PL_CUDA(cudaEventRecord(ev, s->stream));
+      PL_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+      PL_CUDA(cudaEventDestroy(ev));
+    }
+    pl::AttnLaunch a{};
+    a.pool = reinterpret_cast<const uint8_t*>(s->group_base(group));
+    a.unit_bytes = s->unit_bytes;
+    a.fp_bytes = s->fp_bytes;
+    a.s = s->s;
+    a.k = s->k;
+    a.layer = layer;
+    a.table = s->d_table;
+    a.table_stride = s->max_chain;
+    a.rows = rows;
+    a.ctx = ctx;
+    a.B = B;
+    a.n_q = n_q;
+    a.n_kv = n_kv;
+    a.D = D;
+    a.scale = scale;
+    a.max_ctx = max_ctx;
+    a.q = q;
+    a.out = out;
+    pl::launch_paged_attn(a, cs);
+  });
+}
+int pl_paged_attn_decode_raw(const void* pool, int64_t unit_bytes, int64_t fp_bytes, int s, int k,
+                             int layer, const void* q, void* out, const int32_t* tables,
+                             int max_blocks, const int32_t* ctx, int B, int n_q, int n_kv, int D,
+                             float scale, int max_ctx, void* stream) {
+  return guard([&] {
+    pl::AttnLaunch a{};
+    a.pool = static_cast<const uint8_t*>(pool);
+    a.unit_bytes = unit_bytes;
+    a.fp_bytes = fp_bytes;
+    a.s = s;
+    a.k = k;
+    a.layer = layer;
+    a.table = tables;
+    a.table_stride = max_blocks;
+    a.rows = nullptr;
+    a.ctx = ctx;
+    a.B = B;
+    a.n_q = n_q;
+    a.n_kv = n_kv;
+    a.D = D;
+    a.scale = scale;
+    a.max_ctx = max_ctx;
+    a.q = q;
+    a.out = out;
+    pl::launch_paged_attn(a, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,354 @@
+// Internal declarations of libpipelive: host-side block manager (Store), the
+// per-pair patch engine (Patch), the VMM-backed pool arenas and the kernel
+// launchers.  Only pl_abi.cu exposes anything to the outside (include/pipelive.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/pipelive.h"
+
+namespace pl {
+
+// ---------------------------------------------------------------------------
+// errors: thrown inside the library, converted to status codes at the ABI edge
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+void cu_check(CUresult r, const char* what);
+#define PL_CUDA(x) ::pl::cuda_check((x), #x)
+
+void note_launch(int n = 1);  // kernel launch accounting for the bench
+// RAII CUDA-event bracket around one launch (only when timing is enabled)
+struct KernelTimer {
+  const char* name;
+  cudaStream_t stream;
+  cudaEvent_t start = nullptr;
+  KernelTimer(const char* name, cudaStream_t st);
+  ~KernelTimer();
+};
+
+// ---------------------------------------------------------------------------
+// Arena: one reserved virtual range backed by physical chunks mapped with the
+// CUDA VMM driver API.  Pools grow/shrink by mapping/unmapping chunks at the
+// tail; the base address only changes if the reservation itself must grow.
+struct Arena {
+  int device = 0;
+  CUdeviceptr va = 0;
+  size_t va_bytes = 0;
+  size_t chunk_bytes = 0;
+  std::vector<CUmemGenericAllocationHandle> chunks;
+  std::vector<int> peer_devices;  // devices granted access besides `device`
+
+  size_t mapped_bytes() const { return chunks.size() * chunk_bytes; }
+  void ensure(size_t bytes);  // map chunks until mapped >= bytes
+  void trim(size_t bytes);    // unmap chunks wholly beyond `bytes`
+  void release();
+  void grant_peer(int dev);
+};
+size_t vmm_granularity(int device);
+
+// ---------------------------------------------------------------------------
+struct BlockRec {
+  int64_t id = -1;
+  int32_t slot = -1;
+  int32_t owner = -1;      // request handle, -1 = free
+  int32_t chain_idx = -1;  // position in the owner's chain
+};
+
+struct ReqTable {
+  bool present = false;
+  int64_t ins_seq = 0;                // dict insertion order of KvStore.tables
+  std::vector<int64_t> chain;         // block ids
+  std::vector<int64_t> written;       // per model group; 0 = absent
+  std::vector<int32_t> written_order; // groups in dict insertion order
+};
+
+struct Patch;
+struct Interval { int64_t a, b; };  // [a, b)
+
+// Store: one KvStore (kvstore.py:88-360) on one device.  Host side keeps the
+// exact block-id policy; the device holds the KV units, fingerprint headers and
+// the block table the kernels resolve addresses through.
+struct Store {
+  int device = 0, gpu_id = 0, k = 1, s = 1, n_model_groups = 0;
+  int64_t cell_bytes = 0, fp_bytes = 0, unit_bytes = 0, chunk_bytes = 0;
+  cudaStream_t stream = nullptr;
+
+  // block manager state (reference semantics)
+  std::vector<int64_t> blocks;                    // list order
+  std::unordered_map<int64_t, BlockRec> by_id;
+  std::set<int64_t> free_ids;                     // == lazily invalidated heap
+  std::vector<int64_t> slot_block;                // slot -> block id or -1
+  int64_t serial = 0, used = 0, occupied = 0, ins_counter = 0;
+  std::vector<ReqTable> tables;                   // indexed by request handle
+  int64_t n_tables = 0;
+  std::vector<uint8_t> resident;                  // per model group
+  int64_t n_resident = 0;
+
+  // occupancy bitmasks: [slot][model group][occ_words] (PhysicalBlock.cells keys)
+  int occ_words = 1;
+  std::vector<uint64_t> occ;
+
+  // device: per-group pool arenas (materialised iff resident or written)
+  std::vector<Arena> arenas;
+  std::vector<uint8_t> materialised;
+
+  // device block table: table[req * max_chain + idx] = slot; owner maps by slot
+  int32_t* d_table = nullptr;
+  int64_t max_reqs = 0, max_chain = 0;
+  int32_t* d_owner = nullptr;
+  int32_t* d_owner_idx = nullptr;
+  int64_t owner_cap = 0;
+  std::vector<int32_t> h_table, h_owner, h_owner_idx;
+  struct Delta { int32_t which; int64_t idx; int32_t val; };
+  std::vector<Delta> deltas;
+  std::vector<int32_t> released_slots;  // dirty bits to clear in attached patches
+  // scratch
+  void* d_scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void* h_pinned = nullptr;
+  size_t pinned_bytes = 0;
+  cudaEvent_t pinned_ev = nullptr;
+
+  std::vector<Patch*> patches;  // patches whose source is this store
+  uint64_t* d_bases_ = nullptr;  // device copy of the per-group arena bases
+  std::string last_msg;
+  void refresh_bases();
+  int64_t last_resize[4] = {0, 0, 0, 0};
+
+  Store(int device, int gpu_id, int k, int s, int64_t cell_bytes, int n_model_groups,
+        int64_t capacity, const int32_t* groups, int n_groups, int64_t chunk_bytes);
+  ~Store();
+
+  // --- accounting
+  int64_t capacity() const { return (int64_t)blocks.size(); }
+  int64_t free_blocks() const { return capacity() - used; }
+  uint64_t address_of(int64_t block_id) const {
+    return ((uint64_t)gpu_id << 44) | ((uint64_t)block_id << 21);
+  }
+  ReqTable* table(int32_t req);
+  ReqTable& table_create(int32_t req);
+  void table_delete(int32_t req);
+  int64_t longest_written(const ReqTable& t) const;
+
+  // --- block manager (kvstore.py:111-134)
+  int64_t new_block();
+  BlockRec& alloc_block(int32_t req);
+  void release_block(BlockRec& b);
+  void extend_chain(int32_t req, ReqTable& t, int64_t needed);
+
+  // --- occupancy
+  uint64_t* occ_ptr(int32_t slot, int g) {
+    return &occ[((size_t)slot * n_model_groups + g) * occ_words];
+  }
+  bool occ_test(int32_t slot, int g, int off) {
+    return (occ_ptr(slot, g)[off >> 6] >> (off & 63)) & 1ull;
+  }
+  int64_t occ_set_range(int32_t slot, int g, int a, int b);  // returns newly set
+  int64_t block_occupied(int32_t slot);
+  int64_t group_occupied(int32_t slot, int g);
+
+  // --- device mirrors
+  void ensure_table(int64_t req, int64_t chain_len);
+  void ensure_owner(int64_t slots);
+  void set_table(int32_t req, int64_t idx, int32_t slot);
+  void set_owner(int32_t slot, int32_t req, int32_t idx);
+  void flush();
+  void* scratch(size_t bytes);
+  void* pinned(size_t bytes);
+  void materialise(int g);
+  void dematerialise(int g);
+  uint64_t group_base(int g) const { return (uint64_t)arenas[g].va; }
+  int64_t mapped_bytes() const;
+
+  // --- operations (reference semantics)
+  void append(int32_t req, int g, int64_t n, int mode, const uint64_t* payloads, uint64_t seed,
+              const void* kv_dev, int mark);
+  int append_batch(int n_items, const int32_t* reqs, const int32_t* groups,
+                   const int64_t* counts, const uint64_t* seeds, const void* kv_dev, int mark,
+                   int64_t* sched, int n_sched, int* n_done);  // returns status
+  void write_slots(int32_t req, int g, int64_t n, const int64_t* pos, const uint64_t* payloads);
+  int64_t compact();
+  void resize(int64_t new_cap);
+  int64_t drop_groups(const int32_t* groups, int n);
+  int free_request(int32_t req, int64_t* stats, int cap);
+  double utilization() const;
+  void add_groups(const int32_t* groups, int n);
+  void remove_groups(const int32_t* groups, int n);
+  // write_slots bookkeeping (kvstore.py:201-227) for sorted disjoint position intervals,
+  // without the device write; throws KvOverflow like the reference
+  void reserve_positions(int32_t req, int g, const std::vector<Interval>& iv);
+
+  // launch K1 for a list of (req, group, start, count) items
+  struct WriteItem { int32_t req; int32_t group; int64_t start; int64_t count; uint64_t seed; };
+  void launch_write(const std::vector<WriteItem>& items, int mode, const uint64_t* payloads,
+                    const int64_t* positions, const void* kv_dev, int mark);
+};
+
+// ---------------------------------------------------------------------------
+// Packs host arrays into the store's pinned buffer and ships them in one H2D
+// copy on the store's stream; pointers are valid until the next Upload there.
+struct Upload {
+  Store* st;
+  std::vector<std::pair<const void*, size_t>> parts;
+  std::vector<size_t> offs;
+  size_t total = 0;
+  uint8_t* dev = nullptr;
+  explicit Upload(Store* s) : st(s) {}
+  int add(const void* p, size_t bytes);
+  void go(size_t extra_device_bytes = 0);
+  template <class T>
+  T* ptr(int i) { return reinterpret_cast<T*>(dev + offs[i]); }
+  uint8_t* extra() { return dev + total; }
+};
+
+// ---------------------------------------------------------------------------
+// Patch: sender + receiver data plane of one migrating pair.
+
+struct Patch {
+  Store* src = nullptr;
+  std::vector<int32_t> groups;           // model groups of the pair (sorted)
+  std::vector<int32_t> layers_in_group;  // pair layers inside each group
+  std::vector<int32_t> local_of;         // model group -> local index or -1
+  int G = 0;
+  bool active = false;
+
+  // host mirror of the dirty set: (req, local group) -> disjoint sorted intervals
+  std::map<std::pair<int32_t, int32_t>, std::vector<Interval>> dirty;
+  int64_t dirty_keys = 0;
+
+  // device bitmap over source cells: bit ((slot*G + lg)*s + off)
+  uint32_t* d_bits = nullptr;
+  uint32_t* d_snap = nullptr;
+  int32_t* d_local_of = nullptr;  // device copy of local_of
+  int64_t bit_slots = 0;  // slots covered
+  int64_t n_words = 0;
+
+  // scan scratch + drained list
+  int64_t* d_tile_counts = nullptr;
+  int64_t n_tiles_cap = 0;
+  int64_t* d_count = nullptr;   // [0] = drained keys on device, [1] = scratch
+  int64_t* d_cells = nullptr;   // compacted drained bit indices
+  int64_t cells_cap = 0;
+
+  cudaEvent_t ev_gathered = nullptr, ev_applied = nullptr, ev_dst = nullptr;
+  bool applied_recorded = false;
+  // staging of the in-flight patch: rows of [fp 8B][k * cell_bytes]; keys
+  uint8_t* d_rows = nullptr;
+  int32_t* d_keys = nullptr;    // (req, lg, pos_lo, pos_hi) per row
+  int64_t rows_cap = 0;
+  bool in_flight = false;
+  std::vector<std::tuple<int32_t, int32_t, std::vector<Interval>>> drained;
+  int64_t drained_keys = 0;
+  int64_t last_device_drained = -1;
+
+  Patch(Store* src, const int32_t* groups, const int32_t* layers, int n);
+  ~Patch();
+
+  void ensure_bits();
+  void mark(int32_t req, int g, int64_t start, int64_t n, bool device = true);
+  void mark_device(const std::vector<Store::WriteItem>& items);  // batch
+  int64_t seed();
+  int64_t discard(int32_t req);
+  void clear_slots_device(const std::vector<int32_t>& slots);
+  void move_slots_device(const std::vector<std::pair<int32_t, int32_t>>& moves);
+  int64_t host_cells(const std::vector<std::tuple<int32_t, int32_t, std::vector<Interval>>>& d);
+  int64_t take_drained();               // host snapshot -> drained
+  int64_t device_drain_compact();       // K3 into d_cells; returns host-known count
+  void drain(int64_t* keys, int64_t* cells);
+  void extend_dst(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
+                  int64_t n_stale, std::vector<uint8_t>& apply_mask, int* status);
+  void apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
+             int64_t n_stale);
+  void push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells);
+  int64_t device_dirty_count();
+  int32_t* d_groups_ = nullptr;
+  const int32_t* d_groups();
+};
+
+// ---------------------------------------------------------------------------
+// kernel launchers (kernels.cu)
+struct WriteLaunch {
+  // items
+  const int32_t* reqs; const int32_t* groups; const int64_t* starts; const int64_t* offs;
+  const uint64_t* seeds; int n_items; int64_t total;
+  // payload sources
+  int mode; const uint64_t* payloads; const int64_t* positions; const uint8_t* kv;
+  // store layout
+  const uint64_t* group_bases;  // device array [n_model_groups]
+  const int32_t* table; int64_t max_chain;
+  int s, k; int64_t cell_bytes, fp_bytes, unit_bytes;
+  // fused dirty marks: up to 4 patches
+  int n_marks; uint32_t* bits[4]; const int32_t* local_of[4]; int G[4];
+};
+void launch_kv_write(const WriteLaunch& w, cudaStream_t st);
+
+void launch_apply_deltas(int32_t* table, int32_t* owner, int32_t* owner_idx,
+                         const int64_t* idx, const int32_t* val, const int32_t* which, int64_t n,
+                         cudaStream_t st);
+
+struct MarkLaunch {
+  const int32_t* reqs; const int32_t* lgs; const int64_t* starts; const int64_t* offs;
+  int n_items; int64_t total;
+  const int32_t* table; int64_t max_chain; int s; int G; uint32_t* bits;
+};
+void launch_mark(const MarkLaunch& m, cudaStream_t st);
+void launch_clear_slots(uint32_t* bits, int G, int s, const int32_t* slots, int64_t n,
+                        cudaStream_t st);
+void launch_move_slots(uint32_t* bits, int G, int s, const int32_t* from, const int32_t* to,
+                       int64_t n, cudaStream_t st);
+void launch_unit_move(const uint64_t* bases, const int32_t* groups, int n_groups,
+                      const int32_t* from, const int32_t* to, int64_t n_moves,
+                      int64_t unit_bytes, cudaStream_t st);
+void launch_table_remap(int32_t* table, int64_t n_entries, const int32_t* remap, int64_t n_remap,
+                        cudaStream_t st);
+void launch_popcount(const uint32_t* bits, int64_t n_words, int64_t* out, cudaStream_t st);
+
+// K3: snapshot+clear, tile counts, scan, emit
+int64_t drain_tiles(int64_t n_words);
+void launch_drain_snapshot(uint32_t* bits, uint32_t* snap, int64_t n_words, int64_t* tile_counts,
+                           cudaStream_t st);
+void launch_drain_scan(int64_t* tile_counts, int64_t n_tiles, int64_t* total, cudaStream_t st);
+void launch_drain_emit(const uint32_t* snap, int64_t n_words, const int64_t* tile_offsets,
+                       int64_t* cells, int64_t cells_cap, cudaStream_t st);
+
+struct CopyLaunch {
+  int mode;  // 0 gather (pool->rows), 1 scatter (rows->pool), 2 push (pool->pool)
+  const int64_t* cells; const int64_t* count; int64_t n_hint;
+  int G; int k; int64_t cell_bytes, fp_bytes;
+  // source pool
+  const uint64_t* src_bases; const int32_t* src_groups; int src_s; int64_t src_unit;
+  const int32_t* src_owner; const int32_t* src_owner_idx;
+  // destination pool
+  const uint64_t* dst_bases; int dst_s; int64_t dst_unit; const int32_t* dst_table;
+  int64_t dst_max_chain; const uint8_t* apply_mask;
+  // staging
+  uint8_t* rows; int32_t* keys; int64_t row_bytes;
+};
+void launch_copy(const CopyLaunch& c, cudaStream_t st);
+
+void launch_read_fps(uint64_t base, int64_t unit_bytes, const int32_t* slots, int64_t n, int s,
+                     uint64_t* out, cudaStream_t st);
+
+// K2
+struct AttnLaunch {
+  const uint8_t* pool; int64_t unit_bytes, fp_bytes; int s, k, layer;
+  const int32_t* table; int64_t table_stride; const int32_t* rows;  // rows may be null
+  const int32_t* ctx; int B, n_q, n_kv, D; float scale; int max_ctx;
+  const void* q; void* out;
+};
+void launch_paged_attn(const AttnLaunch& a, cudaStream_t st);
+
+}  // namespace pl

@@ -1,0 +1,449 @@
+// Data-plane kernels of the live-reconfiguration path (sm_100a).
+//
+//   K1  kv_write_mark  : KvStore.append / write_slots (kvstore.py:163-227) fused with the
+//                        DirtyBitmap.mark of MigrationStream.on_kv_written (migrator.py:190-197)
+//   K3  drain          : DirtyBitmap.drain (migrator.py:38-41) = atomic snapshot+clear,
+//                        ballot/popc tile counts, scan, ordered compaction
+//   K4/K5 copy         : _drain read loop (migrator.py:231-235) gather into staging,
+//                        PatchReceiver._apply -> write_slots (migrator.py:115-131) scatter,
+//                        and the fused gather->scatter "push" (no staging)
+//   K6 remap           : relocation of live units + block-table remap for KvStore.resize
+//                        (kvstore.py:259-282) so the pool's physical tail can be unmapped
+//
+// All of these are HBM-bound byte movers: 128-bit accesses, one warp per 16B-aligned
+// cell row, grid sized to the SM count, no tensor cores.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace pl {
+
+namespace {
+constexpr int kWarps = 8;  // warps per CTA for the copy-type kernels
+int g_sm_count = 0;
+int sm_count() {
+  if (!g_sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  return g_sm_count;
+}
+int64_t grid_for(int64_t work_items, int per_block, int waves = 8) {
+  int64_t need = (work_items + per_block - 1) / per_block;
+  int64_t cap = (int64_t)sm_count() * waves;
+  if (need < 1) need = 1;
+  return need < cap ? need : cap;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// K1: one warp per written token; writes the fingerprint header word and the k
+// layer cells (expansion of the fingerprint, or real KV bytes), and sets the
+// token's bit in every attached dirty bitmap.
+__global__ void __launch_bounds__(kWarps * 32) kv_write_kernel(WriteLaunch w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t vec_per_cell = w.cell_bytes >> 4;
+  for (int64_t t = warp0; t < w.total; t += nwarps) {
+    const int it = find_item(w.offs, w.n_items, t);
+    const int32_t req = w.reqs[it];
+    const int32_t g = w.groups[it];
+    const int64_t pos = w.positions ? w.positions[t] : w.starts[it] + (t - w.offs[it]);
+    const uint64_t fp = w.mode == PL_PAYLOAD_SEED ? cell_fingerprint(w.seeds[it], (uint64_t)pos)
+                                                  : w.payloads[t];
+    const int32_t slot = w.table[(int64_t)req * w.max_chain + pos / w.s];
+    if (slot < 0) continue;  // host guarantees the chain covers pos
+    const int off = (int)(pos % w.s);
+    uint8_t* unit = reinterpret_cast<uint8_t*>(w.group_bases[g]) + (int64_t)slot * w.unit_bytes;
+    if (lane == 0) reinterpret_cast<uint64_t*>(unit)[off] = fp;
+    for (int j = 0; j < w.k; ++j) {
+      int4* cell = reinterpret_cast<int4*>(unit + w.fp_bytes + ((int64_t)j * w.s + off) * w.cell_bytes);
+      if (w.kv) {
+        const int4* src = reinterpret_cast<const int4*>(w.kv + (t * w.k + j) * w.cell_bytes);
+        for (int64_t v = lane; v < vec_per_cell; v += 32) st_stream(cell + v, ld_stream(src + v));
+      } else {
+        for (int64_t v = lane; v < vec_per_cell; v += 32) {
+          uint64_t a = expand_word(fp, (uint32_t)j, (uint32_t)(2 * v));
+          uint64_t b = expand_word(fp, (uint32_t)j, (uint32_t)(2 * v + 1));
+          int4 val;
+          val.x = (int)(uint32_t)a; val.y = (int)(uint32_t)(a >> 32);
+          val.z = (int)(uint32_t)b; val.w = (int)(uint32_t)(b >> 32);
+          st_stream(cell + v, val);
+        }
+      }
+    }
+    if (lane < w.n_marks) {
+      const int lg = w.local_of[lane][g];
+      if (lg >= 0) {
+        const int64_t bit = ((int64_t)slot * w.G[lane] + lg) * w.s + off;
+        atomicOr(w.bits[lane] + (bit >> 5), 1u << (bit & 31));
+      }
+    }
+  }
+}
+
+void launch_kv_write(const WriteLaunch& w, cudaStream_t st) {
+  if (w.total <= 0) return;
+  int64_t grid = grid_for(w.total, kWarps);
+  KernelTimer timer("kv_write", st);
+  kv_write_kernel<<<(unsigned)grid, kWarps * 32, 0, st>>>(w);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// block-table / owner-map deltas (host mirror -> device), deduplicated on host
+__global__ void apply_deltas_kernel(int32_t* table, int32_t* owner, int32_t* owner_idx,
+                                    const int64_t* idx, const int32_t* val, const int32_t* which,
+                                    int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t* dst = which[i] == 0 ? table : (which[i] == 1 ? owner : owner_idx);
+    dst[idx[i]] = val[i];
+  }
+}
+void launch_apply_deltas(int32_t* table, int32_t* owner, int32_t* owner_idx, const int64_t* idx,
+                         const int32_t* val, const int32_t* which, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  apply_deltas_kernel<<<(unsigned)grid_for(n, 256), 256, 0, st>>>(table, owner, owner_idx, idx,
+                                                                   val, which, n);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// dirty marks of token intervals (MigrationStream.on_kv_written, start seeding)
+__global__ void mark_kernel(MarkLaunch m) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m.total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int it = find_item(m.offs, m.n_items, t);
+    const int64_t pos = m.starts[it] + (t - m.offs[it]);
+    const int32_t slot = m.table[(int64_t)m.reqs[it] * m.max_chain + pos / m.s];
+    if (slot < 0) continue;
+    const int64_t bit = ((int64_t)slot * m.G + m.lgs[it]) * m.s + pos % m.s;
+    atomicOr(m.bits + (bit >> 5), 1u << (bit & 31));
+  }
+}
+void launch_mark(const MarkLaunch& m, cudaStream_t st) {
+  if (m.total <= 0) return;
+  mark_kernel<<<(unsigned)grid_for(m.total, 256), 256, 0, st>>>(m);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+__global__ void clear_slots_kernel(uint32_t* bits, int G, int s, const int32_t* slots, int64_t n) {
+  const int64_t per = (int64_t)G * s;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * per;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bit = (int64_t)slots[i / per] * per + i % per;
+    atomicAnd(bits + (bit >> 5), ~(1u << (bit & 31)));
+  }
+}
+void launch_clear_slots(uint32_t* bits, int G, int s, const int32_t* slots, int64_t n,
+                        cudaStream_t st) {
+  if (n <= 0) return;
+  clear_slots_kernel<<<(unsigned)grid_for(n * G * s, 256), 256, 0, st>>>(bits, G, s, slots, n);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+// relocated units carry their dirty bits: to <- from, from <- 0 (destinations are free slots)
+__global__ void move_slots_kernel(uint32_t* bits, int G, int s, const int32_t* from,
+                                  const int32_t* to, int64_t n) {
+  const int64_t per = (int64_t)G * s;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * per;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / per, r = i % per;
+    const int64_t bf = (int64_t)from[m] * per + r, bt = (int64_t)to[m] * per + r;
+    const uint32_t was = atomicAnd(bits + (bf >> 5), ~(1u << (bf & 31)));
+    if ((was >> (bf & 31)) & 1u) atomicOr(bits + (bt >> 5), 1u << (bt & 31));
+  }
+}
+void launch_move_slots(uint32_t* bits, int G, int s, const int32_t* from, const int32_t* to,
+                       int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  move_slots_kernel<<<(unsigned)grid_for(n * G * s, 256), 256, 0, st>>>(bits, G, s, from, to, n);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+// K6a: copy whole units of relocated live blocks (every materialised group)
+__global__ void unit_move_kernel(const uint64_t* bases, const int32_t* groups, int n_groups,
+                                 const int32_t* from, const int32_t* to, int64_t n_moves,
+                                 int64_t unit_bytes) {
+  const int64_t vecs = unit_bytes >> 4;
+  for (int64_t job = blockIdx.x; job < n_moves * n_groups; job += gridDim.x) {
+    const int64_t m = job / n_groups;
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(bases[groups[job % n_groups]]);
+    const int4* src = reinterpret_cast<const int4*>(base + (int64_t)from[m] * unit_bytes);
+    int4* dst = reinterpret_cast<int4*>(const_cast<uint8_t*>(base) + (int64_t)to[m] * unit_bytes);
+    for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) st_stream(dst + v, ld_plain(src + v));
+  }
+}
+void launch_unit_move(const uint64_t* bases, const int32_t* groups, int n_groups,
+                      const int32_t* from, const int32_t* to, int64_t n_moves,
+                      int64_t unit_bytes, cudaStream_t st) {
+  if (n_moves <= 0 || n_groups <= 0) return;
+  KernelTimer timer("unit_move", st);
+  unit_move_kernel<<<(unsigned)grid_for(n_moves * n_groups, 1), 256, 0, st>>>(
+      bases, groups, n_groups, from, to, n_moves, unit_bytes);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+// K6b: block-table remap: every table entry v -> remap[v]
+__global__ void table_remap_kernel(int32_t* table, int64_t n, const int32_t* remap,
+                                   int64_t n_remap) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = table[i];
+    if (v >= 0 && v < n_remap) table[i] = remap[v];
+  }
+}
+void launch_table_remap(int32_t* table, int64_t n, const int32_t* remap, int64_t n_remap,
+                        cudaStream_t st) {
+  if (n <= 0) return;
+  table_remap_kernel<<<(unsigned)grid_for(n, 256), 256, 0, st>>>(table, n, remap, n_remap);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+__global__ void popcount_kernel(const uint32_t* bits, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += __popc(bits[i]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+void launch_popcount(const uint32_t* bits, int64_t n_words, int64_t* out, cudaStream_t st) {
+  PL_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), st));
+  if (n_words <= 0) return;
+  popcount_kernel<<<(unsigned)grid_for(n_words, 256), 256, 0, st>>>(
+      bits, n_words, reinterpret_cast<unsigned long long*>(out));
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// K3 drain.  Tile = 256 threads x 4 words.  Phase A snapshots-and-clears the
+// live bitmap with atomicExch (marks racing on another stream land in the next
+// round) and counts bits per tile; phase B scans tile counts; phase C emits the
+// set bit indices in ascending order (per-thread popc + CTA scan).
+constexpr int kDrainThreads = 256;
+constexpr int kDrainWordsPerThread = 4;
+constexpr int kTileWords = kDrainThreads * kDrainWordsPerThread;
+
+int64_t drain_tiles(int64_t n_words) { return (n_words + kTileWords - 1) / kTileWords; }
+
+__global__ void __launch_bounds__(kDrainThreads)
+drain_snapshot_kernel(uint32_t* bits, uint32_t* snap, int64_t n_words, int64_t* tile_counts) {
+  using Scan = cub::BlockReduce<int, kDrainThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int64_t base = (int64_t)blockIdx.x * kTileWords + threadIdx.x * kDrainWordsPerThread;
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kDrainWordsPerThread; ++i) {
+    const int64_t wi = base + i;
+    uint32_t w = 0;
+    if (wi < n_words) {
+      w = bits[wi];
+      if (w) w = atomicExch(bits + wi, 0u);
+      snap[wi] = w;
+    }
+    c += __popc(w);
+  }
+  const int total = Scan(tmp).Sum(c);
+  if (threadIdx.x == 0) tile_counts[blockIdx.x] = total;
+}
+
+__global__ void drain_scan_kernel(int64_t* counts, int64_t n, int64_t* total) {
+  using Scan = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    int64_t v = i < n ? counts[i] : 0, ex, agg;
+    Scan(tmp).ExclusiveSum(v, ex, agg);
+    if (i < n) counts[i] = ex + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(kDrainThreads)
+drain_emit_kernel(const uint32_t* snap, int64_t n_words, const int64_t* tile_off, int64_t* cells,
+                  int64_t cap) {
+  using Scan = cub::BlockScan<int, kDrainThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int64_t base = (int64_t)blockIdx.x * kTileWords + threadIdx.x * kDrainWordsPerThread;
+  uint32_t w[kDrainWordsPerThread];
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kDrainWordsPerThread; ++i) {
+    w[i] = base + i < n_words ? snap[base + i] : 0u;
+    c += __popc(w[i]);
+  }
+  int ex;
+  Scan(tmp).ExclusiveSum(c, ex);
+  int64_t out = tile_off[blockIdx.x] + ex;
+#pragma unroll
+  for (int i = 0; i < kDrainWordsPerThread; ++i) {
+    uint32_t v = w[i];
+    while (v) {
+      const int b = __ffs(v) - 1;
+      v &= v - 1;
+      if (out < cap) cells[out] = (base + i) * 32 + b;
+      ++out;
+    }
+  }
+}
+
+void launch_drain_snapshot(uint32_t* bits, uint32_t* snap, int64_t n_words, int64_t* tile_counts,
+                           cudaStream_t st) {
+  const int64_t tiles = drain_tiles(n_words);
+  if (tiles <= 0) return;
+  KernelTimer timer("drain", st);
+  drain_snapshot_kernel<<<(unsigned)tiles, kDrainThreads, 0, st>>>(bits, snap, n_words,
+                                                                   tile_counts);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+void launch_drain_scan(int64_t* tile_counts, int64_t n_tiles, int64_t* total, cudaStream_t st) {
+  drain_scan_kernel<<<1, 1024, 0, st>>>(tile_counts, n_tiles, total);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+void launch_drain_emit(const uint32_t* snap, int64_t n_words, const int64_t* tile_offsets,
+                       int64_t* cells, int64_t cells_cap, cudaStream_t st) {
+  const int64_t tiles = drain_tiles(n_words);
+  if (tiles <= 0) return;
+  drain_emit_kernel<<<(unsigned)tiles, kDrainThreads, 0, st>>>(snap, n_words, tile_offsets, cells,
+                                                               cells_cap);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// K4/K5 copy engine.  Work item = (drained cell, layer); one warp moves one
+// cell_bytes row with 128-bit accesses, 8 loads in flight per lane before the
+// stores.  mode 0 gather pool->staging rows, 1 scatter rows->pool, 2 push pool->pool.
+template <int MODE>
+__global__ void __launch_bounds__(kWarps * 32) copy_kernel(CopyLaunch c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_rows = c.count ? min(*c.count, c.n_hint) : c.n_hint;
+  const int64_t items = n_rows * c.k;
+  const int64_t vecs = c.cell_bytes >> 4;
+  const int64_t per_slot = (int64_t)c.G * c.src_s;
+  for (int64_t item = warp0; item < items; item += nwarps) {
+    const int64_t r = item / c.k;
+    const int j = (int)(item % c.k);
+    const uint8_t* src_cell;
+    const uint64_t* src_fp;
+    int32_t req, lg;
+    int64_t pos;
+    if (MODE == 1) {
+      const int32_t* key = c.keys + r * 4;
+      req = key[0];
+      lg = key[1];
+      pos = (int64_t)(uint32_t)key[2] | ((int64_t)key[3] << 32);
+      const uint8_t* row = c.rows + r * c.row_bytes;
+      src_fp = reinterpret_cast<const uint64_t*>(row);
+      src_cell = row + 8 + (int64_t)j * c.cell_bytes;
+    } else {
+      const int64_t cell = c.cells[r];
+      const int32_t slot = (int32_t)(cell / per_slot);
+      const int64_t rem = cell % per_slot;
+      lg = (int32_t)(rem / c.src_s);
+      const int off = (int)(rem % c.src_s);
+      req = c.src_owner[slot];
+      pos = (int64_t)c.src_owner_idx[slot] * c.src_s + off;
+      const uint8_t* unit =
+          reinterpret_cast<const uint8_t*>(c.src_bases[c.src_groups[lg]]) + (int64_t)slot * c.src_unit;
+      src_fp = reinterpret_cast<const uint64_t*>(unit) + off;
+      src_cell = unit + c.fp_bytes + ((int64_t)j * c.src_s + off) * c.cell_bytes;
+    }
+    uint8_t* dst_cell;
+    uint64_t* dst_fp;
+    if (MODE == 0) {
+      uint8_t* row = c.rows + r * c.row_bytes;
+      dst_fp = reinterpret_cast<uint64_t*>(row);
+      dst_cell = row + 8 + (int64_t)j * c.cell_bytes;
+      if (j == 0 && lane == 0) {
+        int32_t* key = c.keys + r * 4;
+        key[0] = req;
+        key[1] = lg;
+        key[2] = (int32_t)(uint32_t)(pos & 0xffffffff);
+        key[3] = (int32_t)(pos >> 32);
+      }
+      if (req < 0) continue;
+    } else {
+      if (req < 0) continue;
+      if (c.apply_mask && !c.apply_mask[(int64_t)req * c.G + lg]) continue;
+      const int32_t dslot = c.dst_table[(int64_t)req * c.dst_max_chain + pos / c.dst_s];
+      if (dslot < 0) continue;
+      const int doff = (int)(pos % c.dst_s);
+      uint8_t* unit =
+          reinterpret_cast<uint8_t*>(c.dst_bases[c.src_groups[lg]]) + (int64_t)dslot * c.dst_unit;
+      dst_fp = reinterpret_cast<uint64_t*>(unit) + doff;
+      dst_cell = unit + c.fp_bytes + ((int64_t)j * c.dst_s + doff) * c.cell_bytes;
+    }
+    if (j == 0 && lane == 0) *dst_fp = *src_fp;
+    const int4* s4 = reinterpret_cast<const int4*>(src_cell);
+    int4* d4 = reinterpret_cast<int4*>(dst_cell);
+    constexpr int U = 8;
+    int64_t v = lane;
+    for (; v + 32 * (U - 1) < vecs; v += 32 * U) {
+      int4 buf[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) buf[u] = MODE == 1 ? ld_plain(s4 + v + 32 * u) : ld_stream(s4 + v + 32 * u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st_stream(d4 + v + 32 * u, buf[u]);
+    }
+    for (; v < vecs; v += 32) st_stream(d4 + v, MODE == 1 ? ld_plain(s4 + v) : ld_stream(s4 + v));
+  }
+}
+
+void launch_copy(const CopyLaunch& c, cudaStream_t st) {
+  if (c.n_hint <= 0) return;
+  const int64_t grid = grid_for(c.n_hint * c.k, kWarps, 16);
+  KernelTimer timer(c.mode == 0 ? "patch_gather" : (c.mode == 1 ? "patch_scatter" : "patch_push"), st);
+  switch (c.mode) {
+    case 0: copy_kernel<0><<<(unsigned)grid, kWarps * 32, 0, st>>>(c); break;
+    case 1: copy_kernel<1><<<(unsigned)grid, kWarps * 32, 0, st>>>(c); break;
+    default: copy_kernel<2><<<(unsigned)grid, kWarps * 32, 0, st>>>(c); break;
+  }
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+__global__ void read_fps_kernel(uint64_t base, int64_t unit_bytes, const int32_t* slots, int64_t n,
+                                int s, uint64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * s;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t* unit =
+        reinterpret_cast<const uint64_t*>(base + (uint64_t)slots[i / s] * (uint64_t)unit_bytes);
+    out[i] = unit[i % s];
+  }
+}
+void launch_read_fps(uint64_t base, int64_t unit_bytes, const int32_t* slots, int64_t n, int s,
+                     uint64_t* out, cudaStream_t st) {
+  if (n <= 0) return;
+  read_fps_kernel<<<(unsigned)grid_for(n * s, 256), 256, 0, st>>>(base, unit_bytes, slots, n, s,
+                                                                  out);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+}  // namespace pl

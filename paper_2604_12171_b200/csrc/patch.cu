@@ -1,0 +1,441 @@
+// Patch: the incremental KV-patching engine of one migrating (src, dst) pair.
+//
+// Reference: DirtyBitmap (migrator.py:24-48), MigrationStream.start/_drain
+// (migrator.py:170-183, 227-243), PatchReceiver._apply (migrator.py:115-132).
+//
+// The dirty set lives twice, by construction identical: a device bitmap over
+// the source's physical cells (1 bit per (slot, group, offset)), which the
+// kernels scan/compact and move; and a host interval set per (request, group),
+// which gives the control plane token counts and destination chain extents
+// without a device sync (the reference's counters branch on them every poll).
+#include <algorithm>
+#include <cstring>
+
+#include "internal.h"
+
+namespace pl {
+
+Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n) : src(src_) {
+  if (n <= 0) fail(PL_E_INVALID, "a patch needs at least one layer group");
+  std::vector<std::pair<int32_t, int32_t>> gl;
+  for (int i = 0; i < n; ++i) {
+    if (g[i] < 0 || g[i] >= src->n_model_groups) fail(PL_E_INVALID, "group out of range");
+    gl.push_back({g[i], layers ? layers[i] : src->k});
+  }
+  std::sort(gl.begin(), gl.end());
+  gl.erase(std::unique(gl.begin(), gl.end(),
+                       [](auto& a, auto& b) { return a.first == b.first; }),
+           gl.end());
+  for (auto& x : gl) {
+    groups.push_back(x.first);
+    layers_in_group.push_back(x.second);
+  }
+  G = (int)groups.size();
+  local_of.assign(src->n_model_groups, -1);
+  for (int i = 0; i < G; ++i) local_of[groups[i]] = i;
+  PL_CUDA(cudaSetDevice(src->device));
+  PL_CUDA(cudaMalloc(&d_local_of, sizeof(int32_t) * src->n_model_groups));
+  PL_CUDA(cudaMemcpy(d_local_of, local_of.data(), sizeof(int32_t) * src->n_model_groups,
+                     cudaMemcpyHostToDevice));
+  PL_CUDA(cudaMalloc(&d_count, sizeof(int64_t) * 2));
+  PL_CUDA(cudaMemset(d_count, 0, sizeof(int64_t) * 2));
+  PL_CUDA(cudaEventCreateWithFlags(&ev_gathered, cudaEventDisableTiming));
+  PL_CUDA(cudaEventCreateWithFlags(&ev_applied, cudaEventDisableTiming));
+  PL_CUDA(cudaEventCreateWithFlags(&ev_dst, cudaEventDisableTiming));
+  ensure_bits();
+  src->patches.push_back(this);
+}
+
+Patch::~Patch() {
+  cudaSetDevice(src->device);
+  cudaStreamSynchronize(src->stream);
+  auto& v = src->patches;
+  v.erase(std::remove(v.begin(), v.end(), this), v.end());
+  cudaFree(d_bits);
+  cudaFree(d_snap);
+  cudaFree(d_local_of);
+  cudaFree(d_tile_counts);
+  cudaFree(d_count);
+  cudaFree(d_cells);
+  cudaFree(d_rows);
+  cudaFree(d_keys);
+  cudaFree(d_groups_);
+  cudaEventDestroy(ev_gathered);
+  cudaEventDestroy(ev_applied);
+  cudaEventDestroy(ev_dst);
+}
+
+void Patch::ensure_bits() {
+  const int64_t slots = std::max<int64_t>(src->owner_cap, 1);
+  if (slots <= bit_slots && d_bits) return;
+  const int64_t words = (slots * G * src->s + 31) / 32;
+  uint32_t *nb = nullptr, *ns = nullptr;
+  PL_CUDA(cudaSetDevice(src->device));
+  PL_CUDA(cudaMalloc(&nb, words * 4));
+  PL_CUDA(cudaMalloc(&ns, words * 4));
+  PL_CUDA(cudaMemsetAsync(nb, 0, words * 4, src->stream));
+  if (d_bits && n_words)
+    PL_CUDA(cudaMemcpyAsync(nb, d_bits, n_words * 4, cudaMemcpyDeviceToDevice, src->stream));
+  PL_CUDA(cudaStreamSynchronize(src->stream));
+  cudaFree(d_bits);
+  cudaFree(d_snap);
+  d_bits = nb;
+  d_snap = ns;
+  bit_slots = slots;
+  n_words = words;
+  const int64_t tiles = drain_tiles(n_words);
+  if (tiles > n_tiles_cap) {
+    cudaFree(d_tile_counts);
+    PL_CUDA(cudaMalloc(&d_tile_counts, sizeof(int64_t) * tiles));
+    n_tiles_cap = tiles;
+  }
+}
+
+// --- host interval set ------------------------------------------------------------
+static int64_t insert_interval(std::vector<Interval>& v, int64_t a, int64_t b) {
+  // merge [a,b) into sorted disjoint v (adjacent intervals merge); returns newly covered
+  if (b <= a) return 0;
+  int64_t covered_before = 0;
+  std::vector<Interval> out;
+  out.reserve(v.size() + 1);
+  int64_t na = a, nb = b;
+  bool placed = false;
+  for (const Interval& x : v) {
+    if (x.b < na) {
+      out.push_back(x);
+    } else if (x.a > nb) {
+      if (!placed) {
+        out.push_back({na, nb});
+        placed = true;
+      }
+      out.push_back(x);
+    } else {
+      covered_before += std::max<int64_t>(0, std::min(x.b, b) - std::max(x.a, a));
+      na = std::min(na, x.a);
+      nb = std::max(nb, x.b);
+    }
+  }
+  if (!placed) out.push_back({na, nb});
+  v.swap(out);
+  return (b - a) - covered_before;
+}
+
+void Patch::mark(int32_t req, int g, int64_t start, int64_t n, bool device) {
+  if (n <= 0 || g < 0 || g >= (int)local_of.size()) return;
+  const int lg = local_of[g];
+  if (lg < 0) return;
+  dirty_keys += insert_interval(dirty[{req, lg}], start, start + n);
+  if (device) {
+    Store::WriteItem it{req, lg, start, n, 0};
+    mark_device({it});
+  }
+}
+
+// items carry the *local* group index in .group
+void Patch::mark_device(const std::vector<Store::WriteItem>& items) {
+  if (items.empty()) return;
+  src->flush();
+  const int n = (int)items.size();
+  std::vector<int32_t> reqs(n), lgs(n);
+  std::vector<int64_t> starts(n), offs(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    reqs[i] = items[i].req;
+    lgs[i] = items[i].group;
+    starts[i] = items[i].start;
+    offs[i + 1] = offs[i] + items[i].count;
+  }
+  Upload up(src);
+  int a = up.add(reqs.data(), 4 * n), b = up.add(lgs.data(), 4 * n);
+  int c = up.add(starts.data(), 8 * n), d = up.add(offs.data(), 8 * (n + 1));
+  up.go();
+  MarkLaunch m{};
+  m.reqs = up.ptr<int32_t>(a);
+  m.lgs = up.ptr<int32_t>(b);
+  m.starts = up.ptr<int64_t>(c);
+  m.offs = up.ptr<int64_t>(d);
+  m.n_items = n;
+  m.total = offs[n];
+  m.table = src->d_table;
+  m.max_chain = src->max_chain;
+  m.s = src->s;
+  m.G = G;
+  m.bits = d_bits;
+  launch_mark(m, src->stream);
+}
+
+int64_t Patch::seed() {
+  // every occupied prefix of the pair's groups becomes dirty (migrator.py:170-183)
+  int64_t seeded = 0;
+  std::vector<Store::WriteItem> items;
+  for (int32_t req = 0; req < (int32_t)src->tables.size(); ++req) {
+    const ReqTable& t = src->tables[req];
+    if (!t.present) continue;
+    for (int lg = 0; lg < G; ++lg) {
+      const int64_t w = t.written[groups[lg]];
+      if (w <= 0) continue;
+      dirty_keys += insert_interval(dirty[{req, lg}], 0, w);
+      seeded += w;
+      items.push_back({req, lg, 0, w, 0});
+    }
+  }
+  mark_device(items);
+  return seeded;
+}
+
+int64_t Patch::discard(int32_t req) {
+  int64_t dropped = 0;
+  for (int lg = 0; lg < G; ++lg) {
+    auto it = dirty.find({req, lg});
+    if (it == dirty.end()) continue;
+    for (const Interval& x : it->second) dropped += x.b - x.a;
+    dirty.erase(it);
+  }
+  dirty_keys -= dropped;
+  // released blocks already had their bits cleared by the store; a request that
+  // still holds blocks here has them cleared now
+  const ReqTable* t = src->table(req);
+  if (t && !t->chain.empty()) {
+    std::vector<int32_t> slots;
+    for (int64_t id : t->chain) slots.push_back(src->by_id.at(id).slot);
+    clear_slots_device(slots);
+  }
+  return dropped;
+}
+
+void Patch::clear_slots_device(const std::vector<int32_t>& slots) {
+  if (slots.empty()) return;
+  src->flush();
+  Upload up(src);
+  int a = up.add(slots.data(), slots.size() * 4);
+  up.go();
+  launch_clear_slots(d_bits, G, src->s, up.ptr<int32_t>(a), (int64_t)slots.size(), src->stream);
+}
+
+int64_t Patch::host_cells(
+    const std::vector<std::tuple<int32_t, int32_t, std::vector<Interval>>>& d) {
+  int64_t c = 0;
+  for (auto& e : d) {
+    int64_t len = 0;
+    for (const Interval& x : std::get<2>(e)) len += x.b - x.a;
+    c += len * layers_in_group[std::get<1>(e)];
+  }
+  return c;
+}
+
+int64_t Patch::take_drained() {
+  drained.clear();
+  drained.reserve(dirty.size());
+  for (auto& kv : dirty)
+    if (!kv.second.empty())
+      drained.emplace_back(kv.first.first, kv.first.second, std::move(kv.second));
+  dirty.clear();
+  drained_keys = dirty_keys;
+  dirty_keys = 0;
+  return drained_keys;
+}
+
+int64_t Patch::device_drain_compact() {
+  src->flush();
+  const int64_t need = std::max<int64_t>(drained_keys, 1);
+  if (need > cells_cap) {
+    PL_CUDA(cudaStreamSynchronize(src->stream));
+    cudaFree(d_cells);
+    cells_cap = std::max(need, cells_cap * 2);
+    PL_CUDA(cudaMalloc(&d_cells, sizeof(int64_t) * cells_cap));
+  }
+  launch_drain_snapshot(d_bits, d_snap, n_words, d_tile_counts, src->stream);
+  launch_drain_scan(d_tile_counts, drain_tiles(n_words), d_count, src->stream);
+  launch_drain_emit(d_snap, n_words, d_tile_counts, d_cells, cells_cap, src->stream);
+  return drained_keys;
+}
+
+void Patch::drain(int64_t* keys, int64_t* cells) {
+  if (in_flight) fail(PL_E_STATE, "a drained patch of this pair is still in flight");
+  PL_CUDA(cudaSetDevice(src->device));
+  take_drained();
+  // the staging buffer may still be read by the previous apply on the dst stream
+  if (applied_recorded) PL_CUDA(cudaStreamWaitEvent(src->stream, ev_applied, 0));
+  device_drain_compact();
+  const int64_t row_bytes = 8 + (int64_t)src->k * src->cell_bytes;
+  const int64_t need = std::max<int64_t>(drained_keys, 1);
+  if (need > rows_cap) {
+    PL_CUDA(cudaStreamSynchronize(src->stream));
+    cudaFree(d_rows);
+    cudaFree(d_keys);
+    rows_cap = std::max(need, rows_cap + rows_cap / 2);
+    PL_CUDA(cudaMalloc(&d_rows, row_bytes * rows_cap));
+    PL_CUDA(cudaMalloc(&d_keys, sizeof(int32_t) * 4 * rows_cap));
+  }
+  if (drained_keys > 0) {
+    CopyLaunch c{};
+    c.mode = 0;
+    c.cells = d_cells;
+    c.count = d_count;
+    c.n_hint = drained_keys;
+    c.G = G;
+    c.k = src->k;
+    c.cell_bytes = src->cell_bytes;
+    c.fp_bytes = src->fp_bytes;
+    c.src_bases = src->d_bases_;
+    c.src_groups = d_groups();
+    c.src_s = src->s;
+    c.src_unit = src->unit_bytes;
+    c.src_owner = src->d_owner;
+    c.src_owner_idx = src->d_owner_idx;
+    c.rows = d_rows;
+    c.keys = d_keys;
+    c.row_bytes = row_bytes;
+    launch_copy(c, src->stream);
+  }
+  PL_CUDA(cudaEventRecord(ev_gathered, src->stream));
+  in_flight = true;
+  *keys = drained_keys;
+  *cells = host_cells(drained);
+}
+
+void Patch::extend_dst(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
+                       int64_t n_stale, std::vector<uint8_t>& mask, int* status) {
+  // PatchReceiver._apply order: sorted by (request id, group) (migrator.py:124-128)
+  std::vector<size_t> order;
+  for (size_t i = 0; i < drained.size(); ++i) {
+    const int32_t req = std::get<0>(drained[i]);
+    if (stale && req < n_stale && stale[req]) continue;
+    order.push_back(i);
+  }
+  auto rk = [&](int32_t r) -> int64_t { return r < n_rank && rank ? rank[r] : (int64_t)r; };
+  std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+    const int64_t ra = rk(std::get<0>(drained[a])), rb = rk(std::get<0>(drained[b]));
+    if (ra != rb) return ra < rb;
+    return groups[std::get<1>(drained[a])] < groups[std::get<1>(drained[b])];
+  });
+  int64_t max_req = 0;
+  for (auto& e : drained) max_req = std::max<int64_t>(max_req, std::get<0>(e) + 1);
+  mask.assign((size_t)(max_req * G), 0);
+  *status = PL_OK;
+  for (size_t i : order) {
+    const int32_t req = std::get<0>(drained[i]);
+    const int32_t lg = std::get<1>(drained[i]);
+    try {
+      dst->reserve_positions(req, groups[lg], std::get<2>(drained[i]));
+    } catch (const Error& e) {
+      *status = e.code;
+      dst->last_msg = e.what();
+      return;
+    }
+    mask[(size_t)req * G + lg] = 1;
+  }
+}
+
+const int32_t* Patch::d_groups() {
+  if (!d_groups_) {
+    PL_CUDA(cudaMalloc(&d_groups_, sizeof(int32_t) * G));
+    PL_CUDA(cudaMemcpy(d_groups_, groups.data(), sizeof(int32_t) * G, cudaMemcpyHostToDevice));
+  }
+  return d_groups_;
+}
+
+void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
+                  int64_t n_stale) {
+  if (!in_flight) fail(PL_E_STATE, "no drained patch in flight");
+  if (dst->k != src->k || dst->cell_bytes != src->cell_bytes)
+    fail(PL_E_INVALID, "source and destination layouts differ");
+  std::vector<uint8_t> mask;
+  int status = PL_OK;
+  extend_dst(dst, rank, n_rank, stale, n_stale, mask, &status);
+  in_flight = false;
+  const int64_t n_rows = drained_keys;
+  drained.clear();
+  PL_CUDA(cudaSetDevice(dst->device));
+  dst->flush();
+  if (n_rows > 0 && !mask.empty()) {
+    Upload up(dst);
+    int a = up.add(mask.data(), mask.size());
+    up.go();
+    PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_gathered, 0));
+    CopyLaunch c{};
+    c.mode = 1;
+    c.count = d_count;
+    c.n_hint = n_rows;
+    c.G = G;
+    c.k = src->k;
+    c.cell_bytes = src->cell_bytes;
+    c.fp_bytes = src->fp_bytes;
+    c.src_groups = d_groups();
+    c.src_s = src->s;
+    c.dst_bases = dst->d_bases_;
+    c.dst_s = dst->s;
+    c.dst_unit = dst->unit_bytes;
+    c.dst_table = dst->d_table;
+    c.dst_max_chain = dst->max_chain;
+    c.apply_mask = up.ptr<uint8_t>(a);
+    c.rows = d_rows;
+    c.keys = d_keys;
+    c.row_bytes = 8 + (int64_t)src->k * src->cell_bytes;
+    launch_copy(c, dst->stream);
+  }
+  PL_CUDA(cudaEventRecord(ev_applied, dst->stream));
+  applied_recorded = true;
+  if (status != PL_OK) fail(status, dst->last_msg);
+}
+
+void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells) {
+  if (in_flight) fail(PL_E_STATE, "a drained patch of this pair is still in flight");
+  if (dst->k != src->k || dst->cell_bytes != src->cell_bytes)
+    fail(PL_E_INVALID, "source and destination layouts differ");
+  take_drained();
+  *keys = drained_keys;
+  *cells = host_cells(drained);
+  std::vector<uint8_t> mask;
+  int status = PL_OK;
+  extend_dst(dst, rank, n_rank, nullptr, 0, mask, &status);
+  drained.clear();
+  PL_CUDA(cudaSetDevice(dst->device));
+  dst->flush();
+  PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
+  PL_CUDA(cudaSetDevice(src->device));
+  device_drain_compact();
+  if (drained_keys > 0 && !mask.empty()) {
+    Upload up(src);
+    int a = up.add(mask.data(), mask.size());
+    up.go();
+    PL_CUDA(cudaStreamWaitEvent(src->stream, ev_dst, 0));
+    CopyLaunch c{};
+    c.mode = 2;
+    c.cells = d_cells;
+    c.count = d_count;
+    c.n_hint = drained_keys;
+    c.G = G;
+    c.k = src->k;
+    c.cell_bytes = src->cell_bytes;
+    c.fp_bytes = src->fp_bytes;
+    c.src_bases = src->d_bases_;
+    c.src_groups = d_groups();
+    c.src_s = src->s;
+    c.src_unit = src->unit_bytes;
+    c.src_owner = src->d_owner;
+    c.src_owner_idx = src->d_owner_idx;
+    c.dst_bases = dst->d_bases_;
+    c.dst_s = dst->s;
+    c.dst_unit = dst->unit_bytes;
+    c.dst_table = dst->d_table;
+    c.dst_max_chain = dst->max_chain;
+    c.apply_mask = up.ptr<uint8_t>(a);
+    launch_copy(c, src->stream);
+  }
+  PL_CUDA(cudaEventRecord(ev_applied, src->stream));
+  applied_recorded = true;
+  PL_CUDA(cudaSetDevice(dst->device));
+  PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
+  if (status != PL_OK) fail(status, dst->last_msg);
+}
+
+int64_t Patch::device_dirty_count() {
+  src->flush();
+  launch_popcount(d_bits, n_words, d_count + 1, src->stream);
+  int64_t v = 0;
+  PL_CUDA(cudaMemcpyAsync(&v, d_count + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, src->stream));
+  PL_CUDA(cudaStreamSynchronize(src->stream));
+  return v;
+}
+
+}  // namespace pl

@@ -1,0 +1,75 @@
+"""K2 paged-attention decode vs the fp32 numpy oracle (oracle/attention.py).
+
+Tolerance (BASELINE north star): bf16 output within 2e-2 relative of the fp32
+oracle computed on the same bf16 K/V/q values."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle.attention import bf16_to_f32, decode_attention
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 2e-2
+
+
+def _run_case(B, n_q, n_kv, D, s, k, layer, ctxs, seed):
+    import torch
+
+    from paper_2604_12171_b200 import _native as N
+    from paper_2604_12171_b200 import kvstore
+
+    torch.manual_seed(seed)
+    cell = 2 * n_kv * D * 2
+    cap = sum((c + s - 1) // s for c in ctxs) + 4
+    st = kvstore.KvStore(1, k, s, cap, (0,), cell_bytes=cell)
+    kvs = []
+    for b, c in enumerate(ctxs):
+        x = torch.randn(c, k, 2 * n_kv * D, dtype=torch.bfloat16, device="cuda")
+        kvs.append(x)
+        if c:
+            st.append_seeded(f"att{seed}_{b}", 0, c, 1234 + b, kv_dev=x.data_ptr())
+    st.sync()
+    rows = torch.tensor([st._registry.handle(f"att{seed}_{b}") for b in range(B)],
+                        dtype=torch.int32, device="cuda")
+    ctx_t = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    q = torch.randn(B, n_q, D, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty_like(q)
+    scale = D ** -0.5
+    N.check(N.lib().pl_paged_attn_decode(st._h, 0, layer, C.c_void_p(q.data_ptr()),
+                                         C.c_void_p(out.data_ptr()), C.c_void_p(rows.data_ptr()),
+                                         C.c_void_p(ctx_t.data_ptr()), B, n_q, n_kv, D, scale,
+                                         max(ctxs), None))
+    torch.cuda.synchronize()
+    st.sync()
+    qf = bf16_to_f32(q.view(torch.int16).cpu().numpy().view(np.uint16))
+    ks, vs = [], []
+    for x in kvs:
+        u = x[:, layer].view(torch.int16).cpu().numpy().view(np.uint16).reshape(-1, 2, n_kv, D)
+        ks.append(bf16_to_f32(u[:, 0]))
+        vs.append(bf16_to_f32(u[:, 1]))
+    ref = decode_attention(qf, ks, vs, scale)
+    got = bf16_to_f32(out.view(torch.int16).cpu().numpy().view(np.uint16))
+    return got, ref
+
+
+@pytest.mark.parametrize("n_q,n_kv,D", [(32, 8, 128), (64, 8, 128), (8, 8, 128),
+                                         (16, 4, 64), (8, 2, 64)])
+@pytest.mark.parametrize("s", [8, 16])
+def test_decode_matches_fp32_oracle(n_q, n_kv, D, s):
+    ctxs = [1, 17, 0, 100, 255, 33, 512, 5]
+    got, ref = _run_case(len(ctxs), n_q, n_kv, D, s, 2, 1, ctxs, seed=n_q + D + s)
+    err = np.abs(got - ref)
+    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
+    assert np.all(err <= bound + 1e-3), float(err.max())
+    assert np.all(got[2] == 0)  # empty context -> zeros
+
+
+def test_decode_long_context_split_k():
+    ctxs = [2048, 1999, 4096, 64]
+    got, ref = _run_case(len(ctxs), 32, 8, 128, 16, 4, 3, ctxs, seed=7)
+    err = np.abs(got - ref)
+    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
+    assert np.all(err <= bound + 1e-3), float(err.max())

@@ -1,0 +1,138 @@
+"""GPU block manager parity: the CUDA-backed KvStore replays the reference's
+own op sequences (tests/golden/kv_sequences.json) and must match them, and the
+oracle, bit for bit: results, counters, block order, chains, fingerprints,
+state digest.  Mirrors pkg/tests/test_kvstore.py of the reference."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import opgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kv():
+    from paper_2604_12171_b200 import kvstore
+    return kvstore
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_gpu_store_replays_reference(kv, golden, seed):
+    case = golden("kv_sequences.json")[seed]
+    p = case["params"]
+    st = kv.KvStore(p["gpu_id"], p["k"], p["s"], p["capacity"], p["groups"], cell_bytes=64)
+    ref = oracle.OracleStore(p["gpu_id"], p["k"], p["s"], p["capacity"], p["groups"], cell_bytes=64)
+    excs = (kv.KvError, ValueError)
+    for i, op in enumerate(opgen.kv_ops(seed)):
+        got = opgen.apply_op(st, op, excs)
+        assert got == case["results"][i], (i, op)
+        assert opgen.apply_op(ref, op, (oracle.KvError, ValueError)) == got
+        assert opgen.light_state(st) + [st.occupied_cells] == case["lights"][i], (i, op)
+    assert opgen.full_state(st) == case["final"]
+    assert hashlib.sha256(repr(st.state_digest()).encode()).hexdigest() == case["digest_sha"]
+    # the KV bytes behind every fingerprint are the deterministic expansion (oracle)
+    for rid in sorted(st.tables):
+        for g, w in st.tables[rid].written.items():
+            for pos in range(0, w, max(1, w // 5)):
+                try:
+                    fp = st.read_checksum(rid, g, pos)
+                except kv.UnknownSlot:
+                    continue
+                for j in range(p["k"]):
+                    assert st.read_cell(rid, g, pos, j) == oracle.expand_cell(fp, j, 64)
+                    assert ref.read_cell(rid, g, pos, j) == st.read_cell(rid, g, pos, j)
+
+
+class TestReferenceUnitCases:
+    """The reference's known answers (pkg/tests/test_kvstore.py)."""
+
+    def store(self, kv, capacity=10, s=16, k=4, groups=(0,)):
+        return kv.KvStore(1, k, s, capacity, groups)
+
+    def fill(self, st, rid, g, n):
+        start = st.tables[rid].written.get(g, 0) if rid in st.tables else 0
+        return st.append(rid, g, n, [opgen.payload(rid, g, start + i) for i in range(n)])
+
+    def test_forty_tokens_three_blocks(self, kv):
+        st = self.store(kv)
+        slots = self.fill(st, "r1", 0, 40)
+        assert st.used_blocks == 3
+        assert [s.offset for s in slots] == list(range(16)) * 2 + list(range(8))
+        assert [s.block_id for s in slots] == [0] * 16 + [1] * 16 + [2] * 8
+
+    def test_overflow_atomic(self, kv):
+        st = self.store(kv, capacity=2)
+        self.fill(st, "r1", 0, 20)
+        with pytest.raises(kv.KvOverflow):
+            self.fill(st, "r2", 0, 40)
+        assert st.used_blocks == 2 and "r2" not in st.tables
+
+    def test_lookup_token_20(self, kv):
+        st = self.store(kv)
+        self.fill(st, "r1", 0, 25)
+        addr, off = st.lookup("r1", 1, 20)
+        assert off == 4 and addr == st.tables["r1"].chain[1].address
+
+    def test_compaction_partition_and_survival(self, kv):
+        st = self.store(kv, capacity=5)
+        for r in "abcde":
+            self.fill(st, r, 0, 16)
+        st.free_request("b")
+        st.free_request("d")
+        before = {(r, p): st.lookup(r, 1, p) for r in "ace" for p in range(16)}
+        assert st.compact() == 2
+        assert [b.state for b in st.blocks] == ["live"] * 3 + ["free"] * 2
+        for (r, p), v in before.items():
+            assert st.lookup(r, 1, p) == v
+            assert st.read_checksum(r, 0, p) == opgen.payload(r, 0, p)
+
+    def test_resize_relocates_live_units_and_releases_memory(self, kv):
+        # live blocks sitting in the physical tail are moved by K6 so the pool's tail
+        # can be unmapped; every fingerprint and byte survives
+        st = kv.KvStore(1, 2, 16, 64, (0, 1), cell_bytes=4096, chunk_bytes=2 << 20)
+        for i in range(40):
+            self.fill(st, f"x{i}", i % 2, 16)
+        for i in range(0, 38):
+            st.free_request(f"x{i}")
+        keep = ["x38", "x39"]
+        before = {(r, p): st.read_cell(r, int(r[1:]) % 2, p, 1) for r in keep for p in range(16)}
+        mapped0 = st.info()["mapped_bytes"]
+        st.resize(4)
+        stats = st.last_resize_stats()
+        assert st.capacity_blocks == 4 and stats["relocated_blocks"] == 2
+        assert stats["bytes_unmapped"] > 0 and st.info()["mapped_bytes"] < mapped0
+        for (r, p), v in before.items():
+            assert st.read_cell(r, int(r[1:]) % 2, p, 1) == v
+            assert st.read_checksum(r, int(r[1:]) % 2, p) == opgen.payload(r, int(r[1:]) % 2, p)
+        st.resize(64)
+        assert st.info()["mapped_bytes"] >= mapped0
+        self.fill(st, "y", 0, 16 * 60)
+        assert st.used_blocks == 62
+
+    def test_drop_one_group_keeps_shared_blocks(self, kv):
+        st = self.store(kv, capacity=8, groups=(0, 1))
+        self.fill(st, "a", 0, 32)
+        self.fill(st, "a", 1, 32)
+        occ = sum(b.occupied_tokens() for b in st.blocks)
+        assert st.drop_layer_groups([0]) == 32
+        assert st.used_blocks == 2
+        assert st.read_checksum("a", 1, 17) == opgen.payload("a", 1, 17)
+        assert sum(b.occupied_tokens() for b in st.blocks) == occ // 2
+        with pytest.raises(kv.UnknownLayerGroup):
+            st.drop_layer_groups([3])
+
+    def test_utilization_quarter_block(self, kv):
+        st = kv.KvStore(1, 4, 64, 4, (0,))
+        self.fill(st, "a", 0, 16)
+        assert st.effective_utilization() == 0.25
+
+    def test_seeded_append_matches_engine_payloads(self, kv, golden):
+        st = self.store(kv)
+        seed = opgen.stable_hash("r0000", 0)
+        st.append_seeded("r0000", 0, 4, seed)
+        got = [st.read_checksum("r0000", 0, p) for p in range(4)]
+        assert got == golden("fingerprints.json")["engine_r0000_g0"]

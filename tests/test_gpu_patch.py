@@ -1,0 +1,156 @@
+"""GPU KV-patching parity: dirty sets, patch counters, traces and patched bytes of
+the CUDA patch engine against the reference (tests/golden/migration_cases.json)
+and the oracle.  Mirrors pkg/tests/test_migrator.py of the reference."""
+
+import numpy as np
+import pytest
+
+import opgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ns():
+    from paper_2604_12171_b200 import events, fabric, kvstore, migrator
+
+    class NS:
+        EventScheduler = events.EventScheduler
+        EventTrace = events.EventTrace
+        CommFabric = fabric.CommFabric
+        FabricConfig = fabric.FabricConfig
+        KvStore = kvstore.KvStore
+        MigrationManager = migrator.MigrationManager
+
+    return NS
+
+
+@pytest.fixture
+def drain_log(monkeypatch):
+    """Record the drained key set of every patch, and check the device's view of it."""
+    from paper_2604_12171_b200 import migrator
+
+    log = []
+    orig = migrator.MigrationStream._drain
+
+    def drain(self):
+        host_dirty = self._dirty_keys()
+        dev_dirty = self.device_dirty_count()
+        assert dev_dirty == host_dirty, "device bitmap != host dirty set"
+        patch = orig(self)
+        keys = self.drained_keys()
+        assert self.device_drained() == len(keys) == patch.keys
+        log.append([list(k) for k in keys])
+        return patch
+
+    monkeypatch.setattr(migrator.MigrationStream, "_drain", drain)
+    return log
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_gpu_migration_matches_reference(ns, golden, drain_log, seed):
+    case = golden("migration_cases.json")[seed]
+    res = opgen.run_migration_case(ns, case["case"], {"cell_bytes": 64})
+    want = dict(case["result"])
+    assert drain_log == want.pop("drained")  # dirty sets, patch by patch
+    assert res == want
+
+
+def test_patched_bytes_are_bit_exact(ns, drain_log):
+    """Destination KV bytes == source bytes == expansion of the reference fingerprint."""
+    from paper_2604_12171_b200 import kvstore
+
+    case = opgen.migration_case(3)
+    case["events"] = []
+    cb = 4096
+    sched = ns.EventScheduler()
+    trace = ns.EventTrace()
+    fab = ns.CommFabric(sched, trace, [1, 2], ns.FabricConfig())
+    k, s = 4, 16
+    src = kvstore.KvStore(1, k, s, 64, [0, 1, 2], cell_bytes=cb)
+    dst = kvstore.KvStore(2, k, s, 64, [5], cell_bytes=cb)
+    mgr = ns.MigrationManager(sched, trace, fab, {1: src, 2: dst}, 8192, k)
+    for i in range(6):
+        for g in (0, 1, 2):
+            n = 7 + 13 * i
+            src.append(f"b{i}", g, n, [opgen.payload(f"b{i}", g, p) for p in range(n)])
+    dst.resident_groups |= {1, 2}
+    mgr.start_migration({(1, 2): set(range(5, 13))})
+    sched.run()
+    assert mgr.lag(2) == 0
+    for g in (1, 2):
+        assert dst.snapshot_group(g) == src.snapshot_group(g)
+        for rid, fps in src.snapshot_group(g).items():
+            for pos in (0, len(fps) // 2, len(fps) - 1):
+                for j in range(k):
+                    b = dst.read_cell(rid, g, pos, j)
+                    assert b == src.read_cell(rid, g, pos, j)
+                    assert b == oracle.expand_cell(fps[pos], j, cb)
+
+
+def test_stacked_groups_count_cells_not_tokens(ns):
+    from paper_2604_12171_b200 import kvstore
+
+    sched, trace = ns.EventScheduler(), ns.EventTrace()
+    fab = ns.CommFabric(sched, trace, [1, 2], ns.FabricConfig())
+    src = kvstore.KvStore(1, 4, 16, 64, (0, 1))
+    dst = kvstore.KvStore(2, 4, 16, 64, (2,))
+    mgr = ns.MigrationManager(sched, trace, fab, {1: src, 2: dst}, 8192, 4)
+    src.append("a", 0, 10, [opgen.payload("a", 0, p) for p in range(10)])
+    mgr.start_migration({(1, 2): {1, 2, 3, 4}})
+    assert mgr.counters.t_sched[2] == 40
+    sched.run()
+    assert mgr.lag(2) == 0
+
+
+def test_final_sync_residual_arithmetic(ns):
+    from paper_2604_12171_b200 import kvstore
+
+    sched, trace = ns.EventScheduler(), ns.EventTrace()
+    fab = ns.CommFabric(sched, trace, [1, 2], ns.FabricConfig())
+    src = kvstore.KvStore(1, 1, 16, 64, (0, 1))
+    dst = kvstore.KvStore(2, 1, 16, 64, (2,))
+    mgr = ns.MigrationManager(sched, trace, fab, {1: src, 2: dst}, 8192, 1)
+    mgr.start_migration({(1, 2): {1}})
+    sched.run()
+    mgr.streams[(1, 2)].streaming = False
+    src.append("a", 0, 40, [opgen.payload("a", 0, p) for p in range(40)])
+    mgr.on_kv_written(1, "a", 0, 0, 40)
+    pauses = []
+    mgr.final_sync_all(pauses.append)
+    sched.run()
+    transfer = 40 * 8192 / fab.bandwidth(1, 2)
+    assert transfer == pytest.approx(2.62144e-05)
+    assert pauses[0] == pytest.approx(transfer + 2e-4)
+    assert dst.snapshot_group(0) == src.snapshot_group(0)
+
+
+def test_push_path_direct_into_destination(ns):
+    """perf path: drain + fused gather/scatter straight into the destination pool"""
+    import ctypes as C
+
+    from paper_2604_12171_b200 import _native as N
+    from paper_2604_12171_b200 import kvstore
+
+    src = kvstore.KvStore(1, 2, 16, 128, (0, 1), cell_bytes=1024)
+    dst = kvstore.KvStore(2, 2, 16, 128, (3,), cell_bytes=1024)
+    for i in range(10):
+        src.append_seeded(f"p{i}", 1, 30 + i, opgen.stable_hash(f"p{i}", 1))
+    dst.resident_groups |= {1}
+    g = N.as_i32([1])
+    lpg = N.as_i32([2])
+    h = C.c_void_p()
+    N.check(N.lib().pl_patch_create(src._h, N.ptr(g), N.ptr(lpg), 1, C.byref(h)))
+    N.check(N.lib().pl_patch_set_active(h, 1))
+    seeded = C.c_int64()
+    N.check(N.lib().pl_patch_seed(h, C.byref(seeded)))
+    rank = src._registry.rank()
+    keys, cells = C.c_int64(), C.c_int64()
+    N.check(N.lib().pl_patch_push(h, dst._h, N.ptr(rank), len(rank), C.byref(keys), C.byref(cells)))
+    assert keys.value == seeded.value == sum(30 + i for i in range(10))
+    assert cells.value == 2 * keys.value
+    assert dst.snapshot_group(1) == src.snapshot_group(1)
+    for i in range(10):
+        assert dst.read_cell(f"p{i}", 1, 29 + i, 1) == src.read_cell(f"p{i}", 1, 29 + i, 1)
+    N.lib().pl_patch_destroy(h)
