@@ -410,6 +410,11 @@ int pl_patch_create(pl_store* src, const int32_t* groups, const int32_t* layers,
     *out = new pl_patch{p};
   });
 }
+static pl::Patch* live(pl_patch* p) {
+  if (!p || !p->p) pl::fail(PL_E_INVALID, "null patch");
+  if (!p->p->src) pl::fail(PL_E_STATE, "the patch's source store was destroyed");
+  return p->p;
+}
 int pl_patch_destroy(pl_patch* p) {
   return guard([&] {
     if (!p) return;
@@ -418,33 +423,34 @@ int pl_patch_destroy(pl_patch* p) {
   });
 }
 int pl_patch_set_active(pl_patch* p, int active) {
-  return guard([&] { p->p->active = active != 0; });
+  return guard([&] { live(p)->active = active != 0; });
 }
 int pl_patch_mark(pl_patch* p, int32_t req, int group, int64_t start, int64_t n) {
-  return guard([&] { p->p->mark(req, group, start, n, true); });
+  return guard([&] { live(p)->mark(req, group, start, n, true); });
 }
 int pl_patch_seed(pl_patch* p, int64_t* out) {
-  return guard([&] { *out = p->p->seed(); });
+  return guard([&] { *out = live(p)->seed(); });
 }
 int pl_patch_discard_request(pl_patch* p, int32_t req, int64_t* out) {
-  return guard([&] { *out = p->p->discard(req); });
+  return guard([&] { *out = live(p)->discard(req); });
 }
 int pl_patch_dirty_keys(pl_patch* p, int64_t* out) {
-  return guard([&] { *out = p->p->dirty_keys; });
+  return guard([&] { *out = live(p)->dirty_keys; });
 }
 int pl_patch_drain(pl_patch* p, int64_t* keys, int64_t* cells) {
-  return guard([&] { p->p->drain(keys, cells); });
+  return guard([&] { live(p)->drain(keys, cells); });
 }
 int pl_patch_drained_keys(pl_patch* p, int32_t* reqs, int32_t* groups, int64_t* pos, int64_t cap,
                           int64_t* n_out) {
   return guard([&] {
     int64_t n = 0;
-    for (auto& e : p->p->drained)
+    pl::Patch* q = live(p);
+    for (auto& e : q->drained)
       for (const pl::Interval& iv : std::get<2>(e))
         for (int64_t x = iv.a; x < iv.b; ++x) {
           if (n < cap) {
             reqs[n] = std::get<0>(e);
-            groups[n] = p->p->groups[std::get<1>(e)];
+            groups[n] = q->groups[std::get<1>(e)];
             pos[n] = x;
           }
           ++n;
@@ -454,18 +460,18 @@ int pl_patch_drained_keys(pl_patch* p, int32_t* reqs, int32_t* groups, int64_t* 
 }
 int pl_patch_apply(pl_patch* p, pl_store* dst, const int32_t* rank, int64_t n_rank,
                    const uint8_t* stale, int64_t n_stale) {
-  return guard([&] { p->p->apply(dst->s, rank, n_rank, stale, n_stale); });
+  return guard([&] { live(p)->apply(dst->s, rank, n_rank, stale, n_stale); });
 }
 int pl_patch_push(pl_patch* p, pl_store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
                   int64_t* cells) {
-  return guard([&] { p->p->push(dst->s, rank, n_rank, keys, cells); });
+  return guard([&] { live(p)->push(dst->s, rank, n_rank, keys, cells); });
 }
 int pl_patch_device_dirty_count(pl_patch* p, int64_t* out) {
-  return guard([&] { *out = p->p->device_dirty_count(); });
+  return guard([&] { *out = live(p)->device_dirty_count(); });
 }
 int pl_patch_device_drained(pl_patch* p, int64_t* out) {
   return guard([&] {
-    pl::Patch* q = p->p;
+    pl::Patch* q = live(p);
     PL_CUDA(cudaMemcpyAsync(out, q->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, q->src->stream));
     PL_CUDA(cudaStreamSynchronize(q->src->stream));
   });

@@ -196,6 +196,7 @@ struct Store {
   void launch_write(const std::vector<WriteItem>& items, int mode, const uint64_t* payloads,
                     const int64_t* positions, const void* kv_dev, int mark);
 };
+void detach_patches(Store* st);
 
 // ---------------------------------------------------------------------------
 // Packs host arrays into the store's pinned buffer and ships them in one H2D
@@ -218,7 +219,8 @@ struct Upload {
 // Patch: sender + receiver data plane of one migrating pair.
 
 struct Patch {
-  Store* src = nullptr;
+  Store* src = nullptr;  // nulled if the store is destroyed first
+  int device = 0;
   std::vector<int32_t> groups;           // model groups of the pair (sorted)
   std::vector<int32_t> layers_in_group;  // pair layers inside each group
   std::vector<int32_t> local_of;         // model group -> local index or -1
@@ -245,7 +247,7 @@ struct Patch {
 
   cudaEvent_t ev_gathered = nullptr, ev_applied = nullptr, ev_dst = nullptr;
   bool applied_recorded = false;
-  // staging of the in-flight patch: rows of [fp 8B][k * cell_bytes]; keys
+  // staging of the in-flight patch: rows of [fp 8B][pad 8B][k * cell_bytes]; keys
   uint8_t* d_rows = nullptr;
   int32_t* d_keys = nullptr;    // (req, lg, pos_lo, pos_hi) per row
   int64_t rows_cap = 0;

@@ -262,13 +262,15 @@ drain_snapshot_kernel(uint32_t* bits, uint32_t* snap, int64_t n_words, int64_t* 
   if (threadIdx.x == 0) tile_counts[blockIdx.x] = total;
 }
 
-__global__ void drain_scan_kernel(int64_t* counts, int64_t n, int64_t* total) {
-  using Scan = cub::BlockScan<int64_t, 1024>;
+constexpr int kScanThreads = 256;
+__global__ void __launch_bounds__(kScanThreads)
+drain_scan_kernel(int64_t* counts, int64_t n, int64_t* total) {
+  using Scan = cub::BlockScan<int64_t, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int64_t carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int64_t base = 0; base < n; base += 1024) {
+  for (int64_t base = 0; base < n; base += kScanThreads) {
     const int64_t i = base + threadIdx.x;
     int64_t v = i < n ? counts[i] : 0, ex, agg;
     Scan(tmp).ExclusiveSum(v, ex, agg);
@@ -319,7 +321,7 @@ void launch_drain_snapshot(uint32_t* bits, uint32_t* snap, int64_t n_words, int6
   PL_CUDA(cudaGetLastError());
 }
 void launch_drain_scan(int64_t* tile_counts, int64_t n_tiles, int64_t* total, cudaStream_t st) {
-  drain_scan_kernel<<<1, 1024, 0, st>>>(tile_counts, n_tiles, total);
+  drain_scan_kernel<<<1, kScanThreads, 0, st>>>(tile_counts, n_tiles, total);
   note_launch();
   PL_CUDA(cudaGetLastError());
 }
@@ -360,7 +362,7 @@ __global__ void __launch_bounds__(kWarps * 32) copy_kernel(CopyLaunch c) {
       pos = (int64_t)(uint32_t)key[2] | ((int64_t)key[3] << 32);
       const uint8_t* row = c.rows + r * c.row_bytes;
       src_fp = reinterpret_cast<const uint64_t*>(row);
-      src_cell = row + 8 + (int64_t)j * c.cell_bytes;
+      src_cell = row + 16 + (int64_t)j * c.cell_bytes;
     } else {
       const int64_t cell = c.cells[r];
       const int32_t slot = (int32_t)(cell / per_slot);
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(kWarps * 32) copy_kernel(CopyLaunch c) {
     if (MODE == 0) {
       uint8_t* row = c.rows + r * c.row_bytes;
       dst_fp = reinterpret_cast<uint64_t*>(row);
-      dst_cell = row + 8 + (int64_t)j * c.cell_bytes;
+      dst_cell = row + 16 + (int64_t)j * c.cell_bytes;
       if (j == 0 && lane == 0) {
         int32_t* key = c.keys + r * 4;
         key[0] = req;

@@ -15,7 +15,13 @@
 
 namespace pl {
 
-Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n) : src(src_) {
+void detach_patches(Store* st) {
+  for (Patch* p : st->patches) p->src = nullptr;
+  st->patches.clear();
+}
+
+Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n)
+    : src(src_), device(src_->device) {
   if (n <= 0) fail(PL_E_INVALID, "a patch needs at least one layer group");
   std::vector<std::pair<int32_t, int32_t>> gl;
   for (int i = 0; i < n; ++i) {
@@ -47,10 +53,14 @@ Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n) : src(
 }
 
 Patch::~Patch() {
-  cudaSetDevice(src->device);
-  cudaStreamSynchronize(src->stream);
-  auto& v = src->patches;
-  v.erase(std::remove(v.begin(), v.end(), this), v.end());
+  cudaSetDevice(device);
+  if (src) {
+    cudaStreamSynchronize(src->stream);
+    auto& v = src->patches;
+    v.erase(std::remove(v.begin(), v.end(), this), v.end());
+  } else {
+    cudaDeviceSynchronize();
+  }
   cudaFree(d_bits);
   cudaFree(d_snap);
   cudaFree(d_local_of);
@@ -256,7 +266,7 @@ void Patch::drain(int64_t* keys, int64_t* cells) {
   // the staging buffer may still be read by the previous apply on the dst stream
   if (applied_recorded) PL_CUDA(cudaStreamWaitEvent(src->stream, ev_applied, 0));
   device_drain_compact();
-  const int64_t row_bytes = 8 + (int64_t)src->k * src->cell_bytes;
+  const int64_t row_bytes = 16 + (int64_t)src->k * src->cell_bytes;
   const int64_t need = std::max<int64_t>(drained_keys, 1);
   if (need > rows_cap) {
     PL_CUDA(cudaStreamSynchronize(src->stream));
@@ -370,7 +380,7 @@ void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t
     c.apply_mask = up.ptr<uint8_t>(a);
     c.rows = d_rows;
     c.keys = d_keys;
-    c.row_bytes = 8 + (int64_t)src->k * src->cell_bytes;
+    c.row_bytes = 16 + (int64_t)src->k * src->cell_bytes;
     launch_copy(c, dst->stream);
   }
   PL_CUDA(cudaEventRecord(ev_applied, dst->stream));

@@ -69,6 +69,7 @@ Store::Store(int device_, int gpu_id_, int k_, int s_, int64_t cell_bytes_, int 
 Store::~Store() {
   cudaSetDevice(device);
   cudaStreamSynchronize(stream);
+  detach_patches(this);
   for (auto& a : arenas) a.release();
   cudaFree(d_table);
   cudaFree(d_owner);

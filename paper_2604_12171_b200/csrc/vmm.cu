@@ -85,12 +85,15 @@ void Arena::ensure(size_t bytes) {
     // grow the reservation: new range (2x headroom), remap existing chunks there
     size_t new_va_bytes = std::max(want_va, va_bytes * 2);
     CUdeviceptr nva = 0;
-    cu_check(d.AddressReserve(&nva, new_va_bytes, chunk_bytes, 0, 0), "cuMemAddressReserve");
-    for (size_t i = 0; i < chunks.size(); ++i)
+    cu_check(d.AddressReserve(&nva, new_va_bytes, vmm_granularity(device), 0, 0),
+             "cuMemAddressReserve");
+    for (size_t i = 0; i < chunks.size(); ++i) {
       cu_check(d.Map(nva + i * chunk_bytes, chunk_bytes, 0, chunks[i], 0), "cuMemMap");
-    if (!chunks.empty()) set_access(nva, chunks.size() * chunk_bytes, device, peer_devices);
+      set_access(nva + i * chunk_bytes, chunk_bytes, device, peer_devices);
+    }
     if (va) {
-      if (!chunks.empty()) cu_check(d.Unmap(va, chunks.size() * chunk_bytes), "cuMemUnmap");
+      for (size_t i = 0; i < chunks.size(); ++i)
+        cu_check(d.Unmap(va + i * chunk_bytes, chunk_bytes), "cuMemUnmap");
       cu_check(d.AddressFree(va, va_bytes), "cuMemAddressFree");
     }
     va = nva;
@@ -103,35 +106,37 @@ void Arena::ensure(size_t bytes) {
     CUresult r = d.Create(&h, chunk_bytes, &p, 0);
     if (r != CUDA_SUCCESS) {
       // roll back the chunks created by this call
-      if (chunks.size() > first) {
-        cu_check(d.Unmap(va + first * chunk_bytes, (chunks.size() - first) * chunk_bytes),
-                 "cuMemUnmap");
-        for (size_t i = first; i < chunks.size(); ++i) d.Release(chunks[i]);
-        chunks.resize(first);
+      for (size_t i = first; i < chunks.size(); ++i) {
+        d.Unmap(va + i * chunk_bytes, chunk_bytes);
+        d.Release(chunks[i]);
       }
+      chunks.resize(first);
       cu_check(r, "cuMemCreate (device out of memory?)");
     }
     cu_check(d.Map(va + chunks.size() * chunk_bytes, chunk_bytes, 0, h, 0), "cuMemMap");
+    set_access(va + chunks.size() * chunk_bytes, chunk_bytes, device, peer_devices);
     chunks.push_back(h);
   }
-  set_access(va + first * chunk_bytes, (chunks.size() - first) * chunk_bytes, device,
-             peer_devices);
 }
 
 void Arena::trim(size_t bytes) {
   size_t keep = (bytes + chunk_bytes - 1) / chunk_bytes;
   if (keep >= chunks.size()) return;
   Driver& d = drv();
-  cu_check(d.Unmap(va + keep * chunk_bytes, (chunks.size() - keep) * chunk_bytes), "cuMemUnmap");
-  for (size_t i = keep; i < chunks.size(); ++i) cu_check(d.Release(chunks[i]), "cuMemRelease");
+  for (size_t i = keep; i < chunks.size(); ++i) {
+    cu_check(d.Unmap(va + i * chunk_bytes, chunk_bytes), "cuMemUnmap");
+    cu_check(d.Release(chunks[i]), "cuMemRelease");
+  }
   chunks.resize(keep);
 }
 
 void Arena::release() {
   if (!va) return;
   Driver& d = drv();
-  if (!chunks.empty()) d.Unmap(va, chunks.size() * chunk_bytes);
-  for (auto h : chunks) d.Release(h);
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    d.Unmap(va + i * chunk_bytes, chunk_bytes);
+    d.Release(chunks[i]);
+  }
   chunks.clear();
   d.AddressFree(va, va_bytes);
   va = 0;
@@ -142,7 +147,8 @@ void Arena::grant_peer(int dev) {
   for (int p : peer_devices)
     if (p == dev) return;
   peer_devices.push_back(dev);
-  if (!chunks.empty()) set_access(va, chunks.size() * chunk_bytes, device, peer_devices);
+  for (size_t i = 0; i < chunks.size(); ++i)
+    set_access(va + i * chunk_bytes, chunk_bytes, device, peer_devices);
 }
 
 }  // namespace pl

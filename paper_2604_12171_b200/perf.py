@@ -120,7 +120,7 @@ class PatchRig:
 
     def __post_init__(self) -> None:
         wl = self.wl
-        cap = wl.batch * wl.blocks_per_req + 64
+        cap = wl.batch * (wl.blocks_per_req + 2) + 64
         self.src = KvStore(1, wl.k, wl.s, cap, wl.src_groups, num_groups=wl.model_groups,
                            cell_bytes=wl.cell_bytes, device=self.device, registry=self.registry)
         self.dst = KvStore(2, wl.k, wl.s, cap, (), num_groups=wl.model_groups,
