@@ -85,8 +85,11 @@ void Arena::ensure(size_t bytes) {
     // grow the reservation: new range (2x headroom), remap existing chunks there
     size_t new_va_bytes = std::max(want_va, va_bytes * 2);
     CUdeviceptr nva = 0;
-    cu_check(d.AddressReserve(&nva, new_va_bytes, vmm_granularity(device), 0, 0),
-             "cuMemAddressReserve");
+    CUresult rr = d.AddressReserve(&nva, new_va_bytes, 0, 0, 0);
+    if (rr != CUDA_SUCCESS)
+      fail(PL_E_CUDA, "cuMemAddressReserve(" + std::to_string(new_va_bytes) + " B) failed with "
+                          "CUresult " + std::to_string((int)rr) + " (chunk " +
+                          std::to_string(chunk_bytes) + " B)");
     for (size_t i = 0; i < chunks.size(); ++i) {
       cu_check(d.Map(nva + i * chunk_bytes, chunk_bytes, 0, chunks[i], 0), "cuMemMap");
       set_access(nva + i * chunk_bytes, chunk_bytes, device, peer_devices);
