@@ -4,16 +4,20 @@
 // the paper's extended PagedAttention reads KV through the block table's
 // resolved addresses.  Here the block table stores pool slot
 // indices; a (block, group) unit is [fp header][layer 0: s cells]...[layer k-1],
-// a cell is one token of one layer: [K: n_kv x D bf16][V: n_kv x D bf16].
+// a cell is one token of one layer: [K: n_kv x D bf16][V: n_kv x D bf16], so the
+// T tokens of one layer inside one block are T*cell contiguous bytes.
 //
 // Decode is HBM-bound (GQA group g gives 2g flop per KV byte, far below the
-// tensor-core ridge), so the dot products run on CUDA cores:
-//   - CTA = (sequence, context partition); warp = kv head (loops if n_kv > 8)
-//   - half-warp = one token; each lane owns D/16 dims -> one 128-bit load per
-//     lane per K (or V) row, 16 lanes cover the 256-byte head row contiguously
-//   - scores of a 2*NI-token chunk go through a 4-step xor-shuffle reduction,
-//     then one online-softmax rescale per chunk (not per token)
-//   - split-K partitions merged by a second kernel (flash-decoding)
+// tensor-core ridge), so the dot products run on CUDA cores.  Design:
+//   - persistent CTAs (one per SM) walk work items = (sequence, context part);
+//   - one elected thread streams each block's layer slice into shared memory with
+//     cp.async.bulk (TMA bulk copy, 64 KiB per stage for Llama shapes) on an
+//     mbarrier ring of 2-4 stages that runs ahead across item boundaries;
+//   - warp = kv head (or 8/n_kv warps share a head and split its tokens);
+//     half-warp = one token, each lane owns D/16 dims (one 16-byte LDS per row);
+//   - per stage: scores (4-step xor-shuffle reduction), one online-softmax
+//     rescale, then P.V from the same shared-memory tile;
+//   - per-(item, warp) partials (m, l, acc) merged by a small combine kernel.
 #include <cuda_bf16.h>
 
 #include <mutex>
@@ -24,7 +28,8 @@
 namespace pl {
 
 namespace {
-constexpr int kAttnWarps = 8;
+constexpr int kWarps = 8;
+constexpr int kMaxStageTok = 32;
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
@@ -44,7 +49,7 @@ __device__ __forceinline__ void unpack(const uint4& v, float* f) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    float2 x = __bfloat1622float2(h[i]);
+    const float2 x = __bfloat1622float2(h[i]);
     f[2 * i] = x.x;
     f[2 * i + 1] = x.y;
   }
@@ -53,145 +58,246 @@ __device__ __forceinline__ void unpack(const uint2& v, float* f) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    float2 x = __bfloat1622float2(h[i]);
+    const float2 x = __bfloat1622float2(h[i]);
     f[2 * i] = x.x;
     f[2 * i + 1] = x.y;
   }
 }
-template <class T>
-__device__ __forceinline__ T ldg_nc(const T* p) {
-  return __ldg(p);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 }  // namespace
 
-template <int D, int G, int NI>
-__global__ void __launch_bounds__(kAttnWarps * 32)
-paged_attn_kernel(AttnLaunch a, int n_parts, int part_tokens, float* ws_acc, float* ws_ml) {
-  using V = Vec<D>;
-  using VT = typename V::T;
-  constexpr int DPL = V::N;
-  constexpr int CH = 2 * NI;  // tokens per chunk per warp
-  __shared__ float sc[kAttnWarps][CH][G];
+struct AttnPlan {
+  int stage_tok;    // tokens per TMA stage (divides s)
+  int n_stage;      // ring depth
+  int parts;        // context parts per sequence
+  int part_tokens;  // multiple of s
+  int W;            // warps per kv head
+  int items;        // B * parts
+};
 
-  const int b = blockIdx.x / n_parts;
-  const int part = blockIdx.x % n_parts;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+struct ItemGeom {
+  int b, part, t0, n_stages;
+};
+
+__device__ __forceinline__ ItemGeom item_geom(const AttnLaunch& a, const AttnPlan& p, int item) {
+  ItemGeom g;
+  g.b = item / p.parts;
+  g.part = item % p.parts;
+  g.t0 = g.part * p.part_tokens;
+  const int tend = min(a.ctx[g.b], g.t0 + p.part_tokens);
+  g.n_stages = tend > g.t0 ? (tend - g.t0 + p.stage_tok - 1) / p.stage_tok : 0;
+  return g;
+}
+
+template <int D, int G, int NP>
+__global__ void __launch_bounds__(kWarps * 32, 1)
+paged_attn_kernel(AttnLaunch a, AttnPlan p, float* ws_acc, float* ws_ml) {
+  using VT = typename Vec<D>::T;
+  constexpr int DPL = Vec<D>::N;  // dims per lane
+  constexpr int DP2 = DPL / 2;    // float2 pairs per lane
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int64_t cell = 2ll * a.n_kv * D * 2;
+  const int64_t stage_bytes = (int64_t)p.stage_tok * cell;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.n_stage * stage_bytes);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int half = lane >> 4, hl = lane & 15;
-  const int ctx = a.ctx[b];
-  const int t0 = part * part_tokens;
-  const int t1 = min(ctx, t0 + part_tokens);
-  const int row = a.rows ? a.rows[b] : b;
-  const int32_t* tab = a.table + (int64_t)row * a.table_stride;
-  const int64_t cell_bytes = 2ll * a.n_kv * D * 2;
-  const int64_t v_off = (int64_t)a.n_kv * D * 2;
+  const int h = warp / p.W, sub = warp % p.W;
+  const bool active_warp = h < a.n_kv;
   const float qscale = a.scale * kLog2e;
+  const int64_t k_off = (int64_t)h * D * 2 + hl * sizeof(VT);
+  const int64_t v_off = (int64_t)a.n_kv * D * 2 + k_off;
+  const int parts_total = p.parts * p.W;
+  const int pairs_per_warp = p.stage_tok / 2 / p.W;  // a multiple of NP
 
-  for (int h = warp; h < a.n_kv; h += kAttnWarps) {
-    float q[G][DPL];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const VT* qp = reinterpret_cast<const VT*>(
-          static_cast<const __nv_bfloat16*>(a.q) + ((int64_t)b * a.n_q + h * G + g) * D);
-      unpack(qp[hl], q[g]);
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) q[g][d] *= qscale;
+  if (tid == 0) {
+    for (int i = 0; i < p.n_stage; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer cursor (thread 0 only): next (item, stage) to load; runs n_stage ahead
+  int l_item = blockIdx.x, l_st = 0;
+  auto l_norm = [&]() {
+    while (l_item < p.items && l_st >= item_geom(a, p, l_item).n_stages) {
+      l_item += gridDim.x;
+      l_st = 0;
     }
-    float m[G], l[G], acc[G][DPL];
+  };
+  auto issue = [&](int buf) {
+    const ItemGeom g = item_geom(a, p, l_item);
+    const int tok0 = g.t0 + l_st * p.stage_tok;
+    const int ntok = min(p.stage_tok, a.ctx[g.b] - tok0);
+    const int row = a.rows ? a.rows[g.b] : g.b;
+    const int32_t slot = a.table[(int64_t)row * a.table_stride + tok0 / a.s];
+    const uint8_t* src = a.pool + (int64_t)slot * a.unit_bytes + a.fp_bytes +
+                         ((int64_t)a.layer * a.s + tok0 % a.s) * cell;
+    const uint32_t bytes = (uint32_t)(ntok * cell);
+    mbar_expect_tx(&full[buf], bytes);
+    bulk_g2s(smem + buf * stage_bytes, src, bytes, &full[buf]);
+    ++l_st;
+    l_norm();
+  };
+  if (tid == 0) {
+    l_norm();
+    for (int i = 0; i < p.n_stage && l_item < p.items; ++i) issue(i);
+  }
+
+  int buf = 0;
+  uint32_t phase = 0;
+  for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+    const ItemGeom g = item_geom(a, p, item);
+    float2 q[G][DP2], acc[G][DP2];
+    float m[G], l[G];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      m[g] = -INFINITY;
-      l[g] = 0.f;
+    for (int gg = 0; gg < G; ++gg) {
+      m[gg] = -INFINITY;
+      l[gg] = 0.f;
 #pragma unroll
-      for (int d = 0; d < DPL; ++d) acc[g][d] = 0.f;
+      for (int d = 0; d < DP2; ++d) {
+        acc[gg][d] = make_float2(0.f, 0.f);
+        q[gg][d] = make_float2(0.f, 0.f);
+      }
     }
-    for (int base = t0; base < t1; base += CH) {
-      VT kb[NI], vb[NI];
-      // issue all loads of the chunk first (K and V rows, 2 tokens per iteration)
+    if (active_warp) {
 #pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        const int tok = base + 2 * i + half;
-        if (tok < t1) {
-          const int32_t slot = tab[tok / a.s];
-          const uint8_t* cell = a.pool + (int64_t)slot * a.unit_bytes + a.fp_bytes +
-                                ((int64_t)a.layer * a.s + tok % a.s) * cell_bytes +
-                                (int64_t)h * D * 2;
-          kb[i] = ldg_nc(reinterpret_cast<const VT*>(cell) + hl);
-          vb[i] = ldg_nc(reinterpret_cast<const VT*>(cell + v_off) + hl);
-        } else {
-          kb[i] = VT{};
-          vb[i] = VT{};
+      for (int gg = 0; gg < G; ++gg) {
+        float qf[DPL];
+        const VT* qp = reinterpret_cast<const VT*>(static_cast<const __nv_bfloat16*>(a.q) +
+                                                   ((int64_t)g.b * a.n_q + h * G + gg) * D);
+        unpack(qp[hl], qf);
+#pragma unroll
+        for (int d = 0; d < DP2; ++d) q[gg][d] = make_float2(qf[2 * d] * qscale, qf[2 * d + 1] * qscale);
+      }
+    }
+    for (int st = 0; st < g.n_stages; ++st) {
+      const int ntok = min(p.stage_tok, a.ctx[g.b] - (g.t0 + st * p.stage_tok));
+      mbar_wait(&full[buf], phase);
+      const uint8_t* tile = smem + buf * stage_bytes;
+      if (active_warp)
+      for (int sp = 0; sp < pairs_per_warp; sp += NP) {
+        const int tok_base = (sub * pairs_per_warp + sp) * 2 + half;  // tokens tok_base + 2*i
+        // pass 1: scores of this lane's NP tokens (independent chains -> ILP)
+        float sc[NP][G];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const int t = tok_base + 2 * i;
+          float kf[DPL];
+          if (t < ntok) {
+            unpack(*reinterpret_cast<const VT*>(tile + t * cell + k_off), kf);
+          } else {
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) kf[d] = 0.f;
+          }
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) {
+            float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int d = 0; d < DP2; ++d) s2 = __ffma2_rn(q[gg][d], make_float2(kf[2 * d], kf[2 * d + 1]), s2);
+            sc[i][gg] = s2.x + s2.y;
+          }
+        }
+#pragma unroll
+        for (int o = 8; o; o >>= 1)
+#pragma unroll
+          for (int i = 0; i < NP; ++i)
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg) sc[i][gg] += __shfl_xor_sync(0xffffffffu, sc[i][gg], o);
+        // one online-softmax rescale per stage (max over both half-warps' tokens)
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          float cm = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < NP; ++i) {
+            if (tok_base + 2 * i >= ntok) sc[i][gg] = -INFINITY;
+            cm = fmaxf(cm, sc[i][gg]);
+          }
+          cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 16));
+          const float mn = fmaxf(m[gg], cm);
+          const float corr = mn == -INFINITY ? 1.f : exp2f(m[gg] - mn);
+          m[gg] = mn;
+          l[gg] *= corr;
+          const float2 c2 = make_float2(corr, corr);
+#pragma unroll
+          for (int d = 0; d < DP2; ++d) acc[gg][d] = __fmul2_rn(acc[gg][d], c2);
+        }
+        // pass 2: P.V
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const int t = tok_base + 2 * i;
+          if (t < ntok) {
+            float vf[DPL];
+            unpack(*reinterpret_cast<const VT*>(tile + t * cell + v_off), vf);
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg) {
+              const float pr = exp2f(sc[i][gg] - m[gg]);
+              l[gg] += pr;
+              const float2 p2 = make_float2(pr, pr);
+#pragma unroll
+              for (int d = 0; d < DP2; ++d)
+                acc[gg][d] = __ffma2_rn(p2, make_float2(vf[2 * d], vf[2 * d + 1]), acc[gg][d]);
+            }
+          }
         }
       }
-      // scores
+      __syncthreads();  // every warp is done with this tile
+      if (tid == 0 && l_item < p.items) issue(buf);
+      if (++buf == p.n_stage) {
+        buf = 0;
+        phase ^= 1;
+      }
+    }
+    if (active_warp) {
 #pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        float kf[DPL];
-        unpack(kb[i], kf);
+      for (int gg = 0; gg < G; ++gg) {
+        l[gg] += __shfl_xor_sync(0xffffffffu, l[gg], 16);
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          float sdot = 0.f;
-#pragma unroll
-          for (int d = 0; d < DPL; ++d) sdot = fmaf(q[g][d], kf[d], sdot);
-#pragma unroll
-          for (int o = 8; o; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
-          if (hl == 0) sc[warp][2 * i + half][g] = base + 2 * i + half < t1 ? sdot : -INFINITY;
+        for (int d = 0; d < DP2; ++d) {
+          acc[gg][d].x += __shfl_xor_sync(0xffffffffu, acc[gg][d].x, 16);
+          acc[gg][d].y += __shfl_xor_sync(0xffffffffu, acc[gg][d].y, 16);
         }
       }
-      __syncwarp();
-      // one rescale per chunk
+      if (half == 0) {
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float cm = sc[warp][0][g];
+        for (int gg = 0; gg < G; ++gg) {
+          const int64_t pi =
+              ((int64_t)g.b * a.n_q + h * G + gg) * parts_total + g.part * p.W + sub;
+          float2* o = reinterpret_cast<float2*>(ws_acc + pi * D + hl * DPL);
 #pragma unroll
-        for (int t = 1; t < CH; ++t) cm = fmaxf(cm, sc[warp][t][g]);
-        const float mn = fmaxf(m[g], cm);
-        const float corr = exp2f(m[g] - mn);
-        m[g] = mn;
-        l[g] *= corr;
-#pragma unroll
-        for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
-      }
-#pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        float vf[DPL];
-        unpack(vb[i], vf);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float p = exp2f(sc[warp][2 * i + half][g] - m[g]);
-          l[g] += p;
-#pragma unroll
-          for (int d = 0; d < DPL; ++d) acc[g][d] = fmaf(p, vf[d], acc[g][d]);
-        }
-      }
-      __syncwarp();
-    }
-    // merge the two half-warps (same running max m in both)
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      l[g] += __shfl_xor_sync(0xffffffffu, l[g], 16);
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) acc[g][d] += __shfl_xor_sync(0xffffffffu, acc[g][d], 16);
-    }
-    if (half == 0) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int hq = h * G + g;
-        if (n_parts == 1) {
-          const float inv = l[g] > 0.f ? 1.f / l[g] : 0.f;
-          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + ((int64_t)b * a.n_q + hq) * D +
-                             hl * DPL;
-#pragma unroll
-          for (int d = 0; d < DPL; d += 2)
-            *reinterpret_cast<__nv_bfloat162*>(o + d) =
-                __floats2bfloat162_rn(acc[g][d] * inv, acc[g][d + 1] * inv);
-        } else {
-          const int64_t pi = ((int64_t)b * a.n_q + hq) * n_parts + part;
-          float* o = ws_acc + pi * D + hl * DPL;
-#pragma unroll
-          for (int d = 0; d < DPL; ++d) o[d] = acc[g][d];
+          for (int d = 0; d < DP2; ++d) o[d] = acc[gg][d];
           if (hl == 0) {
-            ws_ml[2 * pi] = m[g];
-            ws_ml[2 * pi + 1] = l[g];
+            ws_ml[2 * pi] = m[gg];
+            ws_ml[2 * pi + 1] = l[gg];
           }
         }
       }
@@ -200,9 +306,8 @@ paged_attn_kernel(AttnLaunch a, int n_parts, int part_tokens, float* ws_acc, flo
 }
 
 template <int D>
-__global__ void paged_attn_combine(const float* ws_acc, const float* ws_ml, int n_parts, int n_q,
-                                   void* out) {
-  const int64_t bh = blockIdx.x;  // (b * n_q + hq)
+__global__ void paged_attn_combine(const float* ws_acc, const float* ws_ml, int n_parts, void* out) {
+  const int64_t bh = blockIdx.x;  // b * n_q + hq
   const int d = threadIdx.x;
   if (d >= D) return;
   float M = -INFINITY;
@@ -211,7 +316,9 @@ __global__ void paged_attn_combine(const float* ws_acc, const float* ws_ml, int 
   if (M != -INFINITY) {
     for (int p = 0; p < n_parts; ++p) {
       const int64_t pi = bh * n_parts + p;
-      const float w = exp2f(ws_ml[2 * pi] - M);
+      const float mp = ws_ml[2 * pi];
+      if (mp == -INFINITY) continue;
+      const float w = exp2f(mp - M);
       L += ws_ml[2 * pi + 1] * w;
       O += ws_acc[pi * D + d] * w;
     }
@@ -236,45 +343,74 @@ float* workspace(size_t bytes) {
   return g_ws[dev];
 }
 
+template <int D, int G, int NP>
+void launch_np(const AttnLaunch& a, const AttnPlan& p, size_t smem, int sms, cudaStream_t st);
+
 template <int D, int G>
 void launch_dg(const AttnLaunch& a, cudaStream_t st) {
-  int sms = 148;
-  int dev = 0;
-  cudaGetDevice(&dev);
+  int dev = 0, sms = 148;
+  PL_CUDA(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  constexpr int NI = G <= 4 ? 8 : 4;
+  const int64_t cell = 2ll * a.n_kv * D * 2;
+  AttnPlan p{};
+  // TMA stage: tokens of one block slice, <= 64 KiB, dividing s
+  p.stage_tok = std::min(a.s, kMaxStageTok);
+  while (p.stage_tok > 1 && (a.s % p.stage_tok || p.stage_tok * cell > 65536)) --p.stage_tok;
+  const int64_t stage_bytes = p.stage_tok * cell;
+  const int64_t score_bytes = 0;
+  const int64_t budget = 220 * 1024 - 64;
+  p.n_stage = (int)std::max<int64_t>(2, std::min<int64_t>(4, budget / stage_bytes));
+  const size_t smem = (size_t)(p.n_stage * stage_bytes) + 64 + (size_t)score_bytes;
+  if (smem > 227 * 1024) fail(PL_E_INVALID, "KV cell too large for the shared-memory stage ring");
+  p.W = kWarps / a.n_kv;
   const int max_ctx = std::max(a.max_ctx, 1);
-  const int target = sms * 4;
-  int n_parts = (target + a.B - 1) / a.B;
-  const int max_parts = (max_ctx + 2 * NI - 1) / (2 * NI);
-  n_parts = std::max(1, std::min(n_parts, max_parts));
-  int part_tokens = (max_ctx + n_parts - 1) / n_parts;
-  part_tokens = (part_tokens + 2 * NI - 1) / (2 * NI) * (2 * NI);
-  n_parts = (max_ctx + part_tokens - 1) / part_tokens;
-  float *ws_acc = nullptr, *ws_ml = nullptr;
-  if (n_parts > 1) {
-    const size_t nparts_total = (size_t)a.B * a.n_q * n_parts;
-    float* ws = workspace(nparts_total * (D + 2) * sizeof(float));
-    ws_acc = ws;
-    ws_ml = ws + nparts_total * D;
+  // ~8 work items per SM; part length a multiple of the block size so stages never
+  // straddle two blocks
+  int parts = std::max(1, (8 * sms + a.B - 1) / a.B);
+  parts = std::min(parts, (max_ctx + a.s - 1) / a.s);
+  p.part_tokens = ((max_ctx + parts - 1) / parts + a.s - 1) / a.s * a.s;
+  p.parts = (max_ctx + p.part_tokens - 1) / p.part_tokens;
+  p.items = a.B * p.parts;
+  int np = p.stage_tok / 2 / p.W;
+  if (p.stage_tok % (2 * p.W)) fail(PL_E_INVALID, "stage tokens must split evenly over the warps of a head");
+  // pairs per sub-pass: bounded so q/acc/scores stay in registers
+  const int np_cap = (G >= 8 && D == 128) ? 2 : 8;
+  while (np > np_cap) np /= 2;
+  switch (np) {
+    case 1: return launch_np<D, G, 1>(a, p, smem, sms, st);
+    case 2: return launch_np<D, G, 2>(a, p, smem, sms, st);
+    case 4: return launch_np<D, G, 4>(a, p, smem, sms, st);
+    case 8: return launch_np<D, G, 8>(a, p, smem, sms, st);
+    default: fail(PL_E_INVALID, "tokens per block must give 2/4/8/16/32-token stages");
   }
+}
+
+template <int D, int G, int NP>
+void launch_np(const AttnLaunch& a, const AttnPlan& p, size_t smem, int sms, cudaStream_t st) {
+  auto kern = paged_attn_kernel<D, G, NP>;
+  PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem));
+  const int grid = std::max(1, std::min(p.items, sms * std::max(per_sm, 1)));
+  const int64_t n_parts_total = (int64_t)p.parts * p.W;
+  const size_t np = (size_t)a.B * a.n_q * n_parts_total;
+  float* ws = workspace(np * (D + 2) * sizeof(float));
   KernelTimer timer("paged_attn", st);
-  paged_attn_kernel<D, G, NI><<<(unsigned)(a.B * n_parts), kAttnWarps * 32, 0, st>>>(
-      a, n_parts, part_tokens, ws_acc, ws_ml);
+  kern<<<grid, kWarps * 32, smem, st>>>(a, p, ws, ws + np * D);
   note_launch();
   PL_CUDA(cudaGetLastError());
-  if (n_parts > 1) {
-    paged_attn_combine<D><<<(unsigned)(a.B * a.n_q), D, 0, st>>>(ws_acc, ws_ml, n_parts, a.n_q,
-                                                                 a.out);
-    note_launch();
-    PL_CUDA(cudaGetLastError());
-  }
+  paged_attn_combine<D><<<(unsigned)(a.B * a.n_q), D, 0, st>>>(ws, ws + np * D,
+                                                               (int)n_parts_total, a.out);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
 }
 }  // namespace
 
 void launch_paged_attn(const AttnLaunch& a, cudaStream_t st) {
   if (a.B <= 0) return;
   if (a.n_kv <= 0 || a.n_q % a.n_kv) fail(PL_E_INVALID, "n_q_heads must be a multiple of n_kv_heads");
+  if (a.n_kv > kWarps || kWarps % a.n_kv)
+    fail(PL_E_INVALID, "n_kv_heads must divide 8 (1, 2, 4 or 8 KV heads per stage)");
   const int G = a.n_q / a.n_kv;
 #define PL_ATTN_CASE(DD, GG) \
   if (a.D == DD && G == GG) return launch_dg<DD, GG>(a, st);
