@@ -365,7 +365,7 @@ def measure_decode(rig, stream, torch, wl, hbm_peak, K, W) -> dict:
     achieved = (kv_bytes_layer + q_bytes) / (per_launch / 1e3) / 1e9
     return {"tokens_per_s": round(B / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
             "layers_per_step": len(layers), "batch": B, "ctx": ctx_now,
-            "roofline": {"kernel": "paged_attn_kernel<128,4,8> (+combine)", "bound": "hbm",
+            "roofline": {"kernel": "paged_attn_kernel<128,4,8> (TMA bulk ring, +combine)", "bound": "hbm",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4),
                          "alg_bytes_per_launch": kv_bytes_layer + q_bytes,

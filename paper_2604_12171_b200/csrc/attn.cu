@@ -119,34 +119,101 @@ __device__ __forceinline__ ItemGeom item_geom(const AttnLaunch& a, const AttnPla
   return g;
 }
 
+// bf16x2 -> float2 without the generic conversion path: lo = x << 16, hi = x & 0xffff0000
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t x) {
+  return make_float2(__uint_as_float(x << 16), __uint_as_float(x & 0xffff0000u));
+}
+template <class VT, int DP2>
+__device__ __forceinline__ void load_row(const uint8_t* p, float2* out) {
+  const VT v = *reinterpret_cast<const VT*>(p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+  for (int d = 0; d < DP2; ++d) out[d] = bf2_to_f2(w[d]);
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Transposed butterfly over the 16 lanes of a half-warp: V partial sums per lane in,
+// R = max(1, V/16) fully reduced sums per lane out (lane hl holds values R*hl .. R*hl+R-1
+// when V >= 16).  Halves the shuffle count of V independent 4-step reductions.
+template <int V>
+__device__ __forceinline__ void transpose_reduce(float (&x)[V], int hl) {
+  constexpr int L = V >= 16 ? 4 : (V >= 8 ? 3 : (V >= 4 ? 2 : (V >= 2 ? 1 : 0)));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int o = 8 >> k;
+    if (k < L) {
+      const int n = V >> k;
+      const bool up = hl & o;
+#pragma unroll
+      for (int j = 0; j < n / 2; ++j) {
+        const float send = up ? x[j] : x[j + n / 2];
+        const float keep = up ? x[j + n / 2] : x[j];
+        x[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    } else {
+      x[0] += __shfl_xor_sync(0xffffffffu, x[0], o);
+    }
+  }
+}
+// index of the first value a lane holds after transpose_reduce, and the lane holding v
+template <int V>
+__device__ __forceinline__ int tr_base(int hl) {
+  constexpr int L = V >= 16 ? 4 : (V >= 8 ? 3 : (V >= 4 ? 2 : (V >= 2 ? 1 : 0)));
+  int base = 0;
+#pragma unroll
+  for (int k = 0; k < L; ++k)
+    if (hl & (8 >> k)) base += V >> (k + 1);
+  return base;
+}
+template <int V>
+__host__ __device__ constexpr int tr_owner(int v) {
+  constexpr int L = V >= 16 ? 4 : (V >= 8 ? 3 : (V >= 4 ? 2 : (V >= 2 ? 1 : 0)));
+  if (V >= 16) return v / (V / 16);
+  int lane = 0;
+  for (int k = 0; k < L; ++k)
+    if ((v >> (L - 1 - k)) & 1) lane += 8 >> k;
+  return lane;
+}
+template <int V>
+__device__ __forceinline__ bool tr_canonical(int hl) {
+  constexpr int L = V >= 16 ? 4 : (V >= 8 ? 3 : (V >= 4 ? 2 : (V >= 2 ? 1 : 0)));
+  int rest = 0;
+#pragma unroll
+  for (int k = L; k < 4; ++k) rest |= hl & (8 >> k);
+  return rest == 0;
+}
+
+// Every warp consumes; the last warp to finish with a ring buffer refills it with the
+// stage n_stage positions ahead in this CTA's stream (no producer warp, no CTA barrier).
 template <int D, int G, int NP>
 __global__ void __launch_bounds__(kWarps * 32, 1)
 paged_attn_kernel(AttnLaunch a, AttnPlan p, float* ws_acc, float* ws_ml) {
   using VT = typename Vec<D>::T;
   constexpr int DPL = Vec<D>::N;  // dims per lane
-  constexpr int DP2 = DPL / 2;    // float2 pairs per lane
+  constexpr int DP2 = DPL / 2;    // float2 per lane
+  constexpr int V = NP * G;       // scores per lane per sub-pass
+  constexpr int R = V >= 16 ? V / 16 : 1;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int64_t cell = 2ll * a.n_kv * D * 2;
-  const int64_t stage_bytes = (int64_t)p.stage_tok * cell;
+  const int cell = 2 * a.n_kv * D * 2;
+  const int stage_bytes = p.stage_tok * cell;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.n_stage * stage_bytes);
+  int* done_cnt = reinterpret_cast<int*>(full + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int half = lane >> 4, hl = lane & 15;
-  const int h = warp / p.W, sub = warp % p.W;
-  const bool active_warp = h < a.n_kv;
-  const float qscale = a.scale * kLog2e;
-  const int64_t k_off = (int64_t)h * D * 2 + hl * sizeof(VT);
-  const int64_t v_off = (int64_t)a.n_kv * D * 2 + k_off;
-  const int parts_total = p.parts * p.W;
-  const int pairs_per_warp = p.stage_tok / 2 / p.W;  // a multiple of NP
-
   if (tid == 0) {
-    for (int i = 0; i < p.n_stage; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < p.n_stage; ++i) {
+      mbar_init(&full[i], 1);
+      done_cnt[i] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  // producer cursor (thread 0 only): next (item, stage) to load; runs n_stage ahead
+  // lookahead cursor, advanced identically by every warp
   int l_item = blockIdx.x, l_st = 0;
   auto l_norm = [&]() {
     while (l_item < p.items && l_st >= item_geom(a, p, l_item).n_stages) {
@@ -154,7 +221,7 @@ paged_attn_kernel(AttnLaunch a, AttnPlan p, float* ws_acc, float* ws_ml) {
       l_st = 0;
     }
   };
-  auto issue = [&](int buf) {
+  auto issue = [&](int b) {  // one thread: load the cursor's stage into ring buffer b
     const ItemGeom g = item_geom(a, p, l_item);
     const int tok0 = g.t0 + l_st * p.stage_tok;
     const int ntok = min(p.stage_tok, a.ctx[g.b] - tok0);
@@ -162,125 +229,154 @@ paged_attn_kernel(AttnLaunch a, AttnPlan p, float* ws_acc, float* ws_ml) {
     const int32_t slot = a.table[(int64_t)row * a.table_stride + tok0 / a.s];
     const uint8_t* src = a.pool + (int64_t)slot * a.unit_bytes + a.fp_bytes +
                          ((int64_t)a.layer * a.s + tok0 % a.s) * cell;
-    const uint32_t bytes = (uint32_t)(ntok * cell);
-    mbar_expect_tx(&full[buf], bytes);
-    bulk_g2s(smem + buf * stage_bytes, src, bytes, &full[buf]);
+    mbar_expect_tx(&full[b], (uint32_t)(ntok * cell));
+    bulk_g2s(smem + b * stage_bytes, src, (uint32_t)(ntok * cell), &full[b]);
+  };
+  l_norm();
+  for (int i = 0; i < p.n_stage && l_item < p.items; ++i) {
+    if (tid == 0) issue(i);
     ++l_st;
     l_norm();
-  };
-  if (tid == 0) {
-    l_norm();
-    for (int i = 0; i < p.n_stage && l_item < p.items; ++i) issue(i);
   }
+
+  // ---------------- consumer warps
+  const int half = lane >> 4, hl = lane & 15;
+  const int h = warp / p.W, sub = warp % p.W;
+  const bool active = h < a.n_kv;
+  const float qscale = a.scale * kLog2e;
+  const int k_off = h * D * 2 + hl * (int)sizeof(VT);
+  const int v_off = a.n_kv * D * 2 + k_off;
+  const int parts_total = p.parts * p.W;
+  const int pairs_per_warp = p.stage_tok / 2 / p.W;
+  const int own = tr_base<V>(hl);
+  const bool canon = tr_canonical<V>(hl);
 
   int buf = 0;
   uint32_t phase = 0;
   for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
     const ItemGeom g = item_geom(a, p, item);
     float2 q[G][DP2], acc[G][DP2];
-    float m[G], l[G];
+    float m[G], lsum[G];
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
       m[gg] = -INFINITY;
-      l[gg] = 0.f;
+      lsum[gg] = 0.f;
 #pragma unroll
-      for (int d = 0; d < DP2; ++d) {
-        acc[gg][d] = make_float2(0.f, 0.f);
-        q[gg][d] = make_float2(0.f, 0.f);
-      }
-    }
-    if (active_warp) {
+      for (int d = 0; d < DP2; ++d) acc[gg][d] = make_float2(0.f, 0.f);
+      if (active) {
+        load_row<VT, DP2>(reinterpret_cast<const uint8_t*>(static_cast<const __nv_bfloat16*>(a.q) +
+                                                           ((int64_t)g.b * a.n_q + h * G + gg) * D) +
+                              hl * sizeof(VT),
+                          q[gg]);
 #pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        float qf[DPL];
-        const VT* qp = reinterpret_cast<const VT*>(static_cast<const __nv_bfloat16*>(a.q) +
-                                                   ((int64_t)g.b * a.n_q + h * G + gg) * D);
-        unpack(qp[hl], qf);
-#pragma unroll
-        for (int d = 0; d < DP2; ++d) q[gg][d] = make_float2(qf[2 * d] * qscale, qf[2 * d + 1] * qscale);
+        for (int d = 0; d < DP2; ++d) q[gg][d] = make_float2(q[gg][d].x * qscale, q[gg][d].y * qscale);
       }
     }
     for (int st = 0; st < g.n_stages; ++st) {
       const int ntok = min(p.stage_tok, a.ctx[g.b] - (g.t0 + st * p.stage_tok));
       mbar_wait(&full[buf], phase);
       const uint8_t* tile = smem + buf * stage_bytes;
-      if (active_warp)
-      for (int sp = 0; sp < pairs_per_warp; sp += NP) {
-        const int tok_base = (sub * pairs_per_warp + sp) * 2 + half;  // tokens tok_base + 2*i
-        // pass 1: scores of this lane's NP tokens (independent chains -> ILP)
-        float sc[NP][G];
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          const int t = tok_base + 2 * i;
-          float kf[DPL];
-          if (t < ntok) {
-            unpack(*reinterpret_cast<const VT*>(tile + t * cell + k_off), kf);
-          } else {
-#pragma unroll
-            for (int d = 0; d < DPL; ++d) kf[d] = 0.f;
-          }
-#pragma unroll
-          for (int gg = 0; gg < G; ++gg) {
-            float2 s2 = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int d = 0; d < DP2; ++d) s2 = __ffma2_rn(q[gg][d], make_float2(kf[2 * d], kf[2 * d + 1]), s2);
-            sc[i][gg] = s2.x + s2.y;
-          }
-        }
-#pragma unroll
-        for (int o = 8; o; o >>= 1)
-#pragma unroll
-          for (int i = 0; i < NP; ++i)
-#pragma unroll
-            for (int gg = 0; gg < G; ++gg) sc[i][gg] += __shfl_xor_sync(0xffffffffu, sc[i][gg], o);
-        // one online-softmax rescale per stage (max over both half-warps' tokens)
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-          float cm = -INFINITY;
+      if (active) {
+        for (int sp = 0; sp < pairs_per_warp; sp += NP) {
+          const int tok0 = (sub * pairs_per_warp + sp) * 2;  // first token of this sub-pass
+          const uint8_t* kp = tile + (tok0 + half) * cell + k_off;
+          // QK partial dots: V = NP x G values per lane
+          float x[V];
 #pragma unroll
           for (int i = 0; i < NP; ++i) {
-            if (tok_base + 2 * i >= ntok) sc[i][gg] = -INFINITY;
-            cm = fmaxf(cm, sc[i][gg]);
-          }
-          cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 16));
-          const float mn = fmaxf(m[gg], cm);
-          const float corr = mn == -INFINITY ? 1.f : exp2f(m[gg] - mn);
-          m[gg] = mn;
-          l[gg] *= corr;
-          const float2 c2 = make_float2(corr, corr);
-#pragma unroll
-          for (int d = 0; d < DP2; ++d) acc[gg][d] = __fmul2_rn(acc[gg][d], c2);
-        }
-        // pass 2: P.V
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          const int t = tok_base + 2 * i;
-          if (t < ntok) {
-            float vf[DPL];
-            unpack(*reinterpret_cast<const VT*>(tile + t * cell + v_off), vf);
+            float2 kf[DP2];
+            load_row<VT, DP2>(kp + 2 * i * cell, kf);
 #pragma unroll
             for (int gg = 0; gg < G; ++gg) {
-              const float pr = exp2f(sc[i][gg] - m[gg]);
-              l[gg] += pr;
-              const float2 p2 = make_float2(pr, pr);
+              float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-              for (int d = 0; d < DP2; ++d)
-                acc[gg][d] = __ffma2_rn(p2, make_float2(vf[2 * d], vf[2 * d + 1]), acc[gg][d]);
+              for (int d = 0; d < DP2; ++d) s2 = __ffma2_rn(q[gg][d], kf[d], s2);
+              x[i * G + gg] = s2.x + s2.y;
+            }
+          }
+          transpose_reduce<V>(x, hl);
+          // held scores: values own .. own+R-1 of this half's tokens; mask the tail
+          float cm[G];
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) cm[gg] = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            const int v = own + j;
+            if (tok0 + 2 * (v / G) + half >= ntok) x[j] = -INFINITY;
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg)
+              if (v % G == gg) cm[gg] = fmaxf(cm[gg], x[j]);
+          }
+          // stage max over both halves and all lanes; one rescale per sub-pass
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) cm[gg] = fmaxf(cm[gg], __shfl_xor_sync(0xffffffffu, cm[gg], o));
+            const float mn = fmaxf(m[gg], cm[gg]);
+            const float corr = mn == -INFINITY ? 1.f : fast_exp2(m[gg] - mn);
+            m[gg] = mn;
+            lsum[gg] *= corr;
+            const float2 c2 = make_float2(corr, corr);
+#pragma unroll
+            for (int d = 0; d < DP2; ++d) acc[gg][d] = __fmul2_rn(acc[gg][d], c2);
+          }
+          // probabilities of the held values (one exp per held value, not per lane-token)
+          float pr[R];
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            const int v = own + j;
+            float mv = m[0];
+#pragma unroll
+            for (int gg = 1; gg < G; ++gg)
+              if (v % G == gg) mv = m[gg];
+            pr[j] = x[j] == -INFINITY ? 0.f : fast_exp2(x[j] - mv);
+            if (canon) {
+#pragma unroll
+              for (int gg = 0; gg < G; ++gg)
+                if (v % G == gg) lsum[gg] += pr[j];
+            }
+          }
+          // P.V: broadcast each token's probabilities from their owner lanes
+          const uint8_t* vp = tile + (tok0 + half) * cell + v_off;
+#pragma unroll
+          for (int i = 0; i < NP; ++i) {
+            float2 vf[DP2];
+            load_row<VT, DP2>(vp + 2 * i * cell, vf);
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg) {
+              const int v = i * G + gg;
+              const float pv = __shfl_sync(0xffffffffu, pr[v % R], tr_owner<V>(v) + 16 * half);
+              const float2 p2 = make_float2(pv, pv);
+#pragma unroll
+              for (int d = 0; d < DP2; ++d) acc[gg][d] = __ffma2_rn(p2, vf[d], acc[gg][d]);
             }
           }
         }
       }
-      __syncthreads();  // every warp is done with this tile
-      if (tid == 0 && l_item < p.items) issue(buf);
+      __syncwarp();
+      if (l_item < p.items) {
+        if (lane == 0) {
+          __threadfence_block();
+          if (atomicAdd(&done_cnt[buf], 1) == kWarps - 1) {  // last reader of this buffer
+            done_cnt[buf] = 0;
+            __threadfence_block();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(buf);
+          }
+        }
+        ++l_st;
+        l_norm();
+      }
       if (++buf == p.n_stage) {
         buf = 0;
         phase ^= 1;
       }
     }
-    if (active_warp) {
+    if (active) {
 #pragma unroll
       for (int gg = 0; gg < G; ++gg) {
-        l[gg] += __shfl_xor_sync(0xffffffffu, l[gg], 16);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) lsum[gg] += __shfl_xor_sync(0xffffffffu, lsum[gg], o);
 #pragma unroll
         for (int d = 0; d < DP2; ++d) {
           acc[gg][d].x += __shfl_xor_sync(0xffffffffu, acc[gg][d].x, 16);
@@ -297,7 +393,7 @@ paged_attn_kernel(AttnLaunch a, AttnPlan p, float* ws_acc, float* ws_ml) {
           for (int d = 0; d < DP2; ++d) o[d] = acc[gg][d];
           if (hl == 0) {
             ws_ml[2 * pi] = m[gg];
-            ws_ml[2 * pi + 1] = l[gg];
+            ws_ml[2 * pi + 1] = lsum[gg];
           }
         }
       }
@@ -360,7 +456,7 @@ void launch_dg(const AttnLaunch& a, cudaStream_t st) {
   const int64_t score_bytes = 0;
   const int64_t budget = 220 * 1024 - 64;
   p.n_stage = (int)std::max<int64_t>(2, std::min<int64_t>(4, budget / stage_bytes));
-  const size_t smem = (size_t)(p.n_stage * stage_bytes) + 64 + (size_t)score_bytes;
+  const size_t smem = (size_t)(p.n_stage * stage_bytes) + 128 + (size_t)score_bytes;
   if (smem > 227 * 1024) fail(PL_E_INVALID, "KV cell too large for the shared-memory stage ring");
   p.W = kWarps / a.n_kv;
   const int max_ctx = std::max(a.max_ctx, 1);
@@ -374,7 +470,7 @@ void launch_dg(const AttnLaunch& a, cudaStream_t st) {
   int np = p.stage_tok / 2 / p.W;
   if (p.stage_tok % (2 * p.W)) fail(PL_E_INVALID, "stage tokens must split evenly over the warps of a head");
   // pairs per sub-pass: bounded so q/acc/scores stay in registers
-  const int np_cap = (G >= 8 && D == 128) ? 2 : 8;
+  const int np_cap = 8;
   while (np > np_cap) np /= 2;
   switch (np) {
     case 1: return launch_np<D, G, 1>(a, p, smem, sms, st);
