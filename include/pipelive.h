@@ -110,12 +110,16 @@ int pl_store_block_occupancy(pl_store* st, int64_t block_id, int group, uint64_t
 int pl_store_append(pl_store* st, int32_t req, int group, int64_t n, int payload_mode,
                     const uint64_t* payloads_host, uint64_t seed, const void* kv_dev, int mark);
 /* batched engine path (engine.py:377-404): item i appends counts[i] tokens of group
- * groups[i] to reqs[i] at its current written prefix.  Stops at the first overflow:
- * *n_done = items fully applied; returns PL_E_KV_OVERFLOW for item *n_done.
- * sched_cells_out (optional, per attached patch in attach order) accumulates n*k of the marks */
+ * groups[i] to reqs[i] at its current written prefix, with fingerprints of positions
+ * fp_starts[i].. (NULL: the written prefix; the reference hashes the engine's logical
+ * position, engine.py:398-399, which is where the cells land in every non-replay case).
+ * Stops at the first overflow: *n_done = items fully applied; returns PL_E_KV_OVERFLOW
+ * for item *n_done.  sched_cells_out (optional, per attached patch in attach order)
+ * accumulates n*k of the fused marks. */
 int pl_store_append_batch(pl_store* st, int n_items, const int32_t* reqs, const int32_t* groups,
-                          const int64_t* counts, const uint64_t* seeds, const void* kv_dev,
-                          int mark, int* n_done, int64_t* sched_cells_out, int n_sched);
+                          const int64_t* counts, const uint64_t* seeds, const int64_t* fp_starts,
+                          const void* kv_dev, int mark, int* n_done, int64_t* sched_cells_out,
+                          int n_sched);
 int pl_store_write_slots(pl_store* st, int32_t req, int group, int64_t n,
                          const int64_t* positions_host, const uint64_t* payloads_host);
 

@@ -268,12 +268,12 @@ int pl_store_append(pl_store* st, int32_t req, int group, int64_t n, int mode,
   return guard([&] { st->s->append(req, group, n, mode, payloads, seed, kv, mark); });
 }
 int pl_store_append_batch(pl_store* st, int n_items, const int32_t* reqs, const int32_t* groups,
-                          const int64_t* counts, const uint64_t* seeds, const void* kv, int mark,
-                          int* n_done, int64_t* sched, int n_sched) {
+                          const int64_t* counts, const uint64_t* seeds, const int64_t* fp_starts,
+                          const void* kv, int mark, int* n_done, int64_t* sched, int n_sched) {
   int status = PL_OK;
   int rc = guard([&] {
-    status = st->s->append_batch(n_items, reqs, groups, counts, seeds, kv, mark, sched, n_sched,
-                                 n_done);
+    status = st->s->append_batch(n_items, reqs, groups, counts, seeds, fp_starts, kv, mark, sched,
+                                 n_sched, n_done);
   });
   if (rc != PL_OK) return rc;
   if (status != PL_OK) pl::g_err = st->s->last_msg;

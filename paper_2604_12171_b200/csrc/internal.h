@@ -177,8 +177,9 @@ struct Store {
   void append(int32_t req, int g, int64_t n, int mode, const uint64_t* payloads, uint64_t seed,
               const void* kv_dev, int mark);
   int append_batch(int n_items, const int32_t* reqs, const int32_t* groups,
-                   const int64_t* counts, const uint64_t* seeds, const void* kv_dev, int mark,
-                   int64_t* sched, int n_sched, int* n_done);  // returns status
+                   const int64_t* counts, const uint64_t* seeds, const int64_t* fp_starts,
+                   const void* kv_dev, int mark, int64_t* sched, int n_sched,
+                   int* n_done);  // returns status
   void write_slots(int32_t req, int g, int64_t n, const int64_t* pos, const uint64_t* payloads);
   int64_t compact();
   void resize(int64_t new_cap);
@@ -192,7 +193,10 @@ struct Store {
   void reserve_positions(int32_t req, int g, const std::vector<Interval>& iv);
 
   // launch K1 for a list of (req, group, start, count) items
-  struct WriteItem { int32_t req; int32_t group; int64_t start; int64_t count; uint64_t seed; };
+  struct WriteItem {
+    int32_t req; int32_t group; int64_t start; int64_t count; uint64_t seed;
+    int64_t fp_start;  // position the fingerprints are computed for (== start normally)
+  };
   void launch_write(const std::vector<WriteItem>& items, int mode, const uint64_t* payloads,
                     const int64_t* positions, const void* kv_dev, int mark);
 };
@@ -285,7 +289,7 @@ struct Patch {
 struct WriteLaunch {
   // items
   const int32_t* reqs; const int32_t* groups; const int64_t* starts; const int64_t* offs;
-  const uint64_t* seeds; int n_items; int64_t total;
+  const uint64_t* seeds; const int64_t* fp_starts; int n_items; int64_t total;
   // payload sources
   int mode; const uint64_t* payloads; const int64_t* positions; const uint8_t* kv;
   // store layout

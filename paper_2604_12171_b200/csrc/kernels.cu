@@ -54,8 +54,9 @@ __global__ void __launch_bounds__(kWarps * 32) kv_write_kernel(WriteLaunch w) {
     const int32_t req = w.reqs[it];
     const int32_t g = w.groups[it];
     const int64_t pos = w.positions ? w.positions[t] : w.starts[it] + (t - w.offs[it]);
-    const uint64_t fp = w.mode == PL_PAYLOAD_SEED ? cell_fingerprint(w.seeds[it], (uint64_t)pos)
-                                                  : w.payloads[t];
+    const uint64_t fp = w.mode == PL_PAYLOAD_SEED
+                            ? cell_fingerprint(w.seeds[it], (uint64_t)(w.fp_starts[it] + (t - w.offs[it])))
+                            : w.payloads[t];
     const int32_t slot = w.table[(int64_t)req * w.max_chain + pos / w.s];
     if (slot < 0) continue;  // host guarantees the chain covers pos
     const int off = (int)(pos % w.s);

@@ -136,7 +136,7 @@ void Patch::mark(int32_t req, int g, int64_t start, int64_t n, bool device) {
   if (lg < 0) return;
   dirty_keys += insert_interval(dirty[{req, lg}], start, start + n);
   if (device) {
-    Store::WriteItem it{req, lg, start, n, 0};
+    Store::WriteItem it{req, lg, start, n, 0, start};
     mark_device({it});
   }
 }
@@ -185,7 +185,7 @@ int64_t Patch::seed() {
       if (w <= 0) continue;
       dirty_keys += insert_interval(dirty[{req, lg}], 0, w);
       seeded += w;
-      items.push_back({req, lg, 0, w, 0});
+      items.push_back({req, lg, 0, w, 0, 0});
     }
   }
   mark_device(items);

@@ -373,13 +373,14 @@ void Store::launch_write(const std::vector<WriteItem>& items, int mode, const ui
   flush();
   const int n = (int)items.size();
   std::vector<int32_t> reqs(n), groups(n);
-  std::vector<int64_t> starts(n), offs(n + 1, 0);
+  std::vector<int64_t> starts(n), offs(n + 1, 0), fps(n);
   std::vector<uint64_t> seeds(n);
   for (int i = 0; i < n; ++i) {
     reqs[i] = items[i].req;
     groups[i] = items[i].group;
     starts[i] = items[i].start;
     seeds[i] = items[i].seed;
+    fps[i] = items[i].fp_start;
     offs[i + 1] = offs[i] + items[i].count;
   }
   const int64_t total = offs[n];
@@ -387,6 +388,7 @@ void Store::launch_write(const std::vector<WriteItem>& items, int mode, const ui
   int ir = up.add(reqs.data(), 4 * n), ig = up.add(groups.data(), 4 * n);
   int is = up.add(starts.data(), 8 * n), io = up.add(offs.data(), 8 * (n + 1));
   int id = up.add(seeds.data(), 8 * n);
+  int ifs = up.add(fps.data(), 8 * n);
   int ip = -1, ix = -1;
   if (mode == PL_PAYLOAD_EXPLICIT) ip = up.add(payloads, 8 * total);
   if (positions) ix = up.add(positions, 8 * total);
@@ -397,6 +399,7 @@ void Store::launch_write(const std::vector<WriteItem>& items, int mode, const ui
   w.starts = up.ptr<int64_t>(is);
   w.offs = up.ptr<int64_t>(io);
   w.seeds = up.ptr<uint64_t>(id);
+  w.fp_starts = up.ptr<int64_t>(ifs);
   w.n_items = n;
   w.total = total;
   w.mode = mode;
@@ -467,12 +470,13 @@ void Store::append(int32_t req, int g, int64_t n, int mode, const uint64_t* payl
   occupied += n;
   if (!materialised[g]) materialise(g);
   if (mark) host_mark(this, req, g, start, n, nullptr, 0);
-  launch_write({{req, g, start, n, seed}}, mode, payloads, nullptr, kv_dev, mark);
+  launch_write({{req, g, start, n, seed, start}}, mode, payloads, nullptr, kv_dev, mark);
 }
 
 int Store::append_batch(int n_items, const int32_t* reqs, const int32_t* groups,
-                        const int64_t* counts, const uint64_t* seeds, const void* kv_dev, int mark,
-                        int64_t* sched, int n_sched, int* n_done) {
+                        const int64_t* counts, const uint64_t* seeds, const int64_t* fp_starts,
+                        const void* kv_dev, int mark, int64_t* sched, int n_sched,
+                        int* n_done) {
   std::vector<WriteItem> items;
   items.reserve(n_items);
   int done = 0;
@@ -509,7 +513,8 @@ int Store::append_batch(int n_items, const int32_t* reqs, const int32_t* groups,
     occupied += n;
     if (!materialised[g]) materialise(g);
     if (mark) host_mark(this, req, g, start, n, sched, n_sched);
-    items.push_back({req, g, start, n, seeds ? seeds[done] : 0});
+    items.push_back({req, g, start, n, seeds ? seeds[done] : 0,
+                     fp_starts ? fp_starts[done] : start});
   }
   // kv_dev rows are consumed in item order for the applied prefix
   launch_write(items, PL_PAYLOAD_SEED, nullptr, nullptr, kv_dev, mark);
@@ -556,7 +561,7 @@ void Store::write_slots(int32_t req, int g, int64_t n, const int64_t* pos, const
   if (t.written[g] == 0) t.written_order.push_back(g);
   t.written[g] = std::max(t.written[g], top);
   if (!materialised[g]) materialise(g);
-  std::vector<WriteItem> items{{req, g, 0, (int64_t)upos.size(), 0}};
+  std::vector<WriteItem> items{{req, g, 0, (int64_t)upos.size(), 0, 0}};
   launch_write(items, PL_PAYLOAD_EXPLICIT, upay.data(), upos.data(), nullptr, 0);
 }
 

@@ -478,6 +478,28 @@ class KvStore:
         _check(N.lib().pl_store_append(self._h, h, layer_group, n_tokens, N.PL_PAYLOAD_SEED,
                                        None, seed, kv_dev, 1 if mark else 0))
 
+    def append_groups_seeded(self, request_id, groups: list[int], n_tokens: int,
+                             seeds: list[int], start: int | None = None) -> tuple[int, bool]:
+        """Engine path (engine.py:392-400): append n_tokens to each group in order with
+        fingerprints of positions start.. (default: each group's written prefix), one K1
+        launch.  Stops at the first overflow; returns (groups done, overflowed)."""
+        if not groups or n_tokens <= 0:
+            return 0, False
+        h = self._handle(request_id)
+        m = len(groups)
+        reqs = np.full(m, h, dtype=np.int32)
+        gs = N.as_i32(groups)
+        counts = np.full(m, n_tokens, dtype=np.int64)
+        sd = N.as_u64(seeds)
+        fs = None if start is None else np.full(m, start, dtype=np.int64)
+        done = C.c_int()
+        rc = N.lib().pl_store_append_batch(self._h, m, N.ptr(reqs), N.ptr(gs), N.ptr(counts),
+                                           N.ptr(sd), N.ptr(fs), None, 0, C.byref(done), None, 0)
+        if rc == N.PL_E_KV_OVERFLOW:
+            return done.value, True
+        _check(rc)
+        return done.value, False
+
     def write_slots(self, request_id, layer_group: int,
                     items: Sequence[tuple[int, int]]) -> None:
         if not items:

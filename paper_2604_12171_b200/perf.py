@@ -69,7 +69,7 @@ def append_batch(store: KvStore, reqs: list[int], groups: list[int], counts: lis
     sd = N.as_u64(seeds)
     done = C.c_int()
     rc = N.lib().pl_store_append_batch(store._h, len(reqs), N.ptr(r), N.ptr(g), N.ptr(c),
-                                       N.ptr(sd), kv_dev, 1 if mark else 0, C.byref(done),
+                                       N.ptr(sd), None, kv_dev, 1 if mark else 0, C.byref(done),
                                        None, 0)
     N.check(rc)
     return done.value

@@ -1,0 +1,93 @@
+"""Switch-point parity: full reconfiguration runs in parity mode (reference event
+clock, GPU data plane) must reproduce the reference's own runs bit for bit --
+trace bytes (sha256), convergence/commit timestamps, the micro-batch count at
+the switch, pause, lags, capacities, metrics and the final state digest.
+Mirrors pkg/tests/test_coordinator.py and acceptance criteria 4/6/10."""
+
+import hashlib
+
+import pytest
+
+import sim_scenarios
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(name):
+    from paper_2604_12171_b200.engine import compute_metrics
+    from paper_2604_12171_b200.simulation import RunResult, Simulation
+
+    scen, seed, fill = sim_scenarios.golden_runs()[name]
+    sim = Simulation(scen, seed=seed)
+    if fill:
+        fill(sim)
+    sim.scheduler.run(until=600.0)
+    return sim, RunResult(sim.trace, compute_metrics(sim.trace), sim.statuses, seed)
+
+
+@pytest.mark.parametrize("name", ["fig3_seed5", "fig3_nopatch", "stoptime_L4", "stoptime_L8",
+                                  "hetero_c10_seed123", "hetero_n60_seed7"])
+def test_run_matches_reference(golden, name):
+    want = golden("simulations.json")[name]
+    sim, res = _run(name)
+    jsonl = res.trace.to_jsonl()
+    assert len(res.trace) == want["n_events"]
+    assert hashlib.sha256(jsonl.encode()).hexdigest() == want["trace_sha"]
+    assert len(sim.statuses) == len(want["statuses"])
+    for got, exp in zip(sim.statuses, want["statuses"]):
+        assert got.outcome == exp["outcome"]
+        assert got.timestamps == exp["timestamps"]          # incl. convergence_time / commit_start
+        assert got.pause_duration == exp["pause"]
+        assert {str(k): v for k, v in got.lag_at_final_sync.items()} == exp["lag_at_final_sync"]
+        assert got.steps_at_commit == want["steps_at_commit"]  # the switch iteration
+        # criterion 4 at the commit snapshot
+        for pair, groups in got.migrated_groups.items():
+            for g in groups:
+                assert got.dest_snapshots[pair][g] == got.source_snapshots[pair][g]
+    assert {str(g): s.capacity_blocks for g, s in sim.stores.items()} == want["capacities"]
+    assert res.metrics.as_row() == want["metrics"]
+    assert sim.state_digest() == want["state_digest"]
+
+
+def test_fig3_structure():
+    """pkg/tests/test_coordinator.py:97-173 on the GPU data plane"""
+    from paper_2604_12171_b200.cluster import max_blocks
+
+    sim, res = _run("fig3_seed5")
+    status = sim.statuses[0]
+    assert status.outcome == "success" and sim.engine.committed_config == sim_scenarios.C_B
+    resized = {ev.actor for ev in res.trace if ev.kind == "primitive"
+               and ev.payload["name"] == "ResizeKV"}
+    assert resized == {"gpu1", "gpu2", "gpu3"}
+    ts = status.timestamps
+    assert ts["resize_end"] <= ts["weightload_start"] <= ts["commit_start"]
+    assert ts["commit_start"] >= ts["convergence_time"]
+    assert all(lag < 50 for lag in status.lag_at_final_sync.values())
+    assert 1 not in sim.stores[1].resident_groups
+    assert sim.loader.residency.on_gpu(2) == {2, 3}
+    b_new = min(max_blocks(sim_scenarios.fig3_cluster()[g], len(sim_scenarios.C_B.layers_for(g)),
+                           sim_scenarios.fig3_model(), 0.9) for g in (1, 2, 3))
+    assert all(s.capacity_blocks == b_new for s in sim.stores.values())
+
+
+def test_rollback_restores_state_bit_exact():
+    """pkg/tests/test_coordinator.py:176-201: destination overflow -> rollback"""
+    from paper_2604_12171_b200.events import stable_hash
+    from paper_2604_12171_b200.simulation import Simulation
+
+    sim = Simulation(sim_scenarios.fig3_scenario(num_requests=0), seed=0)
+    s = sim.stores[2].tokens_per_block
+    ghost = 40 * s
+    for g in (sim.model.group_of(3), sim.model.group_of(4)):
+        sim.stores[2].append("ghost", g, ghost, [stable_hash("ghost", g, i) for i in range(ghost)])
+    plan = sim.coordinator.feasibility(sim_scenarios.C_B, tau=50)
+    for i in range(plan.b_shrink - 22):
+        g = sim.model.group_of(5)
+        sim.stores[3].append(f"filler{i:03d}", g, s, [stable_hash("filler", i, j) for j in range(s)])
+    before = sim.state_digest()
+    done = []
+    sim.coordinator.reconfigure(plan, done.append)
+    sim.scheduler.run()
+    assert done[0].outcome == "failed(MigrationOverflow)"
+    assert sim.engine.committed_config == sim_scenarios.C_A
+    assert sim.state_digest() == before
