@@ -28,7 +28,7 @@
 namespace pl {
 
 namespace {
-constexpr int kWarps = 8;
+constexpr int kMaxWarps = 16;
 constexpr int kMaxStageTok = 32;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -189,9 +189,10 @@ __device__ __forceinline__ bool tr_canonical(int hl) {
 
 // Every warp consumes; the last warp to finish with a ring buffer refills it with the
 // stage n_stage positions ahead in this CTA's stream (no producer warp, no CTA barrier).
-template <int D, int G, int NP>
-__global__ void __launch_bounds__(kWarps * 32, 1)
+template <int D, int G, int NP, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
 paged_attn_kernel(AttnLaunch a, AttnPlan p, float* ws_acc, float* ws_ml) {
+  constexpr int kWarps = NW;
   using VT = typename Vec<D>::T;
   constexpr int DPL = Vec<D>::N;  // dims per lane
   constexpr int DP2 = DPL / 2;    // float2 per lane
@@ -439,7 +440,7 @@ float* workspace(size_t bytes) {
   return g_ws[dev];
 }
 
-template <int D, int G, int NP>
+template <int D, int G, int NP, int NW>
 void launch_np(const AttnLaunch& a, const AttnPlan& p, size_t smem, int sms, cudaStream_t st);
 
 template <int D, int G>
@@ -458,7 +459,11 @@ void launch_dg(const AttnLaunch& a, cudaStream_t st) {
   p.n_stage = (int)std::max<int64_t>(2, std::min<int64_t>(4, budget / stage_bytes));
   const size_t smem = (size_t)(p.n_stage * stage_bytes) + 128 + (size_t)score_bytes;
   if (smem > 227 * 1024) fail(PL_E_INVALID, "KV cell too large for the shared-memory stage ring");
-  p.W = kWarps / a.n_kv;
+  // 8 warps (one per KV head of the Llama shapes).  16 warps at <= 128 registers were
+  // measured slower (818 vs 496 us/layer at the 8B shape): the per-sub-pass softmax
+  // bookkeeping doubles and the token split halves the ILP per warp.
+  constexpr int NW = 8;
+  p.W = NW / a.n_kv;
   const int max_ctx = std::max(a.max_ctx, 1);
   // ~8 work items per SM; part length a multiple of the block size so stages never
   // straddle two blocks
@@ -469,21 +474,22 @@ void launch_dg(const AttnLaunch& a, cudaStream_t st) {
   p.items = a.B * p.parts;
   int np = p.stage_tok / 2 / p.W;
   if (p.stage_tok % (2 * p.W)) fail(PL_E_INVALID, "stage tokens must split evenly over the warps of a head");
-  // pairs per sub-pass: bounded so q/acc/scores stay in registers
-  const int np_cap = 8;
+  // pairs per sub-pass: bounded so q/acc/scores stay in registers (no spills, -Xptxas -v)
+  const int np_cap = NW == 8 ? 8 : (D == 128 ? (G >= 4 ? 2 : 4) : (G >= 4 ? 4 : 8));
   while (np > np_cap) np /= 2;
   switch (np) {
-    case 1: return launch_np<D, G, 1>(a, p, smem, sms, st);
-    case 2: return launch_np<D, G, 2>(a, p, smem, sms, st);
-    case 4: return launch_np<D, G, 4>(a, p, smem, sms, st);
-    case 8: return launch_np<D, G, 8>(a, p, smem, sms, st);
+    case 1: return launch_np<D, G, 1, NW>(a, p, smem, sms, st);
+    case 2: return launch_np<D, G, 2, NW>(a, p, smem, sms, st);
+    case 4: return launch_np<D, G, 4, NW>(a, p, smem, sms, st);
+    case 8: return launch_np<D, G, 8, NW>(a, p, smem, sms, st);
     default: fail(PL_E_INVALID, "tokens per block must give 2/4/8/16/32-token stages");
   }
 }
 
-template <int D, int G, int NP>
+template <int D, int G, int NP, int NW>
 void launch_np(const AttnLaunch& a, const AttnPlan& p, size_t smem, int sms, cudaStream_t st) {
-  auto kern = paged_attn_kernel<D, G, NP>;
+  constexpr int kWarps = NW;
+  auto kern = paged_attn_kernel<D, G, NP, NW>;
   PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
   PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem));
@@ -505,7 +511,7 @@ void launch_np(const AttnLaunch& a, const AttnPlan& p, size_t smem, int sms, cud
 void launch_paged_attn(const AttnLaunch& a, cudaStream_t st) {
   if (a.B <= 0) return;
   if (a.n_kv <= 0 || a.n_q % a.n_kv) fail(PL_E_INVALID, "n_q_heads must be a multiple of n_kv_heads");
-  if (a.n_kv > kWarps || kWarps % a.n_kv)
+  if (a.n_kv > 8 || 8 % a.n_kv)
     fail(PL_E_INVALID, "n_kv_heads must divide 8 (1, 2, 4 or 8 KV heads per stage)");
   const int G = a.n_q / a.n_kv;
 #define PL_ATTN_CASE(DD, GG) \

@@ -87,3 +87,132 @@ def golden_runs():
         scen, fill = stoptime_scenario(migrate_layers=L)
         runs[f"stoptime_L{L}"] = (scen, 0, fill)
     return runs
+
+
+# ---------------------------------------------------------------------------------------------
+# BASELINE configs as parity scenarios.  PP-degree changes need GPUs without layers (the
+# idle-GPU extension): configs simply omit idle GPUs.  The builders take the
+# package namespace so the golden generator can build the identical scenario on the
+# reference (with the same extension monkeypatched in, tests/golden/make_golden.py).
+def _ns_default():
+    import types
+
+    import paper_2604_12171_b200 as pkg
+    from paper_2604_12171_b200 import scenario as sc
+    return types.SimpleNamespace(GpuSpec=pkg.GpuSpec, ModelSpec=pkg.ModelSpec,
+                                 PPConfig=pkg.PPConfig, WorkloadSpec=pkg.WorkloadSpec,
+                                 FeatureFlags=pkg.FeatureFlags, Scenario=sc.Scenario,
+                                 ReconfigTrigger=sc.ReconfigTrigger, idle_field=True)
+
+
+def _scenario(ns, **kw):
+    s = ns.Scenario(**kw)
+    if getattr(ns, "idle_field", False):
+        s.allow_idle_gpus = True
+    return s
+
+
+def b200(ns, gid, mem_gib=180, prefill=2e-7, decode=4e-6, gran=2 * MIB):
+    return ns.GpuSpec(id=gid, mem_total=mem_gib * GIB, mem_bandwidth=7.7e12,
+                      prefill_cost=prefill, decode_cost=decode, alloc_granularity=gran)
+
+
+def config0_tiny(ns=None):
+    """configs[0]: tiny 4-layer Llama-style model (d=256, 4 q / 2 kv heads x 64 -> 512 B of
+    KV per token-layer), k=1, 16-token blocks, PP 2->3 on 3 GPUs."""
+    ns = ns or _ns_default()
+    gran = 16 * 512
+    cluster = [b200(ns, i, mem_gib=1, prefill=2e-6, decode=2e-5, gran=gran) for i in (1, 2, 3)]
+    model = ns.ModelSpec(num_layers=4, layer_weight_bytes=1536 * 1024, token_kv_bytes_per_layer=512,
+                         stacking_factor=1, activation_bytes_per_token=512)
+    cur = ns.PPConfig([(1, (1, 2)), (2, (3, 4))])
+    tgt = ns.PPConfig([(1, (1, 1)), (2, (2, 3)), (3, (4, 4))])
+    wl = ns.WorkloadSpec("shift_schedule", rate=40.0, num_requests=24,
+                         shifts=((0.0, "prefill_heavy"), (0.3, "decode_heavy")))
+    return _scenario(ns, cluster=cluster, model=model, initial_config=cur, workload=wl,
+                     triggers=[ns.ReconfigTrigger(at=0.3, target=tgt)], flags=ns.FeatureFlags())
+
+
+def config1_8b(ns=None, n=48):
+    """configs[1]: Llama-3-8B shape (32 L, 4096 B KV per token-layer, 0.436 GB/layer),
+    k=4, 16-token blocks, PP 2->4 with minimal movement on 4 B200s, decode-heavy load."""
+    ns = ns or _ns_default()
+    cluster = [b200(ns, i) for i in (1, 2, 3, 4)]
+    model = ns.ModelSpec(num_layers=32, layer_weight_bytes=436 * 10 ** 6,
+                         token_kv_bytes_per_layer=4096, stacking_factor=4,
+                         activation_bytes_per_token=8 * KIB)
+    cur = ns.PPConfig([(1, (1, 16)), (2, (17, 32))])
+    tgt = ns.PPConfig([(1, (1, 8)), (3, (9, 16)), (2, (17, 24)), (4, (25, 32))])
+    wl = ns.WorkloadSpec("decode_heavy", rate=200.0, num_requests=n)
+    return _scenario(ns, cluster=cluster, model=model, initial_config=cur, workload=wl,
+                     triggers=[ns.ReconfigTrigger(at=0.1, target=tgt)], flags=ns.FeatureFlags())
+
+
+def config2_70b(ns=None, n=32):
+    """configs[2]: Llama-3-70B shape (80 L, 1.711 GB/layer), k=4, PP 4->8 with HBM
+    pre-filled by KV so Phase 2 must shrink every store and cleanup grows them back."""
+    ns = ns or _ns_default()
+    cluster = [b200(ns, i, decode=8e-6) for i in range(1, 9)]
+    model = ns.ModelSpec(num_layers=80, layer_weight_bytes=1711 * 10 ** 6,
+                         token_kv_bytes_per_layer=4096, stacking_factor=4,
+                         activation_bytes_per_token=16 * KIB)
+    cur = ns.PPConfig([(1, (1, 20)), (2, (21, 40)), (3, (41, 60)), (4, (61, 80))])
+    # GPU1 also receives layers 21-24, so its union set (24 layers) exceeds every current
+    # stage and b_shrink < current capacity: a real live shrink
+    tgt = ns.PPConfig([(1, (1, 24)), (5, (25, 32)), (2, (33, 40)), (6, (41, 48)),
+                       (3, (49, 56)), (7, (57, 64)), (4, (65, 72)), (8, (73, 80))])
+    wl = ns.WorkloadSpec("decode_heavy", rate=100.0, num_requests=n)
+    return _scenario(ns, cluster=cluster, model=model, initial_config=cur, workload=wl,
+                     triggers=[ns.ReconfigTrigger(at=0.2, target=tgt)], flags=ns.FeatureFlags())
+
+
+def config3_uneven(ns=None, n=48):
+    """configs[3]: 8 GPUs, 70B shape at k=2: even prefill-optimal split -> uneven
+    generation-heavy split across a prefill_heavy -> decode_heavy trace shift."""
+    ns = ns or _ns_default()
+    cluster = [b200(ns, i, prefill=1e-7 * (1 + i % 3), decode=3e-6 * (1 + (i + 1) % 2))
+               for i in range(1, 9)]
+    model = ns.ModelSpec(num_layers=80, layer_weight_bytes=1711 * 10 ** 6,
+                         token_kv_bytes_per_layer=4096, stacking_factor=2,
+                         activation_bytes_per_token=16 * KIB)
+
+    def split(sizes):
+        out, first = [], 1
+        for gid, size in zip(range(1, 9), sizes):
+            out.append((gid, (first, first + size - 1)))
+            first += size
+        return ns.PPConfig(out)
+
+    cur = split([10] * 8)
+    tgt = split([6, 8, 10, 12, 12, 10, 12, 10])
+    shift = n / 60.0 / 2
+    wl = ns.WorkloadSpec("shift_schedule", rate=60.0, num_requests=n,
+                         shifts=((0.0, "prefill_heavy"), (shift, "decode_heavy")))
+    return _scenario(ns, cluster=cluster, model=model, initial_config=cur, workload=wl,
+                     triggers=[ns.ReconfigTrigger(at=shift, target=tgt)], flags=ns.FeatureFlags())
+
+
+def config_runs(ns=None):
+    """name -> (scenario, seed, fill) of the BASELINE-config parity runs"""
+    return {"config0_tiny": (config0_tiny(ns), 3, None),
+            "config1_8b": (config1_8b(ns), 1, None),
+            "config2_70b": (config2_70b(ns), 2, prefill_kv),
+            "config3_uneven": (config3_uneven(ns), 4, None)}
+
+
+def prefill_kv(sim, fraction=0.6):
+    """Fill every store with synthetic KV up to ``fraction`` of the shrink budget, so the
+    reconfiguration's Phase 2 shrink and post-commit grow act on a near-full HBM."""
+    from math import ceil
+    for gpu_id, store in sim.stores.items():
+        groups = sorted(store.resident_groups)
+        if not groups:
+            continue
+        s = store.tokens_per_block
+        blocks = int(store.capacity_blocks * fraction * 0.5)
+        per_req = 64 * s
+        for r in range(ceil(blocks / 64)):
+            rid = f"prefill{gpu_id}_{r:03d}"
+            for g in groups:
+                store.append(rid, g, per_req, [(gpu_id << 40) + (g << 32) + r * per_req + i
+                                               for i in range(per_req)])

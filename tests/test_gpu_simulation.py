@@ -91,3 +91,32 @@ def test_rollback_restores_state_bit_exact():
     assert done[0].outcome == "failed(MigrationOverflow)"
     assert sim.engine.committed_config == sim_scenarios.C_A
     assert sim.state_digest() == before
+
+
+@pytest.mark.parametrize("name", ["config0_tiny", "config1_8b", "config2_70b", "config3_uneven"])
+def test_baseline_config_matches_reference_with_extension(golden, name):
+    """BASELINE configs 0-3 (PP 2->3, 2->4, 4->8 with a near-full HBM, uneven 8-GPU re-split)
+    against the reference run with the same idle-GPU extension (tests/golden/make_golden.py)."""
+    from paper_2604_12171_b200.engine import compute_metrics
+    from paper_2604_12171_b200.simulation import Simulation
+
+    want = golden("config_runs.json")[name]
+    scen, seed, fill = sim_scenarios.config_runs()[name]
+    sim = Simulation(scen, seed=seed)
+    if fill:
+        fill(sim)
+    sim.scheduler.run(until=600.0)
+    jsonl = sim.trace.to_jsonl()
+    assert len(sim.trace) == want["n_events"]
+    assert hashlib.sha256(jsonl.encode()).hexdigest() == want["trace_sha"]
+    for got, exp in zip(sim.statuses, want["statuses"]):
+        assert got.outcome == exp["outcome"] == "success"
+        assert got.timestamps == exp["timestamps"]
+        assert got.pause_duration == exp["pause"]
+        assert got.steps_at_commit == want["steps_at_commit"]
+        for pair, groups in got.migrated_groups.items():
+            for g in groups:
+                assert got.dest_snapshots[pair][g] == got.source_snapshots[pair][g]
+    assert {str(g): s.capacity_blocks for g, s in sim.stores.items()} == want["capacities"]
+    assert compute_metrics(sim.trace).as_row() == want["metrics"]
+    assert sim.state_digest() == want["state_digest"]
