@@ -442,18 +442,34 @@ def measure_e2e(rig, stream, torch, wl, K, world) -> dict:
 
 def measure_resize(rig, stream, torch, wl) -> dict:
     """Post-commit cleanup on the source stage (coordinator.py:340-354): drop the groups
-    that left, compact + shrink to a smaller budget, then grow back; wall ms each."""
+    that left, compact + shrink to a smaller budget, then grow back; wall ms each.
+
+    The *_ms figures are the critical path of each call (host block manager, K6 moves,
+    block-table remap, VMM map of new chunks).  Physical reclaim of retired chunks runs
+    on the store's reclaimer thread (vmm.cu); `reclaim_ms` is how long forcing it to
+    finish took afterwards (memory back with the driver), reported beside it.  A grow
+    inside the grace period re-takes the still-mapped tail (`grow_warm_ms`); a grow
+    after the reclaim maps fresh chunks from the driver (`grow_cold_ms`)."""
     st = rig.src
     out = {}
+
+    def vdelta(a, b):
+        return {k: b[k] - a[k] for k in ("tail_reused_chunks", "cache_reused_chunks",
+                                         "created_chunks")}
+
     torch.cuda.synchronize()
+    st.reclaim()
     t0 = time.perf_counter()
     freed = st.drop_layer_groups(list(wl.mig_groups))
     out["drop_groups_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    out["drop_pending_reclaim_bytes"] = st.vmm_stats()["pending_reclaim_bytes"]
+    out["drop_reclaim_ms"] = round(st.reclaim(), 3)
     # free a quarter of the requests so the shrink must relocate live tail blocks
     for i in range(0, wl.batch, 4):
         st.free_request(f"r{i:04d}")
     cap = st.capacity_blocks
     target = max(st.used_blocks + 16, int(cap * 0.8))
+    st.sync()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     st.compact()
@@ -461,13 +477,26 @@ def measure_resize(rig, stream, torch, wl) -> dict:
     st.sync()
     out["shrink_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
     out["shrink_stats"] = st.last_resize_stats()
+    v0 = st.vmm_stats()
     t0 = time.perf_counter()
     st.resize(cap)
     st.sync()
-    out["grow_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
-    out["grow_stats"] = st.last_resize_stats()
+    out["grow_warm_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    v1 = st.vmm_stats()
+    out["grow_warm_stats"] = {**st.last_resize_stats(), **vdelta(v0, v1)}
+    st.resize(target)
+    st.sync()
+    out["reclaim_ms"] = round(st.reclaim(), 3)
+    v2 = st.vmm_stats()
+    t0 = time.perf_counter()
+    st.resize(cap)
+    st.sync()
+    out["grow_cold_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    out["grow_cold_stats"] = {**st.last_resize_stats(), **vdelta(v2, st.vmm_stats())}
     out["blocks"] = {"from": cap, "to": target, "live": st.used_blocks}
     out["tokens_freed_by_drop"] = freed
+    out["note"] = ("*_ms = critical path; physical unmap/release deferred to the reclaimer "
+                   "thread (reclaim_ms, drop_reclaim_ms = forced completion)")
     return out
 
 

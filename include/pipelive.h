@@ -144,6 +144,14 @@ int pl_store_free_request(pl_store* st, int32_t req, int64_t* stats_out, int cap
 int pl_store_utilization(pl_store* st, double* out);
 /* resize instrumentation: blocks relocated, table entries remapped, bytes mapped/unmapped */
 int pl_store_last_resize_stats(pl_store* st, int64_t* out4);
+/* physical reclaim (vmm.cu): a shrink or dropped group only retires its chunks; a
+ * helper thread unmaps them after the stream work queued before the call, then returns
+ * them to the driver after a grace period (PL_RECLAIM_*_GRACE_MS).  vmm_stats: chunks
+ * re-taken from the still-mapped tail / re-mapped from the cache / cuMemCreate'd since
+ * the store was created, and physical bytes not yet back with the driver.  reclaim
+ * forces every pending unmap + release now (blocking), returns the wait in ms. */
+int pl_store_vmm_stats(pl_store* st, int64_t* out4);
+int pl_store_reclaim(pl_store* st, double* out_ms);
 
 /* ---- device views for kernels outside the store (K2 attention, perf drivers) */
 int pl_store_group_base(pl_store* st, int group, uint64_t* out_dev_ptr);

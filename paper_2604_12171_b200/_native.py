@@ -87,6 +87,8 @@ SIGNATURES = [
     ("pl_store_free_request", C.c_int, [vp, i32, vp, C.c_int, P(C.c_int)]),
     ("pl_store_utilization", C.c_int, [vp, P(dbl)]),
     ("pl_store_last_resize_stats", C.c_int, [vp, vp]),
+    ("pl_store_vmm_stats", C.c_int, [vp, vp]),
+    ("pl_store_reclaim", C.c_int, [vp, P(dbl)]),
     ("pl_store_group_base", C.c_int, [vp, C.c_int, P(u64)]),
     ("pl_store_table_dev", C.c_int, [vp, P(u64), P(i64)]),
     ("pl_store_flush", C.c_int, [vp]),

@@ -378,6 +378,28 @@ int pl_store_last_resize_stats(pl_store* st, int64_t* out4) {
     for (int i = 0; i < 4; ++i) out4[i] = st->s->last_resize[i];
   });
 }
+int pl_store_vmm_stats(pl_store* st, int64_t* out4) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    int64_t tail = 0, cache = 0, created = 0;
+    for (auto& a : s->arenas) {
+      tail += (int64_t)a.last_tail_reused;
+      cache += (int64_t)a.last_cache_reused;
+      created += (int64_t)a.last_created;
+    }
+    out4[0] = tail;
+    out4[1] = cache;
+    out4[2] = created;
+    out4[3] = s->reclaimer->pending();
+  });
+}
+int pl_store_reclaim(pl_store* st, double* out_ms) {
+  return guard([&] {
+    PL_CUDA(cudaSetDevice(st->s->device));
+    const double ms = st->s->reclaimer->wait_all(true);
+    if (out_ms) *out_ms = ms;
+  });
+}
 int pl_store_group_base(pl_store* st, int group, uint64_t* out) {
   return guard([&] {
     if (group < 0 || group >= st->s->n_model_groups) pl::fail(PL_E_INVALID, "group out of range");

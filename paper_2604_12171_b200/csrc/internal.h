@@ -6,7 +6,12 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <condition_variable>
 #include <cstdint>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <map>
 #include <set>
 #include <stdexcept>
@@ -40,6 +45,40 @@ struct KernelTimer {
 };
 
 // ---------------------------------------------------------------------------
+// Reclaimer: one helper thread per store that takes physical reclaim (range-wide
+// cuMemUnmap after the stream work that may read the range, then cuMemRelease)
+// off the resize critical path, with a grace period in which a grow can take the
+// chunks back (vmm.cu).
+struct Reclaimer {
+  struct Job;
+  int device;
+  size_t chunk_bytes;
+  int unmap_grace_ms, release_grace_ms;
+  Reclaimer(int device, size_t chunk_bytes);
+  ~Reclaimer();
+  // hand a mapped range + its chunks over; returns a job id (cancel() takes it back)
+  uint64_t submit(cudaStream_t st, CUdeviceptr va, size_t bytes,
+                  std::vector<CUmemGenericAllocationHandle> handles, CUdeviceptr free_va,
+                  size_t free_va_bytes, bool immediate);
+  // true + still-mapped range if the job had not started; false after waiting for it
+  bool cancel(uint64_t id, CUdeviceptr* va, std::vector<CUmemGenericAllocationHandle>* hs);
+  std::vector<CUmemGenericAllocationHandle> take(size_t n);  // unmapped cached chunks
+  double wait_all(bool release_cache);  // finish every job (and release the cache)
+  int64_t pending();                    // physical bytes not yet back with the driver
+  double last_unmap_ms = 0;
+
+ private:
+  void loop();
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<std::unique_ptr<Job>> jobs;
+  std::vector<std::pair<CUmemGenericAllocationHandle, std::chrono::steady_clock::time_point>> cache;
+  uint64_t next_id = 0, running = 0;
+  int64_t pending_bytes = 0;
+  bool stopping = false, flush_cache = false;
+  std::thread th;
+};
+
 // Arena: one reserved virtual range backed by physical chunks mapped with the
 // CUDA VMM driver API.  Pools grow/shrink by mapping/unmapping chunks at the
 // tail; the base address only changes if the reservation itself must grow.
@@ -50,12 +89,20 @@ struct Arena {
   size_t chunk_bytes = 0;
   std::vector<CUmemGenericAllocationHandle> chunks;
   std::vector<int> peer_devices;  // devices granted access besides `device`
+  Reclaimer* rc = nullptr;
+  uint64_t tail_job = 0;          // retired tail still mapped (pending reclaim job)
+  // instrumentation of the last resize: chunks taken back from the mapped tail,
+  // re-mapped from the reclaimer's cache, created with cuMemCreate
+  size_t last_tail_reused = 0, last_cache_reused = 0, last_created = 0;
 
   size_t mapped_bytes() const { return chunks.size() * chunk_bytes; }
-  void ensure(size_t bytes);  // map chunks until mapped >= bytes
-  void trim(size_t bytes);    // unmap chunks wholly beyond `bytes`
-  void release();
+  void ensure(size_t bytes);                  // map chunks until mapped >= bytes
+  void trim(size_t bytes, cudaStream_t st);   // retire chunks wholly beyond `bytes`
+  void release(cudaStream_t st);              // retire everything + the reservation
   void grant_peer(int dev);
+
+ private:
+  void reclaim_tail();
 };
 size_t vmm_granularity(int device);
 
@@ -102,6 +149,7 @@ struct Store {
   std::vector<uint64_t> occ;
 
   // device: per-group pool arenas (materialised iff resident or written)
+  std::unique_ptr<Reclaimer> reclaimer;
   std::vector<Arena> arenas;
   std::vector<uint8_t> materialised;
 

@@ -7,6 +7,9 @@
 // kernel resolves addresses through.  Host mutations are mirrored to the
 // device as deduplicated deltas flushed right before the next kernel.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -44,10 +47,12 @@ Store::Store(int device_, int gpu_id_, int k_, int s_, int64_t cell_bytes_, int 
   occ_words = (s + 63) / 64;
   resident.assign(n_model_groups, 0);
   materialised.assign(n_model_groups, 0);
+  reclaimer = std::make_unique<Reclaimer>(device, (size_t)chunk_bytes);
   arenas.resize(n_model_groups);
   for (int g = 0; g < n_model_groups; ++g) {
     arenas[g].device = device;
     arenas[g].chunk_bytes = (size_t)chunk_bytes;
+    arenas[g].rc = reclaimer.get();
   }
   PL_CUDA(cudaMalloc(&d_bases_, sizeof(uint64_t) * n_model_groups));
   PL_CUDA(cudaMemset(d_bases_, 0, sizeof(uint64_t) * n_model_groups));
@@ -70,7 +75,11 @@ Store::~Store() {
   cudaSetDevice(device);
   cudaStreamSynchronize(stream);
   detach_patches(this);
-  for (auto& a : arenas) a.release();
+  try {
+    for (auto& a : arenas) a.release(stream);
+  } catch (...) {
+  }
+  reclaimer.reset();  // joins the helper thread after every unmap/release
   cudaFree(d_table);
   cudaFree(d_owner);
   cudaFree(d_owner_idx);
@@ -354,8 +363,7 @@ void Store::materialise(int g) {
 }
 void Store::dematerialise(int g) {
   if (!materialised[g]) return;
-  PL_CUDA(cudaStreamSynchronize(stream));
-  arenas[g].release();
+  arenas[g].release(stream);  // unmapped by the reclaimer once the stream passes this point
   materialised[g] = 0;
   refresh_bases();
 }
@@ -677,11 +685,11 @@ void Store::resize(int64_t new_cap) {
   for (int64_t sl = new_cap; sl < old_cap; ++sl)
     if (h_owner[sl] != -1) set_owner((int32_t)sl, -1, -1);
   flush();
-  // release the physical tail of every pool
-  PL_CUDA(cudaStreamSynchronize(stream));
+  // retire the physical tail of every pool (unmapped by the reclaimer after the K6
+  // moves queued above have run)
   const int64_t before = mapped_bytes();
   for (int g = 0; g < n_model_groups; ++g)
-    if (materialised[g]) arenas[g].trim((size_t)std::max<int64_t>(new_cap, 1) * unit_bytes);
+    if (materialised[g]) arenas[g].trim((size_t)std::max<int64_t>(new_cap, 1) * unit_bytes, stream);
   last_resize[3] = before - mapped_bytes();
 }
 
@@ -697,6 +705,9 @@ int64_t Store::drop_groups(const int32_t* groups_in, int n) {
     for (size_t i = 0; i < unknown.size(); ++i) m += (i ? ", " : "") + std::to_string(unknown[i]);
     fail(PL_E_UNKNOWN_LAYER_GROUP, m + "] not resident");
   }
+  static const bool trace = std::getenv("PL_TRACE_RESIZE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = now();
   int64_t freed = 0;
   for (int32_t req = 0; req < (int32_t)tables.size(); ++req) {
     ReqTable& t = tables[req];
@@ -729,8 +740,16 @@ int64_t Store::drop_groups(const int32_t* groups_in, int n) {
     resident[g] = 0;
     --n_resident;
   }
+  auto t1 = now();
   flush();
+  auto t2 = now();
   for (int32_t g : groups) dematerialise(g);
+  auto t3 = now();
+  if (trace) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[pl] drop_groups: host %.3f ms, flush %.3f ms, dematerialise %.3f ms\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, t3));
+  }
   return freed;
 }
 

@@ -3,7 +3,26 @@
 // (kvstore.py:259-282) grows/shrinks real memory without moving live KV: the
 // base address (and every resolved block address) stays put.  Driver entry
 // points come from cudaGetDriverEntryPoint so the library links only cudart.
+//
+// Physical reclaim is off the critical path.  Measured on B200 (profiles/
+// vmm_reclaim_r1.txt): a per-chunk cuMemUnmap costs 0.3-12 ms (it flushes GPU
+// TLBs), one range-wide cuMemUnmap over 64 chunks ~6 ms, cuMemRelease 0.1-3 ms per
+// chunk, and none of these stall kernel launches when issued from another thread.
+// So a shrink (trim) or a dropped group (release) only detaches the tail chunks
+// from the arena and hands them to the store's Reclaimer thread, which waits for
+// the stream work that may still read them (a CUDA event), unmaps the whole range
+// in one call after a short grace period, and returns the chunks to the driver
+// after a second grace period.  A grow inside the grace period takes the still
+// mapped tail back (no driver call at all) or re-maps cached physical chunks
+// (no cuMemCreate).  cuMemCreate failing with out-of-memory forces every pending
+// reclaim first, so memory pressure turns the deferral off.
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
+#include <deque>
 #include <mutex>
+#include <thread>
 
 #include "internal.h"
 
@@ -57,6 +76,7 @@ CUmemAllocationProp prop_for(int device) {
 }
 
 void set_access(CUdeviceptr va, size_t bytes, int device, const std::vector<int>& peers) {
+  if (!bytes) return;
   std::vector<CUmemAccessDesc> desc(1 + peers.size());
   for (size_t i = 0; i < desc.size(); ++i) {
     desc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -64,6 +84,19 @@ void set_access(CUdeviceptr va, size_t bytes, int device, const std::vector<int>
     desc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   }
   cu_check(drv().SetAccess(va, bytes, desc.data(), desc.size()), "cuMemSetAccess");
+}
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t).count();
+}
+bool trace_on() {
+  static const bool t = std::getenv("PL_TRACE_RESIZE") != nullptr;
+  return t;
+}
+int env_ms(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
 }
 
 }  // namespace
@@ -76,9 +109,196 @@ size_t vmm_granularity(int device) {
   return g;
 }
 
+// ---------------------------------------------------------------------------
+// Reclaimer
+struct Reclaimer::Job {
+  uint64_t id = 0;
+  Clock::time_point due;
+  cudaEvent_t ev = nullptr;  // stream work that may still touch the range
+  CUdeviceptr va = 0;        // mapped range [va, va + bytes)
+  size_t bytes = 0;
+  std::vector<CUmemGenericAllocationHandle> handles;
+  CUdeviceptr free_va = 0;  // reservation to free after the unmap (whole-arena release)
+  size_t free_va_bytes = 0;
+  Clock::time_point submitted;
+};
+
+Reclaimer::Reclaimer(int dev, size_t chunk)
+    : device(dev), chunk_bytes(chunk),
+      unmap_grace_ms(env_ms("PL_RECLAIM_UNMAP_GRACE_MS", 20)),
+      release_grace_ms(env_ms("PL_RECLAIM_RELEASE_GRACE_MS", 20)) {
+  th = std::thread([this] { loop(); });
+}
+
+Reclaimer::~Reclaimer() {
+  {
+    std::unique_lock<std::mutex> lk(mu);
+    stopping = true;
+    for (auto& j : jobs) j->due = Clock::now();
+  }
+  cv.notify_all();
+  th.join();
+  // the thread finished every job; return the cached chunks
+  for (auto& c : cache) drv().Release(c.first);
+  cache.clear();
+}
+
+uint64_t Reclaimer::submit(cudaStream_t st, CUdeviceptr va, size_t bytes,
+                           std::vector<CUmemGenericAllocationHandle> handles, CUdeviceptr free_va,
+                           size_t free_va_bytes, bool immediate) {
+  auto j = std::make_unique<Job>();
+  PL_CUDA(cudaEventCreateWithFlags(&j->ev, cudaEventDisableTiming));
+  PL_CUDA(cudaEventRecord(j->ev, st));
+  j->va = va;
+  j->bytes = bytes;
+  j->handles = std::move(handles);
+  j->free_va = free_va;
+  j->free_va_bytes = free_va_bytes;
+  j->submitted = Clock::now();
+  j->due = j->submitted + std::chrono::milliseconds(immediate ? 0 : unmap_grace_ms);
+  uint64_t id;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    id = j->id = ++next_id;
+    pending_bytes += (int64_t)(j->handles.size() * chunk_bytes);
+    jobs.push_back(std::move(j));
+  }
+  cv.notify_all();
+  return id;
+}
+
+bool Reclaimer::cancel(uint64_t id, CUdeviceptr* va, std::vector<CUmemGenericAllocationHandle>* hs) {
+  std::unique_lock<std::mutex> lk(mu);
+  for (auto it = jobs.begin(); it != jobs.end(); ++it) {
+    if ((*it)->id != id) continue;
+    *va = (*it)->va;
+    *hs = std::move((*it)->handles);
+    cudaEventDestroy((*it)->ev);
+    pending_bytes -= (int64_t)(hs->size() * chunk_bytes);
+    jobs.erase(it);
+    return true;
+  }
+  // started (or done): wait until its range is unmapped so it can be mapped again
+  cv.wait(lk, [&] { return running != id; });
+  return false;
+}
+
+std::vector<CUmemGenericAllocationHandle> Reclaimer::take(size_t n) {
+  std::lock_guard<std::mutex> lk(mu);
+  std::vector<CUmemGenericAllocationHandle> out;
+  while (n-- && !cache.empty()) {
+    out.push_back(cache.back().first);
+    cache.pop_back();
+    pending_bytes -= (int64_t)chunk_bytes;
+  }
+  return out;
+}
+
+double Reclaimer::wait_all(bool release_cache) {
+  const auto t0 = Clock::now();
+  std::unique_lock<std::mutex> lk(mu);
+  for (auto& j : jobs) j->due = Clock::now();
+  if (release_cache)
+    for (auto& c : cache) c.second = Clock::now();
+  flush_cache = flush_cache || release_cache;
+  cv.notify_all();
+  cv.wait(lk, [&] { return jobs.empty() && running == 0 && (!release_cache || cache.empty()); });
+  flush_cache = false;
+  return ms_since(t0);
+}
+
+int64_t Reclaimer::pending() {
+  std::lock_guard<std::mutex> lk(mu);
+  return pending_bytes;
+}
+
+void Reclaimer::loop() {
+  cudaSetDevice(device);
+  Driver& d = drv();
+  std::unique_lock<std::mutex> lk(mu);
+  for (;;) {
+    const auto now = Clock::now();
+    // 1. the earliest due job
+    auto best = jobs.end();
+    for (auto it = jobs.begin(); it != jobs.end(); ++it)
+      if (best == jobs.end() || (*it)->due < (*best)->due) best = it;
+    if (best != jobs.end() && (*best)->due <= now) {
+      std::unique_ptr<Job> j = std::move(*best);
+      jobs.erase(best);
+      running = j->id;
+      lk.unlock();
+      cudaEventSynchronize(j->ev);
+      cudaEventDestroy(j->ev);
+      if (j->bytes) {
+        CUresult ur = d.Unmap(j->va, j->bytes);
+        if (trace_on())
+          std::fprintf(stderr, "[pl] reclaim job %llu: unmap va=%llx bytes=%zu rc=%d\n",
+                       (unsigned long long)j->id, (unsigned long long)j->va, j->bytes, (int)ur);
+      }
+      if (j->free_va) d.AddressFree(j->free_va, j->free_va_bytes);
+      lk.lock();
+      const auto rel = Clock::now() + std::chrono::milliseconds(release_grace_ms);
+      for (auto h : j->handles) cache.push_back({h, rel});
+      last_unmap_ms = ms_since(j->submitted);
+      running = 0;
+      cv.notify_all();
+      continue;
+    }
+    // 2. cached chunks past their release time go back to the driver
+    bool released = false;
+    for (size_t i = 0; i < cache.size();) {
+      if (cache[i].second <= now || flush_cache) {
+        auto h = cache[i].first;
+        cache.erase(cache.begin() + (long)i);
+        pending_bytes -= (int64_t)chunk_bytes;
+        lk.unlock();
+        d.Release(h);
+        lk.lock();
+        released = true;
+        break;  // the cache may have changed while unlocked
+      }
+      ++i;
+    }
+    if (released) {
+      if (cache.empty()) cv.notify_all();
+      continue;
+    }
+    if (stopping && jobs.empty()) break;
+    // 3. sleep until the next deadline or a new job
+    auto wake = now + std::chrono::seconds(3600);
+    for (auto& j : jobs) wake = std::min(wake, j->due);
+    for (auto& c : cache) wake = std::min(wake, c.second);
+    cv.notify_all();
+    cv.wait_until(lk, wake);
+  }
+  running = 0;
+  cv.notify_all();
+}
+
+// ---------------------------------------------------------------------------
+// Arena
+void Arena::reclaim_tail() {
+  if (!tail_job) return;
+  CUdeviceptr tva = 0;
+  std::vector<CUmemGenericAllocationHandle> hs;
+  const uint64_t id = tail_job;
+  tail_job = 0;
+  const bool got = rc->cancel(id, &tva, &hs);
+  if (trace_on())
+    std::fprintf(stderr, "[pl] reclaim_tail: job %llu %s (%zu chunks back)\n",
+                 (unsigned long long)id, got ? "cancelled" : "already ran", hs.size());
+  if (got) {
+    // still mapped at the arena's tail: take it back as is
+    for (auto h : hs) chunks.push_back(h);
+    last_tail_reused += hs.size();
+  }
+}
+
 void Arena::ensure(size_t bytes) {
   if (bytes <= mapped_bytes()) return;
   Driver& d = drv();
+  reclaim_tail();
+  if (bytes <= mapped_bytes()) return;
   size_t want_chunks = (bytes + chunk_bytes - 1) / chunk_bytes;
   size_t want_va = want_chunks * chunk_bytes;
   if (want_va > va_bytes) {
@@ -90,58 +310,75 @@ void Arena::ensure(size_t bytes) {
       fail(PL_E_CUDA, "cuMemAddressReserve(" + std::to_string(new_va_bytes) + " B) failed with "
                           "CUresult " + std::to_string((int)rr) + " (chunk " +
                           std::to_string(chunk_bytes) + " B)");
-    for (size_t i = 0; i < chunks.size(); ++i) {
+    for (size_t i = 0; i < chunks.size(); ++i)
       cu_check(d.Map(nva + i * chunk_bytes, chunk_bytes, 0, chunks[i], 0), "cuMemMap");
-      set_access(nva + i * chunk_bytes, chunk_bytes, device, peer_devices);
-    }
+    set_access(nva, chunks.size() * chunk_bytes, device, peer_devices);
     if (va) {
-      for (size_t i = 0; i < chunks.size(); ++i)
-        cu_check(d.Unmap(va + i * chunk_bytes, chunk_bytes), "cuMemUnmap");
+      if (!chunks.empty()) cu_check(d.Unmap(va, chunks.size() * chunk_bytes), "cuMemUnmap");
       cu_check(d.AddressFree(va, va_bytes), "cuMemAddressFree");
     }
     va = nva;
     va_bytes = new_va_bytes;
   }
+  const size_t first = chunks.size();
+  const size_t need = want_chunks - first;
+  std::vector<CUmemGenericAllocationHandle> hs = rc->take(need);
+  last_cache_reused += hs.size();
   CUmemAllocationProp p = prop_for(device);
-  size_t first = chunks.size();
-  while (chunks.size() < want_chunks) {
+  bool forced = false;
+  while (hs.size() < need) {
     CUmemGenericAllocationHandle h;
     CUresult r = d.Create(&h, chunk_bytes, &p, 0);
+    if (r == CUDA_ERROR_OUT_OF_MEMORY && !forced) {
+      // memory pressure: finish every deferred unmap, reuse what it returns, free the rest
+      forced = true;
+      rc->wait_all(false);
+      auto more = rc->take(need - hs.size());
+      last_cache_reused += more.size();
+      hs.insert(hs.end(), more.begin(), more.end());
+      rc->wait_all(true);
+      continue;
+    }
     if (r != CUDA_SUCCESS) {
-      // roll back the chunks created by this call
-      for (size_t i = first; i < chunks.size(); ++i) {
-        d.Unmap(va + i * chunk_bytes, chunk_bytes);
-        d.Release(chunks[i]);
-      }
-      chunks.resize(first);
+      for (auto x : hs) d.Release(x);
       cu_check(r, "cuMemCreate (device out of memory?)");
     }
-    cu_check(d.Map(va + chunks.size() * chunk_bytes, chunk_bytes, 0, h, 0), "cuMemMap");
-    set_access(va + chunks.size() * chunk_bytes, chunk_bytes, device, peer_devices);
-    chunks.push_back(h);
+    hs.push_back(h);
+    ++last_created;
   }
+  for (size_t i = 0; i < need; ++i) {
+    CUresult r = d.Map(va + (first + i) * chunk_bytes, chunk_bytes, 0, hs[i], 0);
+    if (r != CUDA_SUCCESS)
+      fail(PL_E_CUDA, "cuMemMap failed with CUresult " + std::to_string((int)r) + " at chunk " +
+                          std::to_string(first + i) + " of " + std::to_string(want_chunks) +
+                          " (va_bytes " + std::to_string(va_bytes) + ", chunk " +
+                          std::to_string(chunk_bytes) + ", handle " + std::to_string((unsigned long long)hs[i]) +
+                          ", cached " + std::to_string(last_cache_reused) + ")");
+  }
+  chunks.insert(chunks.end(), hs.begin(), hs.end());
+  set_access(va + first * chunk_bytes, need * chunk_bytes, device, peer_devices);
 }
 
-void Arena::trim(size_t bytes) {
+void Arena::trim(size_t bytes, cudaStream_t st) {
   size_t keep = (bytes + chunk_bytes - 1) / chunk_bytes;
+  reclaim_tail();  // one contiguous retired tail per arena
   if (keep >= chunks.size()) return;
-  Driver& d = drv();
-  for (size_t i = keep; i < chunks.size(); ++i) {
-    cu_check(d.Unmap(va + i * chunk_bytes, chunk_bytes), "cuMemUnmap");
-    cu_check(d.Release(chunks[i]), "cuMemRelease");
-  }
+  std::vector<CUmemGenericAllocationHandle> tail(chunks.begin() + (long)keep, chunks.end());
   chunks.resize(keep);
+  const size_t n_tail = tail.size();
+  tail_job = rc->submit(st, va + keep * chunk_bytes, n_tail * chunk_bytes, std::move(tail),
+                        0, 0, /*immediate=*/false);
+  if (trace_on())
+    std::fprintf(stderr, "[pl] trim: va=%llx keep %zu chunks, retire %zu as job %llu\n",
+                 (unsigned long long)va, keep, n_tail, (unsigned long long)tail_job);
 }
 
-void Arena::release() {
+void Arena::release(cudaStream_t st) {
   if (!va) return;
-  Driver& d = drv();
-  for (size_t i = 0; i < chunks.size(); ++i) {
-    d.Unmap(va + i * chunk_bytes, chunk_bytes);
-    d.Release(chunks[i]);
-  }
+  reclaim_tail();
+  rc->submit(st, va, chunks.size() * chunk_bytes, std::move(chunks), va, va_bytes,
+             /*immediate=*/true);
   chunks.clear();
-  d.AddressFree(va, va_bytes);
   va = 0;
   va_bytes = 0;
 }
@@ -150,8 +387,7 @@ void Arena::grant_peer(int dev) {
   for (int p : peer_devices)
     if (p == dev) return;
   peer_devices.push_back(dev);
-  for (size_t i = 0; i < chunks.size(); ++i)
-    set_access(va + i * chunk_bytes, chunk_bytes, device, peer_devices);
+  set_access(va, chunks.size() * chunk_bytes, device, peer_devices);
 }
 
 }  // namespace pl

@@ -559,6 +559,21 @@ class KvStore:
         return {"relocated_blocks": int(out[0]), "table_entries_remapped": int(out[1]),
                 "bytes_mapped": int(out[2]), "bytes_unmapped": int(out[3])}
 
+    def vmm_stats(self) -> dict[str, int]:
+        """Physical-memory bookkeeping of the pools (vmm.cu): chunks re-taken from a
+        retired but still mapped tail, re-mapped from the reclaimer's cache, freshly
+        created, and bytes not yet returned to the driver."""
+        out = np.zeros(4, dtype=np.int64)
+        _check(N.lib().pl_store_vmm_stats(self._h, N.ptr(out)))
+        return {"tail_reused_chunks": int(out[0]), "cache_reused_chunks": int(out[1]),
+                "created_chunks": int(out[2]), "pending_reclaim_bytes": int(out[3])}
+
+    def reclaim(self) -> float:
+        """Finish every deferred unmap/release now; returns the wait in ms."""
+        out = C.c_double()
+        _check(N.lib().pl_store_reclaim(self._h, C.byref(out)))
+        return out.value
+
     def drop_layer_groups(self, layer_groups: Iterable[int]) -> int:
         groups = sorted(set(layer_groups))
         g = N.as_i32(groups) if groups else np.zeros(1, np.int32)

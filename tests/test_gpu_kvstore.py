@@ -136,3 +136,68 @@ class TestReferenceUnitCases:
         st.append_seeded("r0000", 0, 4, seed)
         got = [st.read_checksum("r0000", 0, p) for p in range(4)]
         assert got == golden("fingerprints.json")["engine_r0000_g0"]
+
+
+class TestDeferredReclaim:
+    """Physical reclaim off the critical path (vmm.cu): a shrink retires its tail
+    chunks, a grow inside the grace period takes them back still mapped, a forced
+    reclaim returns every byte to the driver, and the live KV never changes."""
+
+    def test_shrink_grow_reuse_and_reclaim(self, kv):
+        gran = 2 << 20
+        # 16-token blocks of 4 x 4096 B cells: 256 KiB + header per unit, 8 units per chunk
+        st = kv.KvStore(1, 4, 16, 64, (0, 1), cell_bytes=4096, chunk_bytes=gran)
+        for i in range(40):
+            st.append_seeded(f"x{i}", i % 2, 16, 1000 + i)
+        for i in range(0, 38):
+            st.free_request(f"x{i}")
+        keep = ["x38", "x39"]
+        before = {(r, p): st.read_cell(r, int(r[1:]) % 2, p, 3) for r in keep for p in (0, 7, 15)}
+        v0 = st.vmm_stats()
+        mapped0 = st.info()["mapped_bytes"]
+        st.resize(4)
+        assert st.info()["mapped_bytes"] < mapped0
+        assert st.vmm_stats()["pending_reclaim_bytes"] > 0
+        # grow back at once: the retired tail is still mapped and is taken back as is
+        st.resize(64)
+        v1 = st.vmm_stats()
+        assert v1["tail_reused_chunks"] > v0["tail_reused_chunks"]
+        assert v1["created_chunks"] == v0["created_chunks"]
+        assert st.info()["mapped_bytes"] >= mapped0
+        for (r, p), v in before.items():
+            assert st.read_cell(r, int(r[1:]) % 2, p, 3) == v
+        # shrink, force the reclaim, grow: fresh chunks from the driver
+        st.resize(4)
+        st.reclaim()
+        assert st.vmm_stats()["pending_reclaim_bytes"] == 0
+        st.resize(64)
+        v2 = st.vmm_stats()
+        assert v2["created_chunks"] > v1["created_chunks"]
+        for (r, p), v in before.items():
+            assert st.read_cell(r, int(r[1:]) % 2, p, 3) == v
+        st.append_seeded("y", 0, 16 * 60, 7)
+        assert st.read_checksum("y", 0, 16 * 60 - 1) == oracle.payload(7, 16 * 60 - 1)
+
+    def test_drop_group_releases_in_background(self, kv):
+        st = kv.KvStore(1, 4, 16, 32, (0, 1), cell_bytes=4096, chunk_bytes=2 << 20)
+        for i in range(8):
+            st.append_seeded(f"a{i}", 0, 40, i)
+            st.append_seeded(f"a{i}", 1, 40, 100 + i)
+        keep = {p: st.read_cell("a3", 1, p, 2) for p in (0, 39)}
+        st.drop_layer_groups([0])
+        assert st.vmm_stats()["pending_reclaim_bytes"] > 0
+        st.reclaim()
+        assert st.vmm_stats()["pending_reclaim_bytes"] == 0
+        for p, v in keep.items():
+            assert st.read_cell("a3", 1, p, 2) == v
+        # the dropped group can come back (fresh reservation) and be written again
+        st.resident_groups.add(0)
+        st.append_seeded("b", 0, 20, 5)
+        assert st.read_cell("a3", 1, 39, 2) == keep[39]
+
+    def test_store_teardown_with_pending_reclaim(self, kv):
+        for _ in range(3):
+            st = kv.KvStore(1, 2, 16, 64, (0,), cell_bytes=4096, chunk_bytes=2 << 20)
+            st.append_seeded("a", 0, 100, 1)
+            st.resize(8)
+            del st

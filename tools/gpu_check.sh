@@ -1,6 +1,7 @@
 set -x
 cd $GRAFT_REPO_ROOT
-
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
+tail -3 gpurun_out/smoke.log
 timeout 900 python -m pytest tests -m gpu -q --timeout=300 -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 tail -15 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
