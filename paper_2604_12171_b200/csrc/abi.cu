@@ -539,6 +539,7 @@ int pl_paged_attn_decode(pl_store* st, int group, int layer, const void* q, void
     a.max_ctx = max_ctx;
     a.q = q;
     a.out = out;
+    a.n_slots = std::max<int64_t>(s->capacity(), 1);
     pl::launch_paged_attn(a, cs);
   });
 }
@@ -566,6 +567,7 @@ int pl_paged_attn_decode_raw(const void* pool, int64_t unit_bytes, int64_t fp_by
     a.max_ctx = max_ctx;
     a.q = q;
     a.out = out;
+    a.n_slots = (int64_t)1 << 30;  // external pool: extent unknown, slots come from `tables`
     pl::launch_paged_attn(a, static_cast<cudaStream_t>(stream));
   });
 }

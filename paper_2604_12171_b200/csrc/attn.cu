@@ -20,6 +20,7 @@
 //   - per-(item, warp) partials (m, l, acc) merged by a small combine kernel.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -423,6 +424,293 @@ __global__ void paged_attn_combine(const float* ws_acc, const float* ws_ml, int 
   static_cast<__nv_bfloat16*>(out)[bh * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
 }
 
+
+// ============================================================================
+// Tensor-core variant (the default for head_dim 64/128, GQA group <= 8, blocks of
+// a multiple of 8 tokens).  ncu on the CUDA-core kernel above showed the 70B shape
+// (group 8) bound by FMA + shuffle issue, not by bytes, so the two contractions
+// move to mma.sync.m16n8k16 (bf16 in, fp32 accumulate) with the GQA group on N:
+//   S^T[16 tok x 8 heads]  = K[16 tok x D] . Q^T[D x 8 heads]       (D/16 mma)
+//   O^T[D x 8 heads]      += V^T[D x 16 tok] . P^T[16 tok x 8 heads] (D/16 mma)
+// K and V tiles come from shared memory with ldmatrix (.trans for V); P^T is the
+// fp32 S^T fragment rounded to bf16 and transposed in registers (movmatrix).
+// Staging is a TMA tensor map over the pool with 128-byte swizzle: box =
+// {64 elems, 8 tokens, cell/128 chunks, 1 slot}, so shared memory holds
+// [chunk][token][128 B] with 16-byte units XOR-swizzled by token -> the eight
+// token rows an ldmatrix phase reads sit in eight different bank groups.
+// One warp per KV head (W warps per head split the stages when n_kv < 8).
+namespace {
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+constexpr int kMmaStage = 16;  // tokens per stage = one M tile = two 8-token TMA boxes
+}  // namespace
+
+struct MmaPlan {
+  int n_stage;      // ring depth
+  int parts;        // context parts per sequence
+  int part_tokens;  // multiple of 16
+  int W;            // warps per kv head
+  int items;        // B * parts
+  int nchunks;      // cell / 128
+  int box_bytes;    // 8 tokens x cell
+};
+
+template <int D, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, MmaPlan p,
+                      float* ws_acc, float* ws_ml) {
+  constexpr int KT = D / 16;  // k-steps of the QK mma = m-tiles of the PV mma
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 128-byte swizzle needs 1024-byte aligned boxes
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int stage_bytes = 2 * p.box_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.n_stage * stage_bytes);
+  int* done_cnt = reinterpret_cast<int*>(full + 8);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < p.n_stage; ++i) {
+      mbar_init(&full[i], 1);
+      done_cnt[i] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int G = a.n_q / a.n_kv;
+  auto geom = [&](int item, int& b, int& part, int& t0, int& nst) {
+    b = item / p.parts;
+    part = item % p.parts;
+    t0 = part * p.part_tokens;
+    const int tend = min(a.ctx[b], t0 + p.part_tokens);
+    nst = tend > t0 ? (tend - t0 + kMmaStage - 1) / kMmaStage : 0;
+  };
+  int l_item = blockIdx.x, l_st = 0;
+  auto l_norm = [&]() {
+    for (;;) {
+      if (l_item >= p.items) return;
+      int b, part, t0, nst;
+      geom(l_item, b, part, t0, nst);
+      if (l_st < nst) return;
+      l_item += gridDim.x;
+      l_st = 0;
+    }
+  };
+  auto issue = [&](int buf) {  // one thread: both 8-token halves of the cursor's stage
+    int b, part, t0, nst;
+    geom(l_item, b, part, t0, nst);
+    const int tok0 = t0 + l_st * kMmaStage;
+    const int ntok = min(kMmaStage, a.ctx[b] - tok0);
+    const int row = a.rows ? a.rows[b] : b;
+    const int halves = ntok > 8 ? 2 : 1;
+    mbar_expect_tx(&full[buf], (uint32_t)(halves * p.box_bytes));
+    for (int h = 0; h < halves; ++h) {
+      const int t = tok0 + 8 * h;
+      const int32_t slot = a.table[(int64_t)row * a.table_stride + t / a.s];
+      tma_load_4d(smem + buf * stage_bytes + h * p.box_bytes, &kv_map, 0, t % a.s, 0, slot, &full[buf]);
+    }
+  };
+  l_norm();
+  for (int i = 0; i < p.n_stage && l_item < p.items; ++i) {
+    if (tid == 0) issue(i);
+    ++l_st;
+    l_norm();
+  }
+
+  const int h = warp / p.W, sub = warp % p.W;
+  const bool active = h < a.n_kv;
+  const float qscale = a.scale * kLog2e;
+  const int parts_total = p.parts * p.W;
+  const int g4 = lane >> 2, q4 = lane & 3;
+  // ldmatrix lane geometry: matrix mi = lane/8, row r = lane%8
+  const int mi = lane >> 3, r8 = lane & 7;
+  // K (non-trans): tok = r8 + (mi&1)*8, 16B unit = 2*kk + (mi>>1)
+  const int k_tok = r8 + (mi & 1) * 8, k_u = mi >> 1;
+  // V (trans): tok = r8 + (mi>>1)*8, unit = 2*mt + (mi&1)
+  const int v_tok = r8 + (mi >> 1) * 8, v_u = mi & 1;
+  const int kc0 = h * D / 64;                  // first 128-B chunk of this head's K
+  const int vc0 = (a.n_kv * D * 2) / 128 + kc0;  // ... and of its V
+  const uint32_t smem0 = smem_u32(smem);
+  auto tile_addr = [&](int buf, int tok, int chunk, int unit16) -> uint32_t {
+    const int r = tok & 7;
+    return smem0 + buf * stage_bytes + (tok >> 3) * p.box_bytes + chunk * 1024 + r * 128 +
+           ((unit16 ^ r) << 4);
+  };
+
+  int buf = 0;
+  uint32_t phase = 0;
+  for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+    int b, part, t0, nst;
+    geom(item, b, part, t0, nst);
+    // Q^T B-fragments: n = head g4 of the group (zero beyond G), k = dims
+    uint32_t qb[KT][2];
+    const bool hq = active && g4 < G;
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(
+        static_cast<const __nv_bfloat16*>(a.q) + ((int64_t)b * a.n_q + h * G + (hq ? g4 : 0)) * D);
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      qb[kk][0] = hq ? qrow[kk * 8 + q4] : 0u;
+      qb[kk][1] = hq ? qrow[kk * 8 + 4 + q4] : 0u;
+    }
+    float acc[KT][4];
+#pragma unroll
+    for (int mt = 0; mt < KT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // heads 2*q4, 2*q4+1
+
+    for (int st = 0; st < nst; ++st) {
+      const int ntok = min(kMmaStage, a.ctx[b] - (t0 + st * kMmaStage));
+      mbar_wait(&full[buf], phase);
+      if (active && st % p.W == sub) {
+        if (ntok < kMmaStage) {
+          // rows past the context hold stale bytes (maybe NaN): zero this head's V rows
+          uint8_t* base = smem + buf * stage_bytes;
+          const int rows = kMmaStage - ntok, per_row = D / 64 * 8;  // 16-B units per V row
+          for (int i = lane; i < rows * per_row; i += 32) {
+            const int tok = ntok + i / per_row, u = i % per_row;
+            const int chunk = vc0 + (u >> 3);
+            *reinterpret_cast<uint4*>(base + (tok >> 3) * p.box_bytes + chunk * 1024 + (tok & 7) * 128 +
+                                      (u & 7) * 16) = make_uint4(0, 0, 0, 0);
+          }
+          __syncwarp();
+        }
+        // S^T = K . Q^T (two accumulators halve the mma dependency chain)
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) {
+          const int u = 2 * kk + k_u;
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4(tile_addr(buf, k_tok, kc0 + (u >> 3), u & 7), a0, a1, a2, a3);
+          if (kk & 1) mma_bf16(s1, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+          else mma_bf16(s0, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+        }
+        // c0,c1: token g4, heads 2q4, 2q4+1; c2,c3: token g4+8
+        float x00 = (s0[0] + s1[0]) * qscale, x01 = (s0[1] + s1[1]) * qscale;
+        float x10 = (s0[2] + s1[2]) * qscale, x11 = (s0[3] + s1[3]) * qscale;
+        if (g4 >= ntok) x00 = x01 = -INFINITY;
+        if (g4 + 8 >= ntok) x10 = x11 = -INFINITY;
+        float c0 = fmaxf(x00, x10), c1 = fmaxf(x01, x11);
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, o));
+          c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, o));
+        }
+        const float n0 = fmaxf(m0, c0), n1 = fmaxf(m1, c1);
+        const float corr0 = n0 == -INFINITY ? 1.f : fast_exp2(m0 - n0);
+        const float corr1 = n1 == -INFINITY ? 1.f : fast_exp2(m1 - n1);
+        m0 = n0;
+        m1 = n1;
+        const float p00 = x00 == -INFINITY ? 0.f : fast_exp2(x00 - n0);
+        const float p01 = x01 == -INFINITY ? 0.f : fast_exp2(x01 - n1);
+        const float p10 = x10 == -INFINITY ? 0.f : fast_exp2(x10 - n0);
+        const float p11 = x11 == -INFINITY ? 0.f : fast_exp2(x11 - n1);
+        l0 = l0 * corr0 + p00 + p10;
+        l1 = l1 * corr1 + p01 + p11;
+        // P^T as the PV B-fragment: transpose the two 8x8 bf16 halves in registers
+        const uint32_t pb0 = movm_t(pack_bf2(p00, p01));
+        const uint32_t pb1 = movm_t(pack_bf2(p10, p11));
+#pragma unroll
+        for (int mt = 0; mt < KT; ++mt) {
+          acc[mt][0] *= corr0;
+          acc[mt][1] *= corr1;
+          acc[mt][2] *= corr0;
+          acc[mt][3] *= corr1;
+          const int u = 2 * mt + v_u;
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4_t(tile_addr(buf, v_tok, vc0 + (u >> 3), u & 7), a0, a1, a2, a3);
+          mma_bf16(acc[mt], a0, a1, a2, a3, pb0, pb1);
+        }
+      }
+      __syncwarp();
+      if (l_item < p.items) {
+        if (lane == 0) {
+          __threadfence_block();
+          if (atomicAdd(&done_cnt[buf], 1) == NW - 1) {  // last reader of this buffer
+            done_cnt[buf] = 0;
+            __threadfence_block();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(buf);
+          }
+        }
+        ++l_st;
+        l_norm();
+      }
+      if (++buf == p.n_stage) {
+        buf = 0;
+        phase ^= 1;
+      }
+    }
+    if (active) {
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+      }
+      const int hA = 2 * q4, hB = hA + 1;
+      const int64_t base = (int64_t)b * a.n_q + h * G;
+      const int pslot = part * p.W + sub;
+      if (hA < G) {
+        const int64_t pi = (base + hA) * parts_total + pslot;
+#pragma unroll
+        for (int mt = 0; mt < KT; ++mt) {
+          ws_acc[pi * D + mt * 16 + g4] = acc[mt][0];
+          ws_acc[pi * D + mt * 16 + g4 + 8] = acc[mt][2];
+        }
+        if (g4 == 0) {
+          ws_ml[2 * pi] = m0;
+          ws_ml[2 * pi + 1] = l0;
+        }
+      }
+      if (hB < G) {
+        const int64_t pi = (base + hB) * parts_total + pslot;
+#pragma unroll
+        for (int mt = 0; mt < KT; ++mt) {
+          ws_acc[pi * D + mt * 16 + g4] = acc[mt][1];
+          ws_acc[pi * D + mt * 16 + g4 + 8] = acc[mt][3];
+        }
+        if (g4 == 0) {
+          ws_ml[2 * pi] = m1;
+          ws_ml[2 * pi + 1] = l1;
+        }
+      }
+    }
+  }
+}
+
 namespace {
 std::mutex g_ws_mu;
 float* g_ws[64] = {nullptr};
@@ -506,6 +794,82 @@ void launch_np(const AttnLaunch& a, const AttnPlan& p, size_t smem, int sms, cud
   note_launch();
   PL_CUDA(cudaGetLastError());
 }
+
+// --- tensor-core path launch ---------------------------------------------------------
+using EncodeTiled = decltype(&cuTensorMapEncodeTiled);
+EncodeTiled encode_tiled() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  });
+  if (!fn) fail(PL_E_CUDA, "driver entry point missing: cuTensorMapEncodeTiled");
+  return fn;
+}
+
+bool mma_path_ok(const AttnLaunch& a) {
+  const int G = a.n_q / a.n_kv;
+  const int64_t cell = 2ll * a.n_kv * a.D * 2;
+  return (a.D == 64 || a.D == 128) && G >= 1 && G <= 8 && a.s % 8 == 0 && a.n_kv <= 8 &&
+         8 % a.n_kv == 0 && cell % 128 == 0 && cell / 128 <= 256 && a.unit_bytes % 16 == 0 &&
+         ((uintptr_t)a.pool + a.fp_bytes) % 16 == 0 && 16 * cell * 2 + 2048 <= 227 * 1024;
+}
+
+template <int D>
+void launch_mma(const AttnLaunch& a, cudaStream_t st) {
+  constexpr int NW = 8;
+  int dev = 0, sms = 148;
+  PL_CUDA(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t cell = 2ll * a.n_kv * D * 2;
+  MmaPlan p{};
+  p.nchunks = (int)(cell / 128);
+  p.box_bytes = (int)(8 * cell);
+  const int64_t stage_bytes = 2 * p.box_bytes;
+  p.n_stage = (int)std::max<int64_t>(2, std::min<int64_t>(4, (220 * 1024 - 2048) / stage_bytes));
+  const size_t smem = (size_t)(p.n_stage * stage_bytes) + 1024 /*align*/ + 128;
+  p.W = NW / a.n_kv;
+  const int max_ctx = std::max(a.max_ctx, 1);
+  // ~8 items per SM; parts are whole 16-token stages
+  int parts = std::max(1, (8 * sms + a.B - 1) / a.B);
+  parts = std::min(parts, (max_ctx + kMmaStage - 1) / kMmaStage);
+  p.part_tokens = ((max_ctx + parts - 1) / parts + kMmaStage - 1) / kMmaStage * kMmaStage;
+  p.parts = (max_ctx + p.part_tokens - 1) / p.part_tokens;
+  p.items = a.B * p.parts;
+
+  // tensor map: {64 elems, token in block (s), 128-B chunk of the cell, slot}
+  CUtensorMap map;
+  const uint8_t* base = a.pool + a.fp_bytes + (int64_t)a.layer * a.s * cell;
+  cuuint64_t dims[4] = {64, (cuuint64_t)a.s, (cuuint64_t)p.nchunks, (cuuint64_t)a.n_slots};
+  cuuint64_t strides[3] = {(cuuint64_t)cell, 128, (cuuint64_t)a.unit_bytes};
+  cuuint32_t box[4] = {64, 8, (cuuint32_t)p.nchunks, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint8_t*>(base),
+                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(PL_E_CUDA, "cuTensorMapEncodeTiled (KV pool map) failed with CUresult " + std::to_string((int)r));
+
+  auto kern = paged_attn_mma_kernel<D, NW>;
+  PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = std::max(1, std::min(p.items, sms));
+  const int64_t n_parts_total = (int64_t)p.parts * p.W;
+  const size_t np = (size_t)a.B * a.n_q * n_parts_total;
+  float* ws = workspace(np * (D + 2) * sizeof(float));
+  KernelTimer timer("paged_attn", st);
+  kern<<<grid, NW * 32, smem, st>>>(map, a, p, ws, ws + np * D);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+  paged_attn_combine<D><<<(unsigned)(a.B * a.n_q), D, 0, st>>>(ws, ws + np * D, (int)n_parts_total,
+                                                               a.out);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
 }  // namespace
 
 void launch_paged_attn(const AttnLaunch& a, cudaStream_t st) {
@@ -513,6 +877,11 @@ void launch_paged_attn(const AttnLaunch& a, cudaStream_t st) {
   if (a.n_kv <= 0 || a.n_q % a.n_kv) fail(PL_E_INVALID, "n_q_heads must be a multiple of n_kv_heads");
   if (a.n_kv > 8 || 8 % a.n_kv)
     fail(PL_E_INVALID, "n_kv_heads must divide 8 (1, 2, 4 or 8 KV heads per stage)");
+  static const bool force_simt = std::getenv("PL_ATTN_SIMT") != nullptr;
+  if (!force_simt && mma_path_ok(a)) {
+    if (a.D == 128) return launch_mma<128>(a, st);
+    return launch_mma<64>(a, st);
+  }
   const int G = a.n_q / a.n_kv;
 #define PL_ATTN_CASE(DD, GG) \
   if (a.D == DD && G == GG) return launch_dg<DD, GG>(a, st);

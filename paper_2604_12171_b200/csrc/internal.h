@@ -402,6 +402,7 @@ struct AttnLaunch {
   const int32_t* table; int64_t table_stride; const int32_t* rows;  // rows may be null
   const int32_t* ctx; int B, n_q, n_kv, D; float scale; int max_ctx;
   const void* q; void* out;
+  int64_t n_slots;  // pool slots addressable through `pool` (TMA tensor-map extent)
 };
 void launch_paged_attn(const AttnLaunch& a, cudaStream_t st);
 

@@ -8,6 +8,7 @@ from paper_2604_12171_b200.perf import Workload, append_batch
 from paper_2604_12171_b200.kvstore import KvStore, RequestRegistry
 from paper_2604_12171_b200.events import stable_hash
 
+import os
 for n_q, n_kv in [(32, 8), (64, 8)]:
     wl = Workload(n_q=n_q, n_kv=n_kv)
     reg = RequestRegistry()
@@ -34,5 +35,5 @@ for n_q, n_kv in [(32, 8), (64, 8)]:
     N.check(N.lib().pl_timing_enable(0))
     per = ms / n
     gb = B * ctx * wl.cell_bytes / 1e9
-    print(f"n_q={n_q} n_kv={n_kv}: {per*1e3:.1f} us/layer  {gb/(per/1e3):.0f} GB/s  ({n} launches)")
+    print(f"{'simt' if os.environ.get('PL_ATTN_SIMT') else 'mma'} n_q={n_q} n_kv={n_kv}: {per*1e3:.1f} us/layer  {gb/(per/1e3):.0f} GB/s  ({n} launches)")
     del st
