@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-sweep", action="store_true")
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--ctx", type=int, default=2048)
     return ap.parse_args()
@@ -73,46 +74,55 @@ def allmax(x: float, world: int) -> float:
 
 # ------------------------------------------------------------------------------ clocks
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled through NVML every 5 ms while the timed
+    region runs (a thread; nvidia-smi's startup is longer than a short timed region)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.path = Path(f"/tmp/pipelive_clocks_{os.getpid()}.csv")
+        self.samples: list[tuple[float, int]] = []
+        self.max_mhz = None
+        self._stop = None
+        self._th = None
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            return self
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                         pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                except Exception:
+                    pass
+                self._stop.wait(0.005)
+
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
         return self
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+        if self._th is not None:
+            self._stop.set()
+            self._th.join()
 
     def summary(self) -> dict:
-        try:
-            rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r]
-        except Exception:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[1]) for r in rows if len(r) >= 9]
-        mx = [float(r[2]) for r in rows if len(r) >= 9]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in rows:
-            for i, n in enumerate(names):
-                if len(r) >= 9 and r[5 + i].strip().lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"],
+                    "samples": 0}
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
 
 
 # ------------------------------------------------------------------------------ CPU legs
@@ -174,6 +184,19 @@ def run_reference(args, wl, rank: int, world: int) -> None:
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def profile_traffic(kernel: str, n_q: int | None = None):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` at this bench's
+    shape, from the committed ncu capture (profiles/traffic_r1.json, tools/gpu_prof.sh)."""
+    try:
+        rows = json.loads((ROOT / "profiles" / "traffic_r1.json").read_text())
+    except Exception:
+        return None
+    for r in rows:
+        if r.get("kernel") == kernel and r.get("n_q") == n_q:
+            return r.get("dram_bytes")
+    return None
 
 
 def config_of(wl, world: int) -> dict:
@@ -250,7 +273,7 @@ def main() -> None:
     roofline = {"kernel": "copy_kernel<2> (K4 gather -> K5 scatter, fused push)",
                 "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                "traffic": profile_traffic("copy_kernel<2>"), "alg_bytes_per_launch": alg_bytes,
                 "avg_launch_ms": round(push_avg, 4),
                 "share_of_step": round(push_ms / ms, 4) if ms else None,
                 "drain_ms_per_step": round(drain_ms / max(K, 1), 4)}
@@ -258,11 +281,19 @@ def main() -> None:
     # ---- switch pause (data-path part): residual patch after one decode round + barrier
     pause = measure_switch_pause(rig, stream, torch, wl)
 
-    # ---- paged-attention decode over the source stage (16 layers)
+    # ---- paged-attention decode over the source stage (16 layers): the 8B shape (GQA 4)
+    # and the 70B shape (64 q heads over the same 8 KV heads x 128, GQA 8)
     decode = measure_decode(rig, stream, torch, wl, hbm_peak, K, W)
+    decode_70b = measure_decode(rig, stream, torch, wl, hbm_peak, K, W, n_q=64)
 
     # ---- resize latency: post-commit cleanup on the source (drop groups, shrink, regrow)
     resize = measure_resize(rig, stream, torch, wl)
+
+    # ---- C5: dirty-rate x block-size sweep of one patch round (configs[4], 1 GPU)
+    sweep = None
+    if not args.skip_sweep:
+        from paper_2604_12171_b200.perf import c5_sweep
+        sweep = c5_sweep(dev)
 
     # ---- e2e: KV arrives from pinned host memory every step, result read back
     e2e = None if args.skip_e2e else measure_e2e(rig, stream, torch, wl, K, world)
@@ -283,7 +314,9 @@ def main() -> None:
         "clocks": clocks.summary(),
         "switch_pause_ms": pause,
         "decode": decode,
+        "decode_70b_shape": decode_70b,
         "resize": resize,
+        "c5_sweep": sweep,
     }
     print(json.dumps(line), flush=True)
 
@@ -321,17 +354,18 @@ def measure_switch_pause(rig, stream, torch, wl) -> dict:
                     "barrier); excludes pipeline drain of model compute"}
 
 
-def measure_decode(rig, stream, torch, wl, hbm_peak, K, W) -> dict:
+def measure_decode(rig, stream, torch, wl, hbm_peak, K, W, n_q=None) -> dict:
     import ctypes as C
 
     from paper_2604_12171_b200 import _native as N
 
     lib = N.lib()
     B = wl.batch
+    n_q = n_q or wl.n_q
     rows = torch.tensor(rig.handles, dtype=torch.int32, device="cuda")
     ctx_now = wl.ctx
     ctx = torch.full((B,), ctx_now, dtype=torch.int32, device="cuda")
-    q = torch.randn(B, wl.n_q, wl.head_dim, dtype=torch.bfloat16, device="cuda")
+    q = torch.randn(B, n_q, wl.head_dim, dtype=torch.bfloat16, device="cuda")
     out = torch.empty_like(q)
     layers = [(g, j) for g in wl.src_groups for j in range(wl.k)]
 
@@ -340,7 +374,7 @@ def measure_decode(rig, stream, torch, wl, hbm_peak, K, W) -> dict:
             N.check(lib.pl_paged_attn_decode(rig.src._h, g, j, C.c_void_p(q.data_ptr()),
                                              C.c_void_p(out.data_ptr()),
                                              C.c_void_p(rows.data_ptr()),
-                                             C.c_void_p(ctx.data_ptr()), B, wl.n_q, wl.n_kv,
+                                             C.c_void_p(ctx.data_ptr()), B, n_q, wl.n_kv,
                                              wl.head_dim, wl.head_dim ** -0.5, ctx_now,
                                              C.c_void_p(stream.cuda_stream)))
 
@@ -361,11 +395,14 @@ def measure_decode(rig, stream, torch, wl, hbm_peak, K, W) -> dict:
     attn_ms, attn_n = N.timing("paged_attn")
     per_launch = attn_ms / max(attn_n, 1)
     kv_bytes_layer = B * ctx_now * wl.cell_bytes
-    q_bytes = 2 * B * wl.n_q * wl.head_dim * 2
+    q_bytes = 2 * B * n_q * wl.head_dim * 2
     achieved = (kv_bytes_layer + q_bytes) / (per_launch / 1e3) / 1e9
     return {"tokens_per_s": round(B / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
-            "layers_per_step": len(layers), "batch": B, "ctx": ctx_now,
-            "roofline": {"kernel": "paged_attn_kernel<128,4,8> (TMA bulk ring, +combine)", "bound": "hbm",
+            "layers_per_step": len(layers), "batch": B, "ctx": ctx_now, "n_q": n_q,
+            "n_kv": wl.n_kv, "head_dim": wl.head_dim,
+            "roofline": {"kernel": "paged_attn_mma_kernel<128,8> (TMA 128B-swizzled ring, "
+                                   "mma.sync bf16, +combine)", "bound": "hbm",
+                         "traffic": profile_traffic("paged_attn_mma", n_q),
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4),
                          "alg_bytes_per_launch": kv_bytes_layer + q_bytes,

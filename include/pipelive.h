@@ -168,6 +168,9 @@ int pl_patch_destroy(pl_patch* p);
 int pl_patch_set_active(pl_patch* p, int active);
 /* DirtyBitmap.mark of n tokens starting at pos (migrator.py:35-36, 194) */
 int pl_patch_mark(pl_patch* p, int32_t req, int group, int64_t start, int64_t n);
+/* the same for n (req, group, start, count) runs with one device launch */
+int pl_patch_mark_batch(pl_patch* p, int n, const int32_t* reqs, const int32_t* groups,
+                        const int64_t* starts, const int64_t* counts);
 /* MigrationStream.start seeding (migrator.py:170-183): *out_tokens = seeded tokens */
 int pl_patch_seed(pl_patch* p, int64_t* out_tokens);
 /* DirtyBitmap.discard_request (migrator.py:43-48): *out_cells = dirty keys dropped */

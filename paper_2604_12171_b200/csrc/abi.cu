@@ -450,6 +450,21 @@ int pl_patch_set_active(pl_patch* p, int active) {
 int pl_patch_mark(pl_patch* p, int32_t req, int group, int64_t start, int64_t n) {
   return guard([&] { live(p)->mark(req, group, start, n, true); });
 }
+int pl_patch_mark_batch(pl_patch* p, int n, const int32_t* reqs, const int32_t* groups,
+                        const int64_t* starts, const int64_t* counts) {
+  return guard([&] {
+    pl::Patch* q = live(p);
+    std::vector<pl::Store::WriteItem> items;
+    items.reserve(n);
+    for (int i = 0; i < n; ++i) {
+      const int g = groups[i];
+      if (counts[i] <= 0 || g < 0 || g >= (int)q->local_of.size() || q->local_of[g] < 0) continue;
+      q->mark(reqs[i], g, starts[i], counts[i], /*device=*/false);
+      items.push_back({reqs[i], q->local_of[g], starts[i], counts[i], 0, starts[i]});
+    }
+    q->mark_device(items);  // one K-mark launch for the whole batch
+  });
+}
 int pl_patch_seed(pl_patch* p, int64_t* out) {
   return guard([&] { *out = live(p)->seed(); });
 }

@@ -98,6 +98,12 @@ class NativePatch:
                                       C.byref(cells)))
         return keys.value, cells.value
 
+    def mark_batch(self, reqs, groups, starts, counts) -> None:
+        r, g = N.as_i32(reqs), N.as_i32(groups)
+        st, c = N.as_i64(starts), N.as_i64(counts)
+        N.check(N.lib().pl_patch_mark_batch(self.h, len(r), N.ptr(r), N.ptr(g), N.ptr(st),
+                                            N.ptr(c)))
+
     def device_drained(self) -> int:
         out = C.c_int64()
         N.check(N.lib().pl_patch_device_drained(self.h, C.byref(out)))
@@ -152,6 +158,73 @@ class PatchRig:
 
     def close(self) -> None:
         self.patch.close()
+
+
+def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16, 32, 64, 128),
+             batch: int = 64, ctx: int = 2048, rounds: int = 3, seed: int = 0) -> list[dict]:
+    """BASELINE configs[4] at one GPU: dirty-rate x block-size sweep of the patch round.
+
+    Per block size: a source stage with ``batch`` requests x ``ctx`` tokens in two
+    migrating k=4 groups (Llama-3 cells, 4096 B), a destination holding those groups, and
+    one patch engine.  Per dirty rate: uniform-random (request, group, position) keys,
+    seeded, are marked (outside the timed region), then one round = drain (K3) + fused
+    gather/scatter push (K4+K5) is timed wall-clock with the device synchronised on
+    both sides.  Plus the structured decode pattern: one key per live request and group
+    (the newest token).  Source and destination share the GPU, so the bound is HBM
+    (payload read + write), not NVLink."""
+    import torch
+
+    rng = np.random.default_rng(seed)
+    out = []
+    k, cell = 4, 4096
+    for s in block_sizes:
+        reg = RequestRegistry()
+        blocks = batch * (ceil(ctx / s) + 1) + 16
+        src = KvStore(1, k, s, blocks, (0, 1), num_groups=2, cell_bytes=cell, device=device,
+                      registry=reg)
+        dst = KvStore(2, k, s, blocks, (0, 1), num_groups=2, cell_bytes=cell, device=device,
+                      registry=reg)
+        hs = [reg.handle(rid(i)) for i in range(batch)]
+        reqs = [h for h in hs for _ in (0, 1)]
+        groups = [g for _ in hs for g in (0, 1)]
+        append_batch(src, reqs, groups, [ctx] * len(reqs),
+                     [stable_hash(rid(i), g) for i in range(batch) for g in (0, 1)])
+        patch = NativePatch(src, (0, 1), k)
+        patch.seed()
+        patch.push(dst, reg.rank())   # bulk copy: destination chains exist from here on
+        src.sync()
+        dst.sync()
+        rank = reg.rank()
+        cases = [("decode", None)] + [(f"{r:g}", r) for r in rates]
+        for name, r in cases:
+            times, keys_n = [], 0
+            for _ in range(rounds + 1):
+                if r is None:
+                    rq, gq, st = reqs, groups, [ctx - 1] * len(reqs)
+                else:
+                    n_keys = max(1, int(round(r * batch * 2 * ctx)))
+                    flat = rng.choice(batch * 2 * ctx, size=n_keys, replace=False)
+                    rq = [hs[x // (2 * ctx)] for x in flat]
+                    gq = [int((x // ctx) % 2) for x in flat]
+                    st = [int(x % ctx) for x in flat]
+                patch.mark_batch(rq, gq, st, [1] * len(rq))
+                src.sync()
+                torch.cuda.synchronize(device)
+                t0 = time.perf_counter()
+                keys, cells = patch.push(dst, rank)
+                dst.sync()
+                src.sync()
+                times.append(time.perf_counter() - t0)
+                keys_n = keys
+            t = float(np.median(times[1:]))
+            payload = keys_n * k * cell
+            out.append({"tokens_per_block": s, "dirty": name, "keys": keys_n,
+                        "payload_bytes": payload, "ms": round(t * 1e3, 4),
+                        "gbs": round(payload / t / 1e9, 2),
+                        "hbm_gbs": round(2 * (payload + 8 * keys_n) / t / 1e9, 2)})
+        patch.close()
+        del src, dst
+    return out
 
 
 def read_peaks(path) -> dict:

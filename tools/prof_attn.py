@@ -8,7 +8,8 @@ from paper_2604_12171_b200.perf import Workload, append_batch
 from paper_2604_12171_b200.kvstore import KvStore, RequestRegistry
 from paper_2604_12171_b200.events import stable_hash
 
-wl = Workload()
+import os
+wl = Workload(n_q=int(os.environ.get("PL_NQ", "32")))
 reg = RequestRegistry()
 B, ctx = wl.batch, wl.ctx
 st = KvStore(1, wl.k, wl.s, B * (wl.blocks_per_req + 1), (0,), num_groups=8, cell_bytes=wl.cell_bytes, registry=reg)
