@@ -136,7 +136,9 @@ int pl_store_destroy(pl_store* st) {
 int pl_store_set_stream(pl_store* st, void* stream) {
   return guard([&] {
     PL_CUDA(cudaStreamSynchronize(st->s->stream));
-    st->s->stream = static_cast<cudaStream_t>(stream);
+    // NULL: back to the store's own stream (the legacy default stream is not NULL here:
+    // callers pass torch's stream handle, which is 0 for the default stream)
+    st->s->stream = stream ? static_cast<cudaStream_t>(stream) : st->s->own_stream;
   });
 }
 int pl_store_get_info(pl_store* st, pl_store_info* o) {

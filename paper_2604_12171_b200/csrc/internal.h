@@ -131,7 +131,8 @@ struct Interval { int64_t a, b; };  // [a, b)
 struct Store {
   int device = 0, gpu_id = 0, k = 1, s = 1, n_model_groups = 0;
   int64_t cell_bytes = 0, fp_bytes = 0, unit_bytes = 0, chunk_bytes = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // stream every store kernel is enqueued on
+  cudaStream_t own_stream = nullptr;  // created by the store; `stream` may be a caller's
 
   // block manager state (reference semantics)
   std::vector<int64_t> blocks;                    // list order

@@ -32,7 +32,8 @@ Store::Store(int device_, int gpu_id_, int k_, int s_, int64_t cell_bytes_, int 
   if (capacity < 0) fail(PL_E_INVALID, "capacity must be non-negative");
   PL_CUDA(cudaSetDevice(device));
   PL_CUDA(cudaFree(0));
-  PL_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  PL_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+  stream = own_stream;
   PL_CUDA(cudaEventCreateWithFlags(&pinned_ev, cudaEventDisableTiming));
   fp_bytes = round_up((int64_t)s * 8, 128);
   unit_bytes = round_up(fp_bytes + (int64_t)k * s * cell_bytes, 128);
@@ -87,7 +88,8 @@ Store::~Store() {
   cudaFree(d_bases_);
   if (h_pinned) cudaFreeHost(h_pinned);
   cudaEventDestroy(pinned_ev);
-  cudaStreamDestroy(stream);
+  cudaStreamSynchronize(own_stream);
+  cudaStreamDestroy(own_stream);  // a caller's stream (pl_store_set_stream) is not ours
 }
 
 // ---------------------------------------------------------------------------

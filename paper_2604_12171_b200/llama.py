@@ -1,0 +1,293 @@
+"""Real stage compute over the live-reconfigurable KV path.
+
+The reference's engine step is a cost model (engine.py:335-351); this module runs
+an actual Llama decoder whose KV lives in the paged stores of the pipeline
+stages, so decode load during a live reconfiguration is real and the generated
+token ids can be checked:
+
+  - every layer's K/V of the new token is written by K1 into the store of the
+    stage that owns the layer, fused with the dirty mark of any migration
+    patch streaming that layer (engine.py:377-404, migrator.py:190-197);
+  - attention is K2 over that store's block table;
+  - dense layers (projections, MLP, LM head) are plain fp32 GEMMs (cuBLAS via
+    torch, plumbing), embeddings/argmax are torch ops;
+  - a live PP reconfiguration moves layers between stages while decode keeps
+    running: bulk copy, one patch round per decode step, residual patch at the
+    switch, then the layer's owner flips and the source drops the group
+    (coordinator.py:232-354).  Bit-exact KV movement means the token stream is
+    identical to a run without the reconfiguration.
+
+Stages are stores (one per pipeline GPU id); on one physical GPU they share the
+device and run in stage order on one stream.  The layer -> group map uses
+stacking factor k = 1 (group = layer - 1), as in BASELINE configs[0].
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .events import stable_hash
+from .kvstore import KvStore, RequestRegistry
+from .perf import NativePatch, append_batch
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    """Tiny Llama-style model of BASELINE configs[0] / SURVEY §8d C1."""
+    n_layers: int = 4
+    d_model: int = 256
+    n_q: int = 4
+    n_kv: int = 2
+    head_dim: int = 64
+    ffn: int = 512
+    vocab: int = 1024
+    rope_theta: float = 10000.0
+    eps: float = 1e-5
+
+    @property
+    def cell_bytes(self) -> int:
+        return 2 * self.n_kv * self.head_dim * 2
+
+
+def init_weights(cfg: LlamaConfig, seed: int = 0) -> dict[str, np.ndarray]:
+    """Random-init fp32 weights (numpy, seeded), scaled so activations stay O(1)."""
+    rng = np.random.default_rng(seed)
+
+    def mat(i, o, gain=1.0):
+        return (rng.standard_normal((i, o)) * gain / np.sqrt(i)).astype(np.float32)
+
+    d, hq, hkv = cfg.d_model, cfg.n_q * cfg.head_dim, cfg.n_kv * cfg.head_dim
+    w = {"embed": rng.standard_normal((cfg.vocab, d)).astype(np.float32)}
+    for li in range(cfg.n_layers):
+        w[f"l{li}.attn_norm"] = (1 + 0.1 * rng.standard_normal(d)).astype(np.float32)
+        w[f"l{li}.wq"] = mat(d, hq, 2.0)
+        w[f"l{li}.wk"] = mat(d, hkv, 2.0)
+        w[f"l{li}.wv"] = mat(d, hkv)
+        w[f"l{li}.wo"] = mat(hq, d)
+        w[f"l{li}.mlp_norm"] = (1 + 0.1 * rng.standard_normal(d)).astype(np.float32)
+        w[f"l{li}.w1"] = mat(d, cfg.ffn)
+        w[f"l{li}.w3"] = mat(d, cfg.ffn)
+        w[f"l{li}.w2"] = mat(cfg.ffn, d)
+    w["final_norm"] = (1 + 0.1 * rng.standard_normal(d)).astype(np.float32)
+    w["lm_head"] = mat(d, cfg.vocab, 4.0)
+    return w
+
+
+class StagedLlama:
+    """A Llama decoder split into pipeline stages, each stage's KV in its own store."""
+
+    def __init__(self, cfg: LlamaConfig, weights: dict[str, np.ndarray],
+                 config: dict[int, list[int]], device: int = 0, tokens_per_block: int = 16,
+                 capacity_blocks: int = 256, registry: RequestRegistry | None = None) -> None:
+        import torch
+
+        self.torch = torch
+        self.cfg = cfg
+        self.device = device
+        self.s = tokens_per_block
+        self.capacity = capacity_blocks
+        self.registry = registry or RequestRegistry()
+        # one non-default stream for the whole stage loop: torch ops, K1, K2 and the patch
+        # rounds are ordered by it (callers run model code under `with model.on_stream()`)
+        self.stream = torch.cuda.Stream(device=device)
+        dev = torch.device("cuda", device)
+        self.w = {k: torch.from_numpy(v).to(dev) for k, v in weights.items()}
+        self.stores: dict[int, KvStore] = {}
+        self.owner: dict[int, int] = {}          # layer (1-based) -> gpu id
+        for gpu, layers in config.items():
+            self._store(gpu, [l - 1 for l in layers])
+            for l in layers:
+                self.owner[l] = gpu
+        assert sorted(self.owner) == list(range(1, cfg.n_layers + 1)), "every layer needs a stage"
+        self.pos: dict = {}                      # rid -> tokens written (context length)
+        self.patches: dict[tuple[int, int], NativePatch] = {}
+        self.moving: dict[tuple[int, int], list[int]] = {}   # pair -> layers
+        self.patched_bytes = 0
+
+    # ---------------------------------------------------------------- stores
+    def _store(self, gpu: int, groups: list[int]) -> KvStore:
+        st = self.stores.get(gpu)
+        if st is None:
+            st = KvStore(gpu, 1, self.s, self.capacity, groups, num_groups=self.cfg.n_layers,
+                         cell_bytes=self.cfg.cell_bytes, device=self.device,
+                         registry=self.registry)
+            N.check(N.lib().pl_store_set_stream(st._h, C.c_void_p(self.stream.cuda_stream)))
+            self.stores[gpu] = st
+        return st
+
+    def on_stream(self):
+        return self.torch.cuda.stream(self.stream)
+
+    def config(self) -> dict[int, list[int]]:
+        out: dict[int, list[int]] = {}
+        for l, g in sorted(self.owner.items()):
+            out.setdefault(g, []).append(l)
+        return out
+
+    # ---------------------------------------------------------------- decode
+    def step(self, rids: list, tokens) -> "object":
+        """One decode step for requests `rids` (token ids on device, [B]) -> fp32 logits
+        [B, vocab].  Each request's new token lands at its current context length."""
+        torch, c, w = self.torch, self.cfg, self.w
+        B = len(rids)
+        handles = [self.registry.handle(r) for r in rids]
+        pos = torch.tensor([self.pos.get(r, 0) for r in rids], device=tokens.device)
+        ctx_host = [self.pos.get(r, 0) + 1 for r in rids]
+        ctx = torch.tensor(ctx_host, dtype=torch.int32, device=tokens.device)
+        rows = torch.tensor(handles, dtype=torch.int32, device=tokens.device)
+        inv = 1.0 / (c.rope_theta ** (torch.arange(0, c.head_dim, 2, device=tokens.device,
+                                                   dtype=torch.float64) / c.head_dim))
+        ang = pos[:, None].double() * inv[None, :]
+        cos = ang.cos().float()[:, None, :]
+        sin = ang.sin().float()[:, None, :]
+
+        def rope(x):
+            x1, x2 = x[..., : c.head_dim // 2], x[..., c.head_dim // 2:]
+            return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
+
+        def rmsnorm(x, g):
+            var = x.double().pow(2).mean(-1, keepdim=True)
+            return (x / (var + c.eps).sqrt()).float() * g
+
+        x = w["embed"][tokens]
+        out = torch.empty(B, c.n_q, c.head_dim, dtype=torch.bfloat16, device=tokens.device)
+        for li in range(c.n_layers):
+            st = self.stores[self.owner[li + 1]]
+            h = rmsnorm(x, w[f"l{li}.attn_norm"])
+            q = rope((h @ w[f"l{li}.wq"]).view(B, c.n_q, c.head_dim)).to(torch.bfloat16)
+            k = rope((h @ w[f"l{li}.wk"]).view(B, c.n_kv, c.head_dim))
+            v = (h @ w[f"l{li}.wv"]).view(B, c.n_kv, c.head_dim)
+            # cell = [K: n_kv x D][V: n_kv x D] bf16, one per (request, layer)
+            kv = torch.cat([k.reshape(B, -1), v.reshape(B, -1)], dim=1).to(torch.bfloat16).contiguous()
+            seeds = [stable_hash(r, li) for r in rids]
+            done = append_batch(st, handles, [li] * B, [1] * B, seeds, kv_dev=kv.data_ptr(),
+                                mark=True)
+            assert done == B
+            N.check(N.lib().pl_paged_attn_decode(
+                st._h, li, 0, C.c_void_p(q.data_ptr()), C.c_void_p(out.data_ptr()),
+                C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B, c.n_q, c.n_kv,
+                c.head_dim, c.head_dim ** -0.5, max(ctx_host),
+                C.c_void_p(self.stream.cuda_stream)))
+            x = x + out.float().view(B, -1) @ w[f"l{li}.wo"]
+            h = rmsnorm(x, w[f"l{li}.mlp_norm"])
+            a = h @ w[f"l{li}.w1"]
+            x = x + (torch.nn.functional.silu(a) * (h @ w[f"l{li}.w3"])) @ w[f"l{li}.w2"]
+            self._keep = (kv, q)  # alive until the stream has consumed them
+        for r in rids:
+            self.pos[r] = self.pos.get(r, 0) + 1
+        return rmsnorm(x, w["final_norm"]) @ w["lm_head"]
+
+    def free(self, rid) -> None:
+        """Request finished: its KV leaves every stage (engine.py:420-430); a migrating
+        pair drops its dirty keys (DirtyBitmap.discard_request, migrator.py:43-48)."""
+        h = self.registry.find(rid)
+        for p in self.patches.values():
+            if h is not None:
+                out = C.c_int64()
+                N.check(N.lib().pl_patch_discard_request(p.h, h, C.byref(out)))
+        for st in self.stores.values():
+            st.free_request(rid)
+        self.pos.pop(rid, None)
+
+    # ---------------------------------------------------------------- live reconfiguration
+    def start_reconfig(self, target: dict[int, list[int]]) -> dict[tuple[int, int], list[int]]:
+        """Phase 3 (coordinator.py:224-230): for every layer whose owner changes, the
+        destination stage maps the layer's pool, a patch engine per (src, dst) pair seeds
+        all live cells of its layers and pushes them (bulk copy); from now on K1 marks
+        every new cell of those layers dirty."""
+        new_owner = {l: g for g, ls in target.items() for l in ls}
+        assert sorted(new_owner) == sorted(self.owner), "target must place every layer"
+        moves: dict[tuple[int, int], list[int]] = {}
+        for l, g in new_owner.items():
+            if self.owner[l] != g:
+                moves.setdefault((self.owner[l], g), []).append(l)
+        for (src, dst), layers in sorted(moves.items()):
+            d = self._store(dst, [])
+            d.resident_groups |= {l - 1 for l in layers}
+            p = NativePatch(self.stores[src], [l - 1 for l in layers], 1)
+            self.patches[(src, dst)] = p
+            self.moving[(src, dst)] = layers
+            p.seed()
+        self.target = new_owner
+        self.pump()
+        return moves
+
+    def pump(self) -> int:
+        """One patch round per migrating pair (MigrationStream.pump -> _drain ->
+        _send_patch -> receive, migrator.py:208-273): drain the dirty cells (K3) and push
+        them into the destination's pools (K4+K5).  Returns the cells moved."""
+        cells_total = 0
+        rank = self.registry.rank()
+        for (src, dst), p in self.patches.items():
+            keys, cells = p.push(self.stores[dst], rank)
+            cells_total += cells
+            self.patched_bytes += cells * self.cfg.cell_bytes
+        return cells_total
+
+    def lag(self) -> int:
+        """Dirty keys not yet drained, over every pair (the converged() test's t_sched -
+        t_applied, migrator.py:341-348, once the in-flight patch has been applied)."""
+        return sum(p.dirty_keys() for p in self.patches.values())
+
+    def switch(self) -> int:
+        """Phase 5 (coordinator.py:275-338): with decode paused between steps, the residual
+        patch of every pair is applied, layer ownership flips to the target, and the
+        sources drop the layers that left (post-commit cleanup, coordinator.py:340-354)."""
+        residual = self.pump()
+        for (src, dst), layers in self.moving.items():
+            for l in layers:
+                self.owner[l] = dst
+        for (src, dst), p in self.patches.items():
+            p.close()
+        for (src, dst), layers in self.moving.items():
+            self.stores[src].drop_layer_groups([l - 1 for l in layers])
+        self.patches.clear()
+        self.moving.clear()
+        return residual
+
+
+def generate(model: StagedLlama, prompts: list[list[int]], joins: list[int], n_gen: int,
+             reconfig: tuple[int, dict] | None = None, switch_at: int | None = None,
+             record: list | None = None) -> list[list[int]]:
+    """Greedy decode of len(prompts) requests that join at steps `joins`, one token per
+    request per step (prompt tokens are fed one at a time).  `reconfig` = (step, target
+    config) starts a live reconfiguration after that step; `switch_at` commits it.
+    `record` (optional) receives (rids, tokens, positions, logits) per step."""
+    with model.on_stream():
+        return _generate(model, prompts, joins, n_gen, reconfig, switch_at, record)
+
+
+def _generate(model, prompts, joins, n_gen, reconfig, switch_at, record):
+    torch = model.torch
+    B = len(prompts)
+    outs: list[list[int]] = [[] for _ in range(B)]
+    t = 0
+    while any(len(o) < n_gen for o in outs):
+        act = [b for b in range(B) if joins[b] <= t and len(outs[b]) < n_gen]
+        if act:
+            toks, poss = [], []
+            for b in act:
+                p = t - joins[b]
+                toks.append(prompts[b][p] if p < len(prompts[b]) else outs[b][-1])
+                poss.append(p)
+            rids = [f"seq{b}" for b in act]
+            tok_t = torch.tensor(toks, dtype=torch.long, device=f"cuda:{model.device}")
+            logits = model.step(rids, tok_t)
+            nxt = logits.argmax(-1).tolist()
+            if record is not None:
+                record.append((rids, toks, poss, logits.cpu().numpy()))
+            for b, p, n in zip(act, poss, nxt):
+                if p >= len(prompts[b]) - 1:
+                    outs[b].append(int(n))
+        if reconfig is not None and t == reconfig[0]:
+            model.start_reconfig(reconfig[1])
+        elif model.patches:
+            model.pump()
+        if switch_at is not None and t == switch_at:
+            model.switch()
+        t += 1
+    return outs

@@ -104,6 +104,11 @@ class NativePatch:
         N.check(N.lib().pl_patch_mark_batch(self.h, len(r), N.ptr(r), N.ptr(g), N.ptr(st),
                                             N.ptr(c)))
 
+    def dirty_keys(self) -> int:
+        out = C.c_int64()
+        N.check(N.lib().pl_patch_dirty_keys(self.h, C.byref(out)))
+        return out.value
+
     def device_drained(self) -> int:
         out = C.c_int64()
         N.check(N.lib().pl_patch_device_drained(self.h, C.byref(out)))
