@@ -196,6 +196,36 @@ int pl_patch_push(pl_patch* p, pl_store* dst, const int32_t* rank_of_req, int64_
 int pl_patch_device_dirty_count(pl_patch* p, int64_t* out);
 int pl_patch_device_drained(pl_patch* p, int64_t* out);
 
+/* ---- cross-process patching (one process per GPU; csrc/ipc.cu).
+ * The receiver's owner exports its pools (VMM chunks as POSIX fds, sent with SCM_RIGHTS)
+ * and its block table (CUDA IPC handle, 64 bytes); the sender imports them into a
+ * pl_remote view.  Each round: sender pl_patch_drain_rows (host snapshot in the
+ * PatchReceiver._apply order, migrator.py:124-128, + K3) -> rows to the receiver ->
+ * receiver pl_store_reserve_rows (write_slots chain extension, kvstore.py:201-227;
+ * stops at the first KvOverflow and reports the items reserved) -> sender
+ * pl_patch_push_remote (fused K4+K5 writes into the remote pools, NVLink stores when the
+ * devices differ).  layout8 = {tokens_per_block, k, cell_bytes, fp_bytes, unit_bytes,
+ * num_model_groups, device, capacity}. */
+typedef struct pl_remote pl_remote;
+int pl_store_layout(pl_store* st, int64_t* out8);
+int pl_store_export_group(pl_store* st, int group, int* fds_out, int cap, int* n_out,
+                          int64_t* chunk_bytes_out);
+int pl_store_export_table(pl_store* st, void* ipc_handle_out, int64_t* max_reqs, int64_t* max_chain);
+int pl_store_table_version(pl_store* st, uint64_t* dev_ptr, int64_t* max_reqs, int64_t* max_chain);
+int pl_store_reserve_rows(pl_store* st, int64_t n_rows, const int32_t* reqs, const int32_t* groups,
+                          const int64_t* starts, const int64_t* ends, int64_t* items_done);
+int pl_remote_create(int device, int tokens_per_block, int stacking_factor, int64_t cell_bytes,
+                     int64_t fp_bytes, int64_t unit_bytes, int num_model_groups, pl_remote** out);
+int pl_remote_destroy(pl_remote* r);
+int pl_remote_import_group(pl_remote* r, int group, const int* fds, int n, int64_t chunk_bytes);
+int pl_remote_drop_group(pl_remote* r, int group);
+int pl_remote_set_table(pl_remote* r, const void* ipc_handle, int64_t max_reqs, int64_t max_chain);
+int pl_patch_drain_rows(pl_patch* p, const int32_t* rank_of_req, int64_t n_rank, int64_t* out_keys,
+                        int64_t* out_cells, int64_t* n_rows);
+int pl_patch_rows(pl_patch* p, int32_t* reqs, int32_t* groups, int64_t* starts, int64_t* ends,
+                  int64_t cap);
+int pl_patch_push_remote(pl_patch* p, pl_remote* r, int64_t n_items_applied);
+
 /* ---- K2 paged-attention decode over the store layout.
  * q_dev [B, n_q, head_dim] bf16; out_dev [B, n_q, head_dim] bf16.
  * req_rows_dev [B] int32 request handles (rows of the store's block table);

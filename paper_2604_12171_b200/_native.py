@@ -107,6 +107,19 @@ SIGNATURES = [
     ("pl_patch_push", C.c_int, [vp, vp, vp, i64, P(i64), P(i64)]),
     ("pl_patch_device_dirty_count", C.c_int, [vp, P(i64)]),
     ("pl_patch_device_drained", C.c_int, [vp, P(i64)]),
+    ("pl_store_layout", C.c_int, [vp, vp]),
+    ("pl_store_export_group", C.c_int, [vp, C.c_int, vp, C.c_int, P(C.c_int), P(i64)]),
+    ("pl_store_export_table", C.c_int, [vp, vp, P(i64), P(i64)]),
+    ("pl_store_table_version", C.c_int, [vp, P(u64), P(i64), P(i64)]),
+    ("pl_store_reserve_rows", C.c_int, [vp, i64, vp, vp, vp, vp, P(i64)]),
+    ("pl_remote_create", C.c_int, [C.c_int, C.c_int, C.c_int, i64, i64, i64, C.c_int, P(vp)]),
+    ("pl_remote_destroy", C.c_int, [vp]),
+    ("pl_remote_import_group", C.c_int, [vp, C.c_int, vp, C.c_int, i64]),
+    ("pl_remote_drop_group", C.c_int, [vp, C.c_int]),
+    ("pl_remote_set_table", C.c_int, [vp, vp, i64, i64]),
+    ("pl_patch_drain_rows", C.c_int, [vp, vp, i64, P(i64), P(i64), P(i64)]),
+    ("pl_patch_rows", C.c_int, [vp, vp, vp, vp, vp, i64]),
+    ("pl_patch_push_remote", C.c_int, [vp, vp, i64]),
     ("pl_paged_attn_decode", C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, C.c_int,
                                        C.c_int, C.c_int, C.c_float, C.c_int, vp]),
     ("pl_paged_attn_decode_raw", C.c_int, [vp, i64, i64, C.c_int, C.c_int, C.c_int, vp, vp, vp,

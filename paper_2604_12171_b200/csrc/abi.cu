@@ -14,6 +14,9 @@ struct pl_store {
 struct pl_patch {
   pl::Patch* p;
 };
+struct pl_remote {
+  pl::Remote* r;
+};
 
 namespace pl {
 namespace {
@@ -589,4 +592,112 @@ int pl_paged_attn_decode_raw(const void* pool, int64_t unit_bytes, int64_t fp_by
   });
 }
 
+}  // extern "C"
+
+// ---- cross-process patching (ipc.cu)
+extern "C" {
+int pl_store_layout(pl_store* st, int64_t* out8) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    const int64_t v[8] = {s->s, s->k, s->cell_bytes, s->fp_bytes, s->unit_bytes,
+                          s->n_model_groups, s->device, s->capacity()};
+    for (int i = 0; i < 8; ++i) out8[i] = v[i];
+  });
+}
+int pl_store_export_group(pl_store* st, int group, int* fds_out, int cap, int* n_out,
+                          int64_t* chunk_bytes_out) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    if (group < 0 || group >= s->n_model_groups || !s->materialised[group])
+      pl::fail(PL_E_INVALID, "group has no pool to export");
+    PL_CUDA(cudaSetDevice(s->device));
+    const auto& chunks = s->arenas[group].chunks;
+    *n_out = (int)chunks.size();
+    *chunk_bytes_out = (int64_t)s->arenas[group].chunk_bytes;
+    if ((int)chunks.size() > cap) pl::fail(PL_E_INVALID, "fd buffer too small");
+    for (size_t i = 0; i < chunks.size(); ++i) fds_out[i] = pl::vmm_export_fd(chunks[i]);
+  });
+}
+int pl_store_export_table(pl_store* st, void* handle_out, int64_t* max_reqs, int64_t* max_chain) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    PL_CUDA(cudaSetDevice(s->device));
+    s->flush();
+    PL_CUDA(cudaStreamSynchronize(s->stream));
+    cudaIpcMemHandle_t h;
+    PL_CUDA(cudaIpcGetMemHandle(&h, s->d_table));
+    std::memcpy(handle_out, &h, sizeof(h));
+    *max_reqs = s->max_reqs;
+    *max_chain = s->max_chain;
+  });
+}
+int pl_store_table_version(pl_store* st, uint64_t* dev_ptr, int64_t* max_reqs, int64_t* max_chain) {
+  return guard([&] {
+    *dev_ptr = (uint64_t)(uintptr_t)st->s->d_table;
+    *max_reqs = st->s->max_reqs;
+    *max_chain = st->s->max_chain;
+  });
+}
+int pl_store_reserve_rows(pl_store* st, int64_t n_rows, const int32_t* reqs, const int32_t* groups,
+                          const int64_t* a, const int64_t* b, int64_t* items_done) {
+  int status = PL_OK;
+  const int rc = guard([&] {
+    PL_CUDA(cudaSetDevice(st->s->device));
+    *items_done = st->s->reserve_rows(n_rows, reqs, groups, a, b, &status);
+  });
+  if (rc != PL_OK) return rc;
+  if (status != PL_OK) pl::g_err = st->s->last_msg;
+  return status;
+}
+int pl_remote_create(int device, int tokens_per_block, int stacking_factor, int64_t cell_bytes,
+                     int64_t fp_bytes, int64_t unit_bytes, int num_model_groups, pl_remote** out) {
+  return guard([&] {
+    *out = new pl_remote{new pl::Remote(device, tokens_per_block, stacking_factor, cell_bytes,
+                                        fp_bytes, unit_bytes, num_model_groups)};
+  });
+}
+int pl_remote_destroy(pl_remote* r) {
+  return guard([&] {
+    if (!r) return;
+    delete r->r;
+    delete r;
+  });
+}
+int pl_remote_import_group(pl_remote* r, int group, const int* fds, int n, int64_t chunk_bytes) {
+  return guard([&] { r->r->import_group(group, fds, n, (size_t)chunk_bytes); });
+}
+int pl_remote_drop_group(pl_remote* r, int group) {
+  return guard([&] {
+    if (group < 0 || group >= r->r->n_model_groups) pl::fail(PL_E_INVALID, "group out of range");
+    PL_CUDA(cudaSetDevice(r->r->device));
+    PL_CUDA(cudaDeviceSynchronize());
+    r->r->drop_group(group);
+  });
+}
+int pl_remote_set_table(pl_remote* r, const void* handle, int64_t max_reqs, int64_t max_chain) {
+  return guard([&] { r->r->set_table(handle, max_reqs, max_chain); });
+}
+int pl_patch_drain_rows(pl_patch* p, const int32_t* rank_of_req, int64_t n_rank, int64_t* out_keys,
+                        int64_t* out_cells, int64_t* n_rows) {
+  return guard([&] {
+    pl::Patch* q = live(p);
+    q->drain_rows(rank_of_req, n_rank, out_keys, out_cells);
+    *n_rows = (int64_t)q->remote_rows.size();
+  });
+}
+int pl_patch_rows(pl_patch* p, int32_t* reqs, int32_t* groups, int64_t* a, int64_t* b, int64_t cap) {
+  return guard([&] {
+    pl::Patch* q = live(p);
+    const int64_t n = std::min<int64_t>(cap, (int64_t)q->remote_rows.size());
+    for (int64_t i = 0; i < n; ++i) {
+      reqs[i] = q->remote_rows[i].req;
+      groups[i] = q->remote_rows[i].group;
+      a[i] = q->remote_rows[i].a;
+      b[i] = q->remote_rows[i].b;
+    }
+  });
+}
+int pl_patch_push_remote(pl_patch* p, pl_remote* r, int64_t n_items_applied) {
+  return guard([&] { live(p)->push_remote(r->r, n_items_applied); });
+}
 }  // extern "C"

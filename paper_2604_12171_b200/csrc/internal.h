@@ -105,6 +105,40 @@ struct Arena {
   void reclaim_tail();
 };
 size_t vmm_granularity(int device);
+// VMM IPC: export a pool chunk as a POSIX fd / import one, map it into a reservation
+int vmm_export_fd(CUmemGenericAllocationHandle h);
+CUmemGenericAllocationHandle vmm_import_fd(int fd);
+CUdeviceptr vmm_reserve(size_t bytes);
+void vmm_map(CUdeviceptr va, size_t bytes, CUmemGenericAllocationHandle h);
+void vmm_unmap(CUdeviceptr va, size_t bytes);
+void vmm_release(CUmemGenericAllocationHandle h);
+void vmm_free_va(CUdeviceptr va, size_t bytes);
+void vmm_set_access(CUdeviceptr va, size_t bytes, int device);
+
+// Remote: this process's view of a store owned by another process (the stage that
+// receives migrating layers).  Its pools are imported from exported VMM chunks and
+// mapped here, its block table is opened through a CUDA IPC handle; the fused push
+// kernel then writes the destination's cells directly (NVLink when the devices
+// differ).  The destination's host block manager stays with its owner.
+struct Remote {
+  int device = 0, s = 0, k = 0, n_model_groups = 0;
+  int64_t cell_bytes = 0, fp_bytes = 0, unit_bytes = 0;
+  struct Pool {
+    CUdeviceptr va = 0;
+    size_t va_bytes = 0, chunk_bytes = 0;
+    std::vector<CUmemGenericAllocationHandle> hs;
+  };
+  std::vector<Pool> pools;
+  uint64_t* d_bases = nullptr;
+  int32_t* table = nullptr;
+  int64_t max_reqs = 0, max_chain = 0;
+  Remote(int device, int s, int k, int64_t cell_bytes, int64_t fp_bytes, int64_t unit_bytes,
+         int n_model_groups);
+  ~Remote();
+  void import_group(int g, const int* fds, int n, size_t chunk_bytes);
+  void drop_group(int g);
+  void set_table(const void* ipc_handle, int64_t max_reqs, int64_t max_chain);
+};
 
 // ---------------------------------------------------------------------------
 struct BlockRec {
@@ -240,6 +274,10 @@ struct Store {
   // write_slots bookkeeping (kvstore.py:201-227) for sorted disjoint position intervals,
   // without the device write; throws KvOverflow like the reference
   void reserve_positions(int32_t req, int g, const std::vector<Interval>& iv);
+  // receiver side of a cross-process patch: consecutive rows with the same (req, group)
+  // are one item; returns the items fully reserved (stops at the first KvOverflow)
+  int64_t reserve_rows(int64_t n_rows, const int32_t* reqs, const int32_t* groups,
+                       const int64_t* a, const int64_t* b, int* status);
 
   // launch K1 for a list of (req, group, start, count) items
   struct WriteItem {
@@ -328,6 +366,14 @@ struct Patch {
   void apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
              int64_t n_stale);
   void push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells);
+  // cross-process push (ipc.cu): drain the dirty set into flat (req, model group, a, b)
+  // interval rows in the receiver's apply order + K3 on device; then, once the owner of
+  // the destination store has reserved the rows' positions (Store::reserve_rows), the
+  // fused K4+K5 writes the cells of the first n_items_applied items into the remote view
+  struct Row { int32_t req, group; int64_t a, b; };
+  std::vector<Row> remote_rows;
+  void drain_rows(const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells);
+  void push_remote(Remote* r, int64_t n_items_applied);
   int64_t device_dirty_count();
   int32_t* d_groups_ = nullptr;
   const int32_t* d_groups();

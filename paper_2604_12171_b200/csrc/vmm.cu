@@ -39,6 +39,8 @@ struct Driver {
   decltype(&cuMemUnmap) Unmap = nullptr;
   decltype(&cuMemSetAccess) SetAccess = nullptr;
   decltype(&cuMemGetAllocationGranularity) Granularity = nullptr;
+  decltype(&cuMemExportToShareableHandle) Export = nullptr;
+  decltype(&cuMemImportFromShareableHandle) Import = nullptr;
 };
 
 template <class F>
@@ -63,6 +65,8 @@ Driver& drv() {
     load(d.Unmap, "cuMemUnmap");
     load(d.SetAccess, "cuMemSetAccess");
     load(d.Granularity, "cuMemGetAllocationGranularity");
+    load(d.Export, "cuMemExportToShareableHandle");
+    load(d.Import, "cuMemImportFromShareableHandle");
   });
   return d;
 }
@@ -72,6 +76,9 @@ CUmemAllocationProp prop_for(int device) {
   p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   p.location.id = device;
+  // every pool chunk can be exported to the process that owns a peer stage
+  // (cross-process NVLink push)
+  p.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
   return p;
 }
 
@@ -108,6 +115,34 @@ size_t vmm_granularity(int device) {
            "cuMemGetAllocationGranularity");
   return g;
 }
+
+// ---------------------------------------------------------------------------
+// VMM IPC helpers (the remote-store view, ipc.cu)
+int vmm_export_fd(CUmemGenericAllocationHandle h) {
+  int fd = -1;
+  cu_check(drv().Export(&fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+           "cuMemExportToShareableHandle");
+  return fd;
+}
+CUmemGenericAllocationHandle vmm_import_fd(int fd) {
+  CUmemGenericAllocationHandle h = 0;
+  cu_check(drv().Import(&h, reinterpret_cast<void*>(static_cast<uintptr_t>(fd)),
+                        CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+           "cuMemImportFromShareableHandle");
+  return h;
+}
+CUdeviceptr vmm_reserve(size_t bytes) {
+  CUdeviceptr va = 0;
+  cu_check(drv().AddressReserve(&va, bytes, 0, 0, 0), "cuMemAddressReserve");
+  return va;
+}
+void vmm_map(CUdeviceptr va, size_t bytes, CUmemGenericAllocationHandle h) {
+  cu_check(drv().Map(va, bytes, 0, h, 0), "cuMemMap");
+}
+void vmm_unmap(CUdeviceptr va, size_t bytes) { drv().Unmap(va, bytes); }
+void vmm_release(CUmemGenericAllocationHandle h) { drv().Release(h); }
+void vmm_free_va(CUdeviceptr va, size_t bytes) { drv().AddressFree(va, bytes); }
+void vmm_set_access(CUdeviceptr va, size_t bytes, int device) { set_access(va, bytes, device, {}); }
 
 // ---------------------------------------------------------------------------
 // Reclaimer

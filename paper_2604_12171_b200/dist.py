@@ -1,0 +1,291 @@
+"""One process per GPU: the cross-process halves of the patch path and stage activations.
+
+- ``Channel``: a Unix-domain stream socket between two local ranks.  It carries pickled
+  control messages (a few KB per patch round) and, with SCM_RIGHTS, the POSIX fds of the
+  destination's exported VMM pool chunks.  Both stages of a migrating pair are on one
+  node (NVSwitch), so a local socket is enough; nothing here touches NCCL.
+- ``RemoteStore``: the sender's view of the receiver's store (pools imported from the
+  fds, block table opened from a CUDA IPC handle), used by the fused push kernel to
+  write the receiver's cells directly (NVLink stores when the GPUs differ).
+- ``PatchSender`` / ``PatchReceiver``: one migrating (src, dst) pair split across the two
+  processes.  Per round (MigrationStream.pump -> _drain -> _send_patch ->
+  PatchReceiver.receive, migrator.py:208-273, 93-132): sender drains rows + K3 ->
+  receiver reserves the positions with the reference's block-id policy and publishes
+  its table -> sender pushes (K4+K5) -> sender's stream is synchronised -> "applied".
+- ``StageLink``: stage-to-stage activations (engine.py:353-375, fabric.py:129-136) as
+  point-to-point send/recv on a torch.distributed group: NCCL moves device tensors over
+  NVLink, gloo stages them through host memory (CPU tests).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import pickle
+import socket
+import struct
+import time
+
+import numpy as np
+
+from . import _native as N
+from .kvstore import KvStore, _check
+from .perf import NativePatch
+
+_HDR = struct.Struct("<QI")
+
+
+class Channel:
+    """Local socket between two processes; ``name`` is shared, one side is the server."""
+
+    def __init__(self, name: str, server: bool, timeout: float = 120.0) -> None:
+        addr = "\0pipelive-" + name   # Linux abstract namespace: no file to clean up
+        if server:
+            ls = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            ls.bind(addr)
+            ls.listen(1)
+            ls.settimeout(timeout)
+            self.sock, _ = ls.accept()
+            ls.close()
+        else:
+            deadline = time.time() + timeout
+            while True:
+                s = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                try:
+                    s.connect(addr)
+                    break
+                except OSError:
+                    s.close()
+                    if time.time() > deadline:
+                        raise
+                    time.sleep(0.02)
+            self.sock = s
+        self.sock.settimeout(None)
+
+    def send(self, obj, fds=()) -> None:
+        data = pickle.dumps(obj)
+        socket.send_fds(self.sock, [_HDR.pack(len(data), len(fds))], list(fds))
+        self.sock.sendall(data)
+
+    def recv(self):
+        hdr, fds, _, _ = socket.recv_fds(self.sock, _HDR.size, 4096)
+        while len(hdr) < _HDR.size:
+            more = self.sock.recv(_HDR.size - len(hdr))
+            if not more:
+                raise ConnectionError("channel closed")
+            hdr += more
+        n, n_fds = _HDR.unpack(hdr)
+        buf = bytearray()
+        while len(buf) < n:
+            chunk = self.sock.recv(n - len(buf))
+            if not chunk:
+                raise ConnectionError("channel closed")
+            buf += chunk
+        assert len(fds) == n_fds, (len(fds), n_fds)
+        return pickle.loads(bytes(buf)), list(fds)
+
+    def close(self) -> None:
+        self.sock.close()
+
+
+def store_layout(store: KvStore) -> list[int]:
+    out = np.zeros(8, dtype=np.int64)
+    _check(N.lib().pl_store_layout(store._h, N.ptr(out)))
+    return [int(x) for x in out]
+
+
+def export_groups(store: KvStore, groups) -> tuple[dict, list[int]]:
+    """(meta {group: (chunk_bytes, n_chunks, base)}, fds in group order)."""
+    meta, fds = {}, []
+    for g in sorted(groups):
+        buf = (C.c_int * 4096)()
+        n, cb = C.c_int(), C.c_int64()
+        _check(N.lib().pl_store_export_group(store._h, g, buf, 4096, C.byref(n), C.byref(cb)))
+        meta[g] = (cb.value, n.value, store.group_base(g))
+        fds += list(buf[: n.value])
+    return meta, fds
+
+
+def export_table(store: KvStore) -> tuple[bytes, int, int]:
+    h = (C.c_ubyte * 64)()
+    mr, mc = C.c_int64(), C.c_int64()
+    _check(N.lib().pl_store_export_table(store._h, h, C.byref(mr), C.byref(mc)))
+    return bytes(h), mr.value, mc.value
+
+
+def table_version(store: KvStore) -> tuple[int, int, int]:
+    p, mr, mc = C.c_uint64(), C.c_int64(), C.c_int64()
+    _check(N.lib().pl_store_table_version(store._h, C.byref(p), C.byref(mr), C.byref(mc)))
+    return p.value, mr.value, mc.value
+
+
+class RemoteStore:
+    """This process's view of a peer process's store (pl_remote)."""
+
+    def __init__(self, device: int, layout: list[int]) -> None:
+        s, k, cell, fp, unit, groups = layout[:6]
+        h = C.c_void_p()
+        N.check(N.lib().pl_remote_create(device, s, k, cell, fp, unit, groups, C.byref(h)))
+        self.h = h
+        self.layout = layout
+
+    def import_groups(self, meta: dict, fds: list[int]) -> None:
+        i = 0
+        for g, (cb, n, _base) in sorted(meta.items()):
+            arr = (C.c_int * n)(*fds[i:i + n])
+            N.check(N.lib().pl_remote_import_group(self.h, g, arr, n, cb))
+            i += n
+        for fd in fds:   # the driver holds its own reference after the import
+            os.close(fd)
+
+    def set_table(self, handle: bytes, max_reqs: int, max_chain: int) -> None:
+        buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+        N.check(N.lib().pl_remote_set_table(self.h, buf, max_reqs, max_chain))
+
+    def close(self) -> None:
+        if self.h is not None:
+            N.lib().pl_remote_destroy(self.h)
+            self.h = None
+
+
+class PatchReceiver:
+    """Destination half of a cross-process pair: maps the migrating groups, exports
+    them, and serves patch rounds until the sender closes the pair."""
+
+    def __init__(self, store: KvStore, groups, chan: Channel) -> None:
+        self.store = store
+        self.groups = sorted(groups)
+        self.chan = chan
+        store.resident_groups |= set(self.groups)
+        self._send_hello()
+        self.rounds = 0
+        self.items_reserved = 0
+
+    def _pool_state(self):
+        return tuple(self.store.group_base(g) for g in self.groups), self.store.info()["mapped_bytes"]
+
+    def _send_hello(self) -> None:
+        meta, fds = export_groups(self.store, self.groups)
+        table = export_table(self.store)
+        self._pools = self._pool_state()
+        self._table = table_version(self.store)
+        self.chan.send(("hello", store_layout(self.store), meta, table), fds)
+        for fd in fds:
+            os.close(fd)
+
+    def serve(self) -> bool:
+        """One round; False once the sender closed the pair."""
+        msg, _ = self.chan.recv()
+        if msg[0] == "close":
+            return False
+        assert msg[0] == "rows", msg[0]
+        reqs, groups, a, b = (np.ascontiguousarray(x) for x in msg[1])
+        done = C.c_int64()
+        rc = N.lib().pl_store_reserve_rows(self.store._h, len(reqs), N.ptr(reqs), N.ptr(groups),
+                                           N.ptr(a), N.ptr(b), C.byref(done))
+        err = None if rc == N.PL_OK else (rc, N.lib().pl_last_error().decode(errors="replace"))
+        update, fds = {}, []
+        if table_version(self.store) != self._table:
+            update["table"] = export_table(self.store)
+            self._table = table_version(self.store)
+        if self._pool_state() != self._pools:
+            update["pools"], fds = export_groups(self.store, self.groups)
+            self._pools = self._pool_state()
+        self.chan.send(("reserved", done.value, err, update), fds)
+        for fd in fds:
+            os.close(fd)
+        ack, _ = self.chan.recv()
+        assert ack[0] == "applied", ack[0]
+        self.rounds += 1
+        self.items_reserved += done.value
+        if err is not None:
+            from .kvstore import _ERRORS
+            raise _ERRORS.get(err[0], N.NativeError)(err[1])
+        return True
+
+
+class PatchSender:
+    """Source half of a cross-process pair: the native patch engine over the local store
+    plus the remote view of the receiver's pools and table."""
+
+    def __init__(self, store: KvStore, groups, layers_per_group: int, chan: Channel,
+                 rank_fn) -> None:
+        self.store = store
+        self.chan = chan
+        self.rank_fn = rank_fn            # () -> int32 rank of every request handle
+        self.patch = NativePatch(store, groups, layers_per_group)
+        msg, fds = chan.recv()
+        assert msg[0] == "hello", msg[0]
+        _, layout, meta, (th, mr, mc) = msg
+        self.remote = RemoteStore(store.device, layout)
+        self.remote.import_groups(meta, fds)
+        self.remote.set_table(th, mr, mc)
+        self.keys = self.cells = 0
+
+    def seed(self) -> int:
+        """MigrationStream.start (migrator.py:170-183): every live cell becomes dirty."""
+        return self.patch.seed()
+
+    def round(self) -> tuple[int, int]:
+        """Drain + push one patch; returns (keys, cells) like MigrationStream._drain."""
+        rank = self.rank_fn()
+        keys, cells, n = C.c_int64(), C.c_int64(), C.c_int64()
+        N.check(N.lib().pl_patch_drain_rows(self.patch.h, N.ptr(rank), len(rank), C.byref(keys),
+                                            C.byref(cells), C.byref(n)))
+        m = n.value
+        rows = (np.empty(m, np.int32), np.empty(m, np.int32), np.empty(m, np.int64),
+                np.empty(m, np.int64))
+        N.check(N.lib().pl_patch_rows(self.patch.h, *(N.ptr(x) for x in rows), m))
+        self.chan.send(("rows", rows))
+        msg, fds = self.chan.recv()
+        assert msg[0] == "reserved", msg[0]
+        _, done, err, update = msg
+        if "pools" in update:
+            self.remote.import_groups(update["pools"], fds)
+        if "table" in update:
+            self.remote.set_table(*update["table"])
+        N.check(N.lib().pl_patch_push_remote(self.patch.h, self.remote.h, done))
+        self.store.sync()   # the cells are in the receiver's HBM before it is told so
+        self.chan.send(("applied",))
+        if err is not None:
+            from .kvstore import _ERRORS
+            raise _ERRORS.get(err[0], N.NativeError)(err[1])
+        self.keys += keys.value
+        self.cells += cells.value
+        return keys.value, cells.value
+
+    def dirty_keys(self) -> int:
+        return self.patch.dirty_keys()
+
+    def close(self) -> None:
+        self.chan.send(("close",))
+        self.patch.close()
+        self.remote.close()
+
+
+class StageLink:
+    """Stage-to-stage activations on a torch.distributed group (K7)."""
+
+    def __init__(self, group=None) -> None:
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.backend = dist.get_backend(group)
+
+    def send(self, t, dst: int) -> None:
+        if self.backend == "nccl":
+            self.dist.send(t.contiguous(), dst, group=self.group)
+        else:
+            self.dist.send(t.detach().to("cpu").contiguous(), dst, group=self.group)
+
+    def recv(self, shape, dtype, src: int, device):
+        import torch
+
+        if self.backend == "nccl":
+            t = torch.empty(shape, dtype=dtype, device=device)
+            self.dist.recv(t, src, group=self.group)
+            return t
+        t = torch.empty(shape, dtype=dtype)
+        self.dist.recv(t, src, group=self.group)
+        return t.to(device)

@@ -1,0 +1,118 @@
+"""Worker processes of the cross-process patch tests (tests/test_gpu_ipc.py): both run
+on cuda:0, in separate processes, exactly like two stage processes on two GPUs."""
+
+import random
+
+N_REQ = 12
+K, S, CELL, CAP = 2, 16, 256, 512
+
+
+def names():
+    return [f"r{i:04d}" for i in range(N_REQ)]
+
+
+def _registry():
+    from paper_2604_12171_b200 import kvstore
+    reg = kvstore.RequestRegistry()
+    for n in names():          # both processes assign the same handles
+        reg.handle(n)
+    return reg
+
+
+def ops(seed):
+    """(initial fill, per-round decode/prefill writes) of the source stage"""
+    rng = random.Random(seed)
+    fill = [(n, g, 5 + rng.randrange(60)) for n in names()[: N_REQ - 3] for g in range(4)]
+    rounds = []
+    for _ in range(4):
+        w = []
+        for n in rng.sample(names(), 6):     # includes requests that join mid-migration
+            for g in rng.sample(range(4), 2):
+                w.append((n, g, 1 + rng.randrange(20)))
+        rounds.append(w)
+    return fill, rounds
+
+
+def src_store(reg):
+    from paper_2604_12171_b200 import kvstore
+    return kvstore.KvStore(1, K, S, CAP, (0, 1, 2, 3), num_groups=4, cell_bytes=CELL, registry=reg)
+
+
+def dst_store(reg):
+    from paper_2604_12171_b200 import kvstore
+    return kvstore.KvStore(2, K, S, CAP, (), num_groups=4, cell_bytes=CELL, registry=reg)
+
+
+def apply_writes(st, writes, mark):
+    from paper_2604_12171_b200.events import stable_hash
+    for n, g, cnt in writes:
+        st.append_seeded(n, g, cnt, stable_hash(n, g), mark=mark)
+
+
+def summary(st, groups=(2, 3)):
+    snaps = {g: st.snapshot_group(g) for g in groups}
+    cells = {}
+    for g in groups:
+        for rid, fps in snaps[g].items():
+            for pos in {0, len(fps) // 2, len(fps) - 1}:
+                for j in range(K):
+                    cells[(rid, g, pos, j)] = st.read_cell(rid, g, pos, j)
+    return snaps, cells, repr(st.state_digest())
+
+
+def receiver(q, chan_name, seed):
+    try:
+        import torch
+        torch.cuda.set_device(0)
+        from paper_2604_12171_b200 import dist as D
+        reg = _registry()
+        st = dst_store(reg)
+        chan = D.Channel(chan_name, server=True)
+        rx = D.PatchReceiver(st, [2, 3], chan)
+        while rx.serve():
+            pass
+        q.put(("rx", summary(st), rx.rounds))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put(("rx-error", traceback.format_exc(), repr(e)))
+
+
+def sender(q, chan_name, seed):
+    try:
+        import torch
+        torch.cuda.set_device(0)
+        from paper_2604_12171_b200 import dist as D
+        reg = _registry()
+        st = src_store(reg)
+        fill, rounds = ops(seed)
+        apply_writes(st, fill, mark=False)
+        chan = D.Channel(chan_name, server=False)
+        tx = D.PatchSender(st, [2, 3], K, chan, reg.rank)
+        tx.seed()
+        log = [tx.round()]
+        for w in rounds:
+            apply_writes(st, w, mark=True)
+            log.append(tx.round())
+        tx.close()
+        q.put(("tx", summary(st), log))
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put(("tx-error", traceback.format_exc(), repr(e)))
+
+
+def single_process(seed):
+    """The same rounds with both stores in one process (local fused push)."""
+    from paper_2604_12171_b200.perf import NativePatch
+    reg = _registry()
+    src, dst = src_store(reg), dst_store(reg)
+    dst.resident_groups |= {2, 3}
+    fill, rounds = ops(seed)
+    apply_writes(src, fill, mark=False)
+    p = NativePatch(src, [2, 3], K)
+    p.seed()
+    log = [p.push(dst, reg.rank())]
+    for w in rounds:
+        apply_writes(src, w, mark=True)
+        log.append(p.push(dst, reg.rank()))
+    p.close()
+    return summary(src), summary(dst), log

@@ -1,0 +1,44 @@
+"""Cross-process KV patching on one GPU: the source and destination stages run in two
+processes (as they would on two GPUs), the destination's pools are exported as VMM
+fds + its block table as a CUDA IPC handle, and the fused push kernel writes the
+destination's cells through the imported view.  The result must equal, bit for bit,
+the single-process push of the same rounds (block ids, chains, fingerprints, KV bytes)
+and the source's own copy of the migrated groups."""
+
+import multiprocessing as mp
+import os
+
+import pytest
+
+import ipc_workers as W
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_two_process_push_matches_single_process(seed):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    name = f"ipc-test-{os.getpid()}-{seed}"
+    procs = [ctx.Process(target=W.receiver, args=(q, name, seed)),
+             ctx.Process(target=W.sender, args=(q, name, seed))]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r = q.get(timeout=240)
+        assert not r[0].endswith("error"), r[1]
+        res[r[0]] = r[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (tx_sum, tx_log), (rx_sum, rx_rounds) = res["tx"], res["rx"]
+    assert rx_rounds == len(tx_log) == 5
+    src_sum, dst_sum, log = W.single_process(seed)
+    assert [tuple(x) for x in tx_log] == [tuple(x) for x in log]   # keys, cells per round
+    assert rx_sum == dst_sum                 # snapshots, sampled cells, full state digest
+    assert rx_sum[0] == tx_sum[0]            # the destination holds the source's groups
+    for (rid, g, pos, j), cell in rx_sum[1].items():
+        fp = rx_sum[0][g][rid][pos]
+        assert cell == oracle.expand_cell(fp, j, W.CELL)
