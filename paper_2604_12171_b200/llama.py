@@ -77,6 +77,80 @@ def init_weights(cfg: LlamaConfig, seed: int = 0) -> dict[str, np.ndarray]:
     return w
 
 
+class LlamaCompute:
+    """The math of one decode step, layer by layer, over whichever store owns a layer."""
+
+    def __init__(self, cfg: LlamaConfig, weights: dict[str, np.ndarray], device: int,
+                 registry: RequestRegistry, stream) -> None:
+        import torch
+
+        self.torch = torch
+        self.cfg = cfg
+        self.registry = registry
+        self.stream = stream
+        dev = torch.device("cuda", device)
+        self.w = {k: torch.from_numpy(v).to(dev) for k, v in weights.items()}
+
+    def begin(self, rids: list, positions: list[int], device) -> dict:
+        """Per-step state: request rows, context lengths after this token, RoPE tables."""
+        torch, c = self.torch, self.cfg
+        handles = [self.registry.handle(r) for r in rids]
+        pos = torch.tensor(positions, device=device)
+        inv = 1.0 / (c.rope_theta ** (torch.arange(0, c.head_dim, 2, device=device,
+                                                   dtype=torch.float64) / c.head_dim))
+        ang = pos[:, None].double() * inv[None, :]
+        ctx_host = [p + 1 for p in positions]
+        return {"rids": rids, "handles": handles, "ctx_host": ctx_host,
+                "ctx": torch.tensor(ctx_host, dtype=torch.int32, device=device),
+                "rows": torch.tensor(handles, dtype=torch.int32, device=device),
+                "cos": ang.cos().float()[:, None, :], "sin": ang.sin().float()[:, None, :],
+                "out": torch.empty(len(rids), c.n_q, c.head_dim, dtype=torch.bfloat16,
+                                   device=device)}
+
+    def _rmsnorm(self, x, g):
+        var = x.double().pow(2).mean(-1, keepdim=True)
+        return (x / (var + self.cfg.eps).sqrt()).float() * g
+
+    def embed(self, tokens):
+        return self.w["embed"][tokens]
+
+    def head(self, x):
+        return self._rmsnorm(x, self.w["final_norm"]) @ self.w["lm_head"]
+
+    def layer(self, li: int, x, st: KvStore, sc: dict):
+        """Layer li (0-based): K/V of the new tokens into `st` by K1 (fused dirty mark),
+        K2 attention over `st`'s block table, then the dense parts."""
+        torch, c, w = self.torch, self.cfg, self.w
+        B = len(sc["rids"])
+        cos, sin, out = sc["cos"], sc["sin"], sc["out"]
+
+        def rope(t):
+            t1, t2 = t[..., : c.head_dim // 2], t[..., c.head_dim // 2:]
+            return torch.cat([t1 * cos - t2 * sin, t2 * cos + t1 * sin], dim=-1)
+
+        h = self._rmsnorm(x, w[f"l{li}.attn_norm"])
+        q = rope((h @ w[f"l{li}.wq"]).view(B, c.n_q, c.head_dim)).to(torch.bfloat16)
+        k = rope((h @ w[f"l{li}.wk"]).view(B, c.n_kv, c.head_dim))
+        v = (h @ w[f"l{li}.wv"]).view(B, c.n_kv, c.head_dim)
+        # cell = [K: n_kv x D][V: n_kv x D] bf16, one per (request, layer)
+        kv = torch.cat([k.reshape(B, -1), v.reshape(B, -1)], dim=1).to(torch.bfloat16).contiguous()
+        seeds = [stable_hash(r, li) for r in sc["rids"]]
+        done = append_batch(st, sc["handles"], [li] * B, [1] * B, seeds, kv_dev=kv.data_ptr(),
+                            mark=True)
+        assert done == B
+        N.check(N.lib().pl_paged_attn_decode(
+            st._h, li, 0, C.c_void_p(q.data_ptr()), C.c_void_p(out.data_ptr()),
+            C.c_void_p(sc["rows"].data_ptr()), C.c_void_p(sc["ctx"].data_ptr()), B, c.n_q,
+            c.n_kv, c.head_dim, c.head_dim ** -0.5, max(sc["ctx_host"]),
+            C.c_void_p(self.stream.cuda_stream)))
+        x = x + out.float().view(B, -1) @ w[f"l{li}.wo"]
+        h = self._rmsnorm(x, w[f"l{li}.mlp_norm"])
+        a = h @ w[f"l{li}.w1"]
+        x = x + (torch.nn.functional.silu(a) * (h @ w[f"l{li}.w3"])) @ w[f"l{li}.w2"]
+        sc.setdefault("keep", []).append((kv, q))  # alive until the stream consumed them
+        return x
+
+
 class StagedLlama:
     """A Llama decoder split into pipeline stages, each stage's KV in its own store."""
 
@@ -94,8 +168,7 @@ class StagedLlama:
         # one non-default stream for the whole stage loop: torch ops, K1, K2 and the patch
         # rounds are ordered by it (callers run model code under `with model.on_stream()`)
         self.stream = torch.cuda.Stream(device=device)
-        dev = torch.device("cuda", device)
-        self.w = {k: torch.from_numpy(v).to(dev) for k, v in weights.items()}
+        self.compute = LlamaCompute(cfg, weights, device, self.registry, self.stream)
         self.stores: dict[int, KvStore] = {}
         self.owner: dict[int, int] = {}          # layer (1-based) -> gpu id
         for gpu, layers in config.items():
@@ -132,54 +205,13 @@ class StagedLlama:
     def step(self, rids: list, tokens) -> "object":
         """One decode step for requests `rids` (token ids on device, [B]) -> fp32 logits
         [B, vocab].  Each request's new token lands at its current context length."""
-        torch, c, w = self.torch, self.cfg, self.w
-        B = len(rids)
-        handles = [self.registry.handle(r) for r in rids]
-        pos = torch.tensor([self.pos.get(r, 0) for r in rids], device=tokens.device)
-        ctx_host = [self.pos.get(r, 0) + 1 for r in rids]
-        ctx = torch.tensor(ctx_host, dtype=torch.int32, device=tokens.device)
-        rows = torch.tensor(handles, dtype=torch.int32, device=tokens.device)
-        inv = 1.0 / (c.rope_theta ** (torch.arange(0, c.head_dim, 2, device=tokens.device,
-                                                   dtype=torch.float64) / c.head_dim))
-        ang = pos[:, None].double() * inv[None, :]
-        cos = ang.cos().float()[:, None, :]
-        sin = ang.sin().float()[:, None, :]
-
-        def rope(x):
-            x1, x2 = x[..., : c.head_dim // 2], x[..., c.head_dim // 2:]
-            return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
-
-        def rmsnorm(x, g):
-            var = x.double().pow(2).mean(-1, keepdim=True)
-            return (x / (var + c.eps).sqrt()).float() * g
-
-        x = w["embed"][tokens]
-        out = torch.empty(B, c.n_q, c.head_dim, dtype=torch.bfloat16, device=tokens.device)
-        for li in range(c.n_layers):
-            st = self.stores[self.owner[li + 1]]
-            h = rmsnorm(x, w[f"l{li}.attn_norm"])
-            q = rope((h @ w[f"l{li}.wq"]).view(B, c.n_q, c.head_dim)).to(torch.bfloat16)
-            k = rope((h @ w[f"l{li}.wk"]).view(B, c.n_kv, c.head_dim))
-            v = (h @ w[f"l{li}.wv"]).view(B, c.n_kv, c.head_dim)
-            # cell = [K: n_kv x D][V: n_kv x D] bf16, one per (request, layer)
-            kv = torch.cat([k.reshape(B, -1), v.reshape(B, -1)], dim=1).to(torch.bfloat16).contiguous()
-            seeds = [stable_hash(r, li) for r in rids]
-            done = append_batch(st, handles, [li] * B, [1] * B, seeds, kv_dev=kv.data_ptr(),
-                                mark=True)
-            assert done == B
-            N.check(N.lib().pl_paged_attn_decode(
-                st._h, li, 0, C.c_void_p(q.data_ptr()), C.c_void_p(out.data_ptr()),
-                C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B, c.n_q, c.n_kv,
-                c.head_dim, c.head_dim ** -0.5, max(ctx_host),
-                C.c_void_p(self.stream.cuda_stream)))
-            x = x + out.float().view(B, -1) @ w[f"l{li}.wo"]
-            h = rmsnorm(x, w[f"l{li}.mlp_norm"])
-            a = h @ w[f"l{li}.w1"]
-            x = x + (torch.nn.functional.silu(a) * (h @ w[f"l{li}.w3"])) @ w[f"l{li}.w2"]
-            self._keep = (kv, q)  # alive until the stream has consumed them
+        sc = self.compute.begin(rids, [self.pos.get(r, 0) for r in rids], tokens.device)
+        x = self.compute.embed(tokens)
+        for li in range(self.cfg.n_layers):
+            x = self.compute.layer(li, x, self.stores[self.owner[li + 1]], sc)
         for r in rids:
             self.pos[r] = self.pos.get(r, 0) + 1
-        return rmsnorm(x, w["final_norm"]) @ w["lm_head"]
+        return self.compute.head(x)
 
     def free(self, rid) -> None:
         """Request finished: its KV leaves every stage (engine.py:420-430); a migrating
@@ -291,3 +323,159 @@ def _generate(model, prompts, joins, n_gen, reconfig, switch_at, record):
             model.switch()
         t += 1
     return outs
+
+
+# ======================================================================================
+# One process per stage GPU: activations over a torch.distributed group
+# (StageLink, K7), KV patches over the cross-process push (dist.PatchSender/Receiver).
+class DistStagedLlama:
+    """This rank's stage of a pipeline whose stages are processes.  Every rank runs the
+    same step schedule; stage i receives the hidden states from the previous stage,
+    runs its layers over its own store and sends them on; the last stage's greedy tokens
+    are broadcast so every rank knows the next inputs."""
+
+    def __init__(self, cfg: LlamaConfig, weights: dict[str, np.ndarray],
+                 config: dict[int, list[int]], rank: int, device: int = 0,
+                 tokens_per_block: int = 16, capacity_blocks: int = 256,
+                 registry: RequestRegistry | None = None, channel_prefix: str = "pl",
+                 group=None) -> None:
+        import torch
+
+        from .dist import StageLink
+
+        self.torch = torch
+        self.cfg = cfg
+        self.rank = rank
+        self.gpu = rank + 1                       # pipeline GPU id of this process
+        self.device = device
+        self.prefix = channel_prefix
+        self.group = group
+        self.registry = registry or RequestRegistry()
+        self.stream = torch.cuda.Stream(device=device)
+        self.compute = LlamaCompute(cfg, weights, device, self.registry, self.stream)
+        self.link = StageLink(group)
+        self.owner = {l: g for g, ls in config.items() for l in ls}
+        mine = [l - 1 for l, g in self.owner.items() if g == self.gpu]
+        self.store = KvStore(self.gpu, 1, tokens_per_block, capacity_blocks, mine,
+                             num_groups=cfg.n_layers, cell_bytes=cfg.cell_bytes, device=device,
+                             registry=self.registry)
+        N.check(N.lib().pl_store_set_stream(self.store._h, C.c_void_p(self.stream.cuda_stream)))
+        self.pos: dict = {}
+        self.senders: dict = {}
+        self.receivers: dict = {}
+        self.moving: dict = {}
+
+    def on_stream(self):
+        return self.torch.cuda.stream(self.stream)
+
+    def _order(self) -> list[int]:
+        """Pipeline order: GPUs holding layers, by their first layer."""
+        first: dict[int, int] = {}
+        for l, g in self.owner.items():
+            first[g] = min(first.get(g, l), l)
+        return sorted(first, key=first.get)
+
+    def step_tokens(self, rids: list, tokens: list[int]) -> list[int]:
+        torch, c = self.torch, self.cfg
+        dev = torch.device("cuda", self.device)
+        order = self._order()
+        B = len(rids)
+        sc = self.compute.begin(rids, [self.pos.get(r, 0) for r in rids], dev)
+        nxt = torch.empty(B, dtype=torch.long)
+        if self.gpu in order:
+            i = order.index(self.gpu)
+            if i == 0:
+                x = self.compute.embed(torch.tensor(tokens, dtype=torch.long, device=dev))
+            else:
+                self.stream.synchronize()
+                x = self.link.recv((B, c.d_model), torch.float32, order[i - 1] - 1, dev)
+            for l in sorted(l for l, g in self.owner.items() if g == self.gpu):
+                x = self.compute.layer(l - 1, x, self.store, sc)
+            if i + 1 < len(order):
+                self.stream.synchronize()
+                self.link.send(x, order[i + 1] - 1)
+            else:
+                nxt = self.compute.head(x).argmax(-1).cpu()
+        self.link.dist.broadcast(nxt, order[-1] - 1, group=self.group)
+        for r in rids:
+            self.pos[r] = self.pos.get(r, 0) + 1
+        return [int(t) for t in nxt]
+
+    # ---------------------------------------------------------------- live reconfiguration
+    def _pairs(self):
+        return sorted(self.moving)
+
+    def start_reconfig(self, target: dict[int, list[int]]) -> None:
+        from .dist import Channel, PatchReceiver, PatchSender
+
+        new_owner = {l: g for g, ls in target.items() for l in ls}
+        moves: dict = {}
+        for l, g in new_owner.items():
+            if self.owner[l] != g:
+                moves.setdefault((self.owner[l], g), []).append(l)
+        self.moving = moves
+        self.target = new_owner
+        # channels are set up in one global pair order on every rank (no wait cycles)
+        for (src, dst) in self._pairs():
+            groups = [l - 1 for l in moves[(src, dst)]]
+            name = f"{self.prefix}-{src}-{dst}"
+            if dst == self.gpu:
+                self.receivers[(src, dst)] = PatchReceiver(self.store, groups,
+                                                           Channel(name, server=True))
+            elif src == self.gpu:
+                tx = PatchSender(self.store, groups, 1, Channel(name, server=False),
+                                 self.registry.rank)
+                tx.seed()
+                self.senders[(src, dst)] = tx
+        self.pump()
+
+    def pump(self) -> None:
+        for pair in self._pairs():
+            if pair in self.senders:
+                self.senders[pair].round()
+            elif pair in self.receivers:
+                assert self.receivers[pair].serve()
+
+    def switch(self) -> None:
+        self.pump()                     # residual patch of every pair
+        for pair in self._pairs():
+            if pair in self.senders:
+                self.senders.pop(pair).close()
+            elif pair in self.receivers:
+                assert not self.receivers.pop(pair).serve()
+        for (src, dst), layers in self.moving.items():
+            for l in layers:
+                self.owner[l] = dst
+            if src == self.gpu:
+                self.store.drop_layer_groups([l - 1 for l in layers])
+        self.moving = {}
+
+
+def generate_dist(model: DistStagedLlama, prompts: list[list[int]], joins: list[int], n_gen: int,
+                  reconfig: tuple[int, dict] | None = None,
+                  switch_at: int | None = None) -> list[list[int]]:
+    """generate() with the stages in separate processes; every rank returns the tokens."""
+    with model.on_stream():
+        B = len(prompts)
+        outs: list[list[int]] = [[] for _ in range(B)]
+        t = 0
+        while any(len(o) < n_gen for o in outs):
+            act = [b for b in range(B) if joins[b] <= t and len(outs[b]) < n_gen]
+            if act:
+                toks, poss = [], []
+                for b in act:
+                    p = t - joins[b]
+                    toks.append(prompts[b][p] if p < len(prompts[b]) else outs[b][-1])
+                    poss.append(p)
+                nxt = model.step_tokens([f"seq{b}" for b in act], toks)
+                for b, p, n in zip(act, poss, nxt):
+                    if p >= len(prompts[b]) - 1:
+                        outs[b].append(int(n))
+            if reconfig is not None and t == reconfig[0]:
+                model.start_reconfig(reconfig[1])
+            elif model.moving:
+                model.pump()
+            if switch_at is not None and t == switch_at:
+                model.switch()
+            t += 1
+        return outs

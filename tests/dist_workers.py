@@ -1,0 +1,32 @@
+"""Stage processes of tests/test_gpu_dist_llama.py: three ranks on cuda:0, gloo for
+activations (NCCL needs distinct GPUs), the cross-process push for KV patches."""
+
+import os
+
+PROMPTS = [[3, 17, 400, 9, 77], [5] * 12, list(range(100, 123)), [1000, 2, 2, 2, 999, 64, 31, 8]]
+JOINS = [0, 2, 5, 9]
+N_GEN = 24
+CONF_A = {1: [1, 2], 2: [3, 4]}          # PP2 on GPUs 1-2, GPU 3 idle (zero-layer extension)
+CONF_B = {1: [1], 2: [2, 3], 3: [4]}     # PP3 (BASELINE configs[0])
+
+
+def stage(rank, world, port, prefix, q, live):
+    try:
+        import torch
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2604_12171_b200.llama import (DistStagedLlama, LlamaConfig, generate_dist,
+                                                  init_weights)
+        cfg = LlamaConfig()
+        m = DistStagedLlama(cfg, init_weights(cfg, 0), CONF_A, rank, channel_prefix=prefix)
+        outs = generate_dist(m, PROMPTS, JOINS, N_GEN,
+                             reconfig=(10, CONF_B) if live else None,
+                             switch_at=20 if live else None)
+        q.put((rank, outs, sorted(m.store.resident_groups)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
