@@ -30,6 +30,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
 HBM_FALLBACK_GBS = 6650.0
+NVLINK_GBS = 900.0
 
 
 def parse():
@@ -186,9 +187,12 @@ def run_reference(args, wl, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
-def profile_traffic(kernel: str, n_q: int | None = None):
+def profile_traffic(kernel: str, n_q: int | None = None, wl=None):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` at this bench's
-    shape, from the committed ncu capture (profiles/traffic_r1.json, tools/gpu_prof.sh)."""
+    shape, from the committed ncu capture (profiles/traffic_r1.json, tools/gpu_prof.sh);
+    None when the run's shape is not the captured one (B = 256, ctx = 2048)."""
+    if wl is not None and (wl.batch, wl.ctx) != (256, 2048):
+        return None
     try:
         rows = json.loads((ROOT / "profiles" / "traffic_r1.json").read_text())
     except Exception:
@@ -206,7 +210,8 @@ def config_of(wl, world: int) -> dict:
             "kv_bytes_per_token_layer": wl.cell_bytes,
             "bytes_per_step": wl.payload_bytes,
             "l2": "inputs (>17 GB per step) exceed the 126 MB L2; no flush needed",
-            "parallelism": f"{world} independent pairs (1 per GPU)"}
+            "parallelism": (f"ring of {world} cross-process pairs (rank r -> r+1, one per GPU)"
+                            if world > 1 else "1 pair on one GPU")}
 
 
 # ------------------------------------------------------------------------------ GPU legs
@@ -225,7 +230,7 @@ def main() -> None:
     from paper_2604_12171_b200 import _native as N
     from paper_2604_12171_b200.perf import PatchRig, read_peaks
 
-    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(dev)
     lib = N.lib()
     peaks = read_peaks(ROOT / "MEASURED_PEAKS.json")
@@ -237,10 +242,18 @@ def main() -> None:
     rig.use_stream(stream.cuda_stream)
     rig.fill()
     K, W = args.steps, args.warmup
+    # N > 1: a ring of cross-process pairs, rank r -> r+1 over the imported peer pools
+    # (NVLink stores); N = 1: the pair's destination is a second store on this GPU
+    ring = None
+    if world > 1:
+        from paper_2604_12171_b200.dist import RingPair
+        ring = RingPair(rig, rank, world, f"bench-{os.environ.get('MASTER_PORT', '0')}")
+        ring.use_stream(stream.cuda_stream)
+    stepper = ring if ring is not None else rig
 
     # ---- value: bulk KV-patch rounds, everything resident in HBM
     for _ in range(W):
-        rig.bulk_round()
+        stepper.bulk_round()
     torch.cuda.synchronize()
     N.check(lib.pl_timing_reset())
     N.check(lib.pl_timing_enable(1))
@@ -253,7 +266,7 @@ def main() -> None:
         t0.record(stream)
         keys_total = 0
         for _ in range(K):
-            keys, cells = rig.bulk_round()
+            keys, cells = stepper.bulk_round()
             keys_total += keys
         t1.record(stream)
         torch.cuda.synchronize()
@@ -267,13 +280,23 @@ def main() -> None:
     push_ms, push_n = N.timing("patch_push")
     drain_ms, drain_n = N.timing("drain")
     push_avg = push_ms / max(push_n, 1)
-    # algorithmic HBM bytes of one push launch: payload read + payload write + 2 x 8 B fp
-    alg_bytes = 2 * wl.payload_bytes + 2 * 8 * wl.batch * wl.ctx * len(wl.mig_groups)
+    if ring is None:
+        # algorithmic HBM bytes of one push launch: payload read + write + 2 x 8 B fp
+        alg_bytes = 2 * wl.payload_bytes + 2 * 8 * wl.batch * wl.ctx * len(wl.mig_groups)
+        bound, peak, psrc, traffic = "hbm", hbm_peak, peak_src, profile_traffic("copy_kernel<2>", None, wl)
+    elif world <= torch.cuda.device_count():
+        # bytes each GPU sends over NVLink per launch (it receives as many concurrently)
+        alg_bytes = wl.payload_bytes + 8 * wl.batch * wl.ctx * len(wl.mig_groups)
+        bound, peak, psrc, traffic = "nvlink", NVLINK_GBS, "nominal 900 GB/s per direction", None
+    else:
+        # ranks share a GPU (functional run of the ring on a smaller box): HBM-bound
+        alg_bytes = 2 * wl.payload_bytes + 2 * 8 * wl.batch * wl.ctx * len(wl.mig_groups)
+        bound, peak, psrc, traffic = "hbm (ranks share one GPU)", hbm_peak, peak_src, None
     achieved = alg_bytes / (push_avg / 1e3) / 1e9
     roofline = {"kernel": "copy_kernel<2> (K4 gather -> K5 scatter, fused push)",
-                "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
-                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                "traffic": profile_traffic("copy_kernel<2>"), "alg_bytes_per_launch": alg_bytes,
+                "bound": bound, "achieved": round(achieved, 1), "peak": peak,
+                "peak_source": psrc, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                 "avg_launch_ms": round(push_avg, 4),
                 "share_of_step": round(push_ms / ms, 4) if ms else None,
                 "drain_ms_per_step": round(drain_ms / max(K, 1), 4)}
@@ -291,11 +314,13 @@ def main() -> None:
 
     # ---- C5: dirty-rate x block-size sweep of one patch round (configs[4], 1 GPU)
     sweep = None
-    if not args.skip_sweep:
+    if not args.skip_sweep and rank == 0:
         from paper_2604_12171_b200.perf import c5_sweep
         sweep = c5_sweep(dev)
 
     # ---- e2e: KV arrives from pinned host memory every step, result read back
+    if ring is not None:
+        ring.close()
     e2e = None if args.skip_e2e else measure_e2e(rig, stream, torch, wl, K, world)
     rig.close()
 
@@ -402,7 +427,7 @@ def measure_decode(rig, stream, torch, wl, hbm_peak, K, W, n_q=None) -> dict:
             "n_kv": wl.n_kv, "head_dim": wl.head_dim,
             "roofline": {"kernel": "paged_attn_mma_kernel<128,8> (TMA 128B-swizzled ring, "
                                    "mma.sync bf16, +combine)", "bound": "hbm",
-                         "traffic": profile_traffic("paged_attn_mma", n_q),
+                         "traffic": profile_traffic("paged_attn_mma", n_q, wl),
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4),
                          "alg_bytes_per_launch": kv_bytes_layer + q_bytes,

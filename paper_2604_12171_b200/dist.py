@@ -36,35 +36,63 @@ _HDR = struct.Struct("<QI")
 
 
 class Channel:
-    """Local socket between two processes; ``name`` is shared, one side is the server."""
+    """Local socket between two processes; ``name`` is shared, one side is the server.
+
+    ``Channel(name, server)`` blocks until connected.  Ranks that are server of one pair
+    and client of another (a ring of pairs) use ``Channel.listen`` first, then
+    ``Channel.connect``, then ``Listener.accept`` so no rank waits in accept while its
+    own peer waits in accept too."""
+
+    class Listener:
+        def __init__(self, name: str, timeout: float) -> None:
+            self.ls = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            self.ls.bind("\0pipelive-" + name)   # Linux abstract namespace: no file
+            self.ls.listen(1)
+            self.ls.settimeout(timeout)
+
+        def accept(self) -> "Channel":
+            sock, _ = self.ls.accept()
+            self.ls.close()
+            return Channel._wrap(sock)
+
+    @classmethod
+    def listen(cls, name: str, timeout: float = 120.0) -> "Channel.Listener":
+        return cls.Listener(name, timeout)
+
+    @classmethod
+    def connect(cls, name: str, timeout: float = 120.0) -> "Channel":
+        deadline = time.time() + timeout
+        while True:
+            s = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            try:
+                s.connect("\0pipelive-" + name)
+                return cls._wrap(s)
+            except OSError:
+                s.close()
+                if time.time() > deadline:
+                    raise
+                time.sleep(0.02)
+
+    @classmethod
+    def _wrap(cls, sock) -> "Channel":
+        ch = cls.__new__(cls)
+        sock.settimeout(None)
+        ch.sock = sock
+        return ch
 
     def __init__(self, name: str, server: bool, timeout: float = 120.0) -> None:
-        addr = "\0pipelive-" + name   # Linux abstract namespace: no file to clean up
-        if server:
-            ls = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-            ls.bind(addr)
-            ls.listen(1)
-            ls.settimeout(timeout)
-            self.sock, _ = ls.accept()
-            ls.close()
-        else:
-            deadline = time.time() + timeout
-            while True:
-                s = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-                try:
-                    s.connect(addr)
-                    break
-                except OSError:
-                    s.close()
-                    if time.time() > deadline:
-                        raise
-                    time.sleep(0.02)
-            self.sock = s
-        self.sock.settimeout(None)
+        ch = (Channel.listen(name, timeout).accept() if server
+              else Channel.connect(name, timeout))
+        self.sock = ch.sock
+
+    MAX_FDS = 250   # SCM_RIGHTS carries at most 253 descriptors per message
 
     def send(self, obj, fds=()) -> None:
         data = pickle.dumps(obj)
-        socket.send_fds(self.sock, [_HDR.pack(len(data), len(fds))], list(fds))
+        fds = list(fds)
+        socket.send_fds(self.sock, [_HDR.pack(len(data), len(fds))], fds[: self.MAX_FDS])
+        for i in range(self.MAX_FDS, len(fds), self.MAX_FDS):
+            socket.send_fds(self.sock, [b"+"], fds[i:i + self.MAX_FDS])
         self.sock.sendall(data)
 
     def recv(self):
@@ -75,6 +103,11 @@ class Channel:
                 raise ConnectionError("channel closed")
             hdr += more
         n, n_fds = _HDR.unpack(hdr)
+        fds = list(fds)
+        while len(fds) < n_fds:
+            mark, more, _, _ = socket.recv_fds(self.sock, 1, self.MAX_FDS)
+            assert mark == b"+", mark
+            fds += more
         buf = bytearray()
         while len(buf) < n:
             chunk = self.sock.recv(n - len(buf))
@@ -175,6 +208,13 @@ class PatchReceiver:
 
     def serve(self) -> bool:
         """One round; False once the sender closed the pair."""
+        if not self.serve_rows():
+            return False
+        self.serve_ack()
+        return True
+
+    def serve_rows(self) -> bool:
+        """First half of a round: reserve the drained rows, publish table/pool updates."""
         msg, _ = self.chan.recv()
         if msg[0] == "close":
             return False
@@ -194,14 +234,19 @@ class PatchReceiver:
         self.chan.send(("reserved", done.value, err, update), fds)
         for fd in fds:
             os.close(fd)
-        ack, _ = self.chan.recv()
-        assert ack[0] == "applied", ack[0]
         self.rounds += 1
         self.items_reserved += done.value
-        if err is not None:
-            from .kvstore import _ERRORS
-            raise _ERRORS.get(err[0], N.NativeError)(err[1])
+        self._err = err
         return True
+
+    def serve_ack(self) -> None:
+        """Second half: the sender's cells are in this store once "applied" arrives."""
+        ack, _ = self.chan.recv()
+        assert ack[0] == "applied", ack[0]
+        if self._err is not None:
+            from .kvstore import _ERRORS
+            err, self._err = self._err, None
+            raise _ERRORS.get(err[0], N.NativeError)(err[1])
 
 
 class PatchSender:
@@ -228,6 +273,11 @@ class PatchSender:
 
     def round(self) -> tuple[int, int]:
         """Drain + push one patch; returns (keys, cells) like MigrationStream._drain."""
+        self.begin()
+        return self.finish()
+
+    def begin(self) -> None:
+        """Drain (host snapshot + K3) and send the rows to the receiver."""
         rank = self.rank_fn()
         keys, cells, n = C.c_int64(), C.c_int64(), C.c_int64()
         N.check(N.lib().pl_patch_drain_rows(self.patch.h, N.ptr(rank), len(rank), C.byref(keys),
@@ -237,6 +287,10 @@ class PatchSender:
                 np.empty(m, np.int64))
         N.check(N.lib().pl_patch_rows(self.patch.h, *(N.ptr(x) for x in rows), m))
         self.chan.send(("rows", rows))
+        self._pending = (keys.value, cells.value)
+
+    def finish(self) -> tuple[int, int]:
+        """Receive the reservation, push the cells into the remote pools, acknowledge."""
         msg, fds = self.chan.recv()
         assert msg[0] == "reserved", msg[0]
         _, done, err, update = msg
@@ -250,9 +304,10 @@ class PatchSender:
         if err is not None:
             from .kvstore import _ERRORS
             raise _ERRORS.get(err[0], N.NativeError)(err[1])
-        self.keys += keys.value
-        self.cells += cells.value
-        return keys.value, cells.value
+        keys, cells = self._pending
+        self.keys += keys
+        self.cells += cells
+        return keys, cells
 
     def dirty_keys(self) -> int:
         return self.patch.dirty_keys()
@@ -289,3 +344,42 @@ class StageLink:
         t = torch.empty(shape, dtype=dtype)
         self.dist.recv(t, src, group=self.group)
         return t.to(device)
+
+
+class RingPair:
+    """Bench topology for N > 1 ranks (one per GPU): rank r's migrating groups stream to
+    rank r+1, so every GPU sends one pair and receives one pair at the same time (N
+    concurrent distinct-source pairs over NVSwitch).  The source is the
+    PatchRig's stage store; the receiving store holds the previous rank's groups."""
+
+    def __init__(self, rig, rank: int, world: int, tag: str) -> None:
+        from .kvstore import KvStore
+
+        wl = rig.wl
+        nxt, prv = (rank + 1) % world, (rank - 1) % world
+        cap = wl.batch * (wl.blocks_per_req + 2) + 64
+        self.dst = KvStore(100 + rank, wl.k, wl.s, cap, (), num_groups=wl.model_groups,
+                           cell_bytes=wl.cell_bytes, device=rig.device, registry=rig.registry)
+        lis = Channel.listen(f"{tag}-{prv}-{rank}")
+        out = Channel.connect(f"{tag}-{rank}-{nxt}")
+        inn = lis.accept()
+        self.rx = PatchReceiver(self.dst, wl.mig_groups, inn)          # sends hello
+        self.tx = PatchSender(rig.src, wl.mig_groups, wl.k, out, rig.registry.rank)
+        self.payload_bytes = wl.payload_bytes
+
+    def use_stream(self, stream_ptr: int) -> None:
+        N.check(N.lib().pl_store_set_stream(self.dst._h, C.c_void_p(stream_ptr)))
+
+    def bulk_round(self) -> tuple[int, int]:
+        """One ring step: every live cell of the migrating groups, both directions."""
+        self.tx.seed()
+        self.tx.begin()
+        self.rx.serve_rows()
+        keys, cells = self.tx.finish()
+        self.rx.serve_ack()
+        return keys, cells
+
+    def close(self) -> None:
+        N.check(N.lib().pl_patch_set_active(self.tx.patch.h, 0))
+        self.tx.close()
+        assert not self.rx.serve()
