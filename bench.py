@@ -309,6 +309,9 @@ def main() -> None:
     decode = measure_decode(rig, stream, torch, wl, hbm_peak, K, W)
     decode_70b = measure_decode(rig, stream, torch, wl, hbm_peak, K, W, n_q=64)
 
+    # ---- AddLayerWeights on the copy engine: the 8 migrating layers' weights (0.436 GB each)
+    wstage = measure_weight_stage(rig, stream, torch, wl, dev)
+
     # ---- resize latency: post-commit cleanup on the source (drop groups, shrink, regrow)
     resize = measure_resize(rig, stream, torch, wl)
 
@@ -341,6 +344,7 @@ def main() -> None:
         "decode": decode,
         "decode_70b_shape": decode_70b,
         "resize": resize,
+        "weight_stage": wstage,
         "c5_sweep": sweep,
     }
     print(json.dumps(line), flush=True)
@@ -432,6 +436,44 @@ def measure_decode(rig, stream, torch, wl, hbm_peak, K, W, n_q=None) -> dict:
                          "frac": round(achieved / hbm_peak, 4),
                          "alg_bytes_per_launch": kv_bytes_layer + q_bytes,
                          "avg_launch_ms": round(per_launch, 4)}}
+
+
+def measure_weight_stage(rig, stream, torch, wl, dev) -> dict:
+    """Stage the weights of the migrating layers (8 x 0.436 GB for the 8B shape, SURVEY
+    §8 sizes) from pinned host memory on the low-priority copy stream, alone and while
+    the stage keeps decoding on its compute stream (inference must not yield)."""
+    from paper_2604_12171_b200.staging import LayerWeightStager
+
+    layer_bytes = 436 * 1000 * 1000
+    n_layers = len(wl.mig_groups) * wl.k
+    host = {l: {"w": torch.empty(layer_bytes, dtype=torch.uint8, pin_memory=True)}
+            for l in range(n_layers)}
+    for l in host:
+        host[l]["w"].fill_(l)
+    st = LayerWeightStager(dev, host)
+    t0 = time.perf_counter()
+    st.stage_layers(range(n_layers))
+    st.wait()
+    ms_alone = (time.perf_counter() - t0) * 1e3
+    st.evict_layers(range(n_layers))
+    torch.cuda.synchronize()
+    # decode alone vs decode while staging
+    dec = lambda: measure_decode(rig, stream, torch, wl, 1.0, 5, 1)["ms_per_step"]  # noqa: E731
+    d_alone = dec()
+    t0 = time.perf_counter()
+    st.stage_layers(range(n_layers))
+    d_during = dec()
+    still = st.staging_active()
+    st.wait()
+    ms_overlap = (time.perf_counter() - t0) * 1e3
+    st.evict_layers(range(n_layers))
+    total = n_layers * layer_bytes
+    return {"layers": n_layers, "bytes": total, "ms": round(ms_alone, 2),
+            "gbs": round(total / ms_alone / 1e6, 2),
+            "decode_ms_per_step_alone": d_alone, "decode_ms_per_step_during_stage": d_during,
+            "stage_ms_with_decode": round(ms_overlap, 2), "stage_still_running_after_decode": still,
+            "note": "pinned host -> HBM, cudaMemcpyAsync in 64 MiB chunks on a lowest-priority "
+                    "stream (copy engine); decode runs on its own stream"}
 
 
 def measure_e2e(rig, stream, torch, wl, K, world) -> dict:

@@ -81,7 +81,9 @@ class LlamaCompute:
     """The math of one decode step, layer by layer, over whichever store owns a layer."""
 
     def __init__(self, cfg: LlamaConfig, weights: dict[str, np.ndarray], device: int,
-                 registry: RequestRegistry, stream) -> None:
+                 registry: RequestRegistry, stream, layers=None) -> None:
+        """`layers` (1-based, default all): which layers' weights go to the device now;
+        the embedding, final norm and LM head always do."""
         import torch
 
         self.torch = torch
@@ -89,7 +91,12 @@ class LlamaCompute:
         self.registry = registry
         self.stream = stream
         dev = torch.device("cuda", device)
-        self.w = {k: torch.from_numpy(v).to(dev) for k, v in weights.items()}
+        keep = None if layers is None else {f"l{l - 1}" for l in layers}
+
+        def wanted(k: str) -> bool:   # per-layer keys are "l<i>.<name>"
+            return keep is None or "." not in k or k.split(".", 1)[0] in keep
+
+        self.w = {k: torch.from_numpy(v).to(dev) for k, v in weights.items() if wanted(k)}
 
     def begin(self, rids: list, positions: list[int], device) -> dict:
         """Per-step state: request rows, context lengths after this token, RoPE tables."""
@@ -352,9 +359,22 @@ class DistStagedLlama:
         self.group = group
         self.registry = registry or RequestRegistry()
         self.stream = torch.cuda.Stream(device=device)
-        self.compute = LlamaCompute(cfg, weights, device, self.registry, self.stream)
         self.link = StageLink(group)
         self.owner = {l: g for g, ls in config.items() for l in ls}
+        own_layers = [l for l, g in self.owner.items() if g == self.gpu]
+        self.compute = LlamaCompute(cfg, weights, device, self.registry, self.stream,
+                                    layers=own_layers)
+        # every layer's weights sit in pinned host memory; arriving layers are staged on
+        # a copy engine during the migration and gate the switch (coordinator.py:239-240)
+        from .staging import LayerWeightStager
+
+        host = {}
+        for l in range(1, cfg.n_layers + 1):
+            pre = f"l{l - 1}."
+            host[l] = {k: torch.from_numpy(v).pin_memory() for k, v in weights.items()
+                       if k.startswith(pre)}
+        self.stager = LayerWeightStager(device, host,
+                                        is_layer_committed=lambda l: self.owner.get(l) == self.gpu)
         mine = [l - 1 for l, g in self.owner.items() if g == self.gpu]
         self.store = KvStore(self.gpu, 1, tokens_per_block, capacity_blocks, mine,
                              num_groups=cfg.n_layers, cell_bytes=cfg.cell_bytes, device=device,
@@ -415,6 +435,9 @@ class DistStagedLlama:
                 moves.setdefault((self.owner[l], g), []).append(l)
         self.moving = moves
         self.target = new_owner
+        arriving = [l for (src, dst), ls in moves.items() if dst == self.gpu for l in ls]
+        if arriving:
+            self.stager.stage_layers(arriving)
         # channels are set up in one global pair order on every rank (no wait cycles)
         for (src, dst) in self._pairs():
             groups = [l - 1 for l in moves[(src, dst)]]
@@ -437,6 +460,13 @@ class DistStagedLlama:
                 assert self.receivers[pair].serve()
 
     def switch(self) -> None:
+        # the commit waits for the arriving layers' weights (coordinator.py:239-240)
+        self.stager.wait()
+        self.stager.make_current_wait(self.stream)
+        for (src, dst), layers in self.moving.items():
+            if dst == self.gpu:
+                for l in layers:
+                    self.compute.w.update(self.stager.resident[l])
         self.pump()                     # residual patch of every pair
         for pair in self._pairs():
             if pair in self.senders:
@@ -448,6 +478,11 @@ class DistStagedLlama:
                 self.owner[l] = dst
             if src == self.gpu:
                 self.store.drop_layer_groups([l - 1 for l in layers])
+                # the leaving layers' weights go too (post-commit evict, coordinator.py:340-354)
+                for l in layers:
+                    for k in [k for k in self.compute.w if k.startswith(f"l{l - 1}.")]:
+                        del self.compute.w[k]
+                self.stager.evict_layers([l for l in layers if l in self.stager.resident])
         self.moving = {}
 
 
