@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-sweep", action="store_true")
+    ap.add_argument("--skip-c3", action="store_true")
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--ctx", type=int, default=2048)
     return ap.parse_args()
@@ -325,7 +326,17 @@ def main() -> None:
     if ring is not None:
         ring.close()
     e2e = None if args.skip_e2e else measure_e2e(rig, stream, torch, wl, K, world)
-    rig.close()
+    rig.destroy()
+    if ring is not None:
+        ring.dst.close()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    # ---- C3: 70B-shape stage with HBM pre-filled, live shrink (K6 relocation) + grow
+    c3 = None
+    if not args.skip_c3 and rank == 0:
+        from paper_2604_12171_b200.perf import c3_live_resize
+        c3 = c3_live_resize(dev)
 
     if rank != 0:
         return
@@ -346,6 +357,7 @@ def main() -> None:
         "resize": resize,
         "weight_stage": wstage,
         "c5_sweep": sweep,
+        "c3_live_resize": c3,
     }
     print(json.dumps(line), flush=True)
 

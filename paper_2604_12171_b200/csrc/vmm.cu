@@ -400,7 +400,7 @@ void Arena::trim(size_t bytes, cudaStream_t st) {
   if (keep >= chunks.size()) return;
   std::vector<CUmemGenericAllocationHandle> tail(chunks.begin() + (long)keep, chunks.end());
   chunks.resize(keep);
-  const size_t n_tail = tail.size();
+  const size_t n_tail = tail.size();  // before the move (unspecified evaluation order)
   tail_job = rc->submit(st, va + keep * chunk_bytes, n_tail * chunk_bytes, std::move(tail),
                         0, 0, /*immediate=*/false);
   if (trace_on())
@@ -411,8 +411,10 @@ void Arena::trim(size_t bytes, cudaStream_t st) {
 void Arena::release(cudaStream_t st) {
   if (!va) return;
   reclaim_tail();
-  rc->submit(st, va, chunks.size() * chunk_bytes, std::move(chunks), va, va_bytes,
-             /*immediate=*/true);
+  // the byte count must be taken before `chunks` is moved into the by-value parameter
+  // (argument evaluation order is unspecified)
+  const size_t mapped = chunks.size() * chunk_bytes;
+  rc->submit(st, va, mapped, std::move(chunks), va, va_bytes, /*immediate=*/true);
   chunks.clear();
   va = 0;
   va_bytes = 0;

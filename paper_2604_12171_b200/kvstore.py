@@ -294,6 +294,11 @@ class KvStore:
         self.tables = TablesView(self)
 
     def __del__(self) -> None:
+        self.close()
+
+    def close(self) -> None:
+        """Destroy the native store now (device pools return to the driver once the
+        reclaimer thread has unmapped them; the destructor joins it)."""
         h = getattr(self, "_h", None)
         if h is not None and N._lib is not None:
             N._lib.pl_store_destroy(h)

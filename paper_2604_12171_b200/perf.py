@@ -164,6 +164,119 @@ class PatchRig:
     def close(self) -> None:
         self.patch.close()
 
+    def destroy(self) -> None:
+        self.close()
+        self.src.close()
+        self.dst.close()
+
+
+def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040) -> dict:
+    """BASELINE configs[2] at one GPU: the source stage of a Llama-3-70B PP 4 -> 8 boundary
+    shift with HBM pre-filled by KV cache.
+
+    Geometry from the reference's own max_blocks (cluster.py:180-201) with M = 180 GB,
+    u = 0.9, 16-token blocks, k = 4 (unit 256 KiB + header): the stage holds layers 1-20
+    (5 groups) at B = max_blocks(20) = 97,488 blocks.  In the target it keeps layers 1-12,
+    sends 13-20 (groups 3, 4) to a new GPU and receives layers 21-24 (group 5) from its
+    neighbour, so |C_cur u C_tgt| = 24 layers and Phase 2 must shrink to
+    b_shrink = max_blocks(24) = 76,888 (coordinator.py:103-110, 189-201) while ~17 GB
+    of live KV sits above that line; after the commit it drops groups 3, 4 and grows to
+    b_new = max_blocks(16) = 128,387 (coordinator.py:340-354).  The migrating groups are
+    pushed to a destination store on the same GPU (HBM-bound here, NVLink across GPUs)."""
+    import torch
+
+    from .cluster import GpuSpec, ModelSpec, max_blocks
+
+    gran = 16 * 4096 * 4
+    gpu = GpuSpec(1, 180 * 10 ** 9 // gran * gran, 8e12, 1e-6, 1e-6, gran)
+    model = ModelSpec(80, 1_711_000_000, 4096, 4)
+    b_cur, b_shrink, b_new = (max_blocks(gpu, n, model, 0.9) for n in (20, 24, 16))
+    reg = RequestRegistry()
+    out: dict = {"b_cur": b_cur, "b_shrink": b_shrink, "b_new": b_new}
+    src = KvStore(1, 4, 16, b_cur, (0, 1, 2, 3, 4), num_groups=20, cell_bytes=4096,
+                  device=device, registry=reg)
+    per_req = ceil(ctx / 16)
+    hs = [reg.handle(rid(i)) for i in range(fill_reqs)]
+    for c0 in range(0, fill_reqs, 64):
+        chunk = hs[c0:c0 + 64]
+        append_batch(src, [h for h in chunk for _ in range(5)], [g for _ in chunk for g in range(5)],
+                     [ctx] * (5 * len(chunk)),
+                     [stable_hash(rid(c0 + i), g) for i in range(len(chunk)) for g in range(5)])
+    src.sync()
+    # holes in the low slots: the shrink must relocate the live blocks above b_shrink
+    freed = 0
+    i = 0
+    while src.used_blocks > b_shrink - 256:
+        src.free_request(rid(i))
+        freed += 1
+        i += 2
+    src.sync()
+    torch.cuda.synchronize(device)
+    out["filled_blocks"] = fill_reqs * per_req
+    out["live_blocks"] = src.used_blocks
+    out["kv_bytes_live"] = src.used_blocks * 5 * src.info()["unit_bytes"]
+    # Phase 2: compact + shrink with relocation, then map the incoming group 5
+    t0 = time.perf_counter()
+    src.compact()
+    src.resize(b_shrink)
+    src.sync()
+    out["phase2_shrink_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    out["phase2_shrink_stats"] = src.last_resize_stats()
+    free_gb = lambda: round(torch.cuda.mem_get_info(device)[0] / 1e9, 1)  # noqa: E731
+    out["free_gb_after_shrink"] = free_gb()
+    t0 = time.perf_counter()
+    src.resident_groups.add(5)
+    src.sync()
+    out["map_incoming_group_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    # Phase 3: bulk + one decode round of the two leaving groups
+    dst = KvStore(2, 4, 16, src.used_blocks + 256, (), num_groups=20, cell_bytes=4096,
+                  device=device, registry=reg)
+    dst.resident_groups |= {3, 4}
+    patch = NativePatch(src, (3, 4), 4)
+    patch.seed()
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    keys, cells = patch.push(dst, reg.rank())
+    src.sync()
+    dst.sync()
+    t = time.perf_counter() - t0
+    out["bulk_patch"] = {"keys": keys, "payload_bytes": cells * 4096, "ms": round(t * 1e3, 3),
+                         "gbs": round(cells * 4096 / t / 1e9, 1)}
+    live = [h for h in hs if src._has_table(h)]
+    names = [reg.name(h) for h in live]
+    append_batch(src, [h for h in live for _ in range(5)], [g for _ in live for g in (0, 1, 2, 3, 4)],
+                 [1] * (5 * len(live)), [stable_hash(n, g) for n in names for g in range(5)],
+                 mark=True)
+    src.sync()
+    t0 = time.perf_counter()
+    keys, cells = patch.push(dst, reg.rank())
+    src.sync()
+    dst.sync()
+    out["residual_patch"] = {"keys": keys, "ms": round((time.perf_counter() - t0) * 1e3, 3)}
+    patch.close()
+    out["free_gb_during_patch"] = free_gb()
+    dst.close()   # the destination is another GPU on hardware; free its HBM here
+    # post-commit: drop the leaving groups, grow to b_new (re-maps their chunks)
+    v0 = src.vmm_stats()
+    t0 = time.perf_counter()
+    src.drop_layer_groups([3, 4])
+    out["drop_groups_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    out["free_gb_before_grow"] = free_gb()
+    import sys
+    print(out, file=sys.stderr, flush=True)
+    t0 = time.perf_counter()
+    src.resize(b_new)
+    src.sync()
+    out["grow_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    v1 = src.vmm_stats()
+    out["grow_stats"] = {**src.last_resize_stats(),
+                         **{k: v1[k] - v0[k] for k in ("tail_reused_chunks", "cache_reused_chunks",
+                                                      "created_chunks")}}
+    out["mapped_bytes_end"] = src.info()["mapped_bytes"]
+    src.reclaim()
+    src.close()
+    return out
+
 
 def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16, 32, 64, 128),
              batch: int = 64, ctx: int = 2048, rounds: int = 3, seed: int = 0) -> list[dict]:
