@@ -251,19 +251,19 @@ int pl_store_blocks(pl_store* st, int64_t* ids, int32_t* owner, int32_t* slot, i
 }
 int pl_store_block_occupied(pl_store* st, int64_t block_id, int64_t* out) {
   return guard([&] {
-    auto it = st->s->by_id.find(block_id);
-    if (it == st->s->by_id.end()) pl::fail(PL_E_INVALID, "unknown block id");
-    *out = st->s->block_occupied(it->second.slot);
+    const pl::BlockRec* b = st->s->by_id.find(block_id);
+    if (!b) pl::fail(PL_E_INVALID, "unknown block id");
+    *out = st->s->block_occupied(b->slot);
   });
 }
 int pl_store_block_occupancy(pl_store* st, int64_t block_id, int group, uint64_t* out, int cap,
                              int* n_words) {
   return guard([&] {
-    auto it = st->s->by_id.find(block_id);
-    if (it == st->s->by_id.end()) pl::fail(PL_E_INVALID, "unknown block id");
+    const pl::BlockRec* b = st->s->by_id.find(block_id);
+    if (!b) pl::fail(PL_E_INVALID, "unknown block id");
     if (group < 0 || group >= st->s->n_model_groups) pl::fail(PL_E_INVALID, "group out of range");
     *n_words = st->s->occ_words;
-    const uint64_t* w = st->s->occ_ptr(it->second.slot, group);
+    const uint64_t* w = st->s->occ_ptr(b->slot, group);
     for (int i = 0; i < st->s->occ_words && i < cap; ++i) out[i] = w[i];
   });
 }

@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <cstdint>
@@ -156,6 +157,74 @@ struct ReqTable {
   std::vector<int32_t> written_order; // groups in dict insertion order
 };
 
+// block id -> record.  Ids are serials (kvstore.py:111-119): dense and never reused, so
+// a vector with a presence flag replaces a hash map on the allocation hot path.
+struct BlockIndex {
+  std::vector<BlockRec> v;
+  std::vector<uint8_t> live;
+  BlockRec& at(int64_t id) {
+    if (id < 0 || id >= (int64_t)v.size() || !live[(size_t)id]) throw std::out_of_range("block id");
+    return v[(size_t)id];
+  }
+  const BlockRec& at(int64_t id) const {
+    if (id < 0 || id >= (int64_t)v.size() || !live[(size_t)id]) throw std::out_of_range("block id");
+    return v[(size_t)id];
+  }
+  void put(int64_t id, const BlockRec& b) {
+    if (id >= (int64_t)v.size()) {
+      v.resize(std::max<size_t>((size_t)id + 1, v.size() * 2));
+      live.resize(v.size(), 0);
+    }
+    v[(size_t)id] = b;
+    live[(size_t)id] = 1;
+  }
+  void erase(int64_t id) {
+    if (id >= 0 && id < (int64_t)v.size()) live[(size_t)id] = 0;
+  }
+  const BlockRec* find(int64_t id) const {
+    return id >= 0 && id < (int64_t)v.size() && live[(size_t)id] ? &v[(size_t)id] : nullptr;
+  }
+};
+
+// The free block ids with "lowest id first" allocation (kvstore.py:121-128: a lazily
+// invalidated min-heap).  A bitset over the dense serial ids plus a cursor at or below
+// the lowest set bit: insert/erase O(1), pop_min amortised O(1) word scans.
+struct FreeIds {
+  std::vector<uint64_t> bits;
+  int64_t cursor = 0;  // no free id below this
+  int64_t n = 0;
+  bool empty() const { return n == 0; }
+  void insert(int64_t id) {
+    const size_t w = (size_t)(id >> 6);
+    if (w >= bits.size()) bits.resize(std::max(w + 1, bits.size() * 2), 0);
+    const uint64_t m = 1ull << (id & 63);
+    if (!(bits[w] & m)) {
+      bits[w] |= m;
+      ++n;
+    }
+    if (id < cursor) cursor = id;
+  }
+  void erase(int64_t id) {
+    const size_t w = (size_t)(id >> 6);
+    if (w >= bits.size()) return;
+    const uint64_t m = 1ull << (id & 63);
+    if (bits[w] & m) {
+      bits[w] &= ~m;
+      --n;
+    }
+  }
+  int64_t pop_min() {  // requires !empty()
+    size_t w = (size_t)(cursor >> 6);
+    uint64_t x = bits[w] & (~0ull << (cursor & 63));
+    while (!x) x = bits[++w];
+    const int64_t id = (int64_t)(w << 6) + __builtin_ctzll(x);
+    bits[w] &= ~(1ull << (id & 63));
+    --n;
+    cursor = id + 1;
+    return id;
+  }
+};
+
 struct Patch;
 struct Interval { int64_t a, b; };  // [a, b)
 
@@ -170,8 +239,8 @@ struct Store {
 
   // block manager state (reference semantics)
   std::vector<int64_t> blocks;                    // list order
-  std::unordered_map<int64_t, BlockRec> by_id;
-  std::set<int64_t> free_ids;                     // == lazily invalidated heap
+  BlockIndex by_id;
+  FreeIds free_ids;                               // == lazily invalidated heap
   std::vector<int64_t> slot_block;                // slot -> block id or -1
   int64_t serial = 0, used = 0, occupied = 0, ins_counter = 0;
   std::vector<ReqTable> tables;                   // indexed by request handle
@@ -197,6 +266,7 @@ struct Store {
   std::vector<int32_t> h_table, h_owner, h_owner_idx;
   struct Delta { int32_t which; int64_t idx; int32_t val; };
   std::vector<Delta> deltas;
+  std::vector<uint8_t> table_q, owner_q;  // flush(): entries already queued this flush
   std::vector<int32_t> released_slots;  // dirty bits to clear in attached patches
   // scratch
   void* d_scratch = nullptr;

@@ -183,7 +183,18 @@ __global__ void unit_move_kernel(const uint64_t* bases, const int32_t* groups, i
     const uint8_t* base = reinterpret_cast<const uint8_t*>(bases[groups[job % n_groups]]);
     const int4* src = reinterpret_cast<const int4*>(base + (int64_t)from[m] * unit_bytes);
     int4* dst = reinterpret_cast<int4*>(const_cast<uint8_t*>(base) + (int64_t)to[m] * unit_bytes);
-    for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) st_stream(dst + v, ld_plain(src + v));
+    // 8 independent 16-B loads in flight per thread before the stores (the move is a
+    // pure HBM copy; sources are live tail units, destinations free low slots: disjoint)
+    constexpr int U = 8;
+    int64_t v = threadIdx.x;
+    for (; v + (int64_t)blockDim.x * (U - 1) < vecs; v += (int64_t)blockDim.x * U) {
+      int4 buf[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) buf[u] = ld_stream(src + v + (int64_t)blockDim.x * u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st_stream(dst + v + (int64_t)blockDim.x * u, buf[u]);
+    }
+    for (; v < vecs; v += blockDim.x) st_stream(dst + v, ld_stream(src + v));
   }
 }
 void launch_unit_move(const uint64_t* bases, const int32_t* groups, int n_groups,

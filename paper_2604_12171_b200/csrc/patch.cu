@@ -11,6 +11,10 @@
 #include <algorithm>
 #include <cstring>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace pl {
@@ -392,15 +396,24 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   if (in_flight) fail(PL_E_STATE, "a drained patch of this pair is still in flight");
   if (dst->k != src->k || dst->cell_bytes != src->cell_bytes)
     fail(PL_E_INVALID, "source and destination layouts differ");
+  static const bool trace = std::getenv("PL_TRACE_PUSH") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   take_drained();
   *keys = drained_keys;
   *cells = host_cells(drained);
   std::vector<uint8_t> mask;
   int status = PL_OK;
+  const auto t1 = now();
   extend_dst(dst, rank, n_rank, nullptr, 0, mask, &status);
   drained.clear();
+  const auto t2 = now();
   PL_CUDA(cudaSetDevice(dst->device));
   dst->flush();
+  if (trace)
+    std::fprintf(stderr, "[pl] push: take %.3f ms, extend_dst %.3f ms, dst flush %.3f ms (%lld keys)\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, now()), (long long)drained_keys);
   PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
   PL_CUDA(cudaSetDevice(src->device));
   device_drain_compact();

@@ -133,7 +133,7 @@ int64_t Store::new_block() {
   BlockRec b;
   b.id = id;
   b.slot = slot;
-  by_id[id] = b;
+  by_id.put(id, b);
   if ((int64_t)slot_block.size() <= slot) slot_block.resize((size_t)slot + 1, -1);
   slot_block[slot] = id;
   free_ids.insert(id);
@@ -146,9 +146,7 @@ int64_t Store::new_block() {
 
 BlockRec& Store::alloc_block(int32_t req) {
   if (free_ids.empty()) fail(PL_E_KV_OVERFLOW, "no free block");
-  auto it = free_ids.begin();
-  BlockRec& b = by_id.at(*it);
-  free_ids.erase(it);
+  BlockRec& b = by_id.at(free_ids.pop_min());
   b.owner = req;
   ++used;
   return b;
@@ -181,12 +179,13 @@ void Store::extend_chain(int32_t req, ReqTable& t, int64_t needed) {
 int64_t Store::occ_set_range(int32_t slot, int g, int a, int b) {
   uint64_t* w = occ_ptr(slot, g);
   int64_t added = 0;
-  for (int o = a; o < b; ++o) {
-    uint64_t m = 1ull << (o & 63);
-    if (!(w[o >> 6] & m)) {
-      w[o >> 6] |= m;
-      ++added;
-    }
+  while (a < b) {  // one 64-bit word at a time
+    const int wi = a >> 6, lo = a & 63;
+    const int hi = std::min(b - (wi << 6), 64);
+    const uint64_t m = (hi == 64 ? ~0ull : ((1ull << hi) - 1)) & (~0ull << lo);
+    added += __builtin_popcountll(m & ~w[wi]);
+    w[wi] |= m;
+    a = (wi + 1) << 6;
   }
   return added;
 }
@@ -306,20 +305,34 @@ void Store::flush() {
   if (deltas.empty() && released_slots.empty()) return;
   PL_CUDA(cudaSetDevice(device));
   if (!deltas.empty()) {
-    // dedupe: the last delta per (array, index) wins
+    // dedupe: one update per touched (array, index), value from the host mirror (which
+    // always holds the latest write); O(deltas) with per-array queued flags
+    if (table_q.size() < h_table.size()) table_q.resize(h_table.size(), 0);
+    if (owner_q.size() < h_owner.size()) owner_q.resize(h_owner.size(), 0);
     std::vector<int64_t> idx;
     std::vector<int32_t> val, which;
-    std::unordered_map<int64_t, size_t> seen;
-    seen.reserve(deltas.size() * 2);
-    for (size_t i = deltas.size(); i-- > 0;) {
-      const Delta& d = deltas[i];
-      const int64_t key = d.idx * 4 + d.which;
-      if (seen.count(key)) continue;
-      seen[key] = i;
-      idx.push_back(d.idx);
-      val.push_back(d.val);
-      which.push_back(d.which);
+    idx.reserve(deltas.size());
+    val.reserve(deltas.size());
+    which.reserve(deltas.size());
+    for (const Delta& d : deltas) {
+      if (d.which == 0) {
+        if (table_q[(size_t)d.idx]) continue;
+        table_q[(size_t)d.idx] = 1;
+        idx.push_back(d.idx);
+        val.push_back(h_table[(size_t)d.idx]);
+        which.push_back(0);
+      } else {
+        if (owner_q[(size_t)d.idx]) continue;
+        owner_q[(size_t)d.idx] = 1;
+        idx.push_back(d.idx);
+        val.push_back(h_owner[(size_t)d.idx]);
+        which.push_back(1);
+        idx.push_back(d.idx);
+        val.push_back(h_owner_idx[(size_t)d.idx]);
+        which.push_back(2);
+      }
     }
+    for (size_t i = 0; i < idx.size(); ++i) (which[i] == 0 ? table_q : owner_q)[(size_t)idx[i]] = 0;
     deltas.clear();
     Upload up(this);
     int a = up.add(idx.data(), idx.size() * 8);
