@@ -21,6 +21,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -712,20 +713,25 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
 }
 
 namespace {
+// Split-K scratch per (device, stream): launches on one stream are ordered, launches on
+// different streams (e.g. two stages' decode) must not share partials.  (A variant that
+// merged the partials inside the decode kernel -- last warp per (sequence, kv head),
+// fence + atomic count per item -- measured 40 % slower than this separate combine
+// launch at the bench shape, so the combine stays a kernel.)
 std::mutex g_ws_mu;
-float* g_ws[64] = {nullptr};
-size_t g_ws_bytes[64] = {0};
-float* workspace(size_t bytes) {
+std::map<std::pair<int, cudaStream_t>, std::pair<float*, size_t>> g_ws;
+float* workspace(size_t bytes, cudaStream_t st) {
   int dev = 0;
   PL_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  if (bytes > g_ws_bytes[dev]) {
-    PL_CUDA(cudaDeviceSynchronize());
-    cudaFree(g_ws[dev]);
-    g_ws_bytes[dev] = std::max(bytes, g_ws_bytes[dev] * 2);
-    PL_CUDA(cudaMalloc(&g_ws[dev], g_ws_bytes[dev]));
+  auto& w = g_ws[{dev, st}];
+  if (bytes > w.second) {
+    PL_CUDA(cudaStreamSynchronize(st));
+    cudaFree(w.first);
+    w.second = std::max(bytes, w.second * 2);
+    PL_CUDA(cudaMalloc(&w.first, w.second));
   }
-  return g_ws[dev];
+  return w.first;
 }
 
 template <int D, int G, int NP, int NW>
@@ -784,7 +790,7 @@ void launch_np(const AttnLaunch& a, const AttnPlan& p, size_t smem, int sms, cud
   const int grid = std::max(1, std::min(p.items, sms * std::max(per_sm, 1)));
   const int64_t n_parts_total = (int64_t)p.parts * p.W;
   const size_t np = (size_t)a.B * a.n_q * n_parts_total;
-  float* ws = workspace(np * (D + 2) * sizeof(float));
+  float* ws = workspace(np * (D + 2) * sizeof(float), st);
   KernelTimer timer("paged_attn", st);
   kern<<<grid, kWarps * 32, smem, st>>>(a, p, ws, ws + np * D);
   note_launch();
@@ -860,7 +866,7 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
   const int grid = std::max(1, std::min(p.items, sms));
   const int64_t n_parts_total = (int64_t)p.parts * p.W;
   const size_t np = (size_t)a.B * a.n_q * n_parts_total;
-  float* ws = workspace(np * (D + 2) * sizeof(float));
+  float* ws = workspace(np * (D + 2) * sizeof(float), st);
   KernelTimer timer("paged_attn", st);
   kern<<<grid, NW * 32, smem, st>>>(map, a, p, ws, ws + np * D);
   note_launch();
