@@ -305,6 +305,10 @@ def main() -> None:
     # ---- switch pause (data-path part): residual patch after one decode round + barrier
     pause = measure_switch_pause(rig, stream, torch, wl)
 
+    # ---- C2 timeline: live migration on a side stream under steady decode
+    from paper_2604_12171_b200.perf import c2_live
+    c2 = c2_live(rig, stream)
+
     # ---- paged-attention decode over the source stage (16 layers): the 8B shape (GQA 4)
     # and the 70B shape (64 q heads over the same 8 KV heads x 128, GQA 8)
     decode = measure_decode(rig, stream, torch, wl, hbm_peak, K, W)
@@ -352,6 +356,7 @@ def main() -> None:
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "switch_pause_ms": pause,
+        "c2_live": c2,
         "decode": decode,
         "decode_70b_shape": decode_70b,
         "resize": resize,

@@ -171,6 +171,11 @@ int pl_patch_mark(pl_patch* p, int32_t req, int group, int64_t start, int64_t n)
 /* the same for n (req, group, start, count) runs with one device launch */
 int pl_patch_mark_batch(pl_patch* p, int n, const int32_t* reqs, const int32_t* groups,
                         const int64_t* starts, const int64_t* counts);
+/* run K3/K4/K5 of this pair on `stream` (e.g. a low-priority stream) instead of the
+ * source store's stream, overlapped with decode on the store's stream; NULL = the store's
+ * stream.  Marks are double-buffered per drain epoch so concurrent K1 marks never leak
+ * into a drain the host snapshot did not include. */
+int pl_patch_set_stream(pl_patch* p, void* stream);
 /* MigrationStream.start seeding (migrator.py:170-183): *out_tokens = seeded tokens */
 int pl_patch_seed(pl_patch* p, int64_t* out_tokens);
 /* DirtyBitmap.discard_request (migrator.py:43-48): *out_cells = dirty keys dropped */

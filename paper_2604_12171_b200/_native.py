@@ -98,6 +98,7 @@ SIGNATURES = [
     ("pl_patch_set_active", C.c_int, [vp, C.c_int]),
     ("pl_patch_mark", C.c_int, [vp, i32, C.c_int, i64, i64]),
     ("pl_patch_mark_batch", C.c_int, [vp, C.c_int, vp, vp, vp, vp]),
+    ("pl_patch_set_stream", C.c_int, [vp, vp]),
     ("pl_patch_seed", C.c_int, [vp, P(i64)]),
     ("pl_patch_discard_request", C.c_int, [vp, i32, P(i64)]),
     ("pl_patch_dirty_keys", C.c_int, [vp, P(i64)]),

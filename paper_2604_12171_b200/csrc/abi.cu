@@ -470,6 +470,14 @@ int pl_patch_mark_batch(pl_patch* p, int n, const int32_t* reqs, const int32_t* 
     q->mark_device(items);  // one K-mark launch for the whole batch
   });
 }
+int pl_patch_set_stream(pl_patch* p, void* stream) {
+  return guard([&] {
+    pl::Patch* q = live(p);
+    PL_CUDA(cudaSetDevice(q->src->device));
+    PL_CUDA(cudaStreamSynchronize(q->pstream()));
+    q->stream = static_cast<cudaStream_t>(stream);
+  });
+}
 int pl_patch_seed(pl_patch* p, int64_t* out) {
   return guard([&] { *out = live(p)->seed(); });
 }

@@ -319,6 +319,9 @@ struct Store {
   void set_table(int32_t req, int64_t idx, int32_t slot);
   void set_owner(int32_t slot, int32_t req, int32_t idx);
   void flush();
+  // order this store's stream after every attached patch's side-stream reads of the
+  // source (K3/K4 on Patch::stream) -- before slots are released, moved or dropped
+  void order_after_patches();
   void* scratch(size_t bytes);
   void* pinned(size_t bytes);
   void materialise(int g);
@@ -392,8 +395,16 @@ struct Patch {
   std::map<std::pair<int32_t, int32_t>, std::vector<Interval>> dirty;
   int64_t dirty_keys = 0;
 
-  // device bitmap over source cells: bit ((slot*G + lg)*s + off)
+  // device bitmaps over source cells: bit ((slot*G + lg)*s + off).  Double-buffered
+  // epochs: K1 marks d_bits; a drain flips the epoch and drains the previous buffer on
+  // the patch stream while decode keeps marking the new one (no mark can slip into a
+  // drain the host snapshot did not see).
   uint32_t* d_bits = nullptr;
+  uint32_t* d_bits_alt = nullptr;
+  cudaStream_t stream = nullptr;  // side stream for K3/K4/K5 (null: the source's stream)
+  cudaStream_t pstream() const { return stream ? stream : src->stream; }
+  cudaEvent_t ev_src = nullptr, ev_snap = nullptr;
+  bool snap_recorded = false, gathered_recorded = false;
   uint32_t* d_snap = nullptr;
   int32_t* d_local_of = nullptr;  // device copy of local_of
   int64_t bit_slots = 0;  // slots covered

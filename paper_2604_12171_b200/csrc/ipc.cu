@@ -129,7 +129,11 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
     if (!r->table) fail(PL_E_STATE, "remote block table not opened");
     Upload up(src);
     int a = up.add(mask.data(), mask.size());
-    up.go();
+    up.go();  // H2D on the source stream
+    if (pstream() != src->stream) {
+      PL_CUDA(cudaEventRecord(ev_src, src->stream));
+      PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
+    }
     CopyLaunch c{};
     c.mode = 2;
     c.cells = d_cells;
@@ -151,9 +155,9 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
     c.dst_table = r->table;
     c.dst_max_chain = r->max_chain;
     c.apply_mask = up.ptr<uint8_t>(a);
-    launch_copy(c, src->stream);
+    launch_copy(c, pstream());
   }
-  PL_CUDA(cudaEventRecord(ev_applied, src->stream));
+  PL_CUDA(cudaEventRecord(ev_applied, pstream()));
   applied_recorded = true;
   drained.clear();
   remote_rows.clear();

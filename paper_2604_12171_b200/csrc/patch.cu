@@ -52,6 +52,8 @@ Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n)
   PL_CUDA(cudaEventCreateWithFlags(&ev_gathered, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_applied, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_dst, cudaEventDisableTiming));
+  PL_CUDA(cudaEventCreateWithFlags(&ev_src, cudaEventDisableTiming));
+  PL_CUDA(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
   ensure_bits();
   src->patches.push_back(this);
 }
@@ -59,6 +61,7 @@ Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n)
 Patch::~Patch() {
   cudaSetDevice(device);
   if (src) {
+    if (stream) cudaStreamSynchronize(stream);
     cudaStreamSynchronize(src->stream);
     auto& v = src->patches;
     v.erase(std::remove(v.begin(), v.end(), this), v.end());
@@ -66,6 +69,7 @@ Patch::~Patch() {
     cudaDeviceSynchronize();
   }
   cudaFree(d_bits);
+  cudaFree(d_bits_alt);
   cudaFree(d_snap);
   cudaFree(d_local_of);
   cudaFree(d_tile_counts);
@@ -77,23 +81,30 @@ Patch::~Patch() {
   cudaEventDestroy(ev_gathered);
   cudaEventDestroy(ev_applied);
   cudaEventDestroy(ev_dst);
+  cudaEventDestroy(ev_src);
+  cudaEventDestroy(ev_snap);
 }
 
 void Patch::ensure_bits() {
   const int64_t slots = std::max<int64_t>(src->owner_cap, 1);
   if (slots <= bit_slots && d_bits) return;
   const int64_t words = (slots * G * src->s + 31) / 32;
-  uint32_t *nb = nullptr, *ns = nullptr;
+  uint32_t *nb = nullptr, *na = nullptr, *ns = nullptr;
   PL_CUDA(cudaSetDevice(src->device));
+  if (stream) PL_CUDA(cudaStreamSynchronize(stream));
   PL_CUDA(cudaMalloc(&nb, words * 4));
+  PL_CUDA(cudaMalloc(&na, words * 4));
   PL_CUDA(cudaMalloc(&ns, words * 4));
   PL_CUDA(cudaMemsetAsync(nb, 0, words * 4, src->stream));
+  PL_CUDA(cudaMemsetAsync(na, 0, words * 4, src->stream));
   if (d_bits && n_words)
     PL_CUDA(cudaMemcpyAsync(nb, d_bits, n_words * 4, cudaMemcpyDeviceToDevice, src->stream));
   PL_CUDA(cudaStreamSynchronize(src->stream));
   cudaFree(d_bits);
+  cudaFree(d_bits_alt);
   cudaFree(d_snap);
   d_bits = nb;
+  d_bits_alt = na;
   d_snap = ns;
   bit_slots = slots;
   n_words = words;
@@ -250,16 +261,29 @@ int64_t Patch::take_drained() {
 
 int64_t Patch::device_drain_compact() {
   src->flush();
+  cudaStream_t ps = pstream();
   const int64_t need = std::max<int64_t>(drained_keys, 1);
   if (need > cells_cap) {
-    PL_CUDA(cudaStreamSynchronize(src->stream));
+    PL_CUDA(cudaStreamSynchronize(ps));
     cudaFree(d_cells);
     cells_cap = std::max(need, cells_cap * 2);
     PL_CUDA(cudaMalloc(&d_cells, sizeof(int64_t) * cells_cap));
   }
-  launch_drain_snapshot(d_bits, d_snap, n_words, d_tile_counts, src->stream);
-  launch_drain_scan(d_tile_counts, drain_tiles(n_words), d_count, src->stream);
-  launch_drain_emit(d_snap, n_words, d_tile_counts, d_cells, cells_cap, src->stream);
+  // epoch flip: every mark enqueued so far (the host snapshot taken by the caller) is in
+  // `old`; K1 launches from now on mark the other buffer, which the previous drain's
+  // snapshot cleared on the patch stream
+  uint32_t* old = d_bits;
+  std::swap(d_bits, d_bits_alt);
+  if (snap_recorded && ps != src->stream) PL_CUDA(cudaStreamWaitEvent(src->stream, ev_snap, 0));
+  if (ps != src->stream) {
+    PL_CUDA(cudaEventRecord(ev_src, src->stream));
+    PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
+  }
+  launch_drain_snapshot(old, d_snap, n_words, d_tile_counts, ps);
+  PL_CUDA(cudaEventRecord(ev_snap, ps));
+  snap_recorded = true;
+  launch_drain_scan(d_tile_counts, drain_tiles(n_words), d_count, ps);
+  launch_drain_emit(d_snap, n_words, d_tile_counts, d_cells, cells_cap, ps);
   return drained_keys;
 }
 
@@ -268,12 +292,12 @@ void Patch::drain(int64_t* keys, int64_t* cells) {
   PL_CUDA(cudaSetDevice(src->device));
   take_drained();
   // the staging buffer may still be read by the previous apply on the dst stream
-  if (applied_recorded) PL_CUDA(cudaStreamWaitEvent(src->stream, ev_applied, 0));
+  if (applied_recorded) PL_CUDA(cudaStreamWaitEvent(pstream(), ev_applied, 0));
   device_drain_compact();
   const int64_t row_bytes = 16 + (int64_t)src->k * src->cell_bytes;
   const int64_t need = std::max<int64_t>(drained_keys, 1);
   if (need > rows_cap) {
-    PL_CUDA(cudaStreamSynchronize(src->stream));
+    PL_CUDA(cudaStreamSynchronize(pstream()));
     cudaFree(d_rows);
     cudaFree(d_keys);
     rows_cap = std::max(need, rows_cap + rows_cap / 2);
@@ -299,9 +323,10 @@ void Patch::drain(int64_t* keys, int64_t* cells) {
     c.rows = d_rows;
     c.keys = d_keys;
     c.row_bytes = row_bytes;
-    launch_copy(c, src->stream);
+    launch_copy(c, pstream());
   }
-  PL_CUDA(cudaEventRecord(ev_gathered, src->stream));
+  PL_CUDA(cudaEventRecord(ev_gathered, pstream()));
+  gathered_recorded = true;
   in_flight = true;
   *keys = drained_keys;
   *cells = host_cells(drained);
@@ -420,8 +445,12 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   if (drained_keys > 0 && !mask.empty()) {
     Upload up(src);
     int a = up.add(mask.data(), mask.size());
-    up.go();
-    PL_CUDA(cudaStreamWaitEvent(src->stream, ev_dst, 0));
+    up.go();  // H2D on the source stream
+    if (pstream() != src->stream) {
+      PL_CUDA(cudaEventRecord(ev_src, src->stream));
+      PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
+    }
+    PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
     CopyLaunch c{};
     c.mode = 2;
     c.cells = d_cells;
@@ -443,9 +472,9 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
     c.dst_table = dst->d_table;
     c.dst_max_chain = dst->max_chain;
     c.apply_mask = up.ptr<uint8_t>(a);
-    launch_copy(c, src->stream);
+    launch_copy(c, pstream());
   }
-  PL_CUDA(cudaEventRecord(ev_applied, src->stream));
+  PL_CUDA(cudaEventRecord(ev_applied, pstream()));
   applied_recorded = true;
   PL_CUDA(cudaSetDevice(dst->device));
   PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
@@ -454,11 +483,13 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
 
 int64_t Patch::device_dirty_count() {
   src->flush();
+  if (stream) PL_CUDA(cudaStreamSynchronize(stream));
+  PL_CUDA(cudaStreamSynchronize(src->stream));
   launch_popcount(d_bits, n_words, d_count + 1, src->stream);
   int64_t v = 0;
   PL_CUDA(cudaMemcpyAsync(&v, d_count + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, src->stream));
   PL_CUDA(cudaStreamSynchronize(src->stream));
-  return v;
+  return v;  // the drained buffer is all-zero once its snapshot ran
 }
 
 }  // namespace pl

@@ -301,9 +301,20 @@ void Upload::go(size_t extra_device_bytes) {
   PL_CUDA(cudaEventRecord(st->pinned_ev, st->stream));
 }
 
+void Store::order_after_patches() {
+  for (Patch* p : patches) {
+    if (!p->stream || p->stream == stream) continue;
+    if (p->applied_recorded) PL_CUDA(cudaStreamWaitEvent(stream, p->ev_applied, 0));
+    if (p->gathered_recorded) PL_CUDA(cudaStreamWaitEvent(stream, p->ev_gathered, 0));
+  }
+}
+
 void Store::flush() {
   if (deltas.empty() && released_slots.empty()) return;
   PL_CUDA(cudaSetDevice(device));
+  // a released slot may still be read by a patch's in-flight copy on its side stream
+  // (owner map, cells): its owner delta and bit clears wait for that copy
+  if (!released_slots.empty()) order_after_patches();
   if (!deltas.empty()) {
     // dedupe: one update per touched (array, index), value from the host mirror (which
     // always holds the latest write); O(deltas) with per-array queued flags
@@ -624,6 +635,7 @@ void Store::resize(int64_t new_cap) {
   for (int64_t i = new_cap; i < old_cap && !live_in_tail; ++i)
     live_in_tail = by_id.at(blocks[i]).owner >= 0;
   if (live_in_tail) compact();
+  order_after_patches();  // K6 moves units an in-flight side-stream copy may read
   for (int64_t i = new_cap; i < old_cap; ++i) {
     const int64_t id = blocks[i];
     BlockRec& b = by_id.at(id);
@@ -723,6 +735,7 @@ int64_t Store::drop_groups(const int32_t* groups_in, int n) {
   static const bool trace = std::getenv("PL_TRACE_RESIZE") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto t0 = now();
+  order_after_patches();
   int64_t freed = 0;
   for (int32_t req = 0; req < (int32_t)tables.size(); ++req) {
     ReqTable& t = tables[req];

@@ -104,6 +104,19 @@ class NativePatch:
         N.check(N.lib().pl_patch_mark_batch(self.h, len(r), N.ptr(r), N.ptr(g), N.ptr(st),
                                             N.ptr(c)))
 
+    def discard_request(self, rid, registry) -> int:
+        """DirtyBitmap.discard_request (migrator.py:43-48) for a finished request."""
+        h = registry.find(rid)
+        if h is None:
+            return 0
+        out = C.c_int64()
+        N.check(N.lib().pl_patch_discard_request(self.h, h, C.byref(out)))
+        return out.value
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        """K3/K4/K5 of this pair on a side stream (overlapped with decode)."""
+        N.check(N.lib().pl_patch_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
     def dirty_keys(self) -> int:
         out = C.c_int64()
         N.check(N.lib().pl_patch_dirty_keys(self.h, C.byref(out)))
@@ -168,6 +181,104 @@ class PatchRig:
         self.close()
         self.src.close()
         self.dst.close()
+
+
+def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
+    """BASELINE configs[1] as a timeline: the PP2 stage keeps decoding (every step: K1
+    appends one token per request to each of its 4 groups with the fused dirty mark, then
+    K2 over its 16 layers) while the pair's patch engine runs on a low-priority side
+    stream: the bulk copy of the two migrating groups, then one patch round per step.
+    Reports decode ms/step before / during the bulk copy / during steady patching, the
+    bulk copy's duration, and the switch pause (drain the decode stream, residual round,
+    barrier).  Decode and patching share HBM, so the interference is the measured cost of
+    live migration."""
+    import torch
+
+    wl = rig.wl
+    lib = N.lib()
+    dev = torch.device("cuda", rig.device)
+    lo, _ = torch.cuda.Stream.priority_range()
+    side = torch.cuda.Stream(device=rig.device, priority=lo)
+    rig.patch.set_stream(side.cuda_stream)
+    B = wl.batch
+    rows = torch.tensor(rig.handles, dtype=torch.int32, device=dev)
+    ctx_now = [rig.src.tables[rid(i)].written.get(wl.src_groups[0], 0) for i in range(B)]
+    q = torch.randn(B, wl.n_q, wl.head_dim, dtype=torch.bfloat16, device=dev)
+    out = torch.empty_like(q)
+    reqs = [h for h in rig.handles for _ in wl.src_groups]
+    groups = [g for _ in rig.handles for g in wl.src_groups]
+    seeds = [stable_hash(rid(i), g) for i in range(B) for g in wl.src_groups]
+
+    def decode_step(mark: bool) -> float:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        append_batch(rig.src, reqs, groups, [1] * len(reqs), seeds, mark=mark)
+        for i in range(B):
+            ctx_now[i] += 1
+        ctx = torch.tensor(ctx_now, dtype=torch.int32, device=dev)
+        for g in wl.src_groups:
+            for j in range(wl.k):
+                N.check(lib.pl_paged_attn_decode(rig.src._h, g, j, C.c_void_p(q.data_ptr()),
+                                                 C.c_void_p(out.data_ptr()),
+                                                 C.c_void_p(rows.data_ptr()),
+                                                 C.c_void_p(ctx.data_ptr()), B, wl.n_q, wl.n_kv,
+                                                 wl.head_dim, wl.head_dim ** -0.5, max(ctx_now),
+                                                 C.c_void_p(stream.cuda_stream)))
+        e1.record(stream)
+        return (e0, e1)
+
+    torch.cuda.synchronize()
+    base = [decode_step(False) for _ in range(steps)]
+    torch.cuda.synchronize()
+    base_ms = [a.elapsed_time(b) for a, b in base]
+    # start: seed every live cell of the migrating groups, first round = bulk copy
+    rig.patch.seed()
+    b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b0.record(side)
+    keys, cells = rig.patch.push(rig.dst, rig.registry.rank())
+    b1.record(side)
+    bulk_payload = cells * wl.cell_bytes
+    during = [decode_step(True)]
+    while not b1.query():
+        during.append(decode_step(True))
+        if len(during) > 50:
+            break
+    torch.cuda.synchronize()
+    bulk_ms = b0.elapsed_time(b1)
+    during_ms = [a.elapsed_time(b) for a, b in during]
+    steady, round_keys = [], []
+    for _ in range(steps):
+        k2, _ = rig.patch.push(rig.dst, rig.registry.rank())   # previous step's writes
+        round_keys.append(k2)
+        steady.append(decode_step(True))
+    torch.cuda.synchronize()
+    steady_ms = [a.elapsed_time(b) for a, b in steady]
+    # switch: pause admission -> drain the in-flight step -> residual round -> barrier
+    decode_step(True)
+    t0 = time.perf_counter()
+    stream.synchronize()                  # the in-flight decode step drains
+    t1 = time.perf_counter()
+    keys_res, cells_res = rig.patch.push(rig.dst, rig.registry.rank())
+    side.synchronize()
+    rig.dst.sync()                        # barrier: residual applied on the destination
+    pause_ms = (time.perf_counter() - t0) * 1e3
+    drain_ms = (t1 - t0) * 1e3
+    rig.patch.set_stream(None)
+    med = lambda xs: round(float(np.median(xs)), 4) if xs else None  # noqa: E731
+    return {"decode_ms_per_step_alone": med(base_ms),
+            "decode_ms_per_step_during_bulk": med(during_ms),
+            "decode_steps_overlapping_bulk": len(during_ms),
+            "decode_ms_per_step_steady_patching": med(steady_ms),
+            "bulk": {"payload_bytes": bulk_payload, "ms": round(bulk_ms, 3),
+                     "gbs": round(bulk_payload / bulk_ms / 1e6, 1)},
+            "steady_round_keys": round_keys[-1] if round_keys else 0,
+            "switch_pause_ms": round(pause_ms, 4),
+            "switch_pause_breakdown_ms": {"drain_in_flight_step": round(drain_ms, 4),
+                                          "residual_patch_and_barrier": round(pause_ms - drain_ms, 4)},
+            "residual_keys": keys_res,
+            "residual_bytes": cells_res * wl.cell_bytes,
+            "note": "decode (K1+K2, store stream) and patching (K3+K4+K5, low-priority side "
+                    "stream) overlap on one GPU and share its HBM"}
 
 
 def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040) -> dict:

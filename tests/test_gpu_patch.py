@@ -154,3 +154,58 @@ def test_push_path_direct_into_destination(ns):
     for i in range(10):
         assert dst.read_cell(f"p{i}", 1, 29 + i, 1) == src.read_cell(f"p{i}", 1, 29 + i, 1)
     N.lib().pl_patch_destroy(h)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_side_stream_push_overlapped_with_decode_writes(seed):
+    """K3/K4/K5 on a low-priority side stream while K1 keeps writing (and marking) on the
+    store's stream with no host sync in between: after the final round the destination
+    holds exactly the source's migrating groups, byte for byte, and requests freed
+    mid-migration are gone from both."""
+    import random
+
+    import torch
+
+    from paper_2604_12171_b200 import kvstore
+    from paper_2604_12171_b200.events import stable_hash
+    from paper_2604_12171_b200.perf import NativePatch
+
+    rng = random.Random(seed)
+    reg = kvstore.RequestRegistry()
+    names = [f"q{i:03d}" for i in range(40)]
+    for n in names:
+        reg.handle(n)
+    src = kvstore.KvStore(1, 2, 16, 2048, (0, 1, 2), num_groups=3, cell_bytes=512, registry=reg)
+    dst = kvstore.KvStore(2, 2, 16, 2048, (), num_groups=3, cell_bytes=512, registry=reg)
+    dst.resident_groups |= {1, 2}
+    lo, _ = torch.cuda.Stream.priority_range()
+    side = torch.cuda.Stream(priority=lo)
+    for n in names[:30]:
+        for g in range(3):
+            src.append_seeded(n, g, 1 + rng.randrange(200), stable_hash(n, g))
+    p = NativePatch(src, (1, 2), 2)
+    p.set_stream(side.cuda_stream)
+    p.seed()
+    p.push(dst, reg.rank())                    # bulk, no sync afterwards
+    live = set(names[:30])
+    for step in range(25):
+        for n in rng.sample(sorted(live | set(names[30:])), 12):
+            for g in range(3):
+                src.append_seeded(n, g, 1 + rng.randrange(5), stable_hash(n, g), mark=True)
+            live.add(n)
+        if step % 7 == 3:                      # a request finishes mid-migration
+            gone = rng.choice(sorted(live))
+            live.discard(gone)
+            p.discard_request(gone, reg)
+            src.free_request(gone)
+            dst.free_request(gone)
+        p.push(dst, reg.rank())                # one round per step, no host sync
+    p.push(dst, reg.rank())                    # residual
+    torch.cuda.synchronize()
+    for g in (1, 2):
+        assert dst.snapshot_group(g) == src.snapshot_group(g)
+        for rid, fps in src.snapshot_group(g).items():
+            for pos in {0, len(fps) // 2, len(fps) - 1}:
+                assert dst.read_cell(rid, g, pos, 1) == src.read_cell(rid, g, pos, 1)
+    assert p.dirty_keys() == 0
+    p.close()
