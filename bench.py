@@ -238,6 +238,16 @@ def main() -> None:
     hbm_peak = float(peaks.get("hbm_gbs", HBM_FALLBACK_GBS))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
+    # ---- C3 first, on a clean GPU: 70B-shape stage with HBM pre-filled by KV (~160 GB
+    # peak), live shrink with K6 relocation, patch of the leaving groups, drop, grow
+    c3 = None
+    if not args.skip_c3 and rank == 0:
+        from paper_2604_12171_b200.perf import c3_live_resize
+        c3 = c3_live_resize(dev)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    barrier(world)
+
     stream = torch.cuda.Stream(device=dev)
     rig = PatchRig(wl, device=dev)
     rig.use_stream(stream.cuda_stream)
@@ -333,14 +343,6 @@ def main() -> None:
     rig.destroy()
     if ring is not None:
         ring.dst.close()
-    torch.cuda.synchronize()
-    torch.cuda.empty_cache()
-
-    # ---- C3: 70B-shape stage with HBM pre-filled, live shrink (K6 relocation) + grow
-    c3 = None
-    if not args.skip_c3 and rank == 0:
-        from paper_2604_12171_b200.perf import c3_live_resize
-        c3 = c3_live_resize(dev)
 
     if rank != 0:
         return

@@ -403,8 +403,14 @@ struct Patch {
   uint32_t* d_bits_alt = nullptr;
   cudaStream_t stream = nullptr;  // side stream for K3/K4/K5 (null: the source's stream)
   cudaStream_t pstream() const { return stream ? stream : src->stream; }
-  cudaEvent_t ev_src = nullptr, ev_snap = nullptr;
-  bool snap_recorded = false, gathered_recorded = false;
+  cudaEvent_t ev_src = nullptr, ev_snap = nullptr, ev_mask = nullptr;
+  bool snap_recorded = false, gathered_recorded = false, mask_recorded = false;
+  // apply mask of the fused push, in patch-owned buffers: the copy on the side stream
+  // reads it while the store's stream (and its scratch) moves on
+  uint8_t* h_mask = nullptr;
+  uint8_t* d_mask = nullptr;
+  size_t mask_cap = 0;
+  const uint8_t* stage_mask(const std::vector<uint8_t>& mask);
   uint32_t* d_snap = nullptr;
   int32_t* d_local_of = nullptr;  // device copy of local_of
   int64_t bit_slots = 0;  // slots covered

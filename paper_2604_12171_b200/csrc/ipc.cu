@@ -127,13 +127,11 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
       fail(PL_E_STATE, "remote pool of group " + std::to_string(g) + " not imported");
   if (drained_keys > 0 && n_applied > 0) {
     if (!r->table) fail(PL_E_STATE, "remote block table not opened");
-    Upload up(src);
-    int a = up.add(mask.data(), mask.size());
-    up.go();  // H2D on the source stream
     if (pstream() != src->stream) {
       PL_CUDA(cudaEventRecord(ev_src, src->stream));
       PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
     }
+    const uint8_t* d_apply = stage_mask(mask);
     CopyLaunch c{};
     c.mode = 2;
     c.cells = d_cells;
@@ -154,7 +152,7 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
     c.dst_unit = r->unit_bytes;
     c.dst_table = r->table;
     c.dst_max_chain = r->max_chain;
-    c.apply_mask = up.ptr<uint8_t>(a);
+    c.apply_mask = d_apply;
     launch_copy(c, pstream());
   }
   PL_CUDA(cudaEventRecord(ev_applied, pstream()));

@@ -54,6 +54,7 @@ Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n)
   PL_CUDA(cudaEventCreateWithFlags(&ev_dst, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_src, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
+  PL_CUDA(cudaEventCreateWithFlags(&ev_mask, cudaEventDisableTiming));
   ensure_bits();
   src->patches.push_back(this);
 }
@@ -83,6 +84,29 @@ Patch::~Patch() {
   cudaEventDestroy(ev_dst);
   cudaEventDestroy(ev_src);
   cudaEventDestroy(ev_snap);
+  cudaEventDestroy(ev_mask);
+  cudaFree(d_mask);
+  if (h_mask) cudaFreeHost(h_mask);
+}
+
+const uint8_t* Patch::stage_mask(const std::vector<uint8_t>& mask) {
+  cudaStream_t ps = pstream();
+  const size_t n = std::max<size_t>(mask.size(), 1);
+  if (n > mask_cap) {
+    PL_CUDA(cudaStreamSynchronize(ps));
+    cudaFree(d_mask);
+    if (h_mask) cudaFreeHost(h_mask);
+    mask_cap = std::max(n, mask_cap * 2);
+    PL_CUDA(cudaMallocHost(&h_mask, mask_cap));
+    PL_CUDA(cudaMalloc(&d_mask, mask_cap));
+    mask_recorded = false;
+  }
+  if (mask_recorded) PL_CUDA(cudaEventSynchronize(ev_mask));  // previous H2D read h_mask
+  std::memcpy(h_mask, mask.data(), mask.size());
+  PL_CUDA(cudaMemcpyAsync(d_mask, h_mask, mask.size(), cudaMemcpyHostToDevice, ps));
+  PL_CUDA(cudaEventRecord(ev_mask, ps));
+  mask_recorded = true;
+  return d_mask;
 }
 
 void Patch::ensure_bits() {
@@ -443,13 +467,11 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   PL_CUDA(cudaSetDevice(src->device));
   device_drain_compact();
   if (drained_keys > 0 && !mask.empty()) {
-    Upload up(src);
-    int a = up.add(mask.data(), mask.size());
-    up.go();  // H2D on the source stream
     if (pstream() != src->stream) {
       PL_CUDA(cudaEventRecord(ev_src, src->stream));
       PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
     }
+    const uint8_t* d_apply = stage_mask(mask);
     PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
     CopyLaunch c{};
     c.mode = 2;
@@ -471,7 +493,7 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
     c.dst_unit = dst->unit_bytes;
     c.dst_table = dst->d_table;
     c.dst_max_chain = dst->max_chain;
-    c.apply_mask = up.ptr<uint8_t>(a);
+    c.apply_mask = d_apply;
     launch_copy(c, pstream());
   }
   PL_CUDA(cudaEventRecord(ev_applied, pstream()));

@@ -11,8 +11,9 @@
 // So a shrink (trim) or a dropped group (release) only detaches the tail chunks
 // from the arena and hands them to the store's Reclaimer thread, which waits for
 // the stream work that may still read them (a CUDA event), unmaps the whole range
-// in one call after a short grace period, and returns the chunks to the driver
-// after a second grace period.  A grow inside the grace period takes the still
+// in one call after a short grace period (20 ms), and returns the chunks to the driver
+// after a second grace period (100 ms: post-commit cleanup drops groups and then grows
+// the remaining pools, which re-maps these chunks instead of creating new ones).  A grow inside the grace period takes the still
 // mapped tail back (no driver call at all) or re-maps cached physical chunks
 // (no cuMemCreate).  cuMemCreate failing with out-of-memory forces every pending
 // reclaim first, so memory pressure turns the deferral off.
@@ -161,7 +162,7 @@ struct Reclaimer::Job {
 Reclaimer::Reclaimer(int dev, size_t chunk)
     : device(dev), chunk_bytes(chunk),
       unmap_grace_ms(env_ms("PL_RECLAIM_UNMAP_GRACE_MS", 20)),
-      release_grace_ms(env_ms("PL_RECLAIM_RELEASE_GRACE_MS", 20)) {
+      release_grace_ms(env_ms("PL_RECLAIM_RELEASE_GRACE_MS", 100)) {
   th = std::thread([this] { loop(); });
 }
 

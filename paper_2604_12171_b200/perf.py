@@ -200,6 +200,10 @@ def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
     lo, _ = torch.cuda.Stream.priority_range()
     side = torch.cuda.Stream(device=rig.device, priority=lo)
     rig.patch.set_stream(side.cuda_stream)
+    # the destination stage has its own stream (it is another GPU on hardware): its wait
+    # for the applied patch must not block this stage's decode stream
+    dst_stream = torch.cuda.Stream(device=rig.device)
+    N.check(N.lib().pl_store_set_stream(rig.dst._h, C.c_void_p(dst_stream.cuda_stream)))
     B = wl.batch
     rows = torch.tensor(rig.handles, dtype=torch.int32, device=dev)
     ctx_now = [rig.src.tables[rid(i)].written.get(wl.src_groups[0], 0) for i in range(B)]
@@ -231,21 +235,24 @@ def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
     base = [decode_step(False) for _ in range(steps)]
     torch.cuda.synchronize()
     base_ms = [a.elapsed_time(b) for a, b in base]
-    # start: seed every live cell of the migrating groups, first round = bulk copy
+    # start: seed every live cell of the migrating groups, first round = bulk copy; decode
+    # keeps stepping; the steps overlapping the bulk are found from the event timestamps
     rig.patch.seed()
     b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    anchor = torch.cuda.Event(enable_timing=True)
+    anchor.record(stream)
+    side.wait_event(anchor)
     b0.record(side)
     keys, cells = rig.patch.push(rig.dst, rig.registry.rank())
     b1.record(side)
     bulk_payload = cells * wl.cell_bytes
-    during = [decode_step(True)]
-    while not b1.query():
-        during.append(decode_step(True))
-        if len(during) > 50:
-            break
+    during = [decode_step(True) for _ in range(steps)]
     torch.cuda.synchronize()
+    assert rig.patch.device_drained() == keys, (rig.patch.device_drained(), keys)
+    bulk_end = anchor.elapsed_time(b1)
     bulk_ms = b0.elapsed_time(b1)
-    during_ms = [a.elapsed_time(b) for a, b in during]
+    overlap = [(a, b) for a, b in during if anchor.elapsed_time(a) < bulk_end]
+    during_ms = [a.elapsed_time(b) for a, b in overlap]
     steady, round_keys = [], []
     for _ in range(steps):
         k2, _ = rig.patch.push(rig.dst, rig.registry.rank())   # previous step's writes
@@ -264,6 +271,7 @@ def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
     pause_ms = (time.perf_counter() - t0) * 1e3
     drain_ms = (t1 - t0) * 1e3
     rig.patch.set_stream(None)
+    N.check(N.lib().pl_store_set_stream(rig.dst._h, C.c_void_p(stream.cuda_stream)))
     med = lambda xs: round(float(np.median(xs)), 4) if xs else None  # noqa: E731
     return {"decode_ms_per_step_alone": med(base_ms),
             "decode_ms_per_step_during_bulk": med(during_ms),
@@ -372,9 +380,6 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040) -> di
     t0 = time.perf_counter()
     src.drop_layer_groups([3, 4])
     out["drop_groups_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
-    out["free_gb_before_grow"] = free_gb()
-    import sys
-    print(out, file=sys.stderr, flush=True)
     t0 = time.perf_counter()
     src.resize(b_new)
     src.sync()
