@@ -77,6 +77,28 @@ def init_weights(cfg: LlamaConfig, seed: int = 0) -> dict[str, np.ndarray]:
     return w
 
 
+def pipeline_order(owner: dict[int, int]) -> list[int]:
+    """GPUs that hold layers, in pipeline order (by their first layer); a GPU with no
+    layers (the zero-layer extension) is not a stage."""
+    first: dict[int, int] = {}
+    for layer, gpu in owner.items():
+        first[gpu] = min(first.get(gpu, layer), layer)
+    return sorted(first, key=first.get)
+
+
+def layer_moves(owner: dict[int, int], target: dict[int, list[int]]) -> dict[tuple[int, int], list[int]]:
+    """M_mig of a reconfiguration (cluster.py:238-270, diff_configs): for every layer whose
+    owner changes, the (src, dst) pair it moves over; pairs and layers sorted."""
+    new_owner = {l: g for g, ls in target.items() for l in ls}
+    if sorted(new_owner) != sorted(owner):
+        raise ValueError("target must place every layer exactly once")
+    moves: dict[tuple[int, int], list[int]] = {}
+    for layer in sorted(owner):
+        if owner[layer] != new_owner[layer]:
+            moves.setdefault((owner[layer], new_owner[layer]), []).append(layer)
+    return dict(sorted(moves.items()))
+
+
 class LlamaCompute:
     """The math of one decode step, layer by layer, over whichever store owns a layer."""
 
@@ -239,12 +261,8 @@ class StagedLlama:
         all live cells of its layers and pushes them (bulk copy); from now on K1 marks
         every new cell of those layers dirty."""
         new_owner = {l: g for g, ls in target.items() for l in ls}
-        assert sorted(new_owner) == sorted(self.owner), "target must place every layer"
-        moves: dict[tuple[int, int], list[int]] = {}
-        for l, g in new_owner.items():
-            if self.owner[l] != g:
-                moves.setdefault((self.owner[l], g), []).append(l)
-        for (src, dst), layers in sorted(moves.items()):
+        moves = layer_moves(self.owner, target)
+        for (src, dst), layers in moves.items():
             d = self._store(dst, [])
             d.resident_groups |= {l - 1 for l in layers}
             p = NativePatch(self.stores[src], [l - 1 for l in layers], 1)
@@ -389,11 +407,7 @@ class DistStagedLlama:
         return self.torch.cuda.stream(self.stream)
 
     def _order(self) -> list[int]:
-        """Pipeline order: GPUs holding layers, by their first layer."""
-        first: dict[int, int] = {}
-        for l, g in self.owner.items():
-            first[g] = min(first.get(g, l), l)
-        return sorted(first, key=first.get)
+        return pipeline_order(self.owner)
 
     def step_tokens(self, rids: list, tokens: list[int]) -> list[int]:
         torch, c = self.torch, self.cfg
@@ -429,10 +443,7 @@ class DistStagedLlama:
         from .dist import Channel, PatchReceiver, PatchSender
 
         new_owner = {l: g for g, ls in target.items() for l in ls}
-        moves: dict = {}
-        for l, g in new_owner.items():
-            if self.owner[l] != g:
-                moves.setdefault((self.owner[l], g), []).append(l)
+        moves = layer_moves(self.owner, target)
         self.moving = moves
         self.target = new_owner
         arriving = [l for (src, dst), ls in moves.items() if dst == self.gpu for l in ls]
