@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-sweep", action="store_true")
     ap.add_argument("--skip-c3", action="store_true")
+    ap.add_argument("--skip-c2", action="store_true")
+    ap.add_argument("--only-step", action="store_true",
+                    help="time the KV-patch step only (for the ncu launch list of the step)")
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--ctx", type=int, default=2048)
     return ap.parse_args()
@@ -240,6 +243,8 @@ def main() -> None:
 
     # ---- C3 first, on a clean GPU: 70B-shape stage with HBM pre-filled by KV (~160 GB
     # peak), live shrink with K6 relocation, patch of the leaving groups, drop, grow
+    if args.only_step:
+        args.skip_c3 = args.skip_c2 = args.skip_sweep = args.skip_e2e = args.skip_cpu = True
     c3 = None
     if not args.skip_c3 and rank == 0:
         from paper_2604_12171_b200.perf import c3_live_resize
@@ -312,23 +317,26 @@ def main() -> None:
                 "share_of_step": round(push_ms / ms, 4) if ms else None,
                 "drain_ms_per_step": round(drain_ms / max(K, 1), 4)}
 
-    # ---- switch pause (data-path part): residual patch after one decode round + barrier
-    pause = measure_switch_pause(rig, stream, torch, wl)
+    pause = c2 = decode = decode_70b = wstage = resize = None
+    if not args.only_step:
+        # ---- switch pause (data-path part): residual patch after one decode round + barrier
+        pause = measure_switch_pause(rig, stream, torch, wl)
 
-    # ---- C2 timeline: live migration on a side stream under steady decode
-    from paper_2604_12171_b200.perf import c2_live
-    c2 = c2_live(rig, stream)
+        # ---- C2 timeline: live migration on a side stream under steady decode
+        if not args.skip_c2:
+            from paper_2604_12171_b200.perf import c2_live
+            c2 = c2_live(rig, stream)
 
-    # ---- paged-attention decode over the source stage (16 layers): the 8B shape (GQA 4)
-    # and the 70B shape (64 q heads over the same 8 KV heads x 128, GQA 8)
-    decode = measure_decode(rig, stream, torch, wl, hbm_peak, K, W)
-    decode_70b = measure_decode(rig, stream, torch, wl, hbm_peak, K, W, n_q=64)
+        # ---- paged-attention decode over the source stage (16 layers): the 8B shape
+        # (GQA 4) and the 70B shape (64 q heads over the same 8 KV heads x 128, GQA 8)
+        decode = measure_decode(rig, stream, torch, wl, hbm_peak, K, W)
+        decode_70b = measure_decode(rig, stream, torch, wl, hbm_peak, K, W, n_q=64)
 
-    # ---- AddLayerWeights on the copy engine: the 8 migrating layers' weights (0.436 GB each)
-    wstage = measure_weight_stage(rig, stream, torch, wl, dev)
+        # ---- AddLayerWeights on the copy engine: the 8 migrating layers' weights
+        wstage = measure_weight_stage(rig, stream, torch, wl, dev)
 
-    # ---- resize latency: post-commit cleanup on the source (drop groups, shrink, regrow)
-    resize = measure_resize(rig, stream, torch, wl)
+        # ---- resize latency: post-commit cleanup on the source (drop, shrink, regrow)
+        resize = measure_resize(rig, stream, torch, wl)
 
     # ---- C5: dirty-rate x block-size sweep of one patch round (configs[4], 1 GPU)
     sweep = None
