@@ -483,13 +483,83 @@ constexpr int kMmaStage = 16;  // tokens per stage = one M tile = two 8-token TM
 
 struct MmaPlan {
   int n_stage;      // ring depth
-  int parts;        // context parts per sequence
-  int part_tokens;  // multiple of 16
   int W;            // warps per kv head
-  int items;        // B * parts
   int nchunks;      // cell / 128
   int box_bytes;    // 8 tokens x cell
+  // stream-K schedule (attn_plan_kernel): sp[b] = first global stage of sequence b
+  // (stages of 16 tokens, sequences in batch order, sp[B] = S), po[b] = first partial
+  // piece of b; CTA c owns global stages [c*S/grid, (c+1)*S/grid)
+  const int* sp;
+  const int* po;
 };
+
+// owner CTA of global stage x when S stages are split evenly over g CTAs
+__device__ __forceinline__ int stage_owner(int64_t x, int64_t S, int g) {
+  return (int)(((x + 1) * g - 1) / S);
+}
+
+// One block: stage prefix sp[0..B] and partial-piece prefix po[0..B] of the schedule.
+// A sequence split over k CTAs yields k pieces; pieces in total <= B + grid - 1.
+__global__ void attn_plan_kernel(const int32_t* ctx, int B, int grid, int* sp, int* po,
+                                 float* ws_ml, int64_t n_slots) {
+  // every partial slot starts as "no data" (NaN m): a CTA whose stage range is empty
+  // never writes the pieces of the sequences it sits inside, and the combine skips them
+  for (int64_t i = threadIdx.x; i < 2 * n_slots; i += blockDim.x) ws_ml[i] = __int_as_float(0x7fffffff);
+  __shared__ int warp_sum[32];
+  __shared__ int carry;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  auto block_scan = [&](int v) -> int {  // exclusive scan over the block, + carry
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = lane < nw ? warp_sum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      if (lane < nw) warp_sum[lane] = w;
+    }
+    __syncthreads();
+    const int excl = carry + (wid ? warp_sum[wid - 1] : 0) + x - v;
+    __syncthreads();
+    if (tid == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+    return excl;
+  };
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < B; b0 += blockDim.x) {
+    const int b = b0 + tid;
+    const int n = b < B ? (max(ctx[b], 0) + kMmaStage - 1) / kMmaStage : 0;
+    const int e = block_scan(n);
+    if (b < B) sp[b] = e;
+  }
+  if (tid == 0) sp[B] = carry;
+  __syncthreads();
+  const int64_t S = carry;
+  __syncthreads();
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < B; b0 += blockDim.x) {
+    const int b = b0 + tid;
+    int pieces = 0;
+    if (b < B && S > 0) {
+      const int first = sp[b], last = sp[b + 1] - 1;
+      if (last >= first) pieces = stage_owner(last, S, grid) - stage_owner(first, S, grid) + 1;
+    }
+    const int e = block_scan(pieces);
+    if (b < B) po[b] = e;
+  }
+  if (tid == 0) po[B] = carry;
+}
+
 
 template <int D, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
@@ -514,30 +584,25 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
   __syncthreads();
 
   const int G = a.n_q / a.n_kv;
-  auto geom = [&](int item, int& b, int& part, int& t0, int& nst) {
-    b = item / p.parts;
-    part = item % p.parts;
-    t0 = part * p.part_tokens;
-    const int tend = min(a.ctx[b], t0 + p.part_tokens);
-    nst = tend > t0 ? (tend - t0 + kMmaStage - 1) / kMmaStage : 0;
-  };
-  int l_item = blockIdx.x, l_st = 0;
-  auto l_norm = [&]() {
-    for (;;) {
-      if (l_item >= p.items) return;
-      int b, part, t0, nst;
-      geom(l_item, b, part, t0, nst);
-      if (l_st < nst) return;
-      l_item += gridDim.x;
-      l_st = 0;
+  const int64_t S = p.sp[a.B];
+  const int g_begin = S ? (int)((int64_t)blockIdx.x * S / gridDim.x) : 0;
+  const int g_end = S ? (int)((int64_t)(blockIdx.x + 1) * S / gridDim.x) : 0;
+  auto seq_of = [&](int g) {  // sequence holding global stage g (binary search on sp)
+    int lo = 0, hi = a.B - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (p.sp[mid] <= g) lo = mid;
+      else hi = mid - 1;
     }
+    return lo;
   };
+  // producer cursor: global stage l_g of sequence l_b
+  int l_g = g_begin, l_b = g_begin < g_end ? seq_of(g_begin) : 0;
   auto issue = [&](int buf) {  // one thread: both 8-token halves of the cursor's stage
-    int b, part, t0, nst;
-    geom(l_item, b, part, t0, nst);
-    const int tok0 = t0 + l_st * kMmaStage;
-    const int ntok = min(kMmaStage, a.ctx[b] - tok0);
-    const int row = a.rows ? a.rows[b] : b;
+    while (p.sp[l_b + 1] <= l_g) ++l_b;
+    const int tok0 = (l_g - p.sp[l_b]) * kMmaStage;
+    const int ntok = min(kMmaStage, a.ctx[l_b] - tok0);
+    const int row = a.rows ? a.rows[l_b] : l_b;
     const int halves = ntok > 8 ? 2 : 1;
     mbar_expect_tx(&full[buf], (uint32_t)(halves * p.box_bytes));
     for (int h = 0; h < halves; ++h) {
@@ -546,17 +611,14 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
       tma_load_4d(smem + buf * stage_bytes + h * p.box_bytes, &kv_map, 0, t % a.s, 0, slot, &full[buf]);
     }
   };
-  l_norm();
-  for (int i = 0; i < p.n_stage && l_item < p.items; ++i) {
+  for (int i = 0; i < p.n_stage && l_g < g_end; ++i) {
     if (tid == 0) issue(i);
-    ++l_st;
-    l_norm();
+    ++l_g;
   }
 
   const int h = warp / p.W, sub = warp % p.W;
   const bool active = h < a.n_kv;
   const float qscale = a.scale * kLog2e;
-  const int parts_total = p.parts * p.W;
   const int g4 = lane >> 2, q4 = lane & 3;
   // ldmatrix lane geometry: matrix mi = lane/8, row r = lane%8
   const int mi = lane >> 3, r8 = lane & 7;
@@ -575,9 +637,12 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
 
   int buf = 0;
   uint32_t phase = 0;
-  for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-    int b, part, t0, nst;
-    geom(item, b, part, t0, nst);
+  int b = g_begin < g_end ? seq_of(g_begin) : 0;
+  for (int g = g_begin; g < g_end;) {
+    while (p.sp[b + 1] <= g) ++b;  // skip sequences without stages
+    const int seg_end = min(g_end, p.sp[b + 1]);
+    const int st0 = g - p.sp[b];     // first stage of this segment inside sequence b
+    const int nst = seg_end - g;
     // Q^T B-fragments: n = head g4 of the group (zero beyond G), k = dims
     uint32_t qb[KT][2];
     const bool hq = active && g4 < G;
@@ -594,7 +659,7 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // heads 2*q4, 2*q4+1
 
     for (int st = 0; st < nst; ++st) {
-      const int ntok = min(kMmaStage, a.ctx[b] - (t0 + st * kMmaStage));
+      const int ntok = min(kMmaStage, a.ctx[b] - (st0 + st) * kMmaStage);
       mbar_wait(&full[buf], phase);
       if (active && st % p.W == sub) {
         if (ntok < kMmaStage) {
@@ -657,7 +722,7 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
         }
       }
       __syncwarp();
-      if (l_item < p.items) {
+      if (l_g < g_end) {
         if (lane == 0) {
           __threadfence_block();
           if (atomicAdd(&done_cnt[buf], 1) == NW - 1) {  // last reader of this buffer
@@ -667,8 +732,7 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
             issue(buf);
           }
         }
-        ++l_st;
-        l_norm();
+        ++l_g;
       }
       if (++buf == p.n_stage) {
         buf = 0;
@@ -682,10 +746,11 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
       }
       const int hA = 2 * q4, hB = hA + 1;
-      const int64_t base = (int64_t)b * a.n_q + h * G;
-      const int pslot = part * p.W + sub;
+      // partial piece of (sequence b, this CTA); slots are [piece][q head][warp of head]
+      const int piece = p.po[b] + blockIdx.x - stage_owner(p.sp[b], S, gridDim.x);
+      const int64_t base = ((int64_t)piece * a.n_q + h * G) * p.W + sub;
       if (hA < G) {
-        const int64_t pi = (base + hA) * parts_total + pslot;
+        const int64_t pi = base + (int64_t)hA * p.W;
 #pragma unroll
         for (int mt = 0; mt < KT; ++mt) {
           ws_acc[pi * D + mt * 16 + g4] = acc[mt][0];
@@ -697,7 +762,7 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
         }
       }
       if (hB < G) {
-        const int64_t pi = (base + hB) * parts_total + pslot;
+        const int64_t pi = base + (int64_t)hB * p.W;
 #pragma unroll
         for (int mt = 0; mt < KT; ++mt) {
           ws_acc[pi * D + mt * 16 + g4] = acc[mt][1];
@@ -709,7 +774,35 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
         }
       }
     }
+    g = seg_end;
   }
+}
+
+// merges the pieces (and the W warps per head) of every (sequence, q head)
+template <int D>
+__global__ void paged_attn_combine_sk(const float* ws_acc, const float* ws_ml, const int* po,
+                                      int n_q, int W, void* out) {
+  const int64_t bh = blockIdx.x;  // b * n_q + hq
+  const int b = (int)(bh / n_q), hq = (int)(bh % n_q);
+  const int d = threadIdx.x;
+  if (d >= D) return;
+  const int p0 = po[b], p1 = po[b + 1];
+  float M = -INFINITY;
+  for (int pc = p0; pc < p1; ++pc)  // fmaxf ignores the NaN of unwritten slots
+    for (int w = 0; w < W; ++w) M = fmaxf(M, ws_ml[2 * (((int64_t)pc * n_q + hq) * W + w)]);
+  float L = 0.f, O = 0.f;
+  if (M != -INFINITY) {
+    for (int pc = p0; pc < p1; ++pc)
+      for (int w = 0; w < W; ++w) {
+        const int64_t pi = ((int64_t)pc * n_q + hq) * W + w;
+        const float mp = ws_ml[2 * pi];
+        if (!(mp > -INFINITY)) continue;  // -inf (no tokens) or NaN (slot not written)
+        const float wt = exp2f(mp - M);
+        L += ws_ml[2 * pi + 1] * wt;
+        O += ws_acc[pi * D + d] * wt;
+      }
+  }
+  static_cast<__nv_bfloat16*>(out)[bh * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
 }
 
 namespace {
@@ -839,13 +932,16 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
   p.n_stage = (int)std::max<int64_t>(2, std::min<int64_t>(4, (220 * 1024 - 2048) / stage_bytes));
   const size_t smem = (size_t)(p.n_stage * stage_bytes) + 1024 /*align*/ + 128;
   p.W = NW / a.n_kv;
-  const int max_ctx = std::max(a.max_ctx, 1);
-  // ~8 items per SM; parts are whole 16-token stages
-  int parts = std::max(1, (8 * sms + a.B - 1) / a.B);
-  parts = std::min(parts, (max_ctx + kMmaStage - 1) / kMmaStage);
-  p.part_tokens = ((max_ctx + parts - 1) / parts + kMmaStage - 1) / kMmaStage * kMmaStage;
-  p.parts = (max_ctx + p.part_tokens - 1) / p.part_tokens;
-  p.items = a.B * p.parts;
+  // stream-K: the grid splits the batch's 16-token stages evenly (ragged contexts
+  // balance too); the plan kernel turns ctx into the stage / piece prefix sums
+  const int grid = sms;
+  const size_t n_pieces = (size_t)a.B + grid;              // >= pieces actually written
+  const size_t np = n_pieces * a.n_q * p.W;                 // partial slots
+  float* ws = workspace(np * (D + 2) * sizeof(float) + 2 * (a.B + 1) * sizeof(int) + 256, st);
+  int* sp = reinterpret_cast<int*>(ws + np * (D + 2));
+  int* po = sp + (a.B + 1);
+  p.sp = sp;
+  p.po = po;
 
   // tensor map: {64 elems, token in block (s), 128-B chunk of the cell, slot}
   CUtensorMap map;
@@ -863,16 +959,15 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
 
   auto kern = paged_attn_mma_kernel<D, NW>;
   PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int grid = std::max(1, std::min(p.items, sms));
-  const int64_t n_parts_total = (int64_t)p.parts * p.W;
-  const size_t np = (size_t)a.B * a.n_q * n_parts_total;
-  float* ws = workspace(np * (D + 2) * sizeof(float), st);
   KernelTimer timer("paged_attn", st);
+  attn_plan_kernel<<<1, 1024, 0, st>>>(a.ctx, a.B, grid, sp, po, ws + np * D, (int64_t)np);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
   kern<<<grid, NW * 32, smem, st>>>(map, a, p, ws, ws + np * D);
   note_launch();
   PL_CUDA(cudaGetLastError());
-  paged_attn_combine<D><<<(unsigned)(a.B * a.n_q), D, 0, st>>>(ws, ws + np * D, (int)n_parts_total,
-                                                               a.out);
+  paged_attn_combine_sk<D><<<(unsigned)(a.B * a.n_q), D, 0, st>>>(ws, ws + np * D, po, a.n_q,
+                                                                  p.W, a.out);
   note_launch();
   PL_CUDA(cudaGetLastError());
 }

@@ -73,3 +73,17 @@ def test_decode_long_context_split_k():
     err = np.abs(got - ref)
     bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
     assert np.all(err <= bound + 1e-3), float(err.max())
+
+
+@pytest.mark.parametrize("ctxs", [[3, 0, 40], [1] * 7, [0, 0, 0], [5000, 1, 1, 1, 900],
+                                  [17] * 300])
+def test_decode_ragged_schedules(ctxs):
+    """stream-K schedule edge cases: fewer stages than CTAs (empty CTA ranges inside a
+    sequence), all-empty batches, one long sequence over many CTAs, B > CTAs."""
+    got, ref = _run_case(len(ctxs), 32, 8, 128, 16, 1, 0, ctxs, seed=len(ctxs))
+    err = np.abs(got - ref)
+    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
+    assert np.all(err <= bound + 1e-3), float(err.max())
+    for b, c in enumerate(ctxs):
+        if c == 0:
+            assert np.all(got[b] == 0)
