@@ -778,31 +778,41 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
   }
 }
 
-// merges the pieces (and the W warps per head) of every (sequence, q head)
+// merges the pieces (and the W warps per head) of every (sequence, q head): one warp per
+// (sequence, q head), D/32 dims per lane, 8 warps per block
 template <int D>
-__global__ void paged_attn_combine_sk(const float* ws_acc, const float* ws_ml, const int* po,
-                                      int n_q, int W, void* out) {
-  const int64_t bh = blockIdx.x;  // b * n_q + hq
+__global__ void __launch_bounds__(256) paged_attn_combine_sk(const float* ws_acc, const float* ws_ml,
+                                                             const int* po, int n_q, int W, int64_t n_bh,
+                                                             void* out) {
+  constexpr int DL = D / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t bh = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // b * n_q + hq
+  if (bh >= n_bh) return;
   const int b = (int)(bh / n_q), hq = (int)(bh % n_q);
-  const int d = threadIdx.x;
-  if (d >= D) return;
   const int p0 = po[b], p1 = po[b + 1];
+  const int n = (p1 - p0) * W;  // partial slots of this (b, hq): pc-major, w-minor
   float M = -INFINITY;
-  for (int pc = p0; pc < p1; ++pc)  // fmaxf ignores the NaN of unwritten slots
-    for (int w = 0; w < W; ++w) M = fmaxf(M, ws_ml[2 * (((int64_t)pc * n_q + hq) * W + w)]);
-  float L = 0.f, O = 0.f;
+  for (int i = lane; i < n; i += 32)  // fmaxf ignores the NaN of unwritten slots
+    M = fmaxf(M, ws_ml[2 * (((int64_t)(p0 + i / W) * n_q + hq) * W + i % W)]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float L = 0.f, o_[DL];
+#pragma unroll
+  for (int i = 0; i < DL; ++i) o_[i] = 0.f;
   if (M != -INFINITY) {
-    for (int pc = p0; pc < p1; ++pc)
-      for (int w = 0; w < W; ++w) {
-        const int64_t pi = ((int64_t)pc * n_q + hq) * W + w;
-        const float mp = ws_ml[2 * pi];
-        if (!(mp > -INFINITY)) continue;  // -inf (no tokens) or NaN (slot not written)
-        const float wt = exp2f(mp - M);
-        L += ws_ml[2 * pi + 1] * wt;
-        O += ws_acc[pi * D + d] * wt;
-      }
+    for (int i = 0; i < n; ++i) {
+      const int64_t pi = ((int64_t)(p0 + i / W) * n_q + hq) * W + i % W;
+      const float mp = ws_ml[2 * pi];
+      if (!(mp > -INFINITY)) continue;  // -inf (no tokens) or NaN (slot not written)
+      const float wt = exp2f(mp - M);
+      L += ws_ml[2 * pi + 1] * wt;
+#pragma unroll
+      for (int k = 0; k < DL; ++k) o_[k] += ws_acc[pi * D + lane + 32 * k] * wt;
+    }
   }
-  static_cast<__nv_bfloat16*>(out)[bh * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+  __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + bh * D;
+#pragma unroll
+  for (int k = 0; k < DL; ++k) dst[lane + 32 * k] = __float2bfloat16_rn(L > 0.f ? o_[k] / L : 0.f);
 }
 
 namespace {
@@ -966,8 +976,9 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
   kern<<<grid, NW * 32, smem, st>>>(map, a, p, ws, ws + np * D);
   note_launch();
   PL_CUDA(cudaGetLastError());
-  paged_attn_combine_sk<D><<<(unsigned)(a.B * a.n_q), D, 0, st>>>(ws, ws + np * D, po, a.n_q,
-                                                                  p.W, a.out);
+  const int64_t n_bh = (int64_t)a.B * a.n_q;
+  paged_attn_combine_sk<D><<<(unsigned)((n_bh + 7) / 8), 256, 0, st>>>(ws, ws + np * D, po, a.n_q,
+                                                                      p.W, n_bh, a.out);
   note_launch();
   PL_CUDA(cudaGetLastError());
 }
