@@ -87,3 +87,55 @@ def test_decode_ragged_schedules(ctxs):
     for b, c in enumerate(ctxs):
         if c == 0:
             assert np.all(got[b] == 0)
+
+
+def test_decode_raw_entry_over_caller_pool():
+    """pl_paged_attn_decode_raw: the same kernel over a pool and block table the caller
+    owns (a pipeshift integration that keeps its own allocator)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2604_12171_b200 import _native as N
+
+    torch.manual_seed(3)
+    B, n_q, n_kv, D, s, k = 3, 32, 8, 128, 16, 2
+    cell = 2 * n_kv * D * 2
+    fp = 128
+    unit = fp + k * s * cell
+    ctxs = [33, 5, 70]
+    nb = [(c + s - 1) // s for c in ctxs]
+    max_blocks = max(nb)
+    slots = torch.randperm(sum(nb) + 3)[: sum(nb)].tolist()   # scattered slots
+    pool = torch.zeros((sum(nb) + 3) * unit, dtype=torch.uint8, device="cuda")
+    table = torch.full((B, max_blocks), -1, dtype=torch.int32)
+    kvs, i = [], 0
+    layer = 1
+    for b, c in enumerate(ctxs):
+        x = torch.randn(c, 2 * n_kv * D, dtype=torch.bfloat16, device="cuda")
+        kvs.append(x)
+        for j in range(nb[b]):
+            table[b, j] = slots[i]
+            toks = x[j * s:(j + 1) * s]
+            off = slots[i] * unit + fp + layer * s * cell
+            pool[off: off + toks.numel() * 2].copy_(toks.contiguous().view(torch.uint8).reshape(-1))
+            i += 1
+    table = table.cuda()
+    ctx_t = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    q = torch.randn(B, n_q, D, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty_like(q)
+    N.check(N.lib().pl_paged_attn_decode_raw(
+        C.c_void_p(pool.data_ptr()), unit, fp, s, k, layer, C.c_void_p(q.data_ptr()),
+        C.c_void_p(out.data_ptr()), C.c_void_p(table.data_ptr()), max_blocks,
+        C.c_void_p(ctx_t.data_ptr()), B, n_q, n_kv, D, D ** -0.5, max(ctxs), None))
+    torch.cuda.synchronize()
+    qf = bf16_to_f32(q.view(torch.int16).cpu().numpy().view(np.uint16))
+    ks, vs = [], []
+    for x in kvs:
+        u = x.view(torch.int16).cpu().numpy().view(np.uint16).reshape(-1, 2, n_kv, D)
+        ks.append(bf16_to_f32(u[:, 0]))
+        vs.append(bf16_to_f32(u[:, 1]))
+    ref = decode_attention(qf, ks, vs, D ** -0.5)
+    got = bf16_to_f32(out.view(torch.int16).cpu().numpy().view(np.uint16))
+    err = np.abs(got - ref)
+    assert np.all(err <= RTOL * np.abs(ref).max(axis=-1, keepdims=True) + 1e-3), float(err.max())
