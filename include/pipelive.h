@@ -120,6 +120,12 @@ int pl_store_append_batch(pl_store* st, int n_items, const int32_t* reqs, const 
                           const int64_t* counts, const uint64_t* seeds, const int64_t* fp_starts,
                           const void* kv_dev, int mark, int* n_done, int64_t* sched_cells_out,
                           int n_sched);
+/* the reference's own call shape batched: KvStore.append(rid, group, n, payloads) for
+ * n_items items, payloads_host = the items' fingerprints concatenated in item order
+ * (sum(counts) words); same stop-at-first-overflow contract as pl_store_append_batch */
+int pl_store_append_batch_payloads(pl_store* st, int n_items, const int32_t* reqs,
+                                   const int32_t* groups, const int64_t* counts,
+                                   const uint64_t* payloads_host, int mark, int* n_done);
 int pl_store_write_slots(pl_store* st, int32_t req, int group, int64_t n,
                          const int64_t* positions_host, const uint64_t* payloads_host);
 

@@ -284,6 +284,18 @@ int pl_store_append_batch(pl_store* st, int n_items, const int32_t* reqs, const 
   if (status != PL_OK) pl::g_err = st->s->last_msg;
   return status;
 }
+int pl_store_append_batch_payloads(pl_store* st, int n_items, const int32_t* reqs,
+                                   const int32_t* groups, const int64_t* counts,
+                                   const uint64_t* payloads, int mark, int* n_done) {
+  int status = PL_OK;
+  int rc = guard([&] {
+    status = st->s->append_batch(n_items, reqs, groups, counts, nullptr, nullptr, nullptr, mark,
+                                 nullptr, 0, n_done, payloads);
+  });
+  if (rc != PL_OK) return rc;
+  if (status != PL_OK) pl::g_err = st->s->last_msg;
+  return status;
+}
 int pl_store_write_slots(pl_store* st, int32_t req, int group, int64_t n, const int64_t* pos,
                          const uint64_t* payloads) {
   return guard([&] { st->s->write_slots(req, group, n, pos, payloads); });

@@ -335,7 +335,7 @@ struct Store {
   int append_batch(int n_items, const int32_t* reqs, const int32_t* groups,
                    const int64_t* counts, const uint64_t* seeds, const int64_t* fp_starts,
                    const void* kv_dev, int mark, int64_t* sched, int n_sched,
-                   int* n_done);  // returns status
+                   int* n_done, const uint64_t* payloads = nullptr);  // returns status
   void write_slots(int32_t req, int g, int64_t n, const int64_t* pos, const uint64_t* payloads);
   int64_t compact();
   void resize(int64_t new_cap);

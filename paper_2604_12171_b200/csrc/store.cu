@@ -510,7 +510,7 @@ void Store::append(int32_t req, int g, int64_t n, int mode, const uint64_t* payl
 int Store::append_batch(int n_items, const int32_t* reqs, const int32_t* groups,
                         const int64_t* counts, const uint64_t* seeds, const int64_t* fp_starts,
                         const void* kv_dev, int mark, int64_t* sched, int n_sched,
-                        int* n_done) {
+                        int* n_done, const uint64_t* payloads) {
   std::vector<WriteItem> items;
   items.reserve(n_items);
   int done = 0;
@@ -550,8 +550,9 @@ int Store::append_batch(int n_items, const int32_t* reqs, const int32_t* groups,
     items.push_back({req, g, start, n, seeds ? seeds[done] : 0,
                      fp_starts ? fp_starts[done] : start});
   }
-  // kv_dev rows are consumed in item order for the applied prefix
-  launch_write(items, PL_PAYLOAD_SEED, nullptr, nullptr, kv_dev, mark);
+  // kv_dev rows (and explicit payloads) are consumed in item order for the applied prefix
+  launch_write(items, payloads ? PL_PAYLOAD_EXPLICIT : PL_PAYLOAD_SEED, payloads, nullptr, kv_dev,
+               mark);
   *n_done = done;
   last_msg = msg;
   return status;

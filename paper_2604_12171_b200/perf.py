@@ -75,6 +75,27 @@ def append_batch(store: KvStore, reqs: list[int], groups: list[int], counts: lis
     return done.value
 
 
+def append_batch_payloads(store: KvStore, reqs: list[int], groups: list[int], counts: list[int],
+                          payloads: np.ndarray, mark: bool = False) -> int:
+    """KvStore.append(rid, group, n, payloads) for many items in one call: host payloads
+    (uint64, items concatenated) -> one H2D + one K1 launch."""
+    r, g, c = N.as_i32(reqs), N.as_i32(groups), N.as_i64(counts)
+    pl = np.ascontiguousarray(payloads, dtype=np.uint64)
+    done = C.c_int()
+    N.check(N.lib().pl_store_append_batch_payloads(store._h, len(r), N.ptr(r), N.ptr(g), N.ptr(c),
+                                                   N.ptr(pl), 1 if mark else 0, C.byref(done)))
+    return done.value
+
+
+def engine_payloads(seed: int, n: int) -> np.ndarray:
+    """PipelineEngine._payloads (engine.py:252-261) for positions 0..n-1, vectorised:
+    (seed * 0x9E3779B97F4A7C15 + pos * 0xBF58476D1CE4E5B9) mod 2^64, top bit cleared."""
+    pos = np.arange(n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        v = np.uint64(seed) * np.uint64(0x9E3779B97F4A7C15) + pos * np.uint64(0xBF58476D1CE4E5B9)
+    return v & np.uint64((1 << 63) - 1)
+
+
 class NativePatch:
     """A pl_patch handle for perf runs (the parity-mode owner is MigrationStream)."""
 
