@@ -147,6 +147,8 @@ int pl_store_resize(pl_store* st, int64_t new_capacity);
 int pl_store_drop_groups(pl_store* st, const int32_t* groups, int n, int64_t* out_freed_tokens);
 /* stats_out holds up to cap triples (group, consumed, allocated) in written-insertion order */
 int pl_store_free_request(pl_store* st, int32_t req, int64_t* stats_out, int cap, int* n_stats);
+/* free_request for n requests in one call (requests finishing in the same engine step) */
+int pl_store_free_requests(pl_store* st, int n, const int32_t* reqs);
 int pl_store_utilization(pl_store* st, double* out);
 /* resize instrumentation: blocks relocated, table entries remapped, bytes mapped/unmapped */
 int pl_store_last_resize_stats(pl_store* st, int64_t* out4);
@@ -206,6 +208,9 @@ int pl_patch_push(pl_patch* p, pl_store* dst, const int32_t* rank_of_req, int64_
 /* verification hooks: device popcount of the live bitmap; keys of the last device drain */
 int pl_patch_device_dirty_count(pl_patch* p, int64_t* out);
 int pl_patch_device_drained(pl_patch* p, int64_t* out);
+/* the same read enqueued on the patch's stream into caller-owned pinned memory (no sync):
+ * a pipelined driver reads each round's result while it prepares the next round */
+int pl_patch_device_drained_async(pl_patch* p, int64_t* pinned_out);
 
 /* ---- cross-process patching (one process per GPU; csrc/ipc.cu).
  * The receiver's owner exports its pools (VMM chunks as POSIX fds, sent with SCM_RIGHTS)

@@ -86,6 +86,7 @@ SIGNATURES = [
     ("pl_store_resize", C.c_int, [vp, i64]),
     ("pl_store_drop_groups", C.c_int, [vp, vp, C.c_int, P(i64)]),
     ("pl_store_free_request", C.c_int, [vp, i32, vp, C.c_int, P(C.c_int)]),
+    ("pl_store_free_requests", C.c_int, [vp, C.c_int, vp]),
     ("pl_store_utilization", C.c_int, [vp, P(dbl)]),
     ("pl_store_last_resize_stats", C.c_int, [vp, vp]),
     ("pl_store_vmm_stats", C.c_int, [vp, vp]),
@@ -109,6 +110,7 @@ SIGNATURES = [
     ("pl_patch_push", C.c_int, [vp, vp, vp, i64, P(i64), P(i64)]),
     ("pl_patch_device_dirty_count", C.c_int, [vp, P(i64)]),
     ("pl_patch_device_drained", C.c_int, [vp, P(i64)]),
+    ("pl_patch_device_drained_async", C.c_int, [vp, vp]),
     ("pl_store_layout", C.c_int, [vp, vp]),
     ("pl_store_export_group", C.c_int, [vp, C.c_int, vp, C.c_int, P(C.c_int), P(i64)]),
     ("pl_store_export_table", C.c_int, [vp, vp, P(i64), P(i64)]),

@@ -387,6 +387,12 @@ int pl_store_drop_groups(pl_store* st, const int32_t* groups, int n, int64_t* ou
 int pl_store_free_request(pl_store* st, int32_t req, int64_t* stats, int cap, int* n_stats) {
   return guard([&] { *n_stats = st->s->free_request(req, stats, cap); });
 }
+int pl_store_free_requests(pl_store* st, int n, const int32_t* reqs) {
+  return guard([&] {
+    int64_t stats[3 * 8];
+    for (int i = 0; i < n; ++i) st->s->free_request(reqs[i], stats, 8);
+  });
+}
 int pl_store_utilization(pl_store* st, double* out) {
   return guard([&] { *out = st->s->utilization(); });
 }
@@ -534,8 +540,15 @@ int pl_patch_device_dirty_count(pl_patch* p, int64_t* out) {
 int pl_patch_device_drained(pl_patch* p, int64_t* out) {
   return guard([&] {
     pl::Patch* q = live(p);
-    PL_CUDA(cudaMemcpyAsync(out, q->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, q->src->stream));
-    PL_CUDA(cudaStreamSynchronize(q->src->stream));
+    PL_CUDA(cudaMemcpyAsync(out, q->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, q->pstream()));
+    PL_CUDA(cudaStreamSynchronize(q->pstream()));
+  });
+}
+int pl_patch_device_drained_async(pl_patch* p, int64_t* pinned_out) {
+  return guard([&] {
+    pl::Patch* q = live(p);
+    PL_CUDA(cudaMemcpyAsync(pinned_out, q->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            q->pstream()));
   });
 }
 

@@ -598,6 +598,13 @@ class KvStore:
         return {int(stats[3 * i]): (int(stats[3 * i + 1]), int(stats[3 * i + 2]))
                 for i in range(min(n.value, cap))}
 
+    def free_requests(self, request_ids: Iterable) -> None:
+        """free_request for many requests at once (one C-ABI call; no per-group stats)."""
+        hs = [h for h in (self._registry.find(r) for r in request_ids) if h is not None]
+        if hs:
+            arr = N.as_i32(hs)
+            _check(N.lib().pl_store_free_requests(self._h, len(hs), N.ptr(arr)))
+
     def effective_utilization(self) -> float:
         out = C.c_double()
         _check(N.lib().pl_store_utilization(self._h, C.byref(out)))
