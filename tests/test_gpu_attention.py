@@ -139,3 +139,15 @@ def test_decode_raw_entry_over_caller_pool():
     got = bf16_to_f32(out.view(torch.int16).cpu().numpy().view(np.uint16))
     err = np.abs(got - ref)
     assert np.all(err <= RTOL * np.abs(ref).max(axis=-1, keepdims=True) + 1e-3), float(err.max())
+
+
+@pytest.mark.parametrize("n_q", [32, 64])
+def test_cuda_core_fallback_for_small_blocks(n_q):
+    """4-token blocks are outside the tensor-core kernel's envelope (8-token TMA boxes):
+    the CUDA-core kernel serves them, with the same tolerance."""
+    ctxs = [1, 17, 0, 100, 255, 33]
+    got, ref = _run_case(len(ctxs), n_q, 8, 128, 4, 2, 1, ctxs, seed=n_q)
+    err = np.abs(got - ref)
+    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
+    assert np.all(err <= bound + 1e-3), float(err.max())
+    assert np.all(got[2] == 0)

@@ -201,3 +201,26 @@ class TestDeferredReclaim:
             st.append_seeded("a", 0, 100, 1)
             st.resize(8)
             del st
+
+
+def test_free_requests_batch_equals_one_by_one():
+    from paper_2604_12171_b200 import kvstore as kv
+    from paper_2604_12171_b200.events import stable_hash
+
+    stores = []
+    for _ in range(2):
+        reg = kv.RequestRegistry()
+        st = kv.KvStore(1, 2, 16, 256, (0, 1), cell_bytes=64, registry=reg)
+        for i in range(20):
+            for g in (0, 1):
+                st.append_seeded(f"q{i}", g, 5 + 9 * i, stable_hash(f"q{i}", g))
+        stores.append(st)
+    gone = [f"q{i}" for i in range(0, 20, 3)] + ["never-seen"]
+    for r in gone:
+        stores[0].free_request(r)
+    stores[1].free_requests(gone)
+    assert repr(stores[0].state_digest()) == repr(stores[1].state_digest())
+    assert stores[0].used_blocks == stores[1].used_blocks
+    stores[0].append_seeded("new", 0, 40, 1)
+    stores[1].append_seeded("new", 0, 40, 1)
+    assert stores[0].tables["new"].chain[0].block_id == stores[1].tables["new"].chain[0].block_id
