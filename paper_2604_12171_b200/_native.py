@@ -136,14 +136,16 @@ SIGNATURES = [
 ]
 
 _lib = None
+_device_ok = False
 
 
 def load_library(path: Path | None = None, require_device: bool = True):
     """Load and type the C-ABI; raise NativeUnavailable when it cannot run here."""
-    global _lib
+    global _lib, _device_ok
     if _lib is not None and path is None:
-        if require_device:
+        if require_device and not _device_ok:
             _require_device(_lib)
+            _device_ok = True
         return _lib
     p = Path(path) if path else LIB_PATH
     if not p.exists():
@@ -170,6 +172,8 @@ def _require_device(lib) -> None:
 
 
 def lib():
+    if _device_ok:          # hot path: every ctypes call of the parity-mode control plane
+        return _lib
     return load_library()
 
 

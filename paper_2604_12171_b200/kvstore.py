@@ -335,17 +335,23 @@ class KvStore:
         _check(N.lib().pl_store_chain_slots(self._h, h, N.ptr(buf), len(buf), C.byref(n)))
         return buf[: n.value]
 
+    _WCAP = 256
+    _wg = (C.c_int32 * _WCAP)()
+    _wc = (C.c_int64 * _WCAP)()
+    _wn = C.c_int()
+
     def _written(self, h: int) -> dict[int, int]:
-        cap = 256
-        gs = np.empty(cap, dtype=np.int32)
-        cs = np.empty(cap, dtype=np.int64)
-        n = C.c_int()
-        _check(N.lib().pl_store_written(self._h, h, N.ptr(gs), N.ptr(cs), cap, C.byref(n)))
-        if n.value > cap:
-            gs = np.empty(n.value, dtype=np.int32)
-            cs = np.empty(n.value, dtype=np.int64)
-            _check(N.lib().pl_store_written(self._h, h, N.ptr(gs), N.ptr(cs), n.value, C.byref(n)))
-        return {int(g): int(c) for g, c in zip(gs[: n.value], cs[: n.value])}
+        """The request's written counts per group, in dict insertion order (one C call;
+        preallocated buffers: this is on the parity-mode control plane's hot path)."""
+        cls = KvStore
+        _check(N.lib().pl_store_written(self._h, h, cls._wg, cls._wc, cls._WCAP, C.byref(cls._wn)))
+        n = cls._wn.value
+        if n > cls._WCAP:
+            gs = (C.c_int32 * n)()
+            cs = (C.c_int64 * n)()
+            _check(N.lib().pl_store_written(self._h, h, gs, cs, n, C.byref(cls._wn)))
+            return dict(zip(gs, cs))
+        return dict(zip(cls._wg[:n], cls._wc[:n]))
 
     def written(self, request_id, group: int) -> int:
         """Fast path for ``tables[rid].written.get(group, 0)``."""
@@ -353,6 +359,11 @@ class KvStore:
         if h is None:
             return 0
         return self._written(h).get(group, 0)
+
+    def written_all(self, request_id) -> dict[int, int]:
+        """``tables[rid].written`` as a plain dict (empty when the request has no table)."""
+        h = self._registry.find(request_id)
+        return {} if h is None else self._written(h)
 
     def _sync_resident(self, wanted: set[int]) -> None:
         cur = set(self._resident_native())
@@ -484,10 +495,13 @@ class KvStore:
                                        None, seed, kv_dev, 1 if mark else 0))
 
     def append_groups_seeded(self, request_id, groups: list[int], n_tokens: int,
-                             seeds: list[int], start: int | None = None) -> tuple[int, bool]:
+                             seeds: list[int], start: int | None = None,
+                             mark: bool = False) -> tuple[int, bool]:
         """Engine path (engine.py:392-400): append n_tokens to each group in order with
         fingerprints of positions start.. (default: each group's written prefix), one K1
-        launch.  Stops at the first overflow; returns (groups done, overflowed)."""
+        launch.  Stops at the first overflow; returns (groups done, overflowed).  With
+        ``mark`` the same launch sets the dirty bits of every active migration patch
+        streaming those groups (the DirtyBitmap.mark of migrator.py:190-197)."""
         if not groups or n_tokens <= 0:
             return 0, False
         h = self._handle(request_id)
@@ -499,7 +513,8 @@ class KvStore:
         fs = None if start is None else np.full(m, start, dtype=np.int64)
         done = C.c_int()
         rc = N.lib().pl_store_append_batch(self._h, m, N.ptr(reqs), N.ptr(gs), N.ptr(counts),
-                                           N.ptr(sd), N.ptr(fs), None, 0, C.byref(done), None, 0)
+                                           N.ptr(sd), N.ptr(fs), None, 1 if mark else 0,
+                                           C.byref(done), None, 0)
         if rc == N.PL_E_KV_OVERFLOW:
             return done.value, True
         _check(rc)

@@ -97,6 +97,26 @@ def time_scenario():
             "seconds": round(time.perf_counter() - t0, 2)}
 
 
+def time_simulations():
+    """The golden runs of tests/golden/simulations.json on the reference (same builders
+    as tests/golden/make_golden.py)."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from pipeshift.simulation import Simulation
+    from scenarios import hetero_scenario
+    from test_coordinator import C_B, fig3_scenario
+
+    runs = {"fig3_seed5": (fig3_scenario(triggers=[(0.02, C_B)], num_requests=4, rate=500.0), 5),
+            "hetero_c10_seed123": (hetero_scenario(rate=7.0, n=40), 123),
+            "hetero_n60_seed7": (hetero_scenario(rate=7.0, n=60), 7)}
+    out = {}
+    for name, (scen, seed) in runs.items():
+        t0 = time.perf_counter()
+        sim = Simulation(scen, seed=seed)
+        sim.scheduler.run(until=600.0)
+        out[name] = {"seconds": round(time.perf_counter() - t0, 3), "events": len(sim.trace)}
+    return out
+
+
 def main():
     cpu = ""
     try:
@@ -108,7 +128,7 @@ def main():
     out = {"what": "reference pipeshift (CPython, 1 thread) timed in the dev container",
            "cpu": cpu, "python": platform.python_version(), "cores_used": 1,
            "append": time_append(), "bulk_round": time_bulk_round(), "resize": time_resize(),
-           "scenario": time_scenario()}
+           "scenario": time_scenario(), "simulations": time_simulations()}
     path = ROOT / "profiles" / "reference_cpu_r1.json"
     path.write_text(json.dumps(out, indent=1) + "\n")
     print(json.dumps(out, indent=1))
