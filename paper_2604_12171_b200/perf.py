@@ -426,7 +426,8 @@ def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16,
     gather/scatter push (K4+K5) is timed wall-clock with the device synchronised on
     both sides.  Plus the structured decode pattern: one key per live request and group
     (the newest token).  Source and destination share the GPU, so the bound is HBM
-    (payload read + write), not NVLink."""
+    (payload read + write), not NVLink.  ``ms`` is the round's wall time (host block
+    manager + launches + device), ``kernel_ms`` the K3 + fused-push kernels alone."""
     import torch
 
     rng = np.random.default_rng(seed)
@@ -452,7 +453,7 @@ def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16,
         rank = reg.rank()
         cases = [("decode", None)] + [(f"{r:g}", r) for r in rates]
         for name, r in cases:
-            times, keys_n = [], 0
+            times, dev, keys_n = [], [], 0
             for _ in range(rounds + 1):
                 if r is None:
                     rq, gq, st = reqs, groups, [ctx - 1] * len(reqs)
@@ -465,18 +466,25 @@ def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16,
                 patch.mark_batch(rq, gq, st, [1] * len(rq))
                 src.sync()
                 torch.cuda.synchronize(device)
+                N.check(N.lib().pl_timing_reset())
+                N.check(N.lib().pl_timing_enable(1))
                 t0 = time.perf_counter()
                 keys, cells = patch.push(dst, rank)
                 dst.sync()
                 src.sync()
                 times.append(time.perf_counter() - t0)
+                N.check(N.lib().pl_timing_enable(0))
+                dev.append(N.timing("drain")[0] + N.timing("patch_push")[0])
                 keys_n = keys
             t = float(np.median(times[1:]))
+            td = float(np.median(dev[1:])) / 1e3
             payload = keys_n * k * cell
             out.append({"tokens_per_block": s, "dirty": name, "keys": keys_n,
                         "payload_bytes": payload, "ms": round(t * 1e3, 4),
                         "gbs": round(payload / t / 1e9, 2),
-                        "hbm_gbs": round(2 * (payload + 8 * keys_n) / t / 1e9, 2)})
+                        "hbm_gbs": round(2 * (payload + 8 * keys_n) / t / 1e9, 2),
+                        "kernel_ms": round(td * 1e3, 4),
+                        "kernel_hbm_gbs": round(2 * (payload + 8 * keys_n) / td / 1e9, 2) if td else None})
         patch.close()
         del src, dst
     return out
