@@ -30,7 +30,6 @@
 namespace pl {
 
 namespace {
-constexpr int kMaxWarps = 16;
 constexpr int kMaxStageTok = 32;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -46,25 +45,6 @@ struct Vec<64> {  // 4 bf16 = 8 B per lane
   using T = uint2;
   static constexpr int N = 4;
 };
-
-__device__ __forceinline__ void unpack(const uint4& v, float* f) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 x = __bfloat1622float2(h[i]);
-    f[2 * i] = x.x;
-    f[2 * i + 1] = x.y;
-  }
-}
-__device__ __forceinline__ void unpack(const uint2& v, float* f) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float2 x = __bfloat1622float2(h[i]);
-    f[2 * i] = x.x;
-    f[2 * i + 1] = x.y;
-  }
-}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -174,7 +154,7 @@ __device__ __forceinline__ int tr_base(int hl) {
 template <int V>
 __host__ __device__ constexpr int tr_owner(int v) {
   constexpr int L = V >= 16 ? 4 : (V >= 8 ? 3 : (V >= 4 ? 2 : (V >= 2 ? 1 : 0)));
-  if (V >= 16) return v / (V / 16);
+  if (V >= 16) return v / (V >= 16 ? V / 16 : 1);
   int lane = 0;
   for (int k = 0; k < L; ++k)
     if ((v >> (L - 1 - k)) & 1) lane += 8 >> k;
