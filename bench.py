@@ -192,6 +192,17 @@ def run_reference(args, wl, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def guarded(name: str, fn):
+    """Run one extra measurement; a failure (e.g. a smaller GPU out of memory for the C3
+    fill) is recorded in the line instead of losing the whole bench line."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001 - reported, not swallowed
+        import traceback
+        traceback.print_exc(file=sys.stderr)
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
 def profile_traffic(kernel: str, n_q: int | None = None, wl=None):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` at this bench's
     shape, from the committed ncu capture (profiles/traffic_r1.json, tools/gpu_prof.sh);
@@ -249,7 +260,7 @@ def main() -> None:
     c3 = None
     if not args.skip_c3 and rank == 0:
         from paper_2604_12171_b200.perf import c3_live_resize
-        c3 = c3_live_resize(dev)
+        c3 = guarded("c3_live_resize", lambda: c3_live_resize(dev))
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
     barrier(world)
@@ -321,38 +332,39 @@ def main() -> None:
     pause = c2 = decode = decode_70b = wstage = resize = None
     if not args.only_step:
         # ---- switch pause (data-path part): residual patch after one decode round + barrier
-        pause = measure_switch_pause(rig, stream, torch, wl)
+        pause = guarded("switch_pause", lambda: measure_switch_pause(rig, stream, torch, wl))
 
         # ---- C2 timeline: live migration on a side stream under steady decode
         if not args.skip_c2:
             from paper_2604_12171_b200.perf import c2_live
-            c2 = c2_live(rig, stream)
+            c2 = guarded("c2_live", lambda: c2_live(rig, stream))
 
         # ---- paged-attention decode over the source stage (16 layers): the 8B shape
         # (GQA 4) and the 70B shape (64 q heads over the same 8 KV heads x 128, GQA 8)
-        decode = measure_decode(rig, stream, torch, wl, hbm_peak, K, W)
-        decode_70b = measure_decode(rig, stream, torch, wl, hbm_peak, K, W, n_q=64)
+        decode = guarded("decode", lambda: measure_decode(rig, stream, torch, wl, hbm_peak, K, W))
+        decode_70b = guarded("decode_70b", lambda: measure_decode(rig, stream, torch, wl, hbm_peak,
+                                                                     K, W, n_q=64))
 
         # ---- AddLayerWeights on the copy engine: the 8 migrating layers' weights
-        wstage = measure_weight_stage(rig, stream, torch, wl, dev)
+        wstage = guarded("weight_stage", lambda: measure_weight_stage(rig, stream, torch, wl, dev))
 
         # ---- resize latency: post-commit cleanup on the source (drop, shrink, regrow)
-        resize = measure_resize(rig, stream, torch, wl)
+        resize = guarded("resize", lambda: measure_resize(rig, stream, torch, wl))
 
     # ---- C5: dirty-rate x block-size sweep of one patch round (configs[4], 1 GPU)
     sweep = None
     if not args.skip_sweep and rank == 0:
         from paper_2604_12171_b200.perf import c5_sweep
-        sweep = c5_sweep(dev)
+        sweep = guarded("c5_sweep", lambda: c5_sweep(dev))
 
     # ---- e2e: KV arrives from pinned host memory every step, result read back
     if ring is not None:
         ring.close()
     e2e = e2e_kv = None
     if not args.skip_e2e:
-        e2e = measure_e2e_api(rig, stream, torch, wl, K, world)
+        e2e = guarded("e2e", lambda: measure_e2e_api(rig, stream, torch, wl, K, world))
         # a heavier variant: the real 17 GB of KV bytes stream from pinned host memory
-        e2e_kv = measure_e2e(rig, stream, torch, wl, K, world)
+        e2e_kv = guarded("e2e_real_kv", lambda: measure_e2e(rig, stream, torch, wl, K, world))
     rig.destroy()
     if ring is not None:
         ring.dst.close()
