@@ -193,6 +193,8 @@ class PatchReceiver:
         self._send_hello()
         self.rounds = 0
         self.items_reserved = 0
+        self.table_reexports = 0   # block table reallocated mid-migration -> re-exported
+        self.pool_reexports = 0
 
     def _pool_state(self):
         return tuple(self.store.group_base(g) for g in self.groups), self.store.info()["mapped_bytes"]
@@ -228,9 +230,11 @@ class PatchReceiver:
         if table_version(self.store) != self._table:
             update["table"] = export_table(self.store)
             self._table = table_version(self.store)
+            self.table_reexports += 1
         if self._pool_state() != self._pools:
             update["pools"], fds = export_groups(self.store, self.groups)
             self._pools = self._pool_state()
+            self.pool_reexports += 1
         self.chan.send(("reserved", done.value, err, update), fds)
         for fd in fds:
             os.close(fd)

@@ -3,18 +3,23 @@ on cuda:0, in separate processes, exactly like two stage processes on two GPUs."
 
 import random
 
-N_REQ = 12
-K, S, CELL, CAP = 2, 16, 256, 512
+K, S, CELL, CAP = 2, 16, 256, 2048
 
 
-def names():
-    return [f"r{i:04d}" for i in range(N_REQ)]
+def n_req(seed):
+    # seeds >= 100: more requests than the receiver's initial block-table rows (64), so
+    # its table is reallocated mid-migration and re-exported to the sender
+    return 90 if seed >= 100 else 12
 
 
-def _registry():
+def names(seed):
+    return [f"r{i:04d}" for i in range(n_req(seed))]
+
+
+def _registry(seed):
     from paper_2604_12171_b200 import kvstore
     reg = kvstore.RequestRegistry()
-    for n in names():          # both processes assign the same handles
+    for n in names(seed):      # both processes assign the same handles
         reg.handle(n)
     return reg
 
@@ -22,11 +27,12 @@ def _registry():
 def ops(seed):
     """(initial fill, per-round decode/prefill writes) of the source stage"""
     rng = random.Random(seed)
-    fill = [(n, g, 5 + rng.randrange(60)) for n in names()[: N_REQ - 3] for g in range(4)]
+    nm = names(seed)
+    fill = [(n, g, 5 + rng.randrange(60)) for n in nm[: len(nm) // 2] for g in range(4)]
     rounds = []
     for _ in range(4):
         w = []
-        for n in rng.sample(names(), 6):     # includes requests that join mid-migration
+        for n in rng.sample(nm, min(len(nm) - 1, 40)):   # includes requests that join later
             for g in rng.sample(range(4), 2):
                 w.append((n, g, 1 + rng.randrange(20)))
         rounds.append(w)
@@ -65,13 +71,13 @@ def receiver(q, chan_name, seed):
         import torch
         torch.cuda.set_device(0)
         from paper_2604_12171_b200 import dist as D
-        reg = _registry()
+        reg = _registry(seed)
         st = dst_store(reg)
         chan = D.Channel(chan_name, server=True)
         rx = D.PatchReceiver(st, [2, 3], chan)
         while rx.serve():
             pass
-        q.put(("rx", summary(st), rx.rounds))
+        q.put(("rx", summary(st), rx.rounds, rx.table_reexports))
     except Exception as e:  # pragma: no cover - reported to the parent
         import traceback
         q.put(("rx-error", traceback.format_exc(), repr(e)))
@@ -82,7 +88,7 @@ def sender(q, chan_name, seed):
         import torch
         torch.cuda.set_device(0)
         from paper_2604_12171_b200 import dist as D
-        reg = _registry()
+        reg = _registry(seed)
         st = src_store(reg)
         fill, rounds = ops(seed)
         apply_writes(st, fill, mark=False)
@@ -103,7 +109,7 @@ def sender(q, chan_name, seed):
 def single_process(seed):
     """The same rounds with both stores in one process (local fused push)."""
     from paper_2604_12171_b200.perf import NativePatch
-    reg = _registry()
+    reg = _registry(seed)
     src, dst = src_store(reg), dst_store(reg)
     dst.resident_groups |= {2, 3}
     fill, rounds = ops(seed)
