@@ -22,12 +22,13 @@ def _free_port():
     return p
 
 
-def _run_dist(live):
+def _run_dist(live, target=None, world=3):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     prefix = f"dl-{os.getpid()}-{port}"
-    procs = [ctx.Process(target=W.stage, args=(r, 3, port, prefix, q, live)) for r in range(3)]
+    procs = [ctx.Process(target=target or W.stage, args=(r, world, port, prefix, q, live))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -54,3 +55,20 @@ def test_process_per_stage_live_reconfig_matches_single_process():
         assert live[r][0] == want
     # after the switch: rank 0 keeps layer 1, rank 1 layers 2-3, rank 2 layer 4
     assert live[0][1] == [0] and live[1][1] == [1, 2] and live[2][1] == [3]
+
+
+def test_eight_stage_uneven_resplit_matches_single_process():
+    """BASELINE configs[3] shape: 8 stage processes, a 16-layer model split evenly, re-split
+    live into an uneven split: 6 pairs move a layer each, concurrently; ranks 2, 3, 6 and
+    7 send one layer while receiving another (the global pair order keeps this
+    deadlock-free)."""
+    from paper_2604_12171_b200.llama import LlamaConfig, StagedLlama, generate, init_weights
+
+    cfg = LlamaConfig(n_layers=16)
+    m = StagedLlama(cfg, init_weights(cfg, 1), W.CONF_EVEN8)
+    want = generate(m, W.PROMPTS, W.JOINS, W.N_GEN)
+    live = _run_dist(True, target=W.stage8, world=8)
+    for r in range(8):
+        assert live[r][0] == want, r
+    for g, layers in W.CONF_UNEVEN8.items():
+        assert live[g - 1][1] == [l - 1 for l in layers]
