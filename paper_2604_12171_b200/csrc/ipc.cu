@@ -131,7 +131,8 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
       PL_CUDA(cudaEventRecord(ev_src, src->stream));
       PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
     }
-    const uint8_t* d_apply = stage_mask(mask);
+    const uint8_t* d_apply =
+        n_applied >= (int64_t)drained.size() ? nullptr : stage_mask(mask);  // all reserved
     CopyLaunch c{};
     c.mode = 2;
     c.cells = d_cells;

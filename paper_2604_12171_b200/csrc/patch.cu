@@ -471,7 +471,8 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
       PL_CUDA(cudaEventRecord(ev_src, src->stream));
       PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
     }
-    const uint8_t* d_apply = stage_mask(mask);
+    // every drained item was reserved (no KvOverflow): no mask needed, the copy applies all
+    const uint8_t* d_apply = status == PL_OK ? nullptr : stage_mask(mask);
     PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
     CopyLaunch c{};
     c.mode = 2;
