@@ -309,43 +309,74 @@ class StagedLlama:
 
 def generate(model: StagedLlama, prompts: list[list[int]], joins: list[int], n_gen: int,
              reconfig: tuple[int, dict] | None = None, switch_at: int | None = None,
-             record: list | None = None) -> list[list[int]]:
+             record: list | None = None, trace=None) -> list[list[int]]:
     """Greedy decode of len(prompts) requests that join at steps `joins`, one token per
     request per step (prompt tokens are fed one at a time).  `reconfig` = (step, target
     config) starts a live reconfiguration after that step; `switch_at` commits it.
-    `record` (optional) receives (rids, tokens, positions, logits) per step."""
-    with model.on_stream():
-        return _generate(model, prompts, joins, n_gen, reconfig, switch_at, record)
-
-
-def _generate(model, prompts, joins, n_gen, reconfig, switch_at, record):
+    `record` (optional) receives (rids, tokens, positions, logits) per step; `trace`
+    (an events.EventTrace) receives the run's events in the reference's trace schema with
+    wall-clock times, so engine.compute_metrics gives TTFT/TPOT (engine.py:112-184)."""
     torch = model.torch
+
+    def step(rids, toks, poss):
+        tok_t = torch.tensor(toks, dtype=torch.long, device=f"cuda:{model.device}")
+        logits = model.step(rids, tok_t)
+        nxt = logits.argmax(-1).tolist()
+        if record is not None:
+            record.append((rids, toks, poss, logits.cpu().numpy()))
+        return nxt
+
+    with model.on_stream():
+        return _drive(model, step, prompts, joins, n_gen, reconfig, switch_at, trace,
+                      lambda: bool(model.patches))
+
+
+def _drive(model, step, prompts, joins, n_gen, reconfig, switch_at, trace, migrating):
+    import time
+
+    t_start = time.perf_counter()
+
+    def emit(kind, **payload):
+        if trace is not None:
+            trace.emit(time.perf_counter() - t_start, "engine", kind, **payload)
+
     B = len(prompts)
     outs: list[list[int]] = [[] for _ in range(B)]
     t = 0
     while any(len(o) < n_gen for o in outs):
         act = [b for b in range(B) if joins[b] <= t and len(outs[b]) < n_gen]
+        for b in act:
+            if t == joins[b]:
+                emit("request_arrival", id=f"seq{b}", input_len=len(prompts[b]), output_len=n_gen)
         if act:
             toks, poss = [], []
             for b in act:
                 p = t - joins[b]
                 toks.append(prompts[b][p] if p < len(prompts[b]) else outs[b][-1])
                 poss.append(p)
-            rids = [f"seq{b}" for b in act]
-            tok_t = torch.tensor(toks, dtype=torch.long, device=f"cuda:{model.device}")
-            logits = model.step(rids, tok_t)
-            nxt = logits.argmax(-1).tolist()
-            if record is not None:
-                record.append((rids, toks, poss, logits.cpu().numpy()))
+            t_step = time.perf_counter()
+            nxt = step([f"seq{b}" for b in act], toks, poss)
+            emit("decode_step", step=t, batch=len(act),
+                 ms=round((time.perf_counter() - t_step) * 1e3, 4))
             for b, p, n in zip(act, poss, nxt):
                 if p >= len(prompts[b]) - 1:
                     outs[b].append(int(n))
+                    if len(outs[b]) == 1:
+                        emit("first_token", id=f"seq{b}")
+                    if len(outs[b]) == n_gen:
+                        emit("request_done", id=f"seq{b}")
         if reconfig is not None and t == reconfig[0]:
+            emit("reconfigure_start", target={str(k): v for k, v in reconfig[1].items()})
             model.start_reconfig(reconfig[1])
-        elif model.patches:
+            emit("migration_seeded")
+        elif migrating():
             model.pump()
+            emit("patch_round")
         if switch_at is not None and t == switch_at:
+            emit("commit_pause_start")
             model.switch()
+            emit("commit_pause_end")
+            emit("reconfigure_end", outcome="success")
         t += 1
     return outs
 
@@ -497,31 +528,33 @@ class DistStagedLlama:
         self.moving = {}
 
 
+def step_latency_around_switch(trace) -> dict:
+    """Median decode-step latency before the reconfiguration, while it migrates, and after
+    the switch (TPOT across the switch), plus the pause."""
+    phase, out = "before", {"before": [], "migrating": [], "after": []}
+    pause = 0.0
+    t0 = None
+    for ev in trace:
+        if ev.kind == "reconfigure_start":
+            phase = "migrating"
+        elif ev.kind == "commit_pause_start":
+            t0 = ev.time
+        elif ev.kind == "commit_pause_end":
+            pause += ev.time - t0
+            phase = "after"
+        elif ev.kind == "decode_step":
+            out[phase].append(ev.payload["ms"])
+    res = {k: (round(float(np.median(v)), 4) if v else None) for k, v in out.items()}
+    res["steps"] = {k: len(v) for k, v in out.items()}
+    res["pause_ms"] = round(pause * 1e3, 4)
+    return res
+
+
 def generate_dist(model: DistStagedLlama, prompts: list[list[int]], joins: list[int], n_gen: int,
                   reconfig: tuple[int, dict] | None = None,
-                  switch_at: int | None = None) -> list[list[int]]:
-    """generate() with the stages in separate processes; every rank returns the tokens."""
+                  switch_at: int | None = None, trace=None) -> list[list[int]]:
+    """generate() with the stages in separate processes; every rank returns the tokens
+    (pass `trace` on one rank to record the run's events)."""
     with model.on_stream():
-        B = len(prompts)
-        outs: list[list[int]] = [[] for _ in range(B)]
-        t = 0
-        while any(len(o) < n_gen for o in outs):
-            act = [b for b in range(B) if joins[b] <= t and len(outs[b]) < n_gen]
-            if act:
-                toks, poss = [], []
-                for b in act:
-                    p = t - joins[b]
-                    toks.append(prompts[b][p] if p < len(prompts[b]) else outs[b][-1])
-                    poss.append(p)
-                nxt = model.step_tokens([f"seq{b}" for b in act], toks)
-                for b, p, n in zip(act, poss, nxt):
-                    if p >= len(prompts[b]) - 1:
-                        outs[b].append(int(n))
-            if reconfig is not None and t == reconfig[0]:
-                model.start_reconfig(reconfig[1])
-            elif model.moving:
-                model.pump()
-            if switch_at is not None and t == switch_at:
-                model.switch()
-            t += 1
-        return outs
+        return _drive(model, lambda rids, toks, poss: model.step_tokens(rids, toks), prompts,
+                      joins, n_gen, reconfig, switch_at, trace, lambda: bool(model.moving))

@@ -90,3 +90,23 @@ def test_logits_and_tokens_match_numpy_oracle(s):
                 decisive += 1
     print(f"s={s}: worst logit err {worst:.4f} of max|logit|, decisive {decisive}/{total}")
     assert decisive >= 0.85 * total, (decisive, total)
+
+
+def test_live_run_trace_in_reference_schema():
+    """The live run's events use the reference trace schema, so compute_metrics gives the
+    serving metrics (TTFT/TPOT, pause, outcome) of a real run."""
+    from paper_2604_12171_b200.engine import compute_metrics
+    from paper_2604_12171_b200.events import EventTrace
+    from paper_2604_12171_b200.llama import (LlamaConfig, StagedLlama, generate, init_weights,
+                                              step_latency_around_switch)
+
+    cfg = LlamaConfig()
+    m = StagedLlama(cfg, init_weights(cfg, 0), CONF_A)
+    tr = EventTrace()
+    generate(m, PROMPTS, JOINS, N_GEN, reconfig=(10, CONF_B), switch_at=20, trace=tr)
+    met = compute_metrics(tr)
+    assert met.completed == len(PROMPTS) and met.reconfig_outcome == "success"
+    assert met.ttft_mean > 0 and met.tpot_mean > 0 and met.stop_time > 0
+    lat = step_latency_around_switch(tr)
+    assert lat["steps"]["before"] == 11 and lat["steps"]["migrating"] == 10
+    assert lat["pause_ms"] > 0
