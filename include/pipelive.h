@@ -159,6 +159,14 @@ int pl_store_last_resize_stats(pl_store* st, int64_t* out4);
  * the store was created, and physical bytes not yet back with the driver.  reclaim
  * forces every pending unmap + release now (blocking), returns the wait in ms. */
 int pl_store_vmm_stats(pl_store* st, int64_t* out4);
+/* ahead of a planned resize(new_capacity) with `groups` resident afterwards (e.g. the
+ * post-commit b_new, coordinator.py:340-354, known once the target is chosen): create the
+ * physical chunks the grow will need on the reclaimer thread now, beyond the cached ones
+ * and those of groups that will be dropped first.  Best effort (stops on out-of-memory);
+ * prepare_wait blocks until the creation is done and returns the wait in ms. */
+int pl_store_prepare_grow(pl_store* st, int64_t new_capacity, const int32_t* groups, int n,
+                          int64_t* chunks_requested);
+int pl_store_prepare_wait(pl_store* st, double* out_ms);
 int pl_store_reclaim(pl_store* st, double* out_ms);
 
 /* ---- device views for kernels outside the store (K2 attention, perf drivers) */

@@ -91,6 +91,8 @@ SIGNATURES = [
     ("pl_store_last_resize_stats", C.c_int, [vp, vp]),
     ("pl_store_vmm_stats", C.c_int, [vp, vp]),
     ("pl_store_reclaim", C.c_int, [vp, P(dbl)]),
+    ("pl_store_prepare_grow", C.c_int, [vp, i64, vp, C.c_int, P(i64)]),
+    ("pl_store_prepare_wait", C.c_int, [vp, P(dbl)]),
     ("pl_store_group_base", C.c_int, [vp, C.c_int, P(u64)]),
     ("pl_store_table_dev", C.c_int, [vp, P(u64), P(i64)]),
     ("pl_store_flush", C.c_int, [vp]),

@@ -406,7 +406,7 @@ int pl_store_vmm_stats(pl_store* st, int64_t* out4) {
     pl::Store* s = st->s;
     int64_t tail = 0, cache = 0, created = 0;
     for (auto& a : s->arenas) {
-      tail += (int64_t)a.last_tail_reused;
+      tail += (int64_t)a.last_tail_reused + (int64_t)a.last_prepared;  // mapped ahead
       cache += (int64_t)a.last_cache_reused;
       created += (int64_t)a.last_created;
     }
@@ -414,6 +414,19 @@ int pl_store_vmm_stats(pl_store* st, int64_t* out4) {
     out4[1] = cache;
     out4[2] = created;
     out4[3] = s->reclaimer->pending();
+  });
+}
+int pl_store_prepare_grow(pl_store* st, int64_t new_capacity, const int32_t* groups, int n,
+                          int64_t* chunks_requested) {
+  return guard([&] {
+    const int64_t c = st->s->prepare_grow(new_capacity, groups, n);
+    if (chunks_requested) *chunks_requested = c;
+  });
+}
+int pl_store_prepare_wait(pl_store* st, double* out_ms) {
+  return guard([&] {
+    const double ms = st->s->reclaimer->wait_prepared();
+    if (out_ms) *out_ms = ms;
   });
 }
 int pl_store_reclaim(pl_store* st, double* out_ms) {

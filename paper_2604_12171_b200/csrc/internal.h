@@ -66,10 +66,27 @@ struct Reclaimer {
   std::vector<CUmemGenericAllocationHandle> take(size_t n);  // unmapped cached chunks
   double wait_all(bool release_cache);  // finish every job (and release the cache)
   int64_t pending();                    // physical bytes not yet back with the driver
+  // planned grow: map n chunks at [va, va + n*chunk) on the helper thread (cached chunks
+  // first, then cuMemCreate; best effort) and set their access; adopt() hands the mapped
+  // chunks to the arena (waits if the job runs, drops it if it has not started)
+  uint64_t submit_prepare(CUdeviceptr va, size_t n, const std::vector<int>& peers);
+  std::vector<CUmemGenericAllocationHandle> adopt(uint64_t id, size_t* created);
+  double wait_prepared();
+  size_t cached();
   double last_unmap_ms = 0;
 
  private:
   void loop();
+  struct Prep {
+    uint64_t id = 0;
+    CUdeviceptr va = 0;
+    size_t n = 0, created = 0;
+    std::vector<int> peers;
+    std::vector<CUmemGenericAllocationHandle> hs;
+    bool done = false;
+  };
+  std::vector<std::unique_ptr<Prep>> preps;
+  uint64_t prep_running = 0;
   std::mutex mu;
   std::condition_variable cv;
   std::vector<std::unique_ptr<Job>> jobs;
@@ -92,18 +109,21 @@ struct Arena {
   std::vector<int> peer_devices;  // devices granted access besides `device`
   Reclaimer* rc = nullptr;
   uint64_t tail_job = 0;          // retired tail still mapped (pending reclaim job)
+  uint64_t prep_job = 0;          // tail being mapped ahead of a planned grow
   // instrumentation of the last resize: chunks taken back from the mapped tail,
   // re-mapped from the reclaimer's cache, created with cuMemCreate
-  size_t last_tail_reused = 0, last_cache_reused = 0, last_created = 0;
+  size_t last_tail_reused = 0, last_cache_reused = 0, last_created = 0, last_prepared = 0;
 
   size_t mapped_bytes() const { return chunks.size() * chunk_bytes; }
   void ensure(size_t bytes);                  // map chunks until mapped >= bytes
   void trim(size_t bytes, cudaStream_t st);   // retire chunks wholly beyond `bytes`
   void release(cudaStream_t st);              // retire everything + the reservation
   void grant_peer(int dev);
+  void prepare(size_t bytes);                 // map the tail for a planned grow, async
 
  private:
   void reclaim_tail();
+  void adopt_prepared();
 };
 size_t vmm_granularity(int device);
 // VMM IPC: export a pool chunk as a POSIX fd / import one, map it into a reservation
@@ -340,6 +360,10 @@ struct Store {
   int64_t compact();
   void resize(int64_t new_cap);
   int64_t drop_groups(const int32_t* groups, int n);
+  // ahead of resize(new_cap) with `groups` resident: physical chunks the grow will need
+  // beyond the reclaimer's cache and the chunks of groups about to be dropped are created
+  // on the reclaimer thread now; returns the chunks requested
+  int64_t prepare_grow(int64_t new_cap, const int32_t* groups, int n);
   int free_request(int32_t req, int64_t* stats, int cap);
   double utilization() const;
   void add_groups(const int32_t* groups, int n);

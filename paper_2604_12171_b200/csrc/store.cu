@@ -721,6 +721,18 @@ void Store::resize(int64_t new_cap) {
   last_resize[3] = before - mapped_bytes();
 }
 
+int64_t Store::prepare_grow(int64_t new_cap, const int32_t* groups, int n) {
+  int64_t asked = 0;
+  const int64_t want = (std::max<int64_t>(new_cap, 1) * unit_bytes + chunk_bytes - 1) / chunk_bytes;
+  for (int i = 0; i < n; ++i) {
+    const int g = groups[i];
+    if (g < 0 || g >= n_model_groups || !materialised[g]) continue;
+    asked += std::max<int64_t>(0, want - (int64_t)arenas[g].chunks.size());
+    arenas[g].prepare((size_t)want * (size_t)chunk_bytes);
+  }
+  return asked;
+}
+
 int64_t Store::drop_groups(const int32_t* groups_in, int n) {
   std::vector<int32_t> groups(groups_in, groups_in + n);
   std::sort(groups.begin(), groups.end());

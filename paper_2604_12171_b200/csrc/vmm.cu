@@ -17,6 +17,7 @@
 // mapped tail back (no driver call at all) or re-maps cached physical chunks
 // (no cuMemCreate).  cuMemCreate failing with out-of-memory forces every pending
 // reclaim first, so memory pressure turns the deferral off.
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
@@ -174,9 +175,15 @@ Reclaimer::~Reclaimer() {
   }
   cv.notify_all();
   th.join();
-  // the thread finished every job; return the cached chunks
+  // the thread finished every job; return the cached chunks and any prepared (mapped,
+  // never adopted) tail -- its arena was released without growing into it
   for (auto& c : cache) drv().Release(c.first);
   cache.clear();
+  for (auto& p : preps) {
+    if (!p->hs.empty()) drv().Unmap(p->va, p->hs.size() * chunk_bytes);
+    for (auto h : p->hs) drv().Release(h);
+  }
+  preps.clear();
 }
 
 uint64_t Reclaimer::submit(cudaStream_t st, CUdeviceptr va, size_t bytes,
@@ -217,6 +224,58 @@ bool Reclaimer::cancel(uint64_t id, CUdeviceptr* va, std::vector<CUmemGenericAll
   // started (or done): wait until its range is unmapped so it can be mapped again
   cv.wait(lk, [&] { return running != id; });
   return false;
+}
+
+uint64_t Reclaimer::submit_prepare(CUdeviceptr va, size_t n, const std::vector<int>& peers) {
+  auto p = std::make_unique<Prep>();
+  p->va = va;
+  p->n = n;
+  p->peers = peers;
+  uint64_t id;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    id = p->id = ++next_id;
+    preps.push_back(std::move(p));
+  }
+  cv.notify_all();
+  return id;
+}
+
+std::vector<CUmemGenericAllocationHandle> Reclaimer::adopt(uint64_t id, size_t* created) {
+  std::unique_lock<std::mutex> lk(mu);
+  auto find = [&] {
+    return std::find_if(preps.begin(), preps.end(),
+                        [&](const std::unique_ptr<Prep>& x) { return x->id == id; });
+  };
+  auto it = find();
+  if (it == preps.end()) return {};
+  if (!(*it)->done && prep_running != id) {  // not started: drop the request
+    preps.erase(it);
+    return {};
+  }
+  cv.wait(lk, [&] { return find() == preps.end() || (*find())->done; });
+  it = find();
+  if (it == preps.end()) return {};
+  std::vector<CUmemGenericAllocationHandle> hs = std::move((*it)->hs);
+  if (created) *created = (*it)->created;
+  preps.erase(it);
+  return hs;
+}
+
+double Reclaimer::wait_prepared() {
+  const auto t0 = Clock::now();
+  std::unique_lock<std::mutex> lk(mu);
+  cv.wait(lk, [&] {
+    for (auto& p : preps)
+      if (!p->done) return false;
+    return true;
+  });
+  return ms_since(t0);
+}
+
+size_t Reclaimer::cached() {
+  std::lock_guard<std::mutex> lk(mu);
+  return cache.size();
 }
 
 std::vector<CUmemGenericAllocationHandle> Reclaimer::take(size_t n) {
@@ -280,7 +339,42 @@ void Reclaimer::loop() {
       cv.notify_all();
       continue;
     }
-    // 2. cached chunks past their release time go back to the driver
+    // 2. a planned grow (prepare_grow): map chunks at the arena's tail now, off the
+    //    caller's critical path (cached chunks first, then cuMemCreate), and set their
+    //    access in one call; the arena adopts them at its next ensure
+    auto pit = std::find_if(preps.begin(), preps.end(),
+                            [](const std::unique_ptr<Prep>& x) { return !x->done; });
+    if (pit != preps.end() && !stopping) {
+      Prep* pr = pit->get();
+      prep_running = pr->id;
+      std::vector<CUmemGenericAllocationHandle> hs;
+      while (hs.size() < pr->n && !cache.empty()) {
+        hs.push_back(cache.back().first);
+        cache.pop_back();
+        pending_bytes -= (int64_t)chunk_bytes;
+      }
+      lk.unlock();
+      CUmemAllocationProp prop = prop_for(device);
+      while (hs.size() < pr->n) {
+        CUmemGenericAllocationHandle h = 0;
+        if (d.Create(&h, chunk_bytes, &prop, 0) != CUDA_SUCCESS) break;  // best effort
+        hs.push_back(h);
+        ++pr->created;
+      }
+      size_t mapped = 0;
+      for (; mapped < hs.size(); ++mapped)
+        if (d.Map(pr->va + mapped * chunk_bytes, chunk_bytes, 0, hs[mapped], 0) != CUDA_SUCCESS) break;
+      for (size_t i = mapped; i < hs.size(); ++i) d.Release(hs[i]);
+      hs.resize(mapped);
+      if (mapped) set_access(pr->va, mapped * chunk_bytes, device, pr->peers);
+      lk.lock();
+      pr->hs = std::move(hs);
+      pr->done = true;
+      prep_running = 0;
+      cv.notify_all();
+      continue;
+    }
+    // 3. cached chunks past their release time go back to the driver
     bool released = false;
     for (size_t i = 0; i < cache.size();) {
       if (cache[i].second <= now || flush_cache) {
@@ -300,7 +394,7 @@ void Reclaimer::loop() {
       continue;
     }
     if (stopping && jobs.empty()) break;
-    // 3. sleep until the next deadline or a new job
+    // 4. sleep until the next deadline or a new job
     auto wake = now + std::chrono::seconds(3600);
     for (auto& j : jobs) wake = std::min(wake, j->due);
     for (auto& c : cache) wake = std::min(wake, c.second);
@@ -330,7 +424,28 @@ void Arena::reclaim_tail() {
   }
 }
 
+void Arena::adopt_prepared() {
+  if (!prep_job) return;
+  size_t created = 0;
+  std::vector<CUmemGenericAllocationHandle> hs = rc->adopt(prep_job, &created);
+  prep_job = 0;
+  // mapped (with access) at va + (chunks.size() + i) * chunk_bytes by the reclaimer thread
+  chunks.insert(chunks.end(), hs.begin(), hs.end());
+  last_prepared += hs.size();
+  (void)created;  // created on the helper thread, off the critical path
+}
+
+void Arena::prepare(size_t bytes) {
+  adopt_prepared();
+  reclaim_tail();
+  const size_t want_chunks = (bytes + chunk_bytes - 1) / chunk_bytes;
+  if (!va || want_chunks <= chunks.size() || want_chunks * chunk_bytes > va_bytes) return;
+  prep_job = rc->submit_prepare(va + chunks.size() * chunk_bytes, want_chunks - chunks.size(),
+                                peer_devices);
+}
+
 void Arena::ensure(size_t bytes) {
+  adopt_prepared();
   if (bytes <= mapped_bytes()) return;
   Driver& d = drv();
   reclaim_tail();
@@ -338,8 +453,9 @@ void Arena::ensure(size_t bytes) {
   size_t want_chunks = (bytes + chunk_bytes - 1) / chunk_bytes;
   size_t want_va = want_chunks * chunk_bytes;
   if (want_va > va_bytes) {
-    // grow the reservation: new range (2x headroom), remap existing chunks there
-    size_t new_va_bytes = std::max(want_va, va_bytes * 2);
+    // grow the reservation: new range with headroom (4x the first time, so later grows --
+    // and prepared grows -- map in place), remap existing chunks there
+    size_t new_va_bytes = std::max(want_va, va ? va_bytes * 2 : want_va * 4);
     CUdeviceptr nva = 0;
     CUresult rr = d.AddressReserve(&nva, new_va_bytes, 0, 0, 0);
     if (rr != CUDA_SUCCESS)
@@ -397,6 +513,7 @@ void Arena::ensure(size_t bytes) {
 
 void Arena::trim(size_t bytes, cudaStream_t st) {
   size_t keep = (bytes + chunk_bytes - 1) / chunk_bytes;
+  adopt_prepared();
   reclaim_tail();  // one contiguous retired tail per arena
   if (keep >= chunks.size()) return;
   std::vector<CUmemGenericAllocationHandle> tail(chunks.begin() + (long)keep, chunks.end());
@@ -411,6 +528,7 @@ void Arena::trim(size_t bytes, cudaStream_t st) {
 
 void Arena::release(cudaStream_t st) {
   if (!va) return;
+  adopt_prepared();
   reclaim_tail();
   // the byte count must be taken before `chunks` is moved into the by-value parameter
   // (argument evaluation order is unspecified)
@@ -424,6 +542,7 @@ void Arena::release(cudaStream_t st) {
 void Arena::grant_peer(int dev) {
   for (int p : peer_devices)
     if (p == dev) return;
+  adopt_prepared();
   peer_devices.push_back(dev);
   set_access(va, chunks.size() * chunk_bytes, device, peer_devices);
 }

@@ -588,6 +588,20 @@ class KvStore:
         return {"tail_reused_chunks": int(out[0]), "cache_reused_chunks": int(out[1]),
                 "created_chunks": int(out[2]), "pending_reclaim_bytes": int(out[3])}
 
+    def prepare_grow(self, new_capacity: int, groups: Iterable[int]) -> int:
+        """Create, on the reclaimer thread, the physical chunks a planned
+        resize(new_capacity) with `groups` resident will need; returns chunks requested."""
+        g = N.as_i32(sorted(groups))
+        out = C.c_int64()
+        _check(N.lib().pl_store_prepare_grow(self._h, new_capacity, N.ptr(g), len(g),
+                                             C.byref(out)))
+        return out.value
+
+    def prepare_wait(self) -> float:
+        out = C.c_double()
+        _check(N.lib().pl_store_prepare_wait(self._h, C.byref(out)))
+        return out.value
+
     def reclaim(self) -> float:
         """Finish every deferred unmap/release now; returns the wait in ms."""
         out = C.c_double()

@@ -224,3 +224,27 @@ def test_free_requests_batch_equals_one_by_one():
     stores[0].append_seeded("new", 0, 40, 1)
     stores[1].append_seeded("new", 0, 40, 1)
     assert stores[0].tables["new"].chain[0].block_id == stores[1].tables["new"].chain[0].block_id
+
+
+def test_prepare_grow_creates_the_chunks_ahead():
+    """prepare_grow maps the tail a planned grow needs on the reclaimer thread (cached
+    chunks first, then new ones); the grow then only adopts it: no cuMemCreate, no map on
+    the critical path; KV survives."""
+    from paper_2604_12171_b200 import kvstore as kv
+
+    st = kv.KvStore(1, 2, 16, 64, (0, 1, 2), cell_bytes=4096, chunk_bytes=2 << 20)
+    for i in range(6):
+        st.append_seeded(f"a{i}", 0, 50, i)
+        st.append_seeded(f"a{i}", 2, 50, 10 + i)
+    keep = st.read_cell("a4", 0, 49, 1)
+    asked = st.prepare_grow(256, (0, 2))
+    assert asked > 0
+    st.prepare_wait()
+    v0 = st.vmm_stats()
+    st.drop_layer_groups([1])
+    st.resize(256)
+    v1 = st.vmm_stats()
+    assert v1["created_chunks"] == v0["created_chunks"]
+    assert v1["tail_reused_chunks"] - v0["tail_reused_chunks"] >= asked
+    assert st.read_cell("a4", 0, 49, 1) == keep
+    st.append_seeded("big", 2, 16 * 200, 3)
