@@ -475,6 +475,14 @@ void Arena::ensure(size_t bytes) {
   const size_t first = chunks.size();
   const size_t need = want_chunks - first;
   std::vector<CUmemGenericAllocationHandle> hs = rc->take(need);
+  if (hs.size() < need && rc->pending() > 0) {
+    // other pools of this store retired chunks that are still waiting out their grace
+    // period: unmapping them now and re-mapping them here is much cheaper than creating
+    // new ones while the helper thread contends for the driver
+    rc->wait_all(false);
+    auto more = rc->take(need - hs.size());
+    hs.insert(hs.end(), more.begin(), more.end());
+  }
   last_cache_reused += hs.size();
   CUmemAllocationProp p = prop_for(device);
   bool forced = false;
