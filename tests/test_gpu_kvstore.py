@@ -248,3 +248,24 @@ def test_prepare_grow_creates_the_chunks_ahead():
     assert v1["tail_reused_chunks"] - v0["tail_reused_chunks"] >= asked
     assert st.read_cell("a4", 0, 49, 1) == keep
     st.append_seeded("big", 2, 16 * 200, 3)
+
+
+def test_prepare_grow_then_shrink_or_teardown():
+    """A prepared (mapped, not yet adopted) tail is adopted by a shrink and retired with
+    the rest of the tail; a store torn down with a prepared tail releases it."""
+    from paper_2604_12171_b200 import kvstore as kv
+
+    st = kv.KvStore(1, 2, 16, 64, (0, 1), cell_bytes=4096, chunk_bytes=2 << 20)
+    st.append_seeded("a", 0, 300, 1)
+    keep = st.read_cell("a", 0, 299, 1)
+    assert st.prepare_grow(512, (0, 1)) > 0
+    st.resize(32)                       # adopts the prepared tail, then retires it
+    assert st.read_cell("a", 0, 299, 1) == keep
+    st.reclaim()
+    assert st.vmm_stats()["pending_reclaim_bytes"] == 0
+    st.resize(128)
+    st.append_seeded("b", 1, 16 * 100, 2)
+    for _ in range(3):
+        t = kv.KvStore(1, 2, 16, 64, (0,), cell_bytes=4096, chunk_bytes=2 << 20)
+        t.prepare_grow(1024, (0,))
+        del t                           # prepared tail never adopted
