@@ -326,7 +326,6 @@ void launch_drain_snapshot(uint32_t* bits, uint32_t* snap, int64_t n_words, int6
                            cudaStream_t st) {
   const int64_t tiles = drain_tiles(n_words);
   if (tiles <= 0) return;
-  KernelTimer timer("drain", st);
   drain_snapshot_kernel<<<(unsigned)tiles, kDrainThreads, 0, st>>>(bits, snap, n_words,
                                                                    tile_counts);
   note_launch();

@@ -303,11 +303,14 @@ int64_t Patch::device_drain_compact() {
     PL_CUDA(cudaEventRecord(ev_src, src->stream));
     PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
   }
-  launch_drain_snapshot(old, d_snap, n_words, d_tile_counts, ps);
-  PL_CUDA(cudaEventRecord(ev_snap, ps));
-  snap_recorded = true;
-  launch_drain_scan(d_tile_counts, drain_tiles(n_words), d_count, ps);
-  launch_drain_emit(d_snap, n_words, d_tile_counts, d_cells, cells_cap, ps);
+  {
+    KernelTimer timer("drain", ps);  // K3: snapshot + clear, tile scan, ordered emit
+    launch_drain_snapshot(old, d_snap, n_words, d_tile_counts, ps);
+    PL_CUDA(cudaEventRecord(ev_snap, ps));
+    snap_recorded = true;
+    launch_drain_scan(d_tile_counts, drain_tiles(n_words), d_count, ps);
+    launch_drain_emit(d_snap, n_words, d_tile_counts, d_cells, cells_cap, ps);
+  }
   return drained_keys;
 }
 
