@@ -342,6 +342,10 @@ struct Store {
   // order this store's stream after every attached patch's side-stream reads of the
   // source (K3/K4 on Patch::stream) -- before slots are released, moved or dropped
   void order_after_patches();
+  // single-process multi-GPU: let kernels on `peer` read this store's device buffers
+  // (block table, bases: CUDA peer access) and read/write its pools (VMM access)
+  void grant_peer_access(int peer);
+  std::vector<int> peer_granted;
   void* scratch(size_t bytes);
   void* pinned(size_t bytes);
   void materialise(int g);

@@ -405,6 +405,8 @@ void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t
   if (!in_flight) fail(PL_E_STATE, "no drained patch in flight");
   if (dst->k != src->k || dst->cell_bytes != src->cell_bytes)
     fail(PL_E_INVALID, "source and destination layouts differ");
+  // staged path across GPUs: the scatter on the destination reads the source's staging
+  if (dst->device != src->device) src->grant_peer_access(dst->device);
   std::vector<uint8_t> mask;
   int status = PL_OK;
   extend_dst(dst, rank, n_rank, stale, n_stale, mask, &status);
@@ -448,6 +450,9 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   if (in_flight) fail(PL_E_STATE, "a drained patch of this pair is still in flight");
   if (dst->k != src->k || dst->cell_bytes != src->cell_bytes)
     fail(PL_E_INVALID, "source and destination layouts differ");
+  // one process, two GPUs: the source's SMs store into the destination's pools over
+  // NVLink and read its block table
+  if (dst->device != src->device) dst->grant_peer_access(src->device);
   static const bool trace = std::getenv("PL_TRACE_PUSH") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };

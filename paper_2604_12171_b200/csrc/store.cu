@@ -301,6 +301,23 @@ void Upload::go(size_t extra_device_bytes) {
   PL_CUDA(cudaEventRecord(st->pinned_ev, st->stream));
 }
 
+void Store::grant_peer_access(int peer) {
+  if (peer == device) return;
+  for (int d : peer_granted)
+    if (d == peer) return;
+  int ok = 0;
+  PL_CUDA(cudaDeviceCanAccessPeer(&ok, peer, device));
+  if (!ok) fail(PL_E_CUDA, "device " + std::to_string(peer) + " cannot access device " +
+                               std::to_string(device) + " (no P2P / NVLink path)");
+  PL_CUDA(cudaSetDevice(peer));
+  cudaError_t e = cudaDeviceEnablePeerAccess(device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+  else PL_CUDA(e);
+  PL_CUDA(cudaSetDevice(device));
+  for (auto& a : arenas) a.grant_peer(peer);  // pools mapped now and later
+  peer_granted.push_back(peer);
+}
+
 void Store::order_after_patches() {
   for (Patch* p : patches) {
     if (!p->stream || p->stream == stream) continue;
