@@ -48,7 +48,7 @@ def drain_log(monkeypatch):
     return log
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", range(80))
 def test_gpu_migration_matches_reference(ns, golden, drain_log, seed):
     case = golden("migration_cases.json")[seed]
     res = opgen.run_migration_case(ns, case["case"], {"cell_bytes": 64})

@@ -65,7 +65,7 @@ class _OracleNS:
     MigrationManager = OracleMigrationManager
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", range(80))
 def test_oracle_replays_reference_migrations(golden, seed):
     case = golden("migration_cases.json")[seed]
     res = opgen.run_migration_case(_OracleNS, case["case"])
