@@ -308,11 +308,13 @@ class StagedLlama:
 
 
 def generate(model: StagedLlama, prompts: list[list[int]], joins: list[int], n_gen: int,
-             reconfig: tuple[int, dict] | None = None, switch_at: int | None = None,
-             record: list | None = None, trace=None) -> list[list[int]]:
+             reconfig: tuple[int, dict] | None = None, switch_at: int | str | None = None,
+             record: list | None = None, trace=None, tau: int = 50) -> list[list[int]]:
     """Greedy decode of len(prompts) requests that join at steps `joins`, one token per
     request per step (prompt tokens are fed one at a time).  `reconfig` = (step, target
-    config) starts a live reconfiguration after that step; `switch_at` commits it.
+    config) starts a live reconfiguration after that step; `switch_at` commits it (a step,
+    or "converged": at the first step whose lag -- cells written since the last patch
+    round -- is below `tau`, the reference's dirty-set threshold).
     `record` (optional) receives (rids, tokens, positions, logits) per step; `trace`
     (an events.EventTrace) receives the run's events in the reference's trace schema with
     wall-clock times, so engine.compute_metrics gives TTFT/TPOT (engine.py:112-184)."""
@@ -328,10 +330,11 @@ def generate(model: StagedLlama, prompts: list[list[int]], joins: list[int], n_g
 
     with model.on_stream():
         return _drive(model, step, prompts, joins, n_gen, reconfig, switch_at, trace,
-                      lambda: bool(model.patches))
+                      lambda: bool(model.patches), tau)
 
 
-def _drive(model, step, prompts, joins, n_gen, reconfig, switch_at, trace, migrating):
+def _drive(model, step, prompts, joins, n_gen, reconfig, switch_at, trace, migrating,
+           tau: int = 50):
     import time
 
     t_start = time.perf_counter()
@@ -365,14 +368,22 @@ def _drive(model, step, prompts, joins, n_gen, reconfig, switch_at, trace, migra
                         emit("first_token", id=f"seq{b}")
                     if len(outs[b]) == n_gen:
                         emit("request_done", id=f"seq{b}")
+        converged = False
         if reconfig is not None and t == reconfig[0]:
             emit("reconfigure_start", target={str(k): v for k, v in reconfig[1].items()})
             model.start_reconfig(reconfig[1])
             emit("migration_seeded")
         elif migrating():
-            model.pump()
-            emit("patch_round")
-        if switch_at is not None and t == switch_at:
+            # the safe-switch test (migrator.py:341-348, tau = 50 cells by default,
+            # scenario.py:82): cells written since the last round and not yet patched
+            lag = model.lag()
+            emit("convergence_check", lag=lag, tau=tau)
+            if switch_at == "converged" and lag < tau:
+                converged = True
+            else:
+                model.pump()
+                emit("patch_round")
+        if converged or (switch_at is not None and t == switch_at):
             emit("commit_pause_start")
             model.switch()
             emit("commit_pause_end")
@@ -501,6 +512,18 @@ class DistStagedLlama:
             elif pair in self.receivers:
                 assert self.receivers[pair].serve()
 
+    def lag(self) -> int:
+        """Dirty cells not yet patched, summed over every pair of every rank (all ranks
+        take the same switch decision)."""
+        import torch
+
+        mine = sum(tx.dirty_keys() for tx in self.senders.values())
+        t = torch.tensor([mine], dtype=torch.int64)
+        if self.link.backend == "nccl":
+            t = t.cuda(self.device)
+        self.link.dist.all_reduce(t, group=self.group)
+        return int(t.item())
+
     def switch(self) -> None:
         # the commit waits for the arriving layers' weights (coordinator.py:239-240)
         self.stager.wait()
@@ -552,9 +575,10 @@ def step_latency_around_switch(trace) -> dict:
 
 def generate_dist(model: DistStagedLlama, prompts: list[list[int]], joins: list[int], n_gen: int,
                   reconfig: tuple[int, dict] | None = None,
-                  switch_at: int | None = None, trace=None) -> list[list[int]]:
+                  switch_at: int | str | None = None, trace=None,
+                  tau: int = 50) -> list[list[int]]:
     """generate() with the stages in separate processes; every rank returns the tokens
     (pass `trace` on one rank to record the run's events)."""
     with model.on_stream():
         return _drive(model, lambda rids, toks, poss: model.step_tokens(rids, toks), prompts,
-                      joins, n_gen, reconfig, switch_at, trace, lambda: bool(model.moving))
+                      joins, n_gen, reconfig, switch_at, trace, lambda: bool(model.moving), tau)

@@ -23,7 +23,7 @@ def stage(rank, world, port, prefix, q, live):
         m = DistStagedLlama(cfg, init_weights(cfg, 0), CONF_A, rank, channel_prefix=prefix)
         outs = generate_dist(m, PROMPTS, JOINS, N_GEN,
                              reconfig=(10, CONF_B) if live else None,
-                             switch_at=20 if live else None)
+                             switch_at=("converged" if live == "converged" else 20) if live else None)
         q.put((rank, outs, sorted(m.store.resident_groups)))
         dist.barrier()
         dist.destroy_process_group()

@@ -50,9 +50,12 @@ def test_process_per_stage_live_reconfig_matches_single_process():
     want = generate(m, W.PROMPTS, W.JOINS, W.N_GEN)
     static = _run_dist(False)
     live = _run_dist(True)
+    conv = _run_dist("converged")   # switch decided by the dirty-set threshold (tau = 50)
     for r in range(3):
         assert static[r][0] == want
         assert live[r][0] == want
+        assert conv[r][0] == want
+        assert conv[r][1] == live[r][1]
     # after the switch: rank 0 keeps layer 1, rank 1 layers 2-3, rank 2 layer 4
     assert live[0][1] == [0] and live[1][1] == [1, 2] and live[2][1] == [3]
 

@@ -110,3 +110,21 @@ def test_live_run_trace_in_reference_schema():
     lat = step_latency_around_switch(tr)
     assert lat["steps"]["before"] == 11 and lat["steps"]["migrating"] == 10
     assert lat["pause_ms"] > 0
+
+
+def test_switch_decided_by_the_dirty_set_threshold():
+    """switch_at="converged": the run switches at the first step whose unpatched cells are
+    below tau (migrator.py:341-348), with tokens identical to the static run."""
+    from paper_2604_12171_b200.events import EventTrace
+    from paper_2604_12171_b200.llama import LlamaConfig, StagedLlama, generate, init_weights
+
+    _, base, _, _ = _run()
+    cfg = LlamaConfig()
+    m = StagedLlama(cfg, init_weights(cfg, 0), CONF_A)
+    tr = EventTrace()
+    outs = generate(m, PROMPTS, JOINS, N_GEN, reconfig=(10, CONF_B), switch_at="converged",
+                    trace=tr)
+    assert outs == base and m.config() == CONF_B
+    checks = [ev.payload["lag"] for ev in tr if ev.kind == "convergence_check"]
+    pause = [ev for ev in tr if ev.kind == "commit_pause_start"]
+    assert len(pause) == 1 and checks[-1] < 50
