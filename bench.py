@@ -441,6 +441,7 @@ def measure_decode(rig, stream, torch, wl, hbm_peak, K, W, n_q=None) -> dict:
     ctx = torch.full((B,), ctx_now, dtype=torch.int32, device="cuda")
     q = torch.randn(B, n_q, wl.head_dim, dtype=torch.bfloat16, device="cuda")
     out = torch.empty_like(q)
+    torch.cuda.synchronize()   # q/rows/ctx come from torch's stream; decode runs on `stream`
     layers = [(g, j) for g in wl.src_groups for j in range(wl.k)]
 
     def step():

@@ -82,6 +82,9 @@ int pl_store_create(int device, int gpu_id, int stacking_factor, int tokens_per_
                     pl_store** out);
 int pl_store_destroy(pl_store* st);
 int pl_store_set_stream(pl_store* st, void* stream);
+/* order the store's stream after all work already enqueued on `stream` (NULL = the CUDA
+ * default stream): call before handing the store device buffers produced there (kv_dev) */
+int pl_store_wait_stream(pl_store* st, void* stream);
 int pl_store_get_info(pl_store* st, pl_store_info* out);
 /* resident_groups mutation (coordinator.py:205-206, kvstore.py:308); maps/unmaps pools */
 int pl_store_add_groups(pl_store* st, const int32_t* groups, int n);
@@ -254,7 +257,8 @@ int pl_patch_push_remote(pl_patch* p, pl_remote* r, int64_t n_items_applied);
  * q_dev [B, n_q, head_dim] bf16; out_dev [B, n_q, head_dim] bf16.
  * req_rows_dev [B] int32 request handles (rows of the store's block table);
  * ctx_lens_dev [B] int32; layer_in_group selects the layer inside the group's unit.
- * Cell layout per (token, layer): [K: n_kv*head_dim bf16][V: n_kv*head_dim bf16]. */
+ * Cell layout per (token, layer): [K: n_kv*head_dim bf16][V: n_kv*head_dim bf16].
+ * `stream` NULL = the CUDA default stream; the store's pending writes are ordered before. */
 int pl_paged_attn_decode(pl_store* st, int group, int layer_in_group, const void* q_dev,
                          void* out_dev, const int32_t* req_rows_dev, const int32_t* ctx_lens_dev,
                          int batch, int n_q_heads, int n_kv_heads, int head_dim, float scale,

@@ -60,6 +60,7 @@ SIGNATURES = [
                                   C.c_int, i64, P(vp)]),
     ("pl_store_destroy", C.c_int, [vp]),
     ("pl_store_set_stream", C.c_int, [vp, vp]),
+    ("pl_store_wait_stream", C.c_int, [vp, vp]),
     ("pl_store_get_info", C.c_int, [vp, P(StoreInfo)]),
     ("pl_store_add_groups", C.c_int, [vp, vp, C.c_int]),
     ("pl_store_remove_groups", C.c_int, [vp, vp, C.c_int]),

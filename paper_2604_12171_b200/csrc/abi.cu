@@ -144,6 +144,19 @@ int pl_store_set_stream(pl_store* st, void* stream) {
     st->s->stream = stream ? static_cast<cudaStream_t>(stream) : st->s->own_stream;
   });
 }
+int pl_store_wait_stream(pl_store* st, void* stream) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    cudaStream_t cs = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    if (cs == s->stream) return;
+    PL_CUDA(cudaSetDevice(s->device));
+    cudaEvent_t ev;
+    PL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    PL_CUDA(cudaEventRecord(ev, cs));
+    PL_CUDA(cudaStreamWaitEvent(s->stream, ev, 0));
+    PL_CUDA(cudaEventDestroy(ev));
+  });
+}
 int pl_store_get_info(pl_store* st, pl_store_info* o) {
   return guard([&] {
     pl::Store* s = st->s;
@@ -577,7 +590,9 @@ int pl_paged_attn_decode(pl_store* st, int group, int layer, const void* q, void
       pl::fail(PL_E_INVALID, "cell_bytes != 2 * n_kv_heads * head_dim * 2");
     if (layer < 0 || layer >= s->k) pl::fail(PL_E_INVALID, "layer_in_group out of range");
     s->flush();
-    cudaStream_t cs = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+    // NULL is the CUDA default (legacy) stream, as everywhere in CUDA: q/out/rows/ctx were
+    // most likely produced there; the store's work is ordered before it below
+    cudaStream_t cs = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
     if (cs != s->stream) {
       // table deltas were pushed on the store stream
       cudaEvent_t ev;

@@ -491,8 +491,21 @@ class KvStore:
         if n_tokens <= 0:
             return
         h = self._handle(request_id)
+        if kv_dev is not None:
+            self.wait_for_caller_stream()
         _check(N.lib().pl_store_append(self._h, h, layer_group, n_tokens, N.PL_PAYLOAD_SEED,
                                        None, seed, kv_dev, 1 if mark else 0))
+
+    def wait_for_caller_stream(self, stream_ptr: int | None = None) -> None:
+        """Order the store's stream after the caller's (default: torch's current stream),
+        so device buffers the caller just produced (kv_dev) are complete when K1 reads."""
+        if stream_ptr is None:
+            try:
+                import torch
+                stream_ptr = torch.cuda.current_stream(self.device).cuda_stream
+            except Exception:  # pragma: no cover - torch is plumbing only
+                stream_ptr = 0
+        _check(N.lib().pl_store_wait_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
 
     def append_groups_seeded(self, request_id, groups: list[int], n_tokens: int,
                              seeds: list[int], start: int | None = None,

@@ -68,6 +68,8 @@ def append_batch(store: KvStore, reqs: list[int], groups: list[int], counts: lis
     c = N.as_i64(counts)
     sd = N.as_u64(seeds)
     done = C.c_int()
+    if kv_dev is not None:
+        store.wait_for_caller_stream()
     rc = N.lib().pl_store_append_batch(store._h, len(reqs), N.ptr(r), N.ptr(g), N.ptr(c),
                                        N.ptr(sd), None, kv_dev, 1 if mark else 0, C.byref(done),
                                        None, 0)
@@ -230,6 +232,7 @@ def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
     ctx_now = [rig.src.tables[rid(i)].written.get(wl.src_groups[0], 0) for i in range(B)]
     q = torch.randn(B, wl.n_q, wl.head_dim, dtype=torch.bfloat16, device=dev)
     out = torch.empty_like(q)
+    torch.cuda.synchronize(dev)   # produced on torch's stream, read on the stage's stream
     reqs = [h for h in rig.handles for _ in wl.src_groups]
     groups = [g for _ in rig.handles for g in wl.src_groups]
     seeds = [stable_hash(rid(i), g) for i in range(B) for g in wl.src_groups]
