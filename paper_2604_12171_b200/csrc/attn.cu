@@ -726,6 +726,25 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
       }
       const int hA = 2 * q4, hB = hA + 1;
+      if (p.W == 1 && p.po[b + 1] - p.po[b] == 1) {
+        // the whole sequence was this CTA's: normalise and write the bf16 output here
+        // (the combine skips it); no partial round trip through global memory
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + ((int64_t)b * a.n_q + h * G) * D;
+        const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+#pragma unroll
+        for (int mt = 0; mt < KT; ++mt) {
+          if (hA < G) {
+            o[hA * D + mt * 16 + g4] = __float2bfloat16_rn(acc[mt][0] * i0);
+            o[hA * D + mt * 16 + g4 + 8] = __float2bfloat16_rn(acc[mt][2] * i0);
+          }
+          if (hB < G) {
+            o[hB * D + mt * 16 + g4] = __float2bfloat16_rn(acc[mt][1] * i1);
+            o[hB * D + mt * 16 + g4 + 8] = __float2bfloat16_rn(acc[mt][3] * i1);
+          }
+        }
+        g = seg_end;
+        continue;
+      }
       // partial piece of (sequence b, this CTA); slots are [piece][q head][warp of head]
       const int piece = p.po[b] + blockIdx.x - stage_owner(p.sp[b], S, gridDim.x);
       const int64_t base = ((int64_t)piece * a.n_q + h * G) * p.W + sub;
@@ -770,6 +789,7 @@ __global__ void __launch_bounds__(256) paged_attn_combine_sk(const float* ws_acc
   if (bh >= n_bh) return;
   const int b = (int)(bh / n_q), hq = (int)(bh % n_q);
   const int p0 = po[b], p1 = po[b + 1];
+  if (W == 1 && p1 - p0 == 1) return;  // written by the decode kernel itself
   const int n = (p1 - p0) * W;  // partial slots of this (b, hq): pc-major, w-minor
   float M = -INFINITY;
   for (int i = lane; i < n; i += 32)  // fmaxf ignores the NaN of unwritten slots
