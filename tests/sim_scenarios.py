@@ -80,6 +80,8 @@ def golden_runs():
         "fig3_seed5": (fig3_scenario(triggers=[(0.02, C_B)], num_requests=4, rate=500.0), 5, None),
         "hetero_c10_seed123": (hetero_scenario(rate=7.0, n=40), 123, None),
         "hetero_n60_seed7": (hetero_scenario(rate=7.0, n=60), 7, None),
+        # = the reference's packaged pkg/scenarios/heterogeneous_shift.yaml, seed 0
+        "packaged_yaml_seed0": (hetero_scenario(rate=8.0, n=200), 0, None),
         "fig3_nopatch": (fig3_scenario(triggers=[(0.02, C_B)], num_requests=4, rate=500.0,
                                        flags=FeatureFlags(kv_patch=False)), 5, None),
     }

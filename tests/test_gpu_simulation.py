@@ -26,7 +26,8 @@ def _run(name):
 
 
 @pytest.mark.parametrize("name", ["fig3_seed5", "fig3_nopatch", "stoptime_L4", "stoptime_L8",
-                                  "hetero_c10_seed123", "hetero_n60_seed7"])
+                                  "hetero_c10_seed123", "hetero_n60_seed7",
+                                  "packaged_yaml_seed0"])
 def test_run_matches_reference(golden, name):
     want = golden("simulations.json")[name]
     sim, res = _run(name)
