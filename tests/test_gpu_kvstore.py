@@ -269,3 +269,52 @@ def test_prepare_grow_then_shrink_or_teardown():
         t = kv.KvStore(1, 2, 16, 64, (0,), cell_bytes=4096, chunk_bytes=2 << 20)
         t.prepare_grow(1024, (0,))
         del t                           # prepared tail never adopted
+
+
+def test_acceptance_criterion_3_randomized_allocator_ops():
+    """Acceptance criterion 3 (pkg/tests/test_acceptance.py:104-150): 10,500 randomized
+    append / free / compact / resize ops on a 48-block store (k=2, 8-token blocks, two
+    groups) never lose a checksum, shrink-below-live fires exactly when live > target,
+    within 10 s -- here on the GPU store, checked against a host shadow."""
+    import random
+    import time
+
+    from paper_2604_12171_b200 import kvstore as kv
+
+    t0 = time.time()
+    rng = random.Random(3003)
+    st = kv.KvStore(1, 2, 8, 48, (0, 1))
+    shadow: dict = {}
+    reqs = [f"r{i}" for i in range(10)]
+    for op in range(1, 10_501):
+        roll, req = rng.random(), rng.choice(reqs)
+        if roll < 0.5:
+            g, n = rng.choice((0, 1)), rng.randint(1, 20)
+            pay = [rng.randrange(2 ** 40) for _ in range(n)]
+            try:
+                st.append(req, g, n, pay)
+                shadow.setdefault((req, g), []).extend(pay)
+            except kv.KvOverflow:
+                pass
+        elif roll < 0.65:
+            st.free_request(req)
+            shadow.pop((req, 0), None)
+            shadow.pop((req, 1), None)
+        elif roll < 0.8:
+            st.compact()
+        else:
+            target, live = rng.randint(0, 56), st.used_blocks
+            try:
+                st.resize(target)
+                assert live <= target
+            except kv.CapacityBelowLive:
+                assert live > target
+        if op % 500 == 0:
+            for (rid, g), pays in shadow.items():
+                for pos in range(len(pays)):
+                    assert st.read_checksum(rid, g, pos) == pays[pos]
+        else:
+            for (rid, g), pays in list(shadow.items())[:3]:
+                pos = rng.randrange(len(pays))
+                assert st.read_checksum(rid, g, pos) == pays[pos]
+    assert time.time() - t0 < 10.0, time.time() - t0
