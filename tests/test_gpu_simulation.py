@@ -121,3 +121,32 @@ def test_baseline_config_matches_reference_with_extension(golden, name):
     assert {str(g): s.capacity_blocks for g, s in sim.stores.items()} == want["capacities"]
     assert compute_metrics(sim.trace).as_row() == want["metrics"]
     assert sim.state_digest() == want["state_digest"]
+
+
+def test_acceptance_criterion_6_stop_time_ablation():
+    """Acceptance criterion 6 (pkg/tests/test_acceptance.py:203-248) on the GPU data plane:
+    with KV patching the pause stays flat in the number of migrated layers and within the
+    analytic bound (residual < tau cells + control overhead); stop-and-copy pauses grow
+    with the layer count and exceed the patching pauses tenfold."""
+    from paper_2604_12171_b200 import FeatureFlags
+    from paper_2604_12171_b200.simulation import Simulation
+
+    tau = 50
+    patch, copy = {}, {}
+    for n in (4, 8, 12):
+        for flags, out in ((None, patch), (FeatureFlags(kv_patch=False, async_weights=False), copy)):
+            scen, fill = sim_scenarios.stoptime_scenario(migrate_layers=n, flags=flags)
+            sim = Simulation(scen, seed=0)
+            fill(sim)
+            sim.scheduler.run(until=600.0)
+            assert sim.statuses[0].outcome == "success"
+            out[n] = sim.statuses[0].pause_duration
+    for n in (4, 8, 12):
+        assert copy[n] >= 10 * patch[n]
+    assert copy[12] > copy[8] > copy[4]
+    assert max(patch.values()) / min(patch.values()) < 2.0
+    scen, _ = sim_scenarios.stoptime_scenario()
+    for n, pause in patch.items():
+        bound = tau * scen.model.token_kv_bytes_per_layer * n / scen.fabric.link_bandwidth \
+            + 8 * scen.fabric.control_latency
+        assert pause <= bound
