@@ -35,6 +35,51 @@ def hetero_scenario(rate=7.0, n=120, k=2, triggers=True, flags=None, tau=50) -> 
                     flags=flags or FeatureFlags())
 
 
+def _random_partition(rng, total: int, parts: int) -> list[int]:
+    """`total` layer groups cut into `parts` positive runs (pkg/tests/helpers.py:36-40)."""
+    cuts = sorted(rng.sample(range(1, total), parts - 1)) if parts > 1 else []
+    bounds = [0] + cuts + [total]
+    return [bounds[i + 1] - bounds[i] for i in range(parts)]
+
+
+def _partition_config(counts: list[int], k: int, ids: list[int]) -> PPConfig:
+    """Consecutive layer ranges of counts[i] groups each (pkg/tests/helpers.py:43-51)."""
+    out, start = [], 1
+    for gid, groups in zip(ids, counts):
+        end = start + groups * k - 1
+        out.append((gid, (start, end)))
+        start = end + 1
+    return PPConfig(out)
+
+
+def random_e2e_scenario(seed: int) -> Scenario:
+    """The randomized reconfiguration scenarios of acceptance criterion 4
+    (pkg/tests/scenarios.py:87-117): 2-4 GPUs, 8-32 layers, same draws in the same order."""
+    import random
+
+    rng = random.Random(seed)
+    n_gpus = rng.randint(2, 4)
+    k = rng.choice([1, 2, 4])
+    groups = rng.randint(max(n_gpus, 8 // k), 8)
+    cluster = [GpuSpec(id=i, mem_total=rng.choice([16, 32]) * GIB, mem_bandwidth=1e12,
+                       prefill_cost=rng.choice([1e-6, 2e-6, 4e-6]),
+                       decode_cost=rng.choice([5e-6, 1e-5, 2e-5]))
+               for i in range(1, n_gpus + 1)]
+    model = ModelSpec(num_layers=groups * k, layer_weight_bytes=rng.choice([256, 512]) * MIB,
+                      token_kv_bytes_per_layer=rng.choice([32, 64]) * KIB, stacking_factor=k,
+                      activation_bytes_per_token=8 * KIB)
+    ids = list(range(1, n_gpus + 1))
+    cur = _partition_config(_random_partition(rng, groups, n_gpus), k, ids)
+    tgt = _partition_config(_random_partition(rng, groups, n_gpus), k, ids)
+    rate = rng.uniform(40.0, 120.0)
+    pattern = rng.choice(["prefill_heavy", "decode_heavy"])
+    n = rng.randint(4, 8)
+    wl = WorkloadSpec(pattern, rate=rate, num_requests=n, jitter=rng.random() < 0.5)
+    trigger_at = (n / rate) * rng.uniform(0.3, 0.8)
+    return Scenario(cluster=cluster, model=model, initial_config=cur, workload=wl,
+                    triggers=[ReconfigTrigger(at=trigger_at, target=tgt, tau=50)])
+
+
 def stoptime_scenario(migrate_layers=4, flags=None, ghost_tokens=6000):
     model = ModelSpec(num_layers=16, layer_weight_bytes=int(2.5 * GIB),
                       token_kv_bytes_per_layer=64 * KIB, stacking_factor=2,

@@ -150,3 +150,35 @@ def test_acceptance_criterion_6_stop_time_ablation():
         bound = tau * scen.model.token_kv_bytes_per_layer * n / scen.fabric.link_bandwidth \
             + 8 * scen.fabric.control_latency
         assert pause <= bound
+
+
+def test_acceptance_criterion_4_randomized_reconfigurations(golden):
+    """Acceptance criterion 4 (pkg/tests/test_acceptance.py:153-182) on the GPU data plane,
+    pinned run by run to the reference: 100 randomized reconfigurations (2-4 GPUs, 8-32
+    layers) reproduce the reference's trace sha256; every committed one has a bit-exact
+    destination KV at the commit snapshot and lag under tau."""
+    import time
+
+    from paper_2604_12171_b200.simulation import Simulation
+
+    want = golden("e2e_runs.json")
+    t0 = time.time()
+    committed = 0
+    for seed in range(100):
+        scen = sim_scenarios.random_e2e_scenario(seed)
+        sim = Simulation(scen, seed=seed)
+        sim.scheduler.run(until=60.0)
+        sha = hashlib.sha256(sim.trace.to_jsonl().encode()).hexdigest()
+        assert sha == want[str(seed)]["trace_sha"], seed
+        assert [s.outcome for s in sim.statuses] == want[str(seed)]["outcomes"], seed
+        if not sim.statuses or sim.statuses[0].outcome != "success":
+            continue
+        committed += 1
+        st = sim.statuses[0]
+        for pair, groups in st.migrated_groups.items():
+            for g in groups:
+                assert st.dest_snapshots[pair][g] == st.source_snapshots[pair][g], (seed, pair, g)
+        for lag in st.lag_at_final_sync.values():
+            assert lag < scen.triggers[0].tau
+    assert committed >= 60
+    assert time.time() - t0 < 120.0
