@@ -439,15 +439,14 @@ struct Patch {
   uint8_t* d_mask = nullptr;
   size_t mask_cap = 0;
   const uint8_t* stage_mask(const std::vector<uint8_t>& mask);
-  uint32_t* d_snap = nullptr;
   int32_t* d_local_of = nullptr;  // device copy of local_of
   int64_t bit_slots = 0;  // slots covered
   int64_t n_words = 0;
 
   // scan scratch + drained list
-  int64_t* d_tile_counts = nullptr;
-  int64_t n_tiles_cap = 0;
-  int64_t* d_count = nullptr;   // [0] = drained keys on device, [1] = scratch
+  int64_t* d_count = nullptr;   // drained keys of the current round (points into d_cnt)
+  int64_t* d_cnt = nullptr;     // [round parity 0, round parity 1, popcount scratch, spare]
+  int cnt_cur = 0;
   int64_t* d_cells = nullptr;   // compacted drained bit indices
   int64_t cells_cap = 0;
 
@@ -533,12 +532,9 @@ void launch_table_remap(int32_t* table, int64_t n_entries, const int32_t* remap,
 void launch_popcount(const uint32_t* bits, int64_t n_words, int64_t* out, cudaStream_t st);
 
 // K3: snapshot+clear, tile counts, scan, emit
-int64_t drain_tiles(int64_t n_words);
-void launch_drain_snapshot(uint32_t* bits, uint32_t* snap, int64_t n_words, int64_t* tile_counts,
-                           cudaStream_t st);
-void launch_drain_scan(int64_t* tile_counts, int64_t n_tiles, int64_t* total, cudaStream_t st);
-void launch_drain_emit(const uint32_t* snap, int64_t n_words, const int64_t* tile_offsets,
-                       int64_t* cells, int64_t cells_cap, cudaStream_t st);
+// K3 in one launch (warp-aggregated reservation; output order not sorted)
+void launch_drain_compact(uint32_t* bits, int64_t n_words, int64_t* cells, int64_t cap,
+                          int64_t* count, int64_t* next_count, cudaStream_t st);
 
 struct CopyLaunch {
   int mode;  // 0 gather (pool->rows), 1 scatter (rows->pool), 2 push (pool->pool)

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Data-plane kernels of the live-reconfiguration path (sm_100a).
 //
 //   K1  kv_write_mark  : KvStore.append / write_slots (kvstore.py:163-227) fused with the
@@ -12,8 +13,6 @@
 //
 // All of these are HBM-bound byte movers: 128-bit accesses, one warp per 16B-aligned
 // cell row, grid sized to the SM count, no tensor cores.
-#include <cub/block/block_reduce.cuh>
-#include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
 #include "internal.h"
@@ -242,109 +241,56 @@ void launch_popcount(const uint32_t* bits, int64_t n_words, int64_t* out, cudaSt
   PL_CUDA(cudaGetLastError());
 }
 
-// ---------------------------------------------------------------------------
-// K3 drain.  Tile = 256 threads x 4 words.  Phase A snapshots-and-clears the
-// live bitmap with atomicExch (marks racing on another stream land in the next
-// round) and counts bits per tile; phase B scans tile counts; phase C emits the
-// set bit indices in ascending order (per-thread popc + CTA scan).
-constexpr int kDrainThreads = 256;
-constexpr int kDrainWordsPerThread = 4;
-constexpr int kTileWords = kDrainThreads * kDrainWordsPerThread;
-
-int64_t drain_tiles(int64_t n_words) { return (n_words + kTileWords - 1) / kTileWords; }
-
-__global__ void __launch_bounds__(kDrainThreads)
-drain_snapshot_kernel(uint32_t* bits, uint32_t* snap, int64_t n_words, int64_t* tile_counts) {
-  using Scan = cub::BlockReduce<int, kDrainThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  const int64_t base = (int64_t)blockIdx.x * kTileWords + threadIdx.x * kDrainWordsPerThread;
-  int c = 0;
-#pragma unroll
-  for (int i = 0; i < kDrainWordsPerThread; ++i) {
-    const int64_t wi = base + i;
-    uint32_t w = 0;
+// K3 in one pass: every warp takes 32 bitmap words, snapshots + clears them (atomicExch:
+// marks racing in from K1 either land before and are drained now, or after and stay for
+// the next round), reserves its output range with ONE atomicAdd (warp popc totals,
+// shuffle prefix = ballot/popc compaction), and emits the set bits' cell indices.  The
+// copy kernels are order-independent, so no global scan is needed.  `next_count` (the
+// other round's counter) is zeroed here for the next drain.
+__global__ void __launch_bounds__(256)
+drain_compact_kernel(uint32_t* bits, int64_t n_words, int64_t* cells, int64_t cap,
+                     unsigned long long* count, unsigned long long* next_count) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *next_count = 0ull;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp0 * 32; base < n_words; base += nwarps * 32) {
+    const int64_t wi = base + lane;
+    uint32_t v = 0;
     if (wi < n_words) {
-      w = bits[wi];
-      if (w) w = atomicExch(bits + wi, 0u);
-      snap[wi] = w;
+      v = bits[wi];
+      if (v) v = atomicExch(bits + wi, 0u);
     }
-    c += __popc(w);
-  }
-  const int total = Scan(tmp).Sum(c);
-  if (threadIdx.x == 0) tile_counts[blockIdx.x] = total;
-}
-
-constexpr int kScanThreads = 256;
-__global__ void __launch_bounds__(kScanThreads)
-drain_scan_kernel(int64_t* counts, int64_t n, int64_t* total) {
-  using Scan = cub::BlockScan<int64_t, kScanThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < n; base += kScanThreads) {
-    const int64_t i = base + threadIdx.x;
-    int64_t v = i < n ? counts[i] : 0, ex, agg;
-    Scan(tmp).ExclusiveSum(v, ex, agg);
-    if (i < n) counts[i] = ex + carry;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += agg;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *total = carry;
-}
-
-__global__ void __launch_bounds__(kDrainThreads)
-drain_emit_kernel(const uint32_t* snap, int64_t n_words, const int64_t* tile_off, int64_t* cells,
-                  int64_t cap) {
-  using Scan = cub::BlockScan<int, kDrainThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  const int64_t base = (int64_t)blockIdx.x * kTileWords + threadIdx.x * kDrainWordsPerThread;
-  uint32_t w[kDrainWordsPerThread];
-  int c = 0;
+    const int c = __popc(v);
+    int incl = c;
 #pragma unroll
-  for (int i = 0; i < kDrainWordsPerThread; ++i) {
-    w[i] = base + i < n_words ? snap[base + i] : 0u;
-    c += __popc(w[i]);
-  }
-  int ex;
-  Scan(tmp).ExclusiveSum(c, ex);
-  int64_t out = tile_off[blockIdx.x] + ex;
-#pragma unroll
-  for (int i = 0; i < kDrainWordsPerThread; ++i) {
-    uint32_t v = w[i];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long start = 0;
+    if (lane == 31 && total) start = atomicAdd(count, (unsigned long long)total);
+    start = __shfl_sync(0xffffffffu, start, 31);
+    int64_t out = (int64_t)start + incl - c;
     while (v) {
       const int b = __ffs(v) - 1;
       v &= v - 1;
-      if (out < cap) cells[out] = (base + i) * 32 + b;
+      if (out < cap) cells[out] = wi * 32 + b;
       ++out;
     }
   }
 }
+void launch_drain_compact(uint32_t* bits, int64_t n_words, int64_t* cells, int64_t cap,
+                          int64_t* count, int64_t* next_count, cudaStream_t st) {
+  const int64_t grid = std::max<int64_t>(1, grid_for((n_words + 255) / 256, 1));
+  drain_compact_kernel<<<(unsigned)grid, 256, 0, st>>>(
+      bits, n_words, cells, cap, reinterpret_cast<unsigned long long*>(count),
+      reinterpret_cast<unsigned long long*>(next_count));
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
 
-void launch_drain_snapshot(uint32_t* bits, uint32_t* snap, int64_t n_words, int64_t* tile_counts,
-                           cudaStream_t st) {
-  const int64_t tiles = drain_tiles(n_words);
-  if (tiles <= 0) return;
-  drain_snapshot_kernel<<<(unsigned)tiles, kDrainThreads, 0, st>>>(bits, snap, n_words,
-                                                                   tile_counts);
-  note_launch();
-  PL_CUDA(cudaGetLastError());
-}
-void launch_drain_scan(int64_t* tile_counts, int64_t n_tiles, int64_t* total, cudaStream_t st) {
-  drain_scan_kernel<<<1, kScanThreads, 0, st>>>(tile_counts, n_tiles, total);
-  note_launch();
-  PL_CUDA(cudaGetLastError());
-}
-void launch_drain_emit(const uint32_t* snap, int64_t n_words, const int64_t* tile_offsets,
-                       int64_t* cells, int64_t cells_cap, cudaStream_t st) {
-  const int64_t tiles = drain_tiles(n_words);
-  if (tiles <= 0) return;
-  drain_emit_kernel<<<(unsigned)tiles, kDrainThreads, 0, st>>>(snap, n_words, tile_offsets, cells,
-                                                               cells_cap);
-  note_launch();
-  PL_CUDA(cudaGetLastError());
-}
 
 // ---------------------------------------------------------------------------
 // K4/K5 copy engine.  Work item = (drained cell, layer); one warp moves one

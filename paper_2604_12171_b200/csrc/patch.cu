@@ -47,8 +47,9 @@ Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n)
   PL_CUDA(cudaMalloc(&d_local_of, sizeof(int32_t) * src->n_model_groups));
   PL_CUDA(cudaMemcpy(d_local_of, local_of.data(), sizeof(int32_t) * src->n_model_groups,
                      cudaMemcpyHostToDevice));
-  PL_CUDA(cudaMalloc(&d_count, sizeof(int64_t) * 2));
-  PL_CUDA(cudaMemset(d_count, 0, sizeof(int64_t) * 2));
+  PL_CUDA(cudaMalloc(&d_cnt, sizeof(int64_t) * 4));
+  PL_CUDA(cudaMemset(d_cnt, 0, sizeof(int64_t) * 4));
+  d_count = d_cnt;
   PL_CUDA(cudaEventCreateWithFlags(&ev_gathered, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_applied, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_dst, cudaEventDisableTiming));
@@ -71,10 +72,8 @@ Patch::~Patch() {
   }
   cudaFree(d_bits);
   cudaFree(d_bits_alt);
-  cudaFree(d_snap);
   cudaFree(d_local_of);
-  cudaFree(d_tile_counts);
-  cudaFree(d_count);
+  cudaFree(d_cnt);
   cudaFree(d_cells);
   cudaFree(d_rows);
   cudaFree(d_keys);
@@ -113,12 +112,11 @@ void Patch::ensure_bits() {
   const int64_t slots = std::max<int64_t>(src->owner_cap, 1);
   if (slots <= bit_slots && d_bits) return;
   const int64_t words = (slots * G * src->s + 31) / 32;
-  uint32_t *nb = nullptr, *na = nullptr, *ns = nullptr;
+  uint32_t *nb = nullptr, *na = nullptr;
   PL_CUDA(cudaSetDevice(src->device));
   if (stream) PL_CUDA(cudaStreamSynchronize(stream));
   PL_CUDA(cudaMalloc(&nb, words * 4));
   PL_CUDA(cudaMalloc(&na, words * 4));
-  PL_CUDA(cudaMalloc(&ns, words * 4));
   PL_CUDA(cudaMemsetAsync(nb, 0, words * 4, src->stream));
   PL_CUDA(cudaMemsetAsync(na, 0, words * 4, src->stream));
   if (d_bits && n_words)
@@ -126,18 +124,10 @@ void Patch::ensure_bits() {
   PL_CUDA(cudaStreamSynchronize(src->stream));
   cudaFree(d_bits);
   cudaFree(d_bits_alt);
-  cudaFree(d_snap);
   d_bits = nb;
   d_bits_alt = na;
-  d_snap = ns;
   bit_slots = slots;
   n_words = words;
-  const int64_t tiles = drain_tiles(n_words);
-  if (tiles > n_tiles_cap) {
-    cudaFree(d_tile_counts);
-    PL_CUDA(cudaMalloc(&d_tile_counts, sizeof(int64_t) * tiles));
-    n_tiles_cap = tiles;
-  }
 }
 
 // --- host interval set ------------------------------------------------------------
@@ -304,12 +294,14 @@ int64_t Patch::device_drain_compact() {
     PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
   }
   {
-    KernelTimer timer("drain", ps);  // K3: snapshot + clear, tile scan, ordered emit
-    launch_drain_snapshot(old, d_snap, n_words, d_tile_counts, ps);
+    // K3: one launch -- snapshot + clear + warp-aggregated compaction into d_cells; the
+    // round's counter alternates so the kernel can zero the next round's
+    KernelTimer timer("drain", ps);
+    cnt_cur ^= 1;
+    d_count = d_cnt + cnt_cur;
+    launch_drain_compact(old, n_words, d_cells, cells_cap, d_count, d_cnt + (cnt_cur ^ 1), ps);
     PL_CUDA(cudaEventRecord(ev_snap, ps));
     snap_recorded = true;
-    launch_drain_scan(d_tile_counts, drain_tiles(n_words), d_count, ps);
-    launch_drain_emit(d_snap, n_words, d_tile_counts, d_cells, cells_cap, ps);
   }
   return drained_keys;
 }
@@ -473,7 +465,10 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
                  ms(t0, t1), ms(t1, t2), ms(t2, now()), (long long)drained_keys);
   PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
   PL_CUDA(cudaSetDevice(src->device));
+  const auto t3 = now();
   device_drain_compact();
+  if (trace)
+    std::fprintf(stderr, "[pl] push: K3 enqueue (src flush + 3 launches) %.3f ms\n", ms(t3, now()));
   if (drained_keys > 0 && !mask.empty()) {
     if (pstream() != src->stream) {
       PL_CUDA(cudaEventRecord(ev_src, src->stream));
@@ -516,9 +511,9 @@ int64_t Patch::device_dirty_count() {
   src->flush();
   if (stream) PL_CUDA(cudaStreamSynchronize(stream));
   PL_CUDA(cudaStreamSynchronize(src->stream));
-  launch_popcount(d_bits, n_words, d_count + 1, src->stream);
+  launch_popcount(d_bits, n_words, d_cnt + 2, src->stream);
   int64_t v = 0;
-  PL_CUDA(cudaMemcpyAsync(&v, d_count + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, src->stream));
+  PL_CUDA(cudaMemcpyAsync(&v, d_cnt + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, src->stream));
   PL_CUDA(cudaStreamSynchronize(src->stream));
   return v;  // the drained buffer is all-zero once its snapshot ran
 }
