@@ -44,6 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     hdr_t = max((HERE / h).stat().st_mtime for h in HEADERS)
     hdr_t = max(hdr_t, (ROOT / "include" / "pipelive.h").stat().st_mtime, Path(__file__).stat().st_mtime)
+    jobs = []
     for src in SOURCES:
         obj = objdir / (src + ".o")
         objs.append(str(obj))
@@ -52,7 +53,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         cmd = [NVCC, *FLAGS, "-c", str(HERE / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
+        jobs.append(cmd)
+    # translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c, check=True), jobs)):
+            pass
     # export only the C-ABI: pl_* symbols are marked default-visibility below
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
            "-o", str(OUT), "--cudart", "static"]
