@@ -1,6 +1,7 @@
 """BASELINE configs[3] machinery on one GPU: 8 stage processes (16-layer tiny Llama), an
 even split re-split live into an uneven one mid-decode.  Rank 0 records the run's trace
-in the reference schema; prints compute_metrics and the decode-step latency before /
+in the reference schema and writes trace.jsonl / metrics.csv / summary.json (outputs.py)
+to gpurun_out/c4_live_run/; prints compute_metrics and the decode-step latency before /
 during / after the switch.  The 8 processes share one B200, so the latencies show the
 mechanism (pause, interference), not 8-GPU pipeline timings."""
 import json
@@ -31,6 +32,9 @@ def stage(rank, world, port, prefix, q):
     generate_dist(m, prompts, [2 * b for b in range(8)], 48, reconfig=(40, W.CONF_UNEVEN8),
                   switch_at=60, trace=tr)
     if rank == 0:
+        from paper_2604_12171_b200 import outputs
+        outputs.write_run("gpurun_out/c4_live_run", tr, "configs[3]:even8->uneven8", 0,
+                          mode="perf", stages=8)
         q.put({"metrics": compute_metrics(tr).as_row(), "steps": step_latency_around_switch(tr),
                "events": len(tr), "stages": 8,
                "note": "8 stage processes share one B200: mechanism (pause, interference), "
