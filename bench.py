@@ -17,6 +17,7 @@ its own GPU (weak scaling, no data-path collective); timing is max over ranks.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -269,6 +270,10 @@ def main() -> None:
     rig = PatchRig(wl, device=dev)
     rig.use_stream(stream.cuda_stream)
     rig.fill()
+    # the host block manager's mirror is millions of small objects: collect once and freeze
+    # them, so a cyclic-GC pass cannot land inside a wall-clock measurement below
+    gc.collect()
+    gc.freeze()
     K, W = args.steps, args.warmup
     # N > 1: a ring of cross-process pairs, rank r -> r+1 over the imported peer pools
     # (NVLink stores); N = 1: the pair's destination is a second store on this GPU

@@ -246,6 +246,7 @@ struct FreeIds {
 };
 
 struct Patch;
+struct CopyLaunch;
 struct Interval { int64_t a, b; };  // [a, b)
 
 // Store: one KvStore (kvstore.py:88-360) on one device.  Host side keeps the
@@ -280,6 +281,7 @@ struct Store {
   // device block table: table[req * max_chain + idx] = slot; owner maps by slot
   int32_t* d_table = nullptr;
   int64_t max_reqs = 0, max_chain = 0;
+  int64_t n_table_grows = 0;  // ensure_table reallocations (diagnostics)
   int32_t* d_owner = nullptr;
   int32_t* d_owner_idx = nullptr;
   int64_t owner_cap = 0;
@@ -439,6 +441,7 @@ struct Patch {
   uint8_t* d_mask = nullptr;
   size_t mask_cap = 0;
   const uint8_t* stage_mask(const std::vector<uint8_t>& mask);
+  const uint8_t* stage_bytes(const uint8_t* p, size_t n);  // H2D into d_mask on pstream
   int32_t* d_local_of = nullptr;  // device copy of local_of
   int64_t bit_slots = 0;  // slots covered
   int64_t n_words = 0;
@@ -449,6 +452,8 @@ struct Patch {
   int cnt_cur = 0;
   int64_t* d_cells = nullptr;   // compacted drained bit indices
   int64_t cells_cap = 0;
+  int64_t* d_part = nullptr;    // chunked push: d_cells bucketed by run
+  int64_t part_cap = 0;
 
   cudaEvent_t ev_gathered = nullptr, ev_applied = nullptr, ev_dst = nullptr;
   bool applied_recorded = false;
@@ -475,8 +480,15 @@ struct Patch {
   int64_t take_drained();               // host snapshot -> drained
   int64_t device_drain_compact();       // K3 into d_cells; returns host-known count
   void drain(int64_t* keys, int64_t* cells);
+  std::vector<size_t> apply_order(const int32_t* rank, int64_t n_rank, const uint8_t* stale,
+                                  int64_t n_stale, int64_t* max_req);
+  bool presize_dst(Store* dst, const std::vector<size_t>& order, int64_t max_req);
+  bool reserve_item(Store* dst, size_t i, int* status);
   void extend_dst(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
                   int64_t n_stale, std::vector<uint8_t>& apply_mask, int* status);
+  CopyLaunch push_launch(Store* dst, const uint8_t* d_apply, uint8_t apply_id);
+  void push_chunked(Store* dst, const int32_t* rank, int64_t n_rank);
+  int64_t new_dst_blocks(Store* dst) const;
   void apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
              int64_t n_stale);
   void push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells);
@@ -533,6 +545,10 @@ void launch_popcount(const uint32_t* bits, int64_t n_words, int64_t* out, cudaSt
 
 // K3: snapshot+clear, tile counts, scan, emit
 // K3 in one launch (warp-aggregated reservation; output order not sorted)
+void launch_partition_runs(const int64_t* cells, const int64_t* count, int64_t n_hint,
+                           const int32_t* owner, int64_t per_slot, int src_s, int G,
+                           const uint8_t* run_of, int64_t n_run_of, const int64_t* run_off,
+                           int64_t* run_cnt, int64_t* out, cudaStream_t st);
 void launch_drain_compact(uint32_t* bits, int64_t n_words, int64_t* cells, int64_t cap,
                           int64_t* count, int64_t* next_count, cudaStream_t st);
 
@@ -546,6 +562,7 @@ struct CopyLaunch {
   // destination pool
   const uint64_t* dst_bases; int dst_s; int64_t dst_unit; const int32_t* dst_table;
   int64_t dst_max_chain; const uint8_t* apply_mask;
+  uint8_t apply_id;  // 0: apply where mask != 0; else only where mask == apply_id (chunked push)
   // staging
   uint8_t* rows; int32_t* keys; int64_t row_bytes;
 };

@@ -292,6 +292,53 @@ void launch_drain_compact(uint32_t* bits, int64_t n_words, int64_t* cells, int64
 }
 
 
+
+// Chunked push (Patch::push_chunked): bucket the drained cells by the run their
+// (request, group) item belongs to, so run c's copy launch walks only its own cells.
+// Drained cells come out of K3 in slot order, so a warp's lanes mostly share one run:
+// match_any groups them and each group reserves its output range with one atomicAdd.
+__global__ void partition_runs_kernel(const int64_t* cells, const unsigned long long* count,
+                                      int64_t n_hint, const int32_t* owner, int64_t per_slot,
+                                      int src_s, int G, const uint8_t* run_of, int64_t n_run_of,
+                                      const int64_t* run_off, unsigned long long* run_cnt,
+                                      int64_t* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = count ? min((int64_t)*count, n_hint) : n_hint;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count: every lane of a warp runs the same iterations
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
+       base += stride) {
+    const int64_t i = base + lane;
+    int run = 0;  // 0: not in any run (a slot released since the drain)
+    int64_t cell = -1;
+    if (i < n) {
+      cell = cells[i];
+      const int32_t slot = (int32_t)(cell / per_slot);
+      const int lg = (int)((cell % per_slot) / src_s);
+      const int32_t req = owner[slot];
+      const int64_t m = (int64_t)req * G + lg;
+      if (req >= 0 && m < n_run_of) run = run_of[m];
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, run);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long start = 0;
+    if (run && lane == leader) start = atomicAdd(run_cnt + (run - 1), (unsigned long long)__popc(peers));
+    start = __shfl_sync(0xffffffffu, start, leader);
+    if (run) out[run_off[run - 1] + (int64_t)start + __popc(peers & ((1u << lane) - 1))] = cell;
+  }
+}
+void launch_partition_runs(const int64_t* cells, const int64_t* count, int64_t n_hint,
+                           const int32_t* owner, int64_t per_slot, int src_s, int G,
+                           const uint8_t* run_of, int64_t n_run_of, const int64_t* run_off,
+                           int64_t* run_cnt, int64_t* out, cudaStream_t st) {
+  if (n_hint <= 0) return;
+  partition_runs_kernel<<<(unsigned)grid_for(n_hint, 256), 256, 0, st>>>(
+      cells, reinterpret_cast<const unsigned long long*>(count), n_hint, owner, per_slot, src_s,
+      G, run_of, n_run_of, run_off, reinterpret_cast<unsigned long long*>(run_cnt), out);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------------------
 // K4/K5 copy engine.  Work item = (drained cell, layer); one warp moves one
 // cell_bytes row with 128-bit accesses, 8 loads in flight per lane before the
@@ -349,7 +396,10 @@ __global__ void __launch_bounds__(kWarps * 32) copy_kernel(CopyLaunch c) {
       if (req < 0) continue;
     } else {
       if (req < 0) continue;
-      if (c.apply_mask && !c.apply_mask[(int64_t)req * c.G + lg]) continue;
+      if (c.apply_mask) {
+        const uint8_t m = c.apply_mask[(int64_t)req * c.G + lg];
+        if (c.apply_id ? m != c.apply_id : !m) continue;
+      }
       const int32_t dslot = c.dst_table[(int64_t)req * c.dst_max_chain + pos / c.dst_s];
       if (dslot < 0) continue;
       const int doff = (int)(pos % c.dst_s);

@@ -75,6 +75,7 @@ Patch::~Patch() {
   cudaFree(d_local_of);
   cudaFree(d_cnt);
   cudaFree(d_cells);
+  cudaFree(d_part);
   cudaFree(d_rows);
   cudaFree(d_keys);
   cudaFree(d_groups_);
@@ -89,8 +90,12 @@ Patch::~Patch() {
 }
 
 const uint8_t* Patch::stage_mask(const std::vector<uint8_t>& mask) {
+  return stage_bytes(mask.data(), mask.size());
+}
+
+const uint8_t* Patch::stage_bytes(const uint8_t* data, size_t bytes) {
   cudaStream_t ps = pstream();
-  const size_t n = std::max<size_t>(mask.size(), 1);
+  const size_t n = std::max<size_t>(bytes, 1);
   if (n > mask_cap) {
     PL_CUDA(cudaStreamSynchronize(ps));
     cudaFree(d_mask);
@@ -101,8 +106,8 @@ const uint8_t* Patch::stage_mask(const std::vector<uint8_t>& mask) {
     mask_recorded = false;
   }
   if (mask_recorded) PL_CUDA(cudaEventSynchronize(ev_mask));  // previous H2D read h_mask
-  std::memcpy(h_mask, mask.data(), mask.size());
-  PL_CUDA(cudaMemcpyAsync(d_mask, h_mask, mask.size(), cudaMemcpyHostToDevice, ps));
+  std::memcpy(h_mask, data, bytes);
+  PL_CUDA(cudaMemcpyAsync(d_mask, h_mask, bytes, cudaMemcpyHostToDevice, ps));
   PL_CUDA(cudaEventRecord(ev_mask, ps));
   mask_recorded = true;
   return d_mask;
@@ -131,6 +136,17 @@ void Patch::ensure_bits() {
 }
 
 // --- host interval set ------------------------------------------------------------
+// rounds that allocate at least this many destination blocks (a cold bulk round) reserve
+// and copy in pipelined runs (push_chunked); warm rounds stay one launch
+// (PL_PUSH_CHUNK_MIN_BLOCKS overrides it, read per round: the tests force tiny runs;
+// PL_PUSH_NO_CHUNK=1 turns the pipelining off for A/B timing)
+constexpr int64_t kChunkedPushMinBlocks = 8192;
+static int64_t chunk_min_blocks() {
+  const char* v = std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS");
+  return v ? std::max<int64_t>(1, std::atoll(v)) : kChunkedPushMinBlocks;
+}
+static bool no_chunking() { return std::getenv("PL_PUSH_NO_CHUNK") != nullptr; }
+
 static int64_t insert_interval(std::vector<Interval>& v, int64_t a, int64_t b) {
   // merge [a,b) into sorted disjoint v (adjacent intervals merge); returns newly covered
   if (b <= a) return 0;
@@ -351,8 +367,8 @@ void Patch::drain(int64_t* keys, int64_t* cells) {
   *cells = host_cells(drained);
 }
 
-void Patch::extend_dst(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
-                       int64_t n_stale, std::vector<uint8_t>& mask, int* status) {
+std::vector<size_t> Patch::apply_order(const int32_t* rank, int64_t n_rank, const uint8_t* stale,
+                                       int64_t n_stale, int64_t* max_req) {
   // PatchReceiver._apply order: sorted by (request id, group) (migrator.py:124-128)
   std::vector<size_t> order;
   for (size_t i = 0; i < drained.size(); ++i) {
@@ -366,21 +382,46 @@ void Patch::extend_dst(Store* dst, const int32_t* rank, int64_t n_rank, const ui
     if (ra != rb) return ra < rb;
     return groups[std::get<1>(drained[a])] < groups[std::get<1>(drained[b])];
   });
+  *max_req = 0;
+  for (auto& e : drained) *max_req = std::max<int64_t>(*max_req, std::get<0>(e) + 1);
+  return order;
+}
+
+bool Patch::presize_dst(Store* dst, const std::vector<size_t>& order, int64_t max_req) {
+  // size the destination block table once for the whole patch (a bulk round reserves
+  // whole chains; growing it request by request costs a device sync per doubling)
+  int64_t top_chain = 0;
+  for (size_t i : order) {
+    const auto& iv = std::get<2>(drained[i]);
+    if (!iv.empty()) top_chain = std::max<int64_t>(top_chain, (iv.back().b + dst->s - 1) / dst->s);
+  }
+  if (max_req <= 0 || top_chain <= 0 || top_chain > dst->capacity()) return false;
+  dst->ensure_table(max_req - 1, top_chain);
+  return true;
+}
+
+bool Patch::reserve_item(Store* dst, size_t i, int* status) {
+  try {
+    dst->reserve_positions(std::get<0>(drained[i]), groups[std::get<1>(drained[i])],
+                           std::get<2>(drained[i]));
+  } catch (const Error& e) {
+    *status = e.code;
+    dst->last_msg = e.what();
+    return false;
+  }
+  return true;
+}
+
+void Patch::extend_dst(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
+                       int64_t n_stale, std::vector<uint8_t>& mask, int* status) {
   int64_t max_req = 0;
-  for (auto& e : drained) max_req = std::max<int64_t>(max_req, std::get<0>(e) + 1);
+  const std::vector<size_t> order = apply_order(rank, n_rank, stale, n_stale, &max_req);
   mask.assign((size_t)(max_req * G), 0);
   *status = PL_OK;
+  presize_dst(dst, order, max_req);
   for (size_t i : order) {
-    const int32_t req = std::get<0>(drained[i]);
-    const int32_t lg = std::get<1>(drained[i]);
-    try {
-      dst->reserve_positions(req, groups[lg], std::get<2>(drained[i]));
-    } catch (const Error& e) {
-      *status = e.code;
-      dst->last_msg = e.what();
-      return;
-    }
-    mask[(size_t)req * G + lg] = 1;
+    if (!reserve_item(dst, i, status)) return;
+    mask[(size_t)std::get<0>(drained[i]) * G + std::get<1>(drained[i])] = 1;
   }
 }
 
@@ -438,6 +479,154 @@ void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t
   if (status != PL_OK) fail(status, dst->last_msg);
 }
 
+int64_t Patch::new_dst_blocks(Store* dst) const {
+  // destination blocks the drained set will allocate: per request, the chain it needs past
+  // the chain it has (the chain is shared by the request's groups)
+  std::vector<int64_t> top;
+  for (const auto& e : drained) {
+    const int32_t req = std::get<0>(e);
+    const auto& iv = std::get<2>(e);
+    if (iv.empty()) continue;
+    if ((size_t)req >= top.size()) top.resize((size_t)req + 1, 0);
+    top[(size_t)req] = std::max(top[(size_t)req], iv.back().b);
+  }
+  int64_t n = 0;
+  for (size_t r = 0; r < top.size(); ++r) {
+    if (!top[r]) continue;
+    const ReqTable* t = dst->table((int32_t)r);
+    const int64_t have = t ? (int64_t)t->chain.size() : 0;
+    n += std::max<int64_t>(0, (top[r] + dst->s - 1) / dst->s - have);
+  }
+  return n;
+}
+
+CopyLaunch Patch::push_launch(Store* dst, const uint8_t* d_apply, uint8_t apply_id) {
+  CopyLaunch c{};
+  c.mode = 2;
+  c.cells = d_cells;
+  c.count = d_count;
+  c.n_hint = drained_keys;
+  c.G = G;
+  c.k = src->k;
+  c.cell_bytes = src->cell_bytes;
+  c.fp_bytes = src->fp_bytes;
+  c.src_bases = src->d_bases_;
+  c.src_groups = d_groups();
+  c.src_s = src->s;
+  c.src_unit = src->unit_bytes;
+  c.src_owner = src->d_owner;
+  c.src_owner_idx = src->d_owner_idx;
+  c.dst_bases = dst->d_bases_;
+  c.dst_s = dst->s;
+  c.dst_unit = dst->unit_bytes;
+  c.dst_table = dst->d_table;
+  c.dst_max_chain = dst->max_chain;
+  c.apply_mask = d_apply;
+  c.apply_id = apply_id;
+  return c;
+}
+
+// A bulk round (the first drain after seeding moves every live cell of the migrating
+// groups) reserves whole destination chains on the host: ~0.1 us per block, i.e. ~10 ms
+// for a 40 GB round, as long as the copy itself.  So the round is cut into consecutive
+// runs of the receiver's apply order.  On the device, K3's drained cells are bucketed by
+// run (one partition launch); then run c is reserved on the host, its block-table deltas
+// flushed, and its copy launched over its own bucket while the host reserves run c + 1.
+// Allocation order -- and so every block id -- is the unchunked order.
+void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
+  static const bool trace = std::getenv("PL_TRACE_PUSH") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  int64_t max_req = 0;
+  const std::vector<size_t> order = apply_order(rank, n_rank, nullptr, 0, &max_req);
+  // runs of about 1/8 of the keys (>= 64 k keys unless forced), at most 254 of them
+  std::vector<size_t> cut{0};
+  std::vector<int64_t> run_keys;
+  {
+    const int64_t target =
+        std::max<int64_t>(drained_keys / 8, std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS") ? 1 : 1 << 16);
+    int64_t acc = 0;
+    for (size_t x = 0; x < order.size(); ++x) {
+      for (const Interval& r : std::get<2>(drained[order[x]])) acc += r.b - r.a;
+      if ((acc >= target && cut.size() < 254) || x + 1 == order.size()) {
+        cut.push_back(x + 1);
+        run_keys.push_back(acc);
+        acc = 0;
+      }
+    }
+  }
+  const size_t n_runs = run_keys.size();
+  // one staged blob: [run id per (req, group), padded to 8 B][run offsets][run counters = 0]
+  const size_t n_mask = (size_t)(max_req * G);
+  const size_t mask_pad = (n_mask + 7) & ~(size_t)7;
+  std::vector<uint8_t> blob(mask_pad + 16 * n_runs, 0);
+  for (size_t c = 0; c < n_runs; ++c)
+    for (size_t x = cut[c]; x < cut[c + 1]; ++x)
+      blob[(size_t)std::get<0>(drained[order[x]]) * G + std::get<1>(drained[order[x]])] =
+          (uint8_t)(c + 1);
+  std::vector<int64_t> run_off(n_runs, 0);
+  for (size_t c = 1; c < n_runs; ++c) run_off[c] = run_off[c - 1] + run_keys[c - 1];
+  std::memcpy(blob.data() + mask_pad, run_off.data(), 8 * n_runs);
+  presize_dst(dst, order, max_req);
+  // K3 (independent of the destination), the blob and the partition go first
+  PL_CUDA(cudaSetDevice(src->device));
+  device_drain_compact();
+  if (pstream() != src->stream) {
+    PL_CUDA(cudaEventRecord(ev_src, src->stream));
+    PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
+  }
+  if (drained_keys > part_cap) {
+    PL_CUDA(cudaStreamSynchronize(pstream()));
+    cudaFree(d_part);
+    part_cap = std::max(drained_keys, part_cap * 2);
+    PL_CUDA(cudaMalloc(&d_part, sizeof(int64_t) * part_cap));
+  }
+  const uint8_t* d_blob = stage_bytes(blob.data(), blob.size());
+  const int64_t* d_run_off = reinterpret_cast<const int64_t*>(d_blob + mask_pad);
+  int64_t* d_run_cnt = const_cast<int64_t*>(d_run_off) + n_runs;
+  launch_partition_runs(d_cells, d_count, drained_keys, src->d_owner, (int64_t)G * src->s, src->s,
+                        G, d_blob, (int64_t)n_mask, d_run_off, d_run_cnt, d_part, pstream());
+  int status = PL_OK;
+  size_t launched = 0;
+  for (size_t c = 0; c < n_runs; ++c) {
+    size_t x = cut[c];
+    for (; x < cut[c + 1]; ++x)
+      if (!reserve_item(dst, order[x], &status)) break;
+    const uint8_t* d_apply = nullptr;
+    if (status != PL_OK) {
+      // KvOverflow inside run c: its items from x on are not applied (the reference's
+      // _apply stops at the failing write; migrator.py:124-131); later runs never launch.
+      // Only the run-id bytes are re-staged: the run offsets/counters stay as partitioned.
+      for (size_t y = x; y < order.size(); ++y)
+        blob[(size_t)std::get<0>(drained[order[y]]) * G + std::get<1>(drained[order[y]])] = 0;
+      PL_CUDA(cudaSetDevice(src->device));
+      d_apply = stage_bytes(blob.data(), n_mask);
+    }
+    PL_CUDA(cudaSetDevice(dst->device));
+    dst->flush();
+    PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
+    PL_CUDA(cudaSetDevice(src->device));
+    PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
+    CopyLaunch cl = push_launch(dst, d_apply, (uint8_t)(c + 1));
+    cl.cells = d_part + run_off[c];
+    cl.count = d_run_cnt + c;
+    cl.n_hint = run_keys[c];
+    launch_copy(cl, pstream());
+    ++launched;
+    if (status != PL_OK) break;
+  }
+  drained.clear();
+  if (trace)
+    std::fprintf(stderr, "[pl] push (chunked): %zu items in %zu runs, %zu launches, host %.3f ms, "
+                 "%lld keys\n", order.size(), n_runs, launched,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+                 (long long)drained_keys);
+  PL_CUDA(cudaEventRecord(ev_applied, pstream()));
+  applied_recorded = true;
+  PL_CUDA(cudaSetDevice(dst->device));
+  PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
+  if (status != PL_OK) fail(status, dst->last_msg);
+}
+
 void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells) {
   if (in_flight) fail(PL_E_STATE, "a drained patch of this pair is still in flight");
   if (dst->k != src->k || dst->cell_bytes != src->cell_bytes)
@@ -452,6 +641,10 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   take_drained();
   *keys = drained_keys;
   *cells = host_cells(drained);
+  if (drained.size() >= 2 && !no_chunking() && new_dst_blocks(dst) >= chunk_min_blocks()) {
+    push_chunked(dst, rank, n_rank);
+    return;
+  }
   std::vector<uint8_t> mask;
   int status = PL_OK;
   const auto t1 = now();
@@ -477,28 +670,7 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
     // every drained item was reserved (no KvOverflow): no mask needed, the copy applies all
     const uint8_t* d_apply = status == PL_OK ? nullptr : stage_mask(mask);
     PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
-    CopyLaunch c{};
-    c.mode = 2;
-    c.cells = d_cells;
-    c.count = d_count;
-    c.n_hint = drained_keys;
-    c.G = G;
-    c.k = src->k;
-    c.cell_bytes = src->cell_bytes;
-    c.fp_bytes = src->fp_bytes;
-    c.src_bases = src->d_bases_;
-    c.src_groups = d_groups();
-    c.src_s = src->s;
-    c.src_unit = src->unit_bytes;
-    c.src_owner = src->d_owner;
-    c.src_owner_idx = src->d_owner_idx;
-    c.dst_bases = dst->d_bases_;
-    c.dst_s = dst->s;
-    c.dst_unit = dst->unit_bytes;
-    c.dst_table = dst->d_table;
-    c.dst_max_chain = dst->max_chain;
-    c.apply_mask = d_apply;
-    launch_copy(c, pstream());
+    launch_copy(push_launch(dst, d_apply, 0), pstream());
   }
   PL_CUDA(cudaEventRecord(ev_applied, pstream()));
   applied_recorded = true;

@@ -204,6 +204,7 @@ int64_t Store::block_occupied(int32_t slot) {
 // --- device mirrors ------------------------------------------------------------
 void Store::ensure_table(int64_t req, int64_t chain_len) {
   if (req < max_reqs && chain_len <= max_chain) return;
+  ++n_table_grows;
   flush();
   int64_t nr = std::max<int64_t>({req + 1, max_reqs * 2, 64});
   if (req < max_reqs) nr = max_reqs;

@@ -448,6 +448,7 @@ void Arena::ensure(size_t bytes) {
   adopt_prepared();
   if (bytes <= mapped_bytes()) return;
   Driver& d = drv();
+  const auto t_begin = Clock::now();
   reclaim_tail();
   if (bytes <= mapped_bytes()) return;
   size_t want_chunks = (bytes + chunk_bytes - 1) / chunk_bytes;
@@ -484,6 +485,8 @@ void Arena::ensure(size_t bytes) {
     hs.insert(hs.end(), more.begin(), more.end());
   }
   last_cache_reused += hs.size();
+  const double ms_take = ms_since(t_begin);
+  const size_t n_reused = hs.size();
   CUmemAllocationProp p = prop_for(device);
   bool forced = false;
   while (hs.size() < need) {
@@ -506,6 +509,7 @@ void Arena::ensure(size_t bytes) {
     hs.push_back(h);
     ++last_created;
   }
+  const double ms_create = ms_since(t_begin);
   for (size_t i = 0; i < need; ++i) {
     CUresult r = d.Map(va + (first + i) * chunk_bytes, chunk_bytes, 0, hs[i], 0);
     if (r != CUDA_SUCCESS)
@@ -516,7 +520,13 @@ void Arena::ensure(size_t bytes) {
                           ", cached " + std::to_string(last_cache_reused) + ")");
   }
   chunks.insert(chunks.end(), hs.begin(), hs.end());
+  const double ms_map = ms_since(t_begin);
   set_access(va + first * chunk_bytes, need * chunk_bytes, device, peer_devices);
+  if (trace_on())
+    std::fprintf(stderr, "[pl] ensure: +%zu chunks of %zu B (%zu reused%s): take %.2f create %.2f "
+                 "map %.2f access %.2f ms\n", need, chunk_bytes, n_reused,
+                 forced ? ", forced reclaim" : "", ms_take, ms_create - ms_take,
+                 ms_map - ms_create, ms_since(t_begin) - ms_map);
 }
 
 void Arena::trim(size_t bytes, cudaStream_t st) {

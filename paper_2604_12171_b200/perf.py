@@ -267,7 +267,9 @@ def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
     anchor.record(stream)
     side.wait_event(anchor)
     b0.record(side)
+    th0 = time.perf_counter()
     keys, cells = rig.patch.push(rig.dst, rig.registry.rank())
+    host_ms = (time.perf_counter() - th0) * 1e3
     b1.record(side)
     bulk_payload = cells * wl.cell_bytes
     during = [decode_step(True) for _ in range(steps)]
@@ -302,7 +304,8 @@ def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
             "decode_steps_overlapping_bulk": len(during_ms),
             "decode_ms_per_step_steady_patching": med(steady_ms),
             "bulk": {"payload_bytes": bulk_payload, "ms": round(bulk_ms, 3),
-                     "gbs": round(bulk_payload / bulk_ms / 1e6, 1)},
+                     "gbs": round(bulk_payload / bulk_ms / 1e6, 1),
+                     "host_enqueue_ms": round(host_ms, 3)},
             "steady_round_keys": round_keys[-1] if round_keys else 0,
             "switch_pause_ms": round(pause_ms, 4),
             "switch_pause_breakdown_ms": {"drain_in_flight_step": round(drain_ms, 4),

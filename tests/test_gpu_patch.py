@@ -156,12 +156,15 @@ def test_push_path_direct_into_destination(ns):
     N.lib().pl_patch_destroy(h)
 
 
-@pytest.mark.parametrize("seed", [0, 1, 2])
-def test_side_stream_push_overlapped_with_decode_writes(seed):
+@pytest.mark.parametrize("seed,chunked", [(0, False), (1, False), (2, False), (0, True), (3, True)])
+def test_side_stream_push_overlapped_with_decode_writes(monkeypatch, seed, chunked):
     """K3/K4/K5 on a low-priority side stream while K1 keeps writing (and marking) on the
     store's stream with no host sync in between: after the final round the destination
     holds exactly the source's migrating groups, byte for byte, and requests freed
-    mid-migration are gone from both."""
+    mid-migration are gone from both.  `chunked`: every round that allocates destination
+    blocks takes the pipelined multi-launch path."""
+    if chunked:
+        monkeypatch.setenv("PL_PUSH_CHUNK_MIN_BLOCKS", "1")
     import random
 
     import torch
@@ -209,3 +212,81 @@ def test_side_stream_push_overlapped_with_decode_writes(seed):
                 assert dst.read_cell(rid, g, pos, 1) == src.read_cell(rid, g, pos, 1)
     assert p.dirty_keys() == 0
     p.close()
+
+
+def _chunk_rig(cap_dst, n_req=48, seed=0):
+    import random
+
+    from paper_2604_12171_b200 import kvstore
+    from paper_2604_12171_b200.events import stable_hash
+
+    rng = random.Random(seed)
+    reg = kvstore.RequestRegistry()
+    names = [f"c{i:03d}" for i in range(n_req)]
+    for n in names:
+        reg.handle(n)
+    src = kvstore.KvStore(1, 2, 16, 4096, (0, 1, 2), num_groups=3, cell_bytes=256, registry=reg)
+    dst = kvstore.KvStore(2, 2, 16, cap_dst, (), num_groups=3, cell_bytes=256, registry=reg)
+    dst.resident_groups |= {1, 2}
+    for n in names:
+        for g in range(3):
+            src.append_seeded(n, g, 1 + rng.randrange(300), stable_hash(n, g))
+    return reg, names, src, dst
+
+
+def _dst_state(dst, names):
+    tables = {n: [b.block_id for b in dst.tables[n].chain] for n in names if n in dst.tables}
+    cells = {(n, g, p): dst.read_cell(n, g, p, j)
+             for n in names if n in dst.tables for g in (1, 2)
+             for p in {0, dst.tables[n].written.get(g, 1) - 1} if dst.tables[n].written.get(g, 0)
+             for j in (0, 1)}
+    return tables, {g: dst.snapshot_group(g) for g in (1, 2)}, cells, dst.used_blocks
+
+
+@pytest.mark.parametrize("cap_dst,seed", [(4096, 0), (4096, 1), (300, 2)])
+def test_chunked_bulk_push_equals_single_launch(monkeypatch, cap_dst, seed):
+    """A cold bulk round that allocates many destination blocks is reserved and copied in
+    pipelined runs (Patch::push_chunked).  Forced down to tiny runs, it must leave the
+    destination exactly as the one-launch push does: same block ids (allocation order),
+    same fingerprints and bytes -- and, when the destination overflows mid-round, the
+    same applied prefix and the same KvOverflow."""
+    from paper_2604_12171_b200 import _native as N
+    from paper_2604_12171_b200.perf import NativePatch
+
+    states = []
+    for chunked in (False, True):
+        if chunked:
+            monkeypatch.delenv("PL_PUSH_NO_CHUNK", raising=False)
+            monkeypatch.setenv("PL_PUSH_CHUNK_MIN_BLOCKS", "1")
+        else:
+            monkeypatch.setenv("PL_PUSH_NO_CHUNK", "1")
+        reg, names, src, dst = _chunk_rig(cap_dst, seed=seed)
+        p = NativePatch(src, (1, 2), 2)
+        p.seed()
+        N.check(N.lib().pl_timing_reset())
+        N.check(N.lib().pl_timing_enable(1))
+        overflow = None
+        try:
+            p.push(dst, reg.rank())
+        except N.NativeError as e:
+            assert e.code == -1            # PL_E_KV_OVERFLOW -> KvOverflow
+            overflow = str(e)
+        src.sync()
+        dst.sync()
+        launches = N.timing("patch_push")[1]
+        N.check(N.lib().pl_timing_enable(0))
+        states.append((overflow, _dst_state(dst, names)))
+        if chunked:
+            assert launches > 2, launches
+        else:
+            assert launches == 1
+        if cap_dst >= 4096:
+            assert overflow is None
+            for g in (1, 2):
+                assert dst.snapshot_group(g) == src.snapshot_group(g)
+        else:
+            assert overflow is not None
+        p.close()
+        src.close()
+        dst.close()
+    assert states[0] == states[1]
