@@ -18,6 +18,7 @@
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
+#include <deque>
 #include <vector>
 
 #include "../../include/pipelive.h"
@@ -293,9 +294,16 @@ struct Store {
   // scratch
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
-  void* h_pinned = nullptr;
-  size_t pinned_bytes = 0;
-  cudaEvent_t pinned_ev = nullptr;
+  // pinned staging ring for H2D uploads: each Upload takes the next span and records an
+  // event behind its copy; a span is reused only once its copy has run, so the host can
+  // queue several uploads ahead of the device (a single buffer would block each upload on
+  // the previous one -- e.g. on every run of a chunked push, behind the last patch)
+  struct PinnedSpan { size_t a, b; cudaEvent_t ev; };
+  uint8_t* h_ring = nullptr;
+  size_t ring_cap = 0, ring_head = 0;
+  std::deque<PinnedSpan> ring_live;
+  std::vector<cudaEvent_t> ring_events;  // idle events
+  size_t ring_a = 0, ring_b = 0;         // span handed out by pinned(), committed by go()
 
   std::vector<Patch*> patches;  // patches whose source is this store
   uint64_t* d_bases_ = nullptr;  // device copy of the per-group arena bases
@@ -349,7 +357,8 @@ struct Store {
   void grant_peer_access(int peer);
   std::vector<int> peer_granted;
   void* scratch(size_t bytes);
-  void* pinned(size_t bytes);
+  void* pinned(size_t bytes);           // next span of the staging ring
+  void pinned_commit(cudaStream_t st);  // the span's H2D is enqueued on st
   void materialise(int g);
   void dematerialise(int g);
   uint64_t group_base(int g) const { return (uint64_t)arenas[g].va; }

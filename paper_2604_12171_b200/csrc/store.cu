@@ -34,7 +34,6 @@ Store::Store(int device_, int gpu_id_, int k_, int s_, int64_t cell_bytes_, int 
   PL_CUDA(cudaFree(0));
   PL_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
   stream = own_stream;
-  PL_CUDA(cudaEventCreateWithFlags(&pinned_ev, cudaEventDisableTiming));
   fp_bytes = round_up((int64_t)s * 8, 128);
   unit_bytes = round_up(fp_bytes + (int64_t)k * s * cell_bytes, 128);
   size_t gran = vmm_granularity(device);
@@ -86,8 +85,12 @@ Store::~Store() {
   cudaFree(d_owner_idx);
   cudaFree(d_scratch);
   cudaFree(d_bases_);
-  if (h_pinned) cudaFreeHost(h_pinned);
-  cudaEventDestroy(pinned_ev);
+  for (auto& sp : ring_live) {
+    cudaEventSynchronize(sp.ev);
+    cudaEventDestroy(sp.ev);
+  }
+  for (auto ev : ring_events) cudaEventDestroy(ev);
+  if (h_ring) cudaFreeHost(h_ring);
   cudaStreamSynchronize(own_stream);
   cudaStreamDestroy(own_stream);  // a caller's stream (pl_store_set_stream) is not ours
 }
@@ -277,14 +280,45 @@ void* Store::scratch(size_t bytes) {
   return d_scratch;
 }
 void* Store::pinned(size_t bytes) {
-  // the previous H2D from the pinned buffer must have completed before reuse
-  PL_CUDA(cudaEventSynchronize(pinned_ev));
-  if (bytes > pinned_bytes) {
-    if (h_pinned) cudaFreeHost(h_pinned);
-    pinned_bytes = std::max(bytes, pinned_bytes * 2);
-    PL_CUDA(cudaMallocHost(&h_pinned, pinned_bytes));
+  const size_t n = round_up((int64_t)std::max<size_t>(bytes, 1), 256);
+  auto retire_front = [&] {
+    PL_CUDA(cudaEventSynchronize(ring_live.front().ev));
+    ring_events.push_back(ring_live.front().ev);
+    ring_live.pop_front();
+  };
+  if (4 * n > ring_cap) {  // room for at least four uploads of this size in flight
+    while (!ring_live.empty()) retire_front();
+    if (h_ring) cudaFreeHost(h_ring);
+    ring_cap = std::max<size_t>((size_t)1 << 20, 1);
+    while (ring_cap < 4 * n) ring_cap *= 2;
+    PL_CUDA(cudaMallocHost(&h_ring, ring_cap));
+    ring_head = 0;
   }
-  return h_pinned;
+  if (ring_head + n > ring_cap) ring_head = 0;
+  const size_t a = ring_head, b = a + n;
+  // wait (oldest first) until no in-flight span overlaps [a, b)
+  for (;;) {
+    bool hit = false;
+    for (const PinnedSpan& sp : ring_live)
+      if (sp.a < b && a < sp.b) { hit = true; break; }
+    if (!hit) break;
+    retire_front();
+  }
+  ring_a = a;
+  ring_b = b;
+  ring_head = b;
+  return h_ring + a;
+}
+void Store::pinned_commit(cudaStream_t st) {
+  cudaEvent_t ev;
+  if (!ring_events.empty()) {
+    ev = ring_events.back();
+    ring_events.pop_back();
+  } else {
+    PL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  PL_CUDA(cudaEventRecord(ev, st));
+  ring_live.push_back({ring_a, ring_b, ev});
 }
 
 int Upload::add(const void* p, size_t bytes) {
@@ -299,7 +333,7 @@ void Upload::go(size_t extra_device_bytes) {
     if (parts[i].second) std::memcpy(h + offs[i], parts[i].first, parts[i].second);
   dev = static_cast<uint8_t*>(st->scratch(total + extra_device_bytes + 256));
   if (total) PL_CUDA(cudaMemcpyAsync(dev, h, total, cudaMemcpyHostToDevice, st->stream));
-  PL_CUDA(cudaEventRecord(st->pinned_ev, st->stream));
+  st->pinned_commit(st->stream);
 }
 
 void Store::grant_peer_access(int peer) {
