@@ -171,7 +171,7 @@ def test_infeasible_trigger_recorded_not_crash():
 
 
 # --- test_engine.py:18-130 -----------------------------------------------------------------
-def tiny(num_requests=3, rate=100.0, n_gpus=1, layers=4, pattern="prefill_heavy"):
+def tiny(num_requests=3, rate=100.0, n_gpus=1, layers=4, pattern="prefill_heavy", max_batch=32):
     from paper_2604_12171_b200.engine import WorkloadSpec
     from paper_2604_12171_b200.scenario import Scenario
     c = _cl()
@@ -181,7 +181,7 @@ def tiny(num_requests=3, rate=100.0, n_gpus=1, layers=4, pattern="prefill_heavy"
         model=c.ModelSpec(layers, 16 * MIB, 8 * KIB, 1, 2 * KIB),
         initial_config=c.PPConfig([(i, ((i - 1) * per + 1, i * per)) for i in range(1, n_gpus + 1)]),
         workload=WorkloadSpec(pattern=pattern, rate=rate, num_requests=num_requests),
-        triggers=[], max_batch=32)
+        triggers=[], max_batch=max_batch)
 
 
 def test_exact_counts_and_means():
@@ -269,3 +269,67 @@ def test_different_seed_differs():
     from paper_2604_12171_b200.simulation import run_scenario
     assert run_scenario(tiny(num_requests=6), seed=1).trace.to_jsonl() != \
         run_scenario(tiny(num_requests=6), seed=2).trace.to_jsonl()
+
+
+# --- TestComputeMetrics / TestScore / TestContinuousBatching (test_engine.py:133-216) -------
+def _trace(events):
+    from paper_2604_12171_b200.events import EventTrace
+    tr = EventTrace()
+    for t, kind, payload in events:
+        tr.emit(t, "engine", kind, **payload)
+    return tr
+
+
+def _req(rid, n_in, n_out, t_first, t_done):
+    return [(0.0, "request_arrival", {"id": rid, "input_len": n_in, "output_len": n_out}),
+            (t_first, "first_token", {"id": rid}), (t_done, "request_done", {"id": rid})]
+
+
+def test_arithmetic_example():
+    from paper_2604_12171_b200.engine import compute_metrics
+    m = compute_metrics(_trace(_req("r", 100, 17, 2.0, 10.0)))
+    assert m.ttft_mean == 2.0 and m.tpot_mean == pytest.approx(0.5)   # 8 s / 16 tokens
+
+
+def test_output_len_1_excluded_from_tpot():
+    from paper_2604_12171_b200.engine import compute_metrics
+    assert compute_metrics(_trace(_req("a", 8, 1, 1.0, 1.0))).tpot_mean == 0.0
+
+
+def test_no_reconfig_means_zero_stop_time():
+    from paper_2604_12171_b200.engine import compute_metrics
+    m = compute_metrics(_trace(_req("a", 8, 4, 1.0, 2.0)))
+    assert (m.stop_time, m.migration_time) == (0.0, 0.0)
+
+
+def _rows(vals):
+    from paper_2604_12171_b200.engine import Metrics
+    out = []
+    for ttft, tpot, tput in vals:
+        m = Metrics()
+        m.ttft_mean, m.tpot_mean, m.throughput = ttft, tpot, tput
+        out.append(m)
+    return out
+
+
+@pytest.mark.parametrize("vals,want", [
+    ([(1.0, 1.0, 10.0), (2.0, 2.0, 5.0)], [1.0, 0.0]),
+    ([(1.0, 3.0, 10.0), (1.0, 4.0, 20.0)], [2.0 / 3, 2.0 / 3]),   # tied ttft counts 1 for both
+    ([(1.0, 1.0, 1.0)] * 3, [1.0, 1.0, 1.0]),
+], ids=["test_best_row_scores_1", "test_degenerate_metric_scores_1_for_all",
+        "test_all_identical_rows"])
+def test_score(vals, want):
+    from paper_2604_12171_b200.engine import score
+    assert score(_rows(vals)) == pytest.approx(want)
+
+
+@gpu
+@pytest.mark.parametrize("n,max_batch", [(4, 4), (6, 2)],
+                         ids=["test_decode_rounds_batch_requests", "test_max_batch_respected"])
+def test_continuous_batching(n, max_batch):
+    from paper_2604_12171_b200.simulation import run_scenario
+    res = run_scenario(tiny(num_requests=n, rate=1e5, pattern="decode_heavy", max_batch=max_batch),
+                       seed=3)
+    sizes = [e.payload["batch"] for e in res.trace
+             if e.kind == "stage_start" and e.payload["mb_kind"] == "decode"]
+    assert 1 < max(sizes) <= max_batch
