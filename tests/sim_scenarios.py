@@ -21,7 +21,8 @@ def _two_gpus():
                     decode_cost=2.4e-5)]
 
 
-def hetero_scenario(rate=7.0, n=120, k=2, triggers=True, flags=None, tau=50) -> Scenario:
+def hetero_scenario(rate=7.0, n=120, k=2, triggers=True, flags=None, tau=50,
+                    init=None) -> Scenario:
     shift = n / rate / 2
     model = ModelSpec(num_layers=16, layer_weight_bytes=int(2.5 * GIB),
                       token_kv_bytes_per_layer=128 * KIB, stacking_factor=k,
@@ -30,9 +31,20 @@ def hetero_scenario(rate=7.0, n=120, k=2, triggers=True, flags=None, tau=50) -> 
                       shifts=((0.0, "prefill_heavy"), (shift, "decode_heavy")))
     tgt = PPConfig([(1, (1, 14)), (2, (15, 16))])
     return Scenario(cluster=_two_gpus(), model=model,
-                    initial_config=PPConfig([(1, (1, 2)), (2, (3, 16))]), workload=wl,
+                    initial_config=init or PPConfig([(1, (1, 2)), (2, (3, 16))]), workload=wl,
                     triggers=[ReconfigTrigger(at=shift, target=tgt, tau=tau)] if triggers else [],
                     flags=flags or FeatureFlags())
+
+
+def stacking_scenario(k: int, n: int = 6) -> Scenario:
+    """Short fixed-length requests on a 16-layer model at stacking k
+    (pkg/tests/scenarios.py:120-134)."""
+    gpus = [GpuSpec(id=i, mem_total=32 * GIB, mem_bandwidth=1e12, prefill_cost=1e-6,
+                    decode_cost=1e-5) for i in (1, 2)]
+    model = ModelSpec(num_layers=16, layer_weight_bytes=256 * MIB, token_kv_bytes_per_layer=8 * KIB,
+                      stacking_factor=k, activation_bytes_per_token=8 * KIB)
+    return Scenario(cluster=gpus, model=model, initial_config=PPConfig([(1, (1, 8)), (2, (9, 16))]),
+                    workload=WorkloadSpec("prefill_heavy", rate=50.0, num_requests=n))
 
 
 def _random_partition(rng, total: int, parts: int) -> list[int]:
