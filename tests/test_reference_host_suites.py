@@ -402,3 +402,57 @@ def test_evicting_committed_layer_rejected():
     ld.is_layer_committed = lambda gpu, layer: layer == 5
     with pytest.raises(LayerInUse):
         ld.evict_layers(1, {5})
+
+
+# --- test_cli.py TestScenarioLoading (scenario files; the argparse front end is out of scope) --
+def scenario_doc(**over):
+    doc = {"schema_version": 1,
+           "cluster": [{"id": i, "mem_total": "8 GiB", "mem_bandwidth": "900 GB/s",
+                        "prefill_cost": f"{i} us", "decode_cost": f"{10 // i} us",
+                        "alloc_granularity": "2 MiB"} for i in (1, 2)],
+           "model": {"num_layers": 8, "layer_weight_bytes": "64 MiB",
+                     "token_kv_bytes_per_layer": "16 KiB", "stacking_factor": 1,
+                     "activation_bytes_per_token": "4 KiB"},
+           "initial_config": [[1, [1, 4]], [2, [5, 8]]],
+           "workload": {"pattern": "prefill_heavy", "rate": "50 req/s", "num_requests": 5}}
+    doc.update(over)
+    return doc
+
+
+def test_roundtrip(tmp_path):
+    import yaml
+
+    from paper_2604_12171_b200.scenario import load_scenario
+    path = tmp_path / "scen.yaml"
+    path.write_text(yaml.safe_dump(scenario_doc()))
+    scen = load_scenario(str(path))
+    assert (scen.model.num_layers, scen.cluster[0].mem_total, scen.workload.rate) == \
+        (8, 8 * GIB, 50.0)
+
+
+@pytest.mark.parametrize("edit,field", [
+    (lambda d: d["model"].__setitem__("layer_weight_bytes", 67108864), "layer_weight_bytes"),
+    (lambda d: d["cluster"][0].__setitem__("prefill_cost", "4 MiB"), "prefill_cost"),
+    (lambda d: d.__setitem__("initial_config", [[1, [1, 4]], [2, [4, 8]]]), "initial_config"),
+], ids=["test_bare_number_rejected", "test_wrong_unit_dimension_rejected",
+        "test_invalid_config_names_field"])
+def test_scenario_errors_name_the_field(edit, field):
+    from paper_2604_12171_b200.scenario import ScenarioError, scenario_from_dict
+    doc = scenario_doc()
+    edit(doc)
+    with pytest.raises(ScenarioError) as err:
+        scenario_from_dict(doc)
+    assert field in str(err.value)
+
+
+def test_packaged_example_loads(tmp_path):
+    import json
+    from pathlib import Path
+
+    from paper_2604_12171_b200.scenario import load_scenario
+    text = json.loads((Path(__file__).parent / "golden" / "cli_outputs.json").read_text())[
+        "packaged_seed0"]["yaml"]                    # pkg/scenarios/heterogeneous_shift.yaml
+    path = tmp_path / "heterogeneous_shift.yaml"
+    path.write_text(text)
+    scen = load_scenario(str(path))
+    assert scen.triggers and scen.workload.pattern == "shift_schedule"
