@@ -498,6 +498,7 @@ struct Patch {
   CopyLaunch push_launch(Store* dst, const uint8_t* d_apply, uint8_t apply_id);
   void push_chunked(Store* dst, const int32_t* rank, int64_t n_rank);
   int64_t new_dst_blocks(Store* dst) const;
+  bool streams_idle(Store* dst) const;
   void apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
              int64_t n_stale);
   void push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells);

@@ -146,6 +146,7 @@ static int64_t chunk_min_blocks() {
   return v ? std::max<int64_t>(1, std::atoll(v)) : kChunkedPushMinBlocks;
 }
 static bool no_chunking() { return std::getenv("PL_PUSH_NO_CHUNK") != nullptr; }
+static bool forced_chunking() { return std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS") != nullptr; }
 
 static int64_t insert_interval(std::vector<Interval>& v, int64_t a, int64_t b) {
   // merge [a,b) into sorted disjoint v (adjacent intervals merge); returns newly covered
@@ -479,6 +480,20 @@ void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t
   if (status != PL_OK) fail(status, dst->last_msg);
 }
 
+// Pipelining the reservation only pays when the device would otherwise wait for it.  If
+// the streams the copy depends on still have work queued (a caller that runs ahead of the
+// device, e.g. the next step's appends already enqueued), the host reservation is hidden
+// behind that work and one launch avoids the per-run grid tails.
+bool Patch::streams_idle(Store* dst) const {
+  const cudaStream_t ss[3] = {pstream(), src->stream, dst->stream};
+  for (cudaStream_t s : ss) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaErrorNotReady) return false;
+    PL_CUDA(q);
+  }
+  return true;
+}
+
 int64_t Patch::new_dst_blocks(Store* dst) const {
   // destination blocks the drained set will allocate: per request, the chain it needs past
   // the chain it has (the chain is shared by the request's groups)
@@ -641,7 +656,8 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   take_drained();
   *keys = drained_keys;
   *cells = host_cells(drained);
-  if (drained.size() >= 2 && !no_chunking() && new_dst_blocks(dst) >= chunk_min_blocks()) {
+  if (drained.size() >= 2 && !no_chunking() && (forced_chunking() || streams_idle(dst)) &&
+      new_dst_blocks(dst) >= chunk_min_blocks()) {
     push_chunked(dst, rank, n_rank);
     return;
   }
