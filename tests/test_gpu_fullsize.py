@@ -1,0 +1,96 @@
+"""Parity at BASELINE configs[1]'s full size (Llama-3-8B shape, B = 256 x 2048 tokens,
+4096 B cells, 17.2 GB per bulk round) through size-independent properties: every
+fingerprint of both migrating groups on the destination equals the source's and the
+engine's payload (engine.py:252-261); sampled cells are bit-exact copies and equal the
+oracle's expansion of their fingerprint; a steady round after random writes moves exactly
+the marked keys; the pipelined cold push (runs) and the one-launch push give identical
+destinations (same block ids)."""
+
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _rig(chunked, monkeypatch):
+    from paper_2604_12171_b200.perf import PatchRig, Workload
+    if chunked:
+        monkeypatch.delenv("PL_PUSH_NO_CHUNK", raising=False)
+    else:
+        monkeypatch.setenv("PL_PUSH_NO_CHUNK", "1")
+    rig = PatchRig(Workload())
+    rig.fill()
+    return rig
+
+
+def _check_group(rig, g, rng, n_samples=64):
+    from paper_2604_12171_b200.events import stable_hash
+    from paper_2604_12171_b200.perf import engine_payloads, rid
+    wl = rig.wl
+    src, dst = rig.src.snapshot_group(g), rig.dst.snapshot_group(g)
+    assert len(dst) == wl.batch and dst == src
+    for i in rng.sample(range(wl.batch), 8):          # fingerprints = the engine's payloads
+        want = engine_payloads(stable_hash(rid(i), g), len(dst[rid(i)]))
+        assert np.array_equal(np.array(dst[rid(i)], dtype=np.uint64), want)
+    for _ in range(n_samples):                        # bytes: copy of the source, = expansion
+        i, pos, j = rng.randrange(wl.batch), rng.randrange(wl.ctx), rng.randrange(wl.k)
+        cell = rig.dst.read_cell(rid(i), g, pos, j)
+        assert cell == rig.src.read_cell(rid(i), g, pos, j)
+        assert cell == oracle.expand_cell(dst[rid(i)][pos], j, wl.cell_bytes)
+
+
+@pytest.fixture(scope="module")
+def runs():
+    return {}
+
+
+@pytest.mark.parametrize("chunked", [True, False])
+def test_fullsize_bulk_round(monkeypatch, runs, chunked):
+    import torch
+    rng = random.Random(7)
+    rig = _rig(chunked, monkeypatch)
+    torch.cuda.synchronize()
+    keys, cells = rig.bulk_round()
+    rig.src.sync()
+    rig.dst.sync()
+    wl = rig.wl
+    assert keys == wl.batch * wl.ctx * len(wl.mig_groups)
+    assert cells * wl.cell_bytes == wl.payload_bytes == 17_179_869_184
+    for g in wl.mig_groups:
+        _check_group(rig, g, rng)
+    # block ids of the destination chains: identical with and without the pipelined runs
+    from paper_2604_12171_b200.perf import rid
+    runs[chunked] = [[b.block_id for b in rig.dst.tables[rid(i)].chain] for i in range(0, wl.batch, 17)]
+    if len(runs) == 2:
+        assert runs[True] == runs[False]
+    rig.destroy()
+
+
+def test_fullsize_steady_round_moves_exactly_the_marked_keys(monkeypatch):
+    """After the bulk round, append one token to a random half of the requests in both
+    migrating groups (K1 with the fused dirty mark): the next round drains exactly those
+    keys and the destination again equals the source."""
+    from paper_2604_12171_b200.events import stable_hash
+    from paper_2604_12171_b200.perf import append_batch, rid
+    rng = random.Random(11)
+    rig = _rig(True, monkeypatch)
+    rig.bulk_round()
+    wl = rig.wl
+    pick = sorted(rng.sample(range(wl.batch), wl.batch // 2))
+    reqs = [rig.handles[i] for i in pick for _ in wl.src_groups]
+    groups = [g for _ in pick for g in wl.src_groups]
+    append_batch(rig.src, reqs, groups, [1] * len(reqs),
+                 [stable_hash(rid(i), g) for i in pick for g in wl.src_groups], mark=True)
+    keys, _ = rig.patch.push(rig.dst, rig.registry.rank())
+    rig.src.sync()
+    rig.dst.sync()
+    assert keys == len(pick) * len(wl.mig_groups)
+    for g in wl.mig_groups:
+        _check_group(rig, g, rng, n_samples=16)
+        for i in pick[:8]:                            # the new token is there, bit-exact
+            assert rig.dst.read_cell(rid(i), g, wl.ctx, 0) == rig.src.read_cell(rid(i), g, wl.ctx, 0)
+    rig.destroy()
