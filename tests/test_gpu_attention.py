@@ -151,3 +151,47 @@ def test_cuda_core_fallback_for_small_blocks(n_q):
     bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
     assert np.all(err <= bound + 1e-3), float(err.max())
     assert np.all(got[2] == 0)
+
+
+@pytest.mark.parametrize("n_q", [32, 64], ids=["llama3_8b", "llama3_70b"])
+def test_decode_full_bench_shape_sampled(n_q):
+    """K2 at the bench's full shape (B = 256, ctx = 2048, 16-token blocks, k = 4, 8 KV heads
+    x 128): the whole batch runs as one launch (stream-K over 148 SMs); 16 sampled
+    sequences are checked against the fp32 oracle."""
+    import torch
+
+    from paper_2604_12171_b200 import _native as N
+    from paper_2604_12171_b200 import kvstore
+
+    B, ctx, n_kv, D, s, k, layer = 256, 2048, 8, 128, 16, 4, 2
+    torch.manual_seed(n_q)
+    cell = 2 * n_kv * D * 2
+    st = kvstore.KvStore(1, k, s, B * ctx // s + 8, (0,), cell_bytes=cell)
+    pick = sorted(np.random.default_rng(n_q).choice(B, 16, replace=False).tolist())
+    keep = {}
+    for b in range(B):
+        x = torch.randn(ctx, k, 2 * n_kv * D, dtype=torch.bfloat16, device="cuda")
+        st.append_seeded(f"full{b}", 0, ctx, 99 + b, kv_dev=x.data_ptr())
+        if b in pick:
+            keep[b] = x[:, layer].view(torch.int16).cpu().numpy().view(np.uint16)
+        st.sync()
+        del x
+    rows = torch.tensor([st._registry.handle(f"full{b}") for b in range(B)], dtype=torch.int32,
+                        device="cuda")
+    ctx_t = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
+    q = torch.randn(B, n_q, D, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty_like(q)
+    N.check(N.lib().pl_paged_attn_decode(st._h, 0, layer, C.c_void_p(q.data_ptr()),
+                                         C.c_void_p(out.data_ptr()), C.c_void_p(rows.data_ptr()),
+                                         C.c_void_p(ctx_t.data_ptr()), B, n_q, n_kv, D, D ** -0.5,
+                                         ctx, None))
+    torch.cuda.synchronize()
+    qf = bf16_to_f32(q.view(torch.int16).cpu().numpy().view(np.uint16))[pick]
+    ks = [bf16_to_f32(keep[b].reshape(-1, 2, n_kv, D)[:, 0]) for b in pick]
+    vs = [bf16_to_f32(keep[b].reshape(-1, 2, n_kv, D)[:, 1]) for b in pick]
+    ref = decode_attention(qf, ks, vs, D ** -0.5)
+    got = bf16_to_f32(out.view(torch.int16).cpu().numpy().view(np.uint16))[pick]
+    err = np.abs(got - ref)
+    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
+    assert np.all(err <= bound + 1e-3), float(err.max())
+    st.close()
