@@ -316,7 +316,8 @@ def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
                     "stream) overlap on one GPU and share its HBM"}
 
 
-def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040) -> dict:
+def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040,
+                   check: bool = False) -> dict:
     """BASELINE configs[2] at one GPU: the source stage of a Llama-3-70B PP 4 -> 8 boundary
     shift with HBM pre-filled by KV cache.
 
@@ -328,7 +329,13 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040) -> di
     b_shrink = max_blocks(24) = 76,888 (coordinator.py:103-110, 189-201) while ~17 GB
     of live KV sits above that line; after the commit it drops groups 3, 4 and grows to
     b_new = max_blocks(16) = 128,387 (coordinator.py:340-354).  The migrating groups are
-    pushed to a destination store on the same GPU (HBM-bound here, NVLink across GPUs)."""
+    pushed to a destination store on the same GPU (HBM-bound here, NVLink across GPUs).
+
+    ``check`` (tests only; off in the bench): sampled fingerprints and cell bytes are read
+    before the shrink and must survive the K6 relocation, the drop and the grow; the
+    destination's migrating groups must equal the source's after the patch rounds."""
+    import random
+
     import torch
 
     from .cluster import GpuSpec, ModelSpec, max_blocks
@@ -361,6 +368,21 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040) -> di
     out["filled_blocks"] = fill_reqs * per_req
     out["live_blocks"] = src.used_blocks
     out["kv_bytes_live"] = src.used_blocks * 5 * src.info()["unit_bytes"]
+    samples = {}
+    if check:
+        rng = random.Random(2)
+        live_ids = [i for i in range(fill_reqs) if src._has_table(hs[i])]
+        for _ in range(96):
+            i, g, p, j = rng.choice(live_ids), rng.randrange(5), rng.randrange(ctx), rng.randrange(4)
+            samples[(rid(i), g, p, j)] = (src.read_checksum(rid(i), g, p), src.read_cell(rid(i), g, p, j))
+
+    def verify(store, groups, what):
+        for (r, g, p, j), (fp, cell) in samples.items():
+            if g in groups:
+                assert store.read_checksum(r, g, p) == fp, (what, r, g, p)
+                assert store.read_cell(r, g, p, j) == cell, (what, r, g, p, j)
+        out.setdefault("checks", []).append(what)
+
     # Phase 2: compact + shrink with relocation, then map the incoming group 5
     t0 = time.perf_counter()
     src.compact()
@@ -368,6 +390,9 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040) -> di
     src.sync()
     out["phase2_shrink_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
     out["phase2_shrink_stats"] = src.last_resize_stats()
+    if check:
+        assert src.capacity_blocks == b_shrink and src.used_blocks == out["live_blocks"]
+        verify(src, range(5), "relocation")
     free_gb = lambda: round(torch.cuda.mem_get_info(device)[0] / 1e9, 1)  # noqa: E731
     out["free_gb_after_shrink"] = free_gb()
     t0 = time.perf_counter()
@@ -399,6 +424,10 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040) -> di
     src.sync()
     dst.sync()
     out["residual_patch"] = {"keys": keys, "ms": round((time.perf_counter() - t0) * 1e3, 3)}
+    if check:
+        for g in (3, 4):
+            assert dst.snapshot_group(g) == src.snapshot_group(g), g
+        verify(dst, (3, 4), "patched")
     patch.close()
     out["free_gb_during_patch"] = free_gb()
     dst.close()   # the destination is another GPU on hardware; free its HBM here
@@ -411,6 +440,9 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040) -> di
     src.resize(b_new)
     src.sync()
     out["grow_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    if check:
+        assert src.capacity_blocks == b_new
+        verify(src, (0, 1, 2), "drop+grow")
     v1 = src.vmm_stats()
     out["grow_stats"] = {**src.last_resize_stats(),
                          **{k: v1[k] - v0[k] for k in ("tail_reused_chunks", "cache_reused_chunks",

@@ -94,3 +94,21 @@ def test_fullsize_steady_round_moves_exactly_the_marked_keys(monkeypatch):
         for i in pick[:8]:                            # the new token is there, bit-exact
             assert rig.dst.read_cell(rid(i), g, wl.ctx, 0) == rig.src.read_cell(rid(i), g, wl.ctx, 0)
     rig.destroy()
+
+
+def test_fullsize_configs2_live_resize():
+    """BASELINE configs[2] (Llama-3-70B shape, PP 4 -> 8, HBM pre-filled to ~100 GB of live
+    KV): Phase-2 shrink relocates >13 k live blocks with K6, the leaving groups are patched
+    to a destination, then dropped, and the stage grows to b_new.  Sampled fingerprints and
+    4096-B cells survive every step; the destination's groups equal the source's."""
+    import gc
+
+    import torch
+
+    from paper_2604_12171_b200.perf import c3_live_resize
+    gc.collect()
+    torch.cuda.empty_cache()
+    out = c3_live_resize(0, check=True)
+    assert out["checks"] == ["relocation", "patched", "drop+grow"]
+    assert out["phase2_shrink_stats"]["relocated_blocks"] > 13_000
+    assert out["bulk_patch"]["payload_bytes"] > 39e9
