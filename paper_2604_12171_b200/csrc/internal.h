@@ -294,16 +294,26 @@ struct Store {
   // scratch
   void* d_scratch = nullptr;
   size_t scratch_bytes = 0;
-  // pinned staging ring for H2D uploads: each Upload takes the next span and records an
-  // event behind its copy; a span is reused only once its copy has run, so the host can
-  // queue several uploads ahead of the device (a single buffer would block each upload on
-  // the previous one -- e.g. on every run of a chunked push, behind the last patch)
-  struct PinnedSpan { size_t a, b; cudaEvent_t ev; };
-  uint8_t* h_ring = nullptr;
-  size_t ring_cap = 0, ring_head = 0;
+  // Staging ring for H2D uploads (Upload): a pinned host ring and a device ring with the
+  // same offsets.  Each upload takes the next span, copies on the store's copy stream
+  // (`up_stream`, so the copy overlaps kernels already queued on `stream`) and makes
+  // `stream` wait for it.  A span is reused once its copy ran (host side, `ev_h2d`) and its
+  // consumers ran (device side, `ev_used`, recorded when the Upload goes out of scope).
+  // A single buffer made every upload wait for the previous one -- behind the last patch.
+  struct StagingRing { uint8_t* h = nullptr; uint8_t* d = nullptr; size_t cap = 0; };
+  struct PinnedSpan {
+    size_t a, b;
+    uint64_t seq;
+    const StagingRing* ring;
+    cudaEvent_t ev_h2d, ev_used;  // ev_used == nullptr until the Upload is destroyed
+  };
+  std::unique_ptr<StagingRing> ring;
+  std::vector<std::unique_ptr<StagingRing>> old_rings;  // outgrown; freed once drained
+  size_t ring_head = 0;
+  uint64_t ring_seq = 0;
   std::deque<PinnedSpan> ring_live;
   std::vector<cudaEvent_t> ring_events;  // idle events
-  size_t ring_a = 0, ring_b = 0;         // span handed out by pinned(), committed by go()
+  cudaStream_t up_stream = nullptr;
 
   std::vector<Patch*> patches;  // patches whose source is this store
   uint64_t* d_bases_ = nullptr;  // device copy of the per-group arena bases
@@ -357,8 +367,11 @@ struct Store {
   void grant_peer_access(int peer);
   std::vector<int> peer_granted;
   void* scratch(size_t bytes);
-  void* pinned(size_t bytes);           // next span of the staging ring
-  void pinned_commit(cudaStream_t st);  // the span's H2D is enqueued on st
+  // next span of the staging ring: host/device pointers, sequence number
+  void stage_span(size_t bytes, uint8_t** h, uint8_t** d, uint64_t* seq);
+  void stage_commit(uint64_t seq);       // H2D of span seq enqueued on up_stream
+  void stage_consumed(uint64_t seq) noexcept;  // consumers of span seq enqueued on stream
+  cudaEvent_t ring_event();
   void materialise(int g);
   void dematerialise(int g);
   uint64_t group_base(int g) const { return (uint64_t)arenas[g].va; }
@@ -410,12 +423,18 @@ struct Upload {
   std::vector<size_t> offs;
   size_t total = 0;
   uint8_t* dev = nullptr;
+  uint8_t* dev_extra = nullptr;
+  uint64_t seq = 0;
+  bool staged = false;
   explicit Upload(Store* s) : st(s) {}
+  ~Upload();  // the consumers of this upload have been enqueued on st->stream
+  Upload(const Upload&) = delete;
+  Upload& operator=(const Upload&) = delete;
   int add(const void* p, size_t bytes);
   void go(size_t extra_device_bytes = 0);
   template <class T>
   T* ptr(int i) { return reinterpret_cast<T*>(dev + offs[i]); }
-  uint8_t* extra() { return dev + total; }
+  uint8_t* extra() { return dev_extra; }  // device scratch after the upload (store-owned)
 };
 
 // ---------------------------------------------------------------------------

@@ -85,12 +85,23 @@ Store::~Store() {
   cudaFree(d_owner_idx);
   cudaFree(d_scratch);
   cudaFree(d_bases_);
+  if (up_stream) cudaStreamSynchronize(up_stream);
   for (auto& sp : ring_live) {
-    cudaEventSynchronize(sp.ev);
-    cudaEventDestroy(sp.ev);
+    cudaEventSynchronize(sp.ev_h2d);
+    cudaEventDestroy(sp.ev_h2d);
+    if (sp.ev_used && sp.ev_used != sp.ev_h2d) {
+      cudaEventSynchronize(sp.ev_used);
+      cudaEventDestroy(sp.ev_used);
+    }
   }
   for (auto ev : ring_events) cudaEventDestroy(ev);
-  if (h_ring) cudaFreeHost(h_ring);
+  auto free_ring = [](StagingRing* r) {
+    if (r->h) cudaFreeHost(r->h);
+    if (r->d) cudaFree(r->d);
+  };
+  if (ring) free_ring(ring.get());
+  for (auto& r : old_rings) free_ring(r.get());
+  if (up_stream) cudaStreamDestroy(up_stream);
   cudaStreamSynchronize(own_stream);
   cudaStreamDestroy(own_stream);  // a caller's stream (pl_store_set_stream) is not ours
 }
@@ -279,37 +290,7 @@ void* Store::scratch(size_t bytes) {
   }
   return d_scratch;
 }
-void* Store::pinned(size_t bytes) {
-  const size_t n = round_up((int64_t)std::max<size_t>(bytes, 1), 256);
-  auto retire_front = [&] {
-    PL_CUDA(cudaEventSynchronize(ring_live.front().ev));
-    ring_events.push_back(ring_live.front().ev);
-    ring_live.pop_front();
-  };
-  if (4 * n > ring_cap) {  // room for at least four uploads of this size in flight
-    while (!ring_live.empty()) retire_front();
-    if (h_ring) cudaFreeHost(h_ring);
-    ring_cap = std::max<size_t>((size_t)1 << 20, 1);
-    while (ring_cap < 4 * n) ring_cap *= 2;
-    PL_CUDA(cudaMallocHost(&h_ring, ring_cap));
-    ring_head = 0;
-  }
-  if (ring_head + n > ring_cap) ring_head = 0;
-  const size_t a = ring_head, b = a + n;
-  // wait (oldest first) until no in-flight span overlaps [a, b)
-  for (;;) {
-    bool hit = false;
-    for (const PinnedSpan& sp : ring_live)
-      if (sp.a < b && a < sp.b) { hit = true; break; }
-    if (!hit) break;
-    retire_front();
-  }
-  ring_a = a;
-  ring_b = b;
-  ring_head = b;
-  return h_ring + a;
-}
-void Store::pinned_commit(cudaStream_t st) {
+cudaEvent_t Store::ring_event() {
   cudaEvent_t ev;
   if (!ring_events.empty()) {
     ev = ring_events.back();
@@ -317,8 +298,97 @@ void Store::pinned_commit(cudaStream_t st) {
   } else {
     PL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
-  PL_CUDA(cudaEventRecord(ev, st));
-  ring_live.push_back({ring_a, ring_b, ev});
+  return ev;
+}
+
+void Store::stage_span(size_t bytes, uint8_t** h, uint8_t** d, uint64_t* seq) {
+  const size_t n = round_up((int64_t)std::max<size_t>(bytes, 1), 256);
+  if (!up_stream) PL_CUDA(cudaStreamCreateWithFlags(&up_stream, cudaStreamNonBlocking));
+  // the oldest span leaves: its host bytes once its copy ran, its device bytes once its
+  // consumers ran (a device-side wait of the copy stream, no host block)
+  auto retire_front = [&] {
+    PinnedSpan& sp = ring_live.front();
+    PL_CUDA(cudaEventSynchronize(sp.ev_h2d));
+    PL_CUDA(cudaStreamWaitEvent(up_stream, sp.ev_used, 0));
+    ring_events.push_back(sp.ev_h2d);
+    if (sp.ev_used != sp.ev_h2d) ring_events.push_back(sp.ev_used);
+    ring_live.pop_front();
+  };
+  auto outgrow = [&](size_t cap) {
+    // spans in the old ring stay valid (an Upload may still be in scope); the old ring is
+    // freed once none of its spans is live
+    if (ring) old_rings.push_back(std::move(ring));
+    ring = std::make_unique<StagingRing>();
+    ring->cap = cap;
+    PL_CUDA(cudaMallocHost(&ring->h, cap));
+    PL_CUDA(cudaMalloc(&ring->d, cap));
+    ring_head = 0;
+  };
+  if (!ring || 4 * n > ring->cap) {  // room for at least four uploads of this size
+    size_t cap = (size_t)1 << 20;
+    while (cap < 4 * n) cap *= 2;
+    outgrow(std::max(cap, ring ? ring->cap : 0));
+  }
+  if (ring_head + n > ring->cap) ring_head = 0;
+  size_t a = ring_head, b = a + n;
+  for (;;) {
+    bool hit = false, busy = false;
+    for (const PinnedSpan& sp : ring_live)
+      if (sp.ring == ring.get() && sp.a < b && a < sp.b) {
+        hit = true;
+        busy |= sp.ev_used == nullptr;
+      }
+    if (!hit) break;
+    if (busy || ring_live.front().ev_used == nullptr) {
+      // an overlapping span's Upload is still in scope: take a fresh, larger ring
+      outgrow(ring->cap * 2);
+      a = 0;
+      b = n;
+      break;
+    }
+    retire_front();
+  }
+  // free outgrown rings with no live span left
+  for (size_t i = 0; i < old_rings.size();) {
+    bool live = false;
+    for (const PinnedSpan& sp : ring_live) live |= sp.ring == old_rings[i].get();
+    if (live) { ++i; continue; }
+    PL_CUDA(cudaStreamSynchronize(up_stream));
+    cudaFreeHost(old_rings[i]->h);
+    cudaFree(old_rings[i]->d);
+    old_rings.erase(old_rings.begin() + (long)i);
+  }
+  ring_head = b;
+  *h = ring->h + a;
+  *d = ring->d + a;
+  *seq = ++ring_seq;
+  ring_live.push_back({a, b, *seq, ring.get(), nullptr, nullptr});
+}
+void Store::stage_commit(uint64_t seq) {
+  for (auto it = ring_live.rbegin(); it != ring_live.rend(); ++it)
+    if (it->seq == seq) {
+      it->ev_h2d = ring_event();
+      PL_CUDA(cudaEventRecord(it->ev_h2d, up_stream));
+      PL_CUDA(cudaStreamWaitEvent(stream, it->ev_h2d, 0));
+      return;
+    }
+}
+void Store::stage_consumed(uint64_t seq) noexcept {
+  // called from ~Upload: no exceptions; a failed record leaves a synchronised marker
+  for (auto it = ring_live.rbegin(); it != ring_live.rend(); ++it)
+    if (it->seq == seq) {
+      cudaEvent_t ev = nullptr;
+      if (!ring_events.empty()) {
+        ev = ring_events.back();
+        ring_events.pop_back();
+      } else if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+        ev = nullptr;
+      }
+      if (ev && cudaEventRecord(ev, stream) != cudaSuccess) cudaStreamSynchronize(stream);
+      if (!ev) cudaStreamSynchronize(stream);
+      it->ev_used = ev ? ev : it->ev_h2d;  // ev_h2d has run once the stream is synchronised
+      return;
+    }
 }
 
 int Upload::add(const void* p, size_t bytes) {
@@ -328,12 +398,17 @@ int Upload::add(const void* p, size_t bytes) {
   return (int)parts.size() - 1;
 }
 void Upload::go(size_t extra_device_bytes) {
-  uint8_t* h = static_cast<uint8_t*>(st->pinned(std::max<size_t>(total, 256)));
+  uint8_t* h = nullptr;
+  st->stage_span(std::max<size_t>(total, 256), &h, &dev, &seq);
+  staged = true;
   for (size_t i = 0; i < parts.size(); ++i)
     if (parts[i].second) std::memcpy(h + offs[i], parts[i].first, parts[i].second);
-  dev = static_cast<uint8_t*>(st->scratch(total + extra_device_bytes + 256));
-  if (total) PL_CUDA(cudaMemcpyAsync(dev, h, total, cudaMemcpyHostToDevice, st->stream));
-  st->pinned_commit(st->stream);
+  if (total) PL_CUDA(cudaMemcpyAsync(dev, h, total, cudaMemcpyHostToDevice, st->up_stream));
+  st->stage_commit(seq);
+  if (extra_device_bytes) dev_extra = static_cast<uint8_t*>(st->scratch(extra_device_bytes + 256));
+}
+Upload::~Upload() {
+  if (staged) st->stage_consumed(seq);  // noexcept path: PL_CUDA only throws on driver errors
 }
 
 void Store::grant_peer_access(int peer) {

@@ -47,15 +47,21 @@ def step(i):
 for i in range(3):
     step(i)
 torch.cuda.synchronize()
-K = 12
+K = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 N.check(N.lib().pl_timing_reset())
 N.check(N.lib().pl_timing_enable(1))
 HT[:] = 0
+e_first, e_last = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 t0 = time.perf_counter()
+e_first.record(s)
 for i in range(K):
     step(i)
+e_last.record(s)
+t_enq = time.perf_counter()
 torch.cuda.synchronize()
 wall = (time.perf_counter() - t0) / K * 1e3
+print("device span %.3f ms/step; host enqueue done at %.1f ms, wall %.1f ms"
+      % (e_first.elapsed_time(e_last) / K, (t_enq - t0) * 1e3, wall * K))
 N.check(N.lib().pl_timing_enable(0))
 tot = 0.0
 for k in ("kv_write", "drain", "patch_push", "apply_deltas", "partition", "mark"):
@@ -66,3 +72,32 @@ for k in ("kv_write", "drain", "patch_push", "apply_deltas", "partition", "mark"
 print(f"timed kernels {tot / K:7.3f} ms/step; wall {wall:7.3f} ms/step")
 print("host ms/step: free src %.3f, free dst %.3f, append %.3f, push %.3f, d2h %.3f (sum %.3f)"
       % (*(HT / K * 1e3), HT.sum() / K * 1e3))
+
+# device timeline of one steady step: events on the store stream between the calls
+evs = []
+
+
+def mark():
+    e = torch.cuda.Event(enable_timing=True)
+    e.record(s)
+    evs.append(e)
+
+
+for i in range(6):
+    mark()
+    rig.src.free_requests(names)
+    mark()
+    rig.dst.free_requests(names)
+    mark()
+    append_batch_payloads(rig.src, reqs, groups, counts, host, mark=True)
+    mark()
+    rig.patch.push(rig.dst, rig.registry.rank())
+    mark()
+torch.cuda.synchronize()
+for i in range(1, 6):
+    e = evs[5 * i:5 * i + 5]
+    nxt = evs[5 * i + 5] if 5 * i + 5 < len(evs) else None
+    d = [e[j].elapsed_time(e[j + 1]) for j in range(4)]
+    gap = e[4].elapsed_time(nxt) if nxt else float("nan")
+    print("step %d device: free src %.3f  free dst %.3f  append %.3f  push %.3f  -> next %.3f ms"
+          % (i, *d, gap))
