@@ -320,9 +320,14 @@ paged_attn_kernel(AttnLaunch a, AttnPlan p, float* ws_acc, float* ws_ml) {
             }
           }
           // P.V: broadcast each token's probabilities from their owner lanes
+          // rows past the context in a partial stage were not loaded this time: they hold an
+          // earlier stage's bytes or whatever the SM's shared memory held before this kernel
+          // (random KV bytes of another kernel include NaN patterns), so 0 x V must not be
+          // summed.  Seen once as a NaN output under compute-sanitizer's slowed schedule.
           const uint8_t* vp = tile + (tok0 + half) * cell + v_off;
 #pragma unroll
           for (int i = 0; i < NP; ++i) {
+            const bool live = tok0 + 2 * i + half < ntok;
             float2 vf[DP2];
             load_row<VT, DP2>(vp + 2 * i * cell, vf);
 #pragma unroll
@@ -330,8 +335,10 @@ paged_attn_kernel(AttnLaunch a, AttnPlan p, float* ws_acc, float* ws_ml) {
               const int v = i * G + gg;
               const float pv = __shfl_sync(0xffffffffu, pr[v % R], tr_owner<V>(v) + 16 * half);
               const float2 p2 = make_float2(pv, pv);
+              if (live) {
 #pragma unroll
-              for (int d = 0; d < DP2; ++d) acc[gg][d] = __ffma2_rn(p2, vf[d], acc[gg][d]);
+                for (int d = 0; d < DP2; ++d) acc[gg][d] = __ffma2_rn(p2, vf[d], acc[gg][d]);
+              }
             }
           }
         }

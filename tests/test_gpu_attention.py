@@ -89,9 +89,15 @@ def test_decode_ragged_schedules(ctxs):
             assert np.all(got[b] == 0)
 
 
-def test_decode_raw_entry_over_caller_pool():
+@pytest.mark.parametrize("s,poison", [(16, False), (16, True), (4, True), (8, True)],
+                         ids=["mma", "mma_stale_nan_rows", "simt_stale_nan_rows",
+                              "mma_8tok_stale_nan_rows"])
+def test_decode_raw_entry_over_caller_pool(s, poison):
     """pl_paged_attn_decode_raw: the same kernel over a pool and block table the caller
-    owns (a pipeshift integration that keeps its own allocator)."""
+    owns (a pipeshift integration that keeps its own allocator).  `poison`: every pool
+    byte the decode must not use -- rows past each context (which the tensor-core kernel's
+    8-token TMA boxes do load), other layers, free units -- is 0xFF (bf16 NaN), as stale
+    pool memory can be; the output must still match (s = 4 runs the CUDA-core kernel)."""
     import ctypes as C
 
     import torch
@@ -99,7 +105,7 @@ def test_decode_raw_entry_over_caller_pool():
     from paper_2604_12171_b200 import _native as N
 
     torch.manual_seed(3)
-    B, n_q, n_kv, D, s, k = 3, 32, 8, 128, 16, 2
+    B, n_q, n_kv, D, k = 3, 32, 8, 128, 2
     cell = 2 * n_kv * D * 2
     fp = 128
     unit = fp + k * s * cell
@@ -107,7 +113,8 @@ def test_decode_raw_entry_over_caller_pool():
     nb = [(c + s - 1) // s for c in ctxs]
     max_blocks = max(nb)
     slots = torch.randperm(sum(nb) + 3)[: sum(nb)].tolist()   # scattered slots
-    pool = torch.zeros((sum(nb) + 3) * unit, dtype=torch.uint8, device="cuda")
+    pool = torch.full(((sum(nb) + 3) * unit,), 0xFF if poison else 0, dtype=torch.uint8,
+                      device="cuda")
     table = torch.full((B, max_blocks), -1, dtype=torch.int32)
     kvs, i = [], 0
     layer = 1
