@@ -489,6 +489,9 @@ __device__ __forceinline__ int stage_owner(int64_t x, int64_t S, int g) {
 // A sequence split over k CTAs yields k pieces; pieces in total <= B + grid - 1.
 __global__ void attn_plan_kernel(const int32_t* ctx, int B, int grid, int* sp, int* po,
                                  float* ws_ml, int64_t n_slots) {
+  // programmatic dependent launch: the decode grid may start its prologue now; it waits
+  // (griddepcontrol.wait) for this grid's completion before reading sp / po / ws_ml
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // every partial slot starts as "no data" (NaN m): a CTA whose stage range is empty
   // never writes the pieces of the sequences it sits inside, and the combine skips them
   for (int64_t i = threadIdx.x; i < 2 * n_slots; i += blockDim.x) ws_ml[i] = __int_as_float(0x7fffffff);
@@ -567,8 +570,13 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
       done_cnt[i] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&kv_map) : "memory");
   }
   __syncthreads();
+  // PDL: the plan grid's sp / po / NaN-initialised slots are visible after this wait; the
+  // combine grid may be launched now (it waits for this grid's completion in turn)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const int G = a.n_q / a.n_kv;
   const int64_t S = p.sp[a.B];
@@ -791,6 +799,7 @@ __global__ void __launch_bounds__(256) paged_attn_combine_sk(const float* ws_acc
                                                              const int* po, int n_q, int W, int64_t n_bh,
                                                              void* out) {
   constexpr int DL = D / 32;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the decode grid has completed
   const int lane = threadIdx.x & 31;
   const int64_t bh = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // b * n_q + hq
   if (bh >= n_bh) return;
@@ -927,6 +936,11 @@ EncodeTiled encode_tiled() {
   return fn;
 }
 
+bool use_pdl() {
+  static const bool off = std::getenv("PL_ATTN_NO_PDL") != nullptr;  // A/B switch
+  return !off;
+}
+
 bool mma_path_ok(const AttnLaunch& a) {
   const int G = a.n_q / a.n_kv;
   const int64_t cell = 2ll * a.n_kv * a.D * 2;
@@ -980,14 +994,29 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
   attn_plan_kernel<<<1, 1024, 0, st>>>(a.ctx, a.B, grid, sp, po, ws + np * D, (int64_t)np);
   note_launch();
   PL_CUDA(cudaGetLastError());
-  kern<<<grid, NW * 32, smem, st>>>(map, a, p, ws, ws + np * D);
+  // plan -> decode -> combine with programmatic dependent launch: each grid is launched
+  // while its predecessor runs and waits for it on the device (griddepcontrol), so the
+  // two small launches no longer add their launch latency to every layer
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = use_pdl() ? 1 : 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  PL_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a, p, ws, ws + np * D));
   note_launch();
-  PL_CUDA(cudaGetLastError());
   const int64_t n_bh = (int64_t)a.B * a.n_q;
-  paged_attn_combine_sk<D><<<(unsigned)((n_bh + 7) / 8), 256, 0, st>>>(ws, ws + np * D, po, a.n_q,
-                                                                      p.W, n_bh, a.out);
+  cudaLaunchConfig_t cfg2 = cfg;
+  cfg2.gridDim = dim3((unsigned)((n_bh + 7) / 8));
+  cfg2.blockDim = dim3(256);
+  cfg2.dynamicSmemBytes = 0;
+  PL_CUDA(cudaLaunchKernelEx(&cfg2, paged_attn_combine_sk<D>, (const float*)ws,
+                             (const float*)(ws + np * D), (const int*)po, a.n_q, p.W, n_bh, a.out));
   note_launch();
-  PL_CUDA(cudaGetLastError());
 }
 }  // namespace
 
