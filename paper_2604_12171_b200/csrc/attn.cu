@@ -478,6 +478,11 @@ struct MmaPlan {
   // piece of b; CTA c owns global stages [c*S/grid, (c+1)*S/grid)
   const int* sp;
   const int* po;
+  // local_plan: every CTA scans ctx itself into shared memory (no plan launch); CTA 0
+  // also writes sp / po to sp_out / po_out for the combine
+  int local_plan;
+  int* sp_out;
+  int* po_out;
 };
 
 // owner CTA of global stage x when S stages are split evenly over g CTAs
@@ -492,9 +497,10 @@ __global__ void attn_plan_kernel(const int32_t* ctx, int B, int grid, int* sp, i
   // programmatic dependent launch: the decode grid may start its prologue now; it waits
   // (griddepcontrol.wait) for this grid's completion before reading sp / po / ws_ml
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // every partial slot starts as "no data" (NaN m): a CTA whose stage range is empty
-  // never writes the pieces of the sequences it sits inside, and the combine skips them
-  for (int64_t i = threadIdx.x; i < 2 * n_slots; i += blockDim.x) ws_ml[i] = __int_as_float(0x7fffffff);
+  // (slots of CTAs with an empty stage range are never written; the combine skips them by
+  // arithmetic, so nothing is initialised here)
+  (void)ws_ml;
+  (void)n_slots;
   __shared__ int warp_sum[32];
   __shared__ int carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -573,20 +579,83 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
     asm volatile("prefetch.tensormap [%0];" ::"l"(&kv_map) : "memory");
   }
   __syncthreads();
-  // PDL: the plan grid's sp / po / NaN-initialised slots are visible after this wait; the
-  // combine grid may be launched now (it waits for this grid's completion in turn)
+  // PDL: whatever the preceding grid wrote (the plan's sp / po, or the caller's q, ctx,
+  // pool) is visible after this wait; the combine grid may be launched now (it waits for
+  // this grid's completion in turn)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
+  const int* sp_ = p.sp;
+  const int* po_ = p.po;
+  if (p.local_plan) {
+    // the schedule, computed by every CTA: sp = stage prefix, po = piece prefix (the plan
+    // kernel's two scans), in shared memory after the barriers
+    int* s_sp = reinterpret_cast<int*>(done_cnt + 8);
+    int* s_po = s_sp + (a.B + 1);
+    int* s_ws = s_po + (a.B + 1);  // warp sums [NW] + carry
+    auto cta_scan = [&](int v) -> int {  // exclusive scan over the CTA, + running carry
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_ws[warp] = x;
+      __syncthreads();
+      int before = s_ws[NW];
+      for (int w = 0; w < warp; ++w) before += s_ws[w];
+      int total = 0;
+      for (int w = 0; w < NW; ++w) total += s_ws[w];
+      __syncthreads();
+      if (tid == 0) s_ws[NW] += total;
+      __syncthreads();
+      return before + x - v;
+    };
+    if (tid == 0) s_ws[NW] = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < a.B; b0 += NW * 32) {
+      const int bb = b0 + tid;
+      const int n = bb < a.B ? (max(a.ctx[bb], 0) + kMmaStage - 1) / kMmaStage : 0;
+      const int e = cta_scan(n);
+      if (bb < a.B) s_sp[bb] = e;
+    }
+    if (tid == 0) {
+      s_sp[a.B] = s_ws[NW];
+      s_ws[NW] = 0;
+    }
+    __syncthreads();
+    const int64_t S0 = s_sp[a.B];
+    for (int b0 = 0; b0 < a.B; b0 += NW * 32) {
+      const int bb = b0 + tid;
+      int pieces = 0;
+      if (bb < a.B && S0 > 0) {
+        const int first = s_sp[bb], last = s_sp[bb + 1] - 1;
+        if (last >= first)
+          pieces = stage_owner(last, S0, gridDim.x) - stage_owner(first, S0, gridDim.x) + 1;
+      }
+      const int e = cta_scan(pieces);
+      if (bb < a.B) s_po[bb] = e;
+    }
+    if (tid == 0) s_po[a.B] = s_ws[NW];
+    __syncthreads();
+    if (blockIdx.x == 0)
+      for (int i = tid; i <= a.B; i += NW * 32) {
+        p.sp_out[i] = s_sp[i];
+        p.po_out[i] = s_po[i];
+      }
+    sp_ = s_sp;
+    po_ = s_po;
+  }
+
   const int G = a.n_q / a.n_kv;
-  const int64_t S = p.sp[a.B];
+  const int64_t S = sp_[a.B];
   const int g_begin = S ? (int)((int64_t)blockIdx.x * S / gridDim.x) : 0;
   const int g_end = S ? (int)((int64_t)(blockIdx.x + 1) * S / gridDim.x) : 0;
   auto seq_of = [&](int g) {  // sequence holding global stage g (binary search on sp)
     int lo = 0, hi = a.B - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (p.sp[mid] <= g) lo = mid;
+      if (sp_[mid] <= g) lo = mid;
       else hi = mid - 1;
     }
     return lo;
@@ -594,8 +663,8 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
   // producer cursor: global stage l_g of sequence l_b
   int l_g = g_begin, l_b = g_begin < g_end ? seq_of(g_begin) : 0;
   auto issue = [&](int buf) {  // one thread: both 8-token halves of the cursor's stage
-    while (p.sp[l_b + 1] <= l_g) ++l_b;
-    const int tok0 = (l_g - p.sp[l_b]) * kMmaStage;
+    while (sp_[l_b + 1] <= l_g) ++l_b;
+    const int tok0 = (l_g - sp_[l_b]) * kMmaStage;
     const int ntok = min(kMmaStage, a.ctx[l_b] - tok0);
     const int row = a.rows ? a.rows[l_b] : l_b;
     const int halves = ntok > 8 ? 2 : 1;
@@ -634,9 +703,9 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
   uint32_t phase = 0;
   int b = g_begin < g_end ? seq_of(g_begin) : 0;
   for (int g = g_begin; g < g_end;) {
-    while (p.sp[b + 1] <= g) ++b;  // skip sequences without stages
-    const int seg_end = min(g_end, p.sp[b + 1]);
-    const int st0 = g - p.sp[b];     // first stage of this segment inside sequence b
+    while (sp_[b + 1] <= g) ++b;  // skip sequences without stages
+    const int seg_end = min(g_end, sp_[b + 1]);
+    const int st0 = g - sp_[b];     // first stage of this segment inside sequence b
     const int nst = seg_end - g;
     // Q^T B-fragments: n = head g4 of the group (zero beyond G), k = dims
     uint32_t qb[KT][2];
@@ -741,7 +810,7 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
       }
       const int hA = 2 * q4, hB = hA + 1;
-      if (p.W == 1 && p.po[b + 1] - p.po[b] == 1) {
+      if (p.W == 1 && po_[b + 1] - po_[b] == 1) {
         // the whole sequence was this CTA's: normalise and write the bf16 output here
         // (the combine skips it); no partial round trip through global memory
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + ((int64_t)b * a.n_q + h * G) * D;
@@ -761,7 +830,7 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
         continue;
       }
       // partial piece of (sequence b, this CTA); slots are [piece][q head][warp of head]
-      const int piece = p.po[b] + blockIdx.x - stage_owner(p.sp[b], S, gridDim.x);
+      const int piece = po_[b] + blockIdx.x - stage_owner(sp_[b], S, gridDim.x);
       const int64_t base = ((int64_t)piece * a.n_q + h * G) * p.W + sub;
       if (hA < G) {
         const int64_t pi = base + (int64_t)hA * p.W;
@@ -796,7 +865,8 @@ paged_attn_mma_kernel(const __grid_constant__ CUtensorMap kv_map, AttnLaunch a, 
 // (sequence, q head), D/32 dims per lane, 8 warps per block
 template <int D>
 __global__ void __launch_bounds__(256) paged_attn_combine_sk(const float* ws_acc, const float* ws_ml,
-                                                             const int* po, int n_q, int W, int64_t n_bh,
+                                                             const int* sp, const int* po, int B,
+                                                             int grid, int n_q, int W, int64_t n_bh,
                                                              void* out) {
   constexpr int DL = D / 32;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the decode grid has completed
@@ -807,9 +877,17 @@ __global__ void __launch_bounds__(256) paged_attn_combine_sk(const float* ws_acc
   const int p0 = po[b], p1 = po[b + 1];
   if (W == 1 && p1 - p0 == 1) return;  // written by the decode kernel itself
   const int n = (p1 - p0) * W;  // partial slots of this (b, hq): pc-major, w-minor
+  // piece j of sequence b came from CTA owner(sp[b]) + j; a CTA whose stage range is empty
+  // (more CTAs than stages) wrote nothing, so its slots are skipped
+  const int64_t S = sp[B];
+  const int c0 = stage_owner(sp[b], S, grid);
+  auto written = [&](int j) {
+    const int64_t c = c0 + j;
+    return c * S / grid != (c + 1) * S / grid;
+  };
   float M = -INFINITY;
-  for (int i = lane; i < n; i += 32)  // fmaxf ignores the NaN of unwritten slots
-    M = fmaxf(M, ws_ml[2 * (((int64_t)(p0 + i / W) * n_q + hq) * W + i % W)]);
+  for (int i = lane; i < n; i += 32)
+    if (written(i / W)) M = fmaxf(M, ws_ml[2 * (((int64_t)(p0 + i / W) * n_q + hq) * W + i % W)]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   float L = 0.f, o_[DL];
@@ -817,9 +895,10 @@ __global__ void __launch_bounds__(256) paged_attn_combine_sk(const float* ws_acc
   for (int i = 0; i < DL; ++i) o_[i] = 0.f;
   if (M != -INFINITY) {
     for (int i = 0; i < n; ++i) {
+      if (!written(i / W)) continue;
       const int64_t pi = ((int64_t)(p0 + i / W) * n_q + hq) * W + i % W;
       const float mp = ws_ml[2 * pi];
-      if (!(mp > -INFINITY)) continue;  // -inf (no tokens) or NaN (slot not written)
+      if (!(mp > -INFINITY)) continue;  // -inf: no tokens
       const float wt = exp2f(mp - M);
       L += ws_ml[2 * pi + 1] * wt;
 #pragma unroll
@@ -936,6 +1015,11 @@ EncodeTiled encode_tiled() {
   return fn;
 }
 
+bool local_plan_ok() {
+  static const bool off = std::getenv("PL_ATTN_PLAN_KERNEL") != nullptr;  // A/B switch
+  return !off;
+}
+
 bool use_pdl() {
   static const bool off = std::getenv("PL_ATTN_NO_PDL") != nullptr;  // A/B switch
   return !off;
@@ -961,7 +1045,11 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
   p.box_bytes = (int)(8 * cell);
   const int64_t stage_bytes = 2 * p.box_bytes;
   p.n_stage = (int)std::max<int64_t>(2, std::min<int64_t>(4, (220 * 1024 - 2048) / stage_bytes));
-  const size_t smem = (size_t)(p.n_stage * stage_bytes) + 1024 /*align*/ + 128;
+  // the schedule scan runs inside the decode kernel when sp / po fit next to the ring
+  const size_t plan_smem = 8 * ((size_t)a.B + 1) + 4 * (NW + 1) + 16;
+  size_t smem = (size_t)(p.n_stage * stage_bytes) + 1024 /*align*/ + 128;
+  p.local_plan = local_plan_ok() && smem + plan_smem <= 227 * 1024 ? 1 : 0;
+  if (p.local_plan) smem += plan_smem;
   p.W = NW / a.n_kv;
   // stream-K: the grid splits the batch's 16-token stages evenly (ragged contexts
   // balance too); the plan kernel turns ctx into the stage / piece prefix sums
@@ -973,6 +1061,8 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
   int* po = sp + (a.B + 1);
   p.sp = sp;
   p.po = po;
+  p.sp_out = sp;
+  p.po_out = po;
 
   // tensor map: {64 elems, token in block (s), 128-B chunk of the cell, slot}
   CUtensorMap map;
@@ -991,9 +1081,11 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
   auto kern = paged_attn_mma_kernel<D, NW>;
   PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   KernelTimer timer("paged_attn", st);
-  attn_plan_kernel<<<1, 1024, 0, st>>>(a.ctx, a.B, grid, sp, po, ws + np * D, (int64_t)np);
-  note_launch();
-  PL_CUDA(cudaGetLastError());
+  if (!p.local_plan) {
+    attn_plan_kernel<<<1, 1024, 0, st>>>(a.ctx, a.B, grid, sp, po, ws + np * D, (int64_t)np);
+    note_launch();
+    PL_CUDA(cudaGetLastError());
+  }
   // plan -> decode -> combine with programmatic dependent launch: each grid is launched
   // while its predecessor runs and waits for it on the device (griddepcontrol), so the
   // two small launches no longer add their launch latency to every layer
@@ -1015,7 +1107,8 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
   cfg2.blockDim = dim3(256);
   cfg2.dynamicSmemBytes = 0;
   PL_CUDA(cudaLaunchKernelEx(&cfg2, paged_attn_combine_sk<D>, (const float*)ws,
-                             (const float*)(ws + np * D), (const int*)po, a.n_q, p.W, n_bh, a.out));
+                             (const float*)(ws + np * D), (const int*)sp, (const int*)po, a.B,
+                             grid, a.n_q, p.W, n_bh, a.out));
   note_launch();
 }
 }  // namespace
