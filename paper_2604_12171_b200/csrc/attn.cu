@@ -915,7 +915,10 @@ namespace {
 // different streams (e.g. two stages' decode) must not share partials.  (A variant that
 // merged the partials inside the decode kernel -- last warp per (sequence, kv head),
 // fence + atomic count per item -- measured 40 % slower than this separate combine
-// launch at the bench shape, so the combine stays a kernel.)
+// launch at the bench shape, so the combine stays a kernel.  Retried with one merge per
+// split sequence by the last CTA to finish it (CTA barrier + fence + one atomic per
+// split segment, no combine launch): 332.5 vs 327.6 us/layer (8B shape) and 350.8 vs
+// 339.2 (70B) -- the merges lengthen the grid's tail more than the launch costs.)
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, std::pair<float*, size_t>> g_ws;
 float* workspace(size_t bytes, cudaStream_t st) {
