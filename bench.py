@@ -357,10 +357,12 @@ def main() -> None:
         resize = guarded("resize", lambda: measure_resize(rig, stream, torch, wl))
 
     # ---- C5: dirty-rate x block-size sweep of one patch round (configs[4], 1 GPU)
-    sweep = None
+    sweep = pairs = None
     if not args.skip_sweep and rank == 0:
         from paper_2604_12171_b200.perf import c5_sweep
         sweep = guarded("c5_sweep", lambda: c5_sweep(dev))
+        from paper_2604_12171_b200.perf import c5_pairs
+        pairs = guarded("c5_pairs", lambda: c5_pairs(dev))
 
     # ---- e2e: KV arrives from pinned host memory every step, result read back
     if ring is not None:
@@ -395,6 +397,7 @@ def main() -> None:
         "resize": resize,
         "weight_stage": wstage,
         "c5_sweep": sweep,
+        "c5_pairs": pairs,
         "c3_live_resize": c3,
     }
     print(json.dumps(line), flush=True)

@@ -528,6 +528,53 @@ def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16,
     return out
 
 
+def c5_pairs(device: int = 0, pairs=(1, 2, 4, 7), batch: int = 32, ctx: int = 2048,
+             rounds: int = 3) -> list[dict]:
+    """BASELINE configs[4]'s concurrent-pairs axis at one GPU: P distinct (src, dst) pairs,
+    each with its own stores and its own low-priority patch stream, push their bulk round
+    at the same time (one host thread enqueues all P, then the device runs them
+    concurrently).  All pairs share one GPU's HBM here, so the aggregate should hold at
+    the single-pair HBM rate whatever P is -- i.e. the engine adds no serialisation;
+    across GPUs each distinct-source pair would get its own NVLink."""
+    import torch
+
+    wl = Workload(batch=batch, ctx=ctx)
+    lo, _ = torch.cuda.Stream.priority_range()
+    out = []
+    for P in pairs:
+        rigs, streams = [], []
+        for _ in range(P):
+            rig = PatchRig(wl, device=device)
+            rig.fill()
+            st = torch.cuda.Stream(device=device, priority=lo)
+            rig.patch.set_stream(st.cuda_stream)
+            rigs.append(rig)
+            streams.append(st)
+        for rig in rigs:                       # cold round: destination chains exist after it
+            rig.bulk_round()
+        torch.cuda.synchronize(device)
+        times = []
+        for _ in range(rounds):
+            for rig in rigs:
+                rig.patch.seed()
+            torch.cuda.synchronize(device)
+            t0 = time.perf_counter()
+            for rig in rigs:
+                rig.patch.push(rig.dst, rig.registry.rank())
+            torch.cuda.synchronize(device)
+            times.append(time.perf_counter() - t0)
+        t = float(np.median(times))
+        payload = P * wl.payload_bytes
+        out.append({"pairs": P, "payload_bytes": payload, "ms": round(t * 1e3, 3),
+                    "aggregate_gbs": round(payload / t / 1e9, 1),
+                    "per_pair_gbs": round(payload / P / t / 1e9, 1)})
+        for rig in rigs:
+            rig.destroy()
+        del rigs, streams
+        torch.cuda.synchronize(device)
+    return out
+
+
 def read_peaks(path) -> dict:
     import json
     try:
