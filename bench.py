@@ -221,12 +221,15 @@ def profile_traffic(kernel: str, n_q: int | None = None, wl=None):
 
 
 def config_of(wl, world: int) -> dict:
-    return {"workload": wl.name, "model_shape": "llama-3-8b (32L, 32q/8kv x 128, bf16)",
+    name = wl.name if (wl.batch, wl.ctx) == (256, 2048) else \
+        f"llama3-8b PP2->4: one migrating pair (layers 9-16), B={wl.batch}, ctx={wl.ctx}"
+    return {"workload": name, "model_shape": "llama-3-8b (32L, 32q/8kv x 128, bf16)",
             "pp_change": "2->4", "migrating_layers": "9-16 (groups 2,3)",
             "stacking_k": wl.k, "tokens_per_block": wl.s, "batch": wl.batch, "ctx": wl.ctx,
             "kv_bytes_per_token_layer": wl.cell_bytes,
             "bytes_per_step": wl.payload_bytes,
-            "l2": "inputs (>17 GB per step) exceed the 126 MB L2; no flush needed",
+            "l2": f"inputs ({wl.payload_bytes / 1e9:.1f} GB per step) exceed the 126 MB L2; "
+                  "no flush needed",
             "parallelism": (f"ring of {world} cross-process pairs (rank r -> r+1, one per GPU)"
                             if world > 1 else "1 pair on one GPU")}
 
