@@ -621,6 +621,7 @@ int pl_paged_attn_decode(pl_store* st, int group, int layer, const void* q, void
     a.q = q;
     a.out = out;
     a.n_slots = std::max<int64_t>(s->capacity(), 1);
+    a.chunk_bytes = s->chunk_bytes;
     pl::launch_paged_attn(a, cs);
   });
 }

@@ -212,8 +212,15 @@ paged_attn_kernel(AttnLaunch a, AttnPlan p, float* ws_acc, float* ws_ml) {
     const int32_t slot = a.table[(int64_t)row * a.table_stride + tok0 / a.s];
     const uint8_t* src = a.pool + (int64_t)slot * a.unit_bytes + a.fp_bytes +
                          ((int64_t)a.layer * a.s + tok0 % a.s) * cell;
-    mbar_expect_tx(&full[b], (uint32_t)(ntok * cell));
-    bulk_g2s(smem + b * stage_bytes, src, (uint32_t)(ntok * cell), &full[b]);
+    const uint32_t len = (uint32_t)(ntok * cell);
+    mbar_expect_tx(&full[b], len);
+    uint32_t first = len;
+    if (a.chunk_bytes) {  // split at a chunk boundary (see AttnLaunch::chunk_bytes)
+      const int64_t off = src - a.pool, edge = (off / a.chunk_bytes + 1) * a.chunk_bytes;
+      if (off + len > edge) first = (uint32_t)(edge - off);
+    }
+    bulk_g2s(smem + b * stage_bytes, src, first, &full[b]);
+    if (first < len) bulk_g2s(smem + b * stage_bytes + first, src + first, len - first, &full[b]);
   };
   l_norm();
   for (int i = 0; i < p.n_stage && l_item < p.items; ++i) {

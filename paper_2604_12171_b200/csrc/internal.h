@@ -607,6 +607,10 @@ struct AttnLaunch {
   const int32_t* ctx; int B, n_q, n_kv, D; float scale; int max_ctx;
   const void* q; void* out;
   int64_t n_slots;  // pool slots addressable through `pool` (TMA tensor-map extent)
+  // the pool's physical chunk size (0: one allocation).  Units are not chunk-aligned, so a
+  // bulk copy is split at chunk boundaries: each cp.async.bulk then stays inside one
+  // mapped allocation (contiguous VA either way; compute-sanitizer checks per allocation)
+  int64_t chunk_bytes;
 };
 void launch_paged_attn(const AttnLaunch& a, cudaStream_t st);
 
