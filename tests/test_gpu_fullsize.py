@@ -112,3 +112,66 @@ def test_fullsize_configs2_live_resize():
     assert out["checks"] == ["relocation", "patched", "drop+grow"]
     assert out["phase2_shrink_stats"]["relocated_blocks"] > 13_000
     assert out["bulk_patch"]["payload_bytes"] > 39e9
+
+
+def test_max_size_pool_8b_pp8():
+    """Maximum size: one Llama-3-8B PP8 stage at the reference budget, max_blocks = 611,320
+    blocks of 16 tokens x k = 4 layers x 4096 B (160 GB of KV in one pool, SURVEY §8 sizes).
+    Fill every block through K1, then: one more token overflows atomically; sampled
+    fingerprints and cells are exact; freeing half the requests and shrinking to half the
+    capacity relocates the live blocks above the line (K6) without changing a byte."""
+    import gc
+    import random
+
+    import torch
+
+    from paper_2604_12171_b200.cluster import GpuSpec, ModelSpec, max_blocks
+    from paper_2604_12171_b200.events import stable_hash
+    from paper_2604_12171_b200.kvstore import KvOverflow, KvStore, RequestRegistry
+    from paper_2604_12171_b200.perf import append_batch, engine_payloads, rid
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    gran = 16 * 4096 * 4
+    gpu = GpuSpec(1, 180 * 10 ** 9 // gran * gran, 8e12, 1e-6, 1e-6, gran)
+    cap = max_blocks(gpu, 4, ModelSpec(32, 436_000_000, 4096, 4), 0.9)
+    assert 600_000 < cap < 620_000
+    if torch.cuda.mem_get_info()[0] < cap * (16 * 4 * 4096 + 128) + (4 << 30):
+        pytest.skip("needs ~165 GB of free HBM")
+    reg = RequestRegistry()
+    st = KvStore(1, 4, 16, cap, (0,), num_groups=8, cell_bytes=4096, registry=reg)
+    tokens = cap * 16
+    n_req = -(-tokens // 2048)
+    lens = [2048] * (n_req - 1) + [tokens - 2048 * (n_req - 1)]
+    hs = [reg.handle(rid(i)) for i in range(n_req)]
+    for c0 in range(0, n_req, 512):
+        sl = range(c0, min(n_req, c0 + 512))
+        append_batch(st, [hs[i] for i in sl], [0] * len(sl), [lens[i] for i in sl],
+                     [stable_hash(rid(i), 0) for i in sl])
+    st.sync()
+    assert st.used_blocks == cap and st.free_blocks == 0
+    with pytest.raises(KvOverflow):
+        st.append(rid(0), 0, 1, [1])
+    assert st.used_blocks == cap and st.tables[rid(0)].written[0] == 2048
+
+    rng = random.Random(5)
+    keep = [i for i in range(n_req) if i % 2 == 1]
+    samples = []
+    for _ in range(48):
+        i = rng.choice(keep)
+        pos, j = rng.randrange(lens[i]), rng.randrange(4)
+        fp = int(engine_payloads(stable_hash(rid(i), 0), pos + 1)[pos])
+        assert st.read_checksum(rid(i), 0, pos) == fp
+        cell = st.read_cell(rid(i), 0, pos, j)
+        assert cell == oracle.expand_cell(fp, j, 4096)
+        samples.append((i, pos, j, fp, cell))
+    st.free_requests([rid(i) for i in range(n_req) if i % 2 == 0])
+    live = st.used_blocks
+    st.compact()
+    st.resize(cap // 2 + 64)
+    st.sync()
+    assert st.used_blocks == live and st.last_resize_stats()["relocated_blocks"] > 100_000
+    for i, pos, j, fp, cell in samples:
+        assert st.read_checksum(rid(i), 0, pos) == fp
+        assert st.read_cell(rid(i), 0, pos, j) == cell
+    st.close()
