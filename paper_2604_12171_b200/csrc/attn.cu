@@ -925,7 +925,10 @@ namespace {
 // launch at the bench shape, so the combine stays a kernel.  Retried with one merge per
 // split sequence by the last CTA to finish it (CTA barrier + fence + one atomic per
 // split segment, no combine launch): 332.5 vs 327.6 us/layer (8B shape) and 350.8 vs
-// 339.2 (70B) -- the merges lengthen the grid's tail more than the launch costs.)
+// 339.2 (70B) -- the merges lengthen the grid's tail more than the launch costs.  A
+// combine over CTA boundaries only (one block per boundary, its warps looping over the
+// q heads of the cut sequence) was slower again: 337.7 vs 332.3 us and 353.5 vs 338.6 --
+// one warp per (sequence, head) keeps the dependent partial loads in parallel.)
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, std::pair<float*, size_t>> g_ws;
 float* workspace(size_t bytes, cudaStream_t st) {
