@@ -508,6 +508,10 @@ def measure_weight_stage(rig, stream, torch, wl, dev) -> dict:
     for l in host:
         host[l]["w"].fill_(l)
     st = LayerWeightStager(dev, host)
+    st.stage_layers(range(n_layers))   # warm-up: device buffers allocated once
+    st.wait()
+    st.evict_layers(range(n_layers))
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     st.stage_layers(range(n_layers))
     st.wait()
