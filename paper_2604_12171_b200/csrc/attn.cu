@@ -480,7 +480,7 @@ struct MmaPlan {
   int W;            // warps per kv head
   int nchunks;      // cell / 128
   int box_bytes;    // 8 tokens x cell
-  // stream-K schedule (attn_plan_kernel): sp[b] = first global stage of sequence b
+  // stream-K schedule (in-kernel scan, or attn_plan_kernel): sp[b] = first global stage of sequence b
   // (stages of 16 tokens, sequences in batch order, sp[B] = S), po[b] = first partial
   // piece of b; CTA c owns global stages [c*S/grid, (c+1)*S/grid)
   const int* sp;
@@ -1065,7 +1065,8 @@ void launch_mma(const AttnLaunch& a, cudaStream_t st) {
   if (p.local_plan) smem += plan_smem;
   p.W = NW / a.n_kv;
   // stream-K: the grid splits the batch's 16-token stages evenly (ragged contexts
-  // balance too); the plan kernel turns ctx into the stage / piece prefix sums
+  // balance too); the decode kernel's prologue (local_plan) or, for batches too large
+  // for shared memory, the plan kernel turns ctx into the stage / piece prefix sums
   const int grid = sms;
   const size_t n_pieces = (size_t)a.B + grid;              // >= pieces actually written
   const size_t np = n_pieces * a.n_q * p.W;                 // partial slots
