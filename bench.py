@@ -594,7 +594,9 @@ def measure_e2e_api(rig, stream, torch, wl, K, world) -> dict:
             "d2h_bytes_per_step": 8, "ms_per_step": round(sec / K * 1e3, 3),
             "path": "host payload fingerprints -> pl_store_append_batch_payloads (K1 expand + "
                     "mark) -> pl_patch_push (K3 + fused K4/K5) -> D2H drained count "
-                    "(pipelined: step i+1 is prepared on the host while step i runs)"}
+                    "(pipelined: step i+1 is prepared on the host while step i runs)"
+                    + ("; N > 1: every rank runs its own stage pair (the cross-process ring "
+                       "round is `value`)" if world > 1 else "")}
 
 
 def measure_e2e(rig, stream, torch, wl, K, world) -> dict:
