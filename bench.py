@@ -271,6 +271,11 @@ def main() -> None:
 
     stream = torch.cuda.Stream(device=dev)
     rig = PatchRig(wl, device=dev)
+    # the e2e requests get their handles now, in the same order on every rank: across a
+    # cross-process pair the rows carry the sender's handles and the receiver frees by its
+    # own, so both registries must agree (later rank-0-only legs register other names)
+    for i in range(wl.batch):
+        rig.registry.handle(f"api{i:04d}")
     rig.use_stream(stream.cuda_stream)
     rig.fill()
     # the host block manager's mirror is millions of small objects: collect once and freeze
@@ -368,11 +373,12 @@ def main() -> None:
         pairs = guarded("c5_pairs", lambda: c5_pairs(dev))
 
     # ---- e2e: KV arrives from pinned host memory every step, result read back
-    if ring is not None:
-        ring.close()
     e2e = e2e_kv = None
     if not args.skip_e2e:
-        e2e = guarded("e2e", lambda: measure_e2e_api(rig, stream, torch, wl, K, world))
+        e2e = guarded("e2e", lambda: measure_e2e_api(rig, stream, torch, wl, K, world, ring))
+    if ring is not None:
+        ring.close()
+    if not args.skip_e2e:
         # a heavier variant: the real 17 GB of KV bytes stream from pinned host memory
         e2e_kv = guarded("e2e_real_kv", lambda: measure_e2e(rig, stream, torch, wl, K, world))
     rig.destroy()
@@ -537,7 +543,7 @@ def measure_weight_stage(rig, stream, torch, wl, dev) -> dict:
                     "stream (copy engine); decode runs on its own stream"}
 
 
-def measure_e2e_api(rig, stream, torch, wl, K, world) -> dict:
+def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
     """The bulk round through the reference-facing call shape with host buffers: every
     step the B requests' migrating groups are appended with host payload arrays
     (KvStore.append(rid, group, n, payloads), kvstore.py:163-199, batched into one
@@ -559,23 +565,40 @@ def measure_e2e_api(rig, stream, torch, wl, K, world) -> dict:
                            for g in wl.mig_groups])
     results = torch.zeros(K + 1, dtype=torch.int64, pin_memory=True)
 
+    # N > 1: the round is the ring's cross-process one (rank r -> r + 1 over the imported
+    # peer pools), as for `value`; the receiving store is ring.dst
+    recv_store = ring.dst if ring is not None else rig.dst
+    sender = ring.tx.patch if ring is not None else rig.patch
+
     def one_step(i):
         rig.src.free_requests(names)   # the previous step's requests leave both stages
-        rig.dst.free_requests(names)
+        recv_store.free_requests(names)
         assert append_batch_payloads(rig.src, reqs, groups, counts, host, mark=True) == len(reqs)
-        keys, _ = rig.patch.push(rig.dst, rig.registry.rank())
+        if ring is None:
+            keys, _ = rig.patch.push(rig.dst, rig.registry.rank())
+        else:
+            ring.tx.begin()
+            ring.rx.serve_rows()
+            keys, _ = ring.tx.finish()
+            ring.rx.serve_ack()
         # D2H of the step's result (drained-key count), enqueued behind the push; the host
         # goes on preparing the next step while the device works (a pipelined driver)
         N.check(N.lib().pl_patch_device_drained_async(
-            rig.patch.h, C.c_void_p(results.data_ptr() + 8 * i)))
+            sender.h, C.c_void_p(results.data_ptr() + 8 * i)))
         return keys
 
     import ctypes as C
 
     from paper_2604_12171_b200 import _native as N
+    if ring is not None:
+        N.check(N.lib().pl_patch_set_active(rig.patch.h, 0))   # only the ring pair marks
     for i in range(wl.batch):   # room: the bulk requests leave both stages
+        # MigrationStream.on_request_freed (migrator.py:199-204): writes still marked for a
+        # finished request (earlier legs' decode appends) are dropped, not shipped
+        for p in {id(rig.patch): rig.patch, id(sender): sender}.values():
+            p.discard_request(f"r{i:04d}", rig.registry)
         rig.src.free_request(f"r{i:04d}")
-        rig.dst.free_request(f"r{i:04d}")
+        recv_store.free_request(f"r{i:04d}")
     one_step(K)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -588,15 +611,17 @@ def measure_e2e_api(rig, stream, torch, wl, K, world) -> dict:
     expect = wl.batch * wl.ctx * len(wl.mig_groups)
     assert keys == expect and all(int(x) == expect for x in results[:K]), results[:K]
     rig.src.free_requests(names)
-    rig.dst.free_requests(names)
+    recv_store.free_requests(names)
+    if ring is not None:
+        N.check(N.lib().pl_patch_set_active(rig.patch.h, 1))
     return {"value": round(world * K * wl.payload_bytes / sec / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": int(host.nbytes + 16 * len(reqs)),
             "d2h_bytes_per_step": 8, "ms_per_step": round(sec / K * 1e3, 3),
             "path": "host payload fingerprints -> pl_store_append_batch_payloads (K1 expand + "
                     "mark) -> pl_patch_push (K3 + fused K4/K5) -> D2H drained count "
                     "(pipelined: step i+1 is prepared on the host while step i runs)"
-                    + ("; N > 1: every rank runs its own stage pair (the cross-process ring "
-                       "round is `value`)" if world > 1 else "")}
+                    + ("; N > 1: the ring's cross-process round (rank r -> r + 1), as `value`"
+                       if ring is not None else "")}
 
 
 def measure_e2e(rig, stream, torch, wl, K, world) -> dict:
