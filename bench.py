@@ -701,7 +701,9 @@ def measure_resize(rig, stream, torch, wl) -> dict:
     on the store's reclaimer thread (vmm.cu); `reclaim_ms` is how long forcing it to
     finish took afterwards (memory back with the driver), reported beside it.  A grow
     inside the grace period re-takes the still-mapped tail (`grow_warm_ms`); a grow
-    after the reclaim maps fresh chunks from the driver (`grow_cold_ms`)."""
+    after the reclaim maps fresh chunks from the driver: the capacity is published at once
+    (`grow_cold_ms`) and the tail is mapped on the reclaimer thread
+    (`grow_cold_background_ms`: until that mapping is done)."""
     st = rig.src
     out = {}
 
@@ -744,6 +746,8 @@ def measure_resize(rig, stream, torch, wl) -> dict:
     st.resize(cap)
     st.sync()
     out["grow_cold_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    # the new tail is mapped by the reclaimer thread (lazy grow); time until it is done
+    out["grow_cold_background_ms"] = round((time.perf_counter() - t0) * 1e3 + st.prepare_wait(), 3)
     out["grow_cold_stats"] = {**st.last_resize_stats(), **vdelta(v2, st.vmm_stats())}
     out["blocks"] = {"from": cap, "to": target, "live": st.used_blocks}
     out["tokens_freed_by_drop"] = freed

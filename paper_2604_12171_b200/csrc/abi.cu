@@ -170,6 +170,7 @@ int pl_store_get_info(pl_store* st, pl_store_info* o) {
     o->cell_bytes = s->cell_bytes;
     o->unit_bytes = s->unit_bytes;
     o->fp_header_bytes = s->fp_bytes;
+    s->settle();
     o->mapped_bytes = s->mapped_bytes();
     o->table_max_chain = s->max_chain;
     o->table_max_reqs = s->max_reqs;
@@ -417,7 +418,8 @@ int pl_store_last_resize_stats(pl_store* st, int64_t* out4) {
 int pl_store_vmm_stats(pl_store* st, int64_t* out4) {
   return guard([&] {
     pl::Store* s = st->s;
-    int64_t tail = 0, cache = 0, created = 0;
+    s->reclaimer->wait_prepared();  // background tail mappings counted once they are done
+    int64_t tail = 0, cache = 0, created = s->reclaimer->bg_created.load();
     for (auto& a : s->arenas) {
       tail += (int64_t)a.last_tail_reused + (int64_t)a.last_prepared;  // mapped ahead
       cache += (int64_t)a.last_cache_reused;
@@ -673,6 +675,7 @@ int pl_store_export_group(pl_store* st, int group, int* fds_out, int cap, int* n
     if (group < 0 || group >= s->n_model_groups || !s->materialised[group])
       pl::fail(PL_E_INVALID, "group has no pool to export");
     PL_CUDA(cudaSetDevice(s->device));
+    s->arenas[group].adopt_prepared();  // a pending tail mapping belongs to the pool
     const auto& chunks = s->arenas[group].chunks;
     *n_out = (int)chunks.size();
     *chunk_bytes_out = (int64_t)s->arenas[group].chunk_bytes;

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <cstdint>
@@ -65,6 +66,7 @@ struct Reclaimer {
   // true + still-mapped range if the job had not started; false after waiting for it
   bool cancel(uint64_t id, CUdeviceptr* va, std::vector<CUmemGenericAllocationHandle>* hs);
   std::vector<CUmemGenericAllocationHandle> take(size_t n);  // unmapped cached chunks
+  std::atomic<int64_t> bg_created{0};  // chunks created by prepare jobs (helper thread)
   double wait_all(bool release_cache);  // finish every job (and release the cache)
   int64_t pending();                    // physical bytes not yet back with the driver
   // planned grow: map n chunks at [va, va + n*chunk) on the helper thread (cached chunks
@@ -120,11 +122,11 @@ struct Arena {
   void trim(size_t bytes, cudaStream_t st);   // retire chunks wholly beyond `bytes`
   void release(cudaStream_t st);              // retire everything + the reservation
   void grant_peer(int dev);
-  void prepare(size_t bytes);                 // map the tail for a planned grow, async
+  bool prepare(size_t bytes);  // map the tail for a planned grow, async; false: not possible
+  void adopt_prepared();       // take a finished (or wait for a running) tail mapping
 
  private:
   void reclaim_tail();
-  void adopt_prepared();
 };
 size_t vmm_granularity(int device);
 // VMM IPC: export a pool chunk as a POSIX fd / import one, map it into a reservation
@@ -373,6 +375,12 @@ struct Store {
   void stage_consumed(uint64_t seq) noexcept;  // consumers of span seq enqueued on stream
   cudaEvent_t ring_event();
   void materialise(int g);
+  // lazy grows: a grow publishes the capacity at once and maps the pools' new tails on the
+  // reclaimer thread; the first allocation (or relocation target) at or past
+  // `mapped_slots` adopts the mapping (waiting for it if it is still running)
+  int64_t mapped_slots = 0;
+  void ensure_slots(int64_t n_slots);
+  void settle();  // adopt every pending tail mapping (diagnostics, exports)
   void dematerialise(int g);
   uint64_t group_base(int g) const { return (uint64_t)arenas[g].va; }
   int64_t mapped_bytes() const;

@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <limits>
+
 #include "internal.h"
 
 namespace pl {
@@ -20,6 +22,11 @@ namespace {
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 }  // namespace
+
+static bool lazy_grow() {
+  static const bool off = std::getenv("PL_EAGER_GROW") != nullptr;  // A/B switch
+  return !off;
+}
 
 Store::Store(int device_, int gpu_id_, int k_, int s_, int64_t cell_bytes_, int n_model_groups_,
              int64_t capacity, const int32_t* groups, int n_groups, int64_t chunk_bytes_)
@@ -158,9 +165,29 @@ int64_t Store::new_block() {
   return id;
 }
 
+void Store::ensure_slots(int64_t n_slots) {
+  if (n_slots <= mapped_slots) return;
+  int64_t lo = std::numeric_limits<int64_t>::max();
+  bool any = false;
+  for (int g = 0; g < n_model_groups; ++g)
+    if (materialised[g]) {
+      const uint64_t va = arenas[g].va;
+      arenas[g].ensure((size_t)n_slots * (size_t)unit_bytes);  // adopts a pending tail first
+      if (va != arenas[g].va) refresh_bases();
+      lo = std::min<int64_t>(lo, (int64_t)(arenas[g].mapped_bytes() / (size_t)unit_bytes));
+      any = true;
+    }
+  mapped_slots = any ? lo : 0;
+}
+void Store::settle() {
+  for (int g = 0; g < n_model_groups; ++g)
+    if (materialised[g]) arenas[g].adopt_prepared();
+}
+
 BlockRec& Store::alloc_block(int32_t req) {
   if (free_ids.empty()) fail(PL_E_KV_OVERFLOW, "no free block");
   BlockRec& b = by_id.at(free_ids.pop_min());
+  if (b.slot >= mapped_slots) ensure_slots((int64_t)b.slot + 1);
   b.owner = req;
   ++used;
   return b;
@@ -512,12 +539,14 @@ void Store::materialise(int g) {
   PL_CUDA(cudaSetDevice(device));
   arenas[g].ensure(want);
   materialised[g] = 1;
+  mapped_slots = 0;  // recomputed at the next allocation past it
   if (!was || before != arenas[g].va) refresh_bases();
 }
 void Store::dematerialise(int g) {
   if (!materialised[g]) return;
   arenas[g].release(stream);  // unmapped by the reclaimer once the stream passes this point
   materialised[g] = 0;
+  mapped_slots = 0;
   refresh_bases();
 }
 int64_t Store::mapped_bytes() const {
@@ -747,18 +776,24 @@ void Store::resize(int64_t new_cap) {
     const int64_t before = mapped_bytes();
     for (int64_t i = old_cap; i < new_cap; ++i) new_block();
     ensure_owner(new_cap);
+    int64_t planned = 0;
     for (int g = 0; g < n_model_groups; ++g)
       if (materialised[g]) {
+        const size_t want = (size_t)new_cap * unit_bytes;
+        planned += (int64_t)(std::max(want, arenas[g].mapped_bytes()) - arenas[g].mapped_bytes());
+        if (lazy_grow() && arenas[g].prepare(want)) continue;  // mapped in the background
         const uint64_t va = arenas[g].va;
-        arenas[g].ensure((size_t)new_cap * unit_bytes);
+        arenas[g].ensure(want);
         if (va != arenas[g].va) refresh_bases();
       }
-    last_resize[2] = mapped_bytes() - before;
+    // bytes mapped now plus bytes being mapped by the reclaimer thread for this grow
+    last_resize[2] = std::max<int64_t>(mapped_bytes() - before, planned);
     return;
   }
   if (used > new_cap)
     fail(PL_E_CAPACITY_BELOW_LIVE, "gpu " + std::to_string(gpu_id) + ": " + std::to_string(used) +
                                        " live blocks > target " + std::to_string(new_cap));
+  ensure_slots(new_cap);   // K6 may move units to any slot below new_cap
   bool live_in_tail = false;
   for (int64_t i = new_cap; i < old_cap && !live_in_tail; ++i)
     live_in_tail = by_id.at(blocks[i]).owner >= 0;
@@ -845,6 +880,7 @@ void Store::resize(int64_t new_cap) {
   const int64_t before = mapped_bytes();
   for (int g = 0; g < n_model_groups; ++g)
     if (materialised[g]) arenas[g].trim((size_t)std::max<int64_t>(new_cap, 1) * unit_bytes, stream);
+  mapped_slots = std::min<int64_t>(mapped_slots, new_cap);
   last_resize[3] = before - mapped_bytes();
 }
 

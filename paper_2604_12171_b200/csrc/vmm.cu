@@ -360,6 +360,7 @@ void Reclaimer::loop() {
         if (d.Create(&h, chunk_bytes, &prop, 0) != CUDA_SUCCESS) break;  // best effort
         hs.push_back(h);
         ++pr->created;
+        ++bg_created;
       }
       size_t mapped = 0;
       for (; mapped < hs.size(); ++mapped)
@@ -435,13 +436,15 @@ void Arena::adopt_prepared() {
   (void)created;  // created on the helper thread, off the critical path
 }
 
-void Arena::prepare(size_t bytes) {
+bool Arena::prepare(size_t bytes) {
   adopt_prepared();
   reclaim_tail();
   const size_t want_chunks = (bytes + chunk_bytes - 1) / chunk_bytes;
-  if (!va || want_chunks <= chunks.size() || want_chunks * chunk_bytes > va_bytes) return;
+  if (want_chunks <= chunks.size()) return true;
+  if (!va || want_chunks * chunk_bytes > va_bytes) return false;  // needs a new VA range
   prep_job = rc->submit_prepare(va + chunks.size() * chunk_bytes, want_chunks - chunks.size(),
                                 peer_devices);
+  return true;
 }
 
 void Arena::ensure(size_t bytes) {

@@ -440,6 +440,8 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040,
     src.resize(b_new)
     src.sync()
     out["grow_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    # lazy grow: the tail is mapped on the reclaimer thread; time until that is done
+    out["grow_background_ms"] = round((time.perf_counter() - t0) * 1e3 + src.prepare_wait(), 3)
     if check:
         assert src.capacity_blocks == b_new
         verify(src, (0, 1, 2), "drop+grow")
