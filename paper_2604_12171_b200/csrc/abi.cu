@@ -335,6 +335,7 @@ int pl_store_read_fps(pl_store* st, int group, const int32_t* slots, int64_t n, 
     if (group < 0 || group >= s->n_model_groups || !s->materialised[group])
       pl::fail(PL_E_INVALID, "group has no pool");
     if (n <= 0) return;
+    s->use_group(group);
     s->flush();
     pl::Upload up(s);
     int a = up.add(slots, (size_t)n * 4);
@@ -354,6 +355,7 @@ int pl_store_read_checksum(pl_store* st, int32_t req, int group, int64_t token, 
     if (!t || group < 0 || group >= s->n_model_groups || token < 0 || token >= t->written[group])
       pl::fail(PL_E_UNKNOWN_SLOT, "request " + std::to_string(req) + " group " +
                                       std::to_string(group) + " token " + std::to_string(token));
+    s->use_group(group);
     const int32_t slot = s->by_id.at(t->chain[token / s->s]).slot;
     if (!s->occ_test(slot, group, (int)(token % s->s)))
       pl::fail(PL_E_UNKNOWN_SLOT, "cell never written");
@@ -372,6 +374,7 @@ int pl_store_read_cell(pl_store* st, int32_t req, int group, int64_t token, int 
     const pl::ReqTable* t = s->table(req);
     if (!t || group < 0 || group >= s->n_model_groups || token < 0 || token >= t->written[group])
       pl::fail(PL_E_UNKNOWN_SLOT, "cell out of range");
+    s->use_group(group);
     if (j < 0 || j >= s->k || nbytes > s->cell_bytes) pl::fail(PL_E_INVALID, "bad layer/size");
     const int32_t slot = s->by_id.at(t->chain[token / s->s]).slot;
     s->flush();
@@ -454,6 +457,7 @@ int pl_store_reclaim(pl_store* st, double* out_ms) {
 int pl_store_group_base(pl_store* st, int group, uint64_t* out) {
   return guard([&] {
     if (group < 0 || group >= st->s->n_model_groups) pl::fail(PL_E_INVALID, "group out of range");
+    st->s->use_group(group);  // the caller may touch the pool: it must be mapped
     *out = st->s->materialised[group] ? st->s->group_base(group) : 0;
   });
 }
@@ -603,6 +607,7 @@ int pl_paged_attn_decode(pl_store* st, int group, int layer, const void* q, void
       PL_CUDA(cudaStreamWaitEvent(cs, ev, 0));
       PL_CUDA(cudaEventDestroy(ev));
     }
+    s->use_group(group);
     pl::AttnLaunch a{};
     a.pool = reinterpret_cast<const uint8_t*>(s->group_base(group));
     a.unit_bytes = s->unit_bytes;
@@ -709,6 +714,7 @@ int pl_store_reserve_rows(pl_store* st, int64_t n_rows, const int32_t* reqs, con
   const int rc = guard([&] {
     PL_CUDA(cudaSetDevice(st->s->device));
     *items_done = st->s->reserve_rows(n_rows, reqs, groups, a, b, &status);
+    st->s->settle();  // the sender writes into these pools next: map them now
   });
   if (rc != PL_OK) return rc;
   if (status != PL_OK) pl::g_err = st->s->last_msg;

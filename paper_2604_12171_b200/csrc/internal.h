@@ -124,6 +124,7 @@ struct Arena {
   void grant_peer(int dev);
   bool prepare(size_t bytes);  // map the tail for a planned grow, async; false: not possible
   void adopt_prepared();       // take a finished (or wait for a running) tail mapping
+  void reserve_for(size_t bytes);  // VA reservation only (a fresh arena), for prepare()
 
  private:
   void reclaim_tail();
@@ -381,6 +382,13 @@ struct Store {
   int64_t mapped_slots = 0;
   void ensure_slots(int64_t n_slots);
   void settle();  // adopt every pending tail mapping (diagnostics, exports)
+  // lazily materialised groups whose pool is still being mapped; use_group() adopts one
+  // before anything reads or writes its pool
+  uint64_t pending_groups = 0;
+  void use_group(int g) {
+    if (pending_groups && g >= 0 && g < 64 && ((pending_groups >> g) & 1)) adopt_group(g);
+  }
+  void adopt_group(int g);
   void dematerialise(int g);
   uint64_t group_base(int g) const { return (uint64_t)arenas[g].va; }
   int64_t mapped_bytes() const;

@@ -89,6 +89,7 @@ void Remote::set_table(const void* ipc_handle, int64_t mr, int64_t mc) {
 
 // ---------------------------------------------------------------------------
 void Patch::drain_rows(const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells) {
+  for (int i = 0; i < G; ++i) src->use_group(groups[i]);
   if (in_flight) fail(PL_E_STATE, "a drained patch of this pair is still in flight");
   take_drained();
   *keys = drained_keys;

@@ -324,6 +324,7 @@ int64_t Patch::device_drain_compact() {
 }
 
 void Patch::drain(int64_t* keys, int64_t* cells) {
+  for (int i = 0; i < G; ++i) src->use_group(groups[i]);
   if (in_flight) fail(PL_E_STATE, "a drained patch of this pair is still in flight");
   PL_CUDA(cudaSetDevice(src->device));
   take_drained();
@@ -436,6 +437,10 @@ const int32_t* Patch::d_groups() {
 
 void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
                   int64_t n_stale) {
+  for (int i = 0; i < G; ++i) {  // lazily mapped pools are adopted before any copy
+    src->use_group(groups[i]);
+    dst->use_group(groups[i]);
+  }
   if (!in_flight) fail(PL_E_STATE, "no drained patch in flight");
   if (dst->k != src->k || dst->cell_bytes != src->cell_bytes)
     fail(PL_E_INVALID, "source and destination layouts differ");
@@ -473,6 +478,7 @@ void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t
     c.rows = d_rows;
     c.keys = d_keys;
     c.row_bytes = 16 + (int64_t)src->k * src->cell_bytes;
+    for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);  // pool mapped (lazy groups)
     launch_copy(c, dst->stream);
   }
   PL_CUDA(cudaEventRecord(ev_applied, dst->stream));
@@ -625,6 +631,7 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
     cl.cells = d_part + run_off[c];
     cl.count = d_run_cnt + c;
     cl.n_hint = run_keys[c];
+    for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);  // pool mapped (lazy groups)
     launch_copy(cl, pstream());
     ++launched;
     if (status != PL_OK) break;
@@ -643,6 +650,10 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
 }
 
 void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells) {
+  for (int i = 0; i < G; ++i) {  // lazily mapped pools are adopted before any copy
+    src->use_group(groups[i]);
+    dst->use_group(groups[i]);
+  }
   if (in_flight) fail(PL_E_STATE, "a drained patch of this pair is still in flight");
   if (dst->k != src->k || dst->cell_bytes != src->cell_bytes)
     fail(PL_E_INVALID, "source and destination layouts differ");
@@ -686,6 +697,7 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
     // every drained item was reserved (no KvOverflow): no mask needed, the copy applies all
     const uint8_t* d_apply = status == PL_OK ? nullptr : stage_mask(mask);
     PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
+    for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);  // pool mapped (lazy groups)
     launch_copy(push_launch(dst, d_apply, 0), pstream());
   }
   PL_CUDA(cudaEventRecord(ev_applied, pstream()));

@@ -171,6 +171,7 @@ void Store::ensure_slots(int64_t n_slots) {
   bool any = false;
   for (int g = 0; g < n_model_groups; ++g)
     if (materialised[g]) {
+      if (g < 64) pending_groups &= ~(1ull << g);
       const uint64_t va = arenas[g].va;
       arenas[g].ensure((size_t)n_slots * (size_t)unit_bytes);  // adopts a pending tail first
       if (va != arenas[g].va) refresh_bases();
@@ -181,7 +182,17 @@ void Store::ensure_slots(int64_t n_slots) {
 }
 void Store::settle() {
   for (int g = 0; g < n_model_groups; ++g)
-    if (materialised[g]) arenas[g].adopt_prepared();
+    if (materialised[g]) {
+      if ((pending_groups >> g) & 1) adopt_group(g);
+      else arenas[g].adopt_prepared();
+    }
+}
+void Store::adopt_group(int g) {
+  pending_groups &= ~(1ull << g);
+  arenas[g].adopt_prepared();
+  const uint64_t va = arenas[g].va;
+  arenas[g].ensure((size_t)std::max<int64_t>(capacity(), 1) * (size_t)unit_bytes);  // any rest
+  if (va != arenas[g].va) refresh_bases();
 }
 
 BlockRec& Store::alloc_block(int32_t req) {
@@ -537,6 +548,18 @@ void Store::materialise(int g) {
   const uint64_t before = arenas[g].va;
   const bool was = materialised[g];
   PL_CUDA(cudaSetDevice(device));
+  if (lazy_grow() && !was && g < 64 && arenas[g].va == 0 && arenas[g].chunks.empty()) {
+    // a new group's pool: reserve its VA now, map it on the reclaimer thread; the first
+    // use (write, copy, read, allocation) adopts it
+    arenas[g].reserve_for(want);
+    if (arenas[g].prepare(want)) {
+      materialised[g] = 1;
+      pending_groups |= 1ull << g;
+      mapped_slots = 0;
+      refresh_bases();
+      return;
+    }
+  }
   arenas[g].ensure(want);
   materialised[g] = 1;
   mapped_slots = 0;  // recomputed at the next allocation past it
@@ -546,6 +569,7 @@ void Store::dematerialise(int g) {
   if (!materialised[g]) return;
   arenas[g].release(stream);  // unmapped by the reclaimer once the stream passes this point
   materialised[g] = 0;
+  if (g < 64) pending_groups &= ~(1ull << g);
   mapped_slots = 0;
   refresh_bases();
 }
@@ -560,6 +584,8 @@ int64_t Store::mapped_bytes() const {
 void Store::launch_write(const std::vector<WriteItem>& items, int mode, const uint64_t* payloads,
                          const int64_t* positions, const void* kv_dev, int mark) {
   if (items.empty()) return;
+  if (pending_groups)
+    for (const WriteItem& it : items) use_group(it.group);
   flush();
   const int n = (int)items.size();
   std::vector<int32_t> reqs(n), groups(n);

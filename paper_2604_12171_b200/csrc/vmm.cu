@@ -436,6 +436,19 @@ void Arena::adopt_prepared() {
   (void)created;  // created on the helper thread, off the critical path
 }
 
+void Arena::reserve_for(size_t bytes) {
+  if (va || !chunks.empty()) return;
+  const size_t want_va = (bytes + chunk_bytes - 1) / chunk_bytes * chunk_bytes;
+  const size_t n = std::max<size_t>(want_va * 4, chunk_bytes);  // headroom as in ensure()
+  CUdeviceptr nva = 0;
+  CUresult rr = drv().AddressReserve(&nva, n, 0, 0, 0);
+  if (rr != CUDA_SUCCESS)
+    fail(PL_E_CUDA, "cuMemAddressReserve(" + std::to_string(n) + " B) failed with CUresult " +
+                        std::to_string((int)rr));
+  va = nva;
+  va_bytes = n;
+}
+
 bool Arena::prepare(size_t bytes) {
   adopt_prepared();
   reclaim_tail();
