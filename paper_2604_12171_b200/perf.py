@@ -399,10 +399,15 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040,
     src.resident_groups.add(5)
     src.sync()
     out["map_incoming_group_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    # the pool itself is mapped on the reclaimer thread (lazy materialisation); Phase 3
+    # starts after weight loading, by when it is done -- time it, outside the patch rounds
+    out["map_incoming_group_background_ms"] = round(
+        (time.perf_counter() - t0) * 1e3 + src.prepare_wait(), 3)
     # Phase 3: bulk + one decode round of the two leaving groups
     dst = KvStore(2, 4, 16, src.used_blocks + 256, (), num_groups=20, cell_bytes=4096,
                   device=device, registry=reg)
     dst.resident_groups |= {3, 4}
+    dst.prepare_wait()   # the destination's pools are mapped before its Phase 3, as above
     patch = NativePatch(src, (3, 4), 4)
     patch.seed()
     torch.cuda.synchronize(device)
