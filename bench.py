@@ -364,14 +364,6 @@ def main() -> None:
         # ---- resize latency: post-commit cleanup on the source (drop, shrink, regrow)
         resize = guarded("resize", lambda: measure_resize(rig, stream, torch, wl))
 
-    # ---- C5: dirty-rate x block-size sweep of one patch round (configs[4], 1 GPU)
-    sweep = pairs = None
-    if not args.skip_sweep and rank == 0:
-        from paper_2604_12171_b200.perf import c5_sweep
-        sweep = guarded("c5_sweep", lambda: c5_sweep(dev))
-        from paper_2604_12171_b200.perf import c5_pairs
-        pairs = guarded("c5_pairs", lambda: c5_pairs(dev))
-
     # ---- e2e: KV arrives from pinned host memory every step, result read back
     e2e = e2e_kv = None
     if not args.skip_e2e:
@@ -384,6 +376,16 @@ def main() -> None:
     rig.destroy()
     if ring is not None:
         ring.dst.close()
+
+    # ---- C5: dirty-rate x block-size sweep and concurrent pairs (configs[4], 1 GPU); after
+    # the e2e legs, so their store churn (dozens of pools created and released) cannot
+    # overlap the headline measurement
+    sweep = pairs = None
+    if not args.skip_sweep and rank == 0:
+        from paper_2604_12171_b200.perf import c5_sweep
+        sweep = guarded("c5_sweep", lambda: c5_sweep(dev))
+        from paper_2604_12171_b200.perf import c5_pairs
+        pairs = guarded("c5_pairs", lambda: c5_pairs(dev))
 
     if rank != 0:
         return
