@@ -601,25 +601,27 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
             p.discard_request(f"r{i:04d}", rig.registry)
         rig.src.free_request(f"r{i:04d}")
         recv_store.free_request(f"r{i:04d}")
-    one_step(K)
-    torch.cuda.synchronize()
-    # no cyclic-GC pass inside the wall-clock region (earlier legs leave many objects)
-    gc.collect()
-    gc.disable()
-    t0 = time.perf_counter()
-    for i in range(K):
-        keys = one_step(i)
-    stream.synchronize()
-    torch.cuda.synchronize()
-    sec = time.perf_counter() - t0
-    gc.enable()
+    try:
+        one_step(K)
+        torch.cuda.synchronize()
+        # no cyclic-GC pass inside the wall-clock region (earlier legs leave many objects)
+        gc.collect()
+        gc.disable()
+        t0 = time.perf_counter()
+        for i in range(K):
+            keys = one_step(i)
+        stream.synchronize()
+        torch.cuda.synchronize()
+        sec = time.perf_counter() - t0
+    finally:
+        gc.enable()
+        if ring is not None:
+            N.check(N.lib().pl_patch_set_active(rig.patch.h, 1))
     sec = allmax(sec, world)
     expect = wl.batch * wl.ctx * len(wl.mig_groups)
     assert keys == expect and all(int(x) == expect for x in results[:K]), results[:K]
     rig.src.free_requests(names)
     recv_store.free_requests(names)
-    if ring is not None:
-        N.check(N.lib().pl_patch_set_active(rig.patch.h, 1))
     return {"value": round(world * K * wl.payload_bytes / sec / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": int(host.nbytes + 16 * len(reqs)),
             "d2h_bytes_per_step": 8, "ms_per_step": round(sec / K * 1e3, 3),
@@ -685,12 +687,14 @@ def measure_e2e(rig, stream, torch, wl, K, world) -> dict:
     torch.cuda.synchronize()
     gc.collect()
     gc.disable()
-    t0 = time.perf_counter()
-    for _ in range(K):
-        keys = one_step()
-        stream.synchronize()
-    sec = time.perf_counter() - t0
-    gc.enable()
+    try:
+        t0 = time.perf_counter()
+        for _ in range(K):
+            keys = one_step()
+            stream.synchronize()
+        sec = time.perf_counter() - t0
+    finally:
+        gc.enable()
     sec = allmax(sec, world)
     assert keys == wl.batch * wl.ctx * len(wl.mig_groups)
     for n in e2e_names:

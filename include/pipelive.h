@@ -142,6 +142,22 @@ int pl_store_read_fps(pl_store* st, int group, const int32_t* slots_host, int64_
 int pl_store_read_cell(pl_store* st, int32_t req, int group, int64_t token, int layer_in_group,
                        void* out_host, int64_t nbytes);
 
+/* ---- full-size verification (test / audit path; csrc/verify.cu).  verify: every live
+ *      (block, group, offset) cell of the store -- all k layer cells equal the parity
+ *      expansion of the cell's fingerprint and, when seeds_host is given
+ *      ([n_seed_reqs][num_model_groups], ~0 = skip), the fingerprint equals the engine
+ *      payload of PipelineEngine._payloads (engine.py:252-261) for its (request, group,
+ *      position).  out4 = {cells checked, cells with a wrong byte, cells with a wrong
+ *      fingerprint, first bad cell index or -1}.
+ *      compare: for each request x group, every written position of store a and store b
+ *      (same device) holds the same fingerprint and k cells, each side resolved through its
+ *      own block table (PatchReceiver._apply / write_slots, migrator.py:115-131,
+ *      kvstore.py:201-227).  out3 = {cells compared, positions that differ, positions
+ *      missing or lengths that differ}. */
+int pl_store_verify(pl_store* st, const uint64_t* seeds_host, int64_t n_seed_reqs, int64_t* out4);
+int pl_store_compare(pl_store* a, pl_store* b, const int32_t* groups, int n_groups,
+                     const int32_t* reqs, int n_reqs, int64_t* out3);
+
 /* ---- lifecycle ops: compact (kvstore.py:247-257), resize (kvstore.py:259-282; K6 remap),
  *      drop_layer_groups (kvstore.py:284-309), free_request (kvstore.py:311-322),
  *      effective_utilization (kvstore.py:324-329) */

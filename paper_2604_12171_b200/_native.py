@@ -83,6 +83,8 @@ SIGNATURES = [
     ("pl_store_read_checksum", C.c_int, [vp, i32, C.c_int, i64, P(u64)]),
     ("pl_store_read_fps", C.c_int, [vp, C.c_int, vp, i64, vp]),
     ("pl_store_read_cell", C.c_int, [vp, i32, C.c_int, i64, C.c_int, vp, i64]),
+    ("pl_store_verify", C.c_int, [vp, vp, i64, vp]),
+    ("pl_store_compare", C.c_int, [vp, vp, vp, C.c_int, vp, C.c_int, vp]),
     ("pl_store_compact", C.c_int, [vp, P(i64)]),
     ("pl_store_resize", C.c_int, [vp, i64]),
     ("pl_store_drop_groups", C.c_int, [vp, vp, C.c_int, P(i64)]),

@@ -170,8 +170,9 @@ int pl_store_get_info(pl_store* st, pl_store_info* o) {
     o->cell_bytes = s->cell_bytes;
     o->unit_bytes = s->unit_bytes;
     o->fp_header_bytes = s->fp_bytes;
-    s->settle();
-    o->mapped_bytes = s->mapped_bytes();
+    // a read-only getter: no adoption of background mappings (that would put them back on
+    // the critical path); bytes being mapped by the reclaimer thread are counted as planned
+    o->mapped_bytes = s->planned_bytes();
     o->table_max_chain = s->max_chain;
     o->table_max_reqs = s->max_reqs;
     o->n_tables = s->n_tables;
@@ -384,6 +385,14 @@ int pl_store_read_cell(pl_store* st, int32_t req, int group, int64_t token, int 
     PL_CUDA(cudaMemcpyAsync(out, p, nbytes, cudaMemcpyDeviceToHost, s->stream));
     PL_CUDA(cudaStreamSynchronize(s->stream));
   });
+}
+
+int pl_store_verify(pl_store* st, const uint64_t* seeds_host, int64_t n_seed_reqs, int64_t* out4) {
+  return guard([&] { pl::verify_store(st->s, seeds_host, n_seed_reqs, out4); });
+}
+int pl_store_compare(pl_store* a, pl_store* b, const int32_t* groups, int n_groups,
+                     const int32_t* reqs, int n_reqs, int64_t* out3) {
+  return guard([&] { pl::compare_stores(a->s, b->s, groups, n_groups, reqs, n_reqs, out3); });
 }
 
 int pl_store_compact(pl_store* st, int64_t* out) {
@@ -680,7 +689,14 @@ int pl_store_export_group(pl_store* st, int group, int* fds_out, int cap, int* n
     if (group < 0 || group >= s->n_model_groups || !s->materialised[group])
       pl::fail(PL_E_INVALID, "group has no pool to export");
     PL_CUDA(cudaSetDevice(s->device));
-    s->arenas[group].adopt_prepared();  // a pending tail mapping belongs to the pool
+    // the exported range must cover the whole capacity: adopt a lazily materialised group
+    // (maps whatever its background job did not), a pending grow tail, and map any rest a
+    // best-effort background creation left out
+    s->use_group(group);
+    s->arenas[group].adopt_prepared();
+    const uint64_t va = s->arenas[group].va;
+    s->arenas[group].ensure((size_t)std::max<int64_t>(s->capacity(), 1) * (size_t)s->unit_bytes);
+    if (va != s->arenas[group].va) s->refresh_bases();
     const auto& chunks = s->arenas[group].chunks;
     *n_out = (int)chunks.size();
     *chunk_bytes_out = (int64_t)s->arenas[group].chunk_bytes;

@@ -16,7 +16,7 @@ HERE = Path(__file__).resolve().parent
 PKG = HERE.parent
 ROOT = PKG.parent
 OUT = PKG / "libpipelive.so"
-SOURCES = ["vmm.cu", "store.cu", "patch.cu", "ipc.cu", "kernels.cu", "attn.cu", "abi.cu"]
+SOURCES = ["vmm.cu", "store.cu", "patch.cu", "ipc.cu", "kernels.cu", "attn.cu", "verify.cu", "abi.cu"]
 HEADERS = ["internal.h", "common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -63,6 +63,10 @@ struct Reclaimer {
   uint64_t submit(cudaStream_t st, CUdeviceptr va, size_t bytes,
                   std::vector<CUmemGenericAllocationHandle> handles, CUdeviceptr free_va,
                   size_t free_va_bytes, bool immediate);
+  // unmap + free a superseded reservation (no chunks change hands) once every stream
+  // of the device has passed this point
+  uint64_t submit_device_wide(CUdeviceptr va, size_t bytes, CUdeviceptr free_va,
+                              size_t free_va_bytes);
   // true + still-mapped range if the job had not started; false after waiting for it
   bool cancel(uint64_t id, CUdeviceptr* va, std::vector<CUmemGenericAllocationHandle>* hs);
   std::vector<CUmemGenericAllocationHandle> take(size_t n);  // unmapped cached chunks
@@ -113,6 +117,7 @@ struct Arena {
   Reclaimer* rc = nullptr;
   uint64_t tail_job = 0;          // retired tail still mapped (pending reclaim job)
   uint64_t prep_job = 0;          // tail being mapped ahead of a planned grow
+  size_t prep_chunks = 0;         // chunks that job was asked to map
   // instrumentation of the last resize: chunks taken back from the mapped tail,
   // re-mapped from the reclaimer's cache, created with cuMemCreate
   size_t last_tail_reused = 0, last_cache_reused = 0, last_created = 0, last_prepared = 0;
@@ -392,6 +397,7 @@ struct Store {
   void dematerialise(int g);
   uint64_t group_base(int g) const { return (uint64_t)arenas[g].va; }
   int64_t mapped_bytes() const;
+  int64_t planned_bytes() const;  // mapped + being mapped by the reclaimer (no adoption)
 
   // --- operations (reference semantics)
   void append(int32_t req, int g, int64_t n, int mode, const uint64_t* payloads, uint64_t seed,
@@ -429,6 +435,13 @@ struct Store {
                     const int64_t* positions, const void* kv_dev, int mark);
 };
 void detach_patches(Store* st);
+// full-size verification (verify.cu): every live cell of a store against the parity
+// expansion of its fingerprint (and the fingerprint against the engine payload of the
+// per-(request, group) seed, seeds[req * n_model_groups + g], ~0 = unchecked); and two
+// stores' (request, group) items byte for byte
+void verify_store(Store* st, const uint64_t* seeds, int64_t n_seed_reqs, int64_t out[4]);
+void compare_stores(Store* a, Store* b, const int32_t* groups, int n_groups, const int32_t* reqs,
+                    int n_reqs, int64_t out[3]);
 
 // ---------------------------------------------------------------------------
 // Packs host arrays into the store's pinned buffer and ships them in one H2D

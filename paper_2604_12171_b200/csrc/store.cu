@@ -171,7 +171,10 @@ void Store::ensure_slots(int64_t n_slots) {
   bool any = false;
   for (int g = 0; g < n_model_groups; ++g)
     if (materialised[g]) {
-      if (g < 64) pending_groups &= ~(1ull << g);
+      // a lazily materialised group is adopted over the whole capacity, not up to n_slots:
+      // chains are shared across groups, so live blocks of other groups can sit at any
+      // slot below capacity and K1 / patch copies / K6 may touch them in this group
+      if (g < 64 && ((pending_groups >> g) & 1)) adopt_group(g);
       const uint64_t va = arenas[g].va;
       arenas[g].ensure((size_t)n_slots * (size_t)unit_bytes);  // adopts a pending tail first
       if (va != arenas[g].va) refresh_bases();
@@ -572,6 +575,12 @@ void Store::dematerialise(int g) {
   if (g < 64) pending_groups &= ~(1ull << g);
   mapped_slots = 0;
   refresh_bases();
+}
+int64_t Store::planned_bytes() const {
+  int64_t b = 0;
+  for (int g = 0; g < n_model_groups; ++g)
+    if (materialised[g]) b += (int64_t)((arenas[g].chunks.size() + arenas[g].prep_chunks) * arenas[g].chunk_bytes);
+  return b;
 }
 int64_t Store::mapped_bytes() const {
   int64_t b = 0;

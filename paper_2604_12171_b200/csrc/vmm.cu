@@ -210,13 +210,33 @@ uint64_t Reclaimer::submit(cudaStream_t st, CUdeviceptr va, size_t bytes,
   return id;
 }
 
+uint64_t Reclaimer::submit_device_wide(CUdeviceptr va, size_t bytes, CUdeviceptr free_va,
+                                       size_t free_va_bytes) {
+  auto j = std::make_unique<Job>();
+  j->ev = nullptr;  // the helper thread synchronises the whole device instead
+  j->va = va;
+  j->bytes = bytes;
+  j->free_va = free_va;
+  j->free_va_bytes = free_va_bytes;
+  j->submitted = Clock::now();
+  j->due = j->submitted;
+  uint64_t id;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    id = j->id = ++next_id;
+    jobs.push_back(std::move(j));
+  }
+  cv.notify_all();
+  return id;
+}
+
 bool Reclaimer::cancel(uint64_t id, CUdeviceptr* va, std::vector<CUmemGenericAllocationHandle>* hs) {
   std::unique_lock<std::mutex> lk(mu);
   for (auto it = jobs.begin(); it != jobs.end(); ++it) {
     if ((*it)->id != id) continue;
     *va = (*it)->va;
     *hs = std::move((*it)->handles);
-    cudaEventDestroy((*it)->ev);
+    if ((*it)->ev) cudaEventDestroy((*it)->ev);
     pending_bytes -= (int64_t)(hs->size() * chunk_bytes);
     jobs.erase(it);
     return true;
@@ -322,8 +342,12 @@ void Reclaimer::loop() {
       jobs.erase(best);
       running = j->id;
       lk.unlock();
-      cudaEventSynchronize(j->ev);
-      cudaEventDestroy(j->ev);
+      if (j->ev) {
+        cudaEventSynchronize(j->ev);
+        cudaEventDestroy(j->ev);
+      } else {
+        cudaDeviceSynchronize();
+      }
       if (j->bytes) {
         CUresult ur = d.Unmap(j->va, j->bytes);
         if (trace_on())
@@ -430,6 +454,7 @@ void Arena::adopt_prepared() {
   size_t created = 0;
   std::vector<CUmemGenericAllocationHandle> hs = rc->adopt(prep_job, &created);
   prep_job = 0;
+  prep_chunks = 0;
   // mapped (with access) at va + (chunks.size() + i) * chunk_bytes by the reclaimer thread
   chunks.insert(chunks.end(), hs.begin(), hs.end());
   last_prepared += hs.size();
@@ -457,6 +482,7 @@ bool Arena::prepare(size_t bytes) {
   if (!va || want_chunks * chunk_bytes > va_bytes) return false;  // needs a new VA range
   prep_job = rc->submit_prepare(va + chunks.size() * chunk_bytes, want_chunks - chunks.size(),
                                 peer_devices);
+  prep_chunks = want_chunks - chunks.size();
   return true;
 }
 
@@ -483,8 +509,11 @@ void Arena::ensure(size_t bytes) {
       cu_check(d.Map(nva + i * chunk_bytes, chunk_bytes, 0, chunks[i], 0), "cuMemMap");
     set_access(nva, chunks.size() * chunk_bytes, device, peer_devices);
     if (va) {
-      if (!chunks.empty()) cu_check(d.Unmap(va, chunks.size() * chunk_bytes), "cuMemUnmap");
-      cu_check(d.AddressFree(va, va_bytes), "cuMemAddressFree");
+      // in-flight kernels on any stream (the store's, a patch side stream, a caller's decode
+      // stream) may still address the old range: its unmap + free go to the reclaimer
+      // thread, gated on a device-wide synchronise (this path is rare: only when a grow
+      // outruns the reservation's 4x headroom); the chunks stay mapped at the new range
+      rc->submit_device_wide(va, chunks.size() * chunk_bytes, va, va_bytes);
     }
     va = nva;
     va_bytes = new_va_bytes;

@@ -578,6 +578,36 @@ class KvStore:
                                           N.ptr(buf), n))
         return buf.tobytes()
 
+    def verify_cells(self, seeds: dict | None = None) -> dict[str, int]:
+        """Every live cell on the device (csrc/verify.cu): all k layer cells must be the
+        parity expansion of the cell's fingerprint; with ``seeds`` ({(request_id, group):
+        seed}), each fingerprint must also be PipelineEngine._payloads' value for its
+        position (engine.py:252-261).  Returns the kernel's counters."""
+        arr, n = None, 0
+        if seeds:
+            n = max(self._registry.handle(r) for r, _ in seeds) + 1
+            arr = np.full((n, self.num_groups), np.iinfo(np.uint64).max, dtype=np.uint64)
+            for (r, g), sd in seeds.items():
+                arr[self._registry.handle(r), g] = sd
+        out = np.zeros(4, dtype=np.int64)
+        _check(N.lib().pl_store_verify(self._h, N.ptr(arr), n, N.ptr(out)))
+        return {"cells": int(out[0]), "bad_bytes": int(out[1]), "bad_fingerprints": int(out[2]),
+                "first_bad": int(out[3])}
+
+    def compare_cells(self, other: "KvStore", groups: Iterable[int],
+                      request_ids: Iterable | None = None) -> dict[str, int]:
+        """Byte-for-byte comparison with another store on the same device: every written
+        position of every (request, group), fingerprint and k cells, each side through its
+        own block table.  Default requests: all of this store's."""
+        rids = list(self.tables) if request_ids is None else list(request_ids)
+        groups = list(groups)
+        hs = N.as_i32([self._registry.handle(r) for r in rids] or [0])
+        gs = N.as_i32(groups or [0])
+        out = np.zeros(3, dtype=np.int64)
+        _check(N.lib().pl_store_compare(self._h, other._h, N.ptr(gs), len(groups),
+                                        N.ptr(hs), len(rids), N.ptr(out)))
+        return {"cells": int(out[0]), "bad_positions": int(out[1]), "missing": int(out[2])}
+
     def compact(self) -> int:
         out = C.c_int64()
         _check(N.lib().pl_store_compact(self._h, C.byref(out)))

@@ -376,12 +376,18 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040,
             i, g, p, j = rng.choice(live_ids), rng.randrange(5), rng.randrange(ctx), rng.randrange(4)
             samples[(rid(i), g, p, j)] = (src.read_checksum(rid(i), g, p), src.read_cell(rid(i), g, p, j))
 
+    seeds = {(rid(i), g): stable_hash(rid(i), g) for i in range(fill_reqs) for g in range(5)}
+
     def verify(store, groups, what):
         for (r, g, p, j), (fp, cell) in samples.items():
             if g in groups:
                 assert store.read_checksum(r, g, p) == fp, (what, r, g, p)
                 assert store.read_cell(r, g, p, j) == cell, (what, r, g, p, j)
         out.setdefault("checks", []).append(what)
+        # every live cell on the device (csrc/verify.cu), not just the samples
+        v = store.verify_cells(seeds)
+        out.setdefault("full_checks", []).append(
+            {"what": what, "cells": v["cells"], "bad": v["bad_bytes"] + v["bad_fingerprints"]})
 
     # Phase 2: compact + shrink with relocation, then map the incoming group 5
     t0 = time.perf_counter()
@@ -432,7 +438,11 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040,
     if check:
         for g in (3, 4):
             assert dst.snapshot_group(g) == src.snapshot_group(g), g
-        verify(dst, (3, 4), "patched")
+        c = src.compare_cells(dst, (3, 4), [reg.name(h) for h in live])
+        assert c["missing"] == 0
+        out.setdefault("full_checks", []).append(
+            {"what": "patched", "cells": c["cells"], "bad": c["bad_positions"]})
+        verify(dst, (3, 4), "patched(dst)")
     patch.close()
     out["free_gb_during_patch"] = free_gb()
     dst.close()   # the destination is another GPU on hardware; free its HBM here

@@ -4,7 +4,10 @@ fingerprint of both migrating groups on the destination equals the source's and 
 engine's payload (engine.py:252-261); sampled cells are bit-exact copies and equal the
 oracle's expansion of their fingerprint; a steady round after random writes moves exactly
 the marked keys; the pipelined cold push (runs) and the one-launch push give identical
-destinations (same block ids)."""
+destinations (same block ids).  Beyond samples, every live cell of every store is
+checked on the device (csrc/verify.cu): all 4096 B of every cell against the expansion
+of its fingerprint, every fingerprint against the engine payload, and the destination
+against the source byte for byte."""
 
 import random
 
@@ -25,6 +28,28 @@ def _rig(chunked, monkeypatch):
     rig = PatchRig(Workload())
     rig.fill()
     return rig
+
+
+def _full_check(rig):
+    """Every live cell of both stores, on the device: all bytes = the expansion of the
+    cell's fingerprint, every fingerprint = the engine payload of its position; and the
+    destination's migrating groups = the source's, byte for byte (csrc/verify.cu)."""
+    from paper_2604_12171_b200.events import stable_hash
+    from paper_2604_12171_b200.perf import rid
+    wl = rig.wl
+    seeds = {(rid(i), g): stable_hash(rid(i), g) for i in range(wl.batch) for g in wl.src_groups}
+    live = sum(len(rig.src.tables[rid(i)].chain) for i in range(wl.batch))
+    v = rig.src.verify_cells(seeds)
+    assert v["bad_bytes"] == 0 and v["bad_fingerprints"] == 0 and v["first_bad"] == -1, v
+    written = sum(rig.src.tables[rid(i)].written[g] for i in range(wl.batch) for g in wl.src_groups)
+    assert v["cells"] == written and live > 0
+    d = rig.dst.verify_cells(seeds)
+    assert d["bad_bytes"] == 0 and d["bad_fingerprints"] == 0, d
+    mig = sum(rig.src.tables[rid(i)].written[g] for i in range(wl.batch) for g in wl.mig_groups)
+    assert d["cells"] == mig
+    c = rig.src.compare_cells(rig.dst, wl.mig_groups)
+    assert c["bad_positions"] == 0 and c["missing"] == 0 and c["cells"] == mig * wl.k, c
+    return v["cells"] + d["cells"]
 
 
 def _check_group(rig, g, rng, n_samples=64):
@@ -62,6 +87,8 @@ def test_fullsize_bulk_round(monkeypatch, runs, chunked):
     assert cells * wl.cell_bytes == wl.payload_bytes == 17_179_869_184
     for g in wl.mig_groups:
         _check_group(rig, g, rng)
+    # every byte: 17.2 GB patched + 34.4 GB of source cells, on the device
+    assert _full_check(rig) == wl.batch * wl.ctx * (len(wl.src_groups) + len(wl.mig_groups))
     # block ids of the destination chains: identical with and without the pipelined runs
     from paper_2604_12171_b200.perf import rid
     runs[chunked] = [[b.block_id for b in rig.dst.tables[rid(i)].chain] for i in range(0, wl.batch, 17)]
@@ -93,6 +120,18 @@ def test_fullsize_steady_round_moves_exactly_the_marked_keys(monkeypatch):
         _check_group(rig, g, rng, n_samples=16)
         for i in pick[:8]:                            # the new token is there, bit-exact
             assert rig.dst.read_cell(rid(i), g, wl.ctx, 0) == rig.src.read_cell(rid(i), g, wl.ctx, 0)
+    _full_check(rig)
+    # more steady rounds, including requests that finish mid-migration
+    for step in range(3):
+        pick = sorted(rng.sample(range(wl.batch), wl.batch // 4))
+        reqs = [rig.handles[i] for i in pick for _ in wl.src_groups]
+        groups = [g for _ in pick for g in wl.src_groups]
+        append_batch(rig.src, reqs, groups, [1 + step] * len(reqs),
+                     [stable_hash(rid(i), g) for i in pick for g in wl.src_groups], mark=True)
+        rig.patch.push(rig.dst, rig.registry.rank())
+    rig.src.sync()
+    rig.dst.sync()
+    _full_check(rig)
     rig.destroy()
 
 
@@ -109,7 +148,13 @@ def test_fullsize_configs2_live_resize():
     gc.collect()
     torch.cuda.empty_cache()
     out = c3_live_resize(0, check=True)
-    assert out["checks"] == ["relocation", "patched", "drop+grow"]
+    assert out["checks"] == ["relocation", "patched(dst)", "drop+grow"]
+    # every live cell, not samples: after the K6 relocation, the patch, the drop + grow
+    full = out["full_checks"]
+    assert [f["what"] for f in full] == ["relocation", "patched", "patched(dst)", "drop+grow"]
+    for f in full:
+        assert f["bad"] == 0 and f["cells"] > 0, f
+    assert full[0]["cells"] > 20e6 and full[1]["cells"] > 9e6
     assert out["phase2_shrink_stats"]["relocated_blocks"] > 13_000
     assert out["bulk_patch"]["payload_bytes"] > 39e9
 
@@ -153,6 +198,10 @@ def test_max_size_pool_8b_pp8():
     with pytest.raises(KvOverflow):
         st.append(rid(0), 0, 1, [1])
     assert st.used_blocks == cap and st.tables[rid(0)].written[0] == 2048
+    # every one of the 9.78 M cells (160 GB): bytes = expansion, fingerprint = engine payload
+    seeds = {(rid(i), 0): stable_hash(rid(i), 0) for i in range(n_req)}
+    v = st.verify_cells(seeds)
+    assert v == {"cells": tokens, "bad_bytes": 0, "bad_fingerprints": 0, "first_bad": -1}, v
 
     rng = random.Random(5)
     keep = [i for i in range(n_req) if i % 2 == 1]
@@ -174,4 +223,7 @@ def test_max_size_pool_8b_pp8():
     for i, pos, j, fp, cell in samples:
         assert st.read_checksum(rid(i), 0, pos) == fp
         assert st.read_cell(rid(i), 0, pos, j) == cell
+    v = st.verify_cells({k: sd for k, sd in seeds.items() if int(k[0][1:]) % 2 == 1})
+    assert v["bad_bytes"] == 0 and v["bad_fingerprints"] == 0
+    assert v["cells"] == sum(lens[i] for i in keep)
     st.close()

@@ -318,3 +318,44 @@ def test_acceptance_criterion_3_randomized_allocator_ops():
                 pos = rng.randrange(len(pays))
                 assert st.read_checksum(rid, g, pos) == pays[pos]
     assert time.time() - t0 < 10.0, time.time() - t0
+
+
+class TestLazyGroupAdoption:
+    """A group added while the reclaimer thread is busy is mapped lazily; the first
+    allocation must adopt it over the whole capacity (ensure_slots used to
+    clear the pending bit and map only up to the allocated slot, while chains shared
+    with other groups already held live blocks at higher slots)."""
+
+    def test_new_group_written_at_high_slots_while_reclaimer_busy(self, kv):
+        import ctypes as C
+
+        import torch
+
+        from paper_2604_12171_b200 import _native as N
+
+        st = kv.KvStore(1, 2, 16, 64, (0, 1), cell_bytes=4096, chunk_bytes=2 << 20)
+        s = torch.cuda.Stream()
+        N.check(N.lib().pl_store_set_stream(st._h, C.c_void_p(s.cuda_stream)))
+        for i in range(60):
+            st.append_seeded(f"x{i}", 0, 16, 100 + i)
+        for i in range(0, 40):
+            st.free_request(f"x{i}")          # holes in the low slots, live blocks above
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(200_000_000)    # ~0.1 s: the release job below waits on it
+        st.drop_layer_groups([1])             # immediate reclaim job, gated on the sleep
+        st.resident_groups.add(2)             # lazy pool: its mapping queues behind the job
+        st.append_seeded("new", 2, 16, 7)     # allocates a low hole first
+        for i in range(40, 60):               # then the shared chains at high slots
+            st.append_seeded(f"x{i}", 2, 16, 200 + i)
+        st.sync()
+        for i in range(40, 60):
+            fp = st.read_checksum(f"x{i}", 2, 15)
+            assert st.read_cell(f"x{i}", 2, 15, 1) == oracle.expand_cell(fp, 1, 4096)
+        # a shrink relocates the live high units of every group, the new one included
+        keep = {(f"x{i}", g): st.read_cell(f"x{i}", g, 3, 0) for i in range(40, 60) for g in (0, 2)}
+        st.compact()
+        st.resize(st.used_blocks + 1)
+        assert st.last_resize_stats()["relocated_blocks"] > 0
+        for (r, g), v in keep.items():
+            assert st.read_cell(r, g, 3, 0) == v
+        torch.cuda.synchronize()

@@ -182,3 +182,55 @@ def test_acceptance_criterion_4_randomized_reconfigurations(golden):
             assert lag < scen.triggers[0].tau
     assert committed >= 60
     assert time.time() - t0 < 120.0
+
+
+@pytest.mark.parametrize("name,source", [("fig3_seed5", "golden"), ("hetero_c10_seed123", "golden"),
+                                         ("config0_tiny", "config")])
+def test_parity_run_with_full_4096_byte_cells(golden, monkeypatch, name, source):
+    """The parity runs above store a 64-B prefix of each cell (kvstore.DEFAULT_CELL_BYTES)
+    so simulated 80 GiB GPUs fit on one B200.  Here the same runs move real 4096-B cells:
+    the trace sha256, timestamps and switch point are unchanged, and at the commit (after
+    the final sync, before the barrier) every written position of every migrated group on
+    every destination equals the source byte for byte -- fingerprint and all k x 4096 B --
+    and every live cell of every store equals the expansion of its fingerprint."""
+    from paper_2604_12171_b200 import coordinator
+    from paper_2604_12171_b200.simulation import Simulation
+
+    if source == "golden":
+        want = golden("simulations.json")[name]
+        scen, seed, fill = sim_scenarios.golden_runs()[name]
+    else:
+        want = golden("config_runs.json")[name]
+        scen, seed, fill = sim_scenarios.config_runs()[name]
+    checks = []
+    barrier = coordinator.Coordinator._barrier
+
+    def checked_barrier(self, plan, status, pause_start, finish):
+        for (src, dst), groups in status.migrated_groups.items():
+            rids = sorted({r for g in groups for r in status.source_snapshots[(src, dst)][g]})
+            c = self.stores[src].compare_cells(self.stores[dst], groups, rids)
+            checks.append(("compare", src, dst, c))
+        for gpu, st in sorted(self.stores.items()):
+            checks.append(("verify", gpu, None, st.verify_cells()))
+        return barrier(self, plan, status, pause_start, finish)
+
+    monkeypatch.setattr(coordinator.Coordinator, "_barrier", checked_barrier)
+    sim = Simulation(scen, seed=seed, cell_bytes=4096)
+    assert all(st.cell_bytes == 4096 for st in sim.stores.values())
+    if fill:
+        fill(sim)
+    sim.scheduler.run(until=600.0)
+    assert hashlib.sha256(sim.trace.to_jsonl().encode()).hexdigest() == want["trace_sha"]
+    assert [s.steps_at_commit for s in sim.statuses][:1] == [want["steps_at_commit"]]
+    for got, exp in zip(sim.statuses, want["statuses"]):
+        assert got.timestamps == exp["timestamps"]
+    assert sim.state_digest() == want["state_digest"]
+    compared = [c for kind, _, _, c in checks if kind == "compare"]
+    assert compared and all(c["bad_positions"] == 0 and c["missing"] == 0 for c in compared)
+    assert sum(c["cells"] for c in compared) > 0
+    for kind, gpu, _, v in checks:
+        if kind == "verify":
+            assert v["bad_bytes"] == 0 and v["first_bad"] == -1, (gpu, v)
+    for st in sim.stores.values():   # and at the end of the run
+        v = st.verify_cells()
+        assert v["bad_bytes"] == 0, v
