@@ -134,9 +134,10 @@ class Clocks:
 
 # ------------------------------------------------------------------------------ CPU legs
 def cpu_patch_rate(wl, seconds: float = 12.0, n_req: int = 8) -> dict:
-    """The oracle port (oracle/oracle.c, the reference's _drain + PatchReceiver._apply
-    restated in C with real KV bytes) on the host cores: KV-patch GB/s of a bounded
-    sample of the same workload (n_req requests x ctx tokens x the migrating groups)."""
+    """The oracle PORT (oracle/oracle.c, the reference's _drain + PatchReceiver._apply
+    restated in C, moving real KV bytes) on all host cores: KV-patch GB/s of a bounded
+    sample of the same workload (n_req requests x ctx tokens x the migrating groups).
+    Reported as `cpu_baseline_port`, beside the reference itself."""
     import numpy as np
 
     import oracle
@@ -175,20 +176,58 @@ def cpu_patch_rate(wl, seconds: float = 12.0, n_req: int = 8) -> dict:
             "seconds": round(t_total, 2)}
 
 
+REF_SAMPLE_REQS = 64   # requests per reference step: 1/4 of the B = 256 workload
+
+
+def reference_rate(wl, steps: int, warmup: int, n_req: int = REF_SAMPLE_REQS) -> dict:
+    """The reference itself (pipeshift from oracle/_ref, staged by oracle/reference.py's
+    recipe) on the host: each step is one bulk KV-patch round of the bench pair --
+    MigrationManager.start_migration + the event loop until the patch is applied
+    (migrator.py:170-273, 93-132) -- over a bounded sample of the workload (n_req of the
+    B requests x ctx tokens, groups 2-3 of 0-3, k = 4).  CPython is single-threaded: 1
+    core.  The reference moves 8-byte fingerprints per cell; GB/s is KV-equivalent
+    (cells x 4096 B), the unit of our arm."""
+    from oracle import reference as R
+
+    assert (wl.ctx, wl.k, wl.s, wl.cell_bytes) == (R.CTX, R.K, R.S, R.CELL)
+    rnd = R.BulkRound(n_req)
+    for _ in range(warmup):
+        rnd.run()
+    secs = [rnd.run() for _ in range(steps)]
+    total = sum(secs)
+    gbs = rnd.cells * R.CELL * steps / total / 1e9
+    return {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "reference",
+            "sample": f"{n_req} of the {wl.batch} requests per step ({n_req} x {wl.ctx} tokens x "
+                      f"{len(wl.mig_groups)} groups x k={wl.k} = {rnd.cells} cells, "
+                      f"{rnd.cells * R.CELL / 1e9:.2f} GB KV-equivalent); pipeshift (oracle/_ref), "
+                      f"CPython 1 thread; the reference moves 8-B fingerprints, bytes are "
+                      f"KV-equivalent (cells x {R.CELL} B)",
+            "steps": steps, "seconds": round(total, 2),
+            "ms_per_step_sample": round(total / steps * 1e3, 2),
+            "host": R.host_info()}
+
+
 def run_reference(args, wl, rank: int, world: int) -> None:
     if rank != 0:
         return
     K, W = args.steps, args.warmup
-    cb = cpu_patch_rate(wl, seconds=max(4.0, 2.0 * (K + W)))
+    from oracle import reference as R
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not staged (run "
+                          "__graft_entry__.build() in the dev container)"}), flush=True)
+        return
+    cb = reference_rate(wl, K, W)
+    extras = {"append": R.time_append(16), "compact_resize": R.time_resize()}
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GB/s",
         "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": round(wl.payload_bytes / (cb["value"] * 1e9) * 1e3, 3),
+        "ms_per_step": cb["ms_per_step_sample"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic", "config": config_of(wl, world),
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reference_extras": extras,
     }
     print(json.dumps(line), flush=True)
 
@@ -292,6 +331,19 @@ def main() -> None:
         ring.use_stream(stream.cuda_stream)
     stepper = ring if ring is not None else rig
 
+    # ---- value_cold: the first bulk round of a reconfiguration, into a destination with no
+    # chains yet (the receiver reserves every block on the host while the copy runs)
+    torch.cuda.synchronize()
+    tc0 = time.perf_counter()
+    cold_keys, _ = stepper.bulk_round()
+    torch.cuda.synchronize()
+    cold_ms = allmax((time.perf_counter() - tc0) * 1e3, world)
+    assert cold_keys == wl.batch * wl.ctx * len(wl.mig_groups)
+    value_cold = {"value": round(world * wl.payload_bytes / (cold_ms / 1e3) / 1e9, 2),
+                  "unit": "GB/s", "ms": round(cold_ms, 3),
+                  "note": "first bulk round into empty destination chains (wall clock, host "
+                          "block reservation + K3 + push); `value` is the warm re-push"}
+
     # ---- value: bulk KV-patch rounds, everything resident in HBM
     for _ in range(W):
         stepper.bulk_round()
@@ -389,29 +441,72 @@ def main() -> None:
 
     if rank != 0:
         return
-    cpu = None if args.skip_cpu else cpu_patch_rate(wl)
+    cpu = cpu_port = None
+    if not args.skip_cpu:
+        from oracle import reference as R
+        # the reference itself (pipeshift, 1 core) ~15 s, and the 16-thread C port beside it
+        cpu = guarded("cpu_baseline", lambda: reference_rate(wl, 10, 1)) if R.available() else None
+        cpu_port = guarded("cpu_baseline_port", lambda: cpu_patch_rate(wl))
+    # the driver keeps the TAIL of stdout: the bulky per-point sweeps go first, the headline
+    # extras (decode, pause, live timeline, resize incl. background mapping) last
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": round(ms / K, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": config_of(wl, world),
-        "roofline": roofline,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "e2e_real_kv_from_host": e2e_kv,
-        "gpu_launches": launches,
-        "clocks": clocks.summary(),
-        "switch_pause_ms": pause,
-        "c2_live": c2,
-        "decode": decode,
-        "decode_70b_shape": decode_70b,
-        "resize": resize,
-        "weight_stage": wstage,
         "c5_sweep": sweep,
         "c5_pairs": pairs,
+        "e2e_real_kv_from_host": e2e_kv,
+        "weight_stage": wstage,
         "c3_live_resize": c3,
+        "c2_live": c2,
+        "resize": resize,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "cpu_baseline_port": cpu_port,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "value_cold": value_cold,
+        "switch_pause_ms": pause,
+        "decode": decode,
+        "decode_70b_shape": decode_70b,
+        "tail": tail_summary(c2, c3, resize, decode, decode_70b, pause, value_cold, hbm_peak),
     }
     print(json.dumps(line), flush=True)
+
+
+def tail_summary(c2, c3, resize, decode, decode_70b, pause, value_cold, hbm_peak) -> dict:
+    """The headline extras in one small object at the very end of the line."""
+    def get(d, *path):
+        for p in path:
+            if not isinstance(d, dict) or p not in d:
+                return None
+            d = d[p]
+        return d
+
+    out = {"value_cold_gbs": get(value_cold, "value"),
+           "decode_8b": {"tokens_per_s": get(decode, "tokens_per_s"),
+                         "hbm_frac": get(decode, "roofline", "frac")},
+           "decode_70b_shape": {"tokens_per_s": get(decode_70b, "tokens_per_s"),
+                                "hbm_frac": get(decode_70b, "roofline", "frac")},
+           "switch_pause_data_path_ms": get(pause, "median")}
+    if isinstance(c2, dict) and "error" not in c2:
+        out["c2_live"] = {k: c2.get(k) for k in (
+            "tpot_ms_before", "tpot_ms_during_bulk", "tpot_ms_steady_patching", "tpot_ms_after",
+            "switch_step", "switch_pause_ms", "switch_pause_breakdown_ms", "bulk")
+            if k in c2}
+    if isinstance(resize, dict) and "error" not in resize:
+        out["resize_full_ms"] = {k: resize.get(k) for k in (
+            "drop_groups_full_ms", "shrink_full_ms", "grow_warm_full_ms", "grow_cold_full_ms")}
+        out["resize_critical_path_ms"] = {k: resize.get(k) for k in (
+            "drop_groups_ms", "shrink_ms", "grow_warm_ms", "grow_cold_ms")}
+    if isinstance(c3, dict) and "error" not in c3:
+        out["c3_70b"] = {k: c3.get(k) for k in (
+            "phase2_shrink_full_ms", "map_incoming_group_full_ms", "grow_full_ms",
+            "phase2_shrink_ms", "map_incoming_group_ms", "grow_ms")}
+        out["c3_70b"]["bulk_patch_gbs"] = get(c3, "bulk_patch", "gbs")
+    return out
 
 
 def measure_switch_pause(rig, stream, torch, wl) -> dict:
@@ -731,6 +826,9 @@ def measure_resize(rig, stream, torch, wl) -> dict:
     out["drop_groups_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
     out["drop_pending_reclaim_bytes"] = st.vmm_stats()["pending_reclaim_bytes"]
     out["drop_reclaim_ms"] = round(st.reclaim(), 3)
+    # resize latency = compact + VMM unmap/map + K6, i.e. until the physical
+    # memory is back with the driver (unmap forced now instead of after the grace period)
+    out["drop_groups_full_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
     # free a quarter of the requests so the shrink must relocate live tail blocks
     for i in range(0, wl.batch, 4):
         st.free_request(f"r{i:04d}")
@@ -749,11 +847,16 @@ def measure_resize(rig, stream, torch, wl) -> dict:
     st.resize(cap)
     st.sync()
     out["grow_warm_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    out["grow_warm_full_ms"] = round((time.perf_counter() - t0) * 1e3 + st.prepare_wait(), 3)
     v1 = st.vmm_stats()
     out["grow_warm_stats"] = {**st.last_resize_stats(), **vdelta(v0, v1)}
+    # the shrink again, now timed until its tail is unmapped (full latency)
+    t0 = time.perf_counter()
+    st.compact()
     st.resize(target)
     st.sync()
     out["reclaim_ms"] = round(st.reclaim(), 3)
+    out["shrink_full_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
     v2 = st.vmm_stats()
     t0 = time.perf_counter()
     st.resize(cap)
@@ -761,11 +864,13 @@ def measure_resize(rig, stream, torch, wl) -> dict:
     out["grow_cold_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
     # the new tail is mapped by the reclaimer thread (lazy grow); time until it is done
     out["grow_cold_background_ms"] = round((time.perf_counter() - t0) * 1e3 + st.prepare_wait(), 3)
+    out["grow_cold_full_ms"] = out["grow_cold_background_ms"]
     out["grow_cold_stats"] = {**st.last_resize_stats(), **vdelta(v2, st.vmm_stats())}
     out["blocks"] = {"from": cap, "to": target, "live": st.used_blocks}
     out["tokens_freed_by_drop"] = freed
-    out["note"] = ("*_ms = critical path; physical unmap/release deferred to the reclaimer "
-                   "thread (reclaim_ms, drop_reclaim_ms = forced completion)")
+    out["note"] = ("*_full_ms = SURVEY 8(d) resize latency: until the VMM unmap/map is done "
+                   "(physical memory returned / mapped); *_ms without 'full' = the critical "
+                   "path of the call (unmap/map run on the store's reclaimer thread)")
     return out
 
 

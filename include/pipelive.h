@@ -152,11 +152,12 @@ int pl_store_read_cell(pl_store* st, int32_t req, int group, int64_t token, int 
  *      compare: for each request x group, every written position of store a and store b
  *      (same device) holds the same fingerprint and k cells, each side resolved through its
  *      own block table (PatchReceiver._apply / write_slots, migrator.py:115-131,
- *      kvstore.py:201-227).  out3 = {cells compared, positions that differ, positions
- *      missing or lengths that differ}. */
+ *      kvstore.py:201-227), over the shorter of the two written prefixes.  out4 = {cells
+ *      compared, positions that differ, positions with no block on one side, (request,
+ *      group) items whose written lengths differ}. */
 int pl_store_verify(pl_store* st, const uint64_t* seeds_host, int64_t n_seed_reqs, int64_t* out4);
 int pl_store_compare(pl_store* a, pl_store* b, const int32_t* groups, int n_groups,
-                     const int32_t* reqs, int n_reqs, int64_t* out3);
+                     const int32_t* reqs, int n_reqs, int64_t* out4);
 
 /* ---- lifecycle ops: compact (kvstore.py:247-257), resize (kvstore.py:259-282; K6 remap),
  *      drop_layer_groups (kvstore.py:284-309), free_request (kvstore.py:311-322),

@@ -391,8 +391,8 @@ int pl_store_verify(pl_store* st, const uint64_t* seeds_host, int64_t n_seed_req
   return guard([&] { pl::verify_store(st->s, seeds_host, n_seed_reqs, out4); });
 }
 int pl_store_compare(pl_store* a, pl_store* b, const int32_t* groups, int n_groups,
-                     const int32_t* reqs, int n_reqs, int64_t* out3) {
-  return guard([&] { pl::compare_stores(a->s, b->s, groups, n_groups, reqs, n_reqs, out3); });
+                     const int32_t* reqs, int n_reqs, int64_t* out4) {
+  return guard([&] { pl::compare_stores(a->s, b->s, groups, n_groups, reqs, n_reqs, out4); });
 }
 
 int pl_store_compact(pl_store* st, int64_t* out) {

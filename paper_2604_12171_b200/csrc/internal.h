@@ -441,7 +441,7 @@ void detach_patches(Store* st);
 // stores' (request, group) items byte for byte
 void verify_store(Store* st, const uint64_t* seeds, int64_t n_seed_reqs, int64_t out[4]);
 void compare_stores(Store* a, Store* b, const int32_t* groups, int n_groups, const int32_t* reqs,
-                    int n_reqs, int64_t out[3]);
+                    int n_reqs, int64_t out[4]);
 
 // ---------------------------------------------------------------------------
 // Packs host arrays into the store's pinned buffer and ships them in one H2D

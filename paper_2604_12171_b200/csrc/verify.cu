@@ -186,7 +186,7 @@ void verify_store(Store* st, const uint64_t* seeds, int64_t n_seed_reqs, int64_t
 }
 
 void compare_stores(Store* a, Store* b, const int32_t* groups, int n_groups, const int32_t* reqs,
-                    int n_reqs, int64_t out[3]) {
+                    int n_reqs, int64_t out[4]) {
   if (a->device != b->device) fail(PL_E_INVALID, "compare: stores on different devices");
   if (a->k != b->k || a->cell_bytes != b->cell_bytes) fail(PL_E_INVALID, "compare: layouts differ");
   PL_CUDA(cudaSetDevice(a->device));
@@ -246,7 +246,8 @@ void compare_stores(Store* a, Store* b, const int32_t* groups, int n_groups, con
   cudaEventDestroy(ev);
   out[0] = (int64_t)h[0];
   out[1] = (int64_t)h[1];
-  out[2] = (int64_t)h[2] + length_mismatch;
+  out[2] = (int64_t)h[2];
+  out[3] = length_mismatch;
 }
 
 }  // namespace pl

@@ -597,16 +597,18 @@ class KvStore:
     def compare_cells(self, other: "KvStore", groups: Iterable[int],
                       request_ids: Iterable | None = None) -> dict[str, int]:
         """Byte-for-byte comparison with another store on the same device: every written
-        position of every (request, group), fingerprint and k cells, each side through its
-        own block table.  Default requests: all of this store's."""
+        position (the shorter prefix of the two) of every (request, group), fingerprint and
+        k cells, each side through its own block table.  Default requests: all of this
+        store's."""
         rids = list(self.tables) if request_ids is None else list(request_ids)
         groups = list(groups)
         hs = N.as_i32([self._registry.handle(r) for r in rids] or [0])
         gs = N.as_i32(groups or [0])
-        out = np.zeros(3, dtype=np.int64)
+        out = np.zeros(4, dtype=np.int64)
         _check(N.lib().pl_store_compare(self._h, other._h, N.ptr(gs), len(groups),
                                         N.ptr(hs), len(rids), N.ptr(out)))
-        return {"cells": int(out[0]), "bad_positions": int(out[1]), "missing": int(out[2])}
+        return {"cells": int(out[0]), "bad_positions": int(out[1]), "missing": int(out[2]),
+                "length_mismatch": int(out[3])}
 
     def compact(self) -> int:
         out = C.c_int64()

@@ -154,7 +154,8 @@ def test_fullsize_configs2_live_resize():
     assert [f["what"] for f in full] == ["relocation", "patched", "patched(dst)", "drop+grow"]
     for f in full:
         assert f["bad"] == 0 and f["cells"] > 0, f
-    assert full[0]["cells"] > 20e6 and full[1]["cells"] > 9e6
+    # 76 k live blocks x 16 tokens x 5 groups token-cells (x 4 layers x 4096 B = 100 GB)
+    assert full[0]["cells"] > 6e6 and full[1]["cells"] > 9e6
     assert out["phase2_shrink_stats"]["relocated_blocks"] > 13_000
     assert out["bulk_patch"]["payload_bytes"] > 39e9
 

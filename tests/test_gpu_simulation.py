@@ -192,8 +192,9 @@ def test_parity_run_with_full_4096_byte_cells(golden, monkeypatch, name, source)
     the trace sha256, timestamps and switch point are unchanged, and at the commit (after
     the final sync, before the barrier) every written position of every migrated group on
     every destination equals the source byte for byte -- fingerprint and all k x 4096 B --
-    and every live cell of every store equals the expansion of its fingerprint."""
-    from paper_2604_12171_b200 import coordinator
+    as it does after every patch the receiver applies, and every live cell of every store
+    equals the expansion of its fingerprint."""
+    from paper_2604_12171_b200 import coordinator, migrator
     from paper_2604_12171_b200.simulation import Simulation
 
     if source == "golden":
@@ -209,12 +210,27 @@ def test_parity_run_with_full_4096_byte_cells(golden, monkeypatch, name, source)
         for (src, dst), groups in status.migrated_groups.items():
             rids = sorted({r for g in groups for r in status.source_snapshots[(src, dst)][g]})
             c = self.stores[src].compare_cells(self.stores[dst], groups, rids)
+            # every snapshotted position x k layers was compared
+            c["expected"] = self.model.stacking_factor * sum(
+                len(v) for g in groups for v in status.source_snapshots[(src, dst)][g].values())
             checks.append(("compare", src, dst, c))
         for gpu, st in sorted(self.stores.items()):
             checks.append(("verify", gpu, None, st.verify_cells()))
         return barrier(self, plan, status, pause_start, finish)
 
     monkeypatch.setattr(coordinator.Coordinator, "_barrier", checked_barrier)
+    # and after every patch the receiver applies: the destination's written prefix of every
+    # (request, group) of the pair equals the source's, byte for byte
+    apply_device = migrator.MigrationStream._apply_device
+
+    def checked_apply(self, dst_store, stale_rids):
+        apply_device(self, dst_store, stale_rids)
+        src_store = sim.stores[self.src]
+        rids = [r for r in dst_store.tables if r in src_store.tables and r not in stale_rids]
+        c = src_store.compare_cells(dst_store, sorted(self.groups), rids)
+        checks.append(("apply", self.src, self.dst, c))
+
+    monkeypatch.setattr(migrator.MigrationStream, "_apply_device", checked_apply)
     sim = Simulation(scen, seed=seed, cell_bytes=4096)
     assert all(st.cell_bytes == 4096 for st in sim.stores.values())
     if fill:
@@ -227,7 +243,10 @@ def test_parity_run_with_full_4096_byte_cells(golden, monkeypatch, name, source)
     assert sim.state_digest() == want["state_digest"]
     compared = [c for kind, _, _, c in checks if kind == "compare"]
     assert compared and all(c["bad_positions"] == 0 and c["missing"] == 0 for c in compared)
-    assert sum(c["cells"] for c in compared) > 0
+    assert all(c["cells"] == c["expected"] for c in compared)
+    applied = [c for kind, _, _, c in checks if kind == "apply"]
+    assert applied and all(c["bad_positions"] == 0 and c["missing"] == 0 for c in applied)
+    assert sum(c["cells"] for c in applied) > 0   # every patch of the run, 4096-B cells
     for kind, gpu, _, v in checks:
         if kind == "verify":
             assert v["bad_bytes"] == 0 and v["first_bad"] == -1, (gpu, v)
