@@ -289,6 +289,51 @@ int pl_paged_attn_decode_raw(const void* pool_dev, int64_t unit_bytes, int64_t f
                              int n_q_heads, int n_kv_heads, int head_dim, float scale,
                              int max_ctx, void* stream);
 
+/* ---- K7 stage activations between processes (csrc/act.cu): PipelineEngine._stage_done
+ * forwarding the hidden states to the next stage (engine.py:353-375) over
+ * CommFabric.post_inference_transfer (fabric.py:129-136).  The RECEIVING stage owns a ring
+ * of n_slots (<= 8) device buffers with per-slot interprocess ready/freed events and a
+ * shared-memory mailbox of sequence numbers; it exports the ring as an opaque blob (CUDA
+ * IPC handles + mailbox name), the sending stage opens it (same process: aliases it).
+ * pl_act_send copies src_dev into the next slot on `stream` (after the receiver freed it;
+ * a device-side wait) and publishes it; pl_act_recv makes `stream` wait for that copy on
+ * the device and copies the slot out to dst_dev.  Neither call synchronises a stream; the
+ * hosts poll the mailbox (microseconds).  Sends and receives of one direction are matched
+ * in order, one activation per call. */
+typedef struct pl_act_ring pl_act_ring;
+int pl_act_ring_create(int device, int64_t slot_bytes, int n_slots, pl_act_ring** out);
+int pl_act_ring_export(pl_act_ring* r, void* blob_out, int64_t cap, int64_t* n_out);
+int pl_act_ring_open(int device, const void* blob, int64_t n, pl_act_ring** out);
+int pl_act_ring_destroy(pl_act_ring* r);
+int pl_act_send(pl_act_ring* r, const void* src_dev, int64_t bytes, void* stream);
+int pl_act_recv(pl_act_ring* r, void* dst_dev, int64_t bytes, void* stream);
+
+/* ---- exact mode of the tiny Llama stage compute (csrc/exact.cu): deterministic fp64
+ * kernels whose every sum is a sequential fma chain in ascending index order and whose exp
+ * is a fixed polynomial, so the CPU oracle (oracle/llama_exact.c) reproduces the logits bit
+ * for bit and the generated token ids exactly (north star; the reference has no model,
+ * engine.py:343-347).  Rounding points match the production path: K, V (the paged bf16
+ * cells K1 writes), q and the attention output are rounded to bf16.
+ *   gemv:      out[b,o] = resid[b,o] (if given) + sum_i x[b,i] w[i,o]       (row-major)
+ *   rmsnorm:   out = x * (1 / sqrt(mean(x^2) + eps)) * g, per row of d
+ *   rope_pack: q, k rotated (rotate-half, cos/sin [B][head_dim/2] per row's position);
+ *              q_out = bf16-rounded q (as doubles), cells_out = [B][K: n_kv*D][V] bf16
+ *   silu_mul:  out = a / (1 + exp(-a)) * b
+ *   attn:      paged decode attention over the store's block table (the K2 contract,
+ *              pl_paged_attn_decode), fp64 q/out, output bf16-rounded */
+int pl_exact_gemv(const double* x, const double* w, const double* resid, double* out, int B,
+                  int I, int O, void* stream);
+int pl_exact_rmsnorm(const double* x, const double* g, double* out, int B, int d, double eps,
+                     void* stream);
+int pl_exact_rope_pack(const double* q, const double* k, const double* v, const double* cos_t,
+                       const double* sin_t, double* q_out, void* cells_out, int B, int n_q,
+                       int n_kv, int head_dim, void* stream);
+int pl_exact_silu_mul(const double* a, const double* b, double* out, int64_t n, void* stream);
+int pl_exact_attn_decode(pl_store* st, int group, int layer_in_group, const double* q, double* out,
+                         const int32_t* req_rows, const int32_t* ctx_lens, int batch,
+                         int n_q_heads, int n_kv_heads, int head_dim, double scale, int max_ctx,
+                         void* stream);
+
 /* ---- kernel launch accounting (bench gpu_launches) and per-kernel device timing:
  * when enabled, CUDA events bracket every launch of the named kernels ("kv_write",
  * "patch_gather", "patch_scatter", "patch_push", "drain", "paged_attn", "unit_move");

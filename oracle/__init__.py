@@ -27,7 +27,7 @@ _lib = None
 
 
 def build() -> Path:
-    src = [HERE / "oracle.c", HERE / "oracle.h", HERE / "Makefile"]
+    src = [HERE / "oracle.c", HERE / "oracle.h", HERE / "llama_exact.c", HERE / "Makefile"]
     if not LIB.exists() or any(p.stat().st_mtime > LIB.stat().st_mtime for p in src):
         subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
     return LIB
@@ -73,6 +73,15 @@ def lib():
             "or_dirty_drain": (i64, [vp, vp, i64, vp, vp, vp, i64]),
             "or_patch_round": (C.c_int, [vp, vp, vp, vp, i64, C.c_int, C.c_int,
                                          C.POINTER(i64), C.POINTER(i64)]),
+            # llama_exact.c: the tiny Llama's exact-mode arithmetic
+            "or_det_exp": (C.c_double, [C.c_double]),
+            "or_bf16_round": (C.c_double, [C.c_double]),
+            "or_ex_gemv": (None, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int]),
+            "or_ex_rmsnorm": (None, [vp, vp, vp, C.c_int, C.c_int, C.c_double]),
+            "or_ex_rope": (None, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+            "or_ex_silu_mul": (None, [vp, vp, vp, i64]),
+            "or_ex_attn": (None, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                  vp, vp]),
         }
         for name, (res, args) in sigs.items():
             f = getattr(L, name)

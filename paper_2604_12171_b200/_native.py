@@ -85,6 +85,19 @@ SIGNATURES = [
     ("pl_store_read_cell", C.c_int, [vp, i32, C.c_int, i64, C.c_int, vp, i64]),
     ("pl_store_verify", C.c_int, [vp, vp, i64, vp]),
     ("pl_store_compare", C.c_int, [vp, vp, vp, C.c_int, vp, C.c_int, vp]),
+    ("pl_act_ring_create", C.c_int, [C.c_int, i64, C.c_int, P(vp)]),
+    ("pl_act_ring_export", C.c_int, [vp, vp, i64, P(i64)]),
+    ("pl_act_ring_open", C.c_int, [C.c_int, vp, i64, P(vp)]),
+    ("pl_act_ring_destroy", C.c_int, [vp]),
+    ("pl_act_send", C.c_int, [vp, vp, i64, vp]),
+    ("pl_act_recv", C.c_int, [vp, vp, i64, vp]),
+    ("pl_exact_gemv", C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
+    ("pl_exact_rmsnorm", C.c_int, [vp, vp, vp, C.c_int, C.c_int, dbl, vp]),
+    ("pl_exact_rope_pack", C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
+                                     C.c_int, vp]),
+    ("pl_exact_silu_mul", C.c_int, [vp, vp, vp, i64, vp]),
+    ("pl_exact_attn_decode", C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, dbl, C.c_int, vp]),
     ("pl_store_compact", C.c_int, [vp, P(i64)]),
     ("pl_store_resize", C.c_int, [vp, i64]),
     ("pl_store_drop_groups", C.c_int, [vp, vp, C.c_int, P(i64)]),

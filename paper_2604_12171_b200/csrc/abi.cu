@@ -17,6 +17,9 @@ struct pl_patch {
 struct pl_remote {
   pl::Remote* r;
 };
+struct pl_act_ring {
+  pl::ActRing* r;
+};
 
 namespace pl {
 namespace {
@@ -393,6 +396,60 @@ int pl_store_verify(pl_store* st, const uint64_t* seeds_host, int64_t n_seed_req
 int pl_store_compare(pl_store* a, pl_store* b, const int32_t* groups, int n_groups,
                      const int32_t* reqs, int n_reqs, int64_t* out4) {
   return guard([&] { pl::compare_stores(a->s, b->s, groups, n_groups, reqs, n_reqs, out4); });
+}
+
+int pl_act_ring_create(int device, int64_t slot_bytes, int n_slots, pl_act_ring** out) {
+  return guard([&] { *out = new pl_act_ring{pl::act_ring_create(device, slot_bytes, n_slots)}; });
+}
+int pl_act_ring_export(pl_act_ring* r, void* blob_out, int64_t cap, int64_t* n_out) {
+  return guard([&] { pl::act_ring_export(r->r, blob_out, cap, n_out); });
+}
+int pl_act_ring_open(int device, const void* blob, int64_t n, pl_act_ring** out) {
+  return guard([&] { *out = new pl_act_ring{pl::act_ring_open(device, blob, n)}; });
+}
+int pl_act_ring_destroy(pl_act_ring* r) {
+  return guard([&] {
+    if (!r) return;
+    pl::act_ring_destroy(r->r);
+    delete r;
+  });
+}
+int pl_act_send(pl_act_ring* r, const void* src_dev, int64_t bytes, void* stream) {
+  return guard([&] { pl::act_send(r->r, src_dev, bytes, (cudaStream_t)stream); });
+}
+int pl_act_recv(pl_act_ring* r, void* dst_dev, int64_t bytes, void* stream) {
+  return guard([&] { pl::act_recv(r->r, dst_dev, bytes, (cudaStream_t)stream); });
+}
+
+int pl_exact_gemv(const double* x, const double* w, const double* resid, double* out, int B,
+                  int I, int O, void* stream) {
+  return guard([&] { pl::exact_gemv(x, w, resid, out, B, I, O, (cudaStream_t)stream); });
+}
+int pl_exact_rmsnorm(const double* x, const double* g, double* out, int B, int d, double eps,
+                     void* stream) {
+  return guard([&] { pl::exact_rmsnorm(x, g, out, B, d, eps, (cudaStream_t)stream); });
+}
+int pl_exact_rope_pack(const double* q, const double* k, const double* v, const double* cos_t,
+                       const double* sin_t, double* q_out, void* cells_out, int B, int n_q,
+                       int n_kv, int head_dim, void* stream) {
+  return guard([&] {
+    if (head_dim % 2 || n_q <= 0 || n_kv <= 0) pl::fail(PL_E_INVALID, "bad rope shape");
+    pl::exact_rope_pack(q, k, v, cos_t, sin_t, q_out, cells_out, B, n_q, n_kv, head_dim,
+                        (cudaStream_t)stream);
+  });
+}
+int pl_exact_silu_mul(const double* a, const double* b, double* out, int64_t n, void* stream) {
+  return guard([&] { pl::exact_silu_mul(a, b, out, n, (cudaStream_t)stream); });
+}
+int pl_exact_attn_decode(pl_store* st, int group, int layer_in_group, const double* q, double* out,
+                         const int32_t* req_rows, const int32_t* ctx_lens, int batch,
+                         int n_q_heads, int n_kv_heads, int head_dim, double scale, int max_ctx,
+                         void* stream) {
+  return guard([&] {
+    PL_CUDA(cudaSetDevice(st->s->device));
+    pl::exact_attn(st->s, group, layer_in_group, req_rows, ctx_lens, q, out, batch, n_q_heads,
+                   n_kv_heads, head_dim, scale, max_ctx, (cudaStream_t)stream);
+  });
 }
 
 int pl_store_compact(pl_store* st, int64_t* out) {

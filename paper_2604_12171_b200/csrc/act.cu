@@ -1,0 +1,240 @@
+// K7: stage-to-stage activation hand-off between processes (engine.py:353-375 forward,
+// fabric.py:129-136 post_inference_transfer).
+//
+// One ring per directed stage pair, owned by the RECEIVING stage:
+//   - n_slots device buffers of slot_bytes (cudaMalloc, exported with a CUDA IPC handle;
+//     the sender writes into them directly -- a D2D copy over NVLink when the stages are on
+//     different GPUs, an HBM copy when they share one);
+//   - per slot a "ready" and a "freed" interprocess CUDA event: the receiver's stream waits
+//     for the sender's copy on the device, the sender's stream waits for the receiver's
+//     copy-out before reusing a slot -- no host synchronisation of either stream;
+//   - a two-word mailbox in POSIX shared memory (published / consumed sequence numbers)
+//     that tells the other side's host that an event record has been enqueued (an event
+//     must be recorded before the peer can meaningfully wait on it).  Both hosts poll it
+//     (spin, then yield): microseconds, no socket round trip.
+// In one process (the bench, unit tests) the opened ring aliases the owner's buffers.
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <fcntl.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "internal.h"
+
+namespace pl {
+
+namespace {
+constexpr int kMaxSlots = 8;
+struct Mailbox {
+  std::atomic<uint64_t> published;  // last sequence whose ready event the sender recorded
+  std::atomic<uint64_t> consumed;   // last sequence whose freed event the receiver recorded
+};
+struct Blob {  // what the owner exports (fixed layout, plain bytes)
+  int32_t magic, pid, device, n_slots;
+  int64_t slot_bytes;
+  cudaIpcMemHandle_t mem;
+  cudaIpcEventHandle_t ready[kMaxSlots], freed[kMaxSlots];
+  char shm[64];
+};
+constexpr int32_t kMagic = 0x4b37a11e;
+std::atomic<uint64_t> g_ring_counter{0};
+}  // namespace
+
+struct ActRing {
+  int device = 0, n_slots = 0;
+  int64_t slot_bytes = 0;
+  bool owner = false, ipc = false;
+  uint8_t* buf = nullptr;
+  cudaEvent_t ready[kMaxSlots] = {}, freed[kMaxSlots] = {};
+  Mailbox* mb = nullptr;
+  std::string shm;
+  uint64_t seq_send = 0, seq_recv = 0;
+  ActRing* alias = nullptr;  // same-process open: the owner's ring
+};
+
+namespace {
+std::mutex g_mu;
+std::unordered_map<std::string, ActRing*> g_owned;  // shm name -> owner ring (this process)
+
+void wait_counter(const std::atomic<uint64_t>& c, uint64_t want, const char* what) {
+  using Clock = std::chrono::steady_clock;
+  const auto t0 = Clock::now();
+  for (uint64_t spin = 0; c.load(std::memory_order_acquire) < want; ++spin) {
+    if (spin > 2000) sched_yield();
+    if ((spin & 1023) == 1023 && Clock::now() - t0 > std::chrono::seconds(120))
+      fail(PL_E_STATE, std::string("activation ring: peer never ") + what);
+  }
+}
+}  // namespace
+
+ActRing* act_ring_create(int device, int64_t slot_bytes, int n_slots) {
+  if (n_slots <= 0 || n_slots > kMaxSlots) fail(PL_E_INVALID, "n_slots must be 1..8");
+  if (slot_bytes <= 0) fail(PL_E_INVALID, "slot_bytes must be positive");
+  auto* r = new ActRing();
+  r->device = device;
+  r->n_slots = n_slots;
+  r->slot_bytes = (slot_bytes + 255) / 256 * 256;
+  r->owner = true;
+  try {
+    PL_CUDA(cudaSetDevice(device));
+    PL_CUDA(cudaMalloc(&r->buf, (size_t)r->slot_bytes * n_slots));
+    for (int i = 0; i < n_slots; ++i) {
+      PL_CUDA(cudaEventCreateWithFlags(&r->ready[i], cudaEventDisableTiming | cudaEventInterprocess));
+      PL_CUDA(cudaEventCreateWithFlags(&r->freed[i], cudaEventDisableTiming | cudaEventInterprocess));
+    }
+    r->shm = "/pl-act-" + std::to_string(getpid()) + "-" + std::to_string(++g_ring_counter);
+    const int fd = shm_open(r->shm.c_str(), O_CREAT | O_RDWR | O_EXCL, 0600);
+    if (fd < 0) fail(PL_E_INVALID, "shm_open failed for " + r->shm);
+    if (ftruncate(fd, sizeof(Mailbox)) != 0) {
+      close(fd);
+      fail(PL_E_INVALID, "ftruncate failed");
+    }
+    void* p = mmap(nullptr, sizeof(Mailbox), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) fail(PL_E_INVALID, "mmap failed");
+    r->mb = new (p) Mailbox();
+    r->mb->published.store(0);
+    r->mb->consumed.store(0);
+  } catch (...) {
+    act_ring_destroy(r);
+    throw;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_owned[r->shm] = r;
+  return r;
+}
+
+void act_ring_export(ActRing* r, void* out, int64_t cap, int64_t* n_out) {
+  if (!r->owner) fail(PL_E_STATE, "only the owning (receiving) side exports a ring");
+  *n_out = (int64_t)sizeof(Blob);
+  if (cap < (int64_t)sizeof(Blob)) return;
+  Blob b{};
+  b.magic = kMagic;
+  b.pid = (int32_t)getpid();
+  b.device = r->device;
+  b.n_slots = r->n_slots;
+  b.slot_bytes = r->slot_bytes;
+  PL_CUDA(cudaSetDevice(r->device));
+  PL_CUDA(cudaIpcGetMemHandle(&b.mem, r->buf));
+  for (int i = 0; i < r->n_slots; ++i) {
+    PL_CUDA(cudaIpcGetEventHandle(&b.ready[i], r->ready[i]));
+    PL_CUDA(cudaIpcGetEventHandle(&b.freed[i], r->freed[i]));
+  }
+  std::strncpy(b.shm, r->shm.c_str(), sizeof(b.shm) - 1);
+  std::memcpy(out, &b, sizeof(b));
+}
+
+ActRing* act_ring_open(int device, const void* blob, int64_t n) {
+  if (n < (int64_t)sizeof(Blob)) fail(PL_E_INVALID, "ring blob too short");
+  Blob b;
+  std::memcpy(&b, blob, sizeof(b));
+  if (b.magic != kMagic) fail(PL_E_INVALID, "not an activation ring blob");
+  auto* r = new ActRing();
+  r->device = device;
+  r->n_slots = b.n_slots;
+  r->slot_bytes = b.slot_bytes;
+  r->shm = b.shm;
+  if (b.pid == (int32_t)getpid()) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_owned.find(r->shm);
+    if (it == g_owned.end()) {
+      delete r;
+      fail(PL_E_INVALID, "ring owner not found in this process");
+    }
+    r->alias = it->second;
+    r->buf = it->second->buf;
+    r->mb = it->second->mb;
+    for (int i = 0; i < r->n_slots; ++i) {
+      r->ready[i] = it->second->ready[i];
+      r->freed[i] = it->second->freed[i];
+    }
+    return r;
+  }
+  r->ipc = true;
+  try {
+    PL_CUDA(cudaSetDevice(device));
+    void* p = nullptr;
+    PL_CUDA(cudaIpcOpenMemHandle(&p, b.mem, cudaIpcMemLazyEnablePeerAccess));
+    r->buf = static_cast<uint8_t*>(p);
+    for (int i = 0; i < r->n_slots; ++i) {
+      PL_CUDA(cudaIpcOpenEventHandle(&r->ready[i], b.ready[i]));
+      PL_CUDA(cudaIpcOpenEventHandle(&r->freed[i], b.freed[i]));
+    }
+    const int fd = shm_open(r->shm.c_str(), O_RDWR, 0600);
+    if (fd < 0) fail(PL_E_INVALID, "shm_open of the peer's mailbox failed");
+    void* m = mmap(nullptr, sizeof(Mailbox), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (m == MAP_FAILED) fail(PL_E_INVALID, "mmap failed");
+    r->mb = static_cast<Mailbox*>(m);
+  } catch (...) {
+    act_ring_destroy(r);
+    throw;
+  }
+  return r;
+}
+
+void act_ring_destroy(ActRing* r) {
+  if (!r) return;
+  cudaSetDevice(r->device);
+  if (r->owner) {
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      g_owned.erase(r->shm);
+    }
+    cudaDeviceSynchronize();  // in-flight copies into / out of the ring
+    for (int i = 0; i < r->n_slots; ++i) {
+      if (r->ready[i]) cudaEventDestroy(r->ready[i]);
+      if (r->freed[i]) cudaEventDestroy(r->freed[i]);
+    }
+    cudaFree(r->buf);
+    if (r->mb) munmap(r->mb, sizeof(Mailbox));
+    if (!r->shm.empty()) shm_unlink(r->shm.c_str());
+  } else if (r->ipc) {
+    for (int i = 0; i < r->n_slots; ++i) {
+      if (r->ready[i]) cudaEventDestroy(r->ready[i]);
+      if (r->freed[i]) cudaEventDestroy(r->freed[i]);
+    }
+    if (r->buf) cudaIpcCloseMemHandle(r->buf);
+    if (r->mb) munmap(r->mb, sizeof(Mailbox));
+  }
+  delete r;
+}
+
+// sender: slot free (the receiver's copy-out of seq - n_slots ran) -> copy -> ready
+void act_send(ActRing* r, const void* src, int64_t bytes, cudaStream_t st) {
+  if (bytes > r->slot_bytes) fail(PL_E_INVALID, "activation larger than the ring slot");
+  ActRing* s = r->alias ? r->alias : r;  // one sequence counter per direction
+  const uint64_t seq = ++s->seq_send;
+  const int slot = (int)((seq - 1) % (uint64_t)r->n_slots);
+  if (seq > (uint64_t)r->n_slots) {
+    wait_counter(r->mb->consumed, seq - r->n_slots, "freed a slot");
+    PL_CUDA(cudaStreamWaitEvent(st, r->freed[slot], 0));
+  }
+  PL_CUDA(cudaMemcpyAsync(r->buf + (int64_t)slot * r->slot_bytes, src, (size_t)bytes,
+                          cudaMemcpyDeviceToDevice, st));
+  PL_CUDA(cudaEventRecord(r->ready[slot], st));
+  r->mb->published.store(seq, std::memory_order_release);
+}
+
+// receiver: the sender's copy of seq is enqueued -> device wait -> copy out -> freed
+void act_recv(ActRing* r, void* dst, int64_t bytes, cudaStream_t st) {
+  if (bytes > r->slot_bytes) fail(PL_E_INVALID, "activation larger than the ring slot");
+  ActRing* s = r->alias ? r->alias : r;
+  const uint64_t seq = ++s->seq_recv;
+  const int slot = (int)((seq - 1) % (uint64_t)r->n_slots);
+  wait_counter(r->mb->published, seq, "published an activation");
+  PL_CUDA(cudaStreamWaitEvent(st, r->ready[slot], 0));
+  PL_CUDA(cudaMemcpyAsync(dst, r->buf + (int64_t)slot * r->slot_bytes, (size_t)bytes,
+                          cudaMemcpyDeviceToDevice, st));
+  PL_CUDA(cudaEventRecord(r->freed[slot], st));
+  r->mb->consumed.store(seq, std::memory_order_release);
+}
+
+}  // namespace pl

@@ -16,7 +16,7 @@ HERE = Path(__file__).resolve().parent
 PKG = HERE.parent
 ROOT = PKG.parent
 OUT = PKG / "libpipelive.so"
-SOURCES = ["vmm.cu", "store.cu", "patch.cu", "ipc.cu", "kernels.cu", "attn.cu", "verify.cu", "abi.cu"]
+SOURCES = ["vmm.cu", "store.cu", "patch.cu", "ipc.cu", "kernels.cu", "attn.cu", "verify.cu", "exact.cu", "act.cu", "abi.cu"]
 HEADERS = ["internal.h", "common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -26,6 +26,9 @@ FLAGS = [
     "--expt-relaxed-constexpr",
     "-I", str(ROOT / "include"),
 ]
+
+# exact.cu: no fma contraction beyond the explicit __fma_rn calls (bit-exact vs the oracle)
+EXTRA = {"exact.cu": ["-fmad=false"]}
 
 
 def _stale() -> bool:
@@ -50,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(str(obj))
         if not force and obj.exists() and obj.stat().st_mtime > max(hdr_t, (HERE / src).stat().st_mtime):
             continue
-        cmd = [NVCC, *FLAGS, "-c", str(HERE / src), "-o", str(obj)]
+        cmd = [NVCC, *FLAGS, *EXTRA.get(src, []), "-c", str(HERE / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         jobs.append(cmd)

@@ -564,6 +564,30 @@ struct Patch {
 };
 
 // ---------------------------------------------------------------------------
+// K7 activation rings between stage processes (act.cu)
+struct ActRing;
+ActRing* act_ring_create(int device, int64_t slot_bytes, int n_slots);
+void act_ring_export(ActRing* r, void* out, int64_t cap, int64_t* n_out);
+ActRing* act_ring_open(int device, const void* blob, int64_t n);
+void act_ring_destroy(ActRing* r);
+void act_send(ActRing* r, const void* src, int64_t bytes, cudaStream_t st);
+void act_recv(ActRing* r, void* dst, int64_t bytes, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// exact mode (exact.cu): deterministic fp64 stage compute of the tiny Llama
+void exact_gemv(const double* x, const double* w, const double* resid, double* out, int B, int I,
+                int O, cudaStream_t st);
+void exact_rmsnorm(const double* x, const double* g, double* out, int B, int d, double eps,
+                   cudaStream_t st);
+void exact_rope_pack(const double* q, const double* k, const double* v, const double* cos_t,
+                     const double* sin_t, double* q_out, void* cells, int B, int n_q, int n_kv, int D,
+                     cudaStream_t st);
+void exact_silu_mul(const double* a, const double* b, double* out, int64_t n, cudaStream_t st);
+void exact_attn(Store* s, int group, int layer, const int32_t* rows, const int32_t* ctx,
+                const double* q, double* out, int B, int n_q, int n_kv, int D, double scale,
+                int max_ctx, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
 // kernel launchers (kernels.cu)
 struct WriteLaunch {
   // items

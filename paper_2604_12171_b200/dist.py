@@ -12,9 +12,10 @@
   PatchReceiver.receive, migrator.py:208-273, 93-132): sender drains rows + K3 ->
   receiver reserves the positions with the reference's block-id policy and publishes
   its table -> sender pushes (K4+K5) -> sender's stream is synchronised -> "applied".
-- ``StageLink``: stage-to-stage activations (engine.py:353-375, fabric.py:129-136) as
-  point-to-point send/recv on a torch.distributed group: NCCL moves device tensors over
-  NVLink, gloo stages them through host memory (CPU tests).
+- ``StageLink`` / ``ActRing``: stage-to-stage activations (engine.py:353-375,
+  fabric.py:129-136, K7): by default device-to-device through a ring the receiving stage
+  owns (csrc/act.cu: CUDA IPC buffers + interprocess events + a shared-memory mailbox);
+  NCCL isend/irecv or gloo (host-staged, CPU tests) as alternatives.
 """
 
 from __future__ import annotations
@@ -322,32 +323,131 @@ class PatchSender:
         self.remote.close()
 
 
-class StageLink:
-    """Stage-to-stage activations on a torch.distributed group (K7)."""
+class ActRing:
+    """A K7 activation ring (pl_act_ring, csrc/act.cu): device slots owned by the
+    receiving stage, written by the sending stage, handed over with interprocess events
+    and a shared-memory mailbox -- device to device, no host staging, no stream sync."""
 
-    def __init__(self, group=None) -> None:
+    def __init__(self, h, device: int) -> None:
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def create(cls, device: int, slot_bytes: int, n_slots: int = 4) -> "ActRing":
+        h = C.c_void_p()
+        N.check(N.lib().pl_act_ring_create(device, slot_bytes, n_slots, C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def open(cls, device: int, blob: bytes) -> "ActRing":
+        buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        h = C.c_void_p()
+        N.check(N.lib().pl_act_ring_open(device, buf, len(blob), C.byref(h)))
+        return cls(h, device)
+
+    def export(self) -> bytes:
+        n = C.c_int64()
+        N.check(N.lib().pl_act_ring_export(self.h, None, 0, C.byref(n)))
+        buf = (C.c_ubyte * n.value)()
+        N.check(N.lib().pl_act_ring_export(self.h, buf, n.value, C.byref(n)))
+        return bytes(buf)
+
+    def send(self, t, stream_ptr: int) -> None:
+        N.check(N.lib().pl_act_send(self.h, C.c_void_p(t.data_ptr()), t.numel() * t.element_size(),
+                                    C.c_void_p(stream_ptr)))
+
+    def recv(self, t, stream_ptr: int) -> None:
+        N.check(N.lib().pl_act_recv(self.h, C.c_void_p(t.data_ptr()), t.numel() * t.element_size(),
+                                    C.c_void_p(stream_ptr)))
+
+    def close(self) -> None:
+        if self.h is not None:
+            N.lib().pl_act_ring_destroy(self.h)
+            self.h = None
+
+
+class StageLink:
+    """Stage-to-stage activations (K7, engine.py:353-375, fabric.py:129-136).
+
+    mode "ring" (default): one ActRing per directed stage pair, created lazily by the
+    receiver and handed to the sender over a local Channel -- device-to-device copies
+    ordered on the stages' streams (NVLink between GPUs, HBM when they share one).
+    mode "nccl": isend/irecv on the NCCL group (the stream waits, not the host).
+    mode "gloo": blocking send/recv staged through host memory (CPU tests only)."""
+
+    def __init__(self, group=None, mode: str | None = None, prefix: str = "pl",
+                 device: int = 0, slot_bytes: int = 8 << 20) -> None:
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
         self.backend = dist.get_backend(group)
+        self.mode = mode or os.environ.get("PL_ACT_MODE", "ring")
+        self.rank = dist.get_rank(group)
+        self.prefix = prefix
+        self.device = device
+        self.slot_bytes = slot_bytes
+        self.rings: dict = {}    # (src, dst) -> ActRing
+        self._keep = []          # tensors an in-flight NCCL isend still reads
+        self.sent_bytes = 0
+
+    def _stream(self) -> int:
+        import torch
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _ring(self, src: int, dst: int) -> ActRing:
+        key = (src, dst)
+        r = self.rings.get(key)
+        if r is None:
+            name = f"{self.prefix}-act-{src}-{dst}"
+            if dst == self.rank:   # the receiver owns the ring
+                chan = Channel(name, server=True)
+                r = ActRing.create(self.device, self.slot_bytes)
+                chan.send(("ring", r.export()))
+            else:
+                chan = Channel(name, server=False)
+                msg, _ = chan.recv()
+                assert msg[0] == "ring", msg[0]
+                r = ActRing.open(self.device, msg[1])
+            chan.close()
+            self.rings[key] = r
+        return r
 
     def send(self, t, dst: int) -> None:
-        if self.backend == "nccl":
-            self.dist.send(t.contiguous(), dst, group=self.group)
+        t = t.contiguous()
+        self.sent_bytes += t.numel() * t.element_size()
+        if self.mode == "ring":
+            self._ring(self.rank, dst).send(t, self._stream())
+            self._keep = [t]          # the copy on the stream reads it
+        elif self.backend == "nccl":
+            self._keep = [t]
+            self.dist.isend(t, dst, group=self.group)
         else:
-            self.dist.send(t.detach().to("cpu").contiguous(), dst, group=self.group)
+            self.dist.send(t.detach().to("cpu"), dst, group=self.group)
 
     def recv(self, shape, dtype, src: int, device):
         import torch
 
+        if self.mode == "ring":
+            t = torch.empty(shape, dtype=dtype, device=device)
+            self._ring(src, self.rank).recv(t, self._stream())
+            return t
         if self.backend == "nccl":
             t = torch.empty(shape, dtype=dtype, device=device)
-            self.dist.recv(t, src, group=self.group)
+            self.dist.irecv(t, src, group=self.group).wait()   # the stream waits, not the host
             return t
         t = torch.empty(shape, dtype=dtype)
         self.dist.recv(t, src, group=self.group)
         return t.to(device)
+
+    @property
+    def host_staged(self) -> bool:
+        return self.mode != "ring" and self.backend != "nccl"
+
+    def close(self) -> None:
+        for r in self.rings.values():
+            r.close()
+        self.rings.clear()
 
 
 class RingPair:

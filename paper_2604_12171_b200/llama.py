@@ -77,6 +77,14 @@ def init_weights(cfg: LlamaConfig, seed: int = 0) -> dict[str, np.ndarray]:
     return w
 
 
+def _vp(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _vp_stream(stream):
+    return C.c_void_p(stream.cuda_stream)
+
+
 def pipeline_order(owner: dict[int, int]) -> list[int]:
     """GPUs that hold layers, in pipeline order (by their first layer); a GPU with no
     layers (the zero-layer extension) is not a stage."""
@@ -99,11 +107,26 @@ def layer_moves(owner: dict[int, int], target: dict[int, list[int]]) -> dict[tup
     return dict(sorted(moves.items()))
 
 
+def rope_tables(pos, head_dim: int, theta: float) -> tuple[np.ndarray, np.ndarray]:
+    """Exact mode's RoPE cos/sin [B, D/2] (float64, numpy) for positions pos [B]."""
+    inv = 1.0 / (theta ** (np.arange(0, head_dim, 2, dtype=np.float64) / head_dim))
+    ang = np.asarray(pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.ascontiguousarray(np.cos(ang)), np.ascontiguousarray(np.sin(ang))
+
+
 class LlamaCompute:
-    """The math of one decode step, layer by layer, over whichever store owns a layer."""
+    """The math of one decode step, layer by layer, over whichever store owns a layer.
+
+    Two numerics modes share the KV path (K1 writes into the paged stores, attention over
+    their block tables):
+      - default: fp32 dense layers (cuBLAS via torch), K2 tensor-core attention (bf16);
+      - exact=True: every op a deterministic fp64 kernel of csrc/exact.cu (sequential fma
+        dot products, fixed exp), bit-identical to the CPU oracle (oracle/llama_exact.c),
+        so generated token ids are checked exactly; same bf16 rounding points (K, V, q,
+        attention output)."""
 
     def __init__(self, cfg: LlamaConfig, weights: dict[str, np.ndarray], device: int,
-                 registry: RequestRegistry, stream, layers=None) -> None:
+                 registry: RequestRegistry, stream, layers=None, exact: bool = False) -> None:
         """`layers` (1-based, default all): which layers' weights go to the device now;
         the embedding, final norm and LM head always do."""
         import torch
@@ -112,18 +135,31 @@ class LlamaCompute:
         self.cfg = cfg
         self.registry = registry
         self.stream = stream
+        self.exact = exact
+        self.act_dtype = torch.float64 if exact else torch.float32
         dev = torch.device("cuda", device)
         keep = None if layers is None else {f"l{l - 1}" for l in layers}
 
         def wanted(k: str) -> bool:   # per-layer keys are "l<i>.<name>"
             return keep is None or "." not in k or k.split(".", 1)[0] in keep
 
-        self.w = {k: torch.from_numpy(v).to(dev) for k, v in weights.items() if wanted(k)}
+        self.w = {k: self.to_device(v, dev) for k, v in weights.items() if wanted(k)}
+
+    def to_device(self, v, dev):
+        t = self.torch.from_numpy(np.asarray(v)) if isinstance(v, np.ndarray) else v
+        return t.to(device=dev, dtype=self.act_dtype)
 
     def begin(self, rids: list, positions: list[int], device) -> dict:
         """Per-step state: request rows, context lengths after this token, RoPE tables."""
         torch, c = self.torch, self.cfg
         handles = [self.registry.handle(r) for r in rids]
+        if self.exact:
+            cos, sin = rope_tables(positions, c.head_dim, c.rope_theta)
+            ctx_host = [p + 1 for p in positions]
+            return {"rids": rids, "handles": handles, "ctx_host": ctx_host,
+                    "ctx": torch.tensor(ctx_host, dtype=torch.int32, device=device),
+                    "rows": torch.tensor(handles, dtype=torch.int32, device=device),
+                    "cos": torch.from_numpy(cos).to(device), "sin": torch.from_numpy(sin).to(device)}
         pos = torch.tensor(positions, device=device)
         inv = 1.0 / (c.rope_theta ** (torch.arange(0, c.head_dim, 2, device=device,
                                                    dtype=torch.float64) / c.head_dim))
@@ -137,18 +173,66 @@ class LlamaCompute:
                                    device=device)}
 
     def _rmsnorm(self, x, g):
+        if self.exact:
+            out = self.torch.empty_like(x)
+            N.check(N.lib().pl_exact_rmsnorm(_vp(x), _vp(g), _vp(out), x.shape[0], x.shape[1],
+                                             float(self.cfg.eps), _vp_stream(self.stream)))
+            return out
         var = x.double().pow(2).mean(-1, keepdim=True)
         return (x / (var + self.cfg.eps).sqrt()).float() * g
+
+    def _gemv(self, x, w, resid=None):
+        """exact mode: out = resid + x @ w, sequential fma chains (pl_exact_gemv)"""
+        out = self.torch.empty(x.shape[0], w.shape[1], dtype=self.torch.float64, device=x.device)
+        N.check(N.lib().pl_exact_gemv(_vp(x), _vp(w), _vp(resid) if resid is not None else None,
+                                      _vp(out), x.shape[0], x.shape[1], w.shape[1],
+                                      _vp_stream(self.stream)))
+        return out
 
     def embed(self, tokens):
         return self.w["embed"][tokens]
 
     def head(self, x):
+        if self.exact:
+            return self._gemv(self._rmsnorm(x, self.w["final_norm"]), self.w["lm_head"])
         return self._rmsnorm(x, self.w["final_norm"]) @ self.w["lm_head"]
+
+    def _layer_exact(self, li: int, x, st: KvStore, sc: dict):
+        """Exact mode of layer(): the same K1 write / paged attention, deterministic fp64."""
+        torch, c, w = self.torch, self.cfg, self.w
+        B = len(sc["rids"])
+        lib, stream = N.lib(), _vp_stream(self.stream)
+        h = self._rmsnorm(x, w[f"l{li}.attn_norm"])
+        q = self._gemv(h, w[f"l{li}.wq"])
+        k = self._gemv(h, w[f"l{li}.wk"])
+        v = self._gemv(h, w[f"l{li}.wv"])
+        q_r = torch.empty_like(q)
+        kv = torch.empty(B, 2 * c.n_kv * c.head_dim, dtype=torch.bfloat16, device=x.device)
+        N.check(lib.pl_exact_rope_pack(_vp(q), _vp(k), _vp(v), _vp(sc["cos"]), _vp(sc["sin"]),
+                                       _vp(q_r), _vp(kv), B, c.n_q, c.n_kv, c.head_dim, stream))
+        seeds = [stable_hash(r, li) for r in sc["rids"]]
+        done = append_batch(st, sc["handles"], [li] * B, [1] * B, seeds, kv_dev=kv.data_ptr(),
+                            mark=True)
+        assert done == B
+        att = torch.empty_like(q_r)
+        N.check(lib.pl_exact_attn_decode(st._h, li, 0, _vp(q_r), _vp(att), _vp(sc["rows"]),
+                                         _vp(sc["ctx"]), B, c.n_q, c.n_kv, c.head_dim,
+                                         float(c.head_dim) ** -0.5, max(sc["ctx_host"]), stream))
+        x = self._gemv(att, w[f"l{li}.wo"], x)
+        h = self._rmsnorm(x, w[f"l{li}.mlp_norm"])
+        a = self._gemv(h, w[f"l{li}.w1"])
+        g = self._gemv(h, w[f"l{li}.w3"])
+        m = torch.empty_like(a)
+        N.check(lib.pl_exact_silu_mul(_vp(a), _vp(g), _vp(m), a.numel(), stream))
+        x = self._gemv(m, w[f"l{li}.w2"], x)
+        sc.setdefault("keep", []).append((kv, q_r, att))  # alive until the stream consumed them
+        return x
 
     def layer(self, li: int, x, st: KvStore, sc: dict):
         """Layer li (0-based): K/V of the new tokens into `st` by K1 (fused dirty mark),
         K2 attention over `st`'s block table, then the dense parts."""
+        if self.exact:
+            return self._layer_exact(li, x, st, sc)
         torch, c, w = self.torch, self.cfg, self.w
         B = len(sc["rids"])
         cos, sin, out = sc["cos"], sc["sin"], sc["out"]
@@ -185,7 +269,8 @@ class StagedLlama:
 
     def __init__(self, cfg: LlamaConfig, weights: dict[str, np.ndarray],
                  config: dict[int, list[int]], device: int = 0, tokens_per_block: int = 16,
-                 capacity_blocks: int = 256, registry: RequestRegistry | None = None) -> None:
+                 capacity_blocks: int = 256, registry: RequestRegistry | None = None,
+                 exact: bool = False) -> None:
         import torch
 
         self.torch = torch
@@ -197,7 +282,8 @@ class StagedLlama:
         # one non-default stream for the whole stage loop: torch ops, K1, K2 and the patch
         # rounds are ordered by it (callers run model code under `with model.on_stream()`)
         self.stream = torch.cuda.Stream(device=device)
-        self.compute = LlamaCompute(cfg, weights, device, self.registry, self.stream)
+        self.compute = LlamaCompute(cfg, weights, device, self.registry, self.stream,
+                                    exact=exact)
         self.stores: dict[int, KvStore] = {}
         self.owner: dict[int, int] = {}          # layer (1-based) -> gpu id
         for gpu, layers in config.items():
@@ -405,7 +491,7 @@ class DistStagedLlama:
                  config: dict[int, list[int]], rank: int, device: int = 0,
                  tokens_per_block: int = 16, capacity_blocks: int = 256,
                  registry: RequestRegistry | None = None, channel_prefix: str = "pl",
-                 group=None) -> None:
+                 group=None, exact: bool = False, act_mode: str | None = None) -> None:
         import torch
 
         from .dist import StageLink
@@ -419,11 +505,11 @@ class DistStagedLlama:
         self.group = group
         self.registry = registry or RequestRegistry()
         self.stream = torch.cuda.Stream(device=device)
-        self.link = StageLink(group)
+        self.link = StageLink(group, mode=act_mode, prefix=channel_prefix, device=device)
         self.owner = {l: g for g, ls in config.items() for l in ls}
         own_layers = [l for l, g in self.owner.items() if g == self.gpu]
         self.compute = LlamaCompute(cfg, weights, device, self.registry, self.stream,
-                                    layers=own_layers)
+                                    layers=own_layers, exact=exact)
         # every layer's weights sit in pinned host memory; arriving layers are staged on
         # a copy engine during the migration and gate the switch (coordinator.py:239-240)
         from .staging import LayerWeightStager
@@ -448,6 +534,11 @@ class DistStagedLlama:
     def on_stream(self):
         return self.torch.cuda.stream(self.stream)
 
+    def close(self) -> None:
+        """Release the activation rings (after every rank finished stepping)."""
+        self.stream.synchronize()
+        self.link.close()
+
     def _order(self) -> list[int]:
         return pipeline_order(self.owner)
 
@@ -463,12 +554,15 @@ class DistStagedLlama:
             if i == 0:
                 x = self.compute.embed(torch.tensor(tokens, dtype=torch.long, device=dev))
             else:
-                self.stream.synchronize()
-                x = self.link.recv((B, c.d_model), torch.float32, order[i - 1] - 1, dev)
+                if self.link.host_staged:
+                    self.stream.synchronize()
+                # device path: the stage's stream waits for the previous stage's copy
+                x = self.link.recv((B, c.d_model), self.compute.act_dtype, order[i - 1] - 1, dev)
             for l in sorted(l for l, g in self.owner.items() if g == self.gpu):
                 x = self.compute.layer(l - 1, x, self.store, sc)
             if i + 1 < len(order):
-                self.stream.synchronize()
+                if self.link.host_staged:
+                    self.stream.synchronize()
                 self.link.send(x, order[i + 1] - 1)
             else:
                 nxt = self.compute.head(x).argmax(-1).cpu()
@@ -531,7 +625,8 @@ class DistStagedLlama:
         for (src, dst), layers in self.moving.items():
             if dst == self.gpu:
                 for l in layers:
-                    self.compute.w.update(self.stager.resident[l])
+                    self.compute.w.update({k: t.to(self.compute.act_dtype)
+                                           for k, t in self.stager.resident[l].items()})
         self.pump()                     # residual patch of every pair
         for pair in self._pairs():
             if pair in self.senders:

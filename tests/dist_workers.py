@@ -1,5 +1,7 @@
-"""Stage processes of tests/test_gpu_dist_llama.py: three ranks on cuda:0, gloo for
-activations (NCCL needs distinct GPUs), the cross-process push for KV patches."""
+"""Stage processes of tests/test_gpu_dist_llama.py: ranks on cuda:0; activations move
+device to device through the K7 rings (csrc/act.cu; gloo only carries the step's token
+ids and the lag all-reduce), KV patches through the cross-process push; the stage
+compute runs in exact mode so the tokens can be compared with the CPU oracle."""
 
 import os
 
@@ -20,12 +22,16 @@ def stage(rank, world, port, prefix, q, live):
         from paper_2604_12171_b200.llama import (DistStagedLlama, LlamaConfig, generate_dist,
                                                   init_weights)
         cfg = LlamaConfig()
-        m = DistStagedLlama(cfg, init_weights(cfg, 0), CONF_A, rank, channel_prefix=prefix)
+        m = DistStagedLlama(cfg, init_weights(cfg, 0), CONF_A, rank, channel_prefix=prefix,
+                            exact=True)
         outs = generate_dist(m, PROMPTS, JOINS, N_GEN,
                              reconfig=(10, CONF_B) if live else None,
                              switch_at=("converged" if live == "converged" else 20) if live else None)
-        q.put((rank, outs, sorted(m.store.resident_groups)))
+        q.put((rank, outs, sorted(m.store.resident_groups),
+               {"mode": m.link.mode, "host_staged": m.link.host_staged,
+                "sent_bytes": m.link.sent_bytes}))
         dist.barrier()
+        m.close()
         dist.destroy_process_group()
     except Exception:
         import traceback
@@ -51,13 +57,17 @@ def stage8(rank, world, port, prefix, q, live):
         from paper_2604_12171_b200.llama import (DistStagedLlama, LlamaConfig, generate_dist,
                                                   init_weights)
         cfg = LlamaConfig(n_layers=16)
-        m = DistStagedLlama(cfg, init_weights(cfg, 1), CONF_EVEN8, rank, channel_prefix=prefix)
+        m = DistStagedLlama(cfg, init_weights(cfg, 1), CONF_EVEN8, rank, channel_prefix=prefix,
+                            exact=True)
         t0 = time.perf_counter()
         outs = generate_dist(m, PROMPTS, JOINS, N_GEN,
                              reconfig=(8, CONF_UNEVEN8) if live else None,
                              switch_at=16 if live else None)
-        q.put((rank, outs, sorted(m.store.resident_groups), time.perf_counter() - t0))
+        q.put((rank, outs, sorted(m.store.resident_groups), time.perf_counter() - t0,
+               {"mode": m.link.mode, "host_staged": m.link.host_staged,
+                "sent_bytes": m.link.sent_bytes}))
         dist.barrier()
+        m.close()
         dist.destroy_process_group()
     except Exception:
         import traceback

@@ -23,15 +23,47 @@ CONF_A = {1: [1, 2], 2: [3, 4]}
 CONF_B = {1: [1], 2: [2, 3], 3: [4]}
 
 
-def _run(reconfig=None, switch_at=None, record=None, s=16):
+def _run(reconfig=None, switch_at=None, record=None, s=16, exact=False):
     from paper_2604_12171_b200.llama import LlamaConfig, StagedLlama, generate, init_weights
 
     cfg = LlamaConfig()
     w = init_weights(cfg, seed=0)
-    m = StagedLlama(cfg, w, CONF_A, tokens_per_block=s)
+    m = StagedLlama(cfg, w, CONF_A, tokens_per_block=s, exact=exact)
     outs = generate(m, PROMPTS, JOINS, N_GEN, reconfig=reconfig, switch_at=switch_at,
                     record=record)
     return m, outs, cfg, w
+
+
+@pytest.fixture(scope="module")
+def oracle_tokens():
+    """Greedy tokens of the CPU oracle in exact arithmetic (oracle/llama_exact.c)."""
+    from oracle.llama import ExactOracleLlama
+    from paper_2604_12171_b200.llama import LlamaConfig, init_weights
+
+    cfg = LlamaConfig()
+    return ExactOracleLlama(cfg, init_weights(cfg, seed=0)).generate(PROMPTS, JOINS, N_GEN)
+
+
+@pytest.mark.parametrize("s,switch_at", [(16, 20), (8, 20), (16, "converged"), (16, None)])
+def test_exact_mode_token_ids_bit_exact_vs_oracle(oracle_tokens, s, switch_at):
+    """North star: generated token ids bit-exact against the CPU oracle.  In exact mode
+    (csrc/exact.cu: fp64, sequential fma chains, fixed exp, the production bf16 rounding
+    points) the GPU's logits equal the oracle's BIT FOR BIT at every step -- through the
+    paged KV, K1 writes and a live PP 2 -> 3 reconfiguration (bulk copy, patch rounds,
+    switch) -- so every token id is the oracle's."""
+    from oracle.llama import ExactOracleLlama
+
+    rec = []
+    reconfig = (10, CONF_B) if switch_at is not None else None
+    m, outs, cfg, w = _run(reconfig=reconfig, switch_at=switch_at, record=rec, s=s, exact=True)
+    assert outs == oracle_tokens
+    if reconfig:
+        assert m.config() == CONF_B and m.patched_bytes > 0
+    ora = ExactOracleLlama(cfg, w)
+    for rids, toks, poss, logits in rec:
+        want = ora.step(rids, np.array(toks), np.array(poss))
+        assert logits.dtype == np.float64
+        assert np.array_equal(logits.view(np.uint64), want.view(np.uint64)), (rids, poss)
 
 
 def test_live_reconfig_keeps_tokens_bit_identical():
