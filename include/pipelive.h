@@ -131,6 +131,14 @@ int pl_store_append_batch_payloads(pl_store* st, int n_items, const int32_t* req
                                    const uint64_t* payloads_host, int mark, int* n_done);
 int pl_store_write_slots(pl_store* st, int32_t req, int group, int64_t n,
                          const int64_t* positions_host, const uint64_t* payloads_host);
+/* one layer's cells of already-appended positions (a decoder stacking k > 1 layers per
+ * group computes layer j's K/V only after layers 0..j-1; the group's KvStore.append --
+ * blocks, fingerprint, dirty mark -- is done once with layer 0's).  Item i writes kv_dev +
+ * i * kv_stride_bytes into (req_rows_dev[i], positions_dev[i]).  Contract: enqueued before
+ * the next drain of a patch streaming the group (the mark was set by the append). */
+int pl_store_write_layer(pl_store* st, int group, int layer_in_group, const int32_t* req_rows_dev,
+                         const int32_t* positions_dev, int n, const void* kv_dev,
+                         int64_t kv_stride_bytes, void* stream);
 
 /* ---- reads: lookup (kvstore.py:229-237), read_checksum (kvstore.py:239-245),
  *      snapshot_group (kvstore.py:331-343) */

@@ -25,10 +25,17 @@ def f32_to_bf16(x: np.ndarray) -> np.ndarray:
 
 
 def decode_attention(q: np.ndarray, k: list[np.ndarray], v: list[np.ndarray],
-                     scale: float) -> np.ndarray:
-    """q [B, n_q, D] fp32; k[b], v[b] [ctx_b, n_kv, D] fp32 -> out [B, n_q, D] fp32."""
+                     scale: float, with_atol: bool = False):
+    """q [B, n_q, D] fp32; k[b], v[b] [ctx_b, n_kv, D] fp32 -> out [B, n_q, D] fp32.
+
+    with_atol: also the elementwise absolute slack of a bf16 kernel, 2^-7 * E_p[|v|]
+    (the softmax-weighted mean of |v| per output element): the kernel rounds P to bf16
+    (2^-9 relative per weight, in numerator and denominator), which moves an output by
+    up to ~2^-8 * E_p[|v|] whatever the output's own magnitude (cancellation), and
+    rounds the output to bf16 (2^-9 relative, inside the 2e-2 relative term)."""
     B, n_q, D = q.shape
     out = np.zeros((B, n_q, D), dtype=np.float32)
+    atol = np.zeros((B, n_q, D), dtype=np.float32)
     for b in range(B):
         kb, vb = k[b], v[b]
         if kb.shape[0] == 0:
@@ -41,7 +48,8 @@ def decode_attention(q: np.ndarray, k: list[np.ndarray], v: list[np.ndarray],
             s = s - s.max()
             p = np.exp(s.astype(np.float64)).astype(np.float32)
             out[b, h] = (p[:, None] * vb[:, kv, :]).sum(0) / p.sum()
-    return out
+            atol[b, h] = 2.0 ** -7 * (p[:, None] * np.abs(vb[:, kv, :])).sum(0) / p.sum()
+    return (out, atol) if with_atol else out
 
 
 def gather_paged(pool: np.ndarray, unit_bytes: int, fp_bytes: int, s: int, layer: int,

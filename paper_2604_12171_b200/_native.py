@@ -79,6 +79,7 @@ SIGNATURES = [
                                         P(C.c_int), vp, C.c_int]),
     ("pl_store_append_batch_payloads", C.c_int, [vp, C.c_int, vp, vp, vp, vp, C.c_int, P(C.c_int)]),
     ("pl_store_write_slots", C.c_int, [vp, i32, C.c_int, i64, vp, vp]),
+    ("pl_store_write_layer", C.c_int, [vp, C.c_int, C.c_int, vp, vp, C.c_int, vp, i64, vp]),
     ("pl_store_lookup", C.c_int, [vp, i32, C.c_int, i64, P(u64), P(i64)]),
     ("pl_store_read_checksum", C.c_int, [vp, i32, C.c_int, i64, P(u64)]),
     ("pl_store_read_fps", C.c_int, [vp, C.c_int, vp, i64, vp]),

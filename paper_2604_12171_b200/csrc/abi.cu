@@ -651,6 +651,41 @@ int pl_patch_device_drained_async(pl_patch* p, int64_t* pinned_out) {
 }
 
 // ---- K2
+int pl_store_write_layer(pl_store* st, int group, int layer_in_group, const int32_t* req_rows_dev,
+                         const int32_t* positions_dev, int n, const void* kv_dev,
+                         int64_t kv_stride_bytes, void* stream) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    if (group < 0 || group >= s->n_model_groups || !s->materialised[group])
+      pl::fail(PL_E_INVALID, "group has no pool");
+    if (layer_in_group < 0 || layer_in_group >= s->k)
+      pl::fail(PL_E_INVALID, "layer_in_group out of range");
+    if (kv_stride_bytes < s->cell_bytes || kv_stride_bytes % 16)
+      pl::fail(PL_E_INVALID, "kv stride must be >= cell_bytes and 16-B aligned");
+    PL_CUDA(cudaSetDevice(s->device));
+    s->use_group(group);
+    s->flush();
+    cudaStream_t cs = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    cudaEvent_t ev;
+    if (cs != s->stream) {  // the appends (chains, table deltas) are on the store stream
+      PL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      PL_CUDA(cudaEventRecord(ev, s->stream));
+      PL_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+      PL_CUDA(cudaEventDestroy(ev));
+    }
+    pl::launch_write_layer(s->d_table, s->max_chain, req_rows_dev, positions_dev, n,
+                           reinterpret_cast<uint8_t*>(s->group_base(group)), s->s, s->unit_bytes,
+                           s->fp_bytes, s->cell_bytes, layer_in_group,
+                           static_cast<const uint8_t*>(kv_dev), kv_stride_bytes, cs);
+    if (cs != s->stream) {  // a later drain / K6 move on the store stream sees the cells
+      PL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      PL_CUDA(cudaEventRecord(ev, cs));
+      PL_CUDA(cudaStreamWaitEvent(s->stream, ev, 0));
+      PL_CUDA(cudaEventDestroy(ev));
+    }
+  });
+}
+
 int pl_paged_attn_decode(pl_store* st, int group, int layer, const void* q, void* out,
                          const int32_t* rows, const int32_t* ctx, int B, int n_q, int n_kv, int D,
                          float scale, int max_ctx, void* stream) {

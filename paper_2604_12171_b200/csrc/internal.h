@@ -603,6 +603,10 @@ struct WriteLaunch {
   int n_marks; uint32_t* bits[4]; const int32_t* local_of[4]; int G[4];
 };
 void launch_kv_write(const WriteLaunch& w, cudaStream_t st);
+void launch_write_layer(const int32_t* table, int64_t max_chain, const int32_t* rows,
+                        const int32_t* pos, int n, uint8_t* base, int s, int64_t unit_bytes,
+                        int64_t fp_bytes, int64_t cell_bytes, int layer, const uint8_t* kv,
+                        int64_t kv_stride, cudaStream_t st);
 
 void launch_apply_deltas(int32_t* table, int32_t* owner, int32_t* owner_idx,
                          const int64_t* idx, const int32_t* val, const int32_t* which, int64_t n,

@@ -97,6 +97,40 @@ void launch_kv_write(const WriteLaunch& w, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
+// K1b: one layer's cell of already-appended positions (a decoder with k > 1 layers per
+// group produces layer j's K/V only after layers 0..j-1 ran; the group's append -- block
+// manager, fingerprint, dirty mark -- happened with layer 0).  One warp per item.
+__global__ void __launch_bounds__(kWarps * 32)
+write_layer_kernel(const int32_t* table, int64_t max_chain, const int32_t* rows,
+                   const int32_t* pos, int n, uint8_t* base, int s, int64_t unit_bytes,
+                   int64_t fp_bytes, int64_t cell_bytes, int layer, const uint8_t* kv,
+                   int64_t kv_stride) {
+  const int lane = threadIdx.x & 31;
+  const int64_t vecs = cell_bytes >> 4;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t p = pos[i];
+    const int32_t slot = table[(int64_t)rows[i] * max_chain + p / s];
+    if (slot < 0) continue;
+    int4* dst = reinterpret_cast<int4*>(base + (int64_t)slot * unit_bytes + fp_bytes +
+                                        ((int64_t)layer * s + p % s) * cell_bytes);
+    const int4* src = reinterpret_cast<const int4*>(kv + i * kv_stride);
+    for (int64_t v = lane; v < vecs; v += 32) st_stream(dst + v, ld_stream(src + v));
+  }
+}
+void launch_write_layer(const int32_t* table, int64_t max_chain, const int32_t* rows,
+                        const int32_t* pos, int n, uint8_t* base, int s, int64_t unit_bytes,
+                        int64_t fp_bytes, int64_t cell_bytes, int layer, const uint8_t* kv,
+                        int64_t kv_stride, cudaStream_t st) {
+  if (n <= 0) return;
+  write_layer_kernel<<<(unsigned)grid_for(n, kWarps), kWarps * 32, 0, st>>>(
+      table, max_chain, rows, pos, n, base, s, unit_bytes, fp_bytes, cell_bytes, layer, kv,
+      kv_stride);
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
 // block-table / owner-map deltas (host mirror -> device), deduplicated on host
 __global__ void apply_deltas_kernel(int32_t* table, int32_t* owner, int32_t* owner_idx,
                                     const int64_t* idx, const int32_t* val, const int32_t* which,

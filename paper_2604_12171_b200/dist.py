@@ -382,7 +382,11 @@ class StageLink:
         self.dist = dist
         self.group = group
         self.backend = dist.get_backend(group)
-        self.mode = mode or os.environ.get("PL_ACT_MODE", "ring")
+        import torch
+
+        # the device ring needs CUDA; CPU-only processes (gloo tests) stage through host memory
+        self.mode = mode or os.environ.get("PL_ACT_MODE") or (
+            "ring" if torch.cuda.is_available() else self.backend)
         self.rank = dist.get_rank(group)
         self.prefix = prefix
         self.device = device

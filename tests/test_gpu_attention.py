@@ -1,7 +1,9 @@
 """K2 paged-attention decode vs the fp32 numpy oracle (oracle/attention.py).
 
-Tolerance (BASELINE north star): bf16 output within 2e-2 relative of the fp32
-oracle computed on the same bf16 K/V/q values."""
+Tolerance (BASELINE north star), elementwise: |out - ref| <= 2e-2 * |ref| + atol, with
+ref the fp32 oracle on the same bf16 K/V/q values and atol = 2^-7 * E_p[|v|] per output
+element (oracle/attention.py: the bf16 rounding of P moves an output by ~2^-8 of the
+softmax-weighted |v| regardless of the output's own size)."""
 
 import ctypes as C
 
@@ -50,9 +52,9 @@ def _run_case(B, n_q, n_kv, D, s, k, layer, ctxs, seed):
         u = x[:, layer].view(torch.int16).cpu().numpy().view(np.uint16).reshape(-1, 2, n_kv, D)
         ks.append(bf16_to_f32(u[:, 0]))
         vs.append(bf16_to_f32(u[:, 1]))
-    ref = decode_attention(qf, ks, vs, scale)
+    ref, atol = decode_attention(qf, ks, vs, scale, with_atol=True)
     got = bf16_to_f32(out.view(torch.int16).cpu().numpy().view(np.uint16))
-    return got, ref
+    return got, ref, atol
 
 
 @pytest.mark.parametrize("n_q,n_kv,D", [(32, 8, 128), (64, 8, 128), (8, 8, 128),
@@ -60,19 +62,17 @@ def _run_case(B, n_q, n_kv, D, s, k, layer, ctxs, seed):
 @pytest.mark.parametrize("s", [8, 16])
 def test_decode_matches_fp32_oracle(n_q, n_kv, D, s):
     ctxs = [1, 17, 0, 100, 255, 33, 512, 5]
-    got, ref = _run_case(len(ctxs), n_q, n_kv, D, s, 2, 1, ctxs, seed=n_q + D + s)
+    got, ref, atol = _run_case(len(ctxs), n_q, n_kv, D, s, 2, 1, ctxs, seed=n_q + D + s)
     err = np.abs(got - ref)
-    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
-    assert np.all(err <= bound + 1e-3), float(err.max())
+    assert np.all(err <= RTOL * np.abs(ref) + atol), float((err - RTOL * np.abs(ref) - atol).max())
     assert np.all(got[2] == 0)  # empty context -> zeros
 
 
 def test_decode_long_context_split_k():
     ctxs = [2048, 1999, 4096, 64]
-    got, ref = _run_case(len(ctxs), 32, 8, 128, 16, 4, 3, ctxs, seed=7)
+    got, ref, atol = _run_case(len(ctxs), 32, 8, 128, 16, 4, 3, ctxs, seed=7)
     err = np.abs(got - ref)
-    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
-    assert np.all(err <= bound + 1e-3), float(err.max())
+    assert np.all(err <= RTOL * np.abs(ref) + atol), float((err - RTOL * np.abs(ref) - atol).max())
 
 
 @pytest.mark.parametrize("ctxs", [[3, 0, 40], [1] * 7, [0, 0, 0], [5000, 1, 1, 1, 900],
@@ -80,10 +80,9 @@ def test_decode_long_context_split_k():
 def test_decode_ragged_schedules(ctxs):
     """stream-K schedule edge cases: fewer stages than CTAs (empty CTA ranges inside a
     sequence), all-empty batches, one long sequence over many CTAs, B > CTAs."""
-    got, ref = _run_case(len(ctxs), 32, 8, 128, 16, 1, 0, ctxs, seed=len(ctxs))
+    got, ref, atol = _run_case(len(ctxs), 32, 8, 128, 16, 1, 0, ctxs, seed=len(ctxs))
     err = np.abs(got - ref)
-    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
-    assert np.all(err <= bound + 1e-3), float(err.max())
+    assert np.all(err <= RTOL * np.abs(ref) + atol), float((err - RTOL * np.abs(ref) - atol).max())
     for b, c in enumerate(ctxs):
         if c == 0:
             assert np.all(got[b] == 0)
@@ -142,10 +141,10 @@ def test_decode_raw_entry_over_caller_pool(s, poison):
         u = x.view(torch.int16).cpu().numpy().view(np.uint16).reshape(-1, 2, n_kv, D)
         ks.append(bf16_to_f32(u[:, 0]))
         vs.append(bf16_to_f32(u[:, 1]))
-    ref = decode_attention(qf, ks, vs, D ** -0.5)
+    ref, atol = decode_attention(qf, ks, vs, D ** -0.5, with_atol=True)
     got = bf16_to_f32(out.view(torch.int16).cpu().numpy().view(np.uint16))
     err = np.abs(got - ref)
-    assert np.all(err <= RTOL * np.abs(ref).max(axis=-1, keepdims=True) + 1e-3), float(err.max())
+    assert np.all(err <= RTOL * np.abs(ref) + atol), float((err - RTOL * np.abs(ref) - atol).max())
 
 
 @pytest.mark.parametrize("n_q", [32, 64])
@@ -153,10 +152,9 @@ def test_cuda_core_fallback_for_small_blocks(n_q):
     """4-token blocks are outside the tensor-core kernel's envelope (8-token TMA boxes):
     the CUDA-core kernel serves them, with the same tolerance."""
     ctxs = [1, 17, 0, 100, 255, 33]
-    got, ref = _run_case(len(ctxs), n_q, 8, 128, 4, 2, 1, ctxs, seed=n_q)
+    got, ref, atol = _run_case(len(ctxs), n_q, 8, 128, 4, 2, 1, ctxs, seed=n_q)
     err = np.abs(got - ref)
-    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
-    assert np.all(err <= bound + 1e-3), float(err.max())
+    assert np.all(err <= RTOL * np.abs(ref) + atol), float((err - RTOL * np.abs(ref) - atol).max())
     assert np.all(got[2] == 0)
 
 
@@ -196,9 +194,8 @@ def test_decode_full_bench_shape_sampled(n_q):
     qf = bf16_to_f32(q.view(torch.int16).cpu().numpy().view(np.uint16))[pick]
     ks = [bf16_to_f32(keep[b].reshape(-1, 2, n_kv, D)[:, 0]) for b in pick]
     vs = [bf16_to_f32(keep[b].reshape(-1, 2, n_kv, D)[:, 1]) for b in pick]
-    ref = decode_attention(qf, ks, vs, D ** -0.5)
+    ref, atol = decode_attention(qf, ks, vs, D ** -0.5, with_atol=True)
     got = bf16_to_f32(out.view(torch.int16).cpu().numpy().view(np.uint16))[pick]
     err = np.abs(got - ref)
-    bound = RTOL * np.maximum(np.abs(ref), np.abs(ref).max(axis=-1, keepdims=True))
-    assert np.all(err <= bound + 1e-3), float(err.max())
+    assert np.all(err <= RTOL * np.abs(ref) + atol), float((err - RTOL * np.abs(ref) - atol).max())
     st.close()
