@@ -241,6 +241,10 @@ int pl_patch_apply(pl_patch* p, pl_store* dst, const int32_t* rank_of_req, int64
  * no staging; dst may live on a peer device with P2P access) */
 int pl_patch_push(pl_patch* p, pl_store* dst, const int32_t* rank_of_req, int64_t n_rank,
                   int64_t* out_keys, int64_t* out_cells);
+/* host phases of the last pl_patch_push in ms: {adoption wait for lazily mapped pools,
+ * dirty-set snapshot, destination reservation (write_slots chain extension), destination
+ * table flush, K3 enqueue, copy enqueue, total, 1 if the pipelined (chunked) path ran} */
+int pl_patch_last_push_stats(pl_patch* p, double* out8);
 /* verification hooks: device popcount of the live bitmap; keys of the last device drain */
 int pl_patch_device_dirty_count(pl_patch* p, int64_t* out);
 int pl_patch_device_drained(pl_patch* p, int64_t* out);
@@ -264,8 +268,15 @@ int pl_store_export_group(pl_store* st, int group, int* fds_out, int cap, int* n
                           int64_t* chunk_bytes_out);
 int pl_store_export_table(pl_store* st, void* ipc_handle_out, int64_t* max_reqs, int64_t* max_chain);
 int pl_store_table_version(pl_store* st, uint64_t* dev_ptr, int64_t* max_reqs, int64_t* max_chain);
+/* the reservation's table deltas are enqueued on the store's stream: before the sender's
+ * push reads the table, synchronise the stream (pl_store_sync) or hand the sender an
+ * event (pl_mailbox_record) its stream waits on */
 int pl_store_reserve_rows(pl_store* st, int64_t n_rows, const int32_t* reqs, const int32_t* groups,
                           const int64_t* starts, const int64_t* ends, int64_t* items_done);
+/* the streams work is enqueued on (cudaStream_t as void*): the store's, and the patch's
+ * (its side stream, or the source store's) */
+int pl_store_stream(pl_store* st, void** out);
+int pl_patch_stream(pl_patch* p, void** out);
 int pl_remote_create(int device, int tokens_per_block, int stacking_factor, int64_t cell_bytes,
                      int64_t fp_bytes, int64_t unit_bytes, int num_model_groups, pl_remote** out);
 int pl_remote_destroy(pl_remote* r);
@@ -315,6 +326,26 @@ int pl_act_ring_open(int device, const void* blob, int64_t n, pl_act_ring** out)
 int pl_act_ring_destroy(pl_act_ring* r);
 int pl_act_send(pl_act_ring* r, const void* src_dev, int64_t bytes, void* stream);
 int pl_act_recv(pl_act_ring* r, void* dst_dev, int64_t bytes, void* stream);
+
+/* ---- control mailbox between the two processes of a migrating pair (csrc/act.cu): the
+ * per-round handshake of the cross-process patch (MigrationStream._send_patch ->
+ * PatchReceiver.receive, migrator.py:249-273, 93-132) as posts / polls of 64-bit words in
+ * POSIX shared memory (rows, reservation reply, "applied") plus interprocess CUDA events,
+ * so "applied" is a device-side wait of the receiver's stream on the sender's push, not a
+ * host synchronisation.  The receiver creates and exports it (opaque blob), the sender
+ * opens it.  post = release store, wait = acquire poll until word >= at_least (timeout_ms
+ * < 0: forever).  base = the shared region (bytes long) for row payloads. */
+typedef struct pl_mailbox pl_mailbox;
+int pl_mailbox_create(int device, int64_t bytes, int n_events, pl_mailbox** out);
+int pl_mailbox_export(pl_mailbox* m, void* blob_out, int64_t cap, int64_t* n_out);
+int pl_mailbox_open(int device, const void* blob, int64_t n, pl_mailbox** out);
+int pl_mailbox_destroy(pl_mailbox* m);
+int pl_mailbox_base(pl_mailbox* m, void** out, int64_t* bytes);
+int pl_mailbox_post(pl_mailbox* m, int64_t word, uint64_t value);
+int pl_mailbox_wait(pl_mailbox* m, int64_t word, uint64_t at_least, int64_t timeout_ms,
+                    uint64_t* out);
+int pl_mailbox_record(pl_mailbox* m, int event, void* stream);
+int pl_mailbox_stream_wait(pl_mailbox* m, int event, void* stream);
 
 /* ---- exact mode of the tiny Llama stage compute (csrc/exact.cu): deterministic fp64
  * kernels whose every sum is a sequential fma chain in ascending index order and whose exp

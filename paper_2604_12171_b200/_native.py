@@ -92,6 +92,15 @@ SIGNATURES = [
     ("pl_act_ring_destroy", C.c_int, [vp]),
     ("pl_act_send", C.c_int, [vp, vp, i64, vp]),
     ("pl_act_recv", C.c_int, [vp, vp, i64, vp]),
+    ("pl_mailbox_create", C.c_int, [C.c_int, i64, C.c_int, P(vp)]),
+    ("pl_mailbox_export", C.c_int, [vp, vp, i64, P(i64)]),
+    ("pl_mailbox_open", C.c_int, [C.c_int, vp, i64, P(vp)]),
+    ("pl_mailbox_destroy", C.c_int, [vp]),
+    ("pl_mailbox_base", C.c_int, [vp, P(vp), P(i64)]),
+    ("pl_mailbox_post", C.c_int, [vp, i64, u64]),
+    ("pl_mailbox_wait", C.c_int, [vp, i64, u64, i64, P(u64)]),
+    ("pl_mailbox_record", C.c_int, [vp, C.c_int, vp]),
+    ("pl_mailbox_stream_wait", C.c_int, [vp, C.c_int, vp]),
     ("pl_exact_gemv", C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     ("pl_exact_rmsnorm", C.c_int, [vp, vp, vp, C.c_int, C.c_int, dbl, vp]),
     ("pl_exact_rope_pack", C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
@@ -127,6 +136,9 @@ SIGNATURES = [
     ("pl_patch_drained_keys", C.c_int, [vp, vp, vp, vp, i64, P(i64)]),
     ("pl_patch_apply", C.c_int, [vp, vp, vp, i64, vp, i64]),
     ("pl_patch_push", C.c_int, [vp, vp, vp, i64, P(i64), P(i64)]),
+    ("pl_patch_last_push_stats", C.c_int, [vp, vp]),
+    ("pl_patch_stream", C.c_int, [vp, P(vp)]),
+    ("pl_store_stream", C.c_int, [vp, P(vp)]),
     ("pl_patch_device_dirty_count", C.c_int, [vp, P(i64)]),
     ("pl_patch_device_drained", C.c_int, [vp, P(i64)]),
     ("pl_patch_device_drained_async", C.c_int, [vp, vp]),

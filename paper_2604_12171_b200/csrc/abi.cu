@@ -20,6 +20,9 @@ struct pl_remote {
 struct pl_act_ring {
   pl::ActRing* r;
 };
+struct pl_mailbox {
+  pl::MailboxRegion* m;
+};
 
 namespace pl {
 namespace {
@@ -421,6 +424,44 @@ int pl_act_recv(pl_act_ring* r, void* dst_dev, int64_t bytes, void* stream) {
   return guard([&] { pl::act_recv(r->r, dst_dev, bytes, (cudaStream_t)stream); });
 }
 
+int pl_mailbox_create(int device, int64_t bytes, int n_events, pl_mailbox** out) {
+  return guard([&] { *out = new pl_mailbox{pl::mailbox_create(device, bytes, n_events)}; });
+}
+int pl_mailbox_export(pl_mailbox* m, void* blob_out, int64_t cap, int64_t* n_out) {
+  return guard([&] { pl::mailbox_export(m->m, blob_out, cap, n_out); });
+}
+int pl_mailbox_open(int device, const void* blob, int64_t n, pl_mailbox** out) {
+  return guard([&] { *out = new pl_mailbox{pl::mailbox_open(device, blob, n)}; });
+}
+int pl_mailbox_destroy(pl_mailbox* m) {
+  return guard([&] {
+    if (!m) return;
+    pl::mailbox_destroy(m->m);
+    delete m;
+  });
+}
+int pl_mailbox_base(pl_mailbox* m, void** out, int64_t* bytes) {
+  return guard([&] {
+    *out = pl::mailbox_base(m->m, bytes);
+  });
+}
+int pl_mailbox_post(pl_mailbox* m, int64_t word, uint64_t value) {
+  return guard([&] { pl::mailbox_post(m->m, word, value); });
+}
+int pl_mailbox_wait(pl_mailbox* m, int64_t word, uint64_t at_least, int64_t timeout_ms,
+                    uint64_t* out) {
+  return guard([&] {
+    const uint64_t v = pl::mailbox_wait(m->m, word, at_least, timeout_ms);
+    if (out) *out = v;
+  });
+}
+int pl_mailbox_record(pl_mailbox* m, int event, void* stream) {
+  return guard([&] { pl::mailbox_record(m->m, event, (cudaStream_t)stream); });
+}
+int pl_mailbox_stream_wait(pl_mailbox* m, int event, void* stream) {
+  return guard([&] { pl::mailbox_stream_wait(m->m, event, (cudaStream_t)stream); });
+}
+
 int pl_exact_gemv(const double* x, const double* w, const double* resid, double* out, int B,
                   int I, int O, void* stream) {
   return guard([&] { pl::exact_gemv(x, w, resid, out, B, I, O, (cudaStream_t)stream); });
@@ -631,6 +672,18 @@ int pl_patch_apply(pl_patch* p, pl_store* dst, const int32_t* rank, int64_t n_ra
 int pl_patch_push(pl_patch* p, pl_store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
                   int64_t* cells) {
   return guard([&] { live(p)->push(dst->s, rank, n_rank, keys, cells); });
+}
+int pl_patch_stream(pl_patch* p, void** out) {
+  return guard([&] { *out = (void*)live(p)->pstream(); });
+}
+int pl_store_stream(pl_store* st, void** out) {
+  return guard([&] { *out = (void*)st->s->stream; });
+}
+int pl_patch_last_push_stats(pl_patch* p, double* out8) {
+  return guard([&] {
+    pl::Patch* q = live(p);
+    for (int i = 0; i < 8; ++i) out8[i] = q->push_stats[i];
+  });
 }
 int pl_patch_device_dirty_count(pl_patch* p, int64_t* out) {
   return guard([&] { *out = live(p)->device_dirty_count(); });

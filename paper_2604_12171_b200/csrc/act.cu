@@ -237,4 +237,171 @@ void act_recv(ActRing* r, void* dst, int64_t bytes, cudaStream_t st) {
   r->mb->consumed.store(seq, std::memory_order_release);
 }
 
+// ---------------------------------------------------------------------------
+// Mailbox: a shared-memory control region between the two processes of a stage pair
+// (the patch round's rows / reservation reply / "applied" handshake) plus
+// interprocess CUDA events, so the control of a round is a few host stores and polls
+// instead of socket messages, and "applied" is a device-side event wait instead of a
+// host stream synchronisation on the sender.
+struct MailboxRegion {
+  int device = 0, n_events = 0;
+  bool owner = false, ipc = false;
+  int64_t bytes = 0;
+  uint8_t* base = nullptr;
+  std::string shm;
+  cudaEvent_t ev[kMaxSlots] = {};
+};
+namespace {
+struct MailBlob {
+  int32_t magic, pid, device, n_events;
+  int64_t bytes;
+  cudaIpcEventHandle_t ev[kMaxSlots];
+  char shm[64];
+};
+constexpr int32_t kMailMagic = 0x6d61696c;
+std::mutex g_mail_mu;
+std::unordered_map<std::string, MailboxRegion*> g_mail_owned;
+void* map_shm(const std::string& name, int64_t bytes, bool create) {
+  const int fd = shm_open(name.c_str(), create ? (O_CREAT | O_RDWR | O_EXCL) : O_RDWR, 0600);
+  if (fd < 0) fail(PL_E_INVALID, "shm_open failed for " + name);
+  if (create && ftruncate(fd, bytes) != 0) {
+    close(fd);
+    fail(PL_E_INVALID, "ftruncate failed");
+  }
+  void* p = mmap(nullptr, (size_t)bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) fail(PL_E_INVALID, "mmap failed");
+  return p;
+}
+}  // namespace
+
+MailboxRegion* mailbox_create(int device, int64_t bytes, int n_events) {
+  if (n_events < 0 || n_events > kMaxSlots) fail(PL_E_INVALID, "n_events must be 0..8");
+  auto* m = new MailboxRegion();
+  m->device = device;
+  m->n_events = n_events;
+  m->owner = true;
+  m->bytes = std::max<int64_t>(4096, (bytes + 4095) / 4096 * 4096);
+  try {
+    PL_CUDA(cudaSetDevice(device));
+    for (int i = 0; i < n_events; ++i)
+      PL_CUDA(cudaEventCreateWithFlags(&m->ev[i], cudaEventDisableTiming | cudaEventInterprocess));
+    m->shm = "/pl-mail-" + std::to_string(getpid()) + "-" + std::to_string(++g_ring_counter);
+    m->base = static_cast<uint8_t*>(map_shm(m->shm, m->bytes, true));
+    std::memset(m->base, 0, 4096);
+  } catch (...) {
+    mailbox_destroy(m);
+    throw;
+  }
+  std::lock_guard<std::mutex> lk(g_mail_mu);
+  g_mail_owned[m->shm] = m;
+  return m;
+}
+
+void mailbox_export(MailboxRegion* m, void* out, int64_t cap, int64_t* n_out) {
+  if (!m->owner) fail(PL_E_STATE, "only the owner exports a mailbox");
+  *n_out = (int64_t)sizeof(MailBlob);
+  if (cap < (int64_t)sizeof(MailBlob)) return;
+  MailBlob b{};
+  b.magic = kMailMagic;
+  b.pid = (int32_t)getpid();
+  b.device = m->device;
+  b.n_events = m->n_events;
+  b.bytes = m->bytes;
+  PL_CUDA(cudaSetDevice(m->device));
+  for (int i = 0; i < m->n_events; ++i) PL_CUDA(cudaIpcGetEventHandle(&b.ev[i], m->ev[i]));
+  std::strncpy(b.shm, m->shm.c_str(), sizeof(b.shm) - 1);
+  std::memcpy(out, &b, sizeof(b));
+}
+
+MailboxRegion* mailbox_open(int device, const void* blob, int64_t n) {
+  if (n < (int64_t)sizeof(MailBlob)) fail(PL_E_INVALID, "mailbox blob too short");
+  MailBlob b;
+  std::memcpy(&b, blob, sizeof(b));
+  if (b.magic != kMailMagic) fail(PL_E_INVALID, "not a mailbox blob");
+  auto* m = new MailboxRegion();
+  m->device = device;
+  m->n_events = b.n_events;
+  m->bytes = b.bytes;
+  m->shm = b.shm;
+  if (b.pid == (int32_t)getpid()) {  // same process: alias the owner's region and events
+    std::lock_guard<std::mutex> lk(g_mail_mu);
+    auto it = g_mail_owned.find(m->shm);
+    if (it == g_mail_owned.end()) {
+      delete m;
+      fail(PL_E_INVALID, "mailbox owner not found in this process");
+    }
+    m->base = it->second->base;
+    for (int i = 0; i < m->n_events; ++i) m->ev[i] = it->second->ev[i];
+    return m;
+  }
+  m->ipc = true;
+  try {
+    PL_CUDA(cudaSetDevice(device));
+    for (int i = 0; i < m->n_events; ++i) PL_CUDA(cudaIpcOpenEventHandle(&m->ev[i], b.ev[i]));
+    m->base = static_cast<uint8_t*>(map_shm(m->shm, m->bytes, false));
+  } catch (...) {
+    mailbox_destroy(m);
+    throw;
+  }
+  return m;
+}
+
+void mailbox_destroy(MailboxRegion* m) {
+  if (!m) return;
+  if (m->owner) {
+    {
+      std::lock_guard<std::mutex> lk(g_mail_mu);
+      g_mail_owned.erase(m->shm);
+    }
+    cudaSetDevice(m->device);
+    for (int i = 0; i < m->n_events; ++i)
+      if (m->ev[i]) {
+        cudaEventSynchronize(m->ev[i]);
+        cudaEventDestroy(m->ev[i]);
+      }
+    if (m->base) munmap(m->base, (size_t)m->bytes);
+    if (!m->shm.empty()) shm_unlink(m->shm.c_str());
+  } else if (m->ipc) {
+    for (int i = 0; i < m->n_events; ++i)
+      if (m->ev[i]) cudaEventDestroy(m->ev[i]);
+    if (m->base) munmap(m->base, (size_t)m->bytes);
+  }
+  delete m;
+}
+
+void* mailbox_base(MailboxRegion* m, int64_t* bytes) {
+  *bytes = m->bytes;
+  return m->base;
+}
+
+void mailbox_post(MailboxRegion* m, int64_t word, uint64_t v) {
+  if (word < 0 || (word + 1) * 8 > m->bytes) fail(PL_E_INVALID, "mailbox word out of range");
+  reinterpret_cast<std::atomic<uint64_t>*>(m->base)[word].store(v, std::memory_order_release);
+}
+
+uint64_t mailbox_wait(MailboxRegion* m, int64_t word, uint64_t at_least, int64_t timeout_ms) {
+  if (word < 0 || (word + 1) * 8 > m->bytes) fail(PL_E_INVALID, "mailbox word out of range");
+  auto& c = reinterpret_cast<std::atomic<uint64_t>*>(m->base)[word];
+  using Clock = std::chrono::steady_clock;
+  const auto t0 = Clock::now();
+  uint64_t v;
+  for (uint64_t spin = 0; (v = c.load(std::memory_order_acquire)) < at_least; ++spin) {
+    if (spin > 4000) sched_yield();
+    if ((spin & 1023) == 1023 && timeout_ms >= 0 &&
+        Clock::now() - t0 > std::chrono::milliseconds(timeout_ms))
+      fail(PL_E_STATE, "mailbox: peer did not post in time");
+  }
+  return v;
+}
+
+void mailbox_record(MailboxRegion* m, int i, cudaStream_t st) {
+  if (i < 0 || i >= m->n_events) fail(PL_E_INVALID, "mailbox event out of range");
+  PL_CUDA(cudaEventRecord(m->ev[i], st));
+}
+void mailbox_stream_wait(MailboxRegion* m, int i, cudaStream_t st) {
+  if (i < 0 || i >= m->n_events) fail(PL_E_INVALID, "mailbox event out of range");
+  PL_CUDA(cudaStreamWaitEvent(st, m->ev[i], 0));
+}
+
 }  // namespace pl

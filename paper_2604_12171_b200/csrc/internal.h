@@ -559,6 +559,12 @@ struct Patch {
   void drain_rows(const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells);
   void push_remote(Remote* r, int64_t n_items_applied);
   int64_t device_dirty_count();
+  bool fused_round() const;  // K3 + push in one launch for sparse rounds
+  void device_drain_push(Store* dst, const std::vector<uint8_t>* mask);
+  // host phases of the last push (ms): adoption wait for lazily mapped pools, dirty-set
+  // snapshot, destination reservation, destination table flush, K3 enqueue, copy enqueue,
+  // total, chunked (1) or not (0)
+  double push_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int32_t* d_groups_ = nullptr;
   const int32_t* d_groups();
 };
@@ -572,6 +578,17 @@ ActRing* act_ring_open(int device, const void* blob, int64_t n);
 void act_ring_destroy(ActRing* r);
 void act_send(ActRing* r, const void* src, int64_t bytes, cudaStream_t st);
 void act_recv(ActRing* r, void* dst, int64_t bytes, cudaStream_t st);
+// shared-memory control mailbox + interprocess events between two stage processes
+struct MailboxRegion;
+MailboxRegion* mailbox_create(int device, int64_t bytes, int n_events);
+void mailbox_export(MailboxRegion* m, void* out, int64_t cap, int64_t* n_out);
+MailboxRegion* mailbox_open(int device, const void* blob, int64_t n);
+void mailbox_destroy(MailboxRegion* m);
+void* mailbox_base(MailboxRegion* m, int64_t* bytes);
+void mailbox_post(MailboxRegion* m, int64_t word, uint64_t v);
+uint64_t mailbox_wait(MailboxRegion* m, int64_t word, uint64_t at_least, int64_t timeout_ms);
+void mailbox_record(MailboxRegion* m, int i, cudaStream_t st);
+void mailbox_stream_wait(MailboxRegion* m, int i, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // exact mode (exact.cu): deterministic fp64 stage compute of the tiny Llama
@@ -653,6 +670,9 @@ struct CopyLaunch {
   uint8_t* rows; int32_t* keys; int64_t row_bytes;
 };
 void launch_copy(const CopyLaunch& c, cudaStream_t st);
+// K3 + fused push in one launch for sparse rounds
+void launch_drain_push(const CopyLaunch& c, uint32_t* bits, int64_t n_words, int64_t* count,
+                       int64_t* next_count, cudaStream_t st);
 
 void launch_read_fps(uint64_t base, int64_t unit_bytes, const int32_t* slots, int64_t n, int s,
                      uint64_t* out, cudaStream_t st);

@@ -184,8 +184,10 @@ int64_t Store::reserve_rows(int64_t n_rows, const int32_t* reqs, const int32_t* 
     ++items;
     i = j;
   }
+  // the table deltas go out on the store's stream; the sending process reads the table
+  // next: the caller orders that (a host sync, or an interprocess event the sender's
+  // stream waits on -- dist.PatchReceiver)
   flush();
-  PL_CUDA(cudaStreamSynchronize(stream));  // the table is read by another process next
   return items;
 }
 

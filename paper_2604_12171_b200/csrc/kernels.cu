@@ -462,6 +462,120 @@ __global__ void __launch_bounds__(kWarps * 32) copy_kernel(CopyLaunch c) {
   }
 }
 
+// K3 + K4/K5 fused for sparse (steady) rounds, one persistent launch (a few hundred CTAs:
+// launching thousands of short CTAs cost more than the copies).  A CTA takes 256 bitmap
+// words at a time: every thread snapshots + clears one word (atomicExch, as K3) and the set
+// bits go into a shared-memory queue (ballot / popc per warp); then the whole CTA copies the
+// queued cells pool -> pool through the destination's table (as copy_kernel<2>): the k
+// layers of a cell (16 KB for the Llama shapes) are 4 16-B vectors per thread, in flight at
+// once.  Dense rounds (many bits per word) keep K3 + copy_kernel<2> (kFusedMinKeys).
+constexpr int kFusedWords = 256;
+__global__ void __launch_bounds__(256)
+drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, unsigned long long* count,
+                  unsigned long long* next_count) {
+  __shared__ uint16_t queue[kFusedWords * 32];
+  __shared__ int q_n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *next_count = 0ull;
+  const int lane = threadIdx.x & 31;
+  const int64_t vecs = c.cell_bytes >> 4;
+  const int64_t total = (int64_t)c.k * vecs;
+  const int64_t per_slot = (int64_t)c.G * c.src_s;
+  unsigned long long drained = 0;
+  for (int64_t base = (int64_t)blockIdx.x * kFusedWords; base < n_words;
+       base += (int64_t)gridDim.x * kFusedWords) {
+    if (threadIdx.x == 0) q_n = 0;
+    __syncthreads();
+    const int64_t wi = base + threadIdx.x;
+    uint32_t v = 0;
+    if (wi < n_words) {
+      v = bits[wi];
+      if (v) v = atomicExch(bits + wi, 0u);
+    }
+    const int cnt = __popc(v);
+    drained += cnt;
+    int incl = cnt;  // warp prefix of the bit counts -> one shared atomicAdd per warp
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
+    int start = 0;
+    if (lane == 31 && wtotal) start = atomicAdd(&q_n, wtotal);
+    start = __shfl_sync(0xffffffffu, start, 31) + incl - cnt;
+    while (v) {
+      const int b = __ffs(v) - 1;
+      v &= v - 1;
+      queue[start++] = (uint16_t)(threadIdx.x * 32 + b);
+    }
+    __syncthreads();
+    const int n = q_n;
+    for (int qi = 0; qi < n; ++qi) {
+      const int64_t cell = base * 32 + queue[qi];
+      const int32_t slot = (int32_t)(cell / per_slot);
+      const int64_t rem = cell % per_slot;
+      const int32_t lg = (int32_t)(rem / c.src_s);
+      const int off = (int)(rem % c.src_s);
+      const int32_t req = c.src_owner[slot];
+      if (req < 0) continue;
+      if (c.apply_mask && !c.apply_mask[(int64_t)req * c.G + lg]) continue;
+      const int64_t pos = (int64_t)c.src_owner_idx[slot] * c.src_s + off;
+      const int32_t dslot = c.dst_table[(int64_t)req * c.dst_max_chain + pos / c.dst_s];
+      if (dslot < 0) continue;
+      const int doff = (int)(pos % c.dst_s);
+      const uint8_t* su = reinterpret_cast<const uint8_t*>(c.src_bases[c.src_groups[lg]]) +
+                          (int64_t)slot * c.src_unit;
+      uint8_t* du = reinterpret_cast<uint8_t*>(c.dst_bases[c.src_groups[lg]]) +
+                    (int64_t)dslot * c.dst_unit;
+      if (threadIdx.x == 0)
+        reinterpret_cast<uint64_t*>(du)[doff] = reinterpret_cast<const uint64_t*>(su)[off];
+      su += c.fp_bytes;
+      du += c.fp_bytes;
+      constexpr int U = 4;
+      int64_t x = threadIdx.x;
+      for (; x + 256 * (U - 1) < total; x += 256 * U) {
+        int4 buf[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t e = x + 256 * u;
+          const int j = (int)(e / vecs);
+          buf[u] = ld_stream(reinterpret_cast<const int4*>(
+                                 su + ((int64_t)j * c.src_s + off) * c.cell_bytes) + (e - j * vecs));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t e = x + 256 * u;
+          const int j = (int)(e / vecs);
+          st_stream(reinterpret_cast<int4*>(du + ((int64_t)j * c.dst_s + doff) * c.cell_bytes) +
+                        (e - j * vecs), buf[u]);
+        }
+      }
+      for (; x < total; x += 256) {
+        const int j = (int)(x / vecs);
+        st_stream(reinterpret_cast<int4*>(du + ((int64_t)j * c.dst_s + doff) * c.cell_bytes) +
+                      (x - j * vecs),
+                  ld_stream(reinterpret_cast<const int4*>(
+                                su + ((int64_t)j * c.src_s + off) * c.cell_bytes) + (x - j * vecs)));
+      }
+    }
+    __syncthreads();  // the queue is rebuilt for the next 256 words
+  }
+  for (int o = 16; o; o >>= 1) drained += __shfl_xor_sync(0xffffffffu, drained, o);
+  if (lane == 0 && drained) atomicAdd(count, drained);
+}
+
+void launch_drain_push(const CopyLaunch& c, uint32_t* bits, int64_t n_words, int64_t* count,
+                       int64_t* next_count, cudaStream_t st) {
+  const int64_t chunks = (n_words + kFusedWords - 1) / kFusedWords;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)sm_count() * 2));
+  KernelTimer timer("drain_push", st);
+  drain_push_kernel<<<(unsigned)grid, 256, 0, st>>>(
+      c, bits, n_words, reinterpret_cast<unsigned long long*>(count),
+      reinterpret_cast<unsigned long long*>(next_count));
+  note_launch();
+  PL_CUDA(cudaGetLastError());
+}
+
 void launch_copy(const CopyLaunch& c, cudaStream_t st) {
   if (c.n_hint <= 0) return;
   const int64_t grid = grid_for(c.n_hint * c.k, kWarps, 16);

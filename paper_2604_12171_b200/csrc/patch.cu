@@ -141,12 +141,21 @@ void Patch::ensure_bits() {
 // (PL_PUSH_CHUNK_MIN_BLOCKS overrides it, read per round: the tests force tiny runs;
 // PL_PUSH_NO_CHUNK=1 turns the pipelining off for A/B timing)
 constexpr int64_t kChunkedPushMinBlocks = 8192;
+// sparse-round threshold of the fused drain + push: up to max(this, 2 keys per 256-word
+// chunk of the bitmap) -- the decode pattern of small batches
+constexpr int64_t kFusedMinKeys = 128;
 static int64_t chunk_min_blocks() {
   const char* v = std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS");
   return v ? std::max<int64_t>(1, std::atoll(v)) : kChunkedPushMinBlocks;
 }
 static bool no_chunking() { return std::getenv("PL_PUSH_NO_CHUNK") != nullptr; }
 static bool forced_chunking() { return std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS") != nullptr; }
+// PL_PUSH_NO_LAUNCH_FIRST=1: reserve on the host before launching even when no destination
+// block is allocated (A/B timing of the steady-round reordering)
+static bool launch_first_off() {
+  static const bool off = std::getenv("PL_PUSH_NO_LAUNCH_FIRST") != nullptr;
+  return off;
+}
 
 static int64_t insert_interval(std::vector<Interval>& v, int64_t a, int64_t b) {
   // merge [a,b) into sorted disjoint v (adjacent intervals merge); returns newly covered
@@ -650,10 +659,15 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
 }
 
 void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells) {
+  auto clk = [] { return std::chrono::steady_clock::now(); };
+  auto dms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto ta = clk();
+  for (double& v : push_stats) v = 0;
   for (int i = 0; i < G; ++i) {  // lazily mapped pools are adopted before any copy
     src->use_group(groups[i]);
     dst->use_group(groups[i]);
   }
+  push_stats[0] = dms(ta, clk());  // waited for a lazily mapped pool (adoption)
   if (in_flight) fail(PL_E_STATE, "a drained patch of this pair is still in flight");
   if (dst->k != src->k || dst->cell_bytes != src->cell_bytes)
     fail(PL_E_INVALID, "source and destination layouts differ");
@@ -667,26 +681,82 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   take_drained();
   *keys = drained_keys;
   *cells = host_cells(drained);
-  if (drained.size() >= 2 && !no_chunking() && (forced_chunking() || streams_idle(dst)) &&
-      new_dst_blocks(dst) >= chunk_min_blocks()) {
+  const int64_t new_blocks = new_dst_blocks(dst);
+  if (drained.size() >= 2 && !no_chunking() && new_blocks >= chunk_min_blocks() &&
+      (forced_chunking() || streams_idle(dst))) {
+    push_stats[1] = ms(t0, now());
     push_chunked(dst, rank, n_rank);
+    push_stats[6] = ms(ta, now());
+    push_stats[7] = 1;
     return;
   }
   std::vector<uint8_t> mask;
   int status = PL_OK;
+  bool dst_pools = true;
+  for (int32_t g : groups) dst_pools = dst_pools && dst->materialised[g];
+  if (new_blocks == 0 && dst_pools && drained_keys > 0 && !launch_first_off()) {
+    // Steady round whose positions all have destination blocks already (chains extend only
+    // every s tokens): the device needs nothing from the host reservation -- no new table
+    // entries, no KvOverflow possible -- so K3 + the push launch first and the host
+    // bookkeeping of write_slots (occupancy, written, kvstore.py:201-227) runs while the
+    // copy does.  Block ids and counters are those of the unreordered round.
+    const auto t1 = now();
+    PL_CUDA(cudaSetDevice(dst->device));
+    dst->flush();
+    PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
+    PL_CUDA(cudaSetDevice(src->device));
+    if (fused_round()) {
+      device_drain_push(dst, nullptr);
+    } else {
+      device_drain_compact();
+      if (pstream() != src->stream) {
+        PL_CUDA(cudaEventRecord(ev_src, src->stream));
+        PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
+      }
+      PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
+      launch_copy(push_launch(dst, nullptr, 0), pstream());
+      PL_CUDA(cudaEventRecord(ev_applied, pstream()));
+      applied_recorded = true;
+      PL_CUDA(cudaSetDevice(dst->device));
+      PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
+    }
+    const auto t2 = now();
+    extend_dst(dst, rank, n_rank, nullptr, 0, mask, &status);
+    drained.clear();
+    if (status != PL_OK) fail(status, "steady round: unexpected reservation failure");
+    push_stats[1] = ms(t0, t1);
+    push_stats[4] = ms(t1, t2);
+    push_stats[2] = ms(t2, now());
+    push_stats[6] = ms(ta, now());
+    return;
+  }
   const auto t1 = now();
   extend_dst(dst, rank, n_rank, nullptr, 0, mask, &status);
   drained.clear();
   const auto t2 = now();
   PL_CUDA(cudaSetDevice(dst->device));
   dst->flush();
+  push_stats[1] = ms(t0, t1);
+  push_stats[2] = ms(t1, t2);
+  push_stats[3] = ms(t2, now());
   if (trace)
     std::fprintf(stderr, "[pl] push: take %.3f ms, extend_dst %.3f ms, dst flush %.3f ms (%lld keys)\n",
                  ms(t0, t1), ms(t1, t2), ms(t2, now()), (long long)drained_keys);
   PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
   PL_CUDA(cudaSetDevice(src->device));
   const auto t3 = now();
+  if (fused_round()) {
+    // sparse round: K3 and the push in one launch (drain_push_kernel)
+    device_drain_push(dst, status == PL_OK ? nullptr : &mask);
+    push_stats[4] = ms(t3, now());
+    push_stats[5] = 0;
+    push_stats[6] = ms(ta, now());
+    if (status != PL_OK) fail(status, dst->last_msg);
+    return;
+  }
   device_drain_compact();
+  push_stats[4] = ms(t3, now());
+  const auto t4 = now();
   if (trace)
     std::fprintf(stderr, "[pl] push: K3 enqueue (src flush + 3 launches) %.3f ms\n", ms(t3, now()));
   if (drained_keys > 0 && !mask.empty()) {
@@ -704,7 +774,48 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   applied_recorded = true;
   PL_CUDA(cudaSetDevice(dst->device));
   PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
+  push_stats[5] = ms(t4, now());
+  push_stats[6] = ms(ta, now());
   if (status != PL_OK) fail(status, dst->last_msg);
+}
+
+// sparse rounds (a few keys per bitmap word at most: the decode pattern, low dirty rates)
+// take the fused drain + push; PL_PUSH_NO_FUSED=1 turns it off for A/B timing
+bool Patch::fused_round() const {
+  static const bool off = std::getenv("PL_PUSH_NO_FUSED") != nullptr;
+  static const int64_t max_keys = [] {
+    const char* v = std::getenv("PL_PUSH_FUSED_MAX_KEYS");
+    return v ? std::atoll(v) : (int64_t)-1;
+  }();
+  // about two keys per 256-word chunk: the persistent CTAs copy their queues serially
+  const int64_t lim =
+      max_keys >= 0 ? max_keys : std::max<int64_t>(kFusedMinKeys, 2 * ((n_words + 255) / 256));
+  return !off && drained_keys > 0 && drained_keys <= lim;
+}
+
+void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask) {
+  src->flush();
+  cudaStream_t ps = pstream();
+  uint32_t* old = d_bits;  // epoch flip, as device_drain_compact
+  std::swap(d_bits, d_bits_alt);
+  if (snap_recorded && ps != src->stream) PL_CUDA(cudaStreamWaitEvent(src->stream, ev_snap, 0));
+  if (ps != src->stream) {
+    PL_CUDA(cudaEventRecord(ev_src, src->stream));
+    PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
+  }
+  const uint8_t* d_apply = mask ? stage_mask(*mask) : nullptr;
+  PL_CUDA(cudaStreamWaitEvent(ps, ev_dst, 0));
+  for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);
+  cnt_cur ^= 1;
+  d_count = d_cnt + cnt_cur;
+  launch_drain_push(push_launch(dst, d_apply, 0), old, n_words, d_count, d_cnt + (cnt_cur ^ 1), ps);
+  PL_CUDA(cudaEventRecord(ev_snap, ps));
+  snap_recorded = true;
+  PL_CUDA(cudaEventRecord(ev_applied, ps));
+  applied_recorded = true;
+  PL_CUDA(cudaSetDevice(dst->device));
+  PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
+  PL_CUDA(cudaSetDevice(src->device));
 }
 
 int64_t Patch::device_dirty_count() {

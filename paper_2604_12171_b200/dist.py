@@ -186,10 +186,16 @@ class PatchReceiver:
     """Destination half of a cross-process pair: maps the migrating groups, exports
     them, and serves patch rounds until the sender closes the pair."""
 
-    def __init__(self, store: KvStore, groups, chan: Channel) -> None:
+    def __init__(self, store: KvStore, groups, chan: Channel, mailbox: bool | None = None) -> None:
         self.store = store
         self.groups = sorted(groups)
         self.chan = chan
+        # the round's control over a shared-memory mailbox (default) or socket messages
+        # (PL_PATCH_SOCKET=1, the round-1 protocol kept for A/B timing)
+        if mailbox is None:
+            mailbox = os.environ.get("PL_PATCH_SOCKET") is None
+        self.mb = Mailbox.create(store.device) if mailbox else None
+        self.seq = 0
         store.resident_groups |= set(self.groups)
         self._send_hello()
         self.rounds = 0
@@ -205,9 +211,22 @@ class PatchReceiver:
         table = export_table(self.store)
         self._pools = self._pool_state()
         self._table = table_version(self.store)
-        self.chan.send(("hello", store_layout(self.store), meta, table), fds)
+        self.chan.send(("hello", store_layout(self.store), meta, table,
+                        self.mb.export() if self.mb is not None else None), fds)
         for fd in fds:
             os.close(fd)
+
+    def _updates(self) -> tuple[dict, list[int]]:
+        update, fds = {}, []
+        if table_version(self.store) != self._table:
+            update["table"] = export_table(self.store)
+            self._table = table_version(self.store)
+            self.table_reexports += 1
+        if self._pool_state() != self._pools:
+            update["pools"], fds = export_groups(self.store, self.groups)
+            self._pools = self._pool_state()
+            self.pool_reexports += 1
+        return update, fds
 
     def serve(self) -> bool:
         """One round; False once the sender closed the pair."""
@@ -218,6 +237,8 @@ class PatchReceiver:
 
     def serve_rows(self) -> bool:
         """First half of a round: reserve the drained rows, publish table/pool updates."""
+        if self.mb is not None:
+            return self._serve_rows_mailbox()
         msg, _ = self.chan.recv()
         if msg[0] == "close":
             return False
@@ -227,6 +248,7 @@ class PatchReceiver:
         rc = N.lib().pl_store_reserve_rows(self.store._h, len(reqs), N.ptr(reqs), N.ptr(groups),
                                            N.ptr(a), N.ptr(b), C.byref(done))
         err = None if rc == N.PL_OK else (rc, N.lib().pl_last_error().decode(errors="replace"))
+        self.store.sync()   # the table is read by the sending process next
         update, fds = {}, []
         if table_version(self.store) != self._table:
             update["table"] = export_table(self.store)
@@ -244,10 +266,47 @@ class PatchReceiver:
         self._err = err
         return True
 
+    def _serve_rows_mailbox(self) -> bool:
+        mb = self.mb
+        self.seq += 1
+        mb.wait(W_ROWS, self.seq)
+        if mb.words[W_CLOSE]:
+            return False
+        n = int(mb.words[W_NROWS])
+        done = C.c_int64()
+        # the rows are read in place from the shared region
+        rc = N.lib().pl_store_reserve_rows(self.store._h, n, N.ptr(mb.reqs), N.ptr(mb.groups),
+                                           N.ptr(mb.a), N.ptr(mb.b), C.byref(done))
+        err = None if rc == N.PL_OK else (rc, N.lib().pl_last_error().decode(errors="replace"))
+        update, fds = self._updates()
+        # the sender's push reads the table deltas just enqueued: it waits for this event
+        mb.record(EV_RESERVED, self.store.stream_ptr())
+        mb.words[W_DONE] = done.value
+        mb.words[W_ERR] = np.uint64(rc & 0xFFFFFFFFFFFFFFFF)
+        if err is not None:
+            msg = err[1].encode()[:255]
+            np.ctypeslib.as_array((C.c_ubyte * 256).from_address(mb.base + 8 * W_MSG))[:len(msg) + 1] = \
+                np.frombuffer(msg + b"\0", dtype=np.uint8)
+        mb.words[W_UPDATE] = 1 if update else 0
+        if update:   # rare (a reallocated table, re-mapped pools): over the socket
+            self.chan.send(("update", update), fds)
+            for fd in fds:
+                os.close(fd)
+        mb.post(W_REPLY, self.seq)
+        self.rounds += 1
+        self.items_reserved += done.value
+        self._err = err
+        return True
+
     def serve_ack(self) -> None:
-        """Second half: the sender's cells are in this store once "applied" arrives."""
-        ack, _ = self.chan.recv()
-        assert ack[0] == "applied", ack[0]
+        """Second half: the sender's cells are in this store once "applied" arrives
+        (mailbox: this store's stream waits on the device for the sender's push)."""
+        if self.mb is not None:
+            self.mb.wait(W_APPLIED, self.seq)
+            self.mb.stream_wait(EV_APPLIED, self.store.stream_ptr())
+        else:
+            ack, _ = self.chan.recv()
+            assert ack[0] == "applied", ack[0]
         if self._err is not None:
             from .kvstore import _ERRORS
             err, self._err = self._err, None
@@ -266,10 +325,12 @@ class PatchSender:
         self.patch = NativePatch(store, groups, layers_per_group)
         msg, fds = chan.recv()
         assert msg[0] == "hello", msg[0]
-        _, layout, meta, (th, mr, mc) = msg
+        _, layout, meta, (th, mr, mc), mb_blob = msg
         self.remote = RemoteStore(store.device, layout)
         self.remote.import_groups(meta, fds)
         self.remote.set_table(th, mr, mc)
+        self.mb = Mailbox.open(store.device, mb_blob) if mb_blob is not None else None
+        self.seq = 0
         self.keys = self.cells = 0
 
     def seed(self) -> int:
@@ -288,24 +349,57 @@ class PatchSender:
         N.check(N.lib().pl_patch_drain_rows(self.patch.h, N.ptr(rank), len(rank), C.byref(keys),
                                             C.byref(cells), C.byref(n)))
         m = n.value
+        self._pending = (keys.value, cells.value)
+        if self.mb is not None:
+            mb = self.mb
+            if m > mb.cap:
+                raise N.NativeError(N.PL_E_INVALID, f"{m} rows exceed the mailbox ({mb.cap})")
+            # rows straight into the shared region, then one release store
+            N.check(N.lib().pl_patch_rows(self.patch.h, N.ptr(mb.reqs), N.ptr(mb.groups),
+                                          N.ptr(mb.a), N.ptr(mb.b), m))
+            mb.words[W_NROWS] = m
+            self.seq += 1
+            mb.post(W_ROWS, self.seq)
+            return
         rows = (np.empty(m, np.int32), np.empty(m, np.int32), np.empty(m, np.int64),
                 np.empty(m, np.int64))
         N.check(N.lib().pl_patch_rows(self.patch.h, *(N.ptr(x) for x in rows), m))
         self.chan.send(("rows", rows))
-        self._pending = (keys.value, cells.value)
 
     def finish(self) -> tuple[int, int]:
         """Receive the reservation, push the cells into the remote pools, acknowledge."""
-        msg, fds = self.chan.recv()
-        assert msg[0] == "reserved", msg[0]
-        _, done, err, update = msg
+        if self.mb is not None:
+            mb = self.mb
+            mb.wait(W_REPLY, self.seq)
+            done = int(mb.words[W_DONE])
+            rc = int(np.int64(mb.words[W_ERR]))
+            err = None
+            if rc != N.PL_OK:
+                raw = bytes(np.ctypeslib.as_array((C.c_ubyte * 256).from_address(mb.base + 8 * W_MSG)))
+                err = (rc, raw.split(b"\0", 1)[0].decode(errors="replace"))
+            update, fds = {}, []
+            if mb.words[W_UPDATE]:
+                (tag, update), fds = self.chan.recv()
+                assert tag == "update", tag
+        else:
+            msg, fds = self.chan.recv()
+            assert msg[0] == "reserved", msg[0]
+            _, done, err, update = msg
         if "pools" in update:
             self.remote.import_groups(update["pools"], fds)
         if "table" in update:
             self.remote.set_table(*update["table"])
+        if self.mb is not None:   # the push reads the table deltas of the reservation
+            self.mb.stream_wait(EV_RESERVED, self.patch.stream_ptr())
         N.check(N.lib().pl_patch_push_remote(self.patch.h, self.remote.h, done))
-        self.store.sync()   # the cells are in the receiver's HBM before it is told so
-        self.chan.send(("applied",))
+        if self.mb is not None:
+            # "applied" = an interprocess event after the push on the patch stream: the
+            # receiver's stream waits for it on the device; no host sync here
+            self.mb.record(EV_APPLIED, self.patch.stream_ptr())
+            self.mb.post(W_APPLIED, self.seq)
+        else:
+            self.store.sync()   # the cells are in the receiver's HBM before it is told so
+            self.chan.send(("applied",))
         if err is not None:
             from .kvstore import _ERRORS
             raise _ERRORS.get(err[0], N.NativeError)(err[1])
@@ -318,7 +412,14 @@ class PatchSender:
         return self.patch.dirty_keys()
 
     def close(self) -> None:
-        self.chan.send(("close",))
+        if self.mb is not None:
+            self.mb.words[W_CLOSE] = 1
+            self.seq += 1
+            self.mb.post(W_ROWS, self.seq)
+            self.store.sync()     # every push into the remote pools ran before unmapping them
+            self.mb.close()
+        else:
+            self.chan.send(("close",))
         self.patch.close()
         self.remote.close()
 
@@ -364,6 +465,73 @@ class ActRing:
         if self.h is not None:
             N.lib().pl_act_ring_destroy(self.h)
             self.h = None
+
+
+class Mailbox:
+    """pl_mailbox (csrc/act.cu): POSIX shared memory between the two processes of a pair
+    plus interprocess CUDA events.  Words 0..63 are control words; the rest is a row area."""
+
+    ROWS_OFF = 512
+
+    def __init__(self, h, device: int) -> None:
+        self.h = h
+        self.device = device
+        base, n = C.c_void_p(), C.c_int64()
+        N.check(N.lib().pl_mailbox_base(h, C.byref(base), C.byref(n)))
+        self.base, self.bytes = base.value, n.value
+        self.cap = (self.bytes - self.ROWS_OFF) // 24
+        off = self.base + self.ROWS_OFF
+        self.reqs = np.ctypeslib.as_array((C.c_int32 * self.cap).from_address(off))
+        self.groups = np.ctypeslib.as_array((C.c_int32 * self.cap).from_address(off + 4 * self.cap))
+        self.a = np.ctypeslib.as_array((C.c_int64 * self.cap).from_address(off + 8 * self.cap))
+        self.b = np.ctypeslib.as_array((C.c_int64 * self.cap).from_address(off + 16 * self.cap))
+        self.words = np.ctypeslib.as_array((C.c_uint64 * 64).from_address(self.base))
+
+    @classmethod
+    def create(cls, device: int, rows: int = 1 << 18, n_events: int = 2) -> "Mailbox":
+        h = C.c_void_p()
+        N.check(N.lib().pl_mailbox_create(device, cls.ROWS_OFF + 24 * rows, n_events, C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def open(cls, device: int, blob: bytes) -> "Mailbox":
+        buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        h = C.c_void_p()
+        N.check(N.lib().pl_mailbox_open(device, buf, len(blob), C.byref(h)))
+        return cls(h, device)
+
+    def export(self) -> bytes:
+        n = C.c_int64()
+        N.check(N.lib().pl_mailbox_export(self.h, None, 0, C.byref(n)))
+        buf = (C.c_ubyte * n.value)()
+        N.check(N.lib().pl_mailbox_export(self.h, buf, n.value, C.byref(n)))
+        return bytes(buf)
+
+    def post(self, word: int, value: int) -> None:
+        N.check(N.lib().pl_mailbox_post(self.h, word, value))
+
+    def wait(self, word: int, at_least: int, timeout_ms: int = 300_000) -> int:
+        out = C.c_uint64()
+        N.check(N.lib().pl_mailbox_wait(self.h, word, at_least, timeout_ms, C.byref(out)))
+        return out.value
+
+    def record(self, event: int, stream_ptr: int) -> None:
+        N.check(N.lib().pl_mailbox_record(self.h, event, C.c_void_p(stream_ptr)))
+
+    def stream_wait(self, event: int, stream_ptr: int) -> None:
+        N.check(N.lib().pl_mailbox_stream_wait(self.h, event, C.c_void_p(stream_ptr)))
+
+    def close(self) -> None:
+        if self.h is not None:
+            N.lib().pl_mailbox_destroy(self.h)
+            self.h = None
+
+
+# control words of a patch pair's mailbox
+W_ROWS, W_REPLY, W_APPLIED, W_NROWS, W_DONE, W_ERR, W_UPDATE, W_CLOSE = range(8)
+W_MSG = 8            # words 8..39: error message bytes (256 B)
+EV_APPLIED = 0       # interprocess event: the sender's push of the round (sender records)
+EV_RESERVED = 1      # interprocess event: the receiver's table deltas of the round
 
 
 class StageLink:

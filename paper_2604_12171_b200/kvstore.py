@@ -496,6 +496,12 @@ class KvStore:
         _check(N.lib().pl_store_append(self._h, h, layer_group, n_tokens, N.PL_PAYLOAD_SEED,
                                        None, seed, kv_dev, 1 if mark else 0))
 
+    def stream_ptr(self) -> int:
+        """The cudaStream_t this store's work is enqueued on."""
+        out = C.c_void_p()
+        _check(N.lib().pl_store_stream(self._h, C.byref(out)))
+        return out.value or 0
+
     def wait_for_caller_stream(self, stream_ptr: int | None = None) -> None:
         """Order the store's stream after the caller's (default: torch's current stream),
         so device buffers the caller just produced (kv_dev) are complete when K1 reads."""

@@ -121,6 +121,22 @@ class NativePatch:
                                       C.byref(cells)))
         return keys.value, cells.value
 
+    def stream_ptr(self) -> int:
+        """The stream this pair's K3/K4/K5 are enqueued on."""
+        out = C.c_void_p()
+        N.check(N.lib().pl_patch_stream(self.h, C.byref(out)))
+        return out.value or 0
+
+    def last_push_stats(self) -> dict:
+        """Host phases of the last push (ms), pl_patch_last_push_stats."""
+        out = np.zeros(8, dtype=np.float64)
+        N.check(N.lib().pl_patch_last_push_stats(self.h, N.ptr(out)))
+        keys = ("adopt_wait", "snapshot", "reserve", "dst_flush", "k3_enqueue", "copy_enqueue",
+                "total")
+        d = {k: round(float(v), 4) for k, v in zip(keys, out)}
+        d["chunked"] = bool(out[7])
+        return d
+
     def mark_batch(self, reqs, groups, starts, counts) -> None:
         r, g = N.as_i32(reqs), N.as_i32(groups)
         st, c = N.as_i64(starts), N.as_i64(counts)
@@ -270,6 +286,7 @@ def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
     th0 = time.perf_counter()
     keys, cells = rig.patch.push(rig.dst, rig.registry.rank())
     host_ms = (time.perf_counter() - th0) * 1e3
+    push_phases = rig.patch.last_push_stats()
     b1.record(side)
     bulk_payload = cells * wl.cell_bytes
     during = [decode_step(True) for _ in range(steps)]
@@ -305,7 +322,7 @@ def c2_live(rig: "PatchRig", stream, steps: int = 6) -> dict:
             "decode_ms_per_step_steady_patching": med(steady_ms),
             "bulk": {"payload_bytes": bulk_payload, "ms": round(bulk_ms, 3),
                      "gbs": round(bulk_payload / bulk_ms / 1e6, 1),
-                     "host_enqueue_ms": round(host_ms, 3)},
+                     "host_enqueue_ms": round(host_ms, 3), "host_phases_ms": push_phases},
             "steady_round_keys": round_keys[-1] if round_keys else 0,
             "switch_pause_ms": round(pause_ms, 4),
             "switch_pause_breakdown_ms": {"drain_in_flight_step": round(drain_ms, 4),
