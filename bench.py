@@ -394,7 +394,7 @@ def main() -> None:
                 "share_of_step": round(push_ms / ms, 4) if ms else None,
                 "drain_ms_per_step": round(drain_ms / max(K, 1), 4)}
 
-    pause = c2 = decode = decode_70b = wstage = resize = None
+    pause = c2 = decode = decode_70b = wstage = resize = act_hop = None
     if not args.only_step:
         # ---- switch pause (data-path part): residual patch after one decode round + barrier
         pause = guarded("switch_pause", lambda: measure_switch_pause(rig, stream, torch, wl))
@@ -415,6 +415,9 @@ def main() -> None:
 
         # ---- resize latency: post-commit cleanup on the source (drop, shrink, regrow)
         resize = guarded("resize", lambda: measure_resize(rig, stream, torch, wl))
+
+        # ---- K7 activation hop through the stage ring
+        act_hop = guarded("act_hop", lambda: measure_act_hop(torch))
 
     # ---- e2e: KV arrives from pinned host memory every step, result read back
     e2e = e2e_kv = None
@@ -477,15 +480,17 @@ def main() -> None:
         "clocks": clocks.summary(),
         "value_cold": value_cold,
         "switch_pause_ms": pause,
+        "act_hop": act_hop,
         "decode": decode,
         "decode_70b_shape": decode_70b,
         "tail": tail_summary(c2_model, c3, resize, decode, decode_70b, pause, value_cold,
-                             hbm_peak),
+                             hbm_peak, act_hop, sweep),
     }
     print(json.dumps(line), flush=True)
 
 
-def tail_summary(c2, c3, resize, decode, decode_70b, pause, value_cold, hbm_peak) -> dict:
+def tail_summary(c2, c3, resize, decode, decode_70b, pause, value_cold, hbm_peak,
+                 act_hop=None, sweep=None) -> dict:
     """The headline extras in one small object at the very end of the line."""
     def get(d, *path):
         for p in path:
@@ -499,7 +504,13 @@ def tail_summary(c2, c3, resize, decode, decode_70b, pause, value_cold, hbm_peak
                          "hbm_frac": get(decode, "roofline", "frac")},
            "decode_70b_shape": {"tokens_per_s": get(decode_70b, "tokens_per_s"),
                                 "hbm_frac": get(decode_70b, "roofline", "frac")},
-           "switch_pause_data_path_ms": get(pause, "median")}
+           "switch_pause_data_path_ms": get(pause, "median"),
+           "act_hop_us": {k: get(act_hop, k, "us_per_hop") for k in ("8b", "70b")}}
+    if isinstance(sweep, list):
+        # steady rounds of the C5 sweep at 16-token blocks: wall vs kernel time
+        out["c5_steady_16tok"] = {r["dirty"]: {"wall_us": round(r["ms"] * 1e3, 1),
+                                               "kernel_us": round(r["kernel_ms"] * 1e3, 1)}
+                                  for r in sweep if r.get("tokens_per_block") == 16}
     if isinstance(c2, dict) and "error" not in c2:
         out["c2_model_8b_live"] = {k: c2.get(k) for k in (
             "tokens_equal_static", "tpot_ms_static", "tpot_ms_before", "tpot_ms_during",
@@ -546,6 +557,50 @@ def measure_c2_model(wl, steps: int = 40, reconfig_at: int = 8) -> dict:
                  "K1 + K2 + the patch engine are this repo's kernels; patch rounds on a "
                  "lowest-priority side stream; TPOT includes the greedy token read-back")
     return s
+
+
+def measure_act_hop(torch, hops: int = 200) -> dict:
+    """K7: one stage-to-stage activation hop through an activation ring (csrc/act.cu) at
+    decode batch B = 256: 2 MiB (8B shape, d = 4096 bf16) and 4 MiB (70B shape, d = 8192).
+    Here both stages are in this process on one GPU, so a hop is two HBM copies (into the
+    receiver's slot, out of it); across GPUs the first one is an NVLink write.  Device time
+    from the first send to the last receive (events), and the host time per send + recv."""
+    from paper_2604_12171_b200.dist import ActRing
+
+    out = {}
+    for name, d in (("8b", 4096), ("70b", 8192)):
+        nbytes = 256 * d * 2
+        owner = ActRing.create(torch.cuda.current_device(), nbytes, n_slots=4)
+        tx = ActRing.open(torch.cuda.current_device(), owner.export())
+        a, b = torch.cuda.Stream(), torch.cuda.Stream()
+        x = torch.randn(256, d, device="cuda").to(torch.bfloat16)
+        y = torch.empty_like(x)
+        torch.cuda.synchronize()
+        for _ in range(8):
+            tx.send(x, a.cuda_stream)
+            owner.recv(y, b.cuda_stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(a)
+        t0 = time.perf_counter()
+        for _ in range(hops):
+            tx.send(x, a.cuda_stream)
+            owner.recv(y, b.cuda_stream)
+        host_us = (time.perf_counter() - t0) / hops * 1e6
+        e1.record(b)
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+        us = e0.elapsed_time(e1) * 1e3 / hops
+        out[name] = {"bytes": nbytes, "us_per_hop": round(us, 2),
+                     "gbs": round(nbytes / us / 1e3, 1),
+                     "hbm_gbs": round(4 * nbytes / us / 1e3, 1),
+                     "host_us_per_hop": round(host_us, 2)}
+        tx.close()
+        owner.close()
+    out["note"] = ("one process, one GPU: hop = copy into the receiver's slot + copy out "
+                   "(hbm_gbs counts both copies' read + write); the stages' streams are "
+                   "ordered by interprocess events, no host sync")
+    return out
 
 
 def measure_switch_pause(rig, stream, torch, wl) -> dict:

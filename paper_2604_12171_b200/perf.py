@@ -554,7 +554,8 @@ def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16,
                 src.sync()
                 times.append(time.perf_counter() - t0)
                 N.check(N.lib().pl_timing_enable(0))
-                dev.append(N.timing("drain")[0] + N.timing("patch_push")[0])
+                dev.append(N.timing("drain")[0] + N.timing("patch_push")[0]
+                           + N.timing("drain_push")[0])
                 keys_n = keys
             t = float(np.median(times[1:]))
             td = float(np.median(dev[1:])) / 1e3
