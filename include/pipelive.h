@@ -347,6 +347,39 @@ int pl_mailbox_wait(pl_mailbox* m, int64_t word, uint64_t at_least, int64_t time
 int pl_mailbox_record(pl_mailbox* m, int event, void* stream);
 int pl_mailbox_stream_wait(pl_mailbox* m, int event, void* stream);
 
+/* ---- one cross-process patch round in four native calls over a pair mailbox (the layout
+ * dist.py uses: control words 0..7 = rows seq, reply seq, applied seq, n rows, items
+ * reserved, status, update flag, close flag; words 8..39 the receiver's error text; rows
+ * from byte 512 as [reqs i32][groups i32][a i64][b i64], cap = (bytes - 512) / 24 each;
+ * event 0 = "applied", event 1 = "reserved").  Replaces MigrationStream._send_patch ->
+ * PatchReceiver.receive -> _apply (migrator.py:249-273, 93-132) for a pair in two processes:
+ *   send_rows  (sender)   pl_patch_drain_rows + the rows into the mailbox + post(rows, seq)
+ *   serve_rows (receiver) wait(rows, seq); closed -> flags 1; pl_store_reserve_rows on the
+ *              rows in place (write_slots, kvstore.py:201-227), record "reserved" on the
+ *              store stream, write items / status; io_versions[2] = (table, pools) hashes
+ *              of what the sender imported -- a change sets flags 2 (table) / 4 (pools)
+ *              and then the reply is NOT posted: the caller sends the re-export and posts;
+ *              flags 8 = served (the reply or the update is due: a non-OK return with
+ *              flags 8 is the reservation's status, without it a failure of the call);
+ *              returns the reservation status (KvOverflow: the items before the failing
+ *              one are served, migrator.py:124-131)
+ *   finish     (sender)   wait(reply, seq); an update not yet imported -> need_update = 1
+ *              and return (import it, call again with update_imported = 1); else the
+ *              patch stream waits for "reserved", pl_patch_push_remote, record "applied",
+ *              post(applied, seq); *rc = the receiver's status
+ *   serve_ack  (receiver) wait(applied, seq); the store stream waits for "applied" */
+int pl_pair_send_rows(pl_patch* p, pl_mailbox* m, const int32_t* rank_of_req, int64_t n_rank,
+                      uint64_t seq, int64_t* out_keys, int64_t* out_cells, int64_t* out_rows);
+int pl_pair_serve_rows(pl_store* st, pl_mailbox* m, const int32_t* groups, int n_groups,
+                       uint64_t seq, int64_t timeout_ms, uint64_t* io_versions, int* out_flags,
+                       int64_t* out_items);
+int pl_pair_finish(pl_patch* p, pl_remote* r, pl_mailbox* m, uint64_t seq, int64_t timeout_ms,
+                   int update_imported, int* out_need_update, int* out_rc, int64_t* out_items);
+int pl_pair_serve_ack(pl_store* st, pl_mailbox* m, uint64_t seq, int64_t timeout_ms);
+/* the (table, pools) hashes pl_pair_serve_rows compares against, as of now (taken when the
+ * receiver exports its table and pools to the sender) */
+int pl_store_export_versions(pl_store* st, const int32_t* groups, int n_groups, uint64_t* out2);
+
 /* ---- exact mode of the tiny Llama stage compute (csrc/exact.cu): deterministic fp64
  * kernels whose every sum is a sequential fma chain in ascending index order and whose exp
  * is a fixed polynomial, so the CPU oracle (oracle/llama_exact.c) reproduces the logits bit

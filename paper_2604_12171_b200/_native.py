@@ -101,6 +101,12 @@ SIGNATURES = [
     ("pl_mailbox_wait", C.c_int, [vp, i64, u64, i64, P(u64)]),
     ("pl_mailbox_record", C.c_int, [vp, C.c_int, vp]),
     ("pl_mailbox_stream_wait", C.c_int, [vp, C.c_int, vp]),
+    ("pl_pair_send_rows", C.c_int, [vp, vp, vp, i64, u64, P(i64), P(i64), P(i64)]),
+    ("pl_pair_serve_rows", C.c_int, [vp, vp, vp, C.c_int, u64, i64, vp, P(C.c_int), P(i64)]),
+    ("pl_pair_finish", C.c_int, [vp, vp, vp, u64, i64, C.c_int, P(C.c_int), P(C.c_int),
+                                 P(i64)]),
+    ("pl_pair_serve_ack", C.c_int, [vp, vp, u64, i64]),
+    ("pl_store_export_versions", C.c_int, [vp, vp, C.c_int, vp]),
     ("pl_exact_gemv", C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     ("pl_exact_rmsnorm", C.c_int, [vp, vp, vp, C.c_int, C.c_int, dbl, vp]),
     ("pl_exact_rope_pack", C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/pipelive.h): exceptions -> status codes, plain
 // pointers in and out, no C++ or torch types across the edge.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <map>
@@ -63,8 +64,147 @@ KernelTimer::~KernelTimer() {
   g_timed[name].push_back({start, end});
 }
 
+// Host bookkeeping worker (internal.h)
+namespace {
+class HostWorker {
+ public:
+  ~HostWorker() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    if (th_.joinable()) th_.join();
+  }
+  void submit(std::function<void()> job, std::vector<const void*> tags) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      if (!th_.joinable()) th_ = std::thread([this] { run(); });
+      for (const void* t : tags) ++busy_[t];
+      q_.push_back({std::move(job), std::move(tags)});
+      pending_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+  }
+  // every job (tags == nullptr) or the jobs touching any of `tags`
+  void join(const void* const* tags = nullptr, int n_tags = 0) {
+    if (pending_.load(std::memory_order_acquire) == 0 && !err_flag_.load()) return;
+    auto idle = [&] {
+      if (!tags) return pending_.load() == 0;
+      for (int i = 0; i < n_tags; ++i) {
+        auto it = busy_.find(tags[i]);
+        if (it != busy_.end() && it->second > 0) return false;
+      }
+      return true;
+    };
+    std::exception_ptr e;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      // the jobs are short (microseconds to a few hundred): spin briefly, then block
+      for (int i = 0; i < 4000 && !idle(); ++i) {
+        lk.unlock();
+        std::this_thread::yield();
+        lk.lock();
+      }
+      done_cv_.wait(lk, idle);
+      e = err_;
+      err_ = nullptr;
+      err_flag_.store(false);
+    }
+    if (e) std::rethrow_exception(e);
+  }
+
+ private:
+  struct Job {
+    std::function<void()> fn;
+    std::vector<const void*> tags;
+  };
+  void run() {
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+      if (q_.empty()) return;
+      Job job = std::move(q_.front());
+      q_.pop_front();
+      lk.unlock();
+      try {
+        job.fn();
+      } catch (...) {
+        std::lock_guard<std::mutex> g(mu_);
+        if (!err_) err_ = std::current_exception();
+        err_flag_.store(true);
+      }
+      lk.lock();
+      for (const void* t : job.tags)
+        if (--busy_[t] == 0) busy_.erase(t);
+      pending_.fetch_sub(1, std::memory_order_release);
+      done_cv_.notify_all();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::deque<Job> q_;
+  std::unordered_map<const void*, int> busy_;  // jobs queued or running per tag
+  std::atomic<int64_t> pending_{0};
+  std::atomic<bool> err_flag_{false};
+  std::exception_ptr err_;
+  bool stop_ = false;
+  std::thread th_;
+};
+HostWorker& host_worker() {
+  static HostWorker* w = new HostWorker();  // never destroyed: no join at static teardown
+  return *w;
+}
+}  // namespace
+
+void host_submit(std::function<void()> job, std::vector<const void*> tags) {
+  host_worker().submit(std::move(job), std::move(tags));
+}
+void host_join() { host_worker().join(); }
+void host_join_tags(std::initializer_list<const void*> tags) {
+  host_worker().join(tags.begin(), (int)tags.size());
+}
+bool host_async_enabled() {
+  static const bool off = std::getenv("PL_SYNC_BOOKKEEPING") != nullptr;
+  return !off;
+}
+
+// every entry point: the pending host bookkeeping lands first
 template <class F>
 int guard(F&& f) {
+  try {
+    host_join();
+    f();
+    return PL_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PL_E_INVALID;
+  }
+}
+// entry points that touch only the stores / patches named: they wait for the bookkeeping
+// jobs tagged with those (a pair's receiver job does not hold up its process's sender)
+template <class F>
+int guard_tags(std::initializer_list<const void*> tags, F&& f) {
+  try {
+    host_join_tags(tags);
+    f();
+    return PL_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PL_E_INVALID;
+  }
+}
+// stream-only entry points (a device sync): they read no host mirror, so they do not
+// wait for the bookkeeping worker -- the bytes of a round are on the device when this
+// returns, its host bookkeeping may still be landing
+template <class F>
+int guard_nojoin(F&& f) {
   try {
     f();
     return PL_OK;
@@ -79,6 +219,8 @@ int guard(F&& f) {
 }  // namespace pl
 
 using pl::guard;
+using pl::guard_nojoin;
+using pl::guard_tags;
 
 extern "C" {
 
@@ -579,7 +721,8 @@ int pl_store_flush(pl_store* st) {
   return guard([&] { st->s->flush(); });
 }
 int pl_store_sync(pl_store* st) {
-  return guard([&] {
+  return guard_nojoin([&] {
+    // deltas are only queued by the caller's thread (the worker never adds any)
     st->s->flush();
     PL_CUDA(cudaStreamSynchronize(st->s->stream));
   });
@@ -594,6 +737,8 @@ int pl_patch_create(pl_store* src, const int32_t* groups, const int32_t* layers,
     *out = new pl_patch{p};
   });
 }
+static const void* patch_of(pl_patch* p) { return p ? (const void*)p->p : nullptr; }
+static const void* src_of(pl_patch* p) { return p && p->p ? (const void*)p->p->src : nullptr; }
 static pl::Patch* live(pl_patch* p) {
   if (!p || !p->p) pl::fail(PL_E_INVALID, "null patch");
   if (!p->p->src) pl::fail(PL_E_STATE, "the patch's source store was destroyed");
@@ -614,7 +759,7 @@ int pl_patch_mark(pl_patch* p, int32_t req, int group, int64_t start, int64_t n)
 }
 int pl_patch_mark_batch(pl_patch* p, int n, const int32_t* reqs, const int32_t* groups,
                         const int64_t* starts, const int64_t* counts) {
-  return guard([&] {
+  return guard_tags({patch_of(p), src_of(p)}, [&] {
     pl::Patch* q = live(p);
     std::vector<pl::Store::WriteItem> items;
     items.reserve(n);
@@ -671,7 +816,8 @@ int pl_patch_apply(pl_patch* p, pl_store* dst, const int32_t* rank, int64_t n_ra
 }
 int pl_patch_push(pl_patch* p, pl_store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
                   int64_t* cells) {
-  return guard([&] { live(p)->push(dst->s, rank, n_rank, keys, cells); });
+  return guard_tags({patch_of(p), src_of(p), dst ? dst->s : nullptr},
+                    [&] { live(p)->push(dst->s, rank, n_rank, keys, cells); });
 }
 int pl_patch_stream(pl_patch* p, void** out) {
   return guard([&] { *out = (void*)live(p)->pstream(); });
@@ -931,5 +1077,176 @@ int pl_patch_rows(pl_patch* p, int32_t* reqs, int32_t* groups, int64_t* a, int64
 }
 int pl_patch_push_remote(pl_patch* p, pl_remote* r, int64_t n_items_applied) {
   return guard([&] { live(p)->push_remote(r->r, n_items_applied); });
+}
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// Native halves of one cross-process patch round over a pair mailbox (dist.py's layout).
+namespace {
+enum : int64_t { W_ROWS = 0, W_REPLY, W_APPLIED, W_NROWS, W_DONE, W_ERR, W_UPDATE, W_CLOSE, W_MSG };
+constexpr int kEvApplied = 0, kEvReserved = 1;
+constexpr int64_t kRowsOff = 512;
+struct MailRows {
+  int32_t* reqs; int32_t* groups; int64_t* a; int64_t* b; int64_t cap;
+};
+std::atomic<uint64_t>* mail_words(pl::MailboxRegion* m) {
+  int64_t bytes = 0;
+  return reinterpret_cast<std::atomic<uint64_t>*>(pl::mailbox_base(m, &bytes));
+}
+MailRows mail_rows(pl::MailboxRegion* m) {
+  int64_t bytes = 0;
+  uint8_t* base = static_cast<uint8_t*>(pl::mailbox_base(m, &bytes));
+  MailRows r;
+  r.cap = (bytes - kRowsOff) / 24;
+  uint8_t* o = base + kRowsOff;
+  r.reqs = reinterpret_cast<int32_t*>(o);
+  r.groups = reinterpret_cast<int32_t*>(o + 4 * r.cap);
+  r.a = reinterpret_cast<int64_t*>(o + 8 * r.cap);
+  r.b = reinterpret_cast<int64_t*>(o + 16 * r.cap);
+  return r;
+}
+uint64_t mix(uint64_t h, uint64_t v) { return (h ^ v) * 0x100000001b3ull + (h >> 29); }
+// hashes of what a peer process imported from this store: the block table (device pointer,
+// shape) and the migrating groups' pools (bases, planned bytes)
+void export_versions(pl::Store* s, const int32_t* groups, int n_groups, uint64_t* tv,
+                     uint64_t* pv) {
+  *tv = mix(mix(mix(0, (uint64_t)(uintptr_t)s->d_table), (uint64_t)s->max_reqs),
+            (uint64_t)s->max_chain);
+  uint64_t h = mix(0, (uint64_t)s->planned_bytes());
+  for (int i = 0; i < n_groups; ++i) {
+    const int g = groups[i];
+    if (g < 0 || g >= s->n_model_groups) pl::fail(PL_E_INVALID, "group out of range");
+    h = mix(h, s->materialised[g] ? s->group_base(g) : 0);
+  }
+  *pv = h;
+}
+}  // namespace
+
+extern "C" {
+int pl_pair_send_rows(pl_patch* p, pl_mailbox* m, const int32_t* rank, int64_t n_rank,
+                      uint64_t seq, int64_t* out_keys, int64_t* out_cells, int64_t* out_rows) {
+  return guard_tags({patch_of(p), src_of(p)}, [&] {
+    pl::Patch* q = live(p);
+    q->drain_rows(rank, n_rank, out_keys, out_cells);
+    const MailRows r = mail_rows(m->m);
+    const int64_t n = (int64_t)q->remote_rows.size();
+    if (n > r.cap) pl::fail(PL_E_INVALID, std::to_string(n) + " rows exceed the mailbox");
+    for (int64_t i = 0; i < n; ++i) {
+      r.reqs[i] = q->remote_rows[i].req;
+      r.groups[i] = q->remote_rows[i].group;
+      r.a[i] = q->remote_rows[i].a;
+      r.b[i] = q->remote_rows[i].b;
+    }
+    std::atomic<uint64_t>* w = mail_words(m->m);
+    w[W_NROWS].store((uint64_t)n, std::memory_order_relaxed);
+    w[W_ROWS].store(seq, std::memory_order_release);
+    *out_rows = n;
+  });
+}
+
+int pl_pair_serve_rows(pl_store* st, pl_mailbox* m, const int32_t* groups, int n_groups,
+                       uint64_t seq, int64_t timeout_ms, uint64_t* io_versions, int* out_flags,
+                       int64_t* out_done) {
+  int status = PL_OK;
+  const int rc = guard_tags({st ? st->s : nullptr}, [&] {
+    pl::Store* s = st->s;
+    std::atomic<uint64_t>* w = mail_words(m->m);
+    *out_flags = 0;
+    *out_done = 0;
+    pl::mailbox_wait(m->m, W_ROWS, seq, timeout_ms);
+    if (w[W_CLOSE].load(std::memory_order_acquire)) {
+      *out_flags = 1;
+      return;
+    }
+    const int64_t n = (int64_t)w[W_NROWS].load(std::memory_order_relaxed);
+    const MailRows r = mail_rows(m->m);
+    PL_CUDA(cudaSetDevice(s->device));
+    int64_t done = 0;
+    std::function<void()> job;  // submitted last: the worker never overlaps this call
+    if (pl::host_async_enabled() && s->rows_covered(n, r.reqs, r.groups, r.b)) {
+      // steady round: every row already has its blocks, so the device needs nothing from
+      // the reservation (no table entries, no KvOverflow possible): reply now and leave the
+      // write_slots bookkeeping (occupancy, written) to the host worker, on a copy of the
+      // rows (the sender overwrites the region next round); the next C-ABI call joins it
+      for (int64_t i = 0; i < n; ++i)
+        if (i == 0 || r.reqs[i] != r.reqs[i - 1] || r.groups[i] != r.groups[i - 1]) ++done;
+      std::vector<int32_t> rq(r.reqs, r.reqs + n), gq(r.groups, r.groups + n);
+      std::vector<int64_t> av(r.a, r.a + n), bv(r.b, r.b + n);
+      s->flush();
+      job = [s, rq = std::move(rq), gq = std::move(gq), av = std::move(av),
+             bv = std::move(bv)]() {
+        int st = PL_OK;
+        s->reserve_rows((int64_t)rq.size(), rq.data(), gq.data(), av.data(), bv.data(), &st,
+                        /*flush_deltas=*/false);
+        if (st != PL_OK) pl::fail(st, "steady round: unexpected reservation failure");
+      };
+    } else {
+      done = s->reserve_rows(n, r.reqs, r.groups, r.a, r.b, &status);
+    }
+    s->settle();  // the sender writes into these pools next: map them now
+    // the sender's push reads the table deltas just enqueued: it waits for this event
+    pl::mailbox_record(m->m, kEvReserved, s->stream);
+    w[W_DONE].store((uint64_t)done, std::memory_order_relaxed);
+    w[W_ERR].store((uint64_t)(int64_t)status, std::memory_order_relaxed);
+    if (status != PL_OK) {
+      char* msg = reinterpret_cast<char*>(w + W_MSG);
+      const size_t len = std::min<size_t>(255, s->last_msg.size());
+      std::memcpy(msg, s->last_msg.data(), len);
+      msg[len] = 0;
+    }
+    // what the sender imported: the block table (pointer, shape) and the pools
+    uint64_t tv = 0, pv = 0;
+    export_versions(s, groups, n_groups, &tv, &pv);
+    int flags = 8;  // served
+    if (tv != io_versions[0]) flags |= 2;
+    if (pv != io_versions[1]) flags |= 4;
+    io_versions[0] = tv;
+    io_versions[1] = pv;
+    w[W_UPDATE].store((flags & 6) ? 1u : 0u, std::memory_order_relaxed);
+    // no update: reply now; else the caller sends the update over its socket and posts
+    if (!(flags & 6)) w[W_REPLY].store(seq, std::memory_order_release);
+    *out_flags = flags;
+    *out_done = done;
+    if (job) pl::host_submit(std::move(job), {s});
+  });
+  if (rc != PL_OK) return rc;
+  // KvOverflow on the receiver: the round is served (the sender pushes the items before
+  // the failing one, migrator.py:124-131) and the error is this call's status
+  if (status != PL_OK) pl::g_err = st->s->last_msg;
+  return status;
+}
+
+int pl_pair_finish(pl_patch* p, pl_remote* rm, pl_mailbox* m, uint64_t seq, int64_t timeout_ms,
+                   int update_imported, int* out_need_update, int* out_rc, int64_t* out_done) {
+  return guard_tags({patch_of(p), src_of(p)}, [&] {
+    pl::Patch* q = live(p);
+    std::atomic<uint64_t>* w = mail_words(m->m);
+    *out_need_update = 0;
+    pl::mailbox_wait(m->m, W_REPLY, seq, timeout_ms);
+    const int64_t done = (int64_t)w[W_DONE].load(std::memory_order_relaxed);
+    *out_rc = (int)(int64_t)w[W_ERR].load(std::memory_order_relaxed);
+    *out_done = done;
+    if (w[W_UPDATE].load(std::memory_order_relaxed) && !update_imported) {
+      *out_need_update = 1;  // the caller imports the update, then calls again
+      return;
+    }
+    pl::mailbox_stream_wait(m->m, kEvReserved, q->pstream());
+    q->push_remote(rm->r, done);
+    // "applied" = an interprocess event after the push on the patch stream: the receiver's
+    // stream waits for it on the device; no host sync here
+    pl::mailbox_record(m->m, kEvApplied, q->pstream());
+    w[W_APPLIED].store(seq, std::memory_order_release);
+  });
+}
+
+int pl_store_export_versions(pl_store* st, const int32_t* groups, int n_groups, uint64_t* out2) {
+  return guard([&] { export_versions(st->s, groups, n_groups, out2, out2 + 1); });
+}
+
+int pl_pair_serve_ack(pl_store* st, pl_mailbox* m, uint64_t seq, int64_t timeout_ms) {
+  return guard_nojoin([&] {  // a poll and a stream wait: no host store state
+    pl::mailbox_wait(m->m, W_APPLIED, seq, timeout_ms);
+    pl::mailbox_stream_wait(m->m, kEvApplied, st->s->stream);
+  });
 }
 }  // extern "C"

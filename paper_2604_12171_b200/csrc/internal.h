@@ -20,6 +20,8 @@
 #include <string>
 #include <unordered_map>
 #include <deque>
+#include <functional>
+#include <initializer_list>
 #include <vector>
 
 #include "../../include/pipelive.h"
@@ -38,6 +40,17 @@ void cu_check(CUresult r, const char* what);
 #define PL_CUDA(x) ::pl::cuda_check((x), #x)
 
 void note_launch(int n = 1);  // kernel launch accounting for the bench
+// Host bookkeeping worker (one per process): jobs that only update host mirrors -- the
+// destination's write_slots bookkeeping of a launch-first patch round -- run here while the
+// caller returns.  Every C-ABI entry point that touches host store / patch state joins it
+// first (abi.cu guard), so no caller ever observes a half-applied mirror; a job's failure
+// is rethrown by the next join.
+// `tags`: the objects (Store*, Patch*) the job touches; guard_tags entry points wait only
+// for jobs sharing a tag, every other entry point for all jobs
+void host_submit(std::function<void()> job, std::vector<const void*> tags);
+void host_join();
+void host_join_tags(std::initializer_list<const void*> tags);
+bool host_async_enabled();  // PL_SYNC_BOOKKEEPING=1 keeps the bookkeeping on the caller
 // RAII CUDA-event bracket around one launch (only when timing is enabled)
 struct KernelTimer {
   const char* name;
@@ -340,6 +353,7 @@ struct Store {
     return ((uint64_t)gpu_id << 44) | ((uint64_t)block_id << 21);
   }
   ReqTable* table(int32_t req);
+  const ReqTable* table(int32_t req) const { return const_cast<Store*>(this)->table(req); }
   ReqTable& table_create(int32_t req);
   void table_delete(int32_t req);
   int64_t longest_written(const ReqTable& t) const;
@@ -424,7 +438,11 @@ struct Store {
   // receiver side of a cross-process patch: consecutive rows with the same (req, group)
   // are one item; returns the items fully reserved (stops at the first KvOverflow)
   int64_t reserve_rows(int64_t n_rows, const int32_t* reqs, const int32_t* groups,
-                       const int64_t* a, const int64_t* b, int* status);
+                       const int64_t* a, const int64_t* b, int* status, bool flush_deltas = true);
+  // true if every row's positions already have blocks in this store (chains cover them,
+  // groups mapped): reserving them is host bookkeeping only, nothing the device needs
+  bool rows_covered(int64_t n_rows, const int32_t* reqs, const int32_t* groups,
+                    const int64_t* b) const;
 
   // launch K1 for a list of (req, group, start, count) items
   struct WriteItem {
@@ -481,6 +499,7 @@ struct Patch {
   // host mirror of the dirty set: (req, local group) -> disjoint sorted intervals
   std::map<std::pair<int32_t, int32_t>, std::vector<Interval>> dirty;
   int64_t dirty_keys = 0;
+  int64_t dirty_cells = 0;  // dirty keys x pair layers of their group
 
   // device bitmaps over source cells: bit ((slot*G + lg)*s + off).  Double-buffered
   // epochs: K1 marks d_bits; a drain flips the epoch and drains the previous buffer on
@@ -491,6 +510,7 @@ struct Patch {
   cudaStream_t stream = nullptr;  // side stream for K3/K4/K5 (null: the source's stream)
   cudaStream_t pstream() const { return stream ? stream : src->stream; }
   cudaEvent_t ev_src = nullptr, ev_snap = nullptr, ev_mask = nullptr;
+  cudaEvent_t snap_ev = nullptr;  // the event the last drain's snapshot completed at
   bool snap_recorded = false, gathered_recorded = false, mask_recorded = false;
   // apply mask of the fused push, in patch-owned buffers: the copy on the side stream
   // reads it while the store's stream (and its scratch) moves on
@@ -519,6 +539,10 @@ struct Patch {
   int32_t* d_keys = nullptr;    // (req, lg, pos_lo, pos_hi) per row
   int64_t rows_cap = 0;
   bool in_flight = false;
+  // cross-process steady round: drain_rows flipped the epoch and left the device drain
+  // of `deferred_bits` to push_remote (one fused drain + push launch)
+  bool deferred = false;
+  uint32_t* deferred_bits = nullptr;
   std::vector<std::tuple<int32_t, int32_t, std::vector<Interval>>> drained;
   int64_t drained_keys = 0;
   int64_t last_device_drained = -1;
@@ -561,6 +585,7 @@ struct Patch {
   int64_t device_dirty_count();
   bool fused_round() const;  // K3 + push in one launch for sparse rounds
   void device_drain_push(Store* dst, const std::vector<uint8_t>* mask);
+  void launch_steady(Store* dst);
   // host phases of the last push (ms): adoption wait for lazily mapped pools, dirty-set
   // snapshot, destination reservation, destination table flush, K3 enqueue, copy enqueue,
   // total, chunked (1) or not (0)

@@ -106,7 +106,22 @@ void Patch::drain_rows(const int32_t* rank, int64_t n_rank, int64_t* keys, int64
     for (const Interval& iv : std::get<2>(e))
       remote_rows.push_back({std::get<0>(e), groups[std::get<1>(e)], iv.a, iv.b});
   PL_CUDA(cudaSetDevice(src->device));
-  device_drain_compact();  // K3 into d_cells, on the source stream
+  if (fused_round()) {
+    // sparse round: flip the marking epoch now (the host snapshot above is exactly the
+    // old buffer's bits) and leave its drain to push_remote's fused drain + push launch
+    src->flush();
+    cudaStream_t ps = pstream();
+    deferred_bits = d_bits;
+    std::swap(d_bits, d_bits_alt);
+    if (snap_recorded && ps != src->stream) PL_CUDA(cudaStreamWaitEvent(src->stream, snap_ev, 0));
+    if (ps != src->stream) {
+      PL_CUDA(cudaEventRecord(ev_src, src->stream));
+      PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
+    }
+    deferred = true;
+  } else {
+    device_drain_compact();  // K3 into d_cells, on the source stream
+  }
   in_flight = true;
 }
 
@@ -126,6 +141,42 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
   for (int32_t g : groups)
     if (!r->pools[g].va && n_applied > 0)
       fail(PL_E_STATE, "remote pool of group " + std::to_string(g) + " not imported");
+  if (deferred) {
+    // the drain of the flipped buffer and the push in one launch; it runs even when no
+    // item was reserved (all masked off) so the drained bits are cleared
+    deferred = false;
+    if (!r->table) fail(PL_E_STATE, "remote block table not opened");
+    cudaStream_t ps = pstream();
+    const uint8_t* d_apply = n_applied >= (int64_t)drained.size() ? nullptr : stage_mask(mask);
+    CopyLaunch c{};
+    c.mode = 2;
+    c.G = G;
+    c.k = src->k;
+    c.cell_bytes = src->cell_bytes;
+    c.fp_bytes = src->fp_bytes;
+    c.src_bases = src->d_bases_;
+    c.src_groups = d_groups();
+    c.src_s = src->s;
+    c.src_unit = src->unit_bytes;
+    c.src_owner = src->d_owner;
+    c.src_owner_idx = src->d_owner_idx;
+    c.dst_bases = r->d_bases;
+    c.dst_s = r->s;
+    c.dst_unit = r->unit_bytes;
+    c.dst_table = r->table;
+    c.dst_max_chain = r->max_chain;
+    c.apply_mask = d_apply;
+    cnt_cur ^= 1;
+    d_count = d_cnt + cnt_cur;
+    launch_drain_push(c, deferred_bits, n_words, d_count, d_cnt + (cnt_cur ^ 1), ps);
+    PL_CUDA(cudaEventRecord(ev_applied, ps));
+    snap_ev = ev_applied;
+    snap_recorded = true;
+    applied_recorded = true;
+    drained.clear();
+    remote_rows.clear();
+    return;
+  }
   if (drained_keys > 0 && n_applied > 0) {
     if (!r->table) fail(PL_E_STATE, "remote block table not opened");
     if (pstream() != src->stream) {
@@ -163,8 +214,19 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
   remote_rows.clear();
 }
 
+bool Store::rows_covered(int64_t n_rows, const int32_t* reqs, const int32_t* groups,
+                         const int64_t* b) const {
+  for (int64_t i = 0; i < n_rows; ++i) {
+    const int g = groups[i];
+    if (g < 0 || g >= n_model_groups || !materialised[g]) return false;
+    const ReqTable* t = table(reqs[i]);
+    if (!t || (int64_t)t->chain.size() * s < b[i]) return false;
+  }
+  return true;
+}
+
 int64_t Store::reserve_rows(int64_t n_rows, const int32_t* reqs, const int32_t* groups,
-                            const int64_t* a, const int64_t* b, int* status) {
+                            const int64_t* a, const int64_t* b, int* status, bool flush_deltas) {
   *status = PL_OK;
   int64_t items = 0;
   for (int64_t i = 0; i < n_rows;) {
@@ -187,7 +249,7 @@ int64_t Store::reserve_rows(int64_t n_rows, const int32_t* reqs, const int32_t* 
   // the table deltas go out on the store's stream; the sending process reads the table
   // next: the caller orders that (a host sync, or an interprocess event the sender's
   // stream waits on -- dist.PatchReceiver)
-  flush();
+  if (flush_deltas) flush();
   return items;
 }
 

@@ -1,4 +1,5 @@
 #include <algorithm>
+#include <cstdlib>
 // Data-plane kernels of the live-reconfiguration path (sm_100a).
 //
 //   K1  kv_write_mark  : KvStore.append / write_slots (kvstore.py:163-227) fused with the
@@ -462,38 +463,58 @@ __global__ void __launch_bounds__(kWarps * 32) copy_kernel(CopyLaunch c) {
   }
 }
 
-// K3 + K4/K5 fused for sparse (steady) rounds, one persistent launch (a few hundred CTAs:
-// launching thousands of short CTAs cost more than the copies).  A CTA takes 256 bitmap
-// words at a time: every thread snapshots + clears one word (atomicExch, as K3) and the set
-// bits go into a shared-memory queue (ballot / popc per warp); then the whole CTA copies the
-// queued cells pool -> pool through the destination's table (as copy_kernel<2>): the k
-// layers of a cell (16 KB for the Llama shapes) are 4 16-B vectors per thread, in flight at
-// once.  Dense rounds (many bits per word) keep K3 + copy_kernel<2> (kFusedMinKeys).
+// K3 + K4/K5 fused for steady rounds, one persistent launch.  A CTA takes W bitmap words
+// at a time (W in 8..256: the narrowest pass whose pass count fits one wave of 2 CTAs per
+// SM -- a decode-pattern round has a few keys per thousand words, and wide passes left most
+// SMs idle while a few CTAs copied their keys one after another).
+//   scan : thread t < W snapshots + clears word t with ONE atomicExch (the drained epoch's
+//          buffer; marks of the next round go to the other buffer) and queues the set bits
+//          in shared memory (warp prefix of the popcounts, one shared atomicAdd per warp);
+//   copy : the (key, layer) cells of the queue are spread over the CTA's warps, TWO cells
+//          per warp in flight (2 x 8 x 16 B per lane, loads issued before anything waits).
+//          The source address comes from the cell index alone, so the source loads go out
+//          at once; lanes 0/1 meanwhile resolve the destination (owner map -> request,
+//          position -> destination block table) and broadcast it; then the stores.
+// Per key the dependent chain is: exchange -> {source load | owner -> table} -> store.
 constexpr int kFusedWords = 256;
+__device__ __forceinline__ uint8_t* fused_dst(const CopyLaunch& c, int64_t cell, int64_t per_slot,
+                                              int* doff_out) {
+  const int32_t slot = (int32_t)(cell / per_slot);
+  const int64_t rem = cell % per_slot;
+  const int32_t lg = (int32_t)(rem / c.src_s);
+  const int off = (int)(rem % c.src_s);
+  const int32_t req = c.src_owner[slot];
+  if (req < 0) return nullptr;
+  if (c.apply_mask && !c.apply_mask[(int64_t)req * c.G + lg]) return nullptr;
+  const int64_t pos = (int64_t)c.src_owner_idx[slot] * c.src_s + off;
+  const int32_t dslot = c.dst_table[(int64_t)req * c.dst_max_chain + pos / c.dst_s];
+  if (dslot < 0) return nullptr;
+  *doff_out = (int)(pos % c.dst_s);
+  return reinterpret_cast<uint8_t*>(c.dst_bases[c.src_groups[lg]]) + (int64_t)dslot * c.dst_unit;
+}
+
 __global__ void __launch_bounds__(256)
-drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, unsigned long long* count,
+drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, int W, unsigned long long* count,
                   unsigned long long* next_count) {
   __shared__ uint16_t queue[kFusedWords * 32];
   __shared__ int q_n;
   if (blockIdx.x == 0 && threadIdx.x == 0) *next_count = 0ull;
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
   const int64_t vecs = c.cell_bytes >> 4;
-  const int64_t total = (int64_t)c.k * vecs;
   const int64_t per_slot = (int64_t)c.G * c.src_s;
+  constexpr int U = 8;
   unsigned long long drained = 0;
-  for (int64_t base = (int64_t)blockIdx.x * kFusedWords; base < n_words;
-       base += (int64_t)gridDim.x * kFusedWords) {
+  for (int64_t base = (int64_t)blockIdx.x * W; base < n_words; base += (int64_t)gridDim.x * W) {
     if (threadIdx.x == 0) q_n = 0;
     __syncthreads();
     const int64_t wi = base + threadIdx.x;
     uint32_t v = 0;
-    if (wi < n_words) {
-      v = bits[wi];
-      if (v) v = atomicExch(bits + wi, 0u);
-    }
+    if (threadIdx.x < W && wi < n_words) v = atomicExch(bits + wi, 0u);
     const int cnt = __popc(v);
     drained += cnt;
-    int incl = cnt;  // warp prefix of the bit counts -> one shared atomicAdd per warp
+    int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -509,56 +530,70 @@ drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, unsigned long l
       queue[start++] = (uint16_t)(threadIdx.x * 32 + b);
     }
     __syncthreads();
-    const int n = q_n;
-    for (int qi = 0; qi < n; ++qi) {
-      const int64_t cell = base * 32 + queue[qi];
-      const int32_t slot = (int32_t)(cell / per_slot);
-      const int64_t rem = cell % per_slot;
-      const int32_t lg = (int32_t)(rem / c.src_s);
-      const int off = (int)(rem % c.src_s);
-      const int32_t req = c.src_owner[slot];
-      if (req < 0) continue;
-      if (c.apply_mask && !c.apply_mask[(int64_t)req * c.G + lg]) continue;
-      const int64_t pos = (int64_t)c.src_owner_idx[slot] * c.src_s + off;
-      const int32_t dslot = c.dst_table[(int64_t)req * c.dst_max_chain + pos / c.dst_s];
-      if (dslot < 0) continue;
-      const int doff = (int)(pos % c.dst_s);
-      const uint8_t* su = reinterpret_cast<const uint8_t*>(c.src_bases[c.src_groups[lg]]) +
-                          (int64_t)slot * c.src_unit;
-      uint8_t* du = reinterpret_cast<uint8_t*>(c.dst_bases[c.src_groups[lg]]) +
-                    (int64_t)dslot * c.dst_unit;
-      if (threadIdx.x == 0)
-        reinterpret_cast<uint64_t*>(du)[doff] = reinterpret_cast<const uint64_t*>(su)[off];
-      su += c.fp_bytes;
-      du += c.fp_bytes;
-      constexpr int U = 4;
-      int64_t x = threadIdx.x;
-      for (; x + 256 * (U - 1) < total; x += 256 * U) {
-        int4 buf[U];
+    const int n_items = q_n * c.k;
+    for (int it = warp; it < n_items; it += 2 * nwarps) {
+      // items it and it + nwarps: (key, layer) = (it / k, it % k)
+      int64_t cell[2];
+      int j[2];
+      bool have[2];
+      const uint8_t* su[2];
+      int off[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int x = it + h * nwarps;
+        have[h] = x < n_items;
+        const int q = have[h] ? x / c.k : 0;
+        j[h] = have[h] ? x - q * c.k : 0;
+        cell[h] = base * 32 + queue[q];
+        const int32_t slot = (int32_t)(cell[h] / per_slot);
+        const int64_t rem = cell[h] % per_slot;
+        off[h] = (int)(rem % c.src_s);
+        su[h] = reinterpret_cast<const uint8_t*>(c.src_bases[c.src_groups[(int)(rem / c.src_s)]]) +
+                (int64_t)slot * c.src_unit;
+      }
+      // source loads first (independent of the destination)
+      int4 buf[2][U];
+      uint64_t fp = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int4* s4 = reinterpret_cast<const int4*>(su[h] + c.fp_bytes +
+                                                       ((int64_t)j[h] * c.src_s + off[h]) * c.cell_bytes);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int64_t e = x + 256 * u;
-          const int j = (int)(e / vecs);
-          buf[u] = ld_stream(reinterpret_cast<const int4*>(
-                                 su + ((int64_t)j * c.src_s + off) * c.cell_bytes) + (e - j * vecs));
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t e = x + 256 * u;
-          const int j = (int)(e / vecs);
-          st_stream(reinterpret_cast<int4*>(du + ((int64_t)j * c.dst_s + doff) * c.cell_bytes) +
-                        (e - j * vecs), buf[u]);
+          const int64_t e = lane + 32 * u;
+          if (have[h] && e < vecs) buf[h][u] = ld_stream(s4 + e);
         }
       }
-      for (; x < total; x += 256) {
-        const int j = (int)(x / vecs);
-        st_stream(reinterpret_cast<int4*>(du + ((int64_t)j * c.dst_s + doff) * c.cell_bytes) +
-                      (x - j * vecs),
-                  ld_stream(reinterpret_cast<const int4*>(
-                                su + ((int64_t)j * c.src_s + off) * c.cell_bytes) + (x - j * vecs)));
+      // destination: lane h resolves item h; the fingerprint word rides along (layer 0)
+      uint8_t* du = nullptr;
+      int doff = 0;
+      if (lane < 2) {
+        const bool hv = lane ? have[1] : have[0];
+        if (hv) {
+          du = fused_dst(c, lane ? cell[1] : cell[0], per_slot, &doff);
+          if (du && (lane ? j[1] : j[0]) == 0)
+            fp = reinterpret_cast<const uint64_t*>(lane ? su[1] : su[0])[lane ? off[1] : off[0]];
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint8_t* d = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(du), h));
+        const int dof = __shfl_sync(0xffffffffu, doff, h);
+        if (!have[h] || !d) continue;
+        if (lane == h && j[h] == 0) reinterpret_cast<uint64_t*>(d)[dof] = fp;
+        int4* d4 = reinterpret_cast<int4*>(d + c.fp_bytes + ((int64_t)j[h] * c.dst_s + dof) * c.cell_bytes);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t e = lane + 32 * u;
+          if (e < vecs) st_stream(d4 + e, buf[h][u]);
+        }
+        // cells wider than 32 x U x 16 B (not the Llama shapes): the rest, plainly
+        const int4* s4 = reinterpret_cast<const int4*>(su[h] + c.fp_bytes +
+                                                       ((int64_t)j[h] * c.src_s + off[h]) * c.cell_bytes);
+        for (int64_t e = lane + 32 * U; e < vecs; e += 32) st_stream(d4 + e, ld_stream(s4 + e));
       }
     }
-    __syncthreads();  // the queue is rebuilt for the next 256 words
+    __syncthreads();  // the queue is rebuilt for the next pass
   }
   for (int o = 16; o; o >>= 1) drained += __shfl_xor_sync(0xffffffffu, drained, o);
   if (lane == 0 && drained) atomicAdd(count, drained);
@@ -566,11 +601,20 @@ drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, unsigned long l
 
 void launch_drain_push(const CopyLaunch& c, uint32_t* bits, int64_t n_words, int64_t* count,
                        int64_t* next_count, cudaStream_t st) {
-  const int64_t chunks = (n_words + kFusedWords - 1) / kFusedWords;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)sm_count() * 2));
+  static const int per_sm = [] {
+    const char* v = std::getenv("PL_FUSED_CTAS_PER_SM");
+    return v ? std::max(1, std::atoi(v)) : 2;
+  }();
+  // the narrowest pass (>= 8 words) whose passes still fit in one wave of `per_sm` CTAs per
+  // SM: every CTA then scans once and copies its own keys, none waits for a second pass
+  const int64_t target = (int64_t)sm_count() * per_sm;
+  int W = 8;
+  while (W < kFusedWords && (n_words + W - 1) / W > target) W <<= 1;
+  const int64_t chunks = (n_words + W - 1) / W;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, target));
   KernelTimer timer("drain_push", st);
   drain_push_kernel<<<(unsigned)grid, 256, 0, st>>>(
-      c, bits, n_words, reinterpret_cast<unsigned long long*>(count),
+      c, bits, n_words, W, reinterpret_cast<unsigned long long*>(count),
       reinterpret_cast<unsigned long long*>(next_count));
   note_launch();
   PL_CUDA(cudaGetLastError());

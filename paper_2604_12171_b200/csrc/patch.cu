@@ -189,7 +189,9 @@ void Patch::mark(int32_t req, int g, int64_t start, int64_t n, bool device) {
   if (n <= 0 || g < 0 || g >= (int)local_of.size()) return;
   const int lg = local_of[g];
   if (lg < 0) return;
-  dirty_keys += insert_interval(dirty[{req, lg}], start, start + n);
+  const int64_t added = insert_interval(dirty[{req, lg}], start, start + n);
+  dirty_keys += added;
+  dirty_cells += added * layers_in_group[lg];
   if (device) {
     Store::WriteItem it{req, lg, start, n, 0, start};
     mark_device({it});
@@ -238,7 +240,9 @@ int64_t Patch::seed() {
     for (int lg = 0; lg < G; ++lg) {
       const int64_t w = t.written[groups[lg]];
       if (w <= 0) continue;
-      dirty_keys += insert_interval(dirty[{req, lg}], 0, w);
+      const int64_t added = insert_interval(dirty[{req, lg}], 0, w);
+      dirty_keys += added;
+      dirty_cells += added * layers_in_group[lg];
       seeded += w;
       items.push_back({req, lg, 0, w, 0, 0});
     }
@@ -252,7 +256,10 @@ int64_t Patch::discard(int32_t req) {
   for (int lg = 0; lg < G; ++lg) {
     auto it = dirty.find({req, lg});
     if (it == dirty.end()) continue;
-    for (const Interval& x : it->second) dropped += x.b - x.a;
+    int64_t d = 0;
+    for (const Interval& x : it->second) d += x.b - x.a;
+    dropped += d;
+    dirty_cells -= d * layers_in_group[lg];
     dirty.erase(it);
   }
   dirty_keys -= dropped;
@@ -296,6 +303,7 @@ int64_t Patch::take_drained() {
   dirty.clear();
   drained_keys = dirty_keys;
   dirty_keys = 0;
+  dirty_cells = 0;
   return drained_keys;
 }
 
@@ -314,7 +322,7 @@ int64_t Patch::device_drain_compact() {
   // snapshot cleared on the patch stream
   uint32_t* old = d_bits;
   std::swap(d_bits, d_bits_alt);
-  if (snap_recorded && ps != src->stream) PL_CUDA(cudaStreamWaitEvent(src->stream, ev_snap, 0));
+  if (snap_recorded && ps != src->stream) PL_CUDA(cudaStreamWaitEvent(src->stream, snap_ev, 0));
   if (ps != src->stream) {
     PL_CUDA(cudaEventRecord(ev_src, src->stream));
     PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
@@ -327,6 +335,7 @@ int64_t Patch::device_drain_compact() {
     d_count = d_cnt + cnt_cur;
     launch_drain_compact(old, n_words, d_cells, cells_cap, d_count, d_cnt + (cnt_cur ^ 1), ps);
     PL_CUDA(cudaEventRecord(ev_snap, ps));
+    snap_ev = ev_snap;
     snap_recorded = true;
   }
   return drained_keys;
@@ -513,9 +522,9 @@ int64_t Patch::new_dst_blocks(Store* dst) const {
   // destination blocks the drained set will allocate: per request, the chain it needs past
   // the chain it has (the chain is shared by the request's groups)
   std::vector<int64_t> top;
-  for (const auto& e : drained) {
-    const int32_t req = std::get<0>(e);
-    const auto& iv = std::get<2>(e);
+  for (const auto& e : dirty) {
+    const int32_t req = e.first.first;
+    const auto& iv = e.second;
     if (iv.empty()) continue;
     if ((size_t)req >= top.size()) top.resize((size_t)req + 1, 0);
     top[(size_t)req] = std::max(top[(size_t)req], iv.back().b);
@@ -658,6 +667,32 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
   if (status != PL_OK) fail(status, dst->last_msg);
 }
 
+// The device side of a launch-first steady round: K3 + the push (or the fused kernel),
+// ordered after the destination stream's queued work; the destination stream then waits
+// for the copy.
+void Patch::launch_steady(Store* dst) {
+  PL_CUDA(cudaSetDevice(dst->device));
+  dst->flush();
+  PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
+  PL_CUDA(cudaSetDevice(src->device));
+  if (fused_round()) {
+    device_drain_push(dst, nullptr);
+    return;
+  }
+  device_drain_compact();
+  if (pstream() != src->stream) {
+    PL_CUDA(cudaEventRecord(ev_src, src->stream));
+    PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
+  }
+  PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
+  launch_copy(push_launch(dst, nullptr, 0), pstream());
+  PL_CUDA(cudaEventRecord(ev_applied, pstream()));
+  applied_recorded = true;
+  PL_CUDA(cudaSetDevice(dst->device));
+  PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
+  PL_CUDA(cudaSetDevice(src->device));
+}
+
 void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells) {
   auto clk = [] { return std::chrono::steady_clock::now(); };
   auto dms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -678,12 +713,49 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
   const auto t0 = now();
-  take_drained();
-  *keys = drained_keys;
-  *cells = host_cells(drained);
+  // keys / cells of the round and the destination blocks it needs come from the host
+  // mirror as it stands (the snapshot itself may move to the bookkeeping worker below)
+  *keys = dirty_keys;
+  *cells = dirty_cells;
   const int64_t new_blocks = new_dst_blocks(dst);
-  if (drained.size() >= 2 && !no_chunking() && new_blocks >= chunk_min_blocks() &&
-      (forced_chunking() || streams_idle(dst))) {
+  bool dst_pools = true;
+  for (int32_t g : groups) dst_pools = dst_pools && dst->materialised[g];
+  const bool chunk = dirty.size() >= 2 && !no_chunking() && new_blocks >= chunk_min_blocks() &&
+                     (forced_chunking() || streams_idle(dst));
+  const bool launch_first = !chunk && new_blocks == 0 && dst_pools && dirty_keys > 0 &&
+                            !launch_first_off();
+  if (launch_first && host_async_enabled()) {
+    // Steady round whose positions all have destination blocks already (chains extend only
+    // every s tokens): the device needs nothing from the host -- no new table entries, no
+    // KvOverflow possible -- so the round launches at once and the host side (the interval
+    // snapshot and write_slots' occupancy / written bookkeeping, kvstore.py:201-227) goes
+    // to the bookkeeping worker; the next C-ABI call joins it, before any mark can reach the
+    // host mirror.  Block ids and counters are those of the unreordered round.
+    drained_keys = dirty_keys;
+    const auto t1 = now();
+    launch_steady(dst);
+    const auto t2 = now();
+    std::vector<int32_t> rk;
+    if (rank && n_rank > 0) rk.assign(rank, rank + n_rank);
+    push_stats[1] = ms(t0, t1);
+    push_stats[4] = ms(t1, t2);
+    push_stats[6] = ms(ta, now());
+    push_stats[7] = 2;
+    host_submit([this, dst, rk = std::move(rk)]() {
+      const auto tb = std::chrono::steady_clock::now();
+      take_drained();
+      std::vector<uint8_t> m;
+      int st = PL_OK;
+      extend_dst(dst, rk.empty() ? nullptr : rk.data(), (int64_t)rk.size(), nullptr, 0, m, &st);
+      drained.clear();
+      push_stats[2] = std::chrono::duration<double, std::milli>(
+                          std::chrono::steady_clock::now() - tb).count();
+      if (st != PL_OK) fail(st, "steady round: unexpected reservation failure");
+    }, {this, src, dst});
+    return;
+  }
+  take_drained();
+  if (chunk) {
     push_stats[1] = ms(t0, now());
     push_chunked(dst, rank, n_rank);
     push_stats[6] = ms(ta, now());
@@ -692,40 +764,16 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   }
   std::vector<uint8_t> mask;
   int status = PL_OK;
-  bool dst_pools = true;
-  for (int32_t g : groups) dst_pools = dst_pools && dst->materialised[g];
-  if (new_blocks == 0 && dst_pools && drained_keys > 0 && !launch_first_off()) {
-    // Steady round whose positions all have destination blocks already (chains extend only
-    // every s tokens): the device needs nothing from the host reservation -- no new table
-    // entries, no KvOverflow possible -- so K3 + the push launch first and the host
-    // bookkeeping of write_slots (occupancy, written, kvstore.py:201-227) runs while the
-    // copy does.  Block ids and counters are those of the unreordered round.
+  if (launch_first) {
+    // the same round with the bookkeeping on the caller (PL_SYNC_BOOKKEEPING=1)
     const auto t1 = now();
-    PL_CUDA(cudaSetDevice(dst->device));
-    dst->flush();
-    PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
-    PL_CUDA(cudaSetDevice(src->device));
-    if (fused_round()) {
-      device_drain_push(dst, nullptr);
-    } else {
-      device_drain_compact();
-      if (pstream() != src->stream) {
-        PL_CUDA(cudaEventRecord(ev_src, src->stream));
-        PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
-      }
-      PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
-      launch_copy(push_launch(dst, nullptr, 0), pstream());
-      PL_CUDA(cudaEventRecord(ev_applied, pstream()));
-      applied_recorded = true;
-      PL_CUDA(cudaSetDevice(dst->device));
-      PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
-    }
+    launch_steady(dst);
     const auto t2 = now();
+    push_stats[1] = ms(t0, t1);
+    push_stats[4] = ms(t1, t2);
     extend_dst(dst, rank, n_rank, nullptr, 0, mask, &status);
     drained.clear();
     if (status != PL_OK) fail(status, "steady round: unexpected reservation failure");
-    push_stats[1] = ms(t0, t1);
-    push_stats[4] = ms(t1, t2);
     push_stats[2] = ms(t2, now());
     push_stats[6] = ms(ta, now());
     return;
@@ -788,8 +836,9 @@ bool Patch::fused_round() const {
     return v ? std::atoll(v) : (int64_t)-1;
   }();
   // about two keys per 256-word chunk: the persistent CTAs copy their queues serially
-  const int64_t lim =
-      max_keys >= 0 ? max_keys : std::max<int64_t>(kFusedMinKeys, 2 * ((n_words + 255) / 256));
+  // the fused kernel spreads a round's cells over every SM (one 4 KiB cell per warp); up to
+  // about one key per bitmap word it beats K3 + copy_kernel<2>'s two launches
+  const int64_t lim = max_keys >= 0 ? max_keys : std::max<int64_t>(kFusedMinKeys, n_words);
   return !off && drained_keys > 0 && drained_keys <= lim;
 }
 
@@ -798,7 +847,7 @@ void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask) {
   cudaStream_t ps = pstream();
   uint32_t* old = d_bits;  // epoch flip, as device_drain_compact
   std::swap(d_bits, d_bits_alt);
-  if (snap_recorded && ps != src->stream) PL_CUDA(cudaStreamWaitEvent(src->stream, ev_snap, 0));
+  if (snap_recorded && ps != src->stream) PL_CUDA(cudaStreamWaitEvent(src->stream, snap_ev, 0));
   if (ps != src->stream) {
     PL_CUDA(cudaEventRecord(ev_src, src->stream));
     PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
@@ -809,9 +858,11 @@ void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask) {
   cnt_cur ^= 1;
   d_count = d_cnt + cnt_cur;
   launch_drain_push(push_launch(dst, d_apply, 0), old, n_words, d_count, d_cnt + (cnt_cur ^ 1), ps);
-  PL_CUDA(cudaEventRecord(ev_snap, ps));
-  snap_recorded = true;
+  // the snapshot and the copy end together in this kernel: one event marks both (a later
+  // re-record of ev_applied only ever moves it past this point)
   PL_CUDA(cudaEventRecord(ev_applied, ps));
+  snap_ev = ev_applied;
+  snap_recorded = true;
   applied_recorded = true;
   PL_CUDA(cudaSetDevice(dst->device));
   PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));

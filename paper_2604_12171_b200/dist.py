@@ -196,6 +196,12 @@ class PatchReceiver:
             mailbox = os.environ.get("PL_PATCH_SOCKET") is None
         self.mb = Mailbox.create(store.device) if mailbox else None
         self.seq = 0
+        self._groups_arr = N.as_i32(self.groups)
+        self._versions = np.zeros(2, dtype=np.uint64)   # (table, pools) hashes, set below
+        # ctypes arguments of the per-round calls, built once (numpy's .ctypes costs ~2 us)
+        self._groups_p, self._versions_p = N.ptr(self._groups_arr), N.ptr(self._versions)
+        self._flags, self._done = C.c_int(), C.c_int64()
+        self._flags_ref, self._done_ref = C.byref(self._flags), C.byref(self._done)
         store.resident_groups |= set(self.groups)
         self._send_hello()
         self.rounds = 0
@@ -211,6 +217,8 @@ class PatchReceiver:
         table = export_table(self.store)
         self._pools = self._pool_state()
         self._table = table_version(self.store)
+        N.check(N.lib().pl_store_export_versions(self.store._h, N.ptr(self._groups_arr),
+                                                 len(self.groups), N.ptr(self._versions)))
         self.chan.send(("hello", store_layout(self.store), meta, table,
                         self.mb.export() if self.mb is not None else None), fds)
         for fd in fds:
@@ -267,32 +275,35 @@ class PatchReceiver:
         return True
 
     def _serve_rows_mailbox(self) -> bool:
-        mb = self.mb
+        # the whole receiver half in one native call (pl_pair_serve_rows): wait for the rows,
+        # reserve them in place, record "reserved", reply -- unless the table or pools the
+        # sender imported changed, in which case the re-export goes over the socket first
         self.seq += 1
-        mb.wait(W_ROWS, self.seq)
-        if mb.words[W_CLOSE]:
+        flags, done = self._flags, self._done
+        rc = N.lib().pl_pair_serve_rows(self.store._h, self.mb.h, self._groups_p,
+                                        len(self.groups), self.seq, 300_000,
+                                        self._versions_p, self._flags_ref, self._done_ref)
+        if flags.value & 1:
             return False
-        n = int(mb.words[W_NROWS])
-        done = C.c_int64()
-        # the rows are read in place from the shared region
-        rc = N.lib().pl_store_reserve_rows(self.store._h, n, N.ptr(mb.reqs), N.ptr(mb.groups),
-                                           N.ptr(mb.a), N.ptr(mb.b), C.byref(done))
         err = None if rc == N.PL_OK else (rc, N.lib().pl_last_error().decode(errors="replace"))
-        update, fds = self._updates()
-        # the sender's push reads the table deltas just enqueued: it waits for this event
-        mb.record(EV_RESERVED, self.store.stream_ptr())
-        mb.words[W_DONE] = done.value
-        mb.words[W_ERR] = np.uint64(rc & 0xFFFFFFFFFFFFFFFF)
-        if err is not None:
-            msg = err[1].encode()[:255]
-            np.ctypeslib.as_array((C.c_ubyte * 256).from_address(mb.base + 8 * W_MSG))[:len(msg) + 1] = \
-                np.frombuffer(msg + b"\0", dtype=np.uint8)
-        mb.words[W_UPDATE] = 1 if update else 0
-        if update:   # rare (a reallocated table, re-mapped pools): over the socket
+        if err is not None and not flags.value & 8:   # the call failed (not the reservation)
+            raise N.NativeError(rc, err[1])
+        if flags.value & 6:   # rare (a reallocated table, re-mapped pools): over the socket
+            update, fds = {}, []
+            if flags.value & 2:
+                update["table"] = export_table(self.store)
+                self._table = table_version(self.store)
+                self.table_reexports += 1
+            if flags.value & 4:
+                update["pools"], fds = export_groups(self.store, self.groups)
+                self._pools = self._pool_state()
+                self.pool_reexports += 1
             self.chan.send(("update", update), fds)
             for fd in fds:
                 os.close(fd)
-        mb.post(W_REPLY, self.seq)
+            N.check(N.lib().pl_store_export_versions(self.store._h, N.ptr(self._groups_arr),
+                                                     len(self.groups), N.ptr(self._versions)))
+            self.mb.post(W_REPLY, self.seq)
         self.rounds += 1
         self.items_reserved += done.value
         self._err = err
@@ -302,8 +313,7 @@ class PatchReceiver:
         """Second half: the sender's cells are in this store once "applied" arrives
         (mailbox: this store's stream waits on the device for the sender's push)."""
         if self.mb is not None:
-            self.mb.wait(W_APPLIED, self.seq)
-            self.mb.stream_wait(EV_APPLIED, self.store.stream_ptr())
+            N.check(N.lib().pl_pair_serve_ack(self.store._h, self.mb.h, self.seq, 300_000))
         else:
             ack, _ = self.chan.recv()
             assert ack[0] == "applied", ack[0]
@@ -331,6 +341,12 @@ class PatchSender:
         self.remote.set_table(th, mr, mc)
         self.mb = Mailbox.open(store.device, mb_blob) if mb_blob is not None else None
         self.seq = 0
+        # ctypes arguments of the per-round calls, built once
+        self._rank, self._rank_args = None, (None, 0)
+        a = (C.c_int64(), C.c_int64(), C.c_int64())
+        self._args = a + tuple(C.byref(x) for x in a)
+        self._fin = (C.c_int(), C.c_int(), C.c_int64())
+        self._fin_refs = tuple(C.byref(x) for x in self._fin)
         self.keys = self.cells = 0
 
     def seed(self) -> int:
@@ -345,22 +361,21 @@ class PatchSender:
     def begin(self) -> None:
         """Drain (host snapshot + K3) and send the rows to the receiver."""
         rank = self.rank_fn()
+        if self.mb is not None:
+            # drain + rows into the shared region + post, in one native call
+            if rank is not self._rank:
+                self._rank, self._rank_args = rank, (N.ptr(rank), len(rank))
+            self.seq += 1
+            a = self._args
+            N.check(N.lib().pl_pair_send_rows(self.patch.h, self.mb.h, *self._rank_args,
+                                              self.seq, a[3], a[4], a[5]))
+            self._pending = (a[0].value, a[1].value)
+            return
         keys, cells, n = C.c_int64(), C.c_int64(), C.c_int64()
         N.check(N.lib().pl_patch_drain_rows(self.patch.h, N.ptr(rank), len(rank), C.byref(keys),
                                             C.byref(cells), C.byref(n)))
         m = n.value
         self._pending = (keys.value, cells.value)
-        if self.mb is not None:
-            mb = self.mb
-            if m > mb.cap:
-                raise N.NativeError(N.PL_E_INVALID, f"{m} rows exceed the mailbox ({mb.cap})")
-            # rows straight into the shared region, then one release store
-            N.check(N.lib().pl_patch_rows(self.patch.h, N.ptr(mb.reqs), N.ptr(mb.groups),
-                                          N.ptr(mb.a), N.ptr(mb.b), m))
-            mb.words[W_NROWS] = m
-            self.seq += 1
-            mb.post(W_ROWS, self.seq)
-            return
         rows = (np.empty(m, np.int32), np.empty(m, np.int32), np.empty(m, np.int64),
                 np.empty(m, np.int64))
         N.check(N.lib().pl_patch_rows(self.patch.h, *(N.ptr(x) for x in rows), m))
@@ -369,35 +384,33 @@ class PatchSender:
     def finish(self) -> tuple[int, int]:
         """Receive the reservation, push the cells into the remote pools, acknowledge."""
         if self.mb is not None:
-            mb = self.mb
-            mb.wait(W_REPLY, self.seq)
-            done = int(mb.words[W_DONE])
-            rc = int(np.int64(mb.words[W_ERR]))
-            err = None
-            if rc != N.PL_OK:
-                raw = bytes(np.ctypeslib.as_array((C.c_ubyte * 256).from_address(mb.base + 8 * W_MSG)))
-                err = (rc, raw.split(b"\0", 1)[0].decode(errors="replace"))
-            update, fds = {}, []
-            if mb.words[W_UPDATE]:
+            # wait for the reply, push into the remote pools, record + post "applied": one
+            # native call, two when the receiver re-exported its table or pools
+            need, rc, done = self._fin
+            N.check(N.lib().pl_pair_finish(self.patch.h, self.remote.h, self.mb.h, self.seq,
+                                           300_000, 0, *self._fin_refs))
+            if need.value:
                 (tag, update), fds = self.chan.recv()
                 assert tag == "update", tag
+                if "pools" in update:
+                    self.remote.import_groups(update["pools"], fds)
+                if "table" in update:
+                    self.remote.set_table(*update["table"])
+                N.check(N.lib().pl_pair_finish(self.patch.h, self.remote.h, self.mb.h, self.seq,
+                                               300_000, 1, *self._fin_refs))
+            err = None
+            if rc.value != N.PL_OK:
+                raw = bytes(np.ctypeslib.as_array((C.c_ubyte * 256).from_address(self.mb.base + 8 * W_MSG)))
+                err = (rc.value, raw.split(b"\0", 1)[0].decode(errors="replace"))
         else:
             msg, fds = self.chan.recv()
             assert msg[0] == "reserved", msg[0]
             _, done, err, update = msg
-        if "pools" in update:
-            self.remote.import_groups(update["pools"], fds)
-        if "table" in update:
-            self.remote.set_table(*update["table"])
-        if self.mb is not None:   # the push reads the table deltas of the reservation
-            self.mb.stream_wait(EV_RESERVED, self.patch.stream_ptr())
-        N.check(N.lib().pl_patch_push_remote(self.patch.h, self.remote.h, done))
-        if self.mb is not None:
-            # "applied" = an interprocess event after the push on the patch stream: the
-            # receiver's stream waits for it on the device; no host sync here
-            self.mb.record(EV_APPLIED, self.patch.stream_ptr())
-            self.mb.post(W_APPLIED, self.seq)
-        else:
+            if "pools" in update:
+                self.remote.import_groups(update["pools"], fds)
+            if "table" in update:
+                self.remote.set_table(*update["table"])
+            N.check(N.lib().pl_patch_push_remote(self.patch.h, self.remote.h, done))
             self.store.sync()   # the cells are in the receiver's HBM before it is told so
             self.chan.send(("applied",))
         if err is not None:

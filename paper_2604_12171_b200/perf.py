@@ -108,6 +108,9 @@ class NativePatch:
         N.check(N.lib().pl_patch_create(src._h, N.ptr(g), N.ptr(lpg), len(groups), C.byref(h)))
         self.h = h
         self.src = src
+        self._rank, self._rank_args = None, (None, 0)
+        self._keys, self._cells = C.c_int64(), C.c_int64()
+        self._keys_ref, self._cells_ref = C.byref(self._keys), C.byref(self._cells)
         N.check(N.lib().pl_patch_set_active(h, 1))
 
     def seed(self) -> int:
@@ -116,10 +119,13 @@ class NativePatch:
         return out.value
 
     def push(self, dst: KvStore, rank: np.ndarray) -> tuple[int, int]:
-        keys, cells = C.c_int64(), C.c_int64()
-        N.check(N.lib().pl_patch_push(self.h, dst._h, N.ptr(rank), len(rank), C.byref(keys),
-                                      C.byref(cells)))
-        return keys.value, cells.value
+        # ctypes argument objects are built once per rank array: numpy's .ctypes costs ~2 us,
+        # as much as a steady round's whole host enqueue
+        if self._rank is not rank:
+            self._rank, self._rank_args = rank, (N.ptr(rank), len(rank))
+        N.check(N.lib().pl_patch_push(self.h, dst._h, *self._rank_args, self._keys_ref,
+                                      self._cells_ref))
+        return self._keys.value, self._cells.value
 
     def stream_ptr(self) -> int:
         """The stream this pair's K3/K4/K5 are enqueued on."""
@@ -134,7 +140,10 @@ class NativePatch:
         keys = ("adopt_wait", "snapshot", "reserve", "dst_flush", "k3_enqueue", "copy_enqueue",
                 "total")
         d = {k: round(float(v), 4) for k, v in zip(keys, out)}
-        d["chunked"] = bool(out[7])
+        d["chunked"] = bool(out[7] == 1)
+        # launch-first steady round: the destination's host bookkeeping ran on the worker
+        # thread ("reserve" is then the worker's time, off the caller's path)
+        d["async_bookkeeping"] = bool(out[7] == 2)
         return d
 
     def mark_batch(self, reqs, groups, starts, counts) -> None:
@@ -533,8 +542,11 @@ def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16,
         rank = reg.rank()
         cases = [("decode", None)] + [(f"{r:g}", r) for r in rates]
         for name, r in cases:
-            times, dev, keys_n = [], [], 0
-            for _ in range(rounds + 1):
+            times, dev, book, keys_n = [], [], [], 0
+            # wall rounds first (kernel timing off: its event pairs would sit on the host
+            # path), then the same number of rounds with the kernels timed
+            for it in range(2 * (rounds + 1)):
+                timed = it > rounds
                 if r is None:
                     rq, gq, st = reqs, groups, [ctx - 1] * len(reqs)
                 else:
@@ -546,25 +558,34 @@ def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16,
                 patch.mark_batch(rq, gq, st, [1] * len(rq))
                 src.sync()
                 torch.cuda.synchronize(device)
-                N.check(N.lib().pl_timing_reset())
-                N.check(N.lib().pl_timing_enable(1))
+                if timed:
+                    N.check(N.lib().pl_timing_reset())
+                    N.check(N.lib().pl_timing_enable(1))
                 t0 = time.perf_counter()
                 keys, cells = patch.push(dst, rank)
                 dst.sync()
                 src.sync()
-                times.append(time.perf_counter() - t0)
-                N.check(N.lib().pl_timing_enable(0))
-                dev.append(N.timing("drain")[0] + N.timing("patch_push")[0]
-                           + N.timing("drain_push")[0])
+                t1 = time.perf_counter()
+                if timed:
+                    N.check(N.lib().pl_timing_enable(0))
+                    dev.append(N.timing("drain")[0] + N.timing("patch_push")[0]
+                               + N.timing("drain_push")[0])
+                elif it > 0:
+                    times.append(t1 - t0)
+                    book.append(patch.last_push_stats()["reserve"])
                 keys_n = keys
+            times = [0.0] + times   # (the first wall round is warm-up)
             t = float(np.median(times[1:]))
-            td = float(np.median(dev[1:])) / 1e3
+            td = float(np.median(dev)) / 1e3
             payload = keys_n * k * cell
             out.append({"tokens_per_block": s, "dirty": name, "keys": keys_n,
                         "payload_bytes": payload, "ms": round(t * 1e3, 4),
                         "gbs": round(payload / t / 1e9, 2),
                         "hbm_gbs": round(2 * (payload + 8 * keys_n) / t / 1e9, 2),
                         "kernel_ms": round(td * 1e3, 4),
+                        # destination write_slots bookkeeping, on the host worker thread for
+                        # launch-first rounds (off the round's wall time)
+                        "host_bookkeeping_ms": round(float(np.median(book)), 4),
                         "kernel_hbm_gbs": round(2 * (payload + 8 * keys_n) / td / 1e9, 2) if td else None})
         patch.close()
         del src, dst

@@ -27,7 +27,7 @@ def test_two_process_push_matches_single_process(seed):
         p.start()
     res = {}
     for _ in procs:
-        r = q.get(timeout=240)
+        r = q.get(timeout=120)
         assert not r[0].endswith("error"), r[1]
         res[r[0]] = r[1:]
     for p in procs:

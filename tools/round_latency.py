@@ -1,7 +1,9 @@
-"""Latency anatomy of one steady patch round (c5_sweep's decode pattern and 1 / 25 %
+"""Latency anatomy of one steady patch round (c5_sweep's decode pattern and 1 / 5 / 25 %
 random dirty rates, 64 requests x 2048 tokens x 2 k=4 groups, 16-token blocks):
-host enqueue time of pl_patch_push, device time of its kernels, wall time to a synced
-destination.  PL_TRACE_PUSH=1 adds the push's host phase split on stderr.
+host enqueue time of pl_patch_push, wall time to a synced destination (kernel timing
+off), the time until the host bookkeeping worker is idle again, and -- in separate rounds
+with kernel timing on -- the device time of the round's kernels.  PL_TRACE_PUSH=1 adds
+the push's host phase split on stderr.
 
     python tools/round_latency.py [rounds]
 """
@@ -38,9 +40,10 @@ dst.sync()
 rank = reg.rank()
 rng = np.random.default_rng(0)
 out = {}
-for name, r in (("decode", None), ("0.01", 0.01), ("0.25", 0.25)):
-    host, wall, dev = [], [], []
-    for it in range(rounds + 2):
+for name, r in (("decode", None), ("0.01", 0.01), ("0.05", 0.05), ("0.25", 0.25)):
+    host, wall, idle, dev, phases = [], [], [], [], []
+    for it in range(2 * rounds + 4):
+        timed_kernels = it >= rounds + 2
         if r is None:
             rq, gq, st = reqs, groups, [ctx - 1] * len(reqs)
         else:
@@ -52,21 +55,32 @@ for name, r in (("decode", None), ("0.01", 0.01), ("0.25", 0.25)):
         patch.mark_batch(rq, gq, st, [1] * len(rq))
         src.sync()
         torch.cuda.synchronize()
-        N.check(N.lib().pl_timing_reset())
-        N.check(N.lib().pl_timing_enable(1))
+        if timed_kernels:
+            N.check(N.lib().pl_timing_reset())
+            N.check(N.lib().pl_timing_enable(1))
         t0 = time.perf_counter()
         patch.push(dst, rank)
         t1 = time.perf_counter()
         dst.sync()
         src.sync()
         t2 = time.perf_counter()
-        N.check(N.lib().pl_timing_enable(0))
-        if it >= 2:
-            host.append((t1 - t0) * 1e6)
-            wall.append((t2 - t0) * 1e6)
+        patch.dirty_keys()          # any C-ABI call joins the host bookkeeping worker
+        t3 = time.perf_counter()
+        if timed_kernels:
+            N.check(N.lib().pl_timing_enable(0))
             dev.append((N.timing("drain")[0] + N.timing("patch_push")[0]
                         + N.timing("drain_push")[0]) * 1e3)
+        elif it >= 2:
+            host.append((t1 - t0) * 1e6)
+            wall.append((t2 - t0) * 1e6)
+            idle.append((t3 - t0) * 1e6)
+            phases.append(patch.last_push_stats())
     out[name] = {"keys": len(rq), "host_us": round(float(np.median(host)), 1),
                  "kernel_us": round(float(np.median(dev)), 1),
-                 "wall_us": round(float(np.median(wall)), 1)}
+                 "wall_us": round(float(np.median(wall)), 1),
+                 "wall_us_min": round(float(np.min(wall)), 1),
+                 "host_idle_us": round(float(np.median(idle)), 1),
+                 "host_phases_us": {k: round(1e3 * float(np.median([p[k] for p in phases])), 1)
+                                    for k in phases[0] if k not in ("chunked", "async_bookkeeping")},
+                 "async_bookkeeping": bool(phases[-1]["async_bookkeeping"])}
 print(json.dumps(out, indent=1))
