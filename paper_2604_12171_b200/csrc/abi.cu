@@ -83,6 +83,9 @@ class HostWorker {
       for (const void* t : tags) ++busy_[t];
       q_.push_back({std::move(job), std::move(tags)});
       pending_.fetch_add(1, std::memory_order_release);
+      queued_.store(true, std::memory_order_release);
+      // a worker still spinning after its last job picks this up without a futex wake
+      if (!sleeping_) return;
     }
     cv_.notify_all();
   }
@@ -122,10 +125,23 @@ class HostWorker {
   void run() {
     std::unique_lock<std::mutex> lk(mu_);
     for (;;) {
-      cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+      if (q_.empty() && !stop_) {
+        // steady rounds come every few tens of microseconds: spin ~50 us for the next job
+        // before sleeping (the submitter then skips the wake-up syscall)
+        lk.unlock();
+        const auto t0 = std::chrono::steady_clock::now();
+        while (!queued_.load(std::memory_order_acquire) &&
+               std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(50)) {
+        }
+        lk.lock();
+        sleeping_ = true;
+        cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+        sleeping_ = false;
+      }
       if (q_.empty()) return;
       Job job = std::move(q_.front());
       q_.pop_front();
+      if (q_.empty()) queued_.store(false, std::memory_order_release);
       lk.unlock();
       try {
         job.fn();
@@ -146,6 +162,8 @@ class HostWorker {
   std::deque<Job> q_;
   std::unordered_map<const void*, int> busy_;  // jobs queued or running per tag
   std::atomic<int64_t> pending_{0};
+  std::atomic<bool> queued_{false};  // q_ non-empty (read by the spinning worker)
+  bool sleeping_ = true;             // worker blocked in cv_.wait (guarded by mu_)
   std::atomic<bool> err_flag_{false};
   std::exception_ptr err_;
   bool stop_ = false;

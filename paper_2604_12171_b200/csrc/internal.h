@@ -392,6 +392,7 @@ struct Store {
   // next span of the staging ring: host/device pointers, sequence number
   void stage_span(size_t bytes, uint8_t** h, uint8_t** d, uint64_t* seq);
   void stage_commit(uint64_t seq);       // H2D of span seq enqueued on up_stream
+  void stage_reserve(size_t cap);        // (re)create an idle ring of at least cap bytes
   void stage_consumed(uint64_t seq) noexcept;  // consumers of span seq enqueued on stream
   cudaEvent_t ring_event();
   void materialise(int g);
@@ -570,7 +571,6 @@ struct Patch {
   CopyLaunch push_launch(Store* dst, const uint8_t* d_apply, uint8_t apply_id);
   void push_chunked(Store* dst, const int32_t* rank, int64_t n_rank);
   int64_t new_dst_blocks(Store* dst) const;
-  bool streams_idle(Store* dst) const;
   void apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
              int64_t n_stale);
   void push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells);
@@ -584,8 +584,9 @@ struct Patch {
   void push_remote(Remote* r, int64_t n_items_applied);
   int64_t device_dirty_count();
   bool fused_round() const;  // K3 + push in one launch for sparse rounds
-  void device_drain_push(Store* dst, const std::vector<uint8_t>* mask);
+  void device_drain_push(Store* dst, const std::vector<uint8_t>* mask, bool wait_dst = true);
   void launch_steady(Store* dst);
+  bool dst_needs_event(const Store* dst) const;
   // host phases of the last push (ms): adoption wait for lazily mapped pools, dirty-set
   // snapshot, destination reservation, destination table flush, K3 enqueue, copy enqueue,
   // total, chunked (1) or not (0)

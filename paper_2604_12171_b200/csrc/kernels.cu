@@ -477,20 +477,24 @@ __global__ void __launch_bounds__(kWarps * 32) copy_kernel(CopyLaunch c) {
 //          position -> destination block table) and broadcast it; then the stores.
 // Per key the dependent chain is: exchange -> {source load | owner -> table} -> store.
 constexpr int kFusedWords = 256;
+constexpr int kFusedMaxGroups = 64;
 __device__ __forceinline__ uint8_t* fused_dst(const CopyLaunch& c, int64_t cell, int64_t per_slot,
-                                              int* doff_out) {
+                                              const uint64_t* s_db, int* doff_out) {
   const int32_t slot = (int32_t)(cell / per_slot);
   const int64_t rem = cell % per_slot;
   const int32_t lg = (int32_t)(rem / c.src_s);
   const int off = (int)(rem % c.src_s);
+  // owner and position loads go out together; the group's pool base is in shared memory
   const int32_t req = c.src_owner[slot];
+  const int32_t oidx = c.src_owner_idx[slot];
   if (req < 0) return nullptr;
   if (c.apply_mask && !c.apply_mask[(int64_t)req * c.G + lg]) return nullptr;
-  const int64_t pos = (int64_t)c.src_owner_idx[slot] * c.src_s + off;
+  const int64_t pos = (int64_t)oidx * c.src_s + off;
   const int32_t dslot = c.dst_table[(int64_t)req * c.dst_max_chain + pos / c.dst_s];
   if (dslot < 0) return nullptr;
   *doff_out = (int)(pos % c.dst_s);
-  return reinterpret_cast<uint8_t*>(c.dst_bases[c.src_groups[lg]]) + (int64_t)dslot * c.dst_unit;
+  const uint64_t dbase = s_db ? s_db[lg] : c.dst_bases[c.src_groups[lg]];
+  return reinterpret_cast<uint8_t*>(dbase) + (int64_t)dslot * c.dst_unit;
 }
 
 __global__ void __launch_bounds__(256)
@@ -498,6 +502,13 @@ drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, int W, unsigned
                   unsigned long long* next_count) {
   __shared__ uint16_t queue[kFusedWords * 32];
   __shared__ int q_n;
+  __shared__ uint64_t s_sb[kFusedMaxGroups], s_db[kFusedMaxGroups];
+  const bool smem_bases = c.G <= kFusedMaxGroups;
+  if (smem_bases && threadIdx.x < c.G) {  // visible after the first pass's barrier
+    const int32_t g = c.src_groups[threadIdx.x];
+    s_sb[threadIdx.x] = c.src_bases[g];
+    s_db[threadIdx.x] = c.dst_bases[g];
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) *next_count = 0ull;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -530,68 +541,86 @@ drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, int W, unsigned
       queue[start++] = (uint16_t)(threadIdx.x * 32 + b);
     }
     __syncthreads();
+    // copy: warp w takes `per` consecutive (key, layer) items of the queue; lane l owns item
+    // l of the batch.  Source pointers need no global load (cell index from the queue,
+    // pool base in shared memory), so the batch's first two cells are loaded before the
+    // lanes resolve their destinations (owner map -> block table: all lanes' chains in
+    // flight together); then the warp streams the batch two cells at a time.
     const int n_items = q_n * c.k;
-    for (int it = warp; it < n_items; it += 2 * nwarps) {
-      // items it and it + nwarps: (key, layer) = (it / k, it % k)
-      int64_t cell[2];
-      int j[2];
-      bool have[2];
-      const uint8_t* su[2];
-      int off[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int x = it + h * nwarps;
-        have[h] = x < n_items;
-        const int q = have[h] ? x / c.k : 0;
-        j[h] = have[h] ? x - q * c.k : 0;
-        cell[h] = base * 32 + queue[q];
-        const int32_t slot = (int32_t)(cell[h] / per_slot);
-        const int64_t rem = cell[h] % per_slot;
-        off[h] = (int)(rem % c.src_s);
-        su[h] = reinterpret_cast<const uint8_t*>(c.src_bases[c.src_groups[(int)(rem / c.src_s)]]) +
-                (int64_t)slot * c.src_unit;
+    const int per = min(32, (n_items + nwarps - 1) / nwarps);
+    for (int b0 = warp * per; b0 < n_items; b0 += nwarps * per) {
+      const int nb = min(per, n_items - b0);
+      const bool mine = lane < nb;
+      const uint8_t* sp = nullptr;
+      const uint64_t* sfp = nullptr;
+      int64_t cell = 0;
+      int j = 0;
+      if (mine) {
+        const int x = b0 + lane;
+        const int q = x / c.k;
+        j = x - q * c.k;
+        cell = base * 32 + queue[q];
+        const int32_t slot = (int32_t)(cell / per_slot);
+        const int64_t rem = cell - (int64_t)slot * per_slot;
+        const int lgh = (int)(rem / c.src_s);
+        const int off = (int)(rem - (int64_t)lgh * c.src_s);
+        const uint8_t* unit =
+            reinterpret_cast<const uint8_t*>(smem_bases ? s_sb[lgh] : c.src_bases[c.src_groups[lgh]]) +
+            (int64_t)slot * c.src_unit;
+        sp = unit + c.fp_bytes + ((int64_t)j * c.src_s + off) * c.cell_bytes;
+        sfp = reinterpret_cast<const uint64_t*>(unit) + off;
       }
-      // source loads first (independent of the destination)
       int4 buf[2][U];
-      uint64_t fp = 0;
+      // the first pair's loads go out before anything waits
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int4* s4 = reinterpret_cast<const int4*>(su[h] + c.fp_bytes +
-                                                       ((int64_t)j[h] * c.src_s + off[h]) * c.cell_bytes);
+        const int4* s4 = reinterpret_cast<const int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), h));
+        if (h < nb)
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t e = lane + 32 * u;
-          if (have[h] && e < vecs) buf[h][u] = ld_stream(s4 + e);
+          for (int u = 0; u < U; ++u)
+            if (lane + 32 * u < vecs) buf[h][u] = ld_stream(s4 + lane + 32 * u);
+      }
+      // destination of the lane's own item; the key's fingerprint word rides along (layer 0)
+      uint8_t* dp = nullptr;
+      uint64_t* dfp = nullptr;
+      uint64_t fpv = 0;
+      if (mine) {
+        int doff = 0;
+        uint8_t* du = fused_dst(c, cell, per_slot, smem_bases ? s_db : nullptr, &doff);
+        if (du) {
+          dp = du + c.fp_bytes + ((int64_t)j * c.dst_s + doff) * c.cell_bytes;
+          if (j == 0) {
+            dfp = reinterpret_cast<uint64_t*>(du) + doff;
+            fpv = *sfp;
+          }
         }
       }
-      // destination: lane h resolves item h; the fingerprint word rides along (layer 0)
-      uint8_t* du = nullptr;
-      int doff = 0;
-      if (lane < 2) {
-        const bool hv = lane ? have[1] : have[0];
-        if (hv) {
-          du = fused_dst(c, lane ? cell[1] : cell[0], per_slot, &doff);
-          if (du && (lane ? j[1] : j[0]) == 0)
-            fp = reinterpret_cast<const uint64_t*>(lane ? su[1] : su[0])[lane ? off[1] : off[0]];
+      for (int i = 0; i < nb; i += 2) {
+        if (i > 0) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int4* s4 = reinterpret_cast<const int4*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), i + h));
+            if (i + h < nb)
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+                if (lane + 32 * u < vecs) buf[h][u] = ld_stream(s4 + lane + 32 * u);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int4* d4 = reinterpret_cast<int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dp), i + h));
+          const int4* s4 = reinterpret_cast<const int4*>(
+              __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), i + h));
+          if (i + h >= nb || !d4) continue;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (lane + 32 * u < vecs) st_stream(d4 + lane + 32 * u, buf[h][u]);
+          // cells wider than 32 x U x 16 B (not the Llama shapes): the rest, plainly
+          for (int64_t e = lane + 32 * U; e < vecs; e += 32) st_stream(d4 + e, ld_stream(s4 + e));
         }
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint8_t* d = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(du), h));
-        const int dof = __shfl_sync(0xffffffffu, doff, h);
-        if (!have[h] || !d) continue;
-        if (lane == h && j[h] == 0) reinterpret_cast<uint64_t*>(d)[dof] = fp;
-        int4* d4 = reinterpret_cast<int4*>(d + c.fp_bytes + ((int64_t)j[h] * c.dst_s + dof) * c.cell_bytes);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t e = lane + 32 * u;
-          if (e < vecs) st_stream(d4 + e, buf[h][u]);
-        }
-        // cells wider than 32 x U x 16 B (not the Llama shapes): the rest, plainly
-        const int4* s4 = reinterpret_cast<const int4*>(su[h] + c.fp_bytes +
-                                                       ((int64_t)j[h] * c.src_s + off[h]) * c.cell_bytes);
-        for (int64_t e = lane + 32 * U; e < vecs; e += 32) st_stream(d4 + e, ld_stream(s4 + e));
-      }
+      if (dfp) *dfp = fpv;
     }
     __syncthreads();  // the queue is rebuilt for the next pass
   }
@@ -620,8 +649,123 @@ void launch_drain_push(const CopyLaunch& c, uint32_t* bits, int64_t n_words, int
   PL_CUDA(cudaGetLastError());
 }
 
+// K4/K5 push, batched resolve (mode 2).  copy_kernel<2> resolves one item at a time: per
+// 4 KiB cell a warp waits on cells[] -> owner -> block table before its loads go out, so a
+// sparse round (random cells, each a separate dependent chain) leaves HBM idle between
+// chains.  Here a warp takes `batch` consecutive items: lane l resolves item l (all
+// lanes' chains in flight together), then the warp copies the batch two cells at a time
+// with the pointers broadcast by shuffle.  Per-local-group pool bases are staged in
+// shared memory once per CTA (no base-pointer loads on the chain).  The fingerprint word
+// of a key (layer 0) is loaded during the resolve and stored after the cells.
+constexpr int kMaxSmemGroups = 64;
+__global__ void __launch_bounds__(kWarps * 32) push_batched_kernel(CopyLaunch c, int batch) {
+  __shared__ uint64_t s_sb[kMaxSmemGroups], s_db[kMaxSmemGroups];
+  const bool smem_bases = c.G <= kMaxSmemGroups;
+  if (smem_bases && threadIdx.x < c.G) {
+    const int32_t g = c.src_groups[threadIdx.x];
+    s_sb[threadIdx.x] = c.src_bases[g];
+    s_db[threadIdx.x] = c.dst_bases[g];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_rows = c.count ? min(*c.count, c.n_hint) : c.n_hint;
+  const int64_t items = n_rows * c.k;
+  const int64_t vecs = c.cell_bytes >> 4;
+  const int64_t per_slot = (int64_t)c.G * c.src_s;
+  constexpr int U = 8;
+  for (int64_t b0 = warp0 * batch; b0 < items; b0 += nwarps * batch) {
+    const uint8_t* sp = nullptr;
+    uint8_t* dp = nullptr;
+    uint64_t* dfp = nullptr;
+    uint64_t fpv = 0;
+    const int64_t item = b0 + lane;
+    if (lane < batch && item < items) {
+      const int64_t r = item / c.k;
+      const int j = (int)(item - r * c.k);
+      const int64_t cell = c.cells[r];
+      const int32_t slot = (int32_t)(cell / per_slot);
+      const int64_t rem = cell - (int64_t)slot * per_slot;
+      const int32_t lg = (int32_t)(rem / c.src_s);
+      const int off = (int)(rem - (int64_t)lg * c.src_s);
+      const int32_t req = c.src_owner[slot];
+      const int32_t oidx = c.src_owner_idx[slot];
+      const uint64_t sbase = smem_bases ? s_sb[lg] : c.src_bases[c.src_groups[lg]];
+      const uint8_t* unit = reinterpret_cast<const uint8_t*>(sbase) + (int64_t)slot * c.src_unit;
+      bool ok = req >= 0;
+      if (ok && c.apply_mask) {
+        const uint8_t m = c.apply_mask[(int64_t)req * c.G + lg];
+        ok = c.apply_id ? m == c.apply_id : m != 0;
+      }
+      if (ok) {
+        const int64_t pos = (int64_t)oidx * c.src_s + off;
+        const int32_t dslot = c.dst_table[(int64_t)req * c.dst_max_chain + pos / c.dst_s];
+        if (dslot >= 0) {
+          const int doff = (int)(pos % c.dst_s);
+          const uint64_t dbase = smem_bases ? s_db[lg] : c.dst_bases[c.src_groups[lg]];
+          uint8_t* du = reinterpret_cast<uint8_t*>(dbase) + (int64_t)dslot * c.dst_unit;
+          sp = unit + c.fp_bytes + ((int64_t)j * c.src_s + off) * c.cell_bytes;
+          dp = du + c.fp_bytes + ((int64_t)j * c.dst_s + doff) * c.cell_bytes;
+          if (j == 0) {
+            dfp = reinterpret_cast<uint64_t*>(du) + doff;
+            fpv = reinterpret_cast<const uint64_t*>(unit)[off];
+          }
+        }
+      }
+    }
+    const int nb = (int)min((int64_t)batch, items - b0);
+    for (int i = 0; i < nb; i += 2) {
+      const int4* s4[2];
+      int4* d4[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        s4[h] = reinterpret_cast<const int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), i + h));
+        d4[h] = reinterpret_cast<int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dp), i + h));
+        if (i + h >= nb) d4[h] = nullptr;
+      }
+      int4 buf[2][U];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (d4[h])
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (lane + 32 * u < vecs) buf[h][u] = ld_stream(s4[h] + lane + 32 * u);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (d4[h]) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (lane + 32 * u < vecs) st_stream(d4[h] + lane + 32 * u, buf[h][u]);
+          // cells wider than 32 x U x 16 B (not the Llama shapes): the rest, plainly
+          for (int64_t e = lane + 32 * U; e < vecs; e += 32) st_stream(d4[h] + e, ld_stream(s4[h] + e));
+        }
+    }
+    if (dfp) *dfp = fpv;
+  }
+}
+
 void launch_copy(const CopyLaunch& c, cudaStream_t st) {
   if (c.n_hint <= 0) return;
+  // mode 2 takes the batched-resolve kernel unless PL_PUSH_BATCHED=0 (A/B timing)
+  static const int batched = [] {
+    const char* v = std::getenv("PL_PUSH_BATCHED");
+    return v ? std::atoi(v) : 1;
+  }();
+  if (c.mode == 2 && batched) {
+    // batch = items per warp over a grid of up to 16 waves of 8-warp CTAs, 2..32
+    const int64_t items = c.n_hint * c.k;
+    const int64_t cap_warps = (int64_t)sm_count() * 16 * kWarps;
+    int64_t b = (items + cap_warps - 1) / cap_warps;
+    b = std::min<int64_t>(32, std::max<int64_t>(2, (b + 1) & ~int64_t(1)));
+    const int64_t grid = std::max<int64_t>(1, (items + b * kWarps - 1) / (b * kWarps));
+    KernelTimer timer("patch_push", st);
+    push_batched_kernel<<<(unsigned)std::min<int64_t>(grid, (int64_t)sm_count() * 16), kWarps * 32,
+                          0, st>>>(c, (int)b);
+    note_launch();
+    PL_CUDA(cudaGetLastError());
+    return;
+  }
   const int64_t grid = grid_for(c.n_hint * c.k, kWarps, 16);
   KernelTimer timer(c.mode == 0 ? "patch_gather" : (c.mode == 1 ? "patch_scatter" : "patch_push"), st);
   switch (c.mode) {

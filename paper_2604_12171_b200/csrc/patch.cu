@@ -57,6 +57,16 @@ Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n)
   PL_CUDA(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_mask, cudaEventDisableTiming));
   ensure_bits();
+  // the drain's cell list, the chunked push's run buckets and the staged apply mask are
+  // sized for a bulk round over every source cell (up to 8 M keys) now: the first round of
+  // a migration then allocates nothing (a cudaMalloc / cudaMallocHost costs milliseconds)
+  const int64_t pre = std::min<int64_t>(n_words * 32, (int64_t)8 << 20);
+  PL_CUDA(cudaMalloc(&d_cells, sizeof(int64_t) * pre));
+  PL_CUDA(cudaMalloc(&d_part, sizeof(int64_t) * pre));
+  cells_cap = part_cap = pre;
+  mask_cap = 64 << 10;
+  PL_CUDA(cudaMallocHost(&h_mask, mask_cap));
+  PL_CUDA(cudaMalloc(&d_mask, mask_cap));
   src->patches.push_back(this);
 }
 
@@ -149,7 +159,6 @@ static int64_t chunk_min_blocks() {
   return v ? std::max<int64_t>(1, std::atoll(v)) : kChunkedPushMinBlocks;
 }
 static bool no_chunking() { return std::getenv("PL_PUSH_NO_CHUNK") != nullptr; }
-static bool forced_chunking() { return std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS") != nullptr; }
 // PL_PUSH_NO_LAUNCH_FIRST=1: reserve on the host before launching even when no destination
 // block is allocated (A/B timing of the steady-round reordering)
 static bool launch_first_off() {
@@ -504,20 +513,6 @@ void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t
   if (status != PL_OK) fail(status, dst->last_msg);
 }
 
-// Pipelining the reservation only pays when the device would otherwise wait for it.  If
-// the streams the copy depends on still have work queued (a caller that runs ahead of the
-// device, e.g. the next step's appends already enqueued), the host reservation is hidden
-// behind that work and one launch avoids the per-run grid tails.
-bool Patch::streams_idle(Store* dst) const {
-  const cudaStream_t ss[3] = {pstream(), src->stream, dst->stream};
-  for (cudaStream_t s : ss) {
-    const cudaError_t q = cudaStreamQuery(s);
-    if (q == cudaErrorNotReady) return false;
-    PL_CUDA(q);
-  }
-  return true;
-}
-
 int64_t Patch::new_dst_blocks(Store* dst) const {
   // destination blocks the drained set will allocate: per request, the chain it needs past
   // the chain it has (the chain is shared by the request's groups)
@@ -626,10 +621,15 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
                         G, d_blob, (int64_t)n_mask, d_run_off, d_run_cnt, d_part, pstream());
   int status = PL_OK;
   size_t launched = 0;
+  double t_reserve = 0, t_flush = 0, t_launch = 0;
+  const double t_pre = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   for (size_t c = 0; c < n_runs; ++c) {
+    const auto tr = std::chrono::steady_clock::now();
     size_t x = cut[c];
     for (; x < cut[c + 1]; ++x)
       if (!reserve_item(dst, order[x], &status)) break;
+    const auto tf = std::chrono::steady_clock::now();
+    t_reserve += std::chrono::duration<double, std::milli>(tf - tr).count();
     const uint8_t* d_apply = nullptr;
     if (status != PL_OK) {
       // KvOverflow inside run c: its items from x on are not applied (the reference's
@@ -642,6 +642,8 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
     }
     PL_CUDA(cudaSetDevice(dst->device));
     dst->flush();
+    const auto tl = std::chrono::steady_clock::now();
+    t_flush += std::chrono::duration<double, std::milli>(tl - tf).count();
     PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
     PL_CUDA(cudaSetDevice(src->device));
     PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
@@ -651,15 +653,23 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
     cl.n_hint = run_keys[c];
     for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);  // pool mapped (lazy groups)
     launch_copy(cl, pstream());
+    t_launch += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
     ++launched;
     if (status != PL_OK) break;
   }
   drained.clear();
+  // host phases of a chunked round: before the first run (order, blob, K3 + partition
+  // enqueue), block reservation, table-delta flushes, copy launches
+  push_stats[2] = t_reserve;
+  push_stats[3] = t_flush;
+  push_stats[4] = t_pre;
+  push_stats[5] = t_launch;
   if (trace)
-    std::fprintf(stderr, "[pl] push (chunked): %zu items in %zu runs, %zu launches, host %.3f ms, "
-                 "%lld keys\n", order.size(), n_runs, launched,
+    std::fprintf(stderr, "[pl] push (chunked): %zu items in %zu runs, %zu launches, host %.3f ms "
+                 "(pre %.3f, reserve %.3f, flush %.3f, launch %.3f), %lld keys\n", order.size(),
+                 n_runs, launched,
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
-                 (long long)drained_keys);
+                 t_pre, t_reserve, t_flush, t_launch, (long long)drained_keys);
   PL_CUDA(cudaEventRecord(ev_applied, pstream()));
   applied_recorded = true;
   PL_CUDA(cudaSetDevice(dst->device));
@@ -670,13 +680,21 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
 // The device side of a launch-first steady round: K3 + the push (or the fused kernel),
 // ordered after the destination stream's queued work; the destination stream then waits
 // for the copy.
+// The copy must follow the destination stream's queued work (ev_dst) unless that stream is
+// the patch stream itself, or the source's stream (whose ev_src, recorded later, covers it).
+bool Patch::dst_needs_event(const Store* dst) const {
+  return dst->stream != pstream() && dst->stream != src->stream;
+}
+
 void Patch::launch_steady(Store* dst) {
-  PL_CUDA(cudaSetDevice(dst->device));
+  const bool same_dev = dst->device == src->device;
+  if (!same_dev) PL_CUDA(cudaSetDevice(dst->device));
   dst->flush();
-  PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
-  PL_CUDA(cudaSetDevice(src->device));
+  const bool dst_ev = dst_needs_event(dst);
+  if (dst_ev) PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
+  if (!same_dev) PL_CUDA(cudaSetDevice(src->device));
   if (fused_round()) {
-    device_drain_push(dst, nullptr);
+    device_drain_push(dst, nullptr, dst_ev);
     return;
   }
   device_drain_compact();
@@ -684,13 +702,15 @@ void Patch::launch_steady(Store* dst) {
     PL_CUDA(cudaEventRecord(ev_src, src->stream));
     PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
   }
-  PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
+  if (dst_ev) PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
   launch_copy(push_launch(dst, nullptr, 0), pstream());
   PL_CUDA(cudaEventRecord(ev_applied, pstream()));
   applied_recorded = true;
-  PL_CUDA(cudaSetDevice(dst->device));
-  PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
-  PL_CUDA(cudaSetDevice(src->device));
+  if (dst->stream != pstream()) {
+    if (!same_dev) PL_CUDA(cudaSetDevice(dst->device));
+    PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
+    if (!same_dev) PL_CUDA(cudaSetDevice(src->device));
+  }
 }
 
 void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells) {
@@ -720,8 +740,10 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   const int64_t new_blocks = new_dst_blocks(dst);
   bool dst_pools = true;
   for (int32_t g : groups) dst_pools = dst_pools && dst->materialised[g];
-  const bool chunk = dirty.size() >= 2 && !no_chunking() && new_blocks >= chunk_min_blocks() &&
-                     (forced_chunking() || streams_idle(dst));
+  // a round that allocates many destination blocks (a cold bulk round) always pipelines
+  // its reservation with the copy: per-run grid tails cost ~0.1 ms, the reservation
+  // ~0.1 us per block on the critical path otherwise
+  const bool chunk = dirty.size() >= 2 && !no_chunking() && new_blocks >= chunk_min_blocks();
   const bool launch_first = !chunk && new_blocks == 0 && dst_pools && dirty_keys > 0 &&
                             !launch_first_off();
   if (launch_first && host_async_enabled()) {
@@ -842,7 +864,7 @@ bool Patch::fused_round() const {
   return !off && drained_keys > 0 && drained_keys <= lim;
 }
 
-void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask) {
+void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask, bool wait_dst) {
   src->flush();
   cudaStream_t ps = pstream();
   uint32_t* old = d_bits;  // epoch flip, as device_drain_compact
@@ -853,7 +875,7 @@ void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask) {
     PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
   }
   const uint8_t* d_apply = mask ? stage_mask(*mask) : nullptr;
-  PL_CUDA(cudaStreamWaitEvent(ps, ev_dst, 0));
+  if (wait_dst) PL_CUDA(cudaStreamWaitEvent(ps, ev_dst, 0));
   for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);
   cnt_cur ^= 1;
   d_count = d_cnt + cnt_cur;
@@ -864,9 +886,12 @@ void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask) {
   snap_ev = ev_applied;
   snap_recorded = true;
   applied_recorded = true;
-  PL_CUDA(cudaSetDevice(dst->device));
-  PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
-  PL_CUDA(cudaSetDevice(src->device));
+  if (dst->stream != ps) {
+    const bool same_dev = dst->device == src->device;
+    if (!same_dev) PL_CUDA(cudaSetDevice(dst->device));
+    PL_CUDA(cudaStreamWaitEvent(dst->stream, ev_applied, 0));
+    if (!same_dev) PL_CUDA(cudaSetDevice(src->device));
+  }
 }
 
 int64_t Patch::device_dirty_count() {

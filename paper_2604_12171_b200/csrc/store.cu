@@ -66,6 +66,9 @@ Store::Store(int device_, int gpu_id_, int k_, int s_, int64_t cell_bytes_, int 
   for (int64_t i = 0; i < capacity; ++i) new_block();
   ensure_owner(std::max<int64_t>(capacity, 1));
   ensure_table(0, 1);
+  // the staging ring is sized for a whole-mirror table upload (flush) at this capacity
+  // now, so the first bulk round does not pay a pinned allocation
+  stage_reserve((size_t)std::min<int64_t>(std::max<int64_t>(capacity * 12 * 4, 1 << 20), 64 << 20));
   for (int i = 0; i < n_groups; ++i) {
     int g = groups[i];
     if (g < 0 || g >= n_model_groups) fail(PL_E_INVALID, "resident group out of range");
@@ -405,6 +408,21 @@ void Store::stage_span(size_t bytes, uint8_t** h, uint8_t** d, uint64_t* seq) {
   *seq = ++ring_seq;
   ring_live.push_back({a, b, *seq, ring.get(), nullptr, nullptr});
 }
+void Store::stage_reserve(size_t cap) {
+  if (ring && ring->cap >= cap) return;
+  if (!up_stream) PL_CUDA(cudaStreamCreateWithFlags(&up_stream, cudaStreamNonBlocking));
+  if (!ring_live.empty()) return;  // spans in flight: stage_span grows the ring itself
+  if (ring) {
+    PL_CUDA(cudaStreamSynchronize(up_stream));
+    cudaFreeHost(ring->h);
+    cudaFree(ring->d);
+  }
+  ring = std::make_unique<StagingRing>();
+  ring->cap = cap;
+  PL_CUDA(cudaMallocHost(&ring->h, cap));
+  PL_CUDA(cudaMalloc(&ring->d, cap));
+  ring_head = 0;
+}
 void Store::stage_commit(uint64_t seq) {
   for (auto it = ring_live.rbegin(); it != ring_live.rend(); ++it)
     if (it->seq == seq) {
@@ -483,6 +501,24 @@ void Store::flush() {
   // a released slot may still be read by a patch's in-flight copy on its side stream
   // (owner map, cells): its owner delta and bit clears wait for that copy
   if (!released_slots.empty()) order_after_patches();
+  const size_t mirror_bytes = 4 * (h_table.size() + 2 * (size_t)owner_cap);
+  if (!deltas.empty() && mirror_bytes <= 16 * deltas.size()) {
+    // as many deltas as mirror entries (a bulk round's reservations): upload the table and
+    // owner mirrors whole -- one contiguous H2D and three device copies instead of the
+    // per-entry dedupe and scatter
+    deltas.clear();
+    Upload up(this);
+    const int a = up.add(h_table.data(), 4 * h_table.size());
+    const int b = up.add(h_owner.data(), 4 * (size_t)owner_cap);
+    const int c = up.add(h_owner_idx.data(), 4 * (size_t)owner_cap);
+    up.go();
+    PL_CUDA(cudaMemcpyAsync(d_table, up.ptr<int32_t>(a), 4 * h_table.size(),
+                            cudaMemcpyDeviceToDevice, stream));
+    PL_CUDA(cudaMemcpyAsync(d_owner, up.ptr<int32_t>(b), 4 * (size_t)owner_cap,
+                            cudaMemcpyDeviceToDevice, stream));
+    PL_CUDA(cudaMemcpyAsync(d_owner_idx, up.ptr<int32_t>(c), 4 * (size_t)owner_cap,
+                            cudaMemcpyDeviceToDevice, stream));
+  }
   if (!deltas.empty()) {
     // dedupe: one update per touched (array, index), value from the host mirror (which
     // always holds the latest write); O(deltas) with per-array queued flags

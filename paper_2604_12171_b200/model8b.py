@@ -158,8 +158,13 @@ class Pipeline8B:
             first[gpu] = min(first.get(gpu, layer), layer)
         return sorted(first, key=first.get)
 
-    def step(self, tokens) -> "object":
-        """One decode step of every request (token ids [B] on device) -> next tokens [B]."""
+    def step(self, tokens, in_step_rounds: bool = False) -> "object":
+        """One decode step of every request (token ids [B] on device) -> next tokens [B].
+
+        With `in_step_rounds`, each migrating pair's patch round is enqueued as soon as
+        the step has written the last layer of the pair's groups (MigrationStream.pump on
+        on_kv_written, migrator.py:190-197, 208-225): the round then overlaps the rest of
+        the step's compute instead of trailing it."""
         torch, sh, B = self.torch, self.sh, self.B
         pos_t = torch.tensor(self.pos, dtype=torch.int32, device=self.dev)
         ctx_t = pos_t + 1
@@ -214,6 +219,10 @@ class Pipeline8B:
                 h = self._rms(x, w["mlp_norm"])
                 a = h @ w["w13"]
                 x = x + ((torch.nn.functional.silu(a[:, : sh.ffn]) * a[:, sh.ffn:]) @ w["w2"]).float()
+                if in_step_rounds:
+                    for pair, layers in self.moving.items():
+                        if l == max(layers):
+                            self.pump(pairs=[pair])
         logits = self._rms(x, self.w["final_norm"]) @ self.w["lm_head"]
         for i in range(B):
             self.pos[i] += 1
@@ -251,7 +260,7 @@ class Pipeline8B:
             before_bulk()
         return self.pump()
 
-    def pump(self) -> dict:
+    def pump(self, pairs=None) -> dict:
         """One patch round per pair (MigrationStream.pump -> _drain -> _send_patch ->
         PatchReceiver.receive): K3 + fused K4/K5 on the side stream; the round's cells
         count as applied once its event has completed."""
@@ -259,6 +268,8 @@ class Pipeline8B:
         rank = self.registry.rank()
         keys_total = cells_total = 0
         for pair, p in self.patches.items():
+            if pairs is not None and pair not in pairs:
+                continue
             keys, cells = p.push(self.stores[pair[1]], rank)
             keys_total += keys
             cells_total += cells
@@ -345,7 +356,10 @@ def run_live(batch: int = 256, ctx: int = 2048, steps: int = 40, reconfig_at: in
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             th = time.perf_counter()
             e0.record(pipe.stream)
-            nxt = pipe.step(tokens)
+            # while migrating, every pair's round is enqueued inside the step right after
+            # the pair's last source layer (overlapping the rest of the step), so the
+            # next step's poll sees the lag the reference's poll would (migrator.py:74-90)
+            nxt = pipe.step(tokens, in_step_rounds=(phase == "migrating"))
             e1.record(pipe.stream)
             tok_host = nxt.cpu()                   # greedy: the next inputs come back
             host_ms = (time.perf_counter() - th) * 1e3
@@ -364,8 +378,6 @@ def run_live(batch: int = 256, ctx: int = 2048, steps: int = 40, reconfig_at: in
                         "host_enqueue_ms": round((time.perf_counter() - tb) * 1e3 - pipe.map_ms, 3),
                         "host_phases_ms": r["host_phases_ms"], "events": (b0, b1)}
                 phase = "migrating"
-            elif phase == "migrating":
-                pipe.pump()                        # one patch round per decode step
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_run
     step_ms = [a.elapsed_time(b) for a, b, _ in out["step_ms"]]
