@@ -280,6 +280,10 @@ int pl_patch_stream(pl_patch* p, void** out);
 int pl_remote_create(int device, int tokens_per_block, int stacking_factor, int64_t cell_bytes,
                      int64_t fp_bytes, int64_t unit_bytes, int num_model_groups, pl_remote** out);
 int pl_remote_destroy(pl_remote* r);
+/* post-commit teardown (Coordinator._post_commit_cleanup, coordinator.py:340-354) without a
+ * host wait: the view is unmapped and freed on a background thread once the work enqueued
+ * on `stream` (the last pushes through it) has run; r is invalid on return */
+int pl_remote_destroy_after(pl_remote* r, void* stream);
 int pl_remote_import_group(pl_remote* r, int group, const int* fds, int n, int64_t chunk_bytes);
 int pl_remote_drop_group(pl_remote* r, int group);
 int pl_remote_set_table(pl_remote* r, const void* ipc_handle, int64_t max_reqs, int64_t max_chain);

@@ -155,6 +155,7 @@ SIGNATURES = [
     ("pl_store_reserve_rows", C.c_int, [vp, i64, vp, vp, vp, vp, P(i64)]),
     ("pl_remote_create", C.c_int, [C.c_int, C.c_int, C.c_int, i64, i64, i64, C.c_int, P(vp)]),
     ("pl_remote_destroy", C.c_int, [vp]),
+    ("pl_remote_destroy_after", C.c_int, [vp, vp]),
     ("pl_remote_import_group", C.c_int, [vp, C.c_int, vp, C.c_int, i64]),
     ("pl_remote_drop_group", C.c_int, [vp, C.c_int]),
     ("pl_remote_set_table", C.c_int, [vp, vp, i64, i64]),

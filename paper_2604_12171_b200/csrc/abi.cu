@@ -129,9 +129,13 @@ class HostWorker {
         // steady rounds come every few tens of microseconds: spin ~50 us for the next job
         // before sleeping (the submitter then skips the wake-up syscall)
         lk.unlock();
+        static const int spin_us = [] {  // PL_WORKER_SPIN_US=0: sleep at once (A/B)
+          const char* v = std::getenv("PL_WORKER_SPIN_US");
+          return v ? std::max(0, std::atoi(v)) : 50;
+        }();
         const auto t0 = std::chrono::steady_clock::now();
         while (!queued_.load(std::memory_order_acquire) &&
-               std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(50)) {
+               std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(spin_us)) {
         }
         lk.lock();
         sleeping_ = true;
@@ -1057,6 +1061,14 @@ int pl_remote_destroy(pl_remote* r) {
     if (!r) return;
     delete r->r;
     delete r;
+  });
+}
+int pl_remote_destroy_after(pl_remote* r, void* stream) {
+  return guard([&] {
+    if (!r) return;
+    pl::Remote* rm = r->r;
+    delete r;
+    pl::remote_destroy_after(rm, static_cast<cudaStream_t>(stream));
   });
 }
 int pl_remote_import_group(pl_remote* r, int group, const int* fds, int n, int64_t chunk_bytes) {

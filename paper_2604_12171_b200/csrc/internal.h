@@ -181,7 +181,10 @@ struct Remote {
   void import_group(int g, const int* fds, int n, size_t chunk_bytes);
   void drop_group(int g);
   void set_table(const void* ipc_handle, int64_t max_reqs, int64_t max_chain);
+  bool detached = false;  // torn down by remote_destroy_after's thread
 };
+// event-gated teardown of a remote view on a detached thread (takes ownership of r)
+void remote_destroy_after(Remote* r, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 struct BlockRec {
@@ -339,7 +342,7 @@ struct Store {
   std::vector<Patch*> patches;  // patches whose source is this store
   uint64_t* d_bases_ = nullptr;  // device copy of the per-group arena bases
   std::string last_msg;
-  void refresh_bases();
+  void refresh_bases(bool wait = true);
   int64_t last_resize[4] = {0, 0, 0, 0};
 
   Store(int device, int gpu_id, int k, int s, int64_t cell_bytes, int n_model_groups,
@@ -501,6 +504,9 @@ struct Patch {
   std::map<std::pair<int32_t, int32_t>, std::vector<Interval>> dirty;
   int64_t dirty_keys = 0;
   int64_t dirty_cells = 0;  // dirty keys x pair layers of their group
+  std::vector<int64_t> top_dirty;  // per request: highest dirty end position (0: none)
+  std::vector<int32_t> top_reqs;   // requests with top_dirty set since the last drain
+  void note_top(int32_t req, int64_t end);
 
   // device bitmaps over source cells: bit ((slot*G + lg)*s + off).  Double-buffered
   // epochs: K1 marks d_bits; a drain flips the epoch and drains the previous buffer on

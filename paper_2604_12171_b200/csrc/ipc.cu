@@ -18,6 +18,7 @@
 // Only the interval rows and a reply cross the control channel (a few KB per round).
 #include <algorithm>
 #include <cstring>
+#include <thread>
 
 #include "internal.h"
 
@@ -35,10 +36,29 @@ Remote::Remote(int dev, int s_, int k_, int64_t cell, int64_t fp, int64_t unit, 
 
 Remote::~Remote() {
   cudaSetDevice(device);
-  cudaDeviceSynchronize();
+  if (!detached) cudaDeviceSynchronize();
   for (int g = 0; g < n_model_groups; ++g) drop_group(g);
   if (table) cudaIpcCloseMemHandle(table);
   cudaFree(d_bases);
+}
+
+// Post-commit teardown of a remote view off the caller's path: an event recorded on the
+// stream that last pushed through the view gates a detached thread that unmaps and
+// releases the imported chunks, closes the table handle and frees the view.  The caller
+// (the sender's post-commit cleanup, coordinator.py:340-354) neither synchronises its
+// stream nor waits for the driver's TLB-flushing unmaps.
+void remote_destroy_after(Remote* r, cudaStream_t st) {
+  cudaEvent_t ev = nullptr;
+  PL_CUDA(cudaSetDevice(r->device));
+  PL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  PL_CUDA(cudaEventRecord(ev, st));
+  std::thread([r, ev] {
+    cudaSetDevice(r->device);
+    cudaEventSynchronize(ev);
+    cudaEventDestroy(ev);
+    r->detached = true;  // ~Remote: no device-wide synchronisation (the event covered it)
+    delete r;
+  }).detach();
 }
 
 void Remote::drop_group(int g) {

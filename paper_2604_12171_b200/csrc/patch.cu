@@ -199,6 +199,7 @@ void Patch::mark(int32_t req, int g, int64_t start, int64_t n, bool device) {
   const int lg = local_of[g];
   if (lg < 0) return;
   const int64_t added = insert_interval(dirty[{req, lg}], start, start + n);
+  note_top(req, start + n);
   dirty_keys += added;
   dirty_cells += added * layers_in_group[lg];
   if (device) {
@@ -250,6 +251,7 @@ int64_t Patch::seed() {
       const int64_t w = t.written[groups[lg]];
       if (w <= 0) continue;
       const int64_t added = insert_interval(dirty[{req, lg}], 0, w);
+      note_top(req, w);
       dirty_keys += added;
       dirty_cells += added * layers_in_group[lg];
       seeded += w;
@@ -310,6 +312,8 @@ int64_t Patch::take_drained() {
     if (!kv.second.empty())
       drained.emplace_back(kv.first.first, kv.first.second, std::move(kv.second));
   dirty.clear();
+  for (int32_t r : top_reqs) top_dirty[(size_t)r] = 0;
+  top_reqs.clear();
   drained_keys = dirty_keys;
   dirty_keys = 0;
   dirty_cells = 0;
@@ -513,23 +517,23 @@ void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t
   if (status != PL_OK) fail(status, dst->last_msg);
 }
 
+// the per-request top of the dirty set is kept as marks arrive (an upper bound: discards
+// do not lower it, which can only send a round down the reserving path)
+void Patch::note_top(int32_t req, int64_t end) {
+  if ((size_t)req >= top_dirty.size()) top_dirty.resize(std::max<size_t>((size_t)req + 1, top_dirty.size() * 2), 0);
+  int64_t& t = top_dirty[(size_t)req];
+  if (!t) top_reqs.push_back(req);
+  t = std::max(t, end);
+}
+
 int64_t Patch::new_dst_blocks(Store* dst) const {
   // destination blocks the drained set will allocate: per request, the chain it needs past
   // the chain it has (the chain is shared by the request's groups)
-  std::vector<int64_t> top;
-  for (const auto& e : dirty) {
-    const int32_t req = e.first.first;
-    const auto& iv = e.second;
-    if (iv.empty()) continue;
-    if ((size_t)req >= top.size()) top.resize((size_t)req + 1, 0);
-    top[(size_t)req] = std::max(top[(size_t)req], iv.back().b);
-  }
   int64_t n = 0;
-  for (size_t r = 0; r < top.size(); ++r) {
-    if (!top[r]) continue;
-    const ReqTable* t = dst->table((int32_t)r);
+  for (int32_t r : top_reqs) {
+    const ReqTable* t = dst->table(r);
     const int64_t have = t ? (int64_t)t->chain.size() : 0;
-    n += std::max<int64_t>(0, (top[r] + dst->s - 1) / dst->s - have);
+    n += std::max<int64_t>(0, (top_dirty[(size_t)r] + dst->s - 1) / dst->s - have);
   }
   return n;
 }

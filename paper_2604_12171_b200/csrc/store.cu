@@ -573,9 +573,18 @@ void Store::flush() {
   }
 }
 
-void Store::refresh_bases() {
+void Store::refresh_bases(bool wait) {
   std::vector<uint64_t> h(n_model_groups, 0);
   for (int g = 0; g < n_model_groups; ++g) h[g] = materialised[g] ? (uint64_t)arenas[g].va : 0;
+  if (!wait) {
+    // through the pinned staging ring (no pageable-copy synchronisation), stream-ordered
+    Upload up(this);
+    const int a = up.add(h.data(), sizeof(uint64_t) * n_model_groups);
+    up.go();
+    PL_CUDA(cudaMemcpyAsync(d_bases_, up.ptr<uint64_t>(a), sizeof(uint64_t) * n_model_groups,
+                            cudaMemcpyDeviceToDevice, stream));
+    return;
+  }
   PL_CUDA(cudaMemcpyAsync(d_bases_, h.data(), sizeof(uint64_t) * n_model_groups,
                           cudaMemcpyHostToDevice, stream));
   PL_CUDA(cudaStreamSynchronize(stream));
@@ -610,7 +619,10 @@ void Store::dematerialise(int g) {
   materialised[g] = 0;
   if (g < 64) pending_groups &= ~(1ull << g);
   mapped_slots = 0;
-  refresh_bases();
+  // a dropped group's base goes to 0 in stream order, without a host wait: nothing may
+  // read the dropped pool after this point on any stream (its unmap is gated on this
+  // stream too), so no other stream needs to see the update at once
+  refresh_bases(/*wait=*/false);
 }
 int64_t Store::planned_bytes() const {
   int64_t b = 0;

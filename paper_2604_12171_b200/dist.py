@@ -176,9 +176,14 @@ class RemoteStore:
         buf = (C.c_ubyte * 64).from_buffer_copy(handle)
         N.check(N.lib().pl_remote_set_table(self.h, buf, max_reqs, max_chain))
 
-    def close(self) -> None:
+    def close(self, after_stream: int | None = None) -> None:
+        """Tear the view down; with `after_stream`, on a background thread once the work
+        enqueued on that stream (the last pushes through the view) has run."""
         if self.h is not None:
-            N.lib().pl_remote_destroy(self.h)
+            if after_stream is not None:
+                N.check(N.lib().pl_remote_destroy_after(self.h, C.c_void_p(after_stream)))
+            else:
+                N.lib().pl_remote_destroy(self.h)
             self.h = None
 
 
@@ -323,6 +328,18 @@ class PatchReceiver:
             raise _ERRORS.get(err[0], N.NativeError)(err[1])
 
 
+_RETIRED: list = []   # closed pairs' patch engines, inactive, destroyed by reap_patches()
+
+
+def reap_patches() -> int:
+    """Destroy the patch engines of closed pairs (synchronises their streams): at a point
+    where a host wait is harmless -- the next reconfiguration's start, or teardown."""
+    n = len(_RETIRED)
+    while _RETIRED:
+        _RETIRED.pop().close()
+    return n
+
+
 class PatchSender:
     """Source half of a cross-process pair: the native patch engine over the local store
     plus the remote view of the receiver's pools and table."""
@@ -425,16 +442,29 @@ class PatchSender:
         return self.patch.dirty_keys()
 
     def close(self) -> None:
+        t = [time.perf_counter()]
+        # the pushes into the remote pools were enqueued on the patch's stream: the view is
+        # unmapped once they have run (background thread, no host wait here)
+        push_stream = self.patch.stream_ptr()
         if self.mb is not None:
             self.mb.words[W_CLOSE] = 1
             self.seq += 1
             self.mb.post(W_ROWS, self.seq)
-            self.store.sync()     # every push into the remote pools ran before unmapping them
+            t.append(time.perf_counter())
             self.mb.close()
         else:
             self.chan.send(("close",))
-        self.patch.close()
-        self.remote.close()
+            t.append(time.perf_counter())
+        t.append(time.perf_counter())
+        self.remote.close(after_stream=push_stream)
+        t.append(time.perf_counter())
+        # the engine stops marking now; its device buffers are freed later (reap_patches:
+        # destroying it here would synchronise its streams inside the decode loop)
+        N.check(N.lib().pl_patch_set_active(self.patch.h, 0))
+        _RETIRED.append(self.patch)
+        t.append(time.perf_counter())
+        self.close_phases_ms = {k: round((t[i + 1] - t[i]) * 1e3, 3) for i, k in
+                                enumerate(("signal", "mailbox", "remote", "patch"))}
 
 
 class ActRing:

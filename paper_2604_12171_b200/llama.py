@@ -25,6 +25,7 @@ stacking factor k = 1 (group = layer - 1), as in BASELINE configs[0].
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -384,13 +385,21 @@ class StagedLlama:
         for (src, dst), layers in self.moving.items():
             for l in layers:
                 self.owner[l] = dst
-        for (src, dst), p in self.patches.items():
-            p.close()
-        for (src, dst), layers in self.moving.items():
-            self.stores[src].drop_layer_groups([l - 1 for l in layers])
+        self._leaving = dict(self.moving)
+        self._closing = dict(self.patches)
         self.patches.clear()
         self.moving.clear()
         return residual
+
+    def post_commit(self) -> None:
+        """After the pause (Coordinator._post_commit_cleanup, coordinator.py:340-354, runs
+        after commit_pause_end): the pairs' patch engines close and the sources drop the
+        layers that left."""
+        for p in getattr(self, "_closing", {}).values():
+            p.close()
+        for (src, dst), layers in getattr(self, "_leaving", {}).items():
+            self.stores[src].drop_layer_groups([l - 1 for l in layers])
+        self._closing, self._leaving = {}, {}
 
 
 def generate(model: StagedLlama, prompts: list[list[int]], joins: list[int], n_gen: int,
@@ -473,6 +482,9 @@ def _drive(model, step, prompts, joins, n_gen, reconfig, switch_at, trace, migra
             emit("commit_pause_start")
             model.switch()
             emit("commit_pause_end")
+            # post-commit cleanup after the pause, as the reference orders it
+            # (coordinator.py:326-334: commit_pause_end, resume, _post_commit_cleanup)
+            model.post_commit()
             emit("reconfigure_end", outcome="success")
         t += 1
     return outs
@@ -535,8 +547,12 @@ class DistStagedLlama:
         return self.torch.cuda.stream(self.stream)
 
     def close(self) -> None:
-        """Release the activation rings (after every rank finished stepping)."""
+        """Release the activation rings and the closed pairs' patch engines (after every
+        rank finished stepping)."""
+        from .dist import reap_patches
+
         self.stream.synchronize()
+        reap_patches()
         self.link.close()
 
     def _order(self) -> list[int]:
@@ -576,8 +592,9 @@ class DistStagedLlama:
         return sorted(self.moving)
 
     def start_reconfig(self, target: dict[int, list[int]]) -> None:
-        from .dist import Channel, PatchReceiver, PatchSender
+        from .dist import Channel, PatchReceiver, PatchSender, reap_patches
 
+        reap_patches()   # engines of an earlier reconfiguration's pairs
         new_owner = {l: g for g, ls in target.items() for l in ls}
         moves = layer_moves(self.owner, target)
         self.moving = moves
@@ -619,6 +636,7 @@ class DistStagedLlama:
         return int(t.item())
 
     def switch(self) -> None:
+        t0 = time.perf_counter()
         # the commit waits for the arriving layers' weights (coordinator.py:239-240)
         self.stager.wait()
         self.stager.make_current_wait(self.stream)
@@ -627,23 +645,54 @@ class DistStagedLlama:
                 for l in layers:
                     self.compute.w.update({k: t.to(self.compute.act_dtype)
                                            for k, t in self.stager.resident[l].items()})
+        t1 = time.perf_counter()
         self.pump()                     # residual patch of every pair
-        for pair in self._pairs():
-            if pair in self.senders:
-                self.senders.pop(pair).close()
-            elif pair in self.receivers:
-                assert not self.receivers.pop(pair).serve()
+        t2 = time.perf_counter()
+        # the residual is applied on every destination once each receiver's stream waits on
+        # its sender's push (serve_ack, device-side); ownership flips and decode resumes.
+        # Tearing the pairs down (sync + unmap of the imported pools) and dropping the
+        # leaving groups is post-commit cleanup (post_commit, after commit_pause_end).
         for (src, dst), layers in self.moving.items():
             for l in layers:
                 self.owner[l] = dst
+        self._leaving = dict(self.moving)
+        self.moving = {}
+        self.switch_phases_ms = {"weights": round((t1 - t0) * 1e3, 3),
+                                 "residual_round": round((t2 - t1) * 1e3, 3)}
+
+    def post_commit(self) -> None:
+        """Coordinator._post_commit_cleanup (coordinator.py:340-354), after the pause: every
+        pair closes (one global pair order on every rank), the sources drop the groups and
+        evict the weights of the layers that left."""
+        t2 = time.perf_counter()
+        close_detail = {}
+        for pair in sorted(getattr(self, "_leaving", {})):
+            if pair in self.senders:
+                tx = self.senders.pop(pair)
+                tx.close()
+                close_detail[f"{pair[0]}->{pair[1]}"] = getattr(tx, "close_phases_ms", None)
+            elif pair in self.receivers:
+                tr = time.perf_counter()
+                assert not self.receivers.pop(pair).serve()
+                close_detail[f"{pair[0]}->{pair[1]} rx"] = round((time.perf_counter() - tr) * 1e3, 3)
+        t3 = time.perf_counter()
+        t_drop = 0.0
+        for (src, dst), layers in getattr(self, "_leaving", {}).items():
             if src == self.gpu:
+                td = time.perf_counter()
                 self.store.drop_layer_groups([l - 1 for l in layers])
+                t_drop += time.perf_counter() - td
                 # the leaving layers' weights go too (post-commit evict, coordinator.py:340-354)
                 for l in layers:
                     for k in [k for k in self.compute.w if k.startswith(f"l{l - 1}.")]:
                         del self.compute.w[k]
                 self.stager.evict_layers([l for l in layers if l in self.stager.resident])
-        self.moving = {}
+        self._leaving = {}
+        ms = lambda a, b: round((b - a) * 1e3, 3)  # noqa: E731
+        # after the pause: pair teardown (close handshake, sync, unmap), drop + evict
+        self.post_commit_ms = {"pair_close": ms(t2, t3), "drop_evict": ms(t3, time.perf_counter()),
+                               "drop": round(t_drop * 1e3, 3),
+                               "close_detail": close_detail}
 
 
 def step_latency_around_switch(trace) -> dict:

@@ -35,10 +35,12 @@ def stage(rank, world, port, prefix, q):
         from paper_2604_12171_b200 import outputs
         outputs.write_run("gpurun_out/c4_live_run", tr, "configs[3]:even8->uneven8", 0,
                           mode="perf", stages=8)
-        q.put({"metrics": compute_metrics(tr).as_row(), "steps": step_latency_around_switch(tr),
-               "events": len(tr), "stages": 8,
-               "note": "8 stage processes share one B200: mechanism (pause, interference), "
-                       "not 8-GPU pipeline timings"})
+        q.put(("main", {"metrics": compute_metrics(tr).as_row(),
+                        "steps": step_latency_around_switch(tr), "events": len(tr), "stages": 8,
+                        "note": "8 stage processes share one B200: mechanism (pause, "
+                                "interference), not 8-GPU pipeline timings"}))
+    q.put(("phases", rank, {"pause": getattr(m, "switch_phases_ms", None),
+                            "post_commit": getattr(m, "post_commit_ms", None)}))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -53,9 +55,18 @@ if __name__ == "__main__":
     ps = [ctx.Process(target=stage, args=(r, 8, port, f"c4-{os.getpid()}", q)) for r in range(8)]
     for p in ps:
         p.start()
-    res = q.get(timeout=600)
+    res, phases = None, {}
+    for _ in range(9):
+        msg = q.get(timeout=600)
+        if msg[0] == "main":
+            res = msg[1]
+        else:
+            phases[msg[1]] = msg[2]
     for p in ps:
         p.join(timeout=120)
+    # every rank's share of the pause (weight gate, residual round) and of the post-commit
+    # cleanup after it (pair teardown, drop + evict)
+    res["switch_phases_ms_by_rank"] = {r: phases[r] for r in sorted(phases)}
     os.makedirs("gpurun_out", exist_ok=True)
-    json.dump(res, open("gpurun_out/c4_live_r1.json", "w"), indent=1)
+    json.dump(res, open("gpurun_out/c4_live.json", "w"), indent=1)
     print(json.dumps(res, indent=1))

@@ -1,6 +1,6 @@
 """Cross-GPU push in one process (needs >= 2 GPUs): source store on cuda:0, destination on
 cuda:1; times the fused push (GB/s over NVLink) and, under
-`ncu --metrics nvltx__bytes.sum,nvlrx__bytes.sum,gpu__time_duration.sum -k regex:copy_kernel`,
+`ncu --metrics nvltx__bytes.sum,nvlrx__bytes.sum,gpu__time_duration.sum -k regex:"push_batched|copy_kernel"`,
 gives the link bytes per launch.  Prints a JSON line; exits 0 with a note on one GPU."""
 import json
 import sys

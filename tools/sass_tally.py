@@ -18,7 +18,9 @@ SO = ROOT / "paper_2604_12171_b200" / "libpipelive.so"
 KERNELS = {
     "K2 paged_attn_mma_kernel<128,8>": r"paged_attn_mma_kernelILi128ELi8E",
     "K2 paged_attn_mma_kernel<64,8>": r"paged_attn_mma_kernelILi64ELi8E",
-    "K4+K5 copy_kernel<2> (fused push)": r"copy_kernelILi2EE",
+    "K4+K5 push_batched_kernel (fused push, batched resolve)": r"push_batched_kernel",
+    "K3+K4+K5 drain_push_kernel (steady rounds)": r"drain_push_kernel",
+    "K4+K5 copy_kernel<2> (per-item resolve, PL_PUSH_BATCHED=0)": r"copy_kernelILi2EE",
     "K1 kv_write_kernel": r"kv_write_kernel",
     "K3 drain_compact_kernel": r"drain_compact_kernel",
     "K6 unit_move_kernel": r"unit_move_kernel",

@@ -1,7 +1,7 @@
 """ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum over a
-bench run -> per-launch DRAM traffic of the dominant kernels (profiles/traffic_r1.json).
+bench run -> per-launch DRAM traffic of the dominant kernels (profiles/traffic_r<N>.json).
 
-Launch order in bench.py: bulk push rounds (copy_kernel<2>, the >1 ms launches), then
+Launch order in bench.py: bulk push rounds (push_batched_kernel, the >1 ms launches), then
 switch-pause pushes (small), then decode at n_q=32 ((W+K) x 16 layers), then n_q=64."""
 import csv
 import json
@@ -30,10 +30,14 @@ def rows(path):
 def main(src, dst, per_shape):
     launches = rows(src)
     res = []
-    push = [m for n, m in launches if "copy_kernel<2>" in n and m["gpu__time_duration.sum"] > 1e6]
+    push_names = ("push_batched_kernel", "copy_kernel<2>")
+    push = [(n, m) for n, m in launches
+            if any(k in n for k in push_names) and m["gpu__time_duration.sum"] > 1e6]
+    kname = next((k for k in push_names if push and k in push[0][0]), None)
+    push = [m for _, m in push]
     if push:
         b = sum(m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"] for m in push) / len(push)
-        res.append({"kernel": "copy_kernel<2>", "n_q": None, "launches": len(push),
+        res.append({"kernel": kname, "n_q": None, "launches": len(push),
                     "dram_bytes": int(b),
                     "read": int(sum(m["dram__bytes_read.sum"] for m in push) / len(push)),
                     "write": int(sum(m["dram__bytes_write.sum"] for m in push) / len(push))})
