@@ -311,9 +311,10 @@ struct Store {
   int32_t* d_owner_idx = nullptr;
   int64_t owner_cap = 0;
   std::vector<int32_t> h_table, h_owner, h_owner_idx;
-  struct Delta { int32_t which; int64_t idx; int32_t val; };
+  // one mirror write queued for the device (16 B, uploaded as is): which = 0 table,
+  // 1 owner, 2 owner_idx; val is refreshed from the mirror at flush time
+  struct Delta { int64_t idx; int32_t val; int32_t which; };
   std::vector<Delta> deltas;
-  std::vector<uint8_t> table_q, owner_q;  // flush(): entries already queued this flush
   std::vector<int32_t> released_slots;  // dirty bits to clear in attached patches
   // scratch
   void* d_scratch = nullptr;
@@ -516,13 +517,15 @@ struct Patch {
   uint32_t* d_bits_alt = nullptr;
   cudaStream_t stream = nullptr;  // side stream for K3/K4/K5 (null: the source's stream)
   cudaStream_t pstream() const { return stream ? stream : src->stream; }
-  cudaEvent_t ev_src = nullptr, ev_snap = nullptr, ev_mask = nullptr;
+  static constexpr int kMaskSlots = 4;
+  cudaEvent_t ev_src = nullptr, ev_snap = nullptr, ev_mask[kMaskSlots] = {};
   cudaEvent_t snap_ev = nullptr;  // the event the last drain's snapshot completed at
-  bool snap_recorded = false, gathered_recorded = false, mask_recorded = false;
+  bool snap_recorded = false, gathered_recorded = false, mask_recorded[kMaskSlots] = {};
+  int mask_slot = 0;
   // apply mask of the fused push, in patch-owned buffers: the copy on the side stream
   // reads it while the store's stream (and its scratch) moves on
-  uint8_t* h_mask = nullptr;
-  uint8_t* d_mask = nullptr;
+  uint8_t* h_mask[kMaskSlots] = {};
+  uint8_t* d_mask[kMaskSlots] = {};
   size_t mask_cap = 0;
   const uint8_t* stage_mask(const std::vector<uint8_t>& mask);
   const uint8_t* stage_bytes(const uint8_t* p, size_t n);  // H2D into d_mask on pstream
@@ -577,6 +580,7 @@ struct Patch {
   CopyLaunch push_launch(Store* dst, const uint8_t* d_apply, uint8_t apply_id);
   void push_chunked(Store* dst, const int32_t* rank, int64_t n_rank);
   int64_t new_dst_blocks(Store* dst) const;
+  bool runs_ahead(Store* dst) const;  // queued device work hides a host reservation
   void apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t* stale,
              int64_t n_stale);
   void push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys, int64_t* cells);
@@ -657,9 +661,8 @@ void launch_write_layer(const int32_t* table, int64_t max_chain, const int32_t* 
                         int64_t fp_bytes, int64_t cell_bytes, int layer, const uint8_t* kv,
                         int64_t kv_stride, cudaStream_t st);
 
-void launch_apply_deltas(int32_t* table, int32_t* owner, int32_t* owner_idx,
-                         const int64_t* idx, const int32_t* val, const int32_t* which, int64_t n,
-                         cudaStream_t st);
+void launch_apply_deltas(int32_t* table, int32_t* owner, int32_t* owner_idx, const void* deltas,
+                         int64_t n, cudaStream_t st);
 
 struct MarkLaunch {
   const int32_t* reqs; const int32_t* lgs; const int64_t* starts; const int64_t* offs;

@@ -133,20 +133,21 @@ void launch_write_layer(const int32_t* table, int64_t max_chain, const int32_t* 
 
 // ---------------------------------------------------------------------------
 // block-table / owner-map deltas (host mirror -> device), deduplicated on host
+struct DevDelta { int64_t idx; int32_t val; int32_t which; };  // == Store::Delta
 __global__ void apply_deltas_kernel(int32_t* table, int32_t* owner, int32_t* owner_idx,
-                                    const int64_t* idx, const int32_t* val, const int32_t* which,
-                                    int64_t n) {
+                                    const DevDelta* d, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t* dst = which[i] == 0 ? table : (which[i] == 1 ? owner : owner_idx);
-    dst[idx[i]] = val[i];
+    const DevDelta x = d[i];
+    int32_t* dst = x.which == 0 ? table : (x.which == 1 ? owner : owner_idx);
+    dst[x.idx] = x.val;
   }
 }
-void launch_apply_deltas(int32_t* table, int32_t* owner, int32_t* owner_idx, const int64_t* idx,
-                         const int32_t* val, const int32_t* which, int64_t n, cudaStream_t st) {
+void launch_apply_deltas(int32_t* table, int32_t* owner, int32_t* owner_idx, const void* deltas,
+                         int64_t n, cudaStream_t st) {
   if (n <= 0) return;
-  apply_deltas_kernel<<<(unsigned)grid_for(n, 256), 256, 0, st>>>(table, owner, owner_idx, idx,
-                                                                   val, which, n);
+  apply_deltas_kernel<<<(unsigned)grid_for(n, 256), 256, 0, st>>>(
+      table, owner, owner_idx, static_cast<const DevDelta*>(deltas), n);
   note_launch();
   PL_CUDA(cudaGetLastError());
 }

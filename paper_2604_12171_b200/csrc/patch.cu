@@ -55,7 +55,8 @@ Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n)
   PL_CUDA(cudaEventCreateWithFlags(&ev_dst, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_src, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
-  PL_CUDA(cudaEventCreateWithFlags(&ev_mask, cudaEventDisableTiming));
+  for (int i = 0; i < kMaskSlots; ++i)
+    PL_CUDA(cudaEventCreateWithFlags(&ev_mask[i], cudaEventDisableTiming));
   ensure_bits();
   // the drain's cell list, the chunked push's run buckets and the staged apply mask are
   // sized for a bulk round over every source cell (up to 8 M keys) now: the first round of
@@ -65,8 +66,10 @@ Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n)
   PL_CUDA(cudaMalloc(&d_part, sizeof(int64_t) * pre));
   cells_cap = part_cap = pre;
   mask_cap = 64 << 10;
-  PL_CUDA(cudaMallocHost(&h_mask, mask_cap));
-  PL_CUDA(cudaMalloc(&d_mask, mask_cap));
+  for (int i = 0; i < kMaskSlots; ++i) {
+    PL_CUDA(cudaMallocHost(&h_mask[i], mask_cap));
+    PL_CUDA(cudaMalloc(&d_mask[i], mask_cap));
+  }
   src->patches.push_back(this);
 }
 
@@ -94,33 +97,44 @@ Patch::~Patch() {
   cudaEventDestroy(ev_dst);
   cudaEventDestroy(ev_src);
   cudaEventDestroy(ev_snap);
-  cudaEventDestroy(ev_mask);
-  cudaFree(d_mask);
-  if (h_mask) cudaFreeHost(h_mask);
+  for (int i = 0; i < kMaskSlots; ++i) {
+    cudaEventDestroy(ev_mask[i]);
+    cudaFree(d_mask[i]);
+    if (h_mask[i]) cudaFreeHost(h_mask[i]);
+  }
 }
 
 const uint8_t* Patch::stage_mask(const std::vector<uint8_t>& mask) {
   return stage_bytes(mask.data(), mask.size());
 }
 
+// Host -> device staging of small per-round blobs (apply masks, run tables) on the patch
+// stream through kMaskSlots pinned/device slot pairs used round-robin: the host waits only
+// if the slot's previous H2D (kMaskSlots stagings back) has not run yet -- a caller that
+// runs ahead of the device is not pulled back to the previous round.  The device slot's
+// readers are on the same stream, so its reuse is stream-ordered.
 const uint8_t* Patch::stage_bytes(const uint8_t* data, size_t bytes) {
   cudaStream_t ps = pstream();
   const size_t n = std::max<size_t>(bytes, 1);
   if (n > mask_cap) {
     PL_CUDA(cudaStreamSynchronize(ps));
-    cudaFree(d_mask);
-    if (h_mask) cudaFreeHost(h_mask);
     mask_cap = std::max(n, mask_cap * 2);
-    PL_CUDA(cudaMallocHost(&h_mask, mask_cap));
-    PL_CUDA(cudaMalloc(&d_mask, mask_cap));
-    mask_recorded = false;
+    for (int i = 0; i < kMaskSlots; ++i) {
+      cudaFree(d_mask[i]);
+      if (h_mask[i]) cudaFreeHost(h_mask[i]);
+      PL_CUDA(cudaMallocHost(&h_mask[i], mask_cap));
+      PL_CUDA(cudaMalloc(&d_mask[i], mask_cap));
+      mask_recorded[i] = false;
+    }
   }
-  if (mask_recorded) PL_CUDA(cudaEventSynchronize(ev_mask));  // previous H2D read h_mask
-  std::memcpy(h_mask, data, bytes);
-  PL_CUDA(cudaMemcpyAsync(d_mask, h_mask, bytes, cudaMemcpyHostToDevice, ps));
-  PL_CUDA(cudaEventRecord(ev_mask, ps));
-  mask_recorded = true;
-  return d_mask;
+  const int i = mask_slot;
+  mask_slot = (mask_slot + 1) % kMaskSlots;
+  if (mask_recorded[i]) PL_CUDA(cudaEventSynchronize(ev_mask[i]));  // its last H2D read h_mask[i]
+  std::memcpy(h_mask[i], data, bytes);
+  PL_CUDA(cudaMemcpyAsync(d_mask[i], h_mask[i], bytes, cudaMemcpyHostToDevice, ps));
+  PL_CUDA(cudaEventRecord(ev_mask[i], ps));
+  mask_recorded[i] = true;
+  return d_mask[i];
 }
 
 void Patch::ensure_bits() {
@@ -159,6 +173,7 @@ static int64_t chunk_min_blocks() {
   return v ? std::max<int64_t>(1, std::atoll(v)) : kChunkedPushMinBlocks;
 }
 static bool no_chunking() { return std::getenv("PL_PUSH_NO_CHUNK") != nullptr; }
+static bool forced_chunking() { return std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS") != nullptr; }
 // PL_PUSH_NO_LAUNCH_FIRST=1: reserve on the host before launching even when no destination
 // block is allocated (A/B timing of the steady-round reordering)
 static bool launch_first_off() {
@@ -526,6 +541,28 @@ void Patch::note_top(int32_t req, int64_t end) {
   t = std::max(t, end);
 }
 
+// Does the caller run ahead of the device by more than a round's host reservation?  The
+// streams the copy depends on are polled for up to ~50 us: a seed's mark kernel drains
+// in that time (the first bulk round then pipelines its reservation), a queued step of
+// appends (a pipelined loop: milliseconds of K1) does not.
+bool Patch::runs_ahead(Store* dst) const {
+  const cudaStream_t ss[3] = {pstream(), src->stream, dst->stream};
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    bool busy = false;
+    for (cudaStream_t st : ss) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaErrorNotReady) {
+        busy = true;
+        break;
+      }
+      PL_CUDA(q);
+    }
+    if (!busy) return false;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(50)) return true;
+  }
+}
+
 int64_t Patch::new_dst_blocks(Store* dst) const {
   // destination blocks the drained set will allocate: per request, the chain it needs past
   // the chain it has (the chain is shared by the request's groups)
@@ -744,10 +781,14 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   const int64_t new_blocks = new_dst_blocks(dst);
   bool dst_pools = true;
   for (int32_t g : groups) dst_pools = dst_pools && dst->materialised[g];
-  // a round that allocates many destination blocks (a cold bulk round) always pipelines
-  // its reservation with the copy: per-run grid tails cost ~0.1 ms, the reservation
-  // ~0.1 us per block on the critical path otherwise
-  const bool chunk = dirty.size() >= 2 && !no_chunking() && new_blocks >= chunk_min_blocks();
+  // a round that allocates many destination blocks (a cold bulk round) pipelines its
+  // reservation with the copy -- unless the caller runs ahead of the device (this pair's
+  // previous copy has not run yet, e.g. a pipelined loop of bulk rounds): the host
+  // reservation is then hidden behind queued work, and one launch avoids the per-run
+  // grid tails and flushes
+  const bool ahead = !forced_chunking() && runs_ahead(dst);
+  const bool chunk = dirty.size() >= 2 && !no_chunking() && new_blocks >= chunk_min_blocks() &&
+                     !ahead;
   const bool launch_first = !chunk && new_blocks == 0 && dst_pools && dirty_keys > 0 &&
                             !launch_first_off();
   if (launch_first && host_async_enabled()) {

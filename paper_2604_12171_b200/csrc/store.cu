@@ -315,14 +315,14 @@ void Store::ensure_owner(int64_t slots) {
 void Store::set_table(int32_t req, int64_t idx, int32_t slot) {
   ensure_table(req, idx + 1);
   h_table[(size_t)(req * max_chain + idx)] = slot;
-  deltas.push_back({0, req * max_chain + idx, slot});
+  deltas.push_back({req * max_chain + idx, slot, 0});
 }
 void Store::set_owner(int32_t slot, int32_t req, int32_t idx) {
   ensure_owner((int64_t)slot + 1);
   h_owner[slot] = req;
   h_owner_idx[slot] = idx;
-  deltas.push_back({1, slot, req});
-  deltas.push_back({2, slot, idx});
+  deltas.push_back({slot, req, 1});
+  deltas.push_back({slot, idx, 2});
 }
 
 void* Store::scratch(size_t bytes) {
@@ -519,43 +519,19 @@ void Store::flush() {
     PL_CUDA(cudaMemcpyAsync(d_owner_idx, up.ptr<int32_t>(c), 4 * (size_t)owner_cap,
                             cudaMemcpyDeviceToDevice, stream));
   }
+  static_assert(sizeof(Delta) == 16, "Store::Delta is uploaded as the kernels' DevDelta");
   if (!deltas.empty()) {
-    // dedupe: one update per touched (array, index), value from the host mirror (which
-    // always holds the latest write); O(deltas) with per-array queued flags
-    if (table_q.size() < h_table.size()) table_q.resize(h_table.size(), 0);
-    if (owner_q.size() < h_owner.size()) owner_q.resize(h_owner.size(), 0);
-    std::vector<int64_t> idx;
-    std::vector<int32_t> val, which;
-    idx.reserve(deltas.size());
-    val.reserve(deltas.size());
-    which.reserve(deltas.size());
-    for (const Delta& d : deltas) {
-      if (d.which == 0) {
-        if (table_q[(size_t)d.idx]) continue;
-        table_q[(size_t)d.idx] = 1;
-        idx.push_back(d.idx);
-        val.push_back(h_table[(size_t)d.idx]);
-        which.push_back(0);
-      } else {
-        if (owner_q[(size_t)d.idx]) continue;
-        owner_q[(size_t)d.idx] = 1;
-        idx.push_back(d.idx);
-        val.push_back(h_owner[(size_t)d.idx]);
-        which.push_back(1);
-        idx.push_back(d.idx);
-        val.push_back(h_owner_idx[(size_t)d.idx]);
-        which.push_back(2);
-      }
-    }
-    for (size_t i = 0; i < idx.size(); ++i) (which[i] == 0 ? table_q : owner_q)[(size_t)idx[i]] = 0;
-    deltas.clear();
+    // every queued write goes up as is, with the mirror's current value (a repeated index
+    // writes the same latest value twice: no dedupe pass needed); one H2D, one scatter
+    for (Delta& d : deltas)
+      d.val = d.which == 0 ? h_table[(size_t)d.idx]
+                           : (d.which == 1 ? h_owner[(size_t)d.idx] : h_owner_idx[(size_t)d.idx]);
     Upload up(this);
-    int a = up.add(idx.data(), idx.size() * 8);
-    int b = up.add(val.data(), val.size() * 4);
-    int c = up.add(which.data(), which.size() * 4);
+    const int a = up.add(deltas.data(), deltas.size() * sizeof(Delta));
     up.go();
-    launch_apply_deltas(d_table, d_owner, d_owner_idx, up.ptr<int64_t>(a), up.ptr<int32_t>(b),
-                        up.ptr<int32_t>(c), (int64_t)idx.size(), stream);
+    launch_apply_deltas(d_table, d_owner, d_owner_idx, up.ptr<void>(a), (int64_t)deltas.size(),
+                        stream);
+    deltas.clear();
   }
   if (!released_slots.empty()) {
     std::vector<int32_t> slots;

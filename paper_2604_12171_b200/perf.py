@@ -563,9 +563,11 @@ def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16,
                     N.check(N.lib().pl_timing_enable(1))
                 t0 = time.perf_counter()
                 keys, cells = patch.push(dst, rank)
+                # the destination's stream waits on the round's copy (ev_applied): its sync
+                # is the round's end on the device
                 dst.sync()
-                src.sync()
                 t1 = time.perf_counter()
+                src.sync()
                 if timed:
                     N.check(N.lib().pl_timing_enable(0))
                     dev.append(N.timing("drain")[0] + N.timing("patch_push")[0]

@@ -61,9 +61,9 @@ for name, r in (("decode", None), ("0.01", 0.01), ("0.05", 0.05), ("0.25", 0.25)
         t0 = time.perf_counter()
         patch.push(dst, rank)
         t1 = time.perf_counter()
-        dst.sync()
-        src.sync()
+        dst.sync()          # the destination stream waits on the round's copy (ev_applied)
         t2 = time.perf_counter()
+        src.sync()
         patch.dirty_keys()          # any C-ABI call joins the host bookkeeping worker
         t3 = time.perf_counter()
         if timed_kernels:
