@@ -703,6 +703,11 @@ struct CopyLaunch {
   uint8_t apply_id;  // 0: apply where mask != 0; else only where mask == apply_id (chunked push)
   // staging
   uint8_t* rows; int32_t* keys; int64_t row_bytes;
+  // the pools' bases per LOCAL group, by value (G <= kInlineGroups): the hot kernels stage
+  // them in shared memory without the src_groups -> bases dependent loads
+  static constexpr int kInlineGroups = 8;
+  int inline_bases;
+  uint64_t src_base_l[kInlineGroups], dst_base_l[kInlineGroups];
 };
 void launch_copy(const CopyLaunch& c, cudaStream_t st);
 // K3 + fused push in one launch for sparse rounds

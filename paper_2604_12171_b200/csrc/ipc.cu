@@ -186,6 +186,13 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
     c.dst_table = r->table;
     c.dst_max_chain = r->max_chain;
     c.apply_mask = d_apply;
+    if (G <= CopyLaunch::kInlineGroups) {
+      c.inline_bases = 1;
+      for (int i = 0; i < G; ++i) {
+        c.src_base_l[i] = src->materialised[groups[i]] ? (uint64_t)src->arenas[groups[i]].va : 0;
+        c.dst_base_l[i] = (uint64_t)r->pools[groups[i]].va;
+      }
+    }
     cnt_cur ^= 1;
     d_count = d_cnt + cnt_cur;
     launch_drain_push(c, deferred_bits, n_words, d_count, d_cnt + (cnt_cur ^ 1), ps);
@@ -226,6 +233,13 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
     c.dst_table = r->table;
     c.dst_max_chain = r->max_chain;
     c.apply_mask = d_apply;
+    if (G <= CopyLaunch::kInlineGroups) {
+      c.inline_bases = 1;
+      for (int i = 0; i < G; ++i) {
+        c.src_base_l[i] = src->materialised[groups[i]] ? (uint64_t)src->arenas[groups[i]].va : 0;
+        c.dst_base_l[i] = (uint64_t)r->pools[groups[i]].va;
+      }
+    }
     launch_copy(c, pstream());
   }
   PL_CUDA(cudaEventRecord(ev_applied, pstream()));

@@ -506,9 +506,14 @@ drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, int W, unsigned
   __shared__ uint64_t s_sb[kFusedMaxGroups], s_db[kFusedMaxGroups];
   const bool smem_bases = c.G <= kFusedMaxGroups;
   if (smem_bases && threadIdx.x < c.G) {  // visible after the first pass's barrier
-    const int32_t g = c.src_groups[threadIdx.x];
-    s_sb[threadIdx.x] = c.src_bases[g];
-    s_db[threadIdx.x] = c.dst_bases[g];
+    if (c.inline_bases) {  // by value in the launch: off the exchange's critical path
+      s_sb[threadIdx.x] = c.src_base_l[threadIdx.x];
+      s_db[threadIdx.x] = c.dst_base_l[threadIdx.x];
+    } else {
+      const int32_t g = c.src_groups[threadIdx.x];
+      s_sb[threadIdx.x] = c.src_bases[g];
+      s_db[threadIdx.x] = c.dst_bases[g];
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *next_count = 0ull;
   const int lane = threadIdx.x & 31;
@@ -663,9 +668,14 @@ __global__ void __launch_bounds__(kWarps * 32) push_batched_kernel(CopyLaunch c,
   __shared__ uint64_t s_sb[kMaxSmemGroups], s_db[kMaxSmemGroups];
   const bool smem_bases = c.G <= kMaxSmemGroups;
   if (smem_bases && threadIdx.x < c.G) {
-    const int32_t g = c.src_groups[threadIdx.x];
-    s_sb[threadIdx.x] = c.src_bases[g];
-    s_db[threadIdx.x] = c.dst_bases[g];
+    if (c.inline_bases) {  // by value in the launch: no dependent loads before the barrier
+      s_sb[threadIdx.x] = c.src_base_l[threadIdx.x];
+      s_db[threadIdx.x] = c.dst_base_l[threadIdx.x];
+    } else {
+      const int32_t g = c.src_groups[threadIdx.x];
+      s_sb[threadIdx.x] = c.src_bases[g];
+      s_db[threadIdx.x] = c.dst_bases[g];
+    }
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;

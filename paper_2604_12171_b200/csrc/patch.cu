@@ -598,6 +598,13 @@ CopyLaunch Patch::push_launch(Store* dst, const uint8_t* d_apply, uint8_t apply_
   c.dst_max_chain = dst->max_chain;
   c.apply_mask = d_apply;
   c.apply_id = apply_id;
+  if (G <= CopyLaunch::kInlineGroups) {
+    c.inline_bases = 1;
+    for (int i = 0; i < G; ++i) {
+      c.src_base_l[i] = src->materialised[groups[i]] ? (uint64_t)src->arenas[groups[i]].va : 0;
+      c.dst_base_l[i] = dst->materialised[groups[i]] ? (uint64_t)dst->arenas[groups[i]].va : 0;
+    }
+  }
   return c;
 }
 
@@ -688,11 +695,11 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
     PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
     PL_CUDA(cudaSetDevice(src->device));
     PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
+    for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);  // pool mapped (lazy groups)
     CopyLaunch cl = push_launch(dst, d_apply, (uint8_t)(c + 1));
     cl.cells = d_part + run_off[c];
     cl.count = d_run_cnt + c;
     cl.n_hint = run_keys[c];
-    for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);  // pool mapped (lazy groups)
     launch_copy(cl, pstream());
     t_launch += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
     ++launched;
@@ -786,9 +793,8 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   // previous copy has not run yet, e.g. a pipelined loop of bulk rounds): the host
   // reservation is then hidden behind queued work, and one launch avoids the per-run
   // grid tails and flushes
-  const bool ahead = !forced_chunking() && runs_ahead(dst);
   const bool chunk = dirty.size() >= 2 && !no_chunking() && new_blocks >= chunk_min_blocks() &&
-                     !ahead;
+                     (forced_chunking() || !runs_ahead(dst));
   const bool launch_first = !chunk && new_blocks == 0 && dst_pools && dirty_keys > 0 &&
                             !launch_first_off();
   if (launch_first && host_async_enabled()) {
