@@ -808,8 +808,10 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
         gc.collect()
         gc.disable()
         t0 = time.perf_counter()
+        marks = []
         for i in range(K):
             keys = one_step(i)
+            marks.append(time.perf_counter())
         stream.synchronize()
         torch.cuda.synchronize()
         sec = time.perf_counter() - t0
@@ -825,6 +827,9 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
     return {"value": round(world * K * wl.payload_bytes / sec / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": int(host.nbytes + 16 * len(reqs)),
             "d2h_bytes_per_step": 8, "ms_per_step": round(sec / K * 1e3, 3),
+            # host time between consecutive step calls returning (the device runs ahead or
+            # behind; a stall anywhere in the loop shows up here as one long step)
+            "host_step_ms_max": round(max(b - a for a, b in zip([t0] + marks, marks)) * 1e3, 3),
             "path": "host payload fingerprints -> pl_store_append_batch_payloads (K1 expand + "
                     "mark) -> pl_patch_push (K3 + fused K4/K5) -> D2H drained count "
                     "(pipelined: step i+1 is prepared on the host while step i runs)"
