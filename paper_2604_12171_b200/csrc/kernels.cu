@@ -152,7 +152,7 @@ void launch_write_layer(const int32_t* table, int64_t max_chain, const int32_t* 
 }
 
 // ---------------------------------------------------------------------------
-// block-table / owner-map deltas (host mirror -> device), deduplicated on host
+// block-table / owner-map writes (host mirror -> device): one 16-B record per queued write
 struct DevDelta { int64_t idx; int32_t val; int32_t which; };  // == Store::Delta
 __global__ void apply_deltas_kernel(int32_t* table, int32_t* owner, int32_t* owner_idx,
                                     const DevDelta* d, int64_t n) {

@@ -702,3 +702,4 @@ class RingPair:
         N.check(N.lib().pl_patch_set_active(self.tx.patch.h, 0))
         self.tx.close()
         assert not self.rx.serve()
+        reap_patches()   # teardown: the closed pair's engine can synchronise now
