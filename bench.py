@@ -446,9 +446,10 @@ def main() -> None:
     # ---- configs[1] live with real stage compute: the 8B-shaped decoder (bf16 GEMMs, K1/K2
     # over the stage stores) under a PP 2 -> 4 reconfiguration switched by the reference's
     # lag < tau test, against a static run (tokens must be equal)
-    c2_model = None
+    c2_model = c4_model = None
     if not args.skip_c2 and rank == 0:
         c2_model = guarded("c2_model", lambda: measure_c2_model(wl))
+        c4_model = guarded("c4_model", lambda: measure_c4_model(wl))
 
     # ---- C5: dirty-rate x block-size sweep and concurrent pairs (configs[4], 1 GPU); after
     # the e2e legs, so their store churn (dozens of pools created and released) cannot
@@ -482,6 +483,7 @@ def main() -> None:
         "c3_live_resize": c3,
         "c2_live": c2,
         "c2_model": c2_model,
+        "c4_model": c4_model,
         "resize": resize,
         "roofline": roofline,
         "cpu_baseline": cpu,
@@ -495,13 +497,13 @@ def main() -> None:
         "decode": decode,
         "decode_70b_shape": decode_70b,
         "tail": tail_summary(c2_model, c3, resize, decode, decode_70b, pause, value_cold,
-                             hbm_peak, act_hop, sweep),
+                             hbm_peak, act_hop, sweep, c4_model),
     }
     print(json.dumps(line), flush=True)
 
 
 def tail_summary(c2, c3, resize, decode, decode_70b, pause, value_cold, hbm_peak,
-                 act_hop=None, sweep=None) -> dict:
+                 act_hop=None, sweep=None, c4=None) -> dict:
     """The headline extras in one small object at the very end of the line."""
     def get(d, *path):
         for p in path:
@@ -527,6 +529,11 @@ def tail_summary(c2, c3, resize, decode, decode_70b, pause, value_cold, hbm_peak
             "tokens_equal_static", "tpot_ms_static", "tpot_ms_before", "tpot_ms_during",
             "tpot_ms_after", "switch_step", "pause") if k in c2}
         out["c2_model_8b_live"]["bulk_gbs"] = get(c2, "bulk", "gbs")
+    if isinstance(c4, dict) and "error" not in c4:
+        out["c4_model_8b_uneven"] = {k: c4.get(k) for k in (
+            "tokens_equal_static", "tpot_ms_static", "tpot_ms_before", "tpot_ms_during",
+            "tpot_ms_after", "switch_step", "pause") if k in c4}
+        out["c4_model_8b_uneven"]["bulk_gbs"] = get(c4, "bulk", "gbs")
     if isinstance(resize, dict) and "error" not in resize:
         out["resize_full_ms"] = {k: resize.get(k) for k in (
             "drop_groups_full_ms", "shrink_full_ms", "grow_warm_full_ms", "grow_cold_full_ms")}
@@ -567,6 +574,41 @@ def measure_c2_model(wl, steps: int = 40, reconfig_at: int = 8) -> dict:
     s["note"] = ("all 4 stage stores on one GPU (distinct on hardware); bf16 GEMMs via cuBLAS, "
                  "K1 + K2 + the patch engine are this repo's kernels; patch rounds on a "
                  "lowest-priority side stream; TPOT includes the greedy token read-back")
+    return s
+
+
+def measure_c4_model(wl, steps: int = 40, reconfig_at: int = 8) -> dict:
+    """BASELINE configs[3] with the 8B-shaped decoder: 8 stage stores (one GPU here, one GPU
+    each on hardware), an even split (4 layers per stage, k = 2) re-split live into the
+    generation-heavy uneven split 2/4/4/6/6/4/4/2 -- six pairs migrate at once, stages 2, 3,
+    6, 7 both send and receive -- under decode at B requests x ctx prefilled positions;
+    switch at the first per-step poll with lag < tau = 50.  TPOT before / while migrating /
+    after, the pause split, and the tokens against the static run.  (TTFT needs prefill,
+    which this decode-only stage model does not run; configs[3]'s TTFT/TPOT trace metrics
+    come from the 8-process tiny-model run, tools/c4_live.py.)"""
+    import gc
+
+    import torch
+
+    from paper_2604_12171_b200.model8b import EVEN8, UNEVEN8, run_live, summarize
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    kw = dict(batch=wl.batch, ctx=wl.ctx, steps=steps, reconfig_at=reconfig_at, src=EVEN8,
+              dst=UNEVEN8, k=2)
+    static = run_live(live=False, **kw)
+    live = run_live(live=True, **kw)
+    s = summarize(live, static)
+    c = s.pop("commit") or {}
+    s["pause"] = {k: c.get(k) for k in ("pause_ms", "drain_ms", "residual_ms",
+                                        "barrier_and_switch_ms", "residual_cells", "lag_at_poll")}
+    s["lag_polls"] = s["lag_polls"][:12]
+    s["split"] = {"from": [len(v) for _, v in sorted(EVEN8.items())],
+                  "to": [len(v) for _, v in sorted(UNEVEN8.items())], "k": 2}
+    s["note"] = ("8 stage stores on one GPU (distinct on hardware); bf16 GEMMs via cuBLAS, "
+                 "K1 + K2 + the patch engine are this repo's kernels; six pairs patch on one "
+                 "lowest-priority side stream; TPOT includes the greedy token read-back")
+    torch.cuda.empty_cache()
     return s
 
 

@@ -66,6 +66,21 @@ PP2 = {1: list(range(1, 17)), 2: list(range(17, 33)), 3: [], 4: []}
 PP4 = {1: list(range(1, 9)), 3: list(range(9, 17)), 2: list(range(17, 25)), 4: list(range(25, 33))}
 
 
+def _split(sizes: list[int]) -> dict[int, list[int]]:
+    out, l = {}, 1
+    for g, n in enumerate(sizes, start=1):
+        out[g] = list(range(l, l + n))
+        l += n
+    return out
+
+
+# BASELINE configs[3] at the 8B shape (SURVEY §8(d) C4 scaled to 32 layers, k = 2): an even
+# 8-stage split re-split live into a generation-heavy uneven one; six pairs migrate
+# (1->2, 2->3, 3->4, 6->5, 7->6, 8->7), stages 2, 3, 6, 7 both send and receive
+EVEN8 = _split([4] * 8)
+UNEVEN8 = _split([2, 4, 4, 6, 6, 4, 4, 2])
+
+
 def _vp(t) -> C.c_void_p:
     return C.c_void_p(t.data_ptr())
 
@@ -331,13 +346,18 @@ def torch_rsqrt(x32, eps):
 
 
 def run_live(batch: int = 256, ctx: int = 2048, steps: int = 40, reconfig_at: int = 8,
-             live: bool = True, tau: int = 50, device: int = 0, seed: int = 0) -> dict:
-    """Greedy decode for `steps` steps; with `live`, the PP 2 -> 4 reconfiguration starts
-    after step `reconfig_at` and commits at the first poll with lag < tau.  Returns the
-    tokens of every step and the timeline (per-step TPOT, phases, pause breakdown)."""
+             live: bool = True, tau: int = 50, device: int = 0, seed: int = 0,
+             src: dict | None = None, dst: dict | None = None, k: int = 4) -> dict:
+    """Greedy decode for `steps` steps over the stages of `src` (default PP2, k = 4); with
+    `live`, the reconfiguration to `dst` (default PP4: configs[1]; EVEN8 -> UNEVEN8 at k = 2
+    is configs[3]) starts after step `reconfig_at` and commits at the first poll with
+    lag < tau.  Returns the tokens of every step and the timeline (per-step TPOT, phases,
+    pause breakdown)."""
     import torch
 
-    pipe = Pipeline8B(PP2, batch, ctx, max_steps=steps + 4, device=device, seed=seed)
+    src, dst = src or PP2, dst or PP4
+    pipe = Pipeline8B(src, batch, ctx, max_steps=steps + 4, device=device, seed=seed,
+                      shape=Shape8B(k=k))
     pipe.fill()
     tokens = torch.arange(batch, device=pipe.dev, dtype=torch.long) * 7 % pipe.sh.vocab
     out = {"tokens": [], "step_ms": [], "phase": [], "lag": []}
@@ -370,7 +390,7 @@ def run_live(batch: int = 256, ctx: int = 2048, steps: int = 40, reconfig_at: in
             if live and t == reconfig_at:
                 tb = time.perf_counter()
                 b0 = torch.cuda.Event(enable_timing=True)
-                r = pipe.start_reconfig(PP4, before_bulk=lambda: b0.record(pipe.side))
+                r = pipe.start_reconfig(dst, before_bulk=lambda: b0.record(pipe.side))
                 b1 = torch.cuda.Event(enable_timing=True)
                 b1.record(pipe.side)
                 bulk = {"cells": r["cells"], "bytes": r["cells"] * pipe.sh.cell_bytes,

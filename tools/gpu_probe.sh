@@ -1,7 +1,6 @@
 cd $GRAFT_REPO_ROOT
-for v in d1 d2 d3 g1 g2 g3; do
-case $v in g*) export PL_RECLAIM_RELEASE_GRACE_MS=0;; esac
-timeout 600 python bench.py --steps 10 --warmup 3 --skip-c3 --skip-c2 --skip-sweep --skip-cpu > gpurun_out/e2e_$v.json 2>gpurun_out/e2e_$v.err; echo rc=$?
+timeout 600 python -m pytest tests/test_gpu_model8b.py -q -x --timeout=400 -p no:cacheprovider 2>&1 | tail -3
+timeout 900 python tools/c4_model_probe.py > gpurun_out/c4_model.json 2>gpurun_out/c4_model.err; echo c4m=$?
 python -c "
-import json; l=json.loads(open('gpurun_out/e2e_$v.json').read().strip().splitlines()[-1]); print('$v', l['value'], l['e2e']['value'], l['e2e']['ms_per_step'], l['e2e_real_kv_from_host']['value'])"
-done
+import json; d=json.load(open('gpurun_out/c4_model.json')); print({k:d[k] for k in d if k not in ('lag_polls','config_end')})"
+tail -3 gpurun_out/c4_model.err
