@@ -179,7 +179,7 @@ struct Remote {
          int n_model_groups);
   ~Remote();
   void import_group(int g, const int* fds, int n, size_t chunk_bytes);
-  void drop_group(int g);
+  void drop_group(int g, bool reset_base = true);
   void set_table(const void* ipc_handle, int64_t max_reqs, int64_t max_chain);
   bool detached = false;  // torn down by remote_destroy_after's thread
 };

@@ -37,7 +37,8 @@ Remote::Remote(int dev, int s_, int k_, int64_t cell, int64_t fp, int64_t unit, 
 Remote::~Remote() {
   cudaSetDevice(device);
   if (!detached) cudaDeviceSynchronize();
-  for (int g = 0; g < n_model_groups; ++g) drop_group(g);
+  // no base resets and nothing that throws: a destructor (possibly on the teardown thread)
+  for (int g = 0; g < n_model_groups; ++g) drop_group(g, /*reset_base=*/false);
   if (table) cudaIpcCloseMemHandle(table);
   cudaFree(d_bases);
 }
@@ -61,13 +62,14 @@ void remote_destroy_after(Remote* r, cudaStream_t st) {
   }).detach();
 }
 
-void Remote::drop_group(int g) {
+void Remote::drop_group(int g, bool reset_base) {
   Pool& p = pools[g];
   if (!p.va) return;
   vmm_unmap(p.va, p.hs.size() * p.chunk_bytes);
   for (auto h : p.hs) vmm_release(h);
   vmm_free_va(p.va, p.va_bytes);
   p = Pool{};
+  if (!reset_base) return;  // teardown: the view is going away, nothing reads the base
   const uint64_t zero = 0;
   PL_CUDA(cudaMemcpy(d_bases + g, &zero, sizeof(zero), cudaMemcpyHostToDevice));
 }
