@@ -521,9 +521,14 @@ def tail_summary(c2, c3, resize, decode, decode_70b, pause, value_cold, hbm_peak
            "act_hop_us": {k: get(act_hop, k, "us_per_hop") for k in ("8b", "70b")}}
     if isinstance(sweep, list):
         # steady rounds of the C5 sweep at 16-token blocks: wall vs kernel time
-        out["c5_steady_16tok"] = {r["dirty"]: {"wall_us": round(r["ms"] * 1e3, 1),
-                                               "kernel_us": round(r["kernel_ms"] * 1e3, 1)}
-                                  for r in sweep if r.get("tokens_per_block") == 16}
+        # (hbm_frac: the round's kernels' algorithmic HBM bytes -- payload read + write --
+        # per kernel second, over the measured copy peak)
+        out["c5_steady_16tok"] = {
+            r["dirty"]: {"wall_us": round(r["ms"] * 1e3, 1),
+                         "kernel_us": round(r["kernel_ms"] * 1e3, 1),
+                         "hbm_frac": round(r["kernel_hbm_gbs"] / hbm_peak, 3)
+                         if r.get("kernel_hbm_gbs") else None}
+            for r in sweep if r.get("tokens_per_block") == 16}
     if isinstance(c2, dict) and "error" not in c2:
         out["c2_model_8b_live"] = {k: c2.get(k) for k in (
             "tokens_equal_static", "tpot_ms_static", "tpot_ms_before", "tpot_ms_during",
