@@ -173,7 +173,9 @@ static int64_t chunk_min_blocks() {
   return v ? std::max<int64_t>(1, std::atoll(v)) : kChunkedPushMinBlocks;
 }
 static bool no_chunking() { return std::getenv("PL_PUSH_NO_CHUNK") != nullptr; }
-static bool forced_chunking() { return std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS") != nullptr; }
+// PL_PUSH_CHUNK_ALWAYS=1: pipeline every round that meets the block threshold, even when
+// queued device work would hide the reservation (tests force tiny runs with it)
+static bool forced_chunking() { return std::getenv("PL_PUSH_CHUNK_ALWAYS") != nullptr; }
 // PL_PUSH_NO_LAUNCH_FIRST=1: reserve on the host before launching even when no destination
 // block is allocated (A/B timing of the steady-round reordering)
 static bool launch_first_off() {

@@ -2,6 +2,8 @@
 the CUDA patch engine against the reference (tests/golden/migration_cases.json)
 and the oracle.  Mirrors pkg/tests/test_migrator.py of the reference."""
 
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -165,6 +167,7 @@ def test_side_stream_push_overlapped_with_decode_writes(monkeypatch, seed, chunk
     blocks takes the pipelined multi-launch path."""
     if chunked:
         monkeypatch.setenv("PL_PUSH_CHUNK_MIN_BLOCKS", "1")
+        monkeypatch.setenv("PL_PUSH_CHUNK_ALWAYS", "1")
     import random
 
     import torch
@@ -258,6 +261,7 @@ def test_chunked_bulk_push_equals_single_launch(monkeypatch, cap_dst, seed):
         if chunked:
             monkeypatch.delenv("PL_PUSH_NO_CHUNK", raising=False)
             monkeypatch.setenv("PL_PUSH_CHUNK_MIN_BLOCKS", "1")
+            monkeypatch.setenv("PL_PUSH_CHUNK_ALWAYS", "1")
         else:
             monkeypatch.setenv("PL_PUSH_NO_CHUNK", "1")
         reg, names, src, dst = _chunk_rig(cap_dst, seed=seed)
@@ -286,6 +290,47 @@ def test_chunked_bulk_push_equals_single_launch(monkeypatch, cap_dst, seed):
                 assert dst.snapshot_group(g) == src.snapshot_group(g)
         else:
             assert overflow is not None
+        p.close()
+        src.close()
+        dst.close()
+    assert states[0] == states[1]
+
+
+def test_cold_round_pipelines_only_when_the_device_waits(monkeypatch):
+    """A cold round pipelines its host reservation with the copy (Patch::push_chunked)
+    unless the caller already runs ahead of the device: with milliseconds of work queued
+    on the source's stream the reservation is hidden behind it, and the round goes out as
+    one launch (Patch::runs_ahead).  Either way the destination is the same."""
+    import torch
+
+    from paper_2604_12171_b200 import _native as N
+    from paper_2604_12171_b200.perf import NativePatch
+
+    monkeypatch.setenv("PL_PUSH_CHUNK_MIN_BLOCKS", "1")
+    monkeypatch.delenv("PL_PUSH_CHUNK_ALWAYS", raising=False)
+    monkeypatch.delenv("PL_PUSH_NO_CHUNK", raising=False)
+    states = []
+    for busy in (False, True):
+        reg, names, src, dst = _chunk_rig(4096, seed=3)
+        p = NativePatch(src, (1, 2), 2)
+        p.seed()
+        src.sync()
+        if busy:   # ~20 ms of queued work on the source's stream (a caller running ahead)
+            out = C.c_void_p()
+            N.check(N.lib().pl_store_stream(src._h, C.byref(out)))
+            with torch.cuda.stream(torch.cuda.ExternalStream(out.value)):
+                torch.cuda._sleep(40_000_000)
+        N.check(N.lib().pl_timing_reset())
+        N.check(N.lib().pl_timing_enable(1))
+        p.push(dst, reg.rank())
+        stats = p.last_push_stats()
+        src.sync()
+        dst.sync()
+        launches = N.timing("patch_push")[1]
+        N.check(N.lib().pl_timing_enable(0))
+        assert stats["chunked"] is (not busy), stats
+        assert (launches == 1) if busy else (launches > 2), launches
+        states.append(_dst_state(dst, names))
         p.close()
         src.close()
         dst.close()
