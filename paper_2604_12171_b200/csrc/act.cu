@@ -35,6 +35,11 @@ constexpr int kMaxSlots = 8;
 struct Mailbox {
   std::atomic<uint64_t> published;  // last sequence whose ready event the sender recorded
   std::atomic<uint64_t> consumed;   // last sequence whose freed event the receiver recorded
+  // a process records only events it created on its own device (an event belongs to its
+  // device; stages on different GPUs): the sending process creates the "ready" events and
+  // publishes their IPC handles here before its first send
+  std::atomic<uint32_t> ready_set;
+  cudaIpcEventHandle_t ready_h[kMaxSlots];
 };
 struct Blob {  // what the owner exports (fixed layout, plain bytes)
   int32_t magic, pid, device, n_slots;
@@ -53,6 +58,8 @@ struct ActRing {
   bool owner = false, ipc = false;
   uint8_t* buf = nullptr;
   cudaEvent_t ready[kMaxSlots] = {}, freed[kMaxSlots] = {};
+  cudaEvent_t ready_peer[kMaxSlots] = {};  // owner: the sending process's ready events
+  bool peer_ready = false;                 // owner: ready_peer opened
   Mailbox* mb = nullptr;
   std::string shm;
   uint64_t seq_send = 0, seq_recv = 0;
@@ -102,6 +109,7 @@ ActRing* act_ring_create(int device, int64_t slot_bytes, int n_slots) {
     r->mb = new (p) Mailbox();
     r->mb->published.store(0);
     r->mb->consumed.store(0);
+    r->mb->ready_set.store(0);
   } catch (...) {
     act_ring_destroy(r);
     throw;
@@ -163,9 +171,11 @@ ActRing* act_ring_open(int device, const void* blob, int64_t n) {
     void* p = nullptr;
     PL_CUDA(cudaIpcOpenMemHandle(&p, b.mem, cudaIpcMemLazyEnablePeerAccess));
     r->buf = static_cast<uint8_t*>(p);
+    // "freed" is recorded by the receiver: opened here, only waited on.  "ready" is
+    // recorded here: created on this device, its handles published through the mailbox
     for (int i = 0; i < r->n_slots; ++i) {
-      PL_CUDA(cudaIpcOpenEventHandle(&r->ready[i], b.ready[i]));
       PL_CUDA(cudaIpcOpenEventHandle(&r->freed[i], b.freed[i]));
+      PL_CUDA(cudaEventCreateWithFlags(&r->ready[i], cudaEventDisableTiming | cudaEventInterprocess));
     }
     const int fd = shm_open(r->shm.c_str(), O_RDWR, 0600);
     if (fd < 0) fail(PL_E_INVALID, "shm_open of the peer's mailbox failed");
@@ -173,6 +183,8 @@ ActRing* act_ring_open(int device, const void* blob, int64_t n) {
     close(fd);
     if (m == MAP_FAILED) fail(PL_E_INVALID, "mmap failed");
     r->mb = static_cast<Mailbox*>(m);
+    for (int i = 0; i < r->n_slots; ++i) PL_CUDA(cudaIpcGetEventHandle(&r->mb->ready_h[i], r->ready[i]));
+    r->mb->ready_set.store(1, std::memory_order_release);
   } catch (...) {
     act_ring_destroy(r);
     throw;
@@ -192,6 +204,7 @@ void act_ring_destroy(ActRing* r) {
     for (int i = 0; i < r->n_slots; ++i) {
       if (r->ready[i]) cudaEventDestroy(r->ready[i]);
       if (r->freed[i]) cudaEventDestroy(r->freed[i]);
+      if (r->ready_peer[i]) cudaEventDestroy(r->ready_peer[i]);
     }
     cudaFree(r->buf);
     if (r->mb) munmap(r->mb, sizeof(Mailbox));
@@ -230,7 +243,15 @@ void act_recv(ActRing* r, void* dst, int64_t bytes, cudaStream_t st) {
   const uint64_t seq = ++s->seq_recv;
   const int slot = (int)((seq - 1) % (uint64_t)r->n_slots);
   wait_counter(r->mb->published, seq, "published an activation");
-  PL_CUDA(cudaStreamWaitEvent(st, r->ready[slot], 0));
+  // a sender in another process recorded its own "ready" events (published before its
+  // first send, so visible once `published` is); in one process the owner's are used
+  if (!r->alias && !r->peer_ready && r->mb->ready_set.load(std::memory_order_acquire)) {
+    PL_CUDA(cudaSetDevice(r->device));
+    for (int i = 0; i < r->n_slots; ++i)
+      PL_CUDA(cudaIpcOpenEventHandle(&r->ready_peer[i], r->mb->ready_h[i]));
+    r->peer_ready = true;
+  }
+  PL_CUDA(cudaStreamWaitEvent(st, r->peer_ready ? r->ready_peer[slot] : r->ready[slot], 0));
   PL_CUDA(cudaMemcpyAsync(dst, r->buf + (int64_t)slot * r->slot_bytes, (size_t)bytes,
                           cudaMemcpyDeviceToDevice, st));
   PL_CUDA(cudaEventRecord(r->freed[slot], st));
@@ -243,13 +264,23 @@ void act_recv(ActRing* r, void* dst, int64_t bytes, cudaStream_t st) {
 // interprocess CUDA events, so the control of a round is a few host stores and polls
 // instead of socket messages, and "applied" is a device-side event wait instead of a
 // host stream synchronisation on the sender.
+// Events: a process records only events it created on its own device (an event belongs to
+// the device it was created on, and the two stages of a pair may be on different GPUs);
+// the peer only waits on them.  So each side has its own events (`self`, recorded by
+// mailbox_record) and the other side's (`peer`, waited on by mailbox_stream_wait), both
+// indexed by the protocol's event number.  The owner's handles travel in the exported
+// blob; the opener publishes its own in the region's tail before it posts anything.  In
+// one process (an aliased open) both sides share the owner's events.
 struct MailboxRegion {
   int device = 0, n_events = 0;
   bool owner = false, ipc = false;
-  int64_t bytes = 0;
+  bool peer_open = false;      // ev_peer usable
+  bool peer_opened_ipc = false;  // ev_peer opened from handles (destroyed with the region)
+  int64_t bytes = 0;           // usable bytes (control words + rows); the tail follows
   uint8_t* base = nullptr;
   std::string shm;
-  cudaEvent_t ev[kMaxSlots] = {};
+  cudaEvent_t ev_self[kMaxSlots] = {}, ev_peer[kMaxSlots] = {};
+  MailboxRegion* owner_region = nullptr;  // aliased open: the owner's region
 };
 namespace {
 struct MailBlob {
@@ -259,6 +290,12 @@ struct MailBlob {
   char shm[64];
 };
 constexpr int32_t kMailMagic = 0x6d61696c;
+constexpr int64_t kMailTail = 4096;  // after the usable bytes: the opener's event handles
+struct MailTail {
+  std::atomic<uint32_t> set;
+  cudaIpcEventHandle_t h[kMaxSlots];
+};
+MailTail* mail_tail(MailboxRegion* m) { return reinterpret_cast<MailTail*>(m->base + m->bytes); }
 std::mutex g_mail_mu;
 std::unordered_map<std::string, MailboxRegion*> g_mail_owned;
 void* map_shm(const std::string& name, int64_t bytes, bool create) {
@@ -285,10 +322,11 @@ MailboxRegion* mailbox_create(int device, int64_t bytes, int n_events) {
   try {
     PL_CUDA(cudaSetDevice(device));
     for (int i = 0; i < n_events; ++i)
-      PL_CUDA(cudaEventCreateWithFlags(&m->ev[i], cudaEventDisableTiming | cudaEventInterprocess));
+      PL_CUDA(cudaEventCreateWithFlags(&m->ev_self[i], cudaEventDisableTiming | cudaEventInterprocess));
     m->shm = "/pl-mail-" + std::to_string(getpid()) + "-" + std::to_string(++g_ring_counter);
-    m->base = static_cast<uint8_t*>(map_shm(m->shm, m->bytes, true));
+    m->base = static_cast<uint8_t*>(map_shm(m->shm, m->bytes + kMailTail, true));
     std::memset(m->base, 0, 4096);
+    std::memset(m->base + m->bytes, 0, kMailTail);
   } catch (...) {
     mailbox_destroy(m);
     throw;
@@ -309,7 +347,7 @@ void mailbox_export(MailboxRegion* m, void* out, int64_t cap, int64_t* n_out) {
   b.n_events = m->n_events;
   b.bytes = m->bytes;
   PL_CUDA(cudaSetDevice(m->device));
-  for (int i = 0; i < m->n_events; ++i) PL_CUDA(cudaIpcGetEventHandle(&b.ev[i], m->ev[i]));
+  for (int i = 0; i < m->n_events; ++i) PL_CUDA(cudaIpcGetEventHandle(&b.ev[i], m->ev_self[i]));
   std::strncpy(b.shm, m->shm.c_str(), sizeof(b.shm) - 1);
   std::memcpy(out, &b, sizeof(b));
 }
@@ -331,15 +369,26 @@ MailboxRegion* mailbox_open(int device, const void* blob, int64_t n) {
       delete m;
       fail(PL_E_INVALID, "mailbox owner not found in this process");
     }
-    m->base = it->second->base;
-    for (int i = 0; i < m->n_events; ++i) m->ev[i] = it->second->ev[i];
+    MailboxRegion* o = it->second;
+    m->base = o->base;
+    m->owner_region = o;
+    for (int i = 0; i < m->n_events; ++i) m->ev_self[i] = m->ev_peer[i] = o->ev_self[i];
+    for (int i = 0; i < o->n_events; ++i) o->ev_peer[i] = o->ev_self[i];
+    m->peer_open = o->peer_open = true;
     return m;
   }
   m->ipc = true;
   try {
     PL_CUDA(cudaSetDevice(device));
-    for (int i = 0; i < m->n_events; ++i) PL_CUDA(cudaIpcOpenEventHandle(&m->ev[i], b.ev[i]));
-    m->base = static_cast<uint8_t*>(map_shm(m->shm, m->bytes, false));
+    for (int i = 0; i < m->n_events; ++i) {
+      PL_CUDA(cudaIpcOpenEventHandle(&m->ev_peer[i], b.ev[i]));
+      PL_CUDA(cudaEventCreateWithFlags(&m->ev_self[i], cudaEventDisableTiming | cudaEventInterprocess));
+    }
+    m->peer_open = m->peer_opened_ipc = true;
+    m->base = static_cast<uint8_t*>(map_shm(m->shm, m->bytes + kMailTail, false));
+    MailTail* t = mail_tail(m);
+    for (int i = 0; i < m->n_events; ++i) PL_CUDA(cudaIpcGetEventHandle(&t->h[i], m->ev_self[i]));
+    t->set.store(1, std::memory_order_release);  // before this side posts anything
   } catch (...) {
     mailbox_destroy(m);
     throw;
@@ -355,17 +404,22 @@ void mailbox_destroy(MailboxRegion* m) {
       g_mail_owned.erase(m->shm);
     }
     cudaSetDevice(m->device);
-    for (int i = 0; i < m->n_events; ++i)
-      if (m->ev[i]) {
-        cudaEventSynchronize(m->ev[i]);
-        cudaEventDestroy(m->ev[i]);
+    for (int i = 0; i < m->n_events; ++i) {
+      if (m->ev_self[i]) {
+        cudaEventSynchronize(m->ev_self[i]);
+        cudaEventDestroy(m->ev_self[i]);
       }
-    if (m->base) munmap(m->base, (size_t)m->bytes);
+      if (m->peer_opened_ipc && m->ev_peer[i]) cudaEventDestroy(m->ev_peer[i]);
+    }
+    if (m->base) munmap(m->base, (size_t)(m->bytes + kMailTail));
     if (!m->shm.empty()) shm_unlink(m->shm.c_str());
   } else if (m->ipc) {
-    for (int i = 0; i < m->n_events; ++i)
-      if (m->ev[i]) cudaEventDestroy(m->ev[i]);
-    if (m->base) munmap(m->base, (size_t)m->bytes);
+    cudaSetDevice(m->device);
+    for (int i = 0; i < m->n_events; ++i) {
+      if (m->ev_self[i]) cudaEventDestroy(m->ev_self[i]);
+      if (m->ev_peer[i]) cudaEventDestroy(m->ev_peer[i]);
+    }
+    if (m->base) munmap(m->base, (size_t)(m->bytes + kMailTail));
   }
   delete m;
 }
@@ -395,13 +449,25 @@ uint64_t mailbox_wait(MailboxRegion* m, int64_t word, uint64_t at_least, int64_t
   return v;
 }
 
+// record this side's event i (created on this side's device)
 void mailbox_record(MailboxRegion* m, int i, cudaStream_t st) {
   if (i < 0 || i >= m->n_events) fail(PL_E_INVALID, "mailbox event out of range");
-  PL_CUDA(cudaEventRecord(m->ev[i], st));
+  PL_CUDA(cudaEventRecord(m->ev_self[i], st));
 }
+// make `st` wait for the other side's last record of event i (cross-device waits are fine)
 void mailbox_stream_wait(MailboxRegion* m, int i, cudaStream_t st) {
   if (i < 0 || i >= m->n_events) fail(PL_E_INVALID, "mailbox event out of range");
-  PL_CUDA(cudaStreamWaitEvent(st, m->ev[i], 0));
+  if (!m->peer_open) {
+    // owner with a peer in another process: its handles were published before its first
+    // post, which this side has observed before waiting on its event
+    MailTail* t = mail_tail(m);
+    if (!t->set.load(std::memory_order_acquire))
+      fail(PL_E_STATE, "mailbox: the peer has not published its events");
+    PL_CUDA(cudaSetDevice(m->device));
+    for (int k = 0; k < m->n_events; ++k) PL_CUDA(cudaIpcOpenEventHandle(&m->ev_peer[k], t->h[k]));
+    m->peer_open = m->peer_opened_ipc = true;
+  }
+  PL_CUDA(cudaStreamWaitEvent(st, m->ev_peer[i], 0));
 }
 
 }  // namespace pl
