@@ -388,6 +388,11 @@ struct Store {
   // order this store's stream after every attached patch's side-stream reads of the
   // source (K3/K4 on Patch::stream) -- before slots are released, moved or dropped
   void order_after_patches();
+  // an event on this store's device recorded on its stream now: the ordering point other
+  // streams (possibly on other devices) wait on -- a process records only its own device's
+  // events into that device's streams.  Each call re-records it; callers wait right away.
+  cudaEvent_t point_ev = nullptr;
+  cudaEvent_t record_point();
   // single-process multi-GPU: let kernels on `peer` read this store's device buffers
   // (block table, bases: CUDA peer access) and read/write its pools (VMM access)
   void grant_peer_access(int peer);
@@ -542,7 +547,7 @@ struct Patch {
   int64_t* d_part = nullptr;    // chunked push: d_cells bucketed by run
   int64_t part_cap = 0;
 
-  cudaEvent_t ev_gathered = nullptr, ev_applied = nullptr, ev_dst = nullptr;
+  cudaEvent_t ev_gathered = nullptr, ev_applied = nullptr;
   bool applied_recorded = false;
   // staging of the in-flight patch: rows of [fp 8B][pad 8B][k * cell_bytes]; keys
   uint8_t* d_rows = nullptr;
@@ -594,7 +599,7 @@ struct Patch {
   void push_remote(Remote* r, int64_t n_items_applied);
   int64_t device_dirty_count();
   bool fused_round() const;  // K3 + push in one launch for sparse rounds
-  void device_drain_push(Store* dst, const std::vector<uint8_t>* mask, bool wait_dst = true);
+  void device_drain_push(Store* dst, const std::vector<uint8_t>* mask, cudaEvent_t dst_point);
   void launch_steady(Store* dst);
   bool dst_needs_event(const Store* dst) const;
   // host phases of the last push (ms): adoption wait for lazily mapped pools, dirty-set

@@ -52,7 +52,6 @@ Patch::Patch(Store* src_, const int32_t* g, const int32_t* layers, int n)
   d_count = d_cnt;
   PL_CUDA(cudaEventCreateWithFlags(&ev_gathered, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_applied, cudaEventDisableTiming));
-  PL_CUDA(cudaEventCreateWithFlags(&ev_dst, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_src, cudaEventDisableTiming));
   PL_CUDA(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
   for (int i = 0; i < kMaskSlots; ++i)
@@ -94,7 +93,6 @@ Patch::~Patch() {
   cudaFree(d_groups_);
   cudaEventDestroy(ev_gathered);
   cudaEventDestroy(ev_applied);
-  cudaEventDestroy(ev_dst);
   cudaEventDestroy(ev_src);
   cudaEventDestroy(ev_snap);
   for (int i = 0; i < kMaskSlots; ++i) {
@@ -529,7 +527,12 @@ void Patch::apply(Store* dst, const int32_t* rank, int64_t n_rank, const uint8_t
     for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);  // pool mapped (lazy groups)
     launch_copy(c, dst->stream);
   }
-  PL_CUDA(cudaEventRecord(ev_applied, dst->stream));
+  // "applied" as seen from the patch stream: an event recorded on the destination's
+  // device (a process records only its own device's events into that device's streams)
+  const cudaEvent_t point = dst->record_point();
+  PL_CUDA(cudaSetDevice(src->device));
+  PL_CUDA(cudaStreamWaitEvent(pstream(), point, 0));
+  PL_CUDA(cudaEventRecord(ev_applied, pstream()));
   applied_recorded = true;
   if (status != PL_OK) fail(status, dst->last_msg);
 }
@@ -694,9 +697,9 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
     dst->flush();
     const auto tl = std::chrono::steady_clock::now();
     t_flush += std::chrono::duration<double, std::milli>(tl - tf).count();
-    PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
+    const cudaEvent_t dst_point = dst->record_point();
     PL_CUDA(cudaSetDevice(src->device));
-    PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
+    PL_CUDA(cudaStreamWaitEvent(pstream(), dst_point, 0));
     for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);  // pool mapped (lazy groups)
     CopyLaunch cl = push_launch(dst, d_apply, (uint8_t)(c + 1));
     cl.cells = d_part + run_off[c];
@@ -730,8 +733,9 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
 // The device side of a launch-first steady round: K3 + the push (or the fused kernel),
 // ordered after the destination stream's queued work; the destination stream then waits
 // for the copy.
-// The copy must follow the destination stream's queued work (ev_dst) unless that stream is
-// the patch stream itself, or the source's stream (whose ev_src, recorded later, covers it).
+// The copy must follow the destination stream's queued work (a record point on it) unless
+// that stream is the patch stream itself, or the source's stream (whose ev_src, recorded
+// later, covers it).
 bool Patch::dst_needs_event(const Store* dst) const {
   return dst->stream != pstream() && dst->stream != src->stream;
 }
@@ -740,11 +744,10 @@ void Patch::launch_steady(Store* dst) {
   const bool same_dev = dst->device == src->device;
   if (!same_dev) PL_CUDA(cudaSetDevice(dst->device));
   dst->flush();
-  const bool dst_ev = dst_needs_event(dst);
-  if (dst_ev) PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
+  const cudaEvent_t dst_point = dst_needs_event(dst) ? dst->record_point() : nullptr;
   if (!same_dev) PL_CUDA(cudaSetDevice(src->device));
   if (fused_round()) {
-    device_drain_push(dst, nullptr, dst_ev);
+    device_drain_push(dst, nullptr, dst_point);
     return;
   }
   device_drain_compact();
@@ -752,7 +755,7 @@ void Patch::launch_steady(Store* dst) {
     PL_CUDA(cudaEventRecord(ev_src, src->stream));
     PL_CUDA(cudaStreamWaitEvent(pstream(), ev_src, 0));
   }
-  if (dst_ev) PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
+  if (dst_point) PL_CUDA(cudaStreamWaitEvent(pstream(), dst_point, 0));
   launch_copy(push_launch(dst, nullptr, 0), pstream());
   PL_CUDA(cudaEventRecord(ev_applied, pstream()));
   applied_recorded = true;
@@ -865,12 +868,12 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
   if (trace)
     std::fprintf(stderr, "[pl] push: take %.3f ms, extend_dst %.3f ms, dst flush %.3f ms (%lld keys)\n",
                  ms(t0, t1), ms(t1, t2), ms(t2, now()), (long long)drained_keys);
-  PL_CUDA(cudaEventRecord(ev_dst, dst->stream));
+  const cudaEvent_t dst_point = dst->record_point();
   PL_CUDA(cudaSetDevice(src->device));
   const auto t3 = now();
   if (fused_round()) {
     // sparse round: K3 and the push in one launch (drain_push_kernel)
-    device_drain_push(dst, status == PL_OK ? nullptr : &mask);
+    device_drain_push(dst, status == PL_OK ? nullptr : &mask, dst_point);
     push_stats[4] = ms(t3, now());
     push_stats[5] = 0;
     push_stats[6] = ms(ta, now());
@@ -889,7 +892,7 @@ void Patch::push(Store* dst, const int32_t* rank, int64_t n_rank, int64_t* keys,
     }
     // every drained item was reserved (no KvOverflow): no mask needed, the copy applies all
     const uint8_t* d_apply = status == PL_OK ? nullptr : stage_mask(mask);
-    PL_CUDA(cudaStreamWaitEvent(pstream(), ev_dst, 0));
+    PL_CUDA(cudaStreamWaitEvent(pstream(), dst_point, 0));
     for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);  // pool mapped (lazy groups)
     launch_copy(push_launch(dst, d_apply, 0), pstream());
   }
@@ -917,7 +920,7 @@ bool Patch::fused_round() const {
   return !off && drained_keys > 0 && drained_keys <= lim;
 }
 
-void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask, bool wait_dst) {
+void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask, cudaEvent_t dst_point) {
   src->flush();
   cudaStream_t ps = pstream();
   uint32_t* old = d_bits;  // epoch flip, as device_drain_compact
@@ -928,7 +931,7 @@ void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask, bool
     PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
   }
   const uint8_t* d_apply = mask ? stage_mask(*mask) : nullptr;
-  if (wait_dst) PL_CUDA(cudaStreamWaitEvent(ps, ev_dst, 0));
+  if (dst_point) PL_CUDA(cudaStreamWaitEvent(ps, dst_point, 0));
   for (int gi = 0; gi < G; ++gi) dst->use_group(groups[gi]);
   cnt_cur ^= 1;
   d_count = d_cnt + cnt_cur;

@@ -41,6 +41,7 @@ Store::Store(int device_, int gpu_id_, int k_, int s_, int64_t cell_bytes_, int 
   PL_CUDA(cudaFree(0));
   PL_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
   stream = own_stream;
+  PL_CUDA(cudaEventCreateWithFlags(&point_ev, cudaEventDisableTiming));
   fp_bytes = round_up((int64_t)s * 8, 128);
   unit_bytes = round_up(fp_bytes + (int64_t)k * s * cell_bytes, 128);
   size_t gran = vmm_granularity(device);
@@ -95,6 +96,7 @@ Store::~Store() {
   cudaFree(d_owner_idx);
   cudaFree(d_scratch);
   cudaFree(d_bases_);
+  if (point_ev) cudaEventDestroy(point_ev);
   if (up_stream) cudaStreamSynchronize(up_stream);
   for (auto& sp : ring_live) {
     cudaEventSynchronize(sp.ev_h2d);
@@ -485,6 +487,11 @@ void Store::grant_peer_access(int peer) {
   PL_CUDA(cudaSetDevice(device));
   for (auto& a : arenas) a.grant_peer(peer);  // pools mapped now and later
   peer_granted.push_back(peer);
+}
+
+cudaEvent_t Store::record_point() {
+  PL_CUDA(cudaEventRecord(point_ev, stream));  // created on this store's device (ctor)
+  return point_ev;
 }
 
 void Store::order_after_patches() {
