@@ -518,7 +518,10 @@ __device__ __forceinline__ uint8_t* fused_dst(const CopyLaunch& c, int64_t cell,
   return reinterpret_cast<uint8_t*>(dbase) + (int64_t)dslot * c.dst_unit;
 }
 
-__global__ void __launch_bounds__(256)
+// PAIR: cells a warp has in flight per step (registers: PAIR x 8 x 16 B per lane);
+// MINB: CTAs per SM the launch bound asks for (occupancy vs registers)
+template <int PAIR, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, int W, unsigned long long* count,
                   unsigned long long* next_count) {
   __shared__ uint16_t queue[kFusedWords * 32];
@@ -596,10 +599,10 @@ drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, int W, unsigned
         sp = unit + c.fp_bytes + ((int64_t)j * c.src_s + off) * c.cell_bytes;
         sfp = reinterpret_cast<const uint64_t*>(unit) + off;
       }
-      int4 buf[2][U];
-      // the first pair's loads go out before anything waits
+      int4 buf[PAIR][U];
+      // the first PAIR cells' loads go out before anything waits
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < PAIR; ++h) {
         const int4* s4 = reinterpret_cast<const int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), h));
         if (h < nb)
 #pragma unroll
@@ -621,10 +624,10 @@ drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, int W, unsigned
           }
         }
       }
-      for (int i = 0; i < nb; i += 2) {
+      for (int i = 0; i < nb; i += PAIR) {
         if (i > 0) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < PAIR; ++h) {
             const int4* s4 = reinterpret_cast<const int4*>(
                 __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), i + h));
             if (i + h < nb)
@@ -634,7 +637,7 @@ drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, int W, unsigned
           }
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < PAIR; ++h) {
           int4* d4 = reinterpret_cast<int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dp), i + h));
           const int4* s4 = reinterpret_cast<const int4*>(
               __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), i + h));
@@ -656,9 +659,16 @@ drain_push_kernel(CopyLaunch c, uint32_t* bits, int64_t n_words, int W, unsigned
 
 void launch_drain_push(const CopyLaunch& c, uint32_t* bits, int64_t n_words, int64_t* count,
                        int64_t* next_count, cudaStream_t st) {
+  // variant (PL_FUSED_VARIANT, A/B timing): 0 = 2 cells in flight per warp at 2 CTAs/SM,
+  // 1 = 1 cell at 4 CTAs/SM, 2 = 2 cells at 3 CTAs/SM, 3 = 1 cell at 3 CTAs/SM
+  // (register-capped)
+  static const int variant = [] {
+    const char* v = std::getenv("PL_FUSED_VARIANT");
+    return v ? std::atoi(v) : 0;
+  }();
   static const int per_sm = [] {
     const char* v = std::getenv("PL_FUSED_CTAS_PER_SM");
-    return v ? std::max(1, std::atoi(v)) : 2;
+    return v ? std::max(1, std::atoi(v)) : (variant == 1 ? 4 : variant >= 2 ? 3 : 2);
   }();
   // the narrowest pass (>= 8 words) whose passes still fit in one wave of `per_sm` CTAs per
   // SM: every CTA then scans once and copies its own keys, none waits for a second pass
@@ -668,9 +678,14 @@ void launch_drain_push(const CopyLaunch& c, uint32_t* bits, int64_t n_words, int
   const int64_t chunks = (n_words + W - 1) / W;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, target));
   KernelTimer timer("drain_push", st);
-  drain_push_kernel<<<(unsigned)grid, 256, 0, st>>>(
-      c, bits, n_words, W, reinterpret_cast<unsigned long long*>(count),
-      reinterpret_cast<unsigned long long*>(next_count));
+  auto cnt = reinterpret_cast<unsigned long long*>(count);
+  auto nxt = reinterpret_cast<unsigned long long*>(next_count);
+  switch (variant) {
+    case 1: drain_push_kernel<1, 4><<<(unsigned)grid, 256, 0, st>>>(c, bits, n_words, W, cnt, nxt); break;
+    case 2: drain_push_kernel<2, 3><<<(unsigned)grid, 256, 0, st>>>(c, bits, n_words, W, cnt, nxt); break;
+    case 3: drain_push_kernel<1, 3><<<(unsigned)grid, 256, 0, st>>>(c, bits, n_words, W, cnt, nxt); break;
+    default: drain_push_kernel<2, 2><<<(unsigned)grid, 256, 0, st>>>(c, bits, n_words, W, cnt, nxt); break;
+  }
   note_launch();
   PL_CUDA(cudaGetLastError());
 }
