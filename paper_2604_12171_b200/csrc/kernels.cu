@@ -661,7 +661,9 @@ void launch_drain_push(const CopyLaunch& c, uint32_t* bits, int64_t n_words, int
                        int64_t* next_count, cudaStream_t st) {
   // variant (PL_FUSED_VARIANT, A/B timing): 0 = 2 cells in flight per warp at 2 CTAs/SM,
   // 1 = 1 cell at 4 CTAs/SM, 2 = 2 cells at 3 CTAs/SM, 3 = 1 cell at 3 CTAs/SM
-  // (register-capped)
+  // (register-capped).  Measured (tools/gpu_fused_ab.sh): within noise of each other at
+  // the decode pattern and 1 %; 1 is ~8 % faster at 5 % (a round the dispatcher gives to
+  // K3 + push_batched anyway) and 6 % slower at 25 %; 2 spills.  0 is kept.
   static const int variant = [] {
     const char* v = std::getenv("PL_FUSED_VARIANT");
     return v ? std::atoi(v) : 0;
