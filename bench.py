@@ -204,6 +204,7 @@ def reference_rate(wl, steps: int, warmup: int, n_req: int = REF_SAMPLE_REQS) ->
                       f"KV-equivalent (cells x {R.CELL} B)",
             "steps": steps, "seconds": round(total, 2),
             "ms_per_step_sample": round(total / steps * 1e3, 2),
+            "sample_bytes": int(rnd.cells * R.CELL),
             "host": R.host_info()}
 
 
@@ -222,6 +223,9 @@ def run_reference(args, wl, rank: int, world: int) -> None:
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GB/s",
         "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": cb["ms_per_step_sample"],
+        # the rate is measured on a bounded sample of the step's workload (cpu_baseline.sample):
+        # ms_per_step is the sample's, and these are the bytes it moved
+        "sample_bytes_per_step": cb.get("sample_bytes"),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic", "config": config_of(wl, world),
         "cpu_baseline": cb,
