@@ -218,7 +218,9 @@ def run_reference(args, wl, rank: int, world: int) -> None:
                           "__graft_entry__.build() in the dev container)"}), flush=True)
         return
     cb = reference_rate(wl, K, W)
-    extras = {"append": R.time_append(16), "compact_resize": R.time_resize()}
+    extras = {"append": R.time_append(16), "compact_resize": R.time_resize(),
+              # the steady patch rounds and the full packaged scenario too
+              "steady_round": R.time_steady(64, 20), "scenario": R.time_scenario()}
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GB/s",
         "n_gpus": world, "steps": K, "warmup": W,

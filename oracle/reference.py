@@ -118,6 +118,44 @@ class BulkRound:
         return dt
 
 
+def time_steady(n_req: int = 64, rounds: int = 20) -> dict:
+    """Steady patch rounds on the reference after the bulk round: every round appends the
+    decode pattern -- one new token per request in each of the stage's groups
+    (engine.py:377-404) -- notifies the migration (on_kv_written, migrator.py:190-197) and
+    runs the event loop until the round's patch is drained, sent and applied."""
+    ps = pipeshift()
+    from pipeshift import events, kvstore, migrator  # noqa: PLC0415
+    b = BulkRound.__new__(BulkRound)
+    b.ps, b.n_req = ps, n_req
+    b.cap = n_req * (CTX // S + 2) + 8
+    b.src = kvstore.KvStore(1, K, S, b.cap, resident_groups=set(SRC_GROUPS))
+    for i in range(n_req):
+        for g in SRC_GROUPS:
+            b.src.append(f"r{i:04d}", g, CTX, _payloads(ps, f"r{i:04d}", g, 0, CTX))
+    sched, trace = events.EventScheduler(), events.EventTrace()
+    fab = ps.CommFabric(sched, trace, [1, 2], ps.FabricConfig())
+    dst = kvstore.KvStore(2, K, S, b.cap, resident_groups=set(MIG_GROUPS))
+    mgr = migrator.MigrationManager(sched, trace, fab, {1: b.src, 2: dst}, token_kv_bytes=CELL, k=K)
+    mgr.start_migration({(1, 2): MIG_LAYERS})
+    sched.run(until=60.0)
+    dt = 0.0
+    for r in range(rounds):
+        pos = CTX + r
+        t0 = time.perf_counter()
+        for i in range(n_req):
+            for g in SRC_GROUPS:
+                b.src.append(f"r{i:04d}", g, 1, _payloads(ps, f"r{i:04d}", g, pos, 1))
+                mgr.on_kv_written(1, f"r{i:04d}", g, pos, 1)
+        sched.run(until=sched.now + 1.0)
+        dt += time.perf_counter() - t0
+        assert mgr.lag(2) == 0
+    cells = n_req * len(MIG_GROUPS) * K
+    return {"requests": n_req, "cells_per_round": cells, "rounds": rounds,
+            "us_per_round": round(dt / rounds * 1e6, 1),
+            "kv_equivalent_gbs": round(cells * CELL * rounds / dt / 1e9, 4),
+            "note": "includes the stage's append of the round's tokens (all 4 groups)"}
+
+
 def time_append(n_req: int = 64) -> dict:
     from pipeshift import kvstore  # noqa: PLC0415
     ps = pipeshift()

@@ -25,4 +25,6 @@ def test_reference_arm_line():
     assert cb["kind"] == "reference" and cb["cores"] == 1 and cb["value"] == line["value"]
     assert line["sample_bytes_per_step"] == cb["sample_bytes"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
-    assert line["reference_extras"]["append"]["cells_per_s"] > 0
+    ex = line["reference_extras"]
+    assert ex["append"]["cells_per_s"] > 0 and ex["steady_round"]["us_per_round"] > 0
+    assert ex["scenario"]["seconds"] > 0
