@@ -558,7 +558,7 @@ def tail_summary(c2, c3, resize, decode, decode_70b, pause, value_cold, hbm_peak
     return out
 
 
-def measure_c2_model(wl, steps: int = 40, reconfig_at: int = 8) -> dict:
+def measure_c2_model(wl, steps: int = 40, reconfig_at: int = 8, run_dir: str | None = None) -> dict:
     """BASELINE configs[1] with the 8B-shaped decoder (paper_2604_12171_b200/model8b.py):
     B = 256 requests at 2048 prefilled positions decode greedily for `steps` steps; the
     live run starts the PP 2 -> 4 reconfiguration (layers 9-16: GPU 1 -> 3, 25-32: 2 -> 4)
@@ -570,14 +570,21 @@ def measure_c2_model(wl, steps: int = 40, reconfig_at: int = 8) -> dict:
 
     import torch
 
+    from paper_2604_12171_b200.engine import compute_metrics
+    from paper_2604_12171_b200.events import EventTrace
     from paper_2604_12171_b200.model8b import run_live, summarize
 
     gc.collect()
     torch.cuda.empty_cache()
     kw = dict(batch=wl.batch, ctx=wl.ctx, steps=steps, reconfig_at=reconfig_at)
     static = run_live(live=False, **kw)
-    live = run_live(live=True, **kw)
+    tr = EventTrace()
+    live = run_live(live=True, trace=tr, **kw)
     s = summarize(live, static)
+    s["trace_metrics"] = compute_metrics(tr).as_row()   # reference schema (engine.py:112-184)
+    if run_dir:   # trace.jsonl / metrics.csv / summary.json in the reference runner's schema
+        from paper_2604_12171_b200 import outputs
+        outputs.write_run(run_dir, tr, "configs[1]:pp2->pp4 (8B shape)", 0, mode="perf", stages=4)
     c = s.pop("commit") or {}
     s["pause"] = {k: c.get(k) for k in ("pause_ms", "drain_ms", "residual_ms",
                                         "barrier_and_switch_ms", "residual_cells", "lag_at_poll")}
@@ -588,7 +595,7 @@ def measure_c2_model(wl, steps: int = 40, reconfig_at: int = 8) -> dict:
     return s
 
 
-def measure_c4_model(wl, steps: int = 40, reconfig_at: int = 8) -> dict:
+def measure_c4_model(wl, steps: int = 40, reconfig_at: int = 8, run_dir: str | None = None) -> dict:
     """BASELINE configs[3] with the 8B-shaped decoder: 8 stage stores (one GPU here, one GPU
     each on hardware), an even split (4 layers per stage, k = 2) re-split live into the
     generation-heavy uneven split 2/4/4/6/6/4/4/2 -- six pairs migrate at once, stages 2, 3,
@@ -601,6 +608,8 @@ def measure_c4_model(wl, steps: int = 40, reconfig_at: int = 8) -> dict:
 
     import torch
 
+    from paper_2604_12171_b200.engine import compute_metrics
+    from paper_2604_12171_b200.events import EventTrace
     from paper_2604_12171_b200.model8b import EVEN8, UNEVEN8, run_live, summarize
 
     gc.collect()
@@ -608,8 +617,14 @@ def measure_c4_model(wl, steps: int = 40, reconfig_at: int = 8) -> dict:
     kw = dict(batch=wl.batch, ctx=wl.ctx, steps=steps, reconfig_at=reconfig_at, src=EVEN8,
               dst=UNEVEN8, k=2)
     static = run_live(live=False, **kw)
-    live = run_live(live=True, **kw)
+    tr = EventTrace()
+    live = run_live(live=True, trace=tr, **kw)
     s = summarize(live, static)
+    s["trace_metrics"] = compute_metrics(tr).as_row()   # reference schema (engine.py:112-184)
+    if run_dir:   # trace.jsonl / metrics.csv / summary.json in the reference runner's schema
+        from paper_2604_12171_b200 import outputs
+        outputs.write_run(run_dir, tr, "configs[3]:even8->uneven8 (8B shape)", 0, mode="perf",
+                          stages=8)
     c = s.pop("commit") or {}
     s["pause"] = {k: c.get(k) for k in ("pause_ms", "drain_ms", "residual_ms",
                                         "barrier_and_switch_ms", "residual_cells", "lag_at_poll")}

@@ -347,12 +347,17 @@ def torch_rsqrt(x32, eps):
 
 def run_live(batch: int = 256, ctx: int = 2048, steps: int = 40, reconfig_at: int = 8,
              live: bool = True, tau: int = 50, device: int = 0, seed: int = 0,
-             src: dict | None = None, dst: dict | None = None, k: int = 4) -> dict:
+             src: dict | None = None, dst: dict | None = None, k: int = 4,
+             trace=None) -> dict:
     """Greedy decode for `steps` steps over the stages of `src` (default PP2, k = 4); with
     `live`, the reconfiguration to `dst` (default PP4: configs[1]; EVEN8 -> UNEVEN8 at k = 2
     is configs[3]) starts after step `reconfig_at` and commits at the first poll with
     lag < tau.  Returns the tokens of every step and the timeline (per-step TPOT, phases,
-    pause breakdown)."""
+    pause breakdown).  `trace` (an events.EventTrace) receives the run in the reference's
+    trace schema with wall-clock times (the engine's request / decode-step events, the
+    coordinator's reconfigure / convergence / commit-pause events), so
+    engine.compute_metrics and outputs.write_run apply; requests arrive with their
+    prefilled context, so TTFT is the first decode step."""
     import torch
 
     src, dst = src or PP2, dst or PP4
@@ -365,13 +370,26 @@ def run_live(batch: int = 256, ctx: int = 2048, steps: int = 40, reconfig_at: in
     commit = None
     bulk = None
     t_run = time.perf_counter()
+
+    def emit(kind, at=None, actor="engine", **payload):
+        if trace is not None:
+            trace.emit((at if at is not None else time.perf_counter()) - t_run, actor, kind,
+                       **payload)
+
+    for rid in pipe.rids:
+        emit("request_arrival", id=rid, input_len=ctx, output_len=steps)
     with torch.cuda.stream(pipe.stream):
         for t in range(steps):
             if phase == "migrating":
                 lag = pipe.lag()                   # the safe-switch poll (once per step)
                 out["lag"].append(lag)
+                emit("convergence_check", actor="coordinator", lag=lag, tau=tau)
                 if lag < tau:
+                    tp = time.perf_counter()
+                    emit("commit_pause_start", at=tp, actor="coordinator")
                     commit = {"step": t, "lag_at_poll": lag, **pipe.switch()}
+                    emit("commit_pause_end", at=tp + commit["pause_ms"] / 1e3, actor="coordinator")
+                    emit("reconfigure_end", actor="coordinator", outcome="success")
                     phase = "after"
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             th = time.perf_counter()
@@ -386,8 +404,16 @@ def run_live(batch: int = 256, ctx: int = 2048, steps: int = 40, reconfig_at: in
             out["tokens"].append(tok_host.tolist())
             out["step_ms"].append((e0, e1, host_ms))
             out["phase"].append(phase)
+            emit("decode_step", step=t, batch=batch, ms=round(host_ms, 4))
+            for rid in pipe.rids:
+                if t == 0:
+                    emit("first_token", id=rid)
+                if t == steps - 1:
+                    emit("request_done", id=rid)
             tokens = nxt
             if live and t == reconfig_at:
+                emit("reconfigure_start", actor="coordinator",
+                     target={str(g): ls for g, ls in sorted(dst.items())})
                 tb = time.perf_counter()
                 b0 = torch.cuda.Event(enable_timing=True)
                 r = pipe.start_reconfig(dst, before_bulk=lambda: b0.record(pipe.side))
@@ -397,6 +423,7 @@ def run_live(batch: int = 256, ctx: int = 2048, steps: int = 40, reconfig_at: in
                         "phase3_map_ms": pipe.map_ms,
                         "host_enqueue_ms": round((time.perf_counter() - tb) * 1e3 - pipe.map_ms, 3),
                         "host_phases_ms": r["host_phases_ms"], "events": (b0, b1)}
+                emit("migration_seeded", actor="coordinator", cells=r["cells"])
                 phase = "migrating"
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_run

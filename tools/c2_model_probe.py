@@ -1,4 +1,4 @@
-"""configs[1] with real 8B-shaped stage compute alone (bench.measure_c2_model) -> stdout."""
+"""configs[1] with real 8B-shaped stage compute alone (bench.measure_c2_model) -> stdout, and the live run's trace.jsonl / metrics.csv / summary.json -> gpurun_out/c2_model_run/."""
 import json
 import sys
 from pathlib import Path
@@ -7,4 +7,4 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 from paper_2604_12171_b200.perf import Workload  # noqa: E402
 
-print(json.dumps(bench.measure_c2_model(Workload()), indent=1))
+print(json.dumps(bench.measure_c2_model(Workload(), run_dir='gpurun_out/c2_model_run'), indent=1))
