@@ -715,6 +715,7 @@ struct CopyLaunch {
   uint64_t src_base_l[kInlineGroups], dst_base_l[kInlineGroups];
 };
 void launch_copy(const CopyLaunch& c, cudaStream_t st);
+void preload_kernels();  // load the data-path kernels now (lazy loading off the first round)
 // K3 + fused push in one launch for sparse rounds
 void launch_drain_push(const CopyLaunch& c, uint32_t* bits, int64_t n_words, int64_t* count,
                        int64_t* next_count, cudaStream_t st);

@@ -1,5 +1,7 @@
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 // Data-plane kernels of the live-reconfiguration path (sm_100a).
 //
 //   K1  kv_write_mark  : KvStore.append / write_slots (kvstore.py:163-227) fused with the
@@ -791,6 +793,31 @@ __global__ void __launch_bounds__(kWarps * 32) push_batched_kernel(CopyLaunch c,
     }
     if (dfp) *dfp = fpv;
   }
+}
+
+// CUDA loads kernels lazily (on first launch) by default: the first reconfiguration's
+// cold bulk round would pay for loading the partition / push kernels inside its wall time.
+// Stores load the data-path kernels when they are created instead (once per process and
+// device).
+void preload_kernels() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  PL_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (int d : done)
+    if (d == dev) return;
+  done.push_back(dev);
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      (const void*)kv_write_kernel, (const void*)write_layer_kernel,
+      (const void*)apply_deltas_kernel, (const void*)mark_kernel, (const void*)clear_slots_kernel,
+      (const void*)move_slots_kernel, (const void*)unit_move_kernel,
+      (const void*)table_remap_kernel, (const void*)popcount_kernel,
+      (const void*)drain_compact_kernel, (const void*)partition_runs_kernel,
+      (const void*)copy_kernel<0>, (const void*)copy_kernel<1>, (const void*)copy_kernel<2>,
+      (const void*)drain_push_kernel<2, 2>, (const void*)push_batched_kernel};
+  for (const void* f : fns) PL_CUDA(cudaFuncGetAttributes(&a, f));
 }
 
 void launch_copy(const CopyLaunch& c, cudaStream_t st) {

@@ -625,16 +625,20 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
   const auto t0 = std::chrono::steady_clock::now();
   int64_t max_req = 0;
   const std::vector<size_t> order = apply_order(rank, n_rank, nullptr, 0, &max_req);
-  // runs of about 1/8 of the keys (>= 64 k keys unless forced), at most 254 of them
+  // runs of about 1/8 of the keys (>= 64 k keys unless forced), at most 254 of them; the
+  // first run is a quarter of that, so the copy starts after a short reservation (the
+  // host reserves about twice as fast as the copy consumes, so it stays ahead after that)
   std::vector<size_t> cut{0};
   std::vector<int64_t> run_keys;
   {
-    const int64_t target =
-        std::max<int64_t>(drained_keys / 8, std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS") ? 1 : 1 << 16);
+    const bool forced = std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS") != nullptr;
+    const int64_t target = std::max<int64_t>(drained_keys / 8, forced ? 1 : 1 << 16);
+    const int64_t first = std::max<int64_t>(target / 4, forced ? 1 : 1 << 12);
     int64_t acc = 0;
     for (size_t x = 0; x < order.size(); ++x) {
       for (const Interval& r : std::get<2>(drained[order[x]])) acc += r.b - r.a;
-      if ((acc >= target && cut.size() < 254) || x + 1 == order.size()) {
+      if ((acc >= (cut.size() == 1 ? first : target) && cut.size() < 254) ||
+          x + 1 == order.size()) {
         cut.push_back(x + 1);
         run_keys.push_back(acc);
         acc = 0;

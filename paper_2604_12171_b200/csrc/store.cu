@@ -42,6 +42,7 @@ Store::Store(int device_, int gpu_id_, int k_, int s_, int64_t cell_bytes_, int 
   PL_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
   stream = own_stream;
   PL_CUDA(cudaEventCreateWithFlags(&point_ev, cudaEventDisableTiming));
+  preload_kernels();
   fp_bytes = round_up((int64_t)s * 8, 128);
   unit_bytes = round_up(fp_bytes + (int64_t)k * s * cell_bytes, 128);
   size_t gran = vmm_granularity(device);
