@@ -766,7 +766,10 @@ def kv_init(gpu: GpuSpec, model: ModelSpec, capacity_blocks: int,
     if kv_bytes + weight_bytes > gpu.mem_total:
         raise InsufficientMemory(
             f"gpu {gpu.id}: {kv_bytes + weight_bytes} B exceeds {gpu.mem_total} B")
+    # the model's group count from the fields every ModelSpec has (the reference's own
+    # ModelSpec has no num_groups: a maintainer's shim hands it to this kv_init unchanged)
+    n_groups = -(-model.num_layers // model.stacking_factor)
     return KvStore(gpu.id, model.stacking_factor, model.tokens_per_block(gpu), capacity_blocks,
-                   groups, num_groups=max(model.num_groups, DEFAULT_MODEL_GROUPS),
+                   groups, num_groups=max(n_groups, DEFAULT_MODEL_GROUPS),
                    cell_bytes=cell_bytes or default_cell_bytes(model), device=device,
                    registry=registry, chunk_bytes=chunk_bytes)
