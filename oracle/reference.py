@@ -28,6 +28,7 @@ HERE = Path(__file__).resolve().parent
 REF_DIR = HERE / "_ref"
 REFERENCE_SRC = Path("/root/reference/pkg/src/pipeshift")
 REFERENCE_SCENARIO = Path("/root/reference/pkg/scenarios/heterogeneous_shift.yaml")
+REFERENCE_TESTS = Path("/root/reference/pkg/tests")
 
 CELL = 4096          # token_kv_bytes_per_layer of the Llama-3 shapes
 K, S, CTX = 4, 16, 2048
@@ -50,6 +51,15 @@ def stage(force: bool = False) -> Path | None:
         (REF_DIR / "scenarios").mkdir(parents=True, exist_ok=True)
         if REFERENCE_SCENARIO.exists():
             shutil.copy2(REFERENCE_SCENARIO, REF_DIR / "scenarios" / REFERENCE_SCENARIO.name)
+    # the reference's own test modules, unmodified: tests/test_gpu_reference_own_suites.py
+    # runs them against this package's data plane through the maintainer shim
+    tdst = REF_DIR / "tests"
+    if REFERENCE_TESTS.is_dir() and (force or not tdst.exists() or any(
+            not (tdst / p.name).exists() or p.stat().st_mtime > (tdst / p.name).stat().st_mtime
+            for p in REFERENCE_TESTS.glob("*.py"))):
+        if tdst.exists():
+            shutil.rmtree(tdst)
+        shutil.copytree(REFERENCE_TESTS, tdst, ignore=shutil.ignore_patterns("__pycache__"))
     return REF_DIR
 
 
