@@ -703,7 +703,10 @@ void launch_drain_push(const CopyLaunch& c, uint32_t* bits, int64_t n_words, int
 // shared memory once per CTA (no base-pointer loads on the chain).  The fingerprint word
 // of a key (layer 0) is loaded during the resolve and stored after the cells.
 constexpr int kMaxSmemGroups = 64;
-__global__ void __launch_bounds__(kWarps * 32) push_batched_kernel(CopyLaunch c, int batch) {
+// FULL: cell_bytes == 32 x U x 16 B (the Llama shapes' 4096-B cells): no per-vector
+// predicates and no remainder loop in the copy
+template <int MINB, bool FULL>
+__global__ void __launch_bounds__(kWarps * 32, MINB) push_batched_kernel(CopyLaunch c, int batch) {
   __shared__ uint64_t s_sb[kMaxSmemGroups], s_db[kMaxSmemGroups];
   const bool smem_bases = c.G <= kMaxSmemGroups;
   if (smem_bases && threadIdx.x < c.G) {
@@ -780,15 +783,16 @@ __global__ void __launch_bounds__(kWarps * 32) push_batched_kernel(CopyLaunch c,
         if (d4[h])
 #pragma unroll
           for (int u = 0; u < U; ++u)
-            if (lane + 32 * u < vecs) buf[h][u] = ld_stream(s4[h] + lane + 32 * u);
+            if (FULL || lane + 32 * u < vecs) buf[h][u] = ld_stream(s4[h] + lane + 32 * u);
 #pragma unroll
       for (int h = 0; h < 2; ++h)
         if (d4[h]) {
 #pragma unroll
           for (int u = 0; u < U; ++u)
-            if (lane + 32 * u < vecs) st_stream(d4[h] + lane + 32 * u, buf[h][u]);
+            if (FULL || lane + 32 * u < vecs) st_stream(d4[h] + lane + 32 * u, buf[h][u]);
           // cells wider than 32 x U x 16 B (not the Llama shapes): the rest, plainly
-          for (int64_t e = lane + 32 * U; e < vecs; e += 32) st_stream(d4[h] + e, ld_stream(s4[h] + e));
+          if (!FULL)
+            for (int64_t e = lane + 32 * U; e < vecs; e += 32) st_stream(d4[h] + e, ld_stream(s4[h] + e));
         }
     }
     if (dfp) *dfp = fpv;
@@ -816,7 +820,8 @@ void preload_kernels() {
       (const void*)table_remap_kernel, (const void*)popcount_kernel,
       (const void*)drain_compact_kernel, (const void*)partition_runs_kernel,
       (const void*)copy_kernel<0>, (const void*)copy_kernel<1>, (const void*)copy_kernel<2>,
-      (const void*)drain_push_kernel<2, 2>, (const void*)push_batched_kernel};
+      (const void*)drain_push_kernel<2, 2>, (const void*)push_batched_kernel<1, true>,
+      (const void*)push_batched_kernel<1, false>};
   for (const void* f : fns) PL_CUDA(cudaFuncGetAttributes(&a, f));
 }
 
@@ -834,9 +839,21 @@ void launch_copy(const CopyLaunch& c, cudaStream_t st) {
     int64_t b = (items + cap_warps - 1) / cap_warps;
     b = std::min<int64_t>(32, std::max<int64_t>(2, (b + 1) & ~int64_t(1)));
     const int64_t grid = std::max<int64_t>(1, (items + b * kWarps - 1) / (b * kWarps));
+    // PL_PUSH_MINB (A/B): CTAs per SM the launch bound asks for (registers vs occupancy)
+    static const int minb = [] {
+      const char* v = std::getenv("PL_PUSH_MINB");
+      return v ? std::atoi(v) : 1;
+    }();
     KernelTimer timer("patch_push", st);
-    push_batched_kernel<<<(unsigned)std::min<int64_t>(grid, (int64_t)sm_count() * 16), kWarps * 32,
-                          0, st>>>(c, (int)b);
+    const unsigned g = (unsigned)std::min<int64_t>(grid, (int64_t)sm_count() * 16);
+    const bool full = c.cell_bytes == 32 * 8 * 16;
+    if (full) {
+      if (minb >= 3) push_batched_kernel<3, true><<<g, kWarps * 32, 0, st>>>(c, (int)b);
+      else if (minb == 2) push_batched_kernel<2, true><<<g, kWarps * 32, 0, st>>>(c, (int)b);
+      else push_batched_kernel<1, true><<<g, kWarps * 32, 0, st>>>(c, (int)b);
+    } else {
+      push_batched_kernel<1, false><<<g, kWarps * 32, 0, st>>>(c, (int)b);
+    }
     note_launch();
     PL_CUDA(cudaGetLastError());
     return;
