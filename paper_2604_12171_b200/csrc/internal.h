@@ -712,6 +712,9 @@ struct CopyLaunch {
   // them in shared memory without the src_groups -> bases dependent loads
   static constexpr int kInlineGroups = 8;
   int inline_bases;
+  // push: lanes of a batch run layer-major (dense rounds: neighbouring positions of one
+  // layer are neighbouring cells in memory) instead of token-major (sparse rounds)
+  int layer_major;
   uint64_t src_base_l[kInlineGroups], dst_base_l[kInlineGroups];
 };
 void launch_copy(const CopyLaunch& c, cudaStream_t st);

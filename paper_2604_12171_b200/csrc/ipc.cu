@@ -188,6 +188,7 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
     c.dst_table = r->table;
     c.dst_max_chain = r->max_chain;
     c.apply_mask = d_apply;
+    c.layer_major = drained_keys * 2 >= n_words * 32 ? 1 : 0;  // as Patch::push_launch
     if (G <= CopyLaunch::kInlineGroups) {
       c.inline_bases = 1;
       for (int i = 0; i < G; ++i) {
@@ -235,6 +236,7 @@ void Patch::push_remote(Remote* r, int64_t n_applied) {
     c.dst_table = r->table;
     c.dst_max_chain = r->max_chain;
     c.apply_mask = d_apply;
+    c.layer_major = drained_keys * 2 >= n_words * 32 ? 1 : 0;  // as Patch::push_launch
     if (G <= CopyLaunch::kInlineGroups) {
       c.inline_bases = 1;
       for (int i = 0; i < G; ++i) {

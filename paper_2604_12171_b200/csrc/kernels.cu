@@ -706,7 +706,8 @@ constexpr int kMaxSmemGroups = 64;
 // FULL: cell_bytes == 32 x U x 16 B (the Llama shapes' 4096-B cells): no per-vector
 // predicates and no remainder loop in the copy
 template <int MINB, bool FULL>
-__global__ void __launch_bounds__(kWarps * 32, MINB) push_batched_kernel(CopyLaunch c, int batch) {
+__global__ void __launch_bounds__(kWarps * 32, MINB) push_batched_kernel(CopyLaunch c, int batch,
+                                                                         int layer_major) {
   __shared__ uint64_t s_sb[kMaxSmemGroups], s_db[kMaxSmemGroups];
   const bool smem_bases = c.G <= kMaxSmemGroups;
   if (smem_bases && threadIdx.x < c.G) {
@@ -728,53 +729,68 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) push_batched_kernel(CopyLau
   const int64_t vecs = c.cell_bytes >> 4;
   const int64_t per_slot = (int64_t)c.G * c.src_s;
   constexpr int U = 8;
-  for (int64_t b0 = warp0 * batch; b0 < items; b0 += nwarps * batch) {
-    const uint8_t* sp = nullptr;
-    uint8_t* dp = nullptr;
-    uint64_t* dfp = nullptr;
-    uint64_t fpv = 0;
-    const int64_t item = b0 + lane;
-    if (lane < batch && item < items) {
-      const int64_t r = item / c.k;
-      const int j = (int)(item - r * c.k);
-      const int64_t cell = c.cells[r];
-      const int32_t slot = (int32_t)(cell / per_slot);
-      const int64_t rem = cell - (int64_t)slot * per_slot;
-      const int32_t lg = (int32_t)(rem / c.src_s);
-      const int off = (int)(rem - (int64_t)lg * c.src_s);
-      const int32_t req = c.src_owner[slot];
-      const int32_t oidx = c.src_owner_idx[slot];
-      const uint64_t sbase = smem_bases ? s_sb[lg] : c.src_bases[c.src_groups[lg]];
-      const uint8_t* unit = reinterpret_cast<const uint8_t*>(sbase) + (int64_t)slot * c.src_unit;
-      bool ok = req >= 0;
-      if (ok && c.apply_mask) {
-        const uint8_t m = c.apply_mask[(int64_t)req * c.G + lg];
-        ok = c.apply_id ? m == c.apply_id : m != 0;
-      }
-      if (ok) {
-        const int64_t pos = (int64_t)oidx * c.src_s + off;
-        const int32_t dslot = c.dst_table[(int64_t)req * c.dst_max_chain + pos / c.dst_s];
-        if (dslot >= 0) {
-          const int doff = (int)(pos % c.dst_s);
-          const uint64_t dbase = smem_bases ? s_db[lg] : c.dst_bases[c.src_groups[lg]];
-          uint8_t* du = reinterpret_cast<uint8_t*>(dbase) + (int64_t)dslot * c.dst_unit;
-          sp = unit + c.fp_bytes + ((int64_t)j * c.src_s + off) * c.cell_bytes;
-          dp = du + c.fp_bytes + ((int64_t)j * c.dst_s + doff) * c.cell_bytes;
-          if (j == 0) {
-            dfp = reinterpret_cast<uint64_t*>(du) + doff;
-            fpv = reinterpret_cast<const uint64_t*>(unit)[off];
-          }
-        }
-      }
+  // lane's item of the batch starting at bx -> source / destination cell, fp word
+  struct Res {
+    const uint8_t* sp;
+    uint8_t* dp;
+    uint64_t* dfp;
+    uint64_t fpv;
+  };
+  // within a batch, lanes run layer-major (lane l -> key l % (batch / k), layer
+  // l / (batch / k)) when the batch is whole keys: a warp's two cells in flight are then
+  // neighbouring positions of one layer -- 8 contiguous KiB of the source unit
+  const bool lm = layer_major && batch % c.k == 0;
+  const int kpb = lm ? batch / c.k : 1;
+  auto resolve = [&](int64_t bx) -> Res {
+    Res o{nullptr, nullptr, nullptr, 0};
+    const int64_t item = lm ? bx + (int64_t)(lane % kpb) * c.k + lane / kpb : bx + lane;
+    if (bx >= items || lane >= batch || item >= items) return o;
+    const int64_t r = item / c.k;
+    const int j = (int)(item - r * c.k);
+    const int64_t cell = c.cells[r];
+    const int32_t slot = (int32_t)(cell / per_slot);
+    const int64_t rem = cell - (int64_t)slot * per_slot;
+    const int32_t lg = (int32_t)(rem / c.src_s);
+    const int off = (int)(rem - (int64_t)lg * c.src_s);
+    const int32_t req = c.src_owner[slot];
+    const int32_t oidx = c.src_owner_idx[slot];
+    const uint64_t sbase = smem_bases ? s_sb[lg] : c.src_bases[c.src_groups[lg]];
+    const uint8_t* unit = reinterpret_cast<const uint8_t*>(sbase) + (int64_t)slot * c.src_unit;
+    bool ok = req >= 0;
+    if (ok && c.apply_mask) {
+      const uint8_t m = c.apply_mask[(int64_t)req * c.G + lg];
+      ok = c.apply_id ? m == c.apply_id : m != 0;
     }
-    const int nb = (int)min((int64_t)batch, items - b0);
+    if (!ok) return o;
+    const int64_t pos = (int64_t)oidx * c.src_s + off;
+    const int32_t dslot = c.dst_table[(int64_t)req * c.dst_max_chain + pos / c.dst_s];
+    if (dslot < 0) return o;
+    const int doff = (int)(pos % c.dst_s);
+    const uint64_t dbase = smem_bases ? s_db[lg] : c.dst_bases[c.src_groups[lg]];
+    uint8_t* du = reinterpret_cast<uint8_t*>(dbase) + (int64_t)dslot * c.dst_unit;
+    o.sp = unit + c.fp_bytes + ((int64_t)j * c.src_s + off) * c.cell_bytes;
+    o.dp = du + c.fp_bytes + ((int64_t)j * c.dst_s + doff) * c.cell_bytes;
+    if (j == 0) {
+      o.dfp = reinterpret_cast<uint64_t*>(du) + doff;
+      o.fpv = reinterpret_cast<const uint64_t*>(unit)[off];
+    }
+    return o;
+  };
+  const int64_t stride = nwarps * batch;
+  int64_t b0 = warp0 * batch;
+  Res cur = resolve(b0);
+  for (; b0 < items; b0 += stride) {
+    // layer-major lanes of a partial last batch are not a prefix: walk every lane (the
+    // ones past the end hold no cell)
+    const int nb = lm ? batch : (int)min((int64_t)batch, items - b0);
+    Res nxt{nullptr, nullptr, nullptr, 0};
     for (int i = 0; i < nb; i += 2) {
       const int4* s4[2];
       int4* d4[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        s4[h] = reinterpret_cast<const int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), i + h));
-        d4[h] = reinterpret_cast<int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dp), i + h));
+        s4[h] = reinterpret_cast<const int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(cur.sp), i + h));
+        d4[h] = reinterpret_cast<int4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(cur.dp), i + h));
         if (i + h >= nb) d4[h] = nullptr;
       }
       int4 buf[2][U];
@@ -784,6 +800,10 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) push_batched_kernel(CopyLau
 #pragma unroll
           for (int u = 0; u < U; ++u)
             if (FULL || lane + 32 * u < vecs) buf[h][u] = ld_stream(s4[h] + lane + 32 * u);
+      // the next batch's addresses resolve while the first pair's loads are in flight
+      // (the warp would otherwise stall on the cell list -> owner map -> block table chain
+      // between batches with nothing of its own in flight)
+      if (i == 0) nxt = resolve(b0 + stride);
 #pragma unroll
       for (int h = 0; h < 2; ++h)
         if (d4[h]) {
@@ -795,7 +815,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) push_batched_kernel(CopyLau
             for (int64_t e = lane + 32 * U; e < vecs; e += 32) st_stream(d4[h] + e, ld_stream(s4[h] + e));
         }
     }
-    if (dfp) *dfp = fpv;
+    if (cur.dfp) *cur.dfp = cur.fpv;
+    cur = nxt;
   }
 }
 
@@ -846,13 +867,14 @@ void launch_copy(const CopyLaunch& c, cudaStream_t st) {
     }();
     KernelTimer timer("patch_push", st);
     const unsigned g = (unsigned)std::min<int64_t>(grid, (int64_t)sm_count() * 16);
+    const int lm = c.layer_major;
     const bool full = c.cell_bytes == 32 * 8 * 16;
     if (full) {
-      if (minb >= 3) push_batched_kernel<3, true><<<g, kWarps * 32, 0, st>>>(c, (int)b);
-      else if (minb == 2) push_batched_kernel<2, true><<<g, kWarps * 32, 0, st>>>(c, (int)b);
-      else push_batched_kernel<1, true><<<g, kWarps * 32, 0, st>>>(c, (int)b);
+      if (minb >= 3) push_batched_kernel<3, true><<<g, kWarps * 32, 0, st>>>(c, (int)b, lm);
+      else if (minb == 2) push_batched_kernel<2, true><<<g, kWarps * 32, 0, st>>>(c, (int)b, lm);
+      else push_batched_kernel<1, true><<<g, kWarps * 32, 0, st>>>(c, (int)b, lm);
     } else {
-      push_batched_kernel<1, false><<<g, kWarps * 32, 0, st>>>(c, (int)b);
+      push_batched_kernel<1, false><<<g, kWarps * 32, 0, st>>>(c, (int)b, lm);
     }
     note_launch();
     PL_CUDA(cudaGetLastError());
