@@ -50,61 +50,79 @@ int64_t grid_for(int64_t work_items, int per_block, int waves = 8) {
 // index advances), so consecutive tokens of a warp share a block; the parity expansion of
 // a 4096-B cell is unrolled with constant store offsets (tools/k1_probe.cu: 2.74 -> 2.49 ms
 // for the 17 GB of the bench step).
-__global__ void __launch_bounds__(kWarps * 32) kv_write_kernel(WriteLaunch w) {
+__device__ __forceinline__ void k1_write_cell(const WriteLaunch& w, int64_t t, int j, uint64_t fp,
+                                              uint8_t* unit, int off, int lane,
+                                              int64_t vec_per_cell) {
+  int4* cell = reinterpret_cast<int4*>(unit + w.fp_bytes + ((int64_t)j * w.s + off) * w.cell_bytes);
+  if (w.kv) {
+    const int4* src = reinterpret_cast<const int4*>(w.kv + (t * w.k + j) * w.cell_bytes);
+    for (int64_t v = lane; v < vec_per_cell; v += 32) st_stream(cell + v, ld_stream(src + v));
+  } else if (vec_per_cell == 256) {
+    // word 2v(+1) of layer j, v = lane + 32u: fp ^ (j << 32 | w) with w = 2 lane + 64 u
+    // (disjoint bits, so OR == XOR), and w + 1 flips bit 0
+    const uint64_t x0 = fp ^ ((uint64_t)j << 32) ^ (uint32_t)(2 * lane);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint64_t xa = x0 ^ (uint32_t)(64 * u);
+      const uint64_t a = splitmix64(xa), b = splitmix64(xa ^ 1u);
+      int4 val;
+      val.x = (int)(uint32_t)a; val.y = (int)(uint32_t)(a >> 32);
+      val.z = (int)(uint32_t)b; val.w = (int)(uint32_t)(b >> 32);
+      st_stream(cell + lane + 32 * u, val);
+    }
+  } else {
+    for (int64_t v = lane; v < vec_per_cell; v += 32) {
+      uint64_t a = expand_word(fp, (uint32_t)j, (uint32_t)(2 * v));
+      uint64_t b = expand_word(fp, (uint32_t)j, (uint32_t)(2 * v + 1));
+      int4 val;
+      val.x = (int)(uint32_t)a; val.y = (int)(uint32_t)(a >> 32);
+      val.z = (int)(uint32_t)b; val.w = (int)(uint32_t)(b >> 32);
+      st_stream(cell + v, val);
+    }
+  }
+}
+
+// `layer_major`: the warp writes its run of tokens one layer at a time (neighbouring
+// tokens of a block are neighbouring cells of a layer: one contiguous stream per layer)
+// instead of a token's k layers at a time; the header word goes with the first layer and
+// the dirty mark with the last, so a token is marked only once all its cells are written.
+__global__ void __launch_bounds__(kWarps * 32) kv_write_kernel(WriteLaunch w, int layer_major) {
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t vec_per_cell = w.cell_bytes >> 4;
   const int64_t per = (w.total + nwarps - 1) / nwarps;
+  const int64_t t_begin = warp0 * per;
   const int64_t t_end = min(w.total, (warp0 + 1) * per);
-  int it = warp0 * per < w.total ? find_item(w.offs, w.n_items, warp0 * per) : 0;
-  for (int64_t t = warp0 * per; t < t_end; ++t) {
-    while (it + 1 < w.n_items && w.offs[it + 1] <= t) ++it;
-    const int32_t req = w.reqs[it];
-    const int32_t g = w.groups[it];
-    const int64_t pos = w.positions ? w.positions[t] : w.starts[it] + (t - w.offs[it]);
-    const uint64_t fp = w.mode == PL_PAYLOAD_SEED
-                            ? cell_fingerprint(w.seeds[it], (uint64_t)(w.fp_starts[it] + (t - w.offs[it])))
-                            : w.payloads[t];
-    const int32_t slot = w.table[(int64_t)req * w.max_chain + pos / w.s];
-    if (slot < 0) continue;  // host guarantees the chain covers pos
-    const int off = (int)(pos % w.s);
-    uint8_t* unit = reinterpret_cast<uint8_t*>(w.group_bases[g]) + (int64_t)slot * w.unit_bytes;
-    if (lane == 0) reinterpret_cast<uint64_t*>(unit)[off] = fp;
-    for (int j = 0; j < w.k; ++j) {
-      int4* cell = reinterpret_cast<int4*>(unit + w.fp_bytes + ((int64_t)j * w.s + off) * w.cell_bytes);
-      if (w.kv) {
-        const int4* src = reinterpret_cast<const int4*>(w.kv + (t * w.k + j) * w.cell_bytes);
-        for (int64_t v = lane; v < vec_per_cell; v += 32) st_stream(cell + v, ld_stream(src + v));
-      } else if (vec_per_cell == 256) {
-        // word 2v(+1) of layer j, v = lane + 32u: fp ^ (j << 32 | w) with w = 2 lane + 64 u
-        // (disjoint bits, so OR == XOR), and w + 1 flips bit 0
-        const uint64_t x0 = fp ^ ((uint64_t)j << 32) ^ (uint32_t)(2 * lane);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint64_t xa = x0 ^ (uint32_t)(64 * u);
-          const uint64_t a = splitmix64(xa), b = splitmix64(xa ^ 1u);
-          int4 val;
-          val.x = (int)(uint32_t)a; val.y = (int)(uint32_t)(a >> 32);
-          val.z = (int)(uint32_t)b; val.w = (int)(uint32_t)(b >> 32);
-          st_stream(cell + lane + 32 * u, val);
-        }
+  if (t_begin >= t_end) return;
+  const int it0 = find_item(w.offs, w.n_items, t_begin);
+  const int passes = layer_major ? w.k : 1;
+  for (int pass = 0; pass < passes; ++pass) {
+    int it = it0;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      while (it + 1 < w.n_items && w.offs[it + 1] <= t) ++it;
+      const int32_t req = w.reqs[it];
+      const int32_t g = w.groups[it];
+      const int64_t pos = w.positions ? w.positions[t] : w.starts[it] + (t - w.offs[it]);
+      const uint64_t fp = w.mode == PL_PAYLOAD_SEED
+                              ? cell_fingerprint(w.seeds[it], (uint64_t)(w.fp_starts[it] + (t - w.offs[it])))
+                              : w.payloads[t];
+      const int32_t slot = w.table[(int64_t)req * w.max_chain + pos / w.s];
+      if (slot < 0) continue;  // host guarantees the chain covers pos
+      const int off = (int)(pos % w.s);
+      uint8_t* unit = reinterpret_cast<uint8_t*>(w.group_bases[g]) + (int64_t)slot * w.unit_bytes;
+      if (pass == 0 && lane == 0) reinterpret_cast<uint64_t*>(unit)[off] = fp;
+      if (layer_major) {
+        k1_write_cell(w, t, pass, fp, unit, off, lane, vec_per_cell);
       } else {
-        for (int64_t v = lane; v < vec_per_cell; v += 32) {
-          uint64_t a = expand_word(fp, (uint32_t)j, (uint32_t)(2 * v));
-          uint64_t b = expand_word(fp, (uint32_t)j, (uint32_t)(2 * v + 1));
-          int4 val;
-          val.x = (int)(uint32_t)a; val.y = (int)(uint32_t)(a >> 32);
-          val.z = (int)(uint32_t)b; val.w = (int)(uint32_t)(b >> 32);
-          st_stream(cell + v, val);
-        }
+        for (int j = 0; j < w.k; ++j) k1_write_cell(w, t, j, fp, unit, off, lane, vec_per_cell);
       }
-    }
-    if (lane < w.n_marks) {
-      const int lg = w.local_of[lane][g];
-      if (lg >= 0) {
-        const int64_t bit = ((int64_t)slot * w.G[lane] + lg) * w.s + off;
-        atomicOr(w.bits[lane] + (bit >> 5), 1u << (bit & 31));
+      if (pass == passes - 1 && lane < w.n_marks) {
+        const int lg = w.local_of[lane][g];
+        if (lg >= 0) {
+          const int64_t bit = ((int64_t)slot * w.G[lane] + lg) * w.s + off;
+          atomicOr(w.bits[lane] + (bit >> 5), 1u << (bit & 31));
+        }
       }
     }
   }
@@ -113,8 +131,14 @@ __global__ void __launch_bounds__(kWarps * 32) kv_write_kernel(WriteLaunch w) {
 void launch_kv_write(const WriteLaunch& w, cudaStream_t st) {
   if (w.total <= 0) return;
   int64_t grid = grid_for(w.total, kWarps, 16);
+  // PL_K1_LAYER_MAJOR=1 (A/B): layer-major writes within a warp's run -- measured slower
+  // for the write-only expansion (2.91 vs 2.74 ms for the 17 GB step), so token-major stays
+  static const int lm = [] {
+    const char* v = std::getenv("PL_K1_LAYER_MAJOR");
+    return v ? std::atoi(v) : 0;
+  }();
   KernelTimer timer("kv_write", st);
-  kv_write_kernel<<<(unsigned)grid, kWarps * 32, 0, st>>>(w);
+  kv_write_kernel<<<(unsigned)grid, kWarps * 32, 0, st>>>(w, lm);
   note_launch();
   PL_CUDA(cudaGetLastError());
 }
