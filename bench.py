@@ -840,10 +840,15 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
     recv_store = ring.dst if ring is not None else rig.dst
     sender = ring.tx.patch if ring is not None else rig.patch
 
+    phases = []   # host ms per step: free, append (H2D + K1), push, D2H enqueue
+
     def one_step(i):
+        p0 = time.perf_counter()
         rig.src.free_requests(names)   # the previous step's requests leave both stages
         recv_store.free_requests(names)
+        p1 = time.perf_counter()
         assert append_batch_payloads(rig.src, reqs, groups, counts, host, mark=True) == len(reqs)
+        p2 = time.perf_counter()
         if ring is None:
             keys, _ = rig.patch.push(rig.dst, rig.registry.rank())
         else:
@@ -851,10 +856,12 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
             ring.rx.serve_rows()
             keys, _ = ring.tx.finish()
             ring.rx.serve_ack()
+        p3 = time.perf_counter()
         # D2H of the step's result (drained-key count), enqueued behind the push; the host
         # goes on preparing the next step while the device works (a pipelined driver)
         N.check(N.lib().pl_patch_device_drained_async(
             sender.h, C.c_void_p(results.data_ptr() + 8 * i)))
+        phases.append((p1 - p0, p2 - p1, p3 - p2, time.perf_counter() - p3))
         return keys
 
     import ctypes as C
@@ -872,9 +879,14 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
     try:
         one_step(K)
         torch.cuda.synchronize()
+        # a host sync point after the warm-up: staging rings it outgrew are freed here
+        rig.src.sync()
+        recv_store.sync()
         # no cyclic-GC pass inside the wall-clock region (earlier legs leave many objects)
         gc.collect()
         gc.disable()
+        phases.clear()
+        st0 = [st.staging_stats() for st in (rig.src, recv_store)]
         t0 = time.perf_counter()
         marks = []
         for i in range(K):
@@ -883,6 +895,7 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
         stream.synchronize()
         torch.cuda.synchronize()
         sec = time.perf_counter() - t0
+        st1 = [st.staging_stats() for st in (rig.src, recv_store)]
     finally:
         gc.enable()
         if ring is not None:
@@ -898,6 +911,15 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
             # host time between consecutive step calls returning (the device runs ahead or
             # behind; a stall anywhere in the loop shows up here as one long step)
             "host_step_ms_max": round(max(b - a for a, b in zip([t0] + marks, marks)) * 1e3, 3),
+            # the slowest step's host phases: free, append (H2D + K1 enqueue), push, D2H
+            "host_step_phases_ms": dict(zip(("free", "append", "push", "d2h"), (
+                round(x * 1e3, 3) for x in max(phases, key=sum)))),
+            # H2D staging rings of the sending / receiving store over the timed steps
+            "staging": {name: {"ring_mb": round(b["ring_bytes"] / 2**20, 1),
+                               "outgrows": b["outgrows"] - a["outgrows"],
+                               "retire_waits": b["retire_waits"] - a["retire_waits"],
+                               "wait_ms": round((b["wait_ns"] - a["wait_ns"]) / 1e6, 3)}
+                        for name, a, b in zip(("src", "dst"), st0, st1)},
             "path": "host payload fingerprints -> pl_store_append_batch_payloads (K1 expand + "
                     "mark) -> pl_patch_push (K3 + fused K4/K5) -> D2H drained count "
                     "(pipelined: step i+1 is prepared on the host while step i runs)"

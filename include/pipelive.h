@@ -187,6 +187,11 @@ int pl_store_last_resize_stats(pl_store* st, int64_t* out4);
  * the store was created, and physical bytes not yet back with the driver.  reclaim
  * forces every pending unmap + release now (blocking), returns the wait in ms. */
 int pl_store_vmm_stats(pl_store* st, int64_t* out4);
+/* H2D staging ring of the store's uploads (no reference counterpart: host-side plumbing
+ * of this data plane): out6 = {ring capacity bytes, ring growths, spans retired with a
+ * host wait, host ns spent acquiring spans in total, the longest single acquisition (ns),
+ * outgrown rings not yet freed (freed at pl_store_sync)}. */
+int pl_store_staging_stats(pl_store* st, int64_t* out6);
 /* ahead of a planned resize(new_capacity) with `groups` resident afterwards (e.g. the
  * post-commit b_new, coordinator.py:340-354, known once the target is chosen): create the
  * physical chunks the grow will need on the reclaimer thread now, beyond the cached ones

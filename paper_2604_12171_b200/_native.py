@@ -122,6 +122,7 @@ SIGNATURES = [
     ("pl_store_utilization", C.c_int, [vp, P(dbl)]),
     ("pl_store_last_resize_stats", C.c_int, [vp, vp]),
     ("pl_store_vmm_stats", C.c_int, [vp, vp]),
+    ("pl_store_staging_stats", C.c_int, [vp, vp]),
     ("pl_store_reclaim", C.c_int, [vp, P(dbl)]),
     ("pl_store_prepare_grow", C.c_int, [vp, i64, vp, C.c_int, P(i64)]),
     ("pl_store_prepare_wait", C.c_int, [vp, P(dbl)]),

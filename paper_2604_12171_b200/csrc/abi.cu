@@ -705,6 +705,17 @@ int pl_store_vmm_stats(pl_store* st, int64_t* out4) {
     out4[3] = s->reclaimer->pending();
   });
 }
+int pl_store_staging_stats(pl_store* st, int64_t* out6) {
+  return guard([&] {
+    pl::Store* s = st->s;
+    out6[0] = s->ring ? (int64_t)s->ring->cap : 0;
+    out6[1] = s->stage_outgrows;
+    out6[2] = s->stage_retire_waits;
+    out6[3] = s->stage_wait_ns;
+    out6[4] = s->stage_span_max_ns;
+    out6[5] = (int64_t)s->old_rings.size();
+  });
+}
 int pl_store_prepare_grow(pl_store* st, int64_t new_capacity, const int32_t* groups, int n,
                           int64_t* chunks_requested) {
   return guard([&] {
@@ -747,6 +758,7 @@ int pl_store_sync(pl_store* st) {
     // deltas are only queued by the caller's thread (the worker never adds any)
     st->s->flush();
     PL_CUDA(cudaStreamSynchronize(st->s->stream));
+    if (!st->s->old_rings.empty()) st->s->release_old_rings();
   });
 }
 

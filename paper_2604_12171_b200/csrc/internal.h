@@ -339,6 +339,10 @@ struct Store {
   std::deque<PinnedSpan> ring_live;
   std::vector<cudaEvent_t> ring_events;  // idle events
   cudaStream_t up_stream = nullptr;
+  void release_old_rings();  // outgrown rings without live spans (synchronises the device)
+  // staging counters (pl_store_staging_stats): ring growths, spans retired with a host
+  // wait, and the host time those took (ns; the longest single stage_span call too)
+  int64_t stage_outgrows = 0, stage_retire_waits = 0, stage_wait_ns = 0, stage_span_max_ns = 0;
 
   std::vector<Patch*> patches;  // patches whose source is this store
   uint64_t* d_bases_ = nullptr;  // device copy of the per-group arena bases

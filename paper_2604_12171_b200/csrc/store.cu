@@ -350,11 +350,14 @@ cudaEvent_t Store::ring_event() {
 
 void Store::stage_span(size_t bytes, uint8_t** h, uint8_t** d, uint64_t* seq) {
   const size_t n = round_up((int64_t)std::max<size_t>(bytes, 1), 256);
+  const auto t_in = std::chrono::steady_clock::now();
   if (!up_stream) PL_CUDA(cudaStreamCreateWithFlags(&up_stream, cudaStreamNonBlocking));
   // the oldest span leaves: its host bytes once its copy ran, its device bytes once its
   // consumers ran (a device-side wait of the copy stream, no host block)
   auto retire_front = [&] {
     PinnedSpan& sp = ring_live.front();
+    if (cudaEventQuery(sp.ev_h2d) == cudaErrorNotReady) ++stage_retire_waits;
+    cudaGetLastError();
     PL_CUDA(cudaEventSynchronize(sp.ev_h2d));
     PL_CUDA(cudaStreamWaitEvent(up_stream, sp.ev_used, 0));
     ring_events.push_back(sp.ev_h2d);
@@ -365,6 +368,7 @@ void Store::stage_span(size_t bytes, uint8_t** h, uint8_t** d, uint64_t* seq) {
     // spans in the old ring stay valid (an Upload may still be in scope); the old ring is
     // freed once none of its spans is live
     if (ring) old_rings.push_back(std::move(ring));
+    ++stage_outgrows;
     ring = std::make_unique<StagingRing>();
     ring->cap = cap;
     PL_CUDA(cudaMallocHost(&ring->h, cap));
@@ -395,6 +399,34 @@ void Store::stage_span(size_t bytes, uint8_t** h, uint8_t** d, uint64_t* seq) {
     }
     retire_front();
   }
+  // outgrown rings wait for a host sync point (release_old_rings from pl_store_sync):
+  // cudaFree / cudaFreeHost synchronise the device, a stall of the whole queue if done
+  // inside an upload.  Only a pile-up of them (bounded memory) is freed here.
+  if (old_rings.size() > 3) release_old_rings();
+  ring_head = b;
+  *h = ring->h + a;
+  *d = ring->d + a;
+  *seq = ++ring_seq;
+  ring_live.push_back({a, b, *seq, ring.get(), nullptr, nullptr});
+  const int64_t ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                         std::chrono::steady_clock::now() - t_in).count();
+  stage_wait_ns += ns;
+  stage_span_max_ns = std::max(stage_span_max_ns, ns);
+}
+void Store::release_old_rings() {
+  // spans of outgrown rings whose copy and consumers have run leave first
+  for (auto it = ring_live.begin(); it != ring_live.end();) {
+    const bool old = it->ring != ring.get();
+    if (!old || !it->ev_used || cudaEventQuery(it->ev_h2d) != cudaSuccess ||
+        cudaEventQuery(it->ev_used) != cudaSuccess) {
+      cudaGetLastError();
+      ++it;
+      continue;
+    }
+    ring_events.push_back(it->ev_h2d);
+    if (it->ev_used != it->ev_h2d) ring_events.push_back(it->ev_used);
+    it = ring_live.erase(it);
+  }
   // free outgrown rings with no live span left
   for (size_t i = 0; i < old_rings.size();) {
     bool live = false;
@@ -405,11 +437,6 @@ void Store::stage_span(size_t bytes, uint8_t** h, uint8_t** d, uint64_t* seq) {
     cudaFree(old_rings[i]->d);
     old_rings.erase(old_rings.begin() + (long)i);
   }
-  ring_head = b;
-  *h = ring->h + a;
-  *d = ring->d + a;
-  *seq = ++ring_seq;
-  ring_live.push_back({a, b, *seq, ring.get(), nullptr, nullptr});
 }
 void Store::stage_reserve(size_t cap) {
   if (ring && ring->cap >= cap) return;

@@ -639,6 +639,15 @@ class KvStore:
         return {"tail_reused_chunks": int(out[0]), "cache_reused_chunks": int(out[1]),
                 "created_chunks": int(out[2]), "pending_reclaim_bytes": int(out[3])}
 
+    def staging_stats(self) -> dict[str, int]:
+        """The H2D staging ring behind every upload (store.cu stage_span): capacity, growths,
+        spans retired with a host wait, host ns spent acquiring spans (total, longest),
+        outgrown rings not yet freed (they are freed at sync(), a host sync point)."""
+        out = np.zeros(6, dtype=np.int64)
+        _check(N.lib().pl_store_staging_stats(self._h, N.ptr(out)))
+        return dict(zip(("ring_bytes", "outgrows", "retire_waits", "wait_ns", "span_max_ns",
+                         "old_rings"), (int(x) for x in out)))
+
     def prepare_grow(self, new_capacity: int, groups: Iterable[int]) -> int:
         """Create, on the reclaimer thread, the physical chunks a planned
         resize(new_capacity) with `groups` resident will need; returns chunks requested."""

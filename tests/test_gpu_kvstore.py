@@ -359,3 +359,35 @@ class TestLazyGroupAdoption:
         for (r, g), v in keep.items():
             assert st.read_cell(r, g, 3, 0) == v
         torch.cuda.synchronize()
+
+
+def test_upload_ring_outgrows_without_a_host_sync_and_frees_at_sync():
+    """Uploads larger than a quarter of the H2D staging ring take a larger ring; the
+    outgrown ones are freed at the next sync() (a host sync point), not inside an upload
+    (cudaFree / cudaFreeHost would stall the device queue there), and every payload
+    staged through the old and new rings lands in its cells."""
+    from paper_2604_12171_b200 import kvstore as kv
+    from paper_2604_12171_b200.events import stable_hash
+    from paper_2604_12171_b200.perf import append_batch_payloads, engine_payloads
+
+    reg = kv.RequestRegistry()
+    st = kv.KvStore(1, 2, 16, 16384, (0, 1), cell_bytes=64, registry=reg)
+    s0 = st.staging_stats()
+    seeds = {}
+    for j, (n_req, n_tok) in enumerate(((16, 512), (64, 512), (64, 1024))):
+        names = [f"u{j}_{i}" for i in range(n_req)]
+        reqs = [reg.handle(r) for r in names for _ in (0, 1)]
+        groups = [g for _ in names for g in (0, 1)]
+        pls = []
+        for r in names:
+            for g in (0, 1):
+                seeds[(r, g)] = stable_hash(r, g)
+                pls.append(engine_payloads(seeds[(r, g)], n_tok))
+        assert append_batch_payloads(st, reqs, groups, [n_tok] * len(reqs),
+                                     np.concatenate(pls)) == len(reqs)
+    s1 = st.staging_stats()
+    assert s1["outgrows"] - s0["outgrows"] >= 2 and s1["old_rings"] >= 1, (s0, s1)
+    st.sync()
+    assert st.staging_stats()["old_rings"] == 0
+    out = st.verify_cells(seeds)
+    assert out["cells"] > 0 and out["bad_bytes"] == 0 and out["bad_fingerprints"] == 0, out
