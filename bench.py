@@ -440,6 +440,12 @@ def main() -> None:
     e2e = e2e_kv = None
     if not args.skip_e2e:
         e2e = guarded("e2e", lambda: measure_e2e_api(rig, stream, torch, wl, K, world, ring))
+        if e2e and "ms_per_step" in e2e:
+            # the step's device work is three passes over the payload: K1 writes the cells,
+            # the push reads and writes them -- the HBM bound of the whole e2e step
+            e2e["hbm_bytes_per_step"] = 3 * wl.payload_bytes
+            e2e["hbm_bound_ms"] = round(3 * wl.payload_bytes / (hbm_peak * 1e9) * 1e3, 3)
+            e2e["hbm_frac"] = round(e2e["hbm_bound_ms"] / e2e["ms_per_step"], 4)
     if ring is not None:
         ring.close()
     if not args.skip_e2e:

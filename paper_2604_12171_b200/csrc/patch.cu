@@ -938,7 +938,6 @@ void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask, cuda
   cudaStream_t ps = pstream();
   uint32_t* old = d_bits;  // epoch flip, as device_drain_compact
   std::swap(d_bits, d_bits_alt);
-  if (snap_recorded && ps != src->stream) PL_CUDA(cudaStreamWaitEvent(src->stream, snap_ev, 0));
   if (ps != src->stream) {
     PL_CUDA(cudaEventRecord(ev_src, src->stream));
     PL_CUDA(cudaStreamWaitEvent(ps, ev_src, 0));
@@ -949,6 +948,10 @@ void Patch::device_drain_push(Store* dst, const std::vector<uint8_t>* mask, cuda
   cnt_cur ^= 1;
   d_count = d_cnt + cnt_cur;
   launch_drain_push(push_launch(dst, d_apply, 0), old, n_words, d_count, d_cnt + (cnt_cur ^ 1), ps);
+  // marks into the new epoch's buffer (the previous round's snapshot) wait for that
+  // snapshot; enqueued after the launch (it only orders later source-stream work) and
+  // before ev_applied is re-recorded below (snap_ev is that event)
+  if (snap_recorded && ps != src->stream) PL_CUDA(cudaStreamWaitEvent(src->stream, snap_ev, 0));
   // the snapshot and the copy end together in this kernel: one event marks both (a later
   // re-record of ev_applied only ever moves it past this point)
   PL_CUDA(cudaEventRecord(ev_applied, ps));
