@@ -847,13 +847,20 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
     sender = ring.tx.patch if ring is not None else rig.patch
 
     phases = []   # host ms per step: free, append (H2D + K1), push, D2H enqueue
+    # the receiving stage's host work runs on its own thread, as it would in its own
+    # process on its own GPU (ctypes drops the GIL for the call; the two stores share no
+    # host state); joined before the push, which reserves on the receiver
+    from concurrent.futures import ThreadPoolExecutor
+    receiver = ThreadPoolExecutor(max_workers=1)
 
     def one_step(i):
         p0 = time.perf_counter()
-        rig.src.free_requests(names)   # the previous step's requests leave both stages
-        recv_store.free_requests(names)
+        # the previous step's requests leave both stages
+        recv_free = receiver.submit(recv_store.free_requests, names)
+        rig.src.free_requests(names)
         p1 = time.perf_counter()
         assert append_batch_payloads(rig.src, reqs, groups, counts, host, mark=True) == len(reqs)
+        recv_free.result()
         p2 = time.perf_counter()
         if ring is None:
             keys, _ = rig.patch.push(rig.dst, rig.registry.rank())
@@ -902,8 +909,10 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
         torch.cuda.synchronize()
         sec = time.perf_counter() - t0
         st1 = [st.staging_stats() for st in (rig.src, recv_store)]
+        last_push = sender.last_push_stats() if hasattr(sender, "last_push_stats") else None
     finally:
         gc.enable()
+        receiver.shutdown()
         if ring is not None:
             N.check(N.lib().pl_patch_set_active(rig.patch.h, 1))
     sec = allmax(sec, world)
@@ -920,6 +929,9 @@ def measure_e2e_api(rig, stream, torch, wl, K, world, ring=None) -> dict:
             # the slowest step's host phases: free, append (H2D + K1 enqueue), push, D2H
             "host_step_phases_ms": dict(zip(("free", "append", "push", "d2h"), (
                 round(x * 1e3, 3) for x in max(phases, key=sum)))),
+            # the last step's push, host phases (ms): snapshot, receiver reservation, table
+            # flush, K3 / copy enqueue (pl_patch_last_push_stats)
+            "last_push_phases_ms": last_push,
             # H2D staging rings of the sending / receiving store over the timed steps
             "staging": {name: {"ring_mb": round(b["ring_bytes"] / 2**20, 1),
                                "outgrows": b["outgrows"] - a["outgrows"],

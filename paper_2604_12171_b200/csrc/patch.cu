@@ -641,16 +641,23 @@ void Patch::push_chunked(Store* dst, const int32_t* rank, int64_t n_rank) {
   std::vector<int64_t> run_keys;
   {
     const bool forced = std::getenv("PL_PUSH_CHUNK_MIN_BLOCKS") != nullptr;
+    // PL_PUSH_RUN_GROW=1: after the first run each run may double (the host reserves
+    // about twice as fast as the copy consumes, so run c + 1 is reserved while run c
+    // copies): fewer launches and flushes for the same head start
+    static const bool grow = [] {
+      const char* v = std::getenv("PL_PUSH_RUN_GROW");
+      return v && std::atoi(v) != 0;
+    }();
     const int64_t target = std::max<int64_t>(drained_keys / 8, forced ? 1 : 1 << 16);
     const int64_t first = std::max<int64_t>(target / 4, forced ? 1 : 1 << 12);
-    int64_t acc = 0;
+    int64_t acc = 0, want = first;
     for (size_t x = 0; x < order.size(); ++x) {
       for (const Interval& r : std::get<2>(drained[order[x]])) acc += r.b - r.a;
-      if ((acc >= (cut.size() == 1 ? first : target) && cut.size() < 254) ||
-          x + 1 == order.size()) {
+      if ((acc >= want && cut.size() < 254) || x + 1 == order.size()) {
         cut.push_back(x + 1);
         run_keys.push_back(acc);
         acc = 0;
+        want = grow ? 2 * run_keys.back() : target;
       }
     }
   }
