@@ -13,6 +13,7 @@
 #include <cstring>
 
 #include <limits>
+#include <thread>
 
 #include "internal.h"
 
@@ -486,12 +487,37 @@ int Upload::add(const void* p, size_t bytes) {
   total += (bytes + 255) / 256 * 256;
   return (int)parts.size() - 1;
 }
+// a large part (a bulk append's payloads: 8 MB for configs[1]) is copied into the pinned
+// ring by a few threads -- one core's memcpy into pinned memory is ~1 ms of host time per
+// step there, most of the e2e loop's margin over the device
+static void copy_part(uint8_t* dst, const void* src, size_t n) {
+  constexpr size_t kSplitMin = 4u << 20, kPiece = 2u << 20;
+  if (n < kSplitMin) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  const size_t n_threads = std::min<size_t>(4, n / kPiece);
+  const size_t per = (n / n_threads + 4095) & ~(size_t)4095;
+  std::thread helpers[3];
+  for (size_t t = 1; t < n_threads; ++t) {
+    const size_t a = t * per;
+    if (a >= n) break;
+    const size_t len = std::min(per, n - a);
+    helpers[t - 1] = std::thread([=] {
+      std::memcpy(dst + a, static_cast<const uint8_t*>(src) + a, len);
+    });
+  }
+  std::memcpy(dst, src, std::min(per, n));
+  for (auto& th : helpers)
+    if (th.joinable()) th.join();
+}
+
 void Upload::go(size_t extra_device_bytes) {
   uint8_t* h = nullptr;
   st->stage_span(std::max<size_t>(total, 256), &h, &dev, &seq);
   staged = true;
   for (size_t i = 0; i < parts.size(); ++i)
-    if (parts[i].second) std::memcpy(h + offs[i], parts[i].first, parts[i].second);
+    if (parts[i].second) copy_part(h + offs[i], parts[i].first, parts[i].second);
   if (total) PL_CUDA(cudaMemcpyAsync(dev, h, total, cudaMemcpyHostToDevice, st->up_stream));
   st->stage_commit(seq);
   if (extra_device_bytes) dev_extra = static_cast<uint8_t*>(st->scratch(extra_device_bytes + 256));
