@@ -17,7 +17,12 @@
 //                source SMs; no staging buffer, no communicator.
 // Only the interval rows and a reply cross the control channel (a few KB per round).
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <system_error>
 #include <thread>
 
 #include "internal.h"
@@ -48,18 +53,47 @@ Remote::~Remote() {
 // releases the imported chunks, closes the table handle and frees the view.  The caller
 // (the sender's post-commit cleanup, coordinator.py:340-354) neither synchronises its
 // stream nor waits for the driver's TLB-flushing unmaps.
+// Teardowns still running when the process exits are waited for by an atexit handler
+// registered at the first call -- after the CUDA runtime's own, so it runs before the
+// runtime is torn down (a detached thread unmapping into a destroyed context would not).
+namespace {
+std::mutex g_teardown_mu;
+std::condition_variable g_teardown_cv;
+int g_teardowns = 0;
+void wait_remote_teardowns() {
+  std::unique_lock<std::mutex> lk(g_teardown_mu);
+  g_teardown_cv.wait_for(lk, std::chrono::seconds(30), [] { return g_teardowns == 0; });
+}
+}  // namespace
+
 void remote_destroy_after(Remote* r, cudaStream_t st) {
+  static std::once_flag at_exit;
+  std::call_once(at_exit, [] { std::atexit(wait_remote_teardowns); });
   cudaEvent_t ev = nullptr;
   PL_CUDA(cudaSetDevice(r->device));
   PL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   PL_CUDA(cudaEventRecord(ev, st));
-  std::thread([r, ev] {
+  {
+    std::lock_guard<std::mutex> lk(g_teardown_mu);
+    ++g_teardowns;
+  }
+  auto teardown = [r, ev] {
     cudaSetDevice(r->device);
     cudaEventSynchronize(ev);
     cudaEventDestroy(ev);
     r->detached = true;  // ~Remote: no device-wide synchronisation (the event covered it)
     delete r;
-  }).detach();
+    {
+      std::lock_guard<std::mutex> lk(g_teardown_mu);
+      --g_teardowns;
+    }
+    g_teardown_cv.notify_all();
+  };
+  try {
+    std::thread(teardown).detach();
+  } catch (const std::system_error&) {
+    teardown();  // no thread available: tear down on the caller
+  }
 }
 
 void Remote::drop_group(int g, bool reset_base) {

@@ -391,3 +391,26 @@ def test_upload_ring_outgrows_without_a_host_sync_and_frees_at_sync():
     assert st.staging_stats()["old_rings"] == 0
     out = st.verify_cells(seeds)
     assert out["cells"] > 0 and out["bad_bytes"] == 0 and out["bad_fingerprints"] == 0, out
+
+
+def test_large_payload_upload_is_copied_exactly():
+    """A bulk append's payload upload (8 MB here, configs[1]'s shape: 256 requests x 2
+    groups x 2048 tokens) is copied into the pinned staging ring by several threads
+    (store.cu copy_part); every fingerprint must land in its cell."""
+    from paper_2604_12171_b200 import kvstore as kv
+    from paper_2604_12171_b200.events import stable_hash
+    from paper_2604_12171_b200.perf import append_batch_payloads, engine_payloads
+
+    reg = kv.RequestRegistry()
+    st = kv.KvStore(1, 2, 16, 33000, (0, 1), cell_bytes=64, registry=reg)
+    names = [f"big{i}" for i in range(256)]
+    reqs = [reg.handle(r) for r in names for _ in (0, 1)]
+    groups = [g for _ in names for g in (0, 1)]
+    seeds = {(r, g): stable_hash(r, g) for r in names for g in (0, 1)}
+    pls = np.concatenate([engine_payloads(seeds[(r, g)], 2048) for r in names for g in (0, 1)])
+    assert pls.nbytes >= 8 << 20
+    assert append_batch_payloads(st, reqs, groups, [2048] * len(reqs), pls) == len(reqs)
+    st.sync()
+    out = st.verify_cells(seeds)
+    assert out["cells"] == 256 * 2 * 2048, out   # (position, group) pairs, k layers each
+    assert out["bad_bytes"] == 0 and out["bad_fingerprints"] == 0, out
