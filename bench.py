@@ -307,8 +307,21 @@ def main() -> None:
 
     # ---- C3 first, on a clean GPU: 70B-shape stage with HBM pre-filled by KV (~160 GB
     # peak), live shrink with K6 relocation, patch of the leaving groups, drop, grow
+    shared_gpu = world > max(torch.cuda.device_count(), 1) and not args.only_step
+    if shared_gpu:
+        # ranks sharing a GPU (a one-GPU box under torchrun): the legs sized for a whole
+        # GPU's HBM (configs[2]'s 160 GB pre-fill, the 8B-shape decoders) cannot fit N times
+        # over, so the line is the bulk round and the e2e round (the ring's), as
+        # `--only-step` plus e2e
+        args.only_step = True
+        if rank == 0:
+            print(f"[bench] {world} ranks on {torch.cuda.device_count()} GPU(s): bulk round "
+                  "+ e2e only", file=sys.stderr)
     if args.only_step:
+        skip_e2e = args.skip_e2e
         args.skip_c3 = args.skip_c2 = args.skip_sweep = args.skip_e2e = args.skip_cpu = True
+        if shared_gpu:
+            args.skip_e2e = skip_e2e
     c3 = None
     if not args.skip_c3 and rank == 0:
         from paper_2604_12171_b200.perf import c3_live_resize
@@ -443,12 +456,14 @@ def main() -> None:
         if e2e and "ms_per_step" in e2e:
             # the step's device work is three passes over the payload: K1 writes the cells,
             # the push reads and writes them -- the HBM bound of the whole e2e step
-            e2e["hbm_bytes_per_step"] = 3 * wl.payload_bytes
-            e2e["hbm_bound_ms"] = round(3 * wl.payload_bytes / (hbm_peak * 1e9) * 1e3, 3)
+            # (ranks sharing one GPU share its HBM: their bytes add up on it)
+            per_gpu = world // max(torch.cuda.device_count(), 1) if shared_gpu else 1
+            e2e["hbm_bytes_per_step"] = 3 * wl.payload_bytes * per_gpu
+            e2e["hbm_bound_ms"] = round(3 * wl.payload_bytes * per_gpu / (hbm_peak * 1e9) * 1e3, 3)
             e2e["hbm_frac"] = round(e2e["hbm_bound_ms"] / e2e["ms_per_step"], 4)
     if ring is not None:
         ring.close()
-    if not args.skip_e2e:
+    if not args.skip_e2e and not shared_gpu:
         # a heavier variant: the real 17 GB of KV bytes stream from pinned host memory
         e2e_kv = guarded("e2e_real_kv", lambda: measure_e2e(rig, stream, torch, wl, K, world))
     rig.destroy()
