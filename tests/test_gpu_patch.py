@@ -377,3 +377,81 @@ def test_concurrent_pairs_on_separate_streams():
                 pos = rng.randrange(wl.ctx + (3 if g == wl.mig_groups[0] else 0))
                 assert rig.dst.read_cell(rid(i), g, pos, 1) == rig.src.read_cell(rid(i), g, pos, 1)
         rig.destroy()
+
+
+@pytest.mark.parametrize("side_stream", [False, True])
+def test_perf_push_edge_rounds(side_stream):
+    """The perf push (pl_patch_push) through the round shapes a live migration meets, each
+    checked byte for byte against the source (every written position, fingerprint + k
+    cells, through both block tables): ragged request lengths (1 .. 2 blocks + 1) in the
+    bulk round; an empty round; a launch-first steady round (every position inside an
+    existing destination block); a round that needs new destination blocks; a round in
+    which a request finished after its writes were marked (discarded, not shipped)."""
+    import torch
+
+    from paper_2604_12171_b200 import kvstore
+    from paper_2604_12171_b200.perf import NativePatch, append_batch
+
+    reg = kvstore.RequestRegistry()
+    k, s = 2, 16
+    src = kvstore.KvStore(1, k, s, 512, (0, 1, 2), num_groups=3, cell_bytes=4096, registry=reg)
+    dst = kvstore.KvStore(2, k, s, 512, (2,), num_groups=3, cell_bytes=4096, registry=reg)
+    dst.resident_groups |= {0, 1}
+    lens = [1, 15, 16, 17, 31, 32, 33, 5]
+    names = [f"e{i}" for i in range(len(lens))]
+    hs = [reg.handle(n) for n in names]
+    seeds = {(n, g): opgen.stable_hash(n, g) for n in names for g in (0, 1, 2)}
+
+    def append(which, counts, mark):
+        reqs = [hs[i] for i in which for _ in (0, 1, 2)]
+        groups = [g for _ in which for g in (0, 1, 2)]
+        cnt = [counts[i] for i in which for _ in (0, 1, 2)]
+        sd = [seeds[(names[i], g)] for i in which for g in (0, 1, 2)]
+        assert append_batch(src, reqs, groups, cnt, sd, mark=mark) == len(reqs)
+
+    def same(live):
+        src.sync()
+        dst.sync()
+        out = src.compare_cells(dst, (0, 1), [names[i] for i in live])
+        assert out["bad_positions"] == 0 and out["missing"] == 0, out
+        assert out["length_mismatch"] == 0, out
+        return out["cells"]
+
+    append(range(len(lens)), lens, mark=False)
+    patch = NativePatch(src, (0, 1), k)
+    side = torch.cuda.Stream() if side_stream else None
+    if side is not None:
+        patch.set_stream(side.cuda_stream)
+    assert patch.seed() == 2 * sum(lens)
+    keys, cells = patch.push(dst, reg.rank())
+    assert (keys, cells) == (2 * sum(lens), 2 * k * sum(lens))
+    assert same(range(len(lens))) == 2 * sum(lens) * k
+    # empty round
+    assert patch.push(dst, reg.rank()) == (0, 0)
+    assert patch.device_drained() == 0
+    # steady decode round: one token per request, group 2 (not migrating) too; positions
+    # 2..16 -> 15, 16, 17 ... lie inside existing destination blocks except lens 16 / 32
+    inside = [i for i, n in enumerate(lens) if n % s != 0]
+    append(inside, [1] * len(lens), mark=True)
+    keys, _ = patch.push(dst, reg.rank())
+    assert keys == 2 * len(inside) and patch.device_drained() == keys
+    lens = [n + 1 if i in inside else n for i, n in enumerate(lens)]
+    same(range(len(lens)))
+    # a round whose positions need new destination blocks (16 -> 17, 32 -> 33 and more)
+    append(range(len(lens)), [s] * len(lens), mark=True)
+    keys, _ = patch.push(dst, reg.rank())
+    assert keys == 2 * s * len(lens)
+    lens = [n + s for n in lens]
+    same(range(len(lens)))
+    # a request finishes after its writes were marked: discarded, never shipped
+    append(range(len(lens)), [3] * len(lens), mark=True)
+    gone = 3
+    assert patch.discard_request(names[gone], reg) > 0
+    src.free_request(names[gone])
+    dst.free_request(names[gone])
+    keys, _ = patch.push(dst, reg.rank())
+    assert keys == 2 * 3 * (len(lens) - 1)
+    lens = [n + 3 for n in lens]
+    live = [i for i in range(len(lens)) if i != gone]
+    same(live)
+    patch.close()
