@@ -16,8 +16,14 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("seed", [0, 1, 100])
-def test_two_process_push_matches_single_process(seed):
+@pytest.mark.parametrize("seed,socket", [(0, False), (1, False), (100, False), (0, True),
+                                         (100, True)])
+def test_two_process_push_matches_single_process(seed, socket, monkeypatch):
+    # the round's control over the shared-memory mailbox (default) or socket messages
+    if socket:
+        monkeypatch.setenv("PL_PATCH_SOCKET", "1")
+    else:
+        monkeypatch.delenv("PL_PATCH_SOCKET", raising=False)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     name = f"ipc-test-{os.getpid()}-{seed}"
