@@ -505,7 +505,7 @@ def c3_live_resize(device: int = 0, fill_reqs: int = 703, ctx: int = 2040,
 
 
 def c5_sweep(device: int = 0, rates=(0.01, 0.05, 0.25, 1.0), block_sizes=(8, 16, 32, 64, 128),
-             batch: int = 64, ctx: int = 2048, rounds: int = 3, seed: int = 0) -> list[dict]:
+             batch: int = 64, ctx: int = 2048, rounds: int = 8, seed: int = 0) -> list[dict]:
     """BASELINE configs[4] at one GPU: dirty-rate x block-size sweep of the patch round.
 
     Per block size: a source stage with ``batch`` requests x ``ctx`` tokens in two
