@@ -111,6 +111,7 @@ class NativePatch:
         self._rank, self._rank_args = None, (None, 0)
         self._keys, self._cells = C.c_int64(), C.c_int64()
         self._keys_ref, self._cells_ref = C.byref(self._keys), C.byref(self._cells)
+        self._push_fn, self._push_args = N.lib().pl_patch_push, (None, None)
         N.check(N.lib().pl_patch_set_active(h, 1))
 
     def seed(self) -> int:
@@ -121,10 +122,15 @@ class NativePatch:
     def push(self, dst: KvStore, rank: np.ndarray) -> tuple[int, int]:
         # ctypes argument objects are built once per rank array: numpy's .ctypes costs ~2 us,
         # as much as a steady round's whole host enqueue
-        if self._rank is not rank:
+        # (and the whole argument tuple once per (destination, rank): a steady round's
+        # Python side is then one foreign call)
+        if self._rank is not rank or self._push_args[0] is not dst:
             self._rank, self._rank_args = rank, (N.ptr(rank), len(rank))
-        N.check(N.lib().pl_patch_push(self.h, dst._h, *self._rank_args, self._keys_ref,
-                                      self._cells_ref))
+            self._push_args = (dst, (self.h, dst._h, *self._rank_args, self._keys_ref,
+                                     self._cells_ref))
+        rc = self._push_fn(*self._push_args[1])
+        if rc:
+            N.check(rc)
         return self._keys.value, self._cells.value
 
     def stream_ptr(self) -> int:
