@@ -44,9 +44,13 @@ def src_store(reg):
     return kvstore.KvStore(1, K, S, CAP, (0, 1, 2, 3), num_groups=4, cell_bytes=CELL, registry=reg)
 
 
-def dst_store(reg):
+def dst_store(reg, cap=CAP):
     from paper_2604_12171_b200 import kvstore
-    return kvstore.KvStore(2, K, S, CAP, (), num_groups=4, cell_bytes=CELL, registry=reg)
+    return kvstore.KvStore(2, K, S, cap, (), num_groups=4, cell_bytes=CELL, registry=reg)
+
+
+# a destination too small for the bulk round: the receiver's reservation fails mid-round
+CAP_SMALL = 5   # < one block per request of the fill: the round must overflow
 
 
 def apply_writes(st, writes, mark):
@@ -122,3 +126,74 @@ def single_process(seed):
         log.append(p.push(dst, reg.rank()))
     p.close()
     return summary(src), summary(dst), log
+
+
+def receiver_overflow(q, chan_name, seed):
+    """The receiver of a bulk round that overflows its pool: the reservation stops at the
+    failing write (migrator.py:124-131), the round is still served, the error surfaces."""
+    try:
+        import torch
+        torch.cuda.set_device(0)
+        from paper_2604_12171_b200 import dist as D
+        from paper_2604_12171_b200 import kvstore
+        reg = _registry(seed)
+        st = dst_store(reg, CAP_SMALL)
+        chan = D.Channel(chan_name, server=True)
+        rx = D.PatchReceiver(st, [2, 3], chan)
+        errors = []
+        while True:
+            try:
+                if not rx.serve():
+                    break
+            except kvstore.KvOverflow as e:
+                errors.append(type(e).__name__)
+        q.put(("rx", summary(st), rx.rounds, errors))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put(("rx-error", traceback.format_exc(), repr(e)))
+
+
+def sender_overflow(q, chan_name, seed):
+    try:
+        import torch
+        torch.cuda.set_device(0)
+        from paper_2604_12171_b200 import dist as D
+        from paper_2604_12171_b200 import kvstore
+        reg = _registry(seed)
+        st = src_store(reg)
+        fill, _ = ops(seed)
+        apply_writes(st, fill, mark=False)
+        chan = D.Channel(chan_name, server=False)
+        tx = D.PatchSender(st, [2, 3], K, chan, reg.rank)
+        tx.seed()
+        errors = []
+        try:
+            tx.round()
+        except kvstore.KvOverflow as e:
+            errors.append(type(e).__name__)
+        tx.close()
+        q.put(("tx", errors))
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put(("tx-error", traceback.format_exc(), repr(e)))
+
+
+def single_process_overflow(seed):
+    """The same overflowing bulk round with both stores in one process."""
+    from paper_2604_12171_b200 import _native as N
+    from paper_2604_12171_b200.perf import NativePatch
+    reg = _registry(seed)
+    src, dst = src_store(reg), dst_store(reg, CAP_SMALL)
+    dst.resident_groups |= {2, 3}
+    fill, _ = ops(seed)
+    apply_writes(src, fill, mark=False)
+    p = NativePatch(src, [2, 3], K)
+    p.seed()
+    code = None
+    try:
+        p.push(dst, reg.rank())
+    except N.NativeError as e:
+        code = e.code
+    dst.sync()
+    p.close()
+    return summary(dst), code

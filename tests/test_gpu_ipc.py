@@ -50,3 +50,36 @@ def test_two_process_push_matches_single_process(seed, socket, monkeypatch):
     for (rid, g, pos, j), cell in rx_sum[1].items():
         fp = rx_sum[0][g][rid][pos]
         assert cell == oracle.expand_cell(fp, j, W.CELL)
+
+
+@pytest.mark.parametrize("socket", [False, True])
+def test_two_process_overflow_applies_the_same_prefix(socket, monkeypatch):
+    """A bulk round the receiver cannot hold: across processes the receiver reserves up to
+    the failing write, the sender pushes exactly that prefix, and both sides raise
+    KvOverflow -- the destination ends identical to the single-process push of the same
+    round (which applies the same prefix and returns the same error)."""
+    if socket:
+        monkeypatch.setenv("PL_PATCH_SOCKET", "1")
+    else:
+        monkeypatch.delenv("PL_PATCH_SOCKET", raising=False)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    name = f"ipc-ovf-{os.getpid()}-{int(socket)}"
+    procs = [ctx.Process(target=W.receiver_overflow, args=(q, name, 0)),
+             ctx.Process(target=W.sender_overflow, args=(q, name, 0))]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r = q.get(timeout=120)
+        assert not r[0].endswith("error"), r[1]
+        res[r[0]] = r[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (tx_errors,), (rx_sum, rx_rounds, rx_errors) = res["tx"], res["rx"]
+    assert rx_rounds == 1 and rx_errors == ["KvOverflow"] and tx_errors == ["KvOverflow"]
+    dst_sum, code = W.single_process_overflow(0)
+    assert code == -1                       # PL_E_KV_OVERFLOW
+    assert rx_sum == dst_sum                # same prefix: snapshots, cells, state digest
+    assert 0 < sum(len(v) for v in rx_sum[0][2].values())   # something was applied
