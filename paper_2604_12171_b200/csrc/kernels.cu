@@ -884,11 +884,16 @@ void launch_copy(const CopyLaunch& c, cudaStream_t st) {
     int64_t b = (items + cap_warps - 1) / cap_warps;
     b = std::min<int64_t>(32, std::max<int64_t>(2, (b + 1) & ~int64_t(1)));
     const int64_t grid = std::max<int64_t>(1, (items + b * kWarps - 1) / (b * kWarps));
-    // PL_PUSH_MINB (A/B): CTAs per SM the launch bound asks for (registers vs occupancy)
-    static const int minb = [] {
+    // CTAs per SM the launch bound asks for (registers vs occupancy).  Sparse rounds with
+    // short batches (b <= 4: a 5 % round of random cells) gain from more warps in flight
+    // per SM (3 CTAs, 80 registers: 103 -> 98 us at the c5 shape) although the kernel then
+    // spills a little; long batches (25 %, the bulk round) keep the register-rich 2 CTAs
+    // (3 CTAs: 376 -> 388 us at 25 %, 6.5 -> 5.9 TB/s in bulk).  PL_PUSH_MINB forces one.
+    static const int minb_env = [] {
       const char* v = std::getenv("PL_PUSH_MINB");
-      return v ? std::atoi(v) : 1;
+      return v ? std::atoi(v) : 0;
     }();
+    const int minb = minb_env > 0 ? minb_env : (b <= 4 ? 3 : 1);
     KernelTimer timer("patch_push", st);
     const unsigned g = (unsigned)std::min<int64_t>(grid, (int64_t)sm_count() * 16);
     const int lm = c.layer_major;
